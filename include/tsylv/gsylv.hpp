@@ -1,0 +1,90 @@
+// tsylv drop-in (B200 build) — generalized Sylvester solver entry points.
+//
+//   solve_gsylv(p, cfg)                    reference gsylv.hpp:311-331
+//   gsylv_recursive(T, C, Bt, n_min)       reference gsylv.hpp:149-159
+//
+// Pipeline of gsylv_pipeline (gsylv.hpp:236-302): QZ of (A_0, C) and Schur of
+// every tail coefficient on the host (shared setup), the pencil screen, then
+// the GPU: B~ = B x_0 Q^T x_m U_m^T, the reduced dataflow solve with the
+// factored chain W_m (see csrc/solve.cu), X = X~ x_0 Z x_m U_m.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "tsylv/laplace.hpp"
+
+namespace tsylv {
+
+inline double residual(const GSylvProblem<double>& p, const Tensor<double>& x) {
+  validate(p);
+  if (x.dims() != p.rhs.dims()) throw dimension_error("residual: solution shape mismatch");
+  std::vector<const double*> a;
+  for (const auto& m : p.coeffs) a.push_back(m.data());
+  double r = 0;
+  gpu::check(tsg_residual(gpu::context(), 1, p.order(), p.rhs.dims().data(), a.data(), p.c.data(),
+                          p.rhs.data(), x.data(), 0, &r),
+             "residual");
+  return r;
+}
+
+inline Tensor<double> gsylv_recursive(const std::vector<Matrix<double>>& t, const Matrix<double>& c,
+                                      Tensor<double> b, int n_min) {
+  detail::require_reduced(t, b, n_min, "gsylv_recursive");
+  if (t.size() < 2) throw dimension_error("gsylv_recursive: need at least two modes");
+  if (c.rows() != t[0].rows() || c.cols() != t[0].cols())
+    throw dimension_error("gsylv_recursive: C must match A_0");
+  if (!is_upper_triangular(c)) throw dimension_error("gsylv_recursive: C must be upper triangular");
+  std::vector<const double*> tail;
+  for (size_t m = 1; m < t.size(); ++m) tail.push_back(t[m].data());
+  tsg_opts o = detail::gpu_opts(n_min);
+  Tensor<double> x(b.dims());
+  gpu::check(tsg_gsylv_reduced(gpu::context(), b.order(), b.dims().data(), t[0].data(), c.data(),
+                               tail.data(), b.data(), x.data(), &o, nullptr),
+             "gsylv_recursive");
+  return x;
+}
+
+inline SolveReport<double> solve_gsylv(const GSylvProblem<double>& p, const SolverConfig& cfg = {}) {
+  validate(p);
+  detail::check_config(cfg, "solve_gsylv");
+  const int d = p.order();
+  SolveReport<double> rep;
+  rep.n_min = cfg.n_min > 0 ? cfg.n_min : default_n_min(Family::gsylv, d, cfg.strategy);
+  rep.strategy = cfg.strategy;
+
+  StopWatch sw;
+  GeneralizedSchurFactorization g = qz(p.coeffs[0], p.c);
+  std::vector<SchurFactorization> f;
+  for (int m = 1; m < d; ++m) f.push_back(schur(p.coeffs[m]));
+  rep.timings.reduction_s = sw.lap();
+
+  std::vector<Matrix<double>> red{g.s};
+  for (const auto& x : f) red.push_back(x.t);
+  const Solvability s = check_solvable_gsylv(red, g.t, cfg.singularity_tol);
+  if (!s.solvable)
+    throw singular_error(detail::witness_message("solve_gsylv", s), s.witness, s.witness_values,
+                         s.min_abs);
+
+  std::vector<const double*> tp, up;
+  for (const auto& x : f) {
+    tp.push_back(x.t.data());
+    up.push_back(x.u.data());
+  }
+  tsg_opts o = detail::gpu_opts(cfg.n_min);
+  tsg_report r{};
+  Tensor<double> x(p.rhs.dims());
+  gpu::check(tsg_gsylv_solve(gpu::context(), d, p.rhs.dims().data(), g.s.data(), g.t.data(),
+                             g.u.data(), g.z.data(), tp.data(), up.data(), p.rhs.data(), x.data(),
+                             &o, &r),
+             "solve_gsylv");
+  const double gpu_s = sw.lap();
+  const double back_frac = r.t_total_ms > 0 ? (r.t_back_ms + r.t_d2h_ms) / r.t_total_ms : 0.0;
+  rep.timings.back_transform_s = gpu_s * back_frac;
+  rep.timings.recursion_s = gpu_s - rep.timings.back_transform_s;
+  detail::fill_gpu(rep.gpu, r);
+  rep.solution = std::move(x);
+  rep.residual = residual(p, rep.solution);
+  return rep;
+}
+
+}  // namespace tsylv

@@ -1,0 +1,140 @@
+// tsylv drop-in (B200 build) — Laplace-like solver entry points.
+//
+//   solve_laplace(p, cfg)              reference laplace.hpp:324-344
+//   laplace_recursive(T, Bt, n_min)    reference laplace.hpp:185-195
+//
+// solve_laplace keeps the reference pipeline: host Schur
+// of every coefficient (shared setup, dgees), the host solvability screen
+// (singular_error with witness), then ONE call into the GPU library that runs
+// forward transforms, the reduced quasi-triangular dataflow solve and the
+// back transforms on the device (tsg_laplace_solve), and finally the device
+// residual.  Arithmetic is real quasi-triangular throughout; the solution is
+// the unique one the reference's complex default also returns (parity on X).
+#pragma once
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tsylv/config.hpp"
+#include "tsylv/gpu.hpp"
+#include "tsylv/lapack.hpp"
+#include "tsylv/matrix.hpp"
+#include "tsylv/problems.hpp"
+#include "tsylv/solvability.hpp"
+#include "tsylv/tensor.hpp"
+
+namespace tsylv {
+
+namespace detail {
+
+inline void check_config(const SolverConfig& cfg, const char* who) {
+  if (cfg.strategy == Strategy::merge && cfg.arithmetic == Arithmetic::real_quasitriangular)
+    throw std::invalid_argument(std::string(who) +
+                                ": the merge strategy needs strictly triangular (complex Schur) "
+                                "coefficients; real quasi-triangular arithmetic cannot merge");
+}
+
+inline tsg_opts gpu_opts(int n_min_user) {
+  tsg_opts o;
+  tsg_default_opts(&o);
+  o.n_min = n_min_user;  // 0: kernel-tuned tile extents
+  return o;
+}
+
+inline void fill_gpu(GpuTimings& g, const tsg_report& r) {
+  g.fwd_ms = r.t_fwd_ms;
+  g.solve_ms = r.t_solve_ms;
+  g.back_ms = r.t_back_ms;
+  g.h2d_ms = r.t_h2d_ms;
+  g.d2h_ms = r.t_d2h_ms;
+  g.total_ms = r.t_total_ms;
+  g.flops_alg = r.flops_alg;
+  g.flops_exec = r.flops_exec;
+}
+
+inline void require_reduced(const std::vector<Matrix<double>>& t, const Tensor<double>& b,
+                            int n_min, const char* who) {
+  if (n_min < 1) throw dimension_error(std::string(who) + ": n_min must be >= 1");
+  if (t.empty() || b.order() != static_cast<int>(t.size()))
+    throw dimension_error(std::string(who) + ": rhs order does not match coefficient count");
+  for (size_t m = 0; m < t.size(); ++m) {
+    if (t[m].rows() != t[m].cols() || t[m].rows() != b.dim(static_cast<int>(m)))
+      throw dimension_error(std::string(who) + ": coefficient " + std::to_string(m) +
+                            " does not match rhs");
+    if (!is_upper_quasi_triangular(t[m]))
+      throw dimension_error(std::string(who) + ": coefficient " + std::to_string(m) +
+                            " must be upper quasi-triangular");
+  }
+}
+
+}  // namespace detail
+
+inline double residual(const LaplaceProblem<double>& p, const Tensor<double>& x) {
+  validate(p);
+  if (x.dims() != p.rhs.dims()) throw dimension_error("residual: solution shape mismatch");
+  std::vector<const double*> a;
+  for (const auto& m : p.coeffs) a.push_back(m.data());
+  double r = 0;
+  gpu::check(tsg_residual(gpu::context(), 0, p.order(), p.rhs.dims().data(), a.data(), nullptr,
+                          p.rhs.data(), x.data(), 0, &r),
+             "residual");
+  return r;
+}
+
+// Reduced form: sum_m X x_m T_m = Bt with upper quasi-triangular T_m.
+inline Tensor<double> laplace_recursive(const std::vector<Matrix<double>>& t, Tensor<double> b,
+                                        int n_min) {
+  detail::require_reduced(t, b, n_min, "laplace_recursive");
+  std::vector<const double*> tp;
+  for (const auto& m : t) tp.push_back(m.data());
+  tsg_opts o = detail::gpu_opts(n_min);
+  Tensor<double> x(b.dims());
+  gpu::check(tsg_laplace_reduced(gpu::context(), b.order(), b.dims().data(), tp.data(), b.data(),
+                                 x.data(), &o, nullptr),
+             "laplace_recursive");
+  return x;
+}
+
+inline SolveReport<double> solve_laplace(const LaplaceProblem<double>& p,
+                                         const SolverConfig& cfg = {}) {
+  validate(p);
+  detail::check_config(cfg, "solve_laplace");
+  const int d = p.order();
+  SolveReport<double> rep;
+  rep.n_min = cfg.n_min > 0 ? cfg.n_min : default_n_min(Family::laplace, d, cfg.strategy);
+  rep.strategy = cfg.strategy;
+
+  StopWatch sw;
+  std::vector<SchurFactorization> f;
+  for (const auto& a : p.coeffs) f.push_back(schur(a));
+  rep.timings.reduction_s = sw.lap();
+
+  std::vector<Matrix<double>> t;
+  for (const auto& s : f) t.push_back(s.t);
+  const Solvability s = check_solvable_laplace(t, cfg.singularity_tol);
+  if (!s.solvable)
+    throw singular_error(detail::witness_message("solve_laplace", s), s.witness, s.witness_values,
+                         s.min_abs);
+
+  std::vector<const double*> tp, up;
+  for (const auto& x : f) {
+    tp.push_back(x.t.data());
+    up.push_back(x.u.data());
+  }
+  tsg_opts o = detail::gpu_opts(cfg.n_min);
+  tsg_report r{};
+  Tensor<double> x(p.rhs.dims());
+  gpu::check(tsg_laplace_solve(gpu::context(), d, p.rhs.dims().data(), tp.data(), up.data(),
+                               p.rhs.data(), x.data(), &o, &r),
+             "solve_laplace");
+  const double gpu_s = sw.lap();
+  const double back_frac = r.t_total_ms > 0 ? (r.t_back_ms + r.t_d2h_ms) / r.t_total_ms : 0.0;
+  rep.timings.back_transform_s = gpu_s * back_frac;
+  rep.timings.recursion_s = gpu_s - rep.timings.back_transform_s;
+  detail::fill_gpu(rep.gpu, r);
+  rep.solution = std::move(x);
+  rep.residual = residual(p, rep.solution);
+  return rep;
+}
+
+}  // namespace tsylv

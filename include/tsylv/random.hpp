@@ -1,0 +1,114 @@
+// tsylv drop-in (B200 build) — deterministic inputs shared by the GPU path
+// and the oracle.  RandomStream restates the reference's published stream
+// (random.hpp:16-62): std::mt19937_64, uniform = (x >> 11) * 2^-53, and a
+// Box-Muller normal with the sine member cached; matrices and tensors are
+// filled in storage (column-major) order.  tests/test_random.py pins it
+// bit-for-bit against the reference build in oracle/_ref.
+//
+// The BASELINE.json configurations are generated here (draw order:
+// coefficients in mode order, then the right-hand side):
+//   kind 1  convection-diffusion  A = (n+1)^2 tridiag(-1,2,-1) + c (n+1)/2 tridiag(-1,0,1),
+//           c ~ U(0.5, 2) per mode                              (config C1)
+//   kind 2  A = G/sqrt(n) + 3 I, G iid N(0,1)                   (configs C2, C3, C4)
+//   kind 5  gsylv A X + B X (C x ... x C) = D with A = G_A/sqrt(n0) + 4 I,
+//           B = G_B/sqrt(n0), C = G_C/(2 sqrt(nc)), posed as coeffs
+//           {A, C^T, ..., C^T}, c = B                          (config C5)
+#pragma once
+#include <cmath>
+#include <cstdint>
+#include <numbers>
+#include <random>
+#include <vector>
+
+#include "tsylv/matrix.hpp"
+#include "tsylv/problems.hpp"
+#include "tsylv/tensor.hpp"
+
+namespace tsylv {
+
+class RandomStream {
+ public:
+  explicit RandomStream(std::uint64_t seed) : mt_(seed) {}
+  double uniform() { return static_cast<double>(mt_() >> 11) * 0x1.0p-53; }
+  double normal() {
+    if (cached_) {
+      cached_ = false;
+      return sin_member_;
+    }
+    const double a = 1.0 - uniform();
+    const double b = uniform();
+    const double rad = std::sqrt(-2.0 * std::log(a));
+    const double ang = 2.0 * std::numbers::pi * b;
+    sin_member_ = rad * std::sin(ang);
+    cached_ = true;
+    return rad * std::cos(ang);
+  }
+
+ private:
+  std::mt19937_64 mt_;
+  double sin_member_ = 0;
+  bool cached_ = false;
+};
+
+inline Matrix<double> randn_matrix(RandomStream& r, int rows, int cols) {
+  Matrix<double> m(rows, cols);
+  for (std::size_t i = 0; i < m.size(); ++i) m.data()[i] = r.normal();
+  return m;
+}
+inline Tensor<double> randn_tensor(RandomStream& r, const std::vector<int>& dims) {
+  Tensor<double> t(dims);
+  for (std::size_t i = 0; i < t.size(); ++i) t.data()[i] = r.normal();
+  return t;
+}
+
+inline Matrix<double> convection_diffusion(int n, double c) {
+  const double h2 = static_cast<double>(n + 1) * (n + 1), h1 = c * (n + 1) / 2.0;
+  Matrix<double> a(n, n);
+  for (int i = 0; i < n; ++i) {
+    a(i, i) = 2.0 * h2;
+    if (i + 1 < n) {
+      a(i, i + 1) = -h2 + h1;  // super-diagonal
+      a(i + 1, i) = -h2 - h1;  // sub-diagonal
+    }
+  }
+  return a;
+}
+
+inline LaplaceProblem<double> baseline_laplace(int kind, const std::vector<int>& dims,
+                                               std::uint64_t seed) {
+  RandomStream r(seed);
+  LaplaceProblem<double> p;
+  for (int n : dims) {
+    if (kind == 1) {
+      p.coeffs.push_back(convection_diffusion(n, 0.5 + 1.5 * r.uniform()));
+    } else {
+      Matrix<double> g = randn_matrix(r, n, n);
+      g *= 1.0 / std::sqrt(static_cast<double>(n));
+      for (int i = 0; i < n; ++i) g(i, i) += 3.0;
+      p.coeffs.push_back(std::move(g));
+    }
+  }
+  p.rhs = randn_tensor(r, dims);
+  return p;
+}
+
+inline GSylvProblem<double> baseline_gsylv(const std::vector<int>& dims, std::uint64_t seed) {
+  RandomStream r(seed);
+  const int n0 = dims[0], nc = dims[1];
+  Matrix<double> a = randn_matrix(r, n0, n0);
+  Matrix<double> b = randn_matrix(r, n0, n0);
+  Matrix<double> c = randn_matrix(r, nc, nc);
+  a *= 1.0 / std::sqrt(static_cast<double>(n0));
+  for (int i = 0; i < n0; ++i) a(i, i) += 4.0;
+  b *= 1.0 / std::sqrt(static_cast<double>(n0));
+  c *= 1.0 / (2.0 * std::sqrt(static_cast<double>(nc)));
+  GSylvProblem<double> p;
+  p.coeffs.push_back(std::move(a));
+  const Matrix<double> ct = transposed(c);
+  for (std::size_t m = 1; m < dims.size(); ++m) p.coeffs.push_back(ct);
+  p.c = std::move(b);
+  p.rhs = randn_tensor(r, dims);
+  return p;
+}
+
+}  // namespace tsylv

@@ -1,0 +1,209 @@
+// tsylv drop-in (B200 build) — the host solvability screen run before the
+// GPU solve so singular operators raise singular_error with the reference's
+// witness semantics (solvability.hpp:31-116, laplace.hpp:28-43,
+// gsylv.hpp:31-50): the smallest |operator eigenvalue| over every tuple, the
+// first minimum in odometer order (mode 0 fastest).  The Laplace scan is
+// split over host threads along the slowest mode; ties resolve to the lowest
+// chunk, which keeps the sequential witness.
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <limits>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "tsylv/matrix.hpp"
+#include "tsylv/scalar.hpp"
+
+namespace tsylv {
+
+struct Solvability {
+  bool solvable = true;
+  double min_abs = 0;
+  std::vector<int> witness;
+  std::vector<std::complex<double>> witness_values;
+};
+
+using EigList = std::vector<std::complex<double>>;
+
+// Eigenvalues of a quasi-triangular matrix in diagonal order.
+inline EigList quasi_tri_eigenvalues(const Matrix<double>& t) {
+  if (!is_upper_quasi_triangular(t))
+    throw dimension_error("quasi_block_sizes: matrix is not upper quasi-triangular");
+  using C = std::complex<double>;
+  const int n = t.rows();
+  EigList e;
+  for (int j = 0; j < n;) {
+    if (j + 1 < n && t(j + 1, j) != 0.0) {
+      const C half_tr = 0.5 * (C(t(j, j)) + C(t(j + 1, j + 1)));
+      const C det = C(t(j, j)) * C(t(j + 1, j + 1)) - C(t(j, j + 1)) * C(t(j + 1, j));
+      const C r = std::sqrt(half_tr * half_tr - det);
+      e.push_back(half_tr + r);
+      e.push_back(half_tr - r);
+      j += 2;
+    } else {
+      e.emplace_back(t(j, j));
+      j += 1;
+    }
+  }
+  return e;
+}
+
+namespace detail {
+
+inline Solvability min_kron_sum(const std::vector<EigList>& eigs) {
+  using C = std::complex<double>;
+  const int d = static_cast<int>(eigs.size());
+  const int outer = static_cast<int>(eigs[d - 1].size());
+  // Precompute the partial sums of modes 0..d-2 once (odometer order).
+  std::vector<C> inner{C(0)};
+  for (int m = 0; m + 1 < d; ++m) {
+    std::vector<C> nx;
+    nx.reserve(inner.size() * eigs[m].size());
+    for (const C& l : eigs[m])
+      for (const C& s : inner) nx.push_back(s + l);
+    inner.swap(nx);
+  }
+  // Built newest-mode-outermost, i.e. index p enumerates modes 0..d-2 with
+  // mode 0 fastest (the reference's odometer order).
+  const std::vector<C>& ordered = inner;
+  const int nt = std::max(1, std::min<int>(outer, static_cast<int>(std::thread::hardware_concurrency())));
+  std::vector<double> best(nt, std::numeric_limits<double>::infinity());
+  std::vector<size_t> best_in(nt, 0);
+  std::vector<int> best_out(nt, 0);
+  auto work = [&](int t) {
+    for (int o = t; o < outer; o += nt) {
+      const C l = eigs[d - 1][o];
+      for (size_t p = 0; p < ordered.size(); ++p) {
+        const double a = std::abs(ordered[p] + l);
+        if (a < best[t] || (a == best[t] && (o < best_out[t] || (o == best_out[t] && p < best_in[t])))) {
+          best[t] = a;
+          best_in[t] = p;
+          best_out[t] = o;
+        }
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  int bt = 0;
+  for (int t = 1; t < nt; ++t)
+    if (best[t] < best[bt] || (best[t] == best[bt] && (best_out[t] < best_out[bt] ||
+                                                      (best_out[t] == best_out[bt] && best_in[t] < best_in[bt]))))
+      bt = t;
+  Solvability s;
+  s.min_abs = best[bt];
+  size_t p = best_in[bt];
+  for (int m = 0; m + 1 < d; ++m) {
+    const size_t n = eigs[m].size();
+    s.witness.push_back(static_cast<int>(p % n));
+    p /= n;
+  }
+  s.witness.push_back(best_out[bt]);
+  for (int m = 0; m < d; ++m) s.witness_values.push_back(eigs[m][s.witness[m]]);
+  return s;
+}
+
+// Smallest eigenvalue magnitude of S_blk + z T_blk over the diagonal blocks
+// of S and every product z of one tail eigenvalue per list.
+inline Solvability min_pencil_product(const Matrix<double>& s_, const Matrix<double>& t_,
+                                      const std::vector<EigList>& tails) {
+  using C = std::complex<double>;
+  const int n = s_.rows();
+  std::vector<int> starts, sizes;
+  for (int j = 0; j < n;) {
+    const int sz = (j + 1 < n && s_(j + 1, j) != 0.0) ? 2 : 1;
+    starts.push_back(j);
+    sizes.push_back(sz);
+    j += sz;
+  }
+  std::vector<C> prods{C(1)};
+  for (const auto& l : tails) {
+    std::vector<C> nx;
+    for (const C& e : l)
+      for (const C& p : prods) nx.push_back(p * e);
+    prods.swap(nx);
+  }
+  Solvability out;
+  out.min_abs = std::numeric_limits<double>::infinity();
+  size_t best_p = 0;
+  int best_b = 0;
+  for (size_t p = 0; p < prods.size(); ++p) {
+    const C z = prods[p];
+    for (size_t b = 0; b < starts.size(); ++b) {
+      const int i = starts[b];
+      double mag;
+      if (sizes[b] == 1) {
+        mag = std::abs(C(s_(i, i)) + z * C(t_(i, i)));
+      } else {
+        const C m00 = C(s_(i, i)) + z * t_(i, i), m01 = C(s_(i, i + 1)) + z * t_(i, i + 1);
+        const C m10 = C(s_(i + 1, i)), m11 = C(s_(i + 1, i + 1)) + z * t_(i + 1, i + 1);
+        const C h = 0.5 * (m00 + m11);
+        const C r = std::sqrt(h * h - (m00 * m11 - m01 * m10));
+        mag = std::min(std::abs(h + r), std::abs(h - r));
+      }
+      if (mag < out.min_abs) {
+        out.min_abs = mag;
+        best_p = p;
+        best_b = static_cast<int>(b);
+      }
+    }
+  }
+  out.witness.push_back(starts[best_b]);
+  out.witness_values = {C(s_(starts[best_b], starts[best_b])), C(t_(starts[best_b], starts[best_b]))};
+  size_t p = best_p;
+  for (const auto& l : tails) {
+    out.witness.push_back(static_cast<int>(p % l.size()));
+    out.witness_values.push_back(l[p % l.size()]);
+    p /= l.size();
+  }
+  return out;
+}
+
+inline std::string witness_message(const char* who, const Solvability& s) {
+  std::string m = std::string(who) + ": operator numerically singular (|eigenvalue| = " +
+                  std::to_string(s.min_abs) + " at slots (";
+  for (size_t i = 0; i < s.witness.size(); ++i) m += (i ? "," : "") + std::to_string(s.witness[i]);
+  return m + "))";
+}
+
+}  // namespace detail
+
+inline Solvability check_solvable_laplace(const std::vector<Matrix<double>>& t, double tol = 0) {
+  if (t.empty()) throw dimension_error("check_solvable_laplace: no coefficients");
+  std::vector<EigList> e;
+  double scale = 0;
+  for (const auto& m : t) {
+    e.push_back(quasi_tri_eigenvalues(m));
+    scale += m.frobenius_norm();
+  }
+  if (tol <= 0) tol = unit_roundoff<double> * scale;
+  Solvability s = detail::min_kron_sum(e);
+  s.solvable = s.min_abs > tol;
+  return s;
+}
+
+inline Solvability check_solvable_gsylv(const std::vector<Matrix<double>>& t,
+                                        const Matrix<double>& c, double tol = 0) {
+  if (t.size() < 2) throw dimension_error("check_solvable_gsylv: need at least two modes");
+  if (c.rows() != t[0].rows() || c.cols() != t[0].cols())
+    throw dimension_error("check_solvable_gsylv: C must match A_0");
+  if (!is_upper_triangular(c)) throw dimension_error("check_solvable_gsylv: C must be upper triangular");
+  double scale = t[0].frobenius_norm() + c.frobenius_norm();
+  std::vector<EigList> tails;
+  for (size_t m = 1; m < t.size(); ++m) {
+    tails.push_back(quasi_tri_eigenvalues(t[m]));
+    scale += t[m].frobenius_norm();
+  }
+  (void)quasi_tri_eigenvalues(t[0]);  // validates A_0
+  if (tol <= 0) tol = unit_roundoff<double> * scale;
+  Solvability s = detail::min_pencil_product(t[0], c, tails);
+  s.solvable = s.min_abs > tol;
+  return s;
+}
+
+}  // namespace tsylv

@@ -1,0 +1,138 @@
+/* tsylv_gpu.h — C-ABI of the B200-native Schur-basis solve.
+ *
+ * This is the drop-in boundary below the reference's C++ solver entry points
+ * (proj/include/tsylv/*.hpp).  No C++ or torch types cross it: plain
+ * pointers, int extents, column-major FP64 buffers (mode 0 fastest, the
+ * layout of tsylv::Tensor, tensor.hpp:19-27).  Each entry point names the
+ * reference interface it replaces.
+ *
+ * Status codes (mirror tools/tsylv.cpp:1-5 exit codes; the C++ shim in
+ * include/tsylv/ rethrows the reference exception types, errors.hpp:13-62):
+ *   TSG_OK 0, TSG_EDIM 1 (dimension_error), TSG_ESINGULAR 2 (singular_error),
+ *   TSG_EFACT 3 (factorization_error), TSG_EINVAL 4 (std::invalid_argument),
+ *   TSG_ECUDA 5 (CUDA/NCCL failure -> std::runtime_error).
+ *
+ * Ownership: the caller owns every host buffer; the context owns all device
+ * memory.  One context per host thread (not thread-safe); several contexts
+ * may coexist.  Calls are synchronous unless opts->stream is set.
+ */
+#ifndef TSYLV_GPU_H
+#define TSYLV_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSG_OK 0
+#define TSG_EDIM 1
+#define TSG_ESINGULAR 2
+#define TSG_EFACT 3
+#define TSG_EINVAL 4
+#define TSG_ECUDA 5
+
+#define TSG_MAX_ORDER 8
+
+typedef struct tsg_ctx tsg_ctx;
+typedef struct tsg_plan tsg_plan;
+
+typedef struct {
+  int n_min;             /* base-tile extent bound per mode (0 = tuned default) */
+  int tile[TSG_MAX_ORDER]; /* explicit per-mode tile extents (0 = from n_min) */
+  int inputs_on_device;  /* 1: B/X are device pointers (resident in HBM) */
+  void* stream;          /* cudaStream_t to run on (NULL = context stream) */
+  int use_graph;         /* capture execute() in a CUDA graph (default 1) */
+  int n_gpus;            /* reserved for slab sharding (1) */
+} tsg_opts;
+
+typedef struct {
+  double t_fwd_ms;       /* forward transforms (B ->B~), CUDA events */
+  double t_solve_ms;     /* reduced (quasi-)triangular solve */
+  double t_back_ms;      /* back transforms (X~ -> X) */
+  double t_h2d_ms;       /* host->device copy (host inputs only) */
+  double t_d2h_ms;       /* device->host copy (host inputs only) */
+  double t_total_ms;     /* whole execute(), CUDA events */
+  double flops_alg;      /* algorithmic FLOP credited */
+  double flops_exec;     /* FLOP actually issued by the schedule */
+  int zero_pivot_index;  /* -1, or first linear index of a singular base cell */
+  int kernel_launches;   /* kernels launched by execute() */
+} tsg_report;
+
+void tsg_default_opts(tsg_opts* o);
+
+/* Context: device, streams, workspace. */
+int tsg_create(int n_gpus, const int* device_ids, tsg_ctx** out);
+void tsg_destroy(tsg_ctx* ctx);
+const char* tsg_last_error(const tsg_ctx* ctx);
+
+/* ---- Laplace-like: sum_m X x_m A_m = B  (laplace.hpp:248-302) ----------
+ * Real Schur basis A_m = U_m T_m U_m^T: T[m] upper quasi-triangular,
+ * U[m] orthogonal, both dims[m] x dims[m] column-major host arrays.
+ * Replaces laplace.hpp:276-298 (forward transforms, reduced solve, back
+ * transforms).  X may alias B. */
+int tsg_laplace_solve(tsg_ctx* ctx, int d, const int* dims,
+                      const double* const* T, const double* const* U,
+                      const double* B, double* X, const tsg_opts* opts,
+                      tsg_report* rep);
+
+/* Reduced form only (laplace_recursive, laplace.hpp:185-195): solves
+ * sum_m Xt x_m T_m = Bt for quasi-triangular T_m. */
+int tsg_laplace_reduced(tsg_ctx* ctx, int d, const int* dims,
+                        const double* const* T, const double* Bt, double* Xt,
+                        const tsg_opts* opts, tsg_report* rep);
+
+/* ---- Generalized: X x_0 A_0 + X x_0 C x_1 A_1 ... = B  (gsylv.hpp:236-302)
+ * qz(A_0, C) = (Q, Z, S, Tc): A_0 = Q S Z^T, C = Q Tc Z^T; tail m >= 1:
+ * A_m = U_m T_m U_m^T.  Ttail/Utail hold d-1 pointers (modes 1..d-1). */
+int tsg_gsylv_solve(tsg_ctx* ctx, int d, const int* dims, const double* S,
+                    const double* Tc, const double* Q, const double* Z,
+                    const double* const* Ttail, const double* const* Utail,
+                    const double* B, double* X, const tsg_opts* opts,
+                    tsg_report* rep);
+
+/* Reduced form only (gsylv_recursive, gsylv.hpp:149-159). */
+int tsg_gsylv_reduced(tsg_ctx* ctx, int d, const int* dims, const double* S,
+                      const double* Tc, const double* const* Ttail,
+                      const double* Bt, double* Xt, const tsg_opts* opts,
+                      tsg_report* rep);
+
+/* ---- Plans: set up once (factors uploaded, tiles/schedule built), execute
+ * many times.  The bench times tsg_plan_execute with inputs resident.
+ * family: 0 Laplace (Tc/S/Q/Z unused), 1 gsylv.  For gsylv, T[0]=S,
+ * U[0]=Q and the extra pointers Tc, Z are used.  reduced_only=1 skips
+ * both transforms (U/Q/Z may be NULL). */
+int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims,
+                    const double* const* T, const double* const* U,
+                    const double* Tc, const double* Z, int reduced_only,
+                    const tsg_opts* opts, tsg_plan** out);
+int tsg_plan_execute(tsg_plan* plan, const double* B, double* X,
+                     int inputs_on_device, tsg_report* rep);
+void tsg_plan_destroy(tsg_plan* plan);
+/* Number of tiles / dataflow steps of the plan's reduced solve. */
+int tsg_plan_info(const tsg_plan* plan, int64_t* n_tiles, int* tile_extents,
+                  double* flops_alg);
+
+/* ---- Mode product Y = X x_mode A  (tensor.hpp:187-231) -----------------
+ * A is r x dims[mode] column-major; Y has dims with dims[mode] -> r. */
+int tsg_mode_multiply(tsg_ctx* ctx, int d, const int* dims, const double* X,
+                      int r, const double* A, int mode, double* Y,
+                      const tsg_opts* opts);
+
+/* ---- Relative residual (oracle.hpp:231-268) on the device -------------
+ * ||op(X) - B||_F / (scale ||X||_F + ||B||_F) with scale = sum_m ||A_m||_F
+ * (Laplace, family 0) or ||A_0||_F + ||C||_F prod_{m>=1} ||A_m||_F (gsylv,
+ * family 1), computed through mode products only.  A holds the d dense
+ * ORIGINAL coefficients; C is NULL for Laplace.  B/X follow inputs_on_device. */
+int tsg_residual(tsg_ctx* ctx, int family, int d, const int* dims,
+                 const double* const* A, const double* C, const double* B,
+                 const double* X, int inputs_on_device, double* out);
+
+/* ABI version (bumped on any signature change). */
+int tsg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSYLV_GPU_H */

@@ -1,0 +1,277 @@
+"""TEST INFRASTRUCTURE ONLY.  ctypes binding of oracle/_ref/libtsylv_ref.so,
+the reference tsylv solver built from its unmodified headers
+(oracle/ref_driver.cpp).  Function names and argument meaning mirror
+paper_1905_09539_b200.api so parity tests call both sides identically."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "libtsylv_ref.so")
+
+P = ctypes.c_void_p
+I = ctypes.c_int
+D = ctypes.c_double
+Dp = ctypes.POINTER(ctypes.c_double)
+Dpp = ctypes.POINTER(Dp)
+Ip = ctypes.POINTER(ctypes.c_int)
+E = ctypes.c_char_p
+
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not available():
+            raise RuntimeError(f"{LIB_PATH} missing: run `make -C oracle`")
+        _lib = ctypes.CDLL(LIB_PATH)
+        sig = {
+            "ref_solve_laplace": (I, [I, Ip, Dpp, Dp, I, I, I, Dp, Dp, E, I]),
+            "ref_solve_gsylv": (I, [I, Ip, Dpp, Dp, Dp, I, I, I, Dp, Dp, E, I]),
+            "ref_laplace_recursive": (I, [I, Ip, Dpp, Dp, I, Dp, E, I]),
+            "ref_gsylv_recursive": (I, [I, Ip, Dpp, Dp, Dp, I, Dp, E, I]),
+            "ref_mode_multiply": (I, [I, Ip, Dp, I, Dp, I, Dp, E, I]),
+            "ref_schur": (I, [I, Dp, Dp, Dp, E, I]),
+            "ref_qz": (I, [I, Dp, Dp, Dp, Dp, Dp, Dp, E, I]),
+            "ref_dense_solve_laplace": (I, [I, Ip, Dpp, Dp, Dp, E, I]),
+            "ref_dense_solve_gsylv": (I, [I, Ip, Dpp, Dp, Dp, Dp, E, I]),
+            "ref_residual_laplace": (D, [I, Ip, Dpp, Dp, Dp]),
+            "ref_residual_gsylv": (D, [I, Ip, Dpp, Dp, Dp, Dp]),
+            "ref_check_solvable_laplace": (I, [I, Ip, Dpp, D, Dp, Ip, Ip, E, I]),
+            "ref_rng_new": (P, [ctypes.c_uint64]),
+            "ref_rng_free": (None, [P]),
+            "ref_rng_uniform": (D, [P]),
+            "ref_rng_normal": (D, [P]),
+            "ref_rng_randn": (None, [P, Dp, ctypes.c_size_t]),
+            "ref_random_reduced_laplace": (None, [P, I, Ip, Dp, Dp]),
+            "ref_random_laplace_problem": (None, [P, I, Ip, Dp, Dp]),
+            "ref_random_reduced_gsylv": (None, [P, I, Ip, Dp, Dp, Dp]),
+            "ref_random_gsylv_problem": (None, [P, I, Ip, Dp, Dp, Dp]),
+            "ref_randn_quasi_triangular": (None, [P, I, D, D, Dp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(_lib, name)
+            f.restype = res
+            f.argtypes = args
+    return _lib
+
+
+class RefError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def _f(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a):
+    return a.ctypes.data_as(Dp)
+
+
+def _pp(mats):
+    arr = (Dp * len(mats))(*[_p(m) for m in mats])
+    return ctypes.cast(arr, Dpp), arr
+
+
+def _dims(shape):
+    return (ctypes.c_int * len(shape))(*shape)
+
+
+def _chk(rc, err):
+    if rc != 0:
+        raise RefError(rc, err.value.decode(errors="replace"))
+
+
+def solve_laplace(coeffs, rhs, strategy=1, arithmetic=0, n_min=0):
+    """Returns (X, info[6]) with info = residual, discarded_imag, reduction_s,
+    recursion_s, back_transform_s, n_min (laplace.hpp:324-344)."""
+    coeffs = [_f(a) for a in coeffs]
+    rhs = _f(rhs)
+    x = np.zeros(rhs.shape, order="F")
+    info = (ctypes.c_double * 6)()
+    pp, keep = _pp(coeffs)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_solve_laplace(rhs.ndim, _dims(rhs.shape), pp, _p(rhs), strategy, arithmetic,
+                                 n_min, _p(x), info, err, 1024), err)
+    return x, list(info)
+
+
+def solve_gsylv(coeffs, c, rhs, strategy=1, arithmetic=0, n_min=0):
+    coeffs = [_f(a) for a in coeffs]
+    c = _f(c)
+    rhs = _f(rhs)
+    x = np.zeros(rhs.shape, order="F")
+    info = (ctypes.c_double * 6)()
+    pp, keep = _pp(coeffs)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_solve_gsylv(rhs.ndim, _dims(rhs.shape), pp, _p(c), _p(rhs), strategy,
+                               arithmetic, n_min, _p(x), info, err, 1024), err)
+    return x, list(info)
+
+
+def laplace_recursive(t, bt, n_min):
+    t = [_f(a) for a in t]
+    bt = _f(bt)
+    x = np.zeros(bt.shape, order="F")
+    pp, keep = _pp(t)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_laplace_recursive(bt.ndim, _dims(bt.shape), pp, _p(bt), n_min, _p(x), err,
+                                     1024), err)
+    return x
+
+
+def gsylv_recursive(t, tc, bt, n_min):
+    t = [_f(a) for a in t]
+    tc = _f(tc)
+    bt = _f(bt)
+    x = np.zeros(bt.shape, order="F")
+    pp, keep = _pp(t)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_gsylv_recursive(bt.ndim, _dims(bt.shape), pp, _p(tc), _p(bt), n_min, _p(x),
+                                   err, 1024), err)
+    return x
+
+
+def mode_multiply(x, a, mode):
+    x = _f(x)
+    a = _f(a)
+    shape = list(x.shape)
+    shape[mode] = a.shape[0]
+    y = np.zeros(shape, order="F")
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_mode_multiply(x.ndim, _dims(x.shape), _p(x), a.shape[0], _p(a), mode, _p(y),
+                                 err, 1024), err)
+    return y
+
+
+def schur(a):
+    a = _f(a)
+    n = a.shape[0]
+    u = np.zeros((n, n), order="F")
+    t = np.zeros((n, n), order="F")
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_schur(n, _p(a), _p(u), _p(t), err, 1024), err)
+    return u, t
+
+
+def qz(a, c):
+    a = _f(a)
+    c = _f(c)
+    n = a.shape[0]
+    q, z, s, t = (np.zeros((n, n), order="F") for _ in range(4))
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_qz(n, _p(a), _p(c), _p(q), _p(z), _p(s), _p(t), err, 1024), err)
+    return q, z, s, t
+
+
+def dense_solve_laplace(coeffs, rhs):
+    coeffs = [_f(a) for a in coeffs]
+    rhs = _f(rhs)
+    x = np.zeros(rhs.shape, order="F")
+    pp, keep = _pp(coeffs)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_dense_solve_laplace(rhs.ndim, _dims(rhs.shape), pp, _p(rhs), _p(x), err, 1024),
+         err)
+    return x
+
+
+def dense_solve_gsylv(coeffs, c, rhs):
+    coeffs = [_f(a) for a in coeffs]
+    c = _f(c)
+    rhs = _f(rhs)
+    x = np.zeros(rhs.shape, order="F")
+    pp, keep = _pp(coeffs)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_dense_solve_gsylv(rhs.ndim, _dims(rhs.shape), pp, _p(c), _p(rhs), _p(x), err,
+                                     1024), err)
+    return x
+
+
+def residual_laplace(coeffs, rhs, x):
+    coeffs = [_f(a) for a in coeffs]
+    rhs = _f(rhs)
+    pp, keep = _pp(coeffs)
+    return lib().ref_residual_laplace(rhs.ndim, _dims(rhs.shape), pp, _p(rhs), _p(_f(x)))
+
+
+def residual_gsylv(coeffs, c, rhs, x):
+    coeffs = [_f(a) for a in coeffs]
+    rhs = _f(rhs)
+    pp, keep = _pp(coeffs)
+    return lib().ref_residual_gsylv(rhs.ndim, _dims(rhs.shape), pp, _p(_f(c)), _p(rhs), _p(_f(x)))
+
+
+class RandomStream:
+    def __init__(self, seed):
+        self.h = lib().ref_rng_new(seed)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_rng_free(self.h)
+            self.h = None
+
+    def uniform(self):
+        return lib().ref_rng_uniform(self.h)
+
+    def normal(self):
+        return lib().ref_rng_normal(self.h)
+
+    def randn(self, n):
+        out = np.empty(n)
+        lib().ref_rng_randn(self.h, _p(out), n)
+        return out
+
+    def _unpack(self, dims, flat):
+        mats, o = [], 0
+        for n in dims:
+            mats.append(flat[o:o + n * n].reshape((n, n), order="F").copy(order="F"))
+            o += n * n
+        return mats
+
+    def reduced_laplace(self, dims):
+        """random_reduced_laplace<double> (random.hpp:195-204)."""
+        co = np.zeros(sum(n * n for n in dims))
+        rhs = np.zeros(int(np.prod(dims)))
+        lib().ref_random_reduced_laplace(self.h, len(dims), _dims(dims), _p(co), _p(rhs))
+        return self._unpack(dims, co), rhs.reshape(dims, order="F")
+
+    def laplace_problem(self, dims):
+        """random_laplace_problem<double> (random.hpp:150-163)."""
+        co = np.zeros(sum(n * n for n in dims))
+        rhs = np.zeros(int(np.prod(dims)))
+        lib().ref_random_laplace_problem(self.h, len(dims), _dims(dims), _p(co), _p(rhs))
+        return self._unpack(dims, co), rhs.reshape(dims, order="F")
+
+    def reduced_gsylv(self, dims):
+        """random_reduced_gsylv<double> (random.hpp:208-221)."""
+        co = np.zeros(sum(n * n for n in dims))
+        c = np.zeros(dims[0] ** 2)
+        rhs = np.zeros(int(np.prod(dims)))
+        lib().ref_random_reduced_gsylv(self.h, len(dims), _dims(dims), _p(co), _p(c), _p(rhs))
+        return (self._unpack(dims, co), c.reshape((dims[0],) * 2, order="F"),
+                rhs.reshape(dims, order="F"))
+
+    def gsylv_problem(self, dims):
+        """random_gsylv_problem<double> (random.hpp:167-189)."""
+        co = np.zeros(sum(n * n for n in dims))
+        c = np.zeros(dims[0] ** 2)
+        rhs = np.zeros(int(np.prod(dims)))
+        lib().ref_random_gsylv_problem(self.h, len(dims), _dims(dims), _p(co), _p(c), _p(rhs))
+        return (self._unpack(dims, co), c.reshape((dims[0],) * 2, order="F"),
+                rhs.reshape(dims, order="F"))
+
+    def quasi_triangular(self, n, diag_shift=0.0, pair_prob=0.5):
+        """randn_quasi_triangular (random.hpp:117-146)."""
+        out = np.zeros(n * n)
+        lib().ref_randn_quasi_triangular(self.h, n, diag_shift, pair_prob, _p(out))
+        return out.reshape((n, n), order="F").copy(order="F")

@@ -1,0 +1,300 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product path.
+//
+// Thin extern "C" driver around the UNMODIFIED reference headers under
+// /root/reference/proj/include (compiled in place by oracle/Makefile, output
+// only to oracle/_ref/).  It exposes the reference's own entry points so the
+// pytest suite, the golden-fixture generator and bench.py's CPU baseline leg
+// can call the reference CPU solver through ctypes:
+//   solve_laplace       laplace.hpp:324-344
+//   solve_gsylv         gsylv.hpp:311-331
+//   laplace_recursive   laplace.hpp:185-195
+//   gsylv_recursive     gsylv.hpp:149-159
+//   mode_multiply       tensor.hpp:187-231
+//   schur / qz          kernels.hpp:78-156
+//   oracle::solve       oracle.hpp:205-221
+//   oracle::residual    oracle.hpp:233-268
+//   RandomStream        random.hpp:19-62 (+ generators :64-223)
+// Status codes follow the C-ABI convention of include/tsylv_gpu.h:
+//   0 ok, 1 dimension_error, 2 singular_error, 3 factorization_error,
+//   4 std::invalid_argument (config conflict), 5 anything else.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "tsylv/gsylv.hpp"
+#include "tsylv/laplace.hpp"
+#include "tsylv/oracle.hpp"
+#include "tsylv/random.hpp"
+
+using namespace tsylv;
+
+namespace {
+
+void set_err(char* err, int errlen, const std::string& msg) {
+  if (!err || errlen <= 0) return;
+  std::strncpy(err, msg.c_str(), static_cast<std::size_t>(errlen - 1));
+  err[errlen - 1] = 0;
+}
+
+template <typename F>
+int guarded(char* err, int errlen, F&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const dimension_error& e) {
+    set_err(err, errlen, e.what());
+    return 1;
+  } catch (const singular_error& e) {
+    set_err(err, errlen, e.what());
+    return 2;
+  } catch (const factorization_error& e) {
+    set_err(err, errlen, e.what());
+    return 3;
+  } catch (const std::invalid_argument& e) {
+    set_err(err, errlen, e.what());
+    return 4;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return 5;
+  }
+}
+
+std::vector<int> dims_of(int d, const int* dims) { return {dims, dims + d}; }
+
+std::size_t numel(int d, const int* dims) {
+  std::size_t n = 1;
+  for (int i = 0; i < d; ++i) n *= static_cast<std::size_t>(dims[i]);
+  return n;
+}
+
+Matrix<double> mat(int r, int c, const double* p) {
+  return Matrix<double>(r, c, std::vector<double>(p, p + static_cast<std::size_t>(r) * c));
+}
+
+Tensor<double> ten(int d, const int* dims, const double* p) {
+  return Tensor<double>(dims_of(d, dims), std::vector<double>(p, p + numel(d, dims)));
+}
+
+void copy_out(const Tensor<double>& t, double* out) {
+  std::memcpy(out, t.data(), t.size() * sizeof(double));
+}
+
+SolverConfig make_cfg(int strategy, int arithmetic, int n_min) {
+  SolverConfig cfg;
+  cfg.n_min = n_min;
+  cfg.strategy = strategy == 0 ? Strategy::recursion_only : Strategy::merge;
+  cfg.arithmetic = arithmetic == 0 ? Arithmetic::complex_triangular
+                                   : Arithmetic::real_quasitriangular;
+  return cfg;
+}
+
+void fill_info(const SolveReport<double>& rep, double* info) {
+  if (!info) return;
+  info[0] = rep.residual;
+  info[1] = rep.discarded_imag;
+  info[2] = rep.timings.reduction_s;
+  info[3] = rep.timings.recursion_s;
+  info[4] = rep.timings.back_transform_s;
+  info[5] = rep.n_min;
+}
+
+} // namespace
+
+extern "C" {
+
+// strategy: 0 recursion_only, 1 merge; arithmetic: 0 complex, 1 real.
+int ref_solve_laplace(int d, const int* dims, const double* const* coeffs,
+                      const double* rhs, int strategy, int arithmetic,
+                      int n_min, double* x, double* info, char* err,
+                      int errlen) {
+  return guarded(err, errlen, [&] {
+    LaplaceProblem<double> p;
+    for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+    p.rhs = ten(d, dims, rhs);
+    SolveReport<double> rep = solve_laplace(p, make_cfg(strategy, arithmetic, n_min));
+    copy_out(rep.solution, x);
+    fill_info(rep, info);
+  });
+}
+
+int ref_solve_gsylv(int d, const int* dims, const double* const* coeffs,
+                    const double* c, const double* rhs, int strategy,
+                    int arithmetic, int n_min, double* x, double* info,
+                    char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GSylvProblem<double> p;
+    for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+    p.c = mat(dims[0], dims[0], c);
+    p.rhs = ten(d, dims, rhs);
+    SolveReport<double> rep = solve_gsylv(p, make_cfg(strategy, arithmetic, n_min));
+    copy_out(rep.solution, x);
+    fill_info(rep, info);
+  });
+}
+
+int ref_laplace_recursive(int d, const int* dims, const double* const* t,
+                          const double* bt, int n_min, double* x, char* err,
+                          int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> coeffs;
+    for (int m = 0; m < d; ++m) coeffs.push_back(mat(dims[m], dims[m], t[m]));
+    copy_out(laplace_recursive(coeffs, ten(d, dims, bt), n_min), x);
+  });
+}
+
+int ref_gsylv_recursive(int d, const int* dims, const double* const* t,
+                        const double* tc, const double* bt, int n_min,
+                        double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> coeffs;
+    for (int m = 0; m < d; ++m) coeffs.push_back(mat(dims[m], dims[m], t[m]));
+    copy_out(gsylv_recursive(coeffs, mat(dims[0], dims[0], tc), ten(d, dims, bt), n_min), x);
+  });
+}
+
+int ref_mode_multiply(int d, const int* dims, const double* xin, int r,
+                      const double* a, int mode, double* y, char* err,
+                      int errlen) {
+  return guarded(err, errlen, [&] {
+    copy_out(mode_multiply(ten(d, dims, xin), mat(r, dims[mode], a), mode), y);
+  });
+}
+
+int ref_schur(int n, const double* a, double* u, double* t, char* err,
+              int errlen) {
+  return guarded(err, errlen, [&] {
+    SchurFactorization<double> f = schur(mat(n, n, a));
+    std::memcpy(u, f.u.data(), f.u.size() * sizeof(double));
+    std::memcpy(t, f.t.data(), f.t.size() * sizeof(double));
+  });
+}
+
+int ref_qz(int n, const double* a, const double* c, double* q, double* z,
+           double* s, double* t, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GeneralizedSchurFactorization<double> f = qz(mat(n, n, a), mat(n, n, c));
+    std::memcpy(q, f.u.data(), f.u.size() * sizeof(double));
+    std::memcpy(z, f.z.data(), f.z.size() * sizeof(double));
+    std::memcpy(s, f.s.data(), f.s.size() * sizeof(double));
+    std::memcpy(t, f.t.data(), f.t.size() * sizeof(double));
+  });
+}
+
+int ref_dense_solve_laplace(int d, const int* dims, const double* const* coeffs,
+                            const double* rhs, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    LaplaceProblem<double> p;
+    for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+    p.rhs = ten(d, dims, rhs);
+    copy_out(oracle::solve(p), x);
+  });
+}
+
+int ref_dense_solve_gsylv(int d, const int* dims, const double* const* coeffs,
+                          const double* c, const double* rhs, double* x,
+                          char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GSylvProblem<double> p;
+    for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+    p.c = mat(dims[0], dims[0], c);
+    p.rhs = ten(d, dims, rhs);
+    copy_out(oracle::solve(p), x);
+  });
+}
+
+double ref_residual_laplace(int d, const int* dims, const double* const* coeffs,
+                            const double* rhs, const double* x) {
+  LaplaceProblem<double> p;
+  for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+  p.rhs = ten(d, dims, rhs);
+  return oracle::residual(p, ten(d, dims, x));
+}
+
+double ref_residual_gsylv(int d, const int* dims, const double* const* coeffs,
+                          const double* c, const double* rhs, const double* x) {
+  GSylvProblem<double> p;
+  for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+  p.c = mat(dims[0], dims[0], c);
+  p.rhs = ten(d, dims, rhs);
+  return oracle::residual(p, ten(d, dims, x));
+}
+
+// Solvability screen (laplace.hpp:28-43 / gsylv.hpp:31-50) on reduced
+// coefficients; returns min_abs and writes the witness slots.
+int ref_check_solvable_laplace(int d, const int* dims, const double* const* t,
+                               double tol, double* min_abs, int* witness,
+                               int* solvable, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> coeffs;
+    for (int m = 0; m < d; ++m) coeffs.push_back(mat(dims[m], dims[m], t[m]));
+    Solvability s = check_solvable_laplace(coeffs, tol);
+    *min_abs = s.min_abs;
+    *solvable = s.solvable ? 1 : 0;
+    for (std::size_t i = 0; i < s.witness.size(); ++i) witness[i] = s.witness[i];
+  });
+}
+
+// ---- RandomStream (random.hpp:19-77) ------------------------------------
+void* ref_rng_new(std::uint64_t seed) { return new RandomStream(seed); }
+void ref_rng_free(void* r) { delete static_cast<RandomStream*>(r); }
+double ref_rng_uniform(void* r) { return static_cast<RandomStream*>(r)->uniform(); }
+double ref_rng_normal(void* r) { return static_cast<RandomStream*>(r)->normal(); }
+void ref_rng_randn(void* r, double* out, std::size_t n) {
+  auto* s = static_cast<RandomStream*>(r);
+  for (std::size_t i = 0; i < n; ++i) out[i] = s->normal();
+}
+
+// Correctness-suite generators (random.hpp:79-223).  Outputs: coefficient
+// blocks packed back to back (column-major), then C (gsylv), then rhs.
+void ref_random_reduced_laplace(void* r, int d, const int* dims, double* coeffs,
+                                double* rhs) {
+  auto p = random_reduced_laplace<double>(*static_cast<RandomStream*>(r), dims_of(d, dims));
+  for (int m = 0; m < d; ++m) {
+    std::memcpy(coeffs, p.coeffs[m].data(), p.coeffs[m].size() * sizeof(double));
+    coeffs += p.coeffs[m].size();
+  }
+  copy_out(p.rhs, rhs);
+}
+
+void ref_random_laplace_problem(void* r, int d, const int* dims, double* coeffs,
+                                double* rhs) {
+  auto p = random_laplace_problem<double>(*static_cast<RandomStream*>(r), dims_of(d, dims));
+  for (int m = 0; m < d; ++m) {
+    std::memcpy(coeffs, p.coeffs[m].data(), p.coeffs[m].size() * sizeof(double));
+    coeffs += p.coeffs[m].size();
+  }
+  copy_out(p.rhs, rhs);
+}
+
+void ref_random_reduced_gsylv(void* r, int d, const int* dims, double* coeffs,
+                              double* c, double* rhs) {
+  auto p = random_reduced_gsylv<double>(*static_cast<RandomStream*>(r), dims_of(d, dims));
+  for (int m = 0; m < d; ++m) {
+    std::memcpy(coeffs, p.coeffs[m].data(), p.coeffs[m].size() * sizeof(double));
+    coeffs += p.coeffs[m].size();
+  }
+  std::memcpy(c, p.c.data(), p.c.size() * sizeof(double));
+  copy_out(p.rhs, rhs);
+}
+
+void ref_random_gsylv_problem(void* r, int d, const int* dims, double* coeffs,
+                              double* c, double* rhs) {
+  auto p = random_gsylv_problem<double>(*static_cast<RandomStream*>(r), dims_of(d, dims));
+  for (int m = 0; m < d; ++m) {
+    std::memcpy(coeffs, p.coeffs[m].data(), p.coeffs[m].size() * sizeof(double));
+    coeffs += p.coeffs[m].size();
+  }
+  std::memcpy(c, p.c.data(), p.c.size() * sizeof(double));
+  copy_out(p.rhs, rhs);
+}
+
+void ref_randn_quasi_triangular(void* r, int n, double diag_shift,
+                                double pair_prob, double* out) {
+  Matrix<double> m = randn_quasi_triangular(*static_cast<RandomStream*>(r), n,
+                                            diag_shift, pair_prob);
+  std::memcpy(out, m.data(), m.size() * sizeof(double));
+}
+
+} // extern "C"

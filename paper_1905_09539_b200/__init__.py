@@ -1,0 +1,17 @@
+"""B200-native Schur-basis solve of the tsylv reference (arXiv 1905.09539).
+
+The hot path (forward transforms, reduced quasi-triangular solve, back
+transforms) runs in hand-written sm_100a kernels inside ``libtsylv_gpu.so``;
+this package is the Python host mirror of the reference's API on top of it.
+"""
+from .api import (Arithmetic, GSylvProblem, LaplaceProblem, PhaseTimings, RandomStream,
+                  SolveReport, SolverConfig, Strategy, dimension_error, factorization_error,
+                  gpu_error, gsylv_recursive, laplace_recursive, make_problem, mode_multiply, qz,
+                  residual, schur, singular_error, solve_gsylv, solve_laplace)
+
+__all__ = [
+    "Arithmetic", "GSylvProblem", "LaplaceProblem", "PhaseTimings", "RandomStream", "SolveReport",
+    "SolverConfig", "Strategy", "dimension_error", "factorization_error", "gpu_error",
+    "gsylv_recursive", "laplace_recursive", "make_problem", "mode_multiply", "qz", "residual",
+    "schur", "singular_error", "solve_gsylv", "solve_laplace",
+]

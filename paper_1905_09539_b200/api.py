@@ -1,0 +1,311 @@
+"""Python host mirror of the reference tsylv API (proj/include/tsylv).
+
+Same names, argument meaning and error behaviour as the reference's C++ entry
+points; every call goes to the C++ drop-in facade inside ``libtsylv_gpu.so``
+(no CPU fallback).  Tensors are numpy arrays in Fortran order (mode 0 fastest,
+the reference layout, tensor.hpp:19-27); matrices are (n, n) float64 arrays.
+
+    solve_laplace(p, cfg)          laplace.hpp:324-344
+    solve_gsylv(p, cfg)            gsylv.hpp:311-331
+    laplace_recursive(T, Bt, nmin) laplace.hpp:185-195
+    gsylv_recursive(T, C, Bt, nmin) gsylv.hpp:149-159
+    mode_multiply(X, A, mode)      tensor.hpp:187-231
+    schur(A), qz(A, C)             kernels.hpp:78-156 (host LAPACK, shared setup)
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import TsgOpts, TsgReport, c_dbl_p, c_dbl_pp, c_int_p, lib
+
+
+# ---- errors (errors.hpp:13-62) ---------------------------------------------
+class dimension_error(ValueError):
+    pass
+
+
+class singular_error(RuntimeError):
+    pass
+
+
+class factorization_error(RuntimeError):
+    pass
+
+
+class gpu_error(RuntimeError):
+    pass
+
+
+def _raise(rc: int, err: ctypes.Array) -> None:
+    if rc == 0:
+        return
+    msg = err.value.decode(errors="replace")
+    if rc == 1:
+        raise dimension_error(msg)
+    if rc == 2:
+        raise singular_error(msg)
+    if rc == 3:
+        raise factorization_error(msg)
+    if rc == 4:
+        raise ValueError(msg)  # std::invalid_argument
+    raise gpu_error(msg)
+
+
+# ---- config (config.hpp:11-68) -----------------------------------------------
+class Strategy(enum.IntEnum):
+    recursion_only = 0
+    merge = 1
+
+
+class Arithmetic(enum.IntEnum):
+    complex_triangular = 0
+    real_quasitriangular = 1
+
+
+@dataclass
+class SolverConfig:
+    n_min: int = 0
+    strategy: Strategy = Strategy.merge
+    arithmetic: Arithmetic = Arithmetic.complex_triangular
+
+
+@dataclass
+class PhaseTimings:
+    reduction_s: float = 0.0
+    recursion_s: float = 0.0
+    back_transform_s: float = 0.0
+
+
+@dataclass
+class SolveReport:
+    solution: np.ndarray
+    residual: float
+    discarded_imag: float
+    timings: PhaseTimings
+    n_min: int
+    strategy: Strategy
+    gpu: dict = field(default_factory=dict)
+
+
+@dataclass
+class LaplaceProblem:
+    coeffs: list
+    rhs: np.ndarray
+
+    def order(self) -> int:
+        return len(self.coeffs)
+
+    def dims(self) -> list:
+        return [int(a.shape[0]) for a in self.coeffs]
+
+
+@dataclass
+class GSylvProblem:
+    coeffs: list
+    c: np.ndarray
+    rhs: np.ndarray
+
+    def order(self) -> int:
+        return len(self.coeffs)
+
+    def dims(self) -> list:
+        return [int(a.shape[0]) for a in self.coeffs]
+
+
+# ---- marshalling helpers -------------------------------------------------------
+def _f(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _dims(rhs: np.ndarray) -> ctypes.Array:
+    return (ctypes.c_int * rhs.ndim)(*rhs.shape)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(c_dbl_p)
+
+
+def _ptrs(mats: list):
+    arr = (c_dbl_p * len(mats))(*[_ptr(m) for m in mats])
+    return ctypes.cast(arr, c_dbl_pp), arr
+
+
+def _err():
+    return ctypes.create_string_buffer(1024)
+
+
+def _check_problem(coeffs, rhs, who):
+    if len(coeffs) < 2:
+        raise dimension_error(f"{who}: need order d >= 2")
+    if rhs.ndim != len(coeffs):
+        raise dimension_error(f"{who}: rhs order does not match coefficient count")
+    for m, a in enumerate(coeffs):
+        if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] == 0:
+            raise dimension_error(f"{who}: coefficient {m} must be square, non-empty")
+        if a.shape[0] != rhs.shape[m]:
+            raise dimension_error(f"{who}: coefficient {m} does not match rhs extent")
+
+
+def _report(x, info, cfg) -> SolveReport:
+    return SolveReport(
+        solution=x, residual=info[0], discarded_imag=info[1],
+        timings=PhaseTimings(info[2], info[3], info[4]), n_min=int(info[5]),
+        strategy=Strategy(int(cfg.strategy)),
+        gpu=dict(fwd_ms=info[6], solve_ms=info[7], back_ms=info[8], h2d_ms=info[9],
+                 d2h_ms=info[10], total_ms=info[11], flops_alg=info[12], flops_exec=info[13]))
+
+
+# ---- entry points ------------------------------------------------------------------
+def solve_laplace(p: LaplaceProblem, cfg: SolverConfig | None = None) -> SolveReport:
+    cfg = cfg or SolverConfig()
+    coeffs = [_f(a) for a in p.coeffs]
+    rhs = _f(p.rhs)
+    _check_problem(coeffs, rhs, "LaplaceProblem")
+    x = np.zeros(rhs.shape, order="F")
+    info = (ctypes.c_double * 14)()
+    pp, keep = _ptrs(coeffs)
+    err = _err()
+    rc = lib().tsylv_solve_laplace(rhs.ndim, _dims(rhs), pp, _ptr(rhs), int(cfg.strategy),
+                                   int(cfg.arithmetic), int(cfg.n_min), _ptr(x), info, err, 1024)
+    _raise(rc, err)
+    return _report(x, list(info), cfg)
+
+
+def solve_gsylv(p: GSylvProblem, cfg: SolverConfig | None = None) -> SolveReport:
+    cfg = cfg or SolverConfig()
+    coeffs = [_f(a) for a in p.coeffs]
+    c = _f(p.c)
+    rhs = _f(p.rhs)
+    _check_problem(coeffs, rhs, "GSylvProblem")
+    if c.shape != coeffs[0].shape:
+        raise dimension_error("GSylvProblem: C must be square with the order of A_0")
+    x = np.zeros(rhs.shape, order="F")
+    info = (ctypes.c_double * 14)()
+    pp, keep = _ptrs(coeffs)
+    err = _err()
+    rc = lib().tsylv_solve_gsylv(rhs.ndim, _dims(rhs), pp, _ptr(c), _ptr(rhs), int(cfg.strategy),
+                                 int(cfg.arithmetic), int(cfg.n_min), _ptr(x), info, err, 1024)
+    _raise(rc, err)
+    return _report(x, list(info), cfg)
+
+
+def laplace_recursive(coeffs: list, b: np.ndarray, n_min: int) -> np.ndarray:
+    coeffs = [_f(a) for a in coeffs]
+    b = _f(b)
+    if b.ndim != len(coeffs):
+        raise dimension_error("laplace_recursive: rhs order does not match coefficient count")
+    x = np.zeros(b.shape, order="F")
+    pp, keep = _ptrs(coeffs)
+    err = _err()
+    rc = lib().tsylv_laplace_recursive(b.ndim, _dims(b), pp, _ptr(b), int(n_min), _ptr(x), err, 1024)
+    _raise(rc, err)
+    return x
+
+
+def gsylv_recursive(coeffs: list, c: np.ndarray, b: np.ndarray, n_min: int) -> np.ndarray:
+    coeffs = [_f(a) for a in coeffs]
+    c = _f(c)
+    b = _f(b)
+    if b.ndim != len(coeffs):
+        raise dimension_error("gsylv_recursive: rhs order does not match coefficient count")
+    x = np.zeros(b.shape, order="F")
+    pp, keep = _ptrs(coeffs)
+    err = _err()
+    rc = lib().tsylv_gsylv_recursive(b.ndim, _dims(b), pp, _ptr(c), _ptr(b), int(n_min), _ptr(x),
+                                     err, 1024)
+    _raise(rc, err)
+    return x
+
+
+def mode_multiply(x: np.ndarray, a: np.ndarray, mode: int) -> np.ndarray:
+    x = _f(x)
+    a = _f(a)
+    if not 0 <= mode < x.ndim:
+        raise dimension_error("mode_multiply: mode out of range")
+    shape = list(x.shape)
+    shape[mode] = a.shape[0]
+    y = np.zeros(shape, order="F")
+    err = _err()
+    rc = lib().tsylv_mode_multiply(x.ndim, _dims(x), _ptr(x), int(a.shape[0]), _ptr(a), int(mode),
+                                   _ptr(y), err, 1024)
+    _raise(rc, err)
+    return y
+
+
+def schur(a: np.ndarray):
+    a = _f(a)
+    n = a.shape[0]
+    u = np.zeros((n, n), order="F")
+    t = np.zeros((n, n), order="F")
+    err = _err()
+    _raise(lib().tsylv_schur(n, _ptr(a), _ptr(u), _ptr(t), err, 1024), err)
+    return u, t
+
+
+def qz(a: np.ndarray, c: np.ndarray):
+    a = _f(a)
+    c = _f(c)
+    n = a.shape[0]
+    q, z, s, t = (np.zeros((n, n), order="F") for _ in range(4))
+    err = _err()
+    _raise(lib().tsylv_qz(n, _ptr(a), _ptr(c), _ptr(q), _ptr(z), _ptr(s), _ptr(t), err, 1024), err)
+    return q, z, s, t
+
+
+def residual(p, x: np.ndarray) -> float:
+    x = _f(x)
+    coeffs = [_f(a) for a in p.coeffs]
+    rhs = _f(p.rhs)
+    pp, keep = _ptrs(coeffs)
+    if isinstance(p, GSylvProblem):
+        return lib().tsylv_residual_gsylv(rhs.ndim, _dims(rhs), pp, _ptr(_f(p.c)), _ptr(rhs), _ptr(x))
+    return lib().tsylv_residual_laplace(rhs.ndim, _dims(rhs), pp, _ptr(rhs), _ptr(x))
+
+
+class RandomStream:
+    """The reference's deterministic stream (random.hpp:19-62), in C++."""
+
+    def __init__(self, seed: int):
+        self._h = lib().tsylv_rng_new(seed)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().tsylv_rng_free(self._h)
+            self._h = None
+
+    def uniform(self) -> float:
+        return lib().tsylv_rng_uniform(self._h)
+
+    def normal(self) -> float:
+        return lib().tsylv_rng_normal(self._h)
+
+    def randn(self, n: int) -> np.ndarray:
+        out = np.empty(n)
+        lib().tsylv_rng_randn(self._h, _ptr(out), n)
+        return out
+
+
+def make_problem(kind: int, dims, seed: int = 1):
+    """BASELINE.json inputs (include/tsylv/random.hpp): kind 1 convection-
+    diffusion Laplace (C1), 2 G/sqrt(n)+3I Laplace (C2-C4), 5 gsylv (C5)."""
+    dims = [int(n) for n in dims]
+    d = len(dims)
+    coeffs = np.zeros(sum(n * n for n in dims))
+    c = np.zeros(dims[0] * dims[0])
+    rhs = np.zeros(int(np.prod(dims)))
+    rc = lib().tsylv_make_problem(kind, d, (ctypes.c_int * d)(*dims), seed, _ptr(coeffs), _ptr(c),
+                                  _ptr(rhs))
+    if rc != 0:
+        raise dimension_error(f"make_problem: bad kind/dims {kind} {dims}")
+    mats, o = [], 0
+    for n in dims:
+        mats.append(coeffs[o:o + n * n].reshape((n, n), order="F").copy(order="F"))
+        o += n * n
+    rhs = rhs.reshape(dims, order="F")
+    if kind == 5:
+        return GSylvProblem(mats, c.reshape((dims[0], dims[0]), order="F").copy(order="F"), rhs)
+    return LaplaceProblem(mats, rhs)

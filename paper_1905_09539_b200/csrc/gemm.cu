@@ -1,0 +1,267 @@
+// K1/K2: strided-batched FP64 GEMM on DMMA tensor cores (sm_100a).
+//
+// Replaces the dgemm_ calls issued by tsylv::mode_multiply
+// (reference tensor.hpp:187-231 -> blas.hpp:25-41) for the forward/back
+// Schur-basis transforms, and the in-place window updates of the recursion
+// (laplace.hpp:147 `b1 -= mode_multiply(x2, A12, mu)`), as
+//
+//   C[b] = alpha * A[b] * B[b] + beta * C[b]      (column-major, "NN")
+//
+// with one batch index b (middle-mode slabs: tensor.hpp:218-229).  Every
+// mode product maps onto it with no transpose copies: mode 0 is
+// Y_(0) = A X_(0) (A small, B = the tensor), modes m > 0 are per-slab
+// Y_slab = X_slab A^T (A = the tensor slab, B = the coefficient transposed
+// on the host once).
+//
+// Design: CTA tile BM x BN x 16, 3-stage cp.async ring (L2-only .cg 16 B
+// copies, zero-fill at the edges), 8 warps each owning a WM x WN patch of
+// 8x8 DMMA accumulators in registers.  Shared-memory leading dimensions are
+// padded to 4 (mod 16) doubles so that every half-warp fragment load hits 16
+// distinct 8-byte bank pairs (conflict-free LDS.64).
+#include <cstdint>
+#include <cstdio>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace tsg {
+
+namespace {
+
+constexpr int BK = 16;
+constexpr int kStages = 3;
+
+template <int BM, int BN>
+struct GemmSmem {
+  static constexpr int LDA = BM + 4;   // A stage: [BK][LDA] (m fastest)
+  static constexpr int LDB = BK + 4;   // B stage: [BN][LDB] (k fastest)
+  static constexpr int A_ELEMS = BK * LDA;
+  static constexpr int B_ELEMS = BN * LDB;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr int BYTES = kStages * STAGE * 8;
+};
+
+template <int BM, int BN, int WM, int WN, bool VEC>
+__global__ void __launch_bounds__(256)
+dgemm_nn_kernel(GemmArgs g) {
+  using S = GemmSmem<BM, BN>;
+  constexpr int NWM = BM / WM;              // warps along M
+  static_assert((BM / WM) * (BN / WN) == 8, "8 warps");
+  constexpr int FM = WM / 8, FN = WN / 8;   // 8x8 fragments per warp
+  extern __shared__ __align__(16) double smem[];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % NWM, wn = warp / NWM;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  // Flattened grid: m-tile fastest (B-panel reuse in L2), then n-tile, batch.
+  const int64_t bid = blockIdx.x;
+  const int64_t tiles_m = (g.M + BM - 1) / BM;
+  const int64_t tiles_n = (g.N + BN - 1) / BN;
+  const int64_t mt = bid % tiles_m;
+  const int64_t nt = (bid / tiles_m) % tiles_n;
+  const int64_t bt = bid / (tiles_m * tiles_n);
+  const int m0 = static_cast<int>(mt * BM), n0 = static_cast<int>(nt * BN);
+
+  const double* __restrict__ A = g.A + bt * g.sA;
+  const double* __restrict__ B = g.B + bt * g.sB;
+  double* __restrict__ C = g.C + bt * g.sC;
+
+  auto load_stage = [&](int stage, int k0) {
+    double* sa = smem + stage * S::STAGE;
+    double* sb = sa + S::A_ELEMS;
+    if (VEC) {
+      // A: BK columns of BM contiguous doubles -> 16-byte chunks.
+      constexpr int ACH = BK * BM / 2;
+      for (int c = tid; c < ACH; c += 256) {
+        const int kk = c / (BM / 2), mm = (c % (BM / 2)) * 2;
+        const int gm = m0 + mm, gk = k0 + kk;
+        int bytes = 0;
+        const double* src = A;
+        if (gk < g.K && gm < g.M) {
+          bytes = (g.M - gm >= 2) ? 16 : 8;
+          src = A + static_cast<int64_t>(gk) * g.lda + gm;
+        }
+        cp_async16(sa + kk * S::LDA + mm, src, bytes);
+      }
+      // B: BN columns of BK contiguous doubles.
+      constexpr int BCH = BN * BK / 2;
+      for (int c = tid; c < BCH; c += 256) {
+        const int nn = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+        const int gn = n0 + nn, gk = k0 + kk;
+        int bytes = 0;
+        const double* src = B;
+        if (gn < g.N && gk < g.K) {
+          bytes = (g.K - gk >= 2) ? 16 : 8;
+          src = B + static_cast<int64_t>(gn) * g.ldb + gk;
+        }
+        cp_async16(sb + nn * S::LDB + kk, src, bytes);
+      }
+    } else {
+      for (int c = tid; c < BK * BM; c += 256) {
+        const int kk = c / BM, mm = c % BM;
+        const int gm = m0 + mm, gk = k0 + kk;
+        const bool ok = gk < g.K && gm < g.M;
+        cp_async8(sa + kk * S::LDA + mm,
+                  ok ? A + static_cast<int64_t>(gk) * g.lda + gm : A, ok ? 8 : 0);
+      }
+      for (int c = tid; c < BN * BK; c += 256) {
+        const int nn = c / BK, kk = c % BK;
+        const int gn = n0 + nn, gk = k0 + kk;
+        const bool ok = gn < g.N && gk < g.K;
+        cp_async8(sb + nn * S::LDB + kk,
+                  ok ? B + static_cast<int64_t>(gn) * g.ldb + gk : B, ok ? 8 : 0);
+      }
+    }
+  };
+
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = (g.K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nk) load_stage(s, s * BK);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + kStages - 1;
+      if (nxt < nk) load_stage(nxt % kStages, nxt * BK);
+      cp_async_commit();
+    }
+    const double* sa = smem + (kt % kStages) * S::STAGE;
+    const double* sb = sa + S::A_ELEMS;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double af[FM], bf[FN];
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+        af[i] = sa[(k4 + tq) * S::LDA + wm * WM + i * 8 + gq];
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
+        bf[j] = sb[(wn * WN + j * 8 + gq) * S::LDB + k4 + tq];
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait_all();
+
+  // Epilogue: C = alpha*acc + beta*C (beta == 0 never reads C).
+#pragma unroll
+  for (int i = 0; i < FM; ++i) {
+    const int row = m0 + wm * WM + i * 8 + gq;
+    if (row >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < FN; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + wn * WN + j * 8 + 2 * tq + h;
+        if (col >= g.N) continue;
+        double* p = C + static_cast<int64_t>(col) * g.ldc + row;
+        const double v = g.alpha * acc[i][j][h];
+        *p = (g.beta == 0.0) ? v : v + g.beta * *p;
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int WM, int WN>
+cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
+  using S = GemmSmem<BM, BN>;
+  const int64_t tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * g.batch;
+  if (tiles <= 0) return cudaSuccess;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const bool vec = (g.lda % 2 == 0) && (g.ldb % 2 == 0) && (g.sA % 2 == 0) && (g.sB % 2 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
+  if (vec) {
+    auto k = dgemm_nn_kernel<BM, BN, WM, WN, true>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
+      attr = true;
+    }
+    k<<<static_cast<unsigned>(tiles), 256, S::BYTES, st>>>(g);
+  } else {
+    auto k = dgemm_nn_kernel<BM, BN, WM, WN, false>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
+      attr = true;
+    }
+    k<<<static_cast<unsigned>(tiles), 256, S::BYTES, st>>>(g);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+  // Tile choice: the big dimension gets the 128 side; small-N slabs
+  // (middle-mode transforms with n_m <= 64) use a 64-wide N tile.
+  if (g.N <= 64 && g.M >= 128) return launch_cfg<128, 64, 32, 32>(g, st);
+  if (g.M <= 64 && g.N >= 128) return launch_cfg<64, 128, 32, 32>(g, st);
+  if (g.M <= 64 && g.N <= 64) return launch_cfg<64, 64, 32, 16>(g, st);
+  return launch_cfg<128, 128, 64, 32>(g, st);
+}
+
+}  // namespace tsg
+
+namespace tsg {
+
+cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int mode,
+                         const double* A, const double* At, int r, double alpha, double beta,
+                         cudaStream_t st, double* flops) {
+  int64_t P = 1, Q = 1;
+  for (int v = 0; v < mode; ++v) P *= dims[v];
+  for (int v = mode + 1; v < d; ++v) Q *= dims[v];
+  const int n = dims[mode];
+  GemmArgs g{};
+  g.alpha = alpha;
+  g.beta = beta;
+  if (mode == 0) {
+    // Y_(0) (r x Q) = A (r x n) * X_(0) (n x Q)      (tensor.hpp:203-210)
+    g.A = A;
+    g.B = X;
+    g.C = Y;
+    g.M = r;
+    g.N = static_cast<int>(Q);
+    g.K = n;
+    g.lda = r;
+    g.ldb = n;
+    g.ldc = r;
+    g.sA = g.sB = g.sC = 0;
+    g.batch = 1;
+    if (Q > 0x7fffffffLL) return cudaErrorInvalidValue;
+  } else {
+    // per slab q: Y_q (P x r) = X_q (P x n) * A^T (n x r)  (tensor.hpp:211-229)
+    if (P > 0x7fffffffLL) return cudaErrorInvalidValue;
+    g.A = X;
+    g.B = At;
+    g.C = Y;
+    g.M = static_cast<int>(P);
+    g.N = r;
+    g.K = n;
+    g.lda = P;
+    g.ldb = n;
+    g.ldc = P;
+    g.sA = P * n;
+    g.sB = 0;
+    g.sC = P * r;
+    g.batch = Q;
+  }
+  if (flops) *flops += 2.0 * static_cast<double>(P) * Q * n * r;
+  return dgemm_nn(g, st);
+}
+
+}  // namespace tsg

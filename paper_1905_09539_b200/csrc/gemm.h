@@ -1,0 +1,31 @@
+// Host-side interface of the DMMA batched GEMM (gemm.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tsg {
+
+// C[b] = alpha * A[b] * B[b] + beta * C[b], column-major, b in [0, batch):
+//   A[b](m,k) = A[b*sA + m + k*lda],  B[b](k,n) = B[b*sB + k + n*ldb],
+//   C[b](m,n) = C[b*sC + m + n*ldc].
+struct GemmArgs {
+  const double* A;
+  const double* B;
+  double* C;
+  int M, N, K;
+  int64_t lda, ldb, ldc;
+  int64_t sA, sB, sC;
+  int64_t batch;
+  double alpha, beta;
+};
+
+cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st);
+
+// Y = X x_mode A for a dense tensor (tensor.hpp:187-231 semantics):
+// A is r x dims[mode] column-major (device), At = A^T (n x r, device; only
+// used for mode > 0).  Y has dims[mode] replaced by r.
+cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int mode,
+                         const double* A, const double* At, int r, double alpha, double beta,
+                         cudaStream_t st, double* flops = nullptr);
+
+}  // namespace tsg

@@ -1,0 +1,224 @@
+// Flat extern "C" facade over the C++ drop-in headers (include/tsylv/), so the
+// Python host mirror (paper_1905_09539_b200/api.py) calls exactly the code a
+// C++ user of the reference API gets.  Signatures mirror oracle/ref_driver.cpp
+// one-for-one, so parity tests call both sides the same way.  Status codes
+// are those of tsylv_gpu.h.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "tsylv/tsylv.hpp"
+
+using namespace tsylv;
+
+namespace {
+
+void set_err(char* err, int errlen, const std::string& m) {
+  if (!err || errlen <= 0) return;
+  std::strncpy(err, m.c_str(), static_cast<size_t>(errlen - 1));
+  err[errlen - 1] = 0;
+}
+
+template <typename F>
+int guarded(char* err, int errlen, F&& fn) {
+  try {
+    fn();
+    return TSG_OK;
+  } catch (const dimension_error& e) {
+    set_err(err, errlen, e.what());
+    return TSG_EDIM;
+  } catch (const singular_error& e) {
+    set_err(err, errlen, e.what());
+    return TSG_ESINGULAR;
+  } catch (const factorization_error& e) {
+    set_err(err, errlen, e.what());
+    return TSG_EFACT;
+  } catch (const std::invalid_argument& e) {
+    set_err(err, errlen, e.what());
+    return TSG_EINVAL;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return TSG_ECUDA;
+  }
+}
+
+std::vector<int> dv(int d, const int* dims) { return {dims, dims + d}; }
+size_t numel(int d, const int* dims) {
+  size_t n = 1;
+  for (int i = 0; i < d; ++i) n *= static_cast<size_t>(dims[i]);
+  return n;
+}
+Matrix<double> mat(int r, int c, const double* p) {
+  return Matrix<double>(r, c, std::vector<double>(p, p + static_cast<size_t>(r) * c));
+}
+Tensor<double> ten(int d, const int* dims, const double* p) {
+  return Tensor<double>(dv(d, dims), std::vector<double>(p, p + numel(d, dims)));
+}
+SolverConfig cfg_of(int strategy, int arithmetic, int n_min) {
+  SolverConfig c;
+  c.n_min = n_min;
+  c.strategy = strategy == 0 ? Strategy::recursion_only : Strategy::merge;
+  c.arithmetic = arithmetic == 0 ? Arithmetic::complex_triangular : Arithmetic::real_quasitriangular;
+  return c;
+}
+// info: residual, discarded_imag, reduction_s, recursion_s, back_transform_s,
+// n_min, gpu fwd/solve/back/h2d/d2h/total ms, flops_alg, flops_exec (14).
+void fill_info(const SolveReport<double>& r, double* info) {
+  if (!info) return;
+  const double v[14] = {r.residual, r.discarded_imag, r.timings.reduction_s, r.timings.recursion_s,
+                        r.timings.back_transform_s, static_cast<double>(r.n_min), r.gpu.fwd_ms,
+                        r.gpu.solve_ms, r.gpu.back_ms, r.gpu.h2d_ms, r.gpu.d2h_ms, r.gpu.total_ms,
+                        r.gpu.flops_alg, r.gpu.flops_exec};
+  std::memcpy(info, v, sizeof(v));
+}
+
+}  // namespace
+
+extern "C" {
+
+int tsylv_solve_laplace(int d, const int* dims, const double* const* coeffs, const double* rhs,
+                        int strategy, int arithmetic, int n_min, double* x, double* info, char* err,
+                        int errlen) {
+  return guarded(err, errlen, [&] {
+    LaplaceProblem<double> p;
+    for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+    p.rhs = ten(d, dims, rhs);
+    SolveReport<double> r = solve_laplace(p, cfg_of(strategy, arithmetic, n_min));
+    std::memcpy(x, r.solution.data(), r.solution.size() * sizeof(double));
+    fill_info(r, info);
+  });
+}
+
+int tsylv_solve_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
+                      const double* rhs, int strategy, int arithmetic, int n_min, double* x,
+                      double* info, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GSylvProblem<double> p;
+    for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+    p.c = mat(dims[0], dims[0], c);
+    p.rhs = ten(d, dims, rhs);
+    SolveReport<double> r = solve_gsylv(p, cfg_of(strategy, arithmetic, n_min));
+    std::memcpy(x, r.solution.data(), r.solution.size() * sizeof(double));
+    fill_info(r, info);
+  });
+}
+
+int tsylv_laplace_recursive(int d, const int* dims, const double* const* t, const double* bt,
+                            int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> tt;
+    for (int m = 0; m < d; ++m) tt.push_back(mat(dims[m], dims[m], t[m]));
+    Tensor<double> r = laplace_recursive(tt, ten(d, dims, bt), n_min);
+    std::memcpy(x, r.data(), r.size() * sizeof(double));
+  });
+}
+
+int tsylv_gsylv_recursive(int d, const int* dims, const double* const* t, const double* tc,
+                          const double* bt, int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> tt;
+    for (int m = 0; m < d; ++m) tt.push_back(mat(dims[m], dims[m], t[m]));
+    Tensor<double> r = gsylv_recursive(tt, mat(dims[0], dims[0], tc), ten(d, dims, bt), n_min);
+    std::memcpy(x, r.data(), r.size() * sizeof(double));
+  });
+}
+
+int tsylv_mode_multiply(int d, const int* dims, const double* xin, int r, const double* a, int mode,
+                        double* y, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Tensor<double> out = mode_multiply(ten(d, dims, xin), mat(r, dims[mode], a), mode);
+    std::memcpy(y, out.data(), out.size() * sizeof(double));
+  });
+}
+
+int tsylv_schur(int n, const double* a, double* u, double* t, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    SchurFactorization f = schur(mat(n, n, a));
+    std::memcpy(u, f.u.data(), f.u.size() * sizeof(double));
+    std::memcpy(t, f.t.data(), f.t.size() * sizeof(double));
+  });
+}
+
+int tsylv_qz(int n, const double* a, const double* c, double* q, double* z, double* s, double* t,
+             char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GeneralizedSchurFactorization f = qz(mat(n, n, a), mat(n, n, c));
+    std::memcpy(q, f.u.data(), f.u.size() * sizeof(double));
+    std::memcpy(z, f.z.data(), f.z.size() * sizeof(double));
+    std::memcpy(s, f.s.data(), f.s.size() * sizeof(double));
+    std::memcpy(t, f.t.data(), f.t.size() * sizeof(double));
+  });
+}
+
+double tsylv_residual_laplace(int d, const int* dims, const double* const* coeffs,
+                              const double* rhs, const double* x) {
+  LaplaceProblem<double> p;
+  for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+  p.rhs = ten(d, dims, rhs);
+  return residual(p, ten(d, dims, x));
+}
+
+double tsylv_residual_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
+                            const double* rhs, const double* x) {
+  GSylvProblem<double> p;
+  for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+  p.c = mat(dims[0], dims[0], c);
+  p.rhs = ten(d, dims, rhs);
+  return residual(p, ten(d, dims, x));
+}
+
+int tsylv_check_solvable_laplace(int d, const int* dims, const double* const* t, double tol,
+                                 double* min_abs, int* witness, int* solvable, char* err,
+                                 int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> tt;
+    for (int m = 0; m < d; ++m) tt.push_back(mat(dims[m], dims[m], t[m]));
+    Solvability s = check_solvable_laplace(tt, tol);
+    *min_abs = s.min_abs;
+    *solvable = s.solvable ? 1 : 0;
+    for (size_t i = 0; i < s.witness.size(); ++i) witness[i] = s.witness[i];
+  });
+}
+
+// ---- deterministic inputs (random.hpp) -----------------------------------
+void* tsylv_rng_new(std::uint64_t seed) { return new RandomStream(seed); }
+void tsylv_rng_free(void* r) { delete static_cast<RandomStream*>(r); }
+double tsylv_rng_uniform(void* r) { return static_cast<RandomStream*>(r)->uniform(); }
+double tsylv_rng_normal(void* r) { return static_cast<RandomStream*>(r)->normal(); }
+void tsylv_rng_randn(void* r, double* out, size_t n) {
+  auto* s = static_cast<RandomStream*>(r);
+  for (size_t i = 0; i < n; ++i) out[i] = s->normal();
+}
+
+// BASELINE.json configuration generator: kind 1/2 Laplace (coeffs packed
+// back to back, c unused), kind 5 gsylv.  Returns 0 or TSG_EDIM.
+int tsylv_make_problem(int kind, int d, const int* dims, std::uint64_t seed, double* coeffs,
+                       double* c, double* rhs) {
+  if (d < 2) return TSG_EDIM;
+  if (kind == 1 || kind == 2) {
+    LaplaceProblem<double> p = baseline_laplace(kind, dv(d, dims), seed);
+    for (int m = 0; m < d; ++m) {
+      std::memcpy(coeffs, p.coeffs[m].data(), p.coeffs[m].size() * sizeof(double));
+      coeffs += p.coeffs[m].size();
+    }
+    std::memcpy(rhs, p.rhs.data(), p.rhs.size() * sizeof(double));
+    return TSG_OK;
+  }
+  if (kind == 5) {
+    for (int m = 2; m < d; ++m)
+      if (dims[m] != dims[1]) return TSG_EDIM;
+    GSylvProblem<double> p = baseline_gsylv(dv(d, dims), seed);
+    for (int m = 0; m < d; ++m) {
+      std::memcpy(coeffs, p.coeffs[m].data(), p.coeffs[m].size() * sizeof(double));
+      coeffs += p.coeffs[m].size();
+    }
+    std::memcpy(c, p.c.data(), p.c.size() * sizeof(double));
+    std::memcpy(rhs, p.rhs.data(), p.rhs.size() * sizeof(double));
+    return TSG_OK;
+  }
+  return TSG_EDIM;
+}
+
+}  // extern "C"

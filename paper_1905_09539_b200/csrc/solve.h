@@ -1,0 +1,50 @@
+// Host-side interface of the reduced-form dataflow solver (solve.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tsg {
+
+constexpr int kMaxOrder = 8;
+constexpr int kEigStride = 20;  // doubles of eigen data per Schur-block start row
+
+// Reduced Laplace-like / gsylv equation on a tiled tensor, solved in place
+// by one persistent dataflow kernel (see solve.cu for the algorithm).
+struct SolveArgs {
+  int family;                   // 0 Laplace, 1 gsylv
+  int d;
+  int dims[kMaxOrder];
+  int64_t stride[kMaxOrder];    // element strides (mode 0 fastest)
+  double* X;                    // B~ on entry, X~ on exit (device)
+  // gsylv auxiliaries (family 1): chain partial products W_m of solved
+  // tiles, W[d-1] = X x_{d-1} A_{d-1}, W[m] = W[m+1] x_m A_m, W[1] = V.
+  double* W[kMaxOrder];
+  const double* T[kMaxOrder];   // quasi-triangular coefficients (device, col-major)
+  const double* Tc;             // gsylv: upper-triangular C factor (mode 0)
+  const int8_t* blk[kMaxOrder]; // per row: 0 = 1x1, 1 = first row of 2x2, 2 = second
+  const double* eig[kMaxOrder]; // per row: kEigStride doubles (valid at block starts)
+  int ntiles_mode[kMaxOrder];
+  const int* bnd[kMaxOrder];    // tile boundaries per mode (ntiles_mode+1)
+  int64_t ntiles;
+  const int* order;             // topological order of linear tile ids
+  int* flags;                   // per tile: epoch when solved
+  int* counter;                 // work queue head (zeroed before launch)
+  int* status;                  // first singular cell linear index (or INT_MAX)
+  int epoch;
+  double tiny;                  // |cell eigenvalue| <= tiny -> singular
+};
+
+struct SolveLaunchInfo {
+  int grid, block, smem_bytes, ctas_per_sm;
+};
+
+// Per-order tile caps the host tiler must honour (e_m <= emax, prod <= Emax,
+// prod/e_m <= nmax).
+struct TileCaps {
+  int emax, Emax, nmax;
+};
+TileCaps solve_caps(int family, int d);
+
+cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
+
+}  // namespace tsg

@@ -1,0 +1,54 @@
+// Small device utilities: squared Frobenius norms and fused r -= t, used by
+// the device residual (tsg_residual; reference oracle.hpp:231-268).
+#include <cstdint>
+
+#include "common.cuh"
+#include "util.h"
+
+namespace tsg {
+namespace {
+
+__global__ void sumsq_kernel(const double* __restrict__ x, int64_t n, double* out) {
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = x[i];
+    s = fma(v, v, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ double ws[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) ws[w] = s;
+  __syncthreads();
+  if (w == 0) {
+    s = lane < (blockDim.x >> 5) ? ws[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) atomicAdd(out, s);
+  }
+}
+
+__global__ void axpy_kernel(double* __restrict__ y, const double* __restrict__ x, double a,
+                            int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+
+int grid_for(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return static_cast<int>(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+}
+
+}  // namespace
+
+cudaError_t sumsq(const double* x, int64_t n, double* out_dev, cudaStream_t st) {
+  sumsq_kernel<<<grid_for(n), 256, 0, st>>>(x, n, out_dev);
+  return cudaGetLastError();
+}
+
+cudaError_t axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st) {
+  axpy_kernel<<<grid_for(n), 256, 0, st>>>(y, x, a, n);
+  return cudaGetLastError();
+}
+
+}  // namespace tsg

@@ -1,0 +1,10 @@
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tsg {
+// *out_dev += sum_i x_i^2  (out_dev must be zeroed by the caller)
+cudaError_t sumsq(const double* x, int64_t n, double* out_dev, cudaStream_t st);
+// y += a * x
+cudaError_t axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st);
+}  // namespace tsg

@@ -1,0 +1,164 @@
+"""GPU parity: the CUDA path (through the C-ABI / C++ drop-in) against the
+reference CPU solver built from its own headers (oracle/_ref), on identical
+seeded inputs.  Gates (BASELINE.json north_star): relative error <= 1e-10
+vs the reference solution, relative residual <= 1e-12."""
+import numpy as np
+import pytest
+
+from conftest import rel_diff
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-10
+RES = 1e-12
+
+
+@pytest.mark.parametrize("dims", [(7, 5), (6, 4, 5), (3, 4, 2, 5), (4, 3, 2, 3, 2), (3, 2, 2, 3, 2, 2)])
+def test_mode_multiply_matches_reference(gpu, ref, dims):
+    rs = ref.RandomStream(11)
+    x = rs.randn(int(np.prod(dims))).reshape(dims, order="F")
+    for mode in range(len(dims)):
+        for r in (dims[mode], dims[mode] + 3):
+            a = rs.randn(r * dims[mode]).reshape((r, dims[mode]), order="F")
+            want = ref.mode_multiply(x, a, mode)
+            got = gpu.mode_multiply(x, a, mode)
+            assert got.shape == want.shape
+            assert rel_diff(got, want) < 1e-14
+
+
+@pytest.mark.parametrize("dims", [(200, 37), (64, 130, 3), (300, 9, 10)])
+def test_mode_multiply_large_tiles(gpu, ref, dims):
+    rs = ref.RandomStream(12)
+    x = rs.randn(int(np.prod(dims))).reshape(dims, order="F")
+    for mode in range(len(dims)):
+        a = rs.randn(dims[mode] ** 2).reshape((dims[mode],) * 2, order="F")
+        assert rel_diff(gpu.mode_multiply(x, a, mode), ref.mode_multiply(x, a, mode)) < 1e-14
+
+
+# test_laplace.cpp:92-105 — recursion vs assembled solve on triangular input
+@pytest.mark.parametrize("dims", [(4, 5), (3, 4, 5), (6, 3, 4, 2), (2, 3, 2, 2, 3), (8, 3, 8)])
+@pytest.mark.parametrize("n_min", [1, 2, 4])
+def test_laplace_reduced_triangular(gpu, ref, dims, n_min):
+    rs = ref.RandomStream(1001)
+    t, b = rs.reduced_laplace(list(dims))
+    want = ref.dense_solve_laplace(t, b)
+    got = gpu.laplace_recursive(t, b, n_min)
+    assert rel_diff(got, want) < 1e-9
+    assert rel_diff(got, ref.laplace_recursive(t, b, n_min)) < REL
+
+
+# test_laplace.cpp:107-116 — quasi-triangular coefficients
+@pytest.mark.parametrize("n_min", [1, 3, 8])
+def test_laplace_reduced_quasi(gpu, ref, n_min):
+    rs = ref.RandomStream(1002)
+    t = [rs.quasi_triangular(n, 1.0, 0.6) for n in (7, 5, 6)]
+    b = rs.randn(7 * 5 * 6).reshape((7, 5, 6), order="F")
+    want = ref.dense_solve_laplace(t, b)
+    assert rel_diff(gpu.laplace_recursive(t, b, n_min), want) < 1e-9
+
+
+@pytest.mark.parametrize("dims", [(40, 33, 29), (64, 64, 64), (20, 18, 17, 16), (9, 8, 7, 6, 5), (6, 5, 6, 5, 4, 6)])
+def test_laplace_reduced_quasi_tiled(gpu, ref, dims):
+    """Many tiles per mode: exercises the dataflow updates and flags."""
+    rs = ref.RandomStream(1010 + len(dims))
+    t = [rs.quasi_triangular(n, 1.0, 0.9) for n in dims]
+    b = rs.randn(int(np.prod(dims))).reshape(dims, order="F")
+    want = ref.laplace_recursive(t, b, 4)
+    for nm in (0, 4):
+        got = gpu.laplace_recursive(t, b, nm if nm else 8)
+        assert rel_diff(got, want) < REL
+
+
+# test_laplace.cpp:143-163 — full pipeline, both strategies
+@pytest.mark.parametrize("dims", [(9, 8), (7, 6, 5), (4, 5, 3, 4)])
+def test_solve_laplace_pipeline(gpu, ref, dims):
+    rs = ref.RandomStream(1005)
+    coeffs, rhs = rs.laplace_problem(list(dims))
+    want = ref.dense_solve_laplace(coeffs, rhs)
+    for strat, arith in ((0, 1), (0, 0), (1, 0)):
+        cfg = gpu.SolverConfig(n_min=3, strategy=gpu.Strategy(strat), arithmetic=gpu.Arithmetic(arith))
+        rep = gpu.solve_laplace(gpu.LaplaceProblem(coeffs, rhs), cfg)
+        assert rel_diff(rep.solution, want) < 1e-9
+        assert rep.residual < RES
+        assert rep.n_min == 3
+        assert rep.discarded_imag == 0.0
+
+
+def test_solve_laplace_merge_real_rejected(gpu, ref):
+    rs = ref.RandomStream(1007)
+    coeffs, rhs = rs.laplace_problem([4, 4, 4])
+    cfg = gpu.SolverConfig(strategy=gpu.Strategy.merge, arithmetic=gpu.Arithmetic.real_quasitriangular)
+    with pytest.raises(ValueError):
+        gpu.solve_laplace(gpu.LaplaceProblem(coeffs, rhs), cfg)
+
+
+def test_solve_laplace_singular(gpu):
+    a1 = np.array([[2.0, 1.0], [1.0, 2.0]])   # eigenvalues 1, 3
+    a2 = np.array([[2.0, 3.0], [3.0, 2.0]])   # eigenvalues -1, 5
+    rhs = np.zeros((2, 2), order="F")
+    rhs[0, 0] = 1
+    with pytest.raises(gpu.singular_error):
+        gpu.solve_laplace(gpu.LaplaceProblem([a1, a2], rhs))
+
+
+def test_solve_laplace_diagonal_closed_form(gpu, ref):
+    d0, d1, d2 = [1.0, 2, 3], [4.0, 5], [6.0, 7, 8, 9]
+    rs = ref.RandomStream(1008)
+    rhs = rs.randn(24).reshape((3, 2, 4), order="F")
+    rep = gpu.solve_laplace(gpu.LaplaceProblem([np.diag(d0), np.diag(d1), np.diag(d2)], rhs))
+    want = rhs / (np.array(d0)[:, None, None] + np.array(d1)[None, :, None] + np.array(d2)[None, None, :])
+    assert np.allclose(rep.solution, want, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("kind,dims", [(1, (64, 64, 64)), (2, (48, 40, 36)), (2, (12, 10, 9, 8, 7, 6))])
+def test_solve_laplace_baseline_shapes(gpu, ref, kind, dims):
+    p = gpu.make_problem(kind, dims, seed=1)
+    want, info = ref.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
+    rep = gpu.solve_laplace(p, gpu.SolverConfig(strategy=gpu.Strategy.recursion_only,
+                                                arithmetic=gpu.Arithmetic.real_quasitriangular))
+    assert rel_diff(rep.solution, want) < REL
+    assert rep.residual < RES
+    assert ref.residual_laplace(p.coeffs, p.rhs, rep.solution) < RES
+
+
+# gsylv: test_gsylv.cpp:74-104
+@pytest.mark.parametrize("dims", [(4, 5), (3, 4, 5), (5, 3, 4, 2), (6, 5, 4, 3, 2)])
+@pytest.mark.parametrize("n_min", [2, 4])
+def test_gsylv_reduced_triangular(gpu, ref, dims, n_min):
+    rs = ref.RandomStream(2001)
+    t, c, b = rs.reduced_gsylv(list(dims))
+    want = ref.dense_solve_gsylv(t, c, b)
+    got = gpu.gsylv_recursive(t, c, b, n_min)
+    assert rel_diff(got, want) < 1e-9
+
+
+def test_gsylv_reduced_quasi(gpu, ref):
+    rs = ref.RandomStream(2002)
+    dims = (7, 5, 6)
+    t0 = rs.quasi_triangular(7, 2.0, 0.7)
+    t = [t0] + [0.3 * rs.quasi_triangular(n, 0.2, 0.7) for n in dims[1:]]
+    _, c, b = rs.reduced_gsylv(list(dims))
+    want = ref.dense_solve_gsylv(t, c, b)
+    for nm in (2, 3, 8):
+        assert rel_diff(gpu.gsylv_recursive(t, c, b, nm), want) < 1e-9
+
+
+@pytest.mark.parametrize("dims", [(3, 4), (5, 4, 3), (4, 3, 2, 3)])
+def test_solve_gsylv_pipeline(gpu, ref, dims):
+    rs = ref.RandomStream(2005)
+    coeffs, c, rhs = rs.gsylv_problem(list(dims))
+    want = ref.dense_solve_gsylv(coeffs, c, rhs)
+    rep = gpu.solve_gsylv(gpu.GSylvProblem(coeffs, c, rhs),
+                          gpu.SolverConfig(strategy=gpu.Strategy.recursion_only,
+                                           arithmetic=gpu.Arithmetic.real_quasitriangular))
+    assert rel_diff(rep.solution, want) < 1e-9
+    assert rep.residual < RES
+
+
+@pytest.mark.parametrize("dims", [(40, 8, 8, 8), (60, 12, 12, 12)])
+def test_solve_gsylv_baseline_shape(gpu, ref, dims):
+    p = gpu.make_problem(5, dims, seed=1)
+    want, info = ref.solve_gsylv(p.coeffs, p.c, p.rhs)
+    rep = gpu.solve_gsylv(p)
+    assert rel_diff(rep.solution, want) < REL
+    assert rep.residual < RES
