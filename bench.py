@@ -1,0 +1,357 @@
+"""Benchmark of the B200 Schur-basis solve (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One "step" is one full solve of the BASELINE configuration — forward
+transforms B~ = B x_m U_m^T, the reduced quasi-triangular dataflow solve,
+back transforms X = X~ x_m U_m — on synthetic seeded inputs
+(include/tsylv/random.hpp).  The Schur/QZ factors are shared host setup
+(BASELINE.json north_star) and are computed once, outside the timed region.
+
+  value : unknowns/s of the whole job with B resident in HBM (device-timed,
+          CUDA events on the library's stream, max over ranks)
+  e2e   : the same metric through the C-ABI with HOST buffers (pinned),
+          H2D + D2H inside every timed step
+  roofline : dominant kernel's algorithmic FLOP / its average launch time,
+          against the measured FP64 DMMA peak (profiles/r01_fp64_peak_probe.log)
+  cpu_baseline : the reference solver itself (oracle/_ref, built from the
+          unmodified reference headers) on the host cores, rank 0 at N=1
+
+Multi-GPU (N>1, torchrun): each rank solves its own replica of the
+configuration (weak scaling, no data-path collective yet — slab sharding is
+the next step).  `--impl reference` times the reference CPU
+solver (rank 0 only; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs (kind: 1 convection-diffusion Laplace, 2 G/sqrt(n)+3I
+# Laplace, 5 gsylv posed as coeffs {A, C^T, C^T, C^T}, c = B).
+CONFIGS = {
+    "C1": (1, (64, 64, 64), "Laplace d=3 64^3 convection-diffusion"),
+    "C2": (2, (256, 256, 256), "Laplace d=3 256^3, A_mu = G/sqrt(n)+3I"),
+    "C3": (2, (24,) * 6, "Laplace d=6 24^6, A_mu = G/sqrt(24)+3I"),
+    "C4": (2, (1024, 512, 256), "Laplace d=3 1024x512x256, A_mu = G/sqrt(n)+3I"),
+    "C5": (5, (200, 40, 40, 40), "gsylv A X + B X (C(x)C(x)C) = D, 200x64000"),
+}
+PEAK_FP64_TFLOPS = 37.07  # measured DMMA peak, profiles/r01_fp64_peak_probe.log
+METRIC = "FP64 Schur-basis solve throughput"
+UNIT = "unknowns/s"
+
+
+def flops_alg(kind: int, dims) -> tuple[float, float]:
+    """(transform FLOP, solve FLOP) credited per solve."""
+    N = float(np.prod(dims))
+    sn = float(sum(dims))
+    tr = 4.0 * N * sn
+    if kind == 5:
+        solve = N * ((dims[0] - 1) + (dims[0] + sum(dims[1:])))
+    else:
+        solve = N * sum(n - 1 for n in dims)
+    return tr, solve
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_plan(T, ctx, kind, p):
+    from paper_1905_09539_b200.plan import Plan
+    if kind == 5:
+        q, z, s, tc = T.qz(p.coeffs[0], p.c)
+        fs = [T.schur(a) for a in p.coeffs[1:]]
+        return Plan(ctx, 1, [s] + [f[1] for f in fs], [q] + [f[0] for f in fs], Tc=tc, Z=z)
+    fs = [T.schur(a) for a in p.coeffs]
+    return Plan(ctx, 0, [f[1] for f in fs], [f[0] for f in fs])
+
+
+def traffic_from_profiles(config: str):
+    """ncu dram bytes per launch of the dominant kernel, if a capture was
+    summarised into profiles/ncu_traffic.json (written from an ncu --set full
+    report of this config)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(config)
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_reference_solve(kind, dims, seed=1):
+    """One reference solve (oracle/_ref) on the box's host cores.
+    Returns (seconds like-for-like, seconds total, info, cores)."""
+    cores = os.cpu_count() or 1
+    os.environ["OPENBLAS_NUM_THREADS"] = str(cores)
+    os.environ.pop("TSYLV_THREADS", None)
+    import oracle.ref as R
+    import paper_1905_09539_b200 as T
+    p = T.make_problem(kind, dims, seed=seed)
+    t0 = time.perf_counter()
+    if kind == 5:
+        # the reference's own default (merge + complex); real recursion takes minutes at C5
+        _, info = R.solve_gsylv(p.coeffs, p.c, p.rhs, strategy=1, arithmetic=0)
+    else:
+        _, info = R.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
+    total = time.perf_counter() - t0
+    like = info[3] + info[4]  # recursion_s + back_transform_s (Schur excluded)
+    return like, total, info, cores
+
+
+def run_reference(a, rank):
+    if rank != 0:
+        return
+    kind, dims, desc = CONFIGS[a.config]
+    N = float(np.prod(dims))
+    cfg_name = "recursion_only+real_quasitriangular" if kind != 5 else "merge+complex (default)"
+    vals, tots = [], []
+    for i in range(min(a.warmup, 1) + a.steps):
+        like, total, info, cores = cpu_reference_solve(kind, dims)
+        if i >= min(a.warmup, 1):
+            vals.append(like)
+            tots.append(total)
+    t = statistics.median(vals)
+    v = N / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": min(a.warmup, 1), "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded RandomStream, BASELINE.json distributions)",
+        "config": {"workload": a.config, "desc": desc, "dims": list(dims),
+                   "reference_config": cfg_name},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"one full {a.config} solve per step ({cfg_name}); value = N / "
+                                   f"(recursion_s + back_transform_s), Schur setup excluded; "
+                                   f"median total incl. Schur {statistics.median(tots):.2f} s"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a, rank, world, local):
+    import torch
+    import paper_1905_09539_b200 as T
+    from paper_1905_09539_b200.plan import Context
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    kind, dims, desc = CONFIGS[a.config]
+    N = int(np.prod(dims))
+    p = T.make_problem(kind, dims, seed=1 + rank)
+    ctx = Context(local)
+    plan = build_plan(T, ctx, kind, p)
+    info = plan.info()
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
+    b_host = torch.from_numpy(np.ascontiguousarray(p.rhs.reshape(-1, order="F"))).pin_memory()
+    x_host = torch.empty_like(b_host).pin_memory()
+    b = b_host.cuda()
+    x = torch.empty_like(b)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (device-resident and host-buffer paths)
+    for _ in range(max(a.warmup, 3)):
+        plan.execute_device(b.data_ptr(), x.data_ptr())
+    plan.execute_host(b_host.numpy(), x_host.numpy())
+
+    # ---- device-resident timed region --------------------------------------
+    clocks = ClockSampler(local)
+    reps = []
+    barrier()
+    clocks.start()
+    time.sleep(0.2)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+    for _ in range(a.steps):
+        reps.append(plan.execute_device(b.data_ptr(), x.data_ptr()))
+    with torch.cuda.stream(stream):
+        e1.record(stream)
+    e1.synchronize()
+    clk = clocks.stop()
+    barrier()
+    ms = e0.elapsed_time(e1) / a.steps
+    launches = sum(r.kernel_launches for r in reps)
+
+    # ---- end-to-end through the C-ABI with host buffers -----------------------
+    barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        f0.record(stream)
+    for _ in range(a.steps):
+        plan.execute_host(b_host.numpy(), x_host.numpy())
+    with torch.cuda.stream(stream):
+        f1.record(stream)
+    f1.synchronize()
+    barrier()
+    ms_e2e = f0.elapsed_time(f1) / a.steps
+
+    # max over ranks
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms, ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_e2e = float(t[0]), float(t[1])
+
+    # correctness of the timed output (device residual through mode products)
+    xs = x.cpu().numpy().reshape(dims, order="F")
+    res = T.residual(p, xs)
+
+    tr_f, solve_f = flops_alg(kind, dims)
+    t_fwd = statistics.median(r.t_fwd_ms for r in reps)
+    t_solve = statistics.median(r.t_solve_ms for r in reps)
+    t_back = statistics.median(r.t_back_ms for r in reps)
+    # dominant kernel: the dataflow solve (1 launch) vs the DMMA transform GEMM
+    # (2d launches per step); achieved = algorithmic FLOP per launch / launch time
+    d = len(dims)
+    if t_solve >= t_fwd + t_back:
+        dom = {"kernel": "solve_kernel (reduced dataflow solve, K2+K3)",
+               "achieved": solve_f / (t_solve * 1e-3) / 1e12, "launch_ms": t_solve}
+    else:
+        dom = {"kernel": "dgemm_nn_kernel (mode transforms, K1)",
+               "achieved": tr_f / ((t_fwd + t_back) * 1e-3) / 1e12,
+               "launch_ms": (t_fwd + t_back) / (2 * d)}
+    traffic = traffic_from_profiles(a.config)
+    roofline = {"bound": "tensor", "achieved": dom["achieved"], "peak": PEAK_FP64_TFLOPS,
+                "unit": "TFLOP/s", "frac": dom["achieved"] / PEAK_FP64_TFLOPS,
+                "traffic": traffic, "kernel": dom["kernel"],
+                "peak_source": "measured FP64 DMMA peak (mma.sync m8n8k4 f64 loop, "
+                               "profiles/r01_fp64_peak_probe.log); MEASURED_PEAKS.json has no FP64 entry"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": world * N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded RandomStream, BASELINE.json distributions)",
+            "config": {"workload": a.config, "desc": desc, "dims": list(dims),
+                       "unknowns": N, "l2": "inputs larger than L2 (8N bytes per tensor, "
+                       "plus two N-sized work buffers, > 126 MB L2)",
+                       "parallelism": f"{world} independent replicas (no sharding)" if world > 1
+                       else "single GPU", "tiles": info["n_tiles"], "tile": info["tile"],
+                       "schur_setup": "host LAPACK dgees/dgges, outside the timed region"},
+            "phases_ms": {"forward_transforms": t_fwd, "reduced_solve": t_solve,
+                          "back_transforms": t_back},
+            "fp64_tflops_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12,
+            "frac_fp64_peak_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12 / PEAK_FP64_TFLOPS,
+            "residual": res,
+            "roofline": roofline,
+            "e2e": {"value": world * N / (ms_e2e * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+                    "ms_per_step": ms_e2e},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if world == 1 and not a.no_cpu_baseline:
+            like, total, rinfo, cores = cpu_reference_solve(kind, dims)
+            line["cpu_baseline"] = {
+                "value": N / like, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"one full {a.config} solve of the reference tsylv (oracle/_ref, "
+                          f"unmodified headers + OpenBLAS, OPENBLAS_NUM_THREADS={cores}); value = "
+                          f"N/(recursion_s+back_transform_s) = N/{like:.2f}s, Schur excluded "
+                          f"(total incl. Schur {total:.2f}s)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    rank, world, local = dist_env()
+    if a.impl == "reference":
+        run_reference(a, rank)
+    else:
+        run_ours(a, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -61,6 +61,11 @@ inline Tensor<double> randn_tensor(RandomStream& r, const std::vector<int>& dims
   return t;
 }
 
+// Elementwise m / s (division, as BASELINE.json writes G/sqrt(n)).
+inline void divide(Matrix<double>& m, double s) {
+  for (std::size_t i = 0; i < m.size(); ++i) m.data()[i] /= s;
+}
+
 inline Matrix<double> convection_diffusion(int n, double c) {
   const double h2 = static_cast<double>(n + 1) * (n + 1), h1 = c * (n + 1) / 2.0;
   Matrix<double> a(n, n);
@@ -83,7 +88,7 @@ inline LaplaceProblem<double> baseline_laplace(int kind, const std::vector<int>&
       p.coeffs.push_back(convection_diffusion(n, 0.5 + 1.5 * r.uniform()));
     } else {
       Matrix<double> g = randn_matrix(r, n, n);
-      g *= 1.0 / std::sqrt(static_cast<double>(n));
+      divide(g, std::sqrt(static_cast<double>(n)));
       for (int i = 0; i < n; ++i) g(i, i) += 3.0;
       p.coeffs.push_back(std::move(g));
     }
@@ -98,10 +103,10 @@ inline GSylvProblem<double> baseline_gsylv(const std::vector<int>& dims, std::ui
   Matrix<double> a = randn_matrix(r, n0, n0);
   Matrix<double> b = randn_matrix(r, n0, n0);
   Matrix<double> c = randn_matrix(r, nc, nc);
-  a *= 1.0 / std::sqrt(static_cast<double>(n0));
+  divide(a, std::sqrt(static_cast<double>(n0)));
   for (int i = 0; i < n0; ++i) a(i, i) += 4.0;
-  b *= 1.0 / std::sqrt(static_cast<double>(n0));
-  c *= 1.0 / (2.0 * std::sqrt(static_cast<double>(nc)));
+  divide(b, std::sqrt(static_cast<double>(n0)));
+  divide(c, 2.0 * std::sqrt(static_cast<double>(nc)));
   GSylvProblem<double> p;
   p.coeffs.push_back(std::move(a));
   const Matrix<double> ct = transposed(c);

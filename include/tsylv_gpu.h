@@ -66,6 +66,9 @@ void tsg_default_opts(tsg_opts* o);
 int tsg_create(int n_gpus, const int* device_ids, tsg_ctx** out);
 void tsg_destroy(tsg_ctx* ctx);
 const char* tsg_last_error(const tsg_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) — lets callers time execute()
+ * with CUDA events on the stream the kernels are launched on. */
+void* tsg_ctx_stream(const tsg_ctx* ctx);
 
 /* ---- Laplace-like: sum_m X x_m A_m = B  (laplace.hpp:248-302) ----------
  * Real Schur basis A_m = U_m T_m U_m^T: T[m] upper quasi-triangular,

@@ -34,7 +34,8 @@ class TsgReport(ctypes.Structure):
 
 # Every symbol include/tsylv_gpu.h declares (checked by tests/test_abi.py).
 TSG_SYMBOLS = [
-    "tsg_default_opts", "tsg_create", "tsg_destroy", "tsg_last_error", "tsg_laplace_solve",
+    "tsg_default_opts", "tsg_create", "tsg_destroy", "tsg_last_error", "tsg_ctx_stream",
+    "tsg_laplace_solve",
     "tsg_laplace_reduced", "tsg_gsylv_solve", "tsg_gsylv_reduced", "tsg_plan_create",
     "tsg_plan_execute", "tsg_plan_destroy", "tsg_plan_info", "tsg_mode_multiply",
     "tsg_residual", "tsg_abi_version",
@@ -49,6 +50,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tsg_create": (I, [I, c_int_p, ctypes.POINTER(P)]),
         "tsg_destroy": (None, [P]),
         "tsg_last_error": (E, [P]),
+        "tsg_ctx_stream": (P, [P]),
         "tsg_default_opts": (None, [ctypes.POINTER(TsgOpts)]),
         "tsg_abi_version": (I, []),
         "tsg_plan_create": (I, [P, I, I, c_int_p, c_dbl_pp, c_dbl_pp, c_dbl_p, c_dbl_p, I,

@@ -18,6 +18,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -64,7 +65,7 @@ struct tsg_plan {
   // device factors
   std::vector<DevBuf> T, Fwd, FwdT, Bwd, BwdT, eig;  // per mode
   DevBuf Tc;
-  std::vector<int8_t*> blk;
+  std::vector<tsg::TileMode*> tmode;
   std::vector<int*> bnd;
   int* order = nullptr;
   int* flags = nullptr;
@@ -76,6 +77,8 @@ struct tsg_plan {
   std::vector<DevBuf> wchain;  // gsylv W_m, m = 1..d-1
   double flops_alg = 0, flops_exec = 0;
   double tiny = 0;
+  double max_cond = 0;  // worst 2x2 eigenbasis condition (Frobenius)
+  int refine = 0;
   tsg::SolveLaunchInfo solve_info{};
   // graph cache
   cudaGraphExec_t gexec = nullptr;
@@ -83,7 +86,7 @@ struct tsg_plan {
   double* g_out = nullptr;
   int launches = 0;
   ~tsg_plan() {
-    for (auto* b : blk)
+    for (auto* b : tmode)
       if (b) cudaFree(b);
     for (auto* b : bnd)
       if (b) cudaFree(b);
@@ -149,50 +152,64 @@ std::vector<int8_t> block_codes(const double* t, int n) {
   return c;
 }
 
-// Closed-form eigen data of every 2x2 diagonal block: eigenvalues, V^{-1}, V
-// (complex, kEigStride doubles at the block's first row).  1x1 rows store
-// their diagonal entry as lambda_0.
-std::vector<double> eigen_data(const double* t, int n, const std::vector<int8_t>& code) {
-  using C = std::complex<double>;
-  std::vector<double> e(static_cast<size_t>(n) * tsg::kEigStride, 0.0);
+// Real normal form of every 2x2 diagonal block (kEigStride doubles at the
+// block's first row; layout documented in solve.cu): a complex pair is
+// W (alpha I + beta J) W^{-1} with W = [Re v, Im v] for the eigenvector v of
+// alpha + i beta; a real pair is W diag(l0, l1) W^{-1}.  1x1 rows store t_ii.
+// Returns false for a defective 2x2 block (equal real eigenvalues).
+bool normal_form(const double* t, int n, const std::vector<int8_t>& code, std::vector<double>& e,
+                 double* max_cond) {
+  e.assign(static_cast<size_t>(n) * tsg::kEigStride, 0.0);
   for (int i = 0; i < n; ++i) {
-    double* ed = e.data() + static_cast<size_t>(i) * tsg::kEigStride;
+    double* w = e.data() + static_cast<size_t>(i) * tsg::kEigStride;
     if (code[i] == 0) {
-      ed[0] = at(t, n, i, i);
-      ed[2] = 1.0;
-      ed[4] = 1.0;  // Vinv = I
-      ed[10] = 1.0;
-      ed[12] = 1.0;  // V = I
-      ed[18] = 1.0;
+      w[0] = w[1] = at(t, n, i, i);
+      w[4] = w[7] = w[8] = w[11] = 1.0;
       continue;
     }
     if (code[i] != 1) continue;
     const double a = at(t, n, i, i), b = at(t, n, i, i + 1);
     const double c = at(t, n, i + 1, i), dd = at(t, n, i + 1, i + 1);
-    const C tr = 0.5 * (a + dd);
-    const C disc = std::sqrt(C(0.25 * (a - dd) * (a - dd) + b * c, 0.0));
-    const C l0 = tr + disc, l1 = tr - disc;
-    C v00, v10, v01, v11;  // columns = eigenvectors
-    if (std::abs(b) >= std::abs(c)) {
-      v00 = b;
-      v10 = l0 - a;
-      v01 = b;
-      v11 = l1 - a;
+    const double h = 0.5 * (a + dd), disc = 0.25 * (a - dd) * (a - dd) + b * c;
+    double W[4];  // row-major
+    if (disc < 0) {
+      const double beta = std::sqrt(-disc);
+      // eigenvector of h + i beta:  (b, h - a + i beta)  or  (h - dd + i beta, c)
+      double p0, q0, p1, q1;
+      if (std::abs(b) >= std::abs(c)) {
+        p0 = b, q0 = 0.0, p1 = h - a, q1 = beta;
+      } else {
+        p0 = h - dd, q0 = beta, p1 = c, q1 = 0.0;
+      }
+      W[0] = p0, W[1] = q0, W[2] = p1, W[3] = q1;
+      w[0] = w[1] = h;
+      w[2] = beta;
+      w[3] = 1.0;
     } else {
-      v00 = l0 - dd;
-      v10 = c;
-      v01 = l1 - dd;
-      v11 = c;
+      const double r = std::sqrt(disc);
+      const double l0 = h + r, l1 = h - r;
+      if (std::abs(b) >= std::abs(c)) {
+        W[0] = b, W[1] = b, W[2] = l0 - a, W[3] = l1 - a;
+      } else {
+        W[0] = l0 - dd, W[1] = l1 - dd, W[2] = c, W[3] = c;
+      }
+      w[0] = l0;
+      w[1] = l1;
+      w[2] = 0.0;
+      w[3] = 2.0;
     }
-    const C det = v00 * v11 - v01 * v10;
-    const C i00 = v11 / det, i01 = -v01 / det, i10 = -v10 / det, i11 = v00 / det;
-    const C vals[10] = {l0, l1, i00, i01, i10, i11, v00, v01, v10, v11};
-    for (int k = 0; k < 10; ++k) {
-      ed[2 * k] = vals[k].real();
-      ed[2 * k + 1] = vals[k].imag();
+    const double det = W[0] * W[3] - W[1] * W[2];
+    const double nw = std::sqrt(W[0] * W[0] + W[1] * W[1] + W[2] * W[2] + W[3] * W[3]);
+    if (!(std::abs(det) > 1e-300) || !(std::abs(det) > 1e-14 * nw * nw)) return false;
+    const double Wi[4] = {W[3] / det, -W[1] / det, -W[2] / det, W[0] / det};
+    for (int k = 0; k < 4; ++k) {
+      w[4 + k] = Wi[k];
+      w[8 + k] = W[k];
     }
+    const double ni = std::sqrt(Wi[0] * Wi[0] + Wi[1] * Wi[1] + Wi[2] * Wi[2] + Wi[3] * Wi[3]);
+    if (max_cond) *max_cond = std::max(*max_cond, nw * ni);
   }
-  return e;
+  return true;
 }
 
 template <typename T>
@@ -296,6 +313,8 @@ void tsg_destroy(tsg_ctx* ctx) {
 
 const char* tsg_last_error(const tsg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
+void* tsg_ctx_stream(const tsg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
 int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const double* const* T,
                     const double* const* U, const double* Tc, const double* Z, int reduced_only,
                     const tsg_opts* opts, tsg_plan** out) {
@@ -338,7 +357,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   pl->Bwd.resize(d);
   pl->BwdT.resize(d);
   pl->eig.resize(d);
-  pl->blk.assign(d, nullptr);
+  pl->tmode.assign(d, nullptr);
   pl->bnd.assign(d, nullptr);
 
   double scale = 0;
@@ -348,9 +367,11 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     const size_t nn = static_cast<size_t>(n) * n;
     TSG_CU(upload_mat(pl->T[m], T[m], nn));
     codes[m] = block_codes(T[m], n);
-    TSG_CU(upload(&pl->blk[m], codes[m]));
-    TSG_CU(upload_mat(pl->eig[m], eigen_data(T[m], n, codes[m]).data(),
-                      static_cast<size_t>(n) * tsg::kEigStride));
+    std::vector<double> nf;
+    if (!normal_form(T[m], n, codes[m], nf, &pl->max_cond))
+      return fail(ctx, TSG_EDIM, "coefficient " + std::to_string(m) +
+                                     " has a defective 2x2 diagonal block (equal real eigenvalues)");
+    TSG_CU(upload_mat(pl->eig[m], nf.data(), nf.size()));
     scale += fro(T[m], nn);
     if (!reduced_only) {
       // forward: A = U^T (mode 0), At = U (m > 0); back: A = U, At = U^T.
@@ -369,6 +390,10 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     scale += fro(Tc, nn);
   }
   pl->tiny = 0.5 * std::numeric_limits<double>::epsilon() * scale;
+  // Closed-form base cells lose ~eps*cond(V); refine when some block's
+  // eigenbasis is poorly conditioned (rare for LAPACK-standardised blocks).
+  pl->refine = pl->max_cond > 1e3 ? 1 : 0;
+  if (const char* e = std::getenv("TSG_REFINE")) pl->refine = std::atoi(e);
 
   // Tiles.
   pl->tile_ext = choose_tiles(family, pl->dims, o);
@@ -380,6 +405,27 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     pl->ntiles_mode[m] = static_cast<int>(bds[m].size()) - 1;
     pl->ntiles *= pl->ntiles_mode[m];
     TSG_CU(upload(&pl->bnd[m], bds[m]));
+    std::vector<tsg::TileMode> tms(pl->ntiles_mode[m]);
+    for (int t = 0; t < pl->ntiles_mode[m]; ++t) {
+      tsg::TileMode& tmd = tms[t];
+      std::memset(&tmd, 0, sizeof(tmd));
+      tmd.start = bds[m][t];
+      const int ex = bds[m][t + 1] - bds[m][t];
+      if (ex > 255) return fail(ctx, TSG_EDIM, "tile extent too large");
+      tmd.ext = static_cast<unsigned char>(ex);
+      int nc = 0;
+      for (int r = 0; r < ex;) {
+        const int sz = codes[m][tmd.start + r] == 1 ? 2 : 1;
+        if (nc >= tsg::kMaxCells) return fail(ctx, TSG_EDIM, "too many Schur cells in a tile");
+        tmd.cs[nc] = static_cast<unsigned char>(r);
+        tmd.cz[nc] = static_cast<unsigned char>(sz);
+        if (sz == 2) tmd.pair = 1;
+        ++nc;
+        r += sz;
+      }
+      tmd.nc = static_cast<unsigned char>(nc);
+    }
+    TSG_CU(upload(&pl->tmode[m], tms));
   }
   if (pl->ntiles > INT_MAX / 2) return fail(ctx, TSG_EDIM, "too many tiles");
   // Topological order: hyperplane sum_m t_m descending.
@@ -702,7 +748,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     a.dims[m] = pl->dims[m];
     a.stride[m] = pl->stride[m];
     a.T[m] = pl->T[m].p;
-    a.blk[m] = pl->blk[m];
+    a.tmode[m] = pl->tmode[m];
     a.eig[m] = pl->eig[m].p;
     a.ntiles_mode[m] = pl->ntiles_mode[m];
     a.bnd[m] = pl->bnd[m];
@@ -717,8 +763,15 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   a.status = pl->counter + 1;
   a.epoch = 1;
   a.tiny = pl->tiny;
+  a.refine = pl->refine;
+  if (const char* e = std::getenv("TSG_DBG")) a.dbg = std::atoi(e);
   TSG_CU(tsg::launch_solve(a, st, &pl->solve_info));
   ++pl->launches;
+  if (std::getenv("TSG_VERBOSE"))
+    std::fprintf(stderr, "[tsg] solve grid=%d block=%d smem=%d ctas/sm=%d tiles=%lld refine=%d cond=%.3g\n",
+                 pl->solve_info.grid, pl->solve_info.block, pl->solve_info.smem_bytes,
+                 pl->solve_info.ctas_per_sm, static_cast<long long>(pl->ntiles), pl->refine,
+                 pl->max_cond);
   if (timing) TSG_CU(cudaEventRecord(ev[3], st));
   // Back transforms: outputs alternate (w2, out) and end in `out`.
   if (!pl->reduced_only) {

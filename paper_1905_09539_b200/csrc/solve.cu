@@ -51,7 +51,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxCells = 32;  // Schur cells per mode inside one tile
 
 template <int D, int FAM>
 struct Cfg {
@@ -60,12 +59,12 @@ struct Cfg {
   static constexpr int NBW = (D == 2) ? 1 : (D == 3 ? 4 : (D == 4 ? 8 : 16));
   static constexpr int NMAX = 64 * NBW;                         // cross-section cap
   static constexpr int KC = (D == 2) ? 16 : (D <= 4 ? 8 : 4);   // K rows per chunk
+  static constexpr int NSTAGE = 3;                              // cp.async ring depth
   static constexpr int LDB = NMAX + 4;                          // == 4 (mod 16)
   static constexpr int MPAD = 8 * MB;
   static constexpr int LDA = MPAD + 4;
   static constexpr int NWB = FAM == 0 ? 0 : D - 1;              // W buffers in smem
   static constexpr int UMAX = D > 5 ? (1 << (D - 5)) : 1;       // unknowns per lane
-  static constexpr int HMAX = D * kMaxCells;
   static constexpr int STAGE_B = KC * LDB;
   static constexpr int STAGE_A = KC * LDA;
   static constexpr int DBLK = MPAD * MPAD;                      // diag block per mode
@@ -73,12 +72,13 @@ struct Cfg {
   static constexpr int OFF_ACC = 0;
   static constexpr int OFF_W = OFF_ACC + EMAX;
   static constexpr int OFF_B = OFF_W + NWB * EMAX;
-  static constexpr int OFF_A = OFF_B + 2 * STAGE_B;
-  static constexpr int OFF_D = OFF_A + 2 * STAGE_A;
+  static constexpr int OFF_A = OFF_B + NSTAGE * STAGE_B;
+  static constexpr int OFF_D = OFF_A + NSTAGE * STAGE_A;
   static constexpr int NDBLK = FAM == 0 ? D : D + 1;            // + Tc block for gsylv
-  static constexpr int OFF_CS = OFF_D + NDBLK * DBLK;           // int64 csoff[NMAX]
+  static constexpr int OFF_EIG = OFF_D + NDBLK * DBLK;          // eigen data of tile rows
+  static constexpr int OFF_CS = OFF_EIG + D * MPAD * kEigStride; // int64 csoff[NMAX]
   static constexpr int DOUBLES = OFF_CS + NMAX;
-  static constexpr int BYTES = DOUBLES * 8 + EMAX * 2 /*cell list u16*/;
+  static constexpr int BYTES = DOUBLES * 8 + EMAX * 4 /*slot table u32*/;
 };
 
 struct TileGeom {
@@ -91,8 +91,6 @@ struct TileGeom {
   int pm[kMaxOrder], kp;  // pair modes (have a 2x2 cell), count
   int pidx[kMaxOrder];    // index j of mode m in pm, or -1
   unsigned char cs[kMaxOrder][kMaxCells], cz[kMaxOrder][kMaxCells];
-  int hoff[Cfg<8, 0>::HMAX + 2];
-  int cursor[Cfg<8, 0>::HMAX + 2];
 };
 
 struct Cplx {
@@ -111,27 +109,28 @@ TSG_DEVINL Cplx cdiv(Cplx a, Cplx b) {
 }
 
 // ---------------------------------------------------------------------------
-// Left-looking update pass:  dst -= sum_j  coef_j[rows t_m, later] x_m src_j
-// over every tile s later than t along mode m, on DMMA.  The accumulator
-// (dst restricted to the tile, M = e_m rows x N = E/e_m cross-section columns)
-// stays in registers for the whole pass.
+// Left-looking update pass over one contiguous K range of mode m:
+//   dst -= sign * sum_j coef_j[rows of t along m, k_lo:k_hi] x_m src_j[k_lo:k_hi]
+// (sign = -1 subtracts; gsylv W partials accumulate with +1).  The K range
+// is either the "far" tiles t_m+2.. (ready long before) or the nearest tile
+// t_m+1, so one flag wait covers the whole pass.  The accumulator (dst
+// restricted to the tile: M = e_m rows x N = E/e_m cross-section columns)
+// lives in registers across an NSTAGE-deep cp.async ring of K chunks.
 // ---------------------------------------------------------------------------
 template <int D, int FAM>
-TSG_DEVINL void update_pass(const SolveArgs& a, const TileGeom& tg, double* smem, double* dst,
-                            int m, const double* coef0, const double* src0,
-                            const double* coef1, const double* src1, int nsrc,
-                            double sign) {
+__device__ __noinline__ void update_pass(const SolveArgs& a, const TileGeom& tg, double* smem, double* dst,
+                            int m, int k_lo, int k_hi, int64_t wait_tile,
+                            const double* coef0, const double* src0,
+                            const double* coef1, const double* src1, int nsrc, double sign) {
   using C = Cfg<D, FAM>;
+  if (k_hi <= k_lo) return;  // uniform
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, tq = lane & 3;
-  const int tm = tg.tco[m];
-  const int pm_tiles = a.ntiles_mode[m];
-  if (tm + 1 >= pm_tiles) return;  // no later tiles along m (uniform)
-
   const int em = tg.ext[m];
   const int P = tg.tstride[m];
   const int N = tg.E / em;
   const int NB = (N + 7) >> 3;
+  const int NP = NB * 8;
   const int MBv = (em + 7) >> 3;
   const int nm = a.dims[m];
   const int64_t sm_stride = a.stride[m];
@@ -139,6 +138,10 @@ TSG_DEVINL void update_pass(const SolveArgs& a, const TileGeom& tg, double* smem
   double* sB = smem + C::OFF_B;
   double* sA = smem + C::OFF_A;
 
+  if (tid == 0 && wait_tile >= 0) {
+    const int* f = a.flags + wait_tile;
+    while (ld_acquire(f) < a.epoch) __nanosleep(32);
+  }
   // Cross-section offsets (modes != m, mode 0 fastest) of the tile.
   for (int n = tid; n < N; n += kThreads) {
     int rem = n;
@@ -154,7 +157,6 @@ TSG_DEVINL void update_pass(const SolveArgs& a, const TileGeom& tg, double* smem
   }
   __syncthreads();
 
-  // Load accumulators (C = dst restricted to rows i < em, cols n < N).
   double c[C::MB][C::NBW][2];
 #pragma unroll
   for (int ib = 0; ib < C::MB; ++ib)
@@ -171,98 +173,55 @@ TSG_DEVINL void update_pass(const SolveArgs& a, const TileGeom& tg, double* smem
         c[ib][jj][h] = v;
       }
 
-  // Chunk sequence: s from farthest to nearest, each source, K rows by KC.
-  struct Chunk {
-    int s, j, k0, kv;
-  };
-  auto first_chunk = [&](Chunk& ch) {
-    ch.s = pm_tiles - 1;
-    ch.j = 0;
-    ch.k0 = 0;
-    const int ext_s = a.bnd[m][ch.s + 1] - a.bnd[m][ch.s];
-    ch.kv = min(C::KC, ext_s);
-  };
-  auto next_chunk = [&](Chunk& ch) -> bool {
-    const int ext_s = a.bnd[m][ch.s + 1] - a.bnd[m][ch.s];
-    ch.k0 += C::KC;
-    if (ch.k0 >= ext_s) {
-      ch.k0 = 0;
-      if (++ch.j >= nsrc) {
-        ch.j = 0;
-        if (--ch.s <= tm) return false;
-      }
-    }
-    const int ext2 = a.bnd[m][ch.s + 1] - a.bnd[m][ch.s];
-    ch.kv = min(C::KC, ext2 - ch.k0);
-    return true;
-  };
-  // Neighbour tile id along m at index s.
-  auto nb_tile = [&](int s) -> int64_t {
-    int64_t mul = 1;
-    for (int v = 0; v < m; ++v) mul *= a.ntiles_mode[v];
-    return tg.lt + static_cast<int64_t>(s - tm) * mul;
-  };
-  auto issue = [&](const Chunk& ch, int buf) {
-    const double* coef = ch.j == 0 ? coef0 : coef1;
-    const double* src = ch.j == 0 ? src0 : src1;
-    const int col0 = a.bnd[m][ch.s] + ch.k0;
-    const int row0 = tg.start[m];
+  const int kr = k_hi - k_lo;
+  const int nck = (kr + C::KC - 1) / C::KC;  // chunks per source
+  const int nchunks = nck * nsrc;
+  const int row0 = tg.start[m];
+  auto issue = [&](int ci, int buf) {
+    const int j = ci / nck;
+    const int k0 = k_lo + (ci - j * nck) * C::KC;
+    const int kv = min(C::KC, k_hi - k0);
+    const double* coef = j == 0 ? coef0 : coef1;
+    const double* src = j == 0 ? src0 : src1;
     double* A = sA + buf * C::STAGE_A;
     double* B = sB + buf * C::STAGE_B;
-    // A chunk: A[k][i] = coef[(row0+i) + (col0+k)*nm]
     for (int e = tid; e < C::KC * C::MPAD; e += kThreads) {
       const int k = e / C::MPAD, i = e - k * C::MPAD;
-      const bool ok = (i < em) && (k < ch.kv);
+      const bool ok = (i < em) && (k < kv);
       cp_async8(A + k * C::LDA + i,
-                ok ? coef + (row0 + i) + static_cast<int64_t>(col0 + k) * nm : coef, ok ? 8 : 0);
+                ok ? coef + (row0 + i) + static_cast<int64_t>(k0 + k) * nm : coef, ok ? 8 : 0);
     }
-    const int NP = NB * 8;
     if (m == 0) {
-      // fibres contiguous along k
       for (int e = tid; e < C::KC * NP; e += kThreads) {
         const int n = e / C::KC, k = e - n * C::KC;
-        const bool ok = (k < ch.kv) && (n < N);
+        const bool ok = (k < kv) && (n < N);
         cp_async8(B + k * C::LDB + n,
-                  ok ? src + csoff[n] + static_cast<int64_t>(col0 + k) * sm_stride : src,
-                  ok ? 8 : 0);
+                  ok ? src + csoff[n] + static_cast<int64_t>(k0 + k) * sm_stride : src, ok ? 8 : 0);
       }
     } else {
       for (int e = tid; e < C::KC * NP; e += kThreads) {
         const int k = e / NP, n = e - k * NP;
-        const bool ok = (k < ch.kv) && (n < N);
+        const bool ok = (k < kv) && (n < N);
         cp_async8(B + k * C::LDB + n,
-                  ok ? src + csoff[n] + static_cast<int64_t>(col0 + k) * sm_stride : src,
-                  ok ? 8 : 0);
+                  ok ? src + csoff[n] + static_cast<int64_t>(k0 + k) * sm_stride : src, ok ? 8 : 0);
       }
     }
   };
 
-  __shared__ int s_waited;
-  Chunk cur, nxt;
-  first_chunk(cur);
-  if (tid == 0) {
-    const int* f = a.flags + nb_tile(cur.s);
-    while (ld_acquire(f) < a.epoch) __nanosleep(64);
-    s_waited = cur.s;
-  }
-  __syncthreads();
-  issue(cur, 0);
-  cp_async_commit();
-  int buf = 0;
-  bool more = true;
-  while (more) {
-    nxt = cur;
-    const bool has_next = next_chunk(nxt);
-    if (has_next && tid == 0 && nxt.s != s_waited) {
-      const int* f = a.flags + nb_tile(nxt.s);
-      while (ld_acquire(f) < a.epoch) __nanosleep(64);
-      s_waited = nxt.s;
-    }
-    __syncthreads();
-    if (has_next) issue(nxt, buf ^ 1);
+#pragma unroll
+  for (int st = 0; st < C::NSTAGE - 1; ++st) {
+    if (st < nchunks) issue(st, st);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int ci = 0; ci < nchunks; ++ci) {
+    cp_async_wait<C::NSTAGE - 2>();
     __syncthreads();
+    {
+      const int nx = ci + C::NSTAGE - 1;
+      if (nx < nchunks) issue(nx, nx % C::NSTAGE);
+      cp_async_commit();
+    }
+    const int buf = ci % C::NSTAGE;
     const double* A = sA + buf * C::STAGE_A;
     const double* B = sB + buf * C::STAGE_B;
 #pragma unroll
@@ -285,13 +244,9 @@ TSG_DEVINL void update_pass(const SolveArgs& a, const TileGeom& tg, double* smem
         }
       }
     }
-    cur = nxt;
-    more = has_next;
-    buf ^= 1;
   }
   cp_async_wait_all();
 
-  // Store accumulators back.
 #pragma unroll
   for (int ib = 0; ib < C::MB; ++ib)
 #pragma unroll
@@ -337,13 +292,6 @@ TSG_DEVINL void partner_r(const double (&z)[U], double (&pz)[U], int j, int LB) 
   }
 }
 
-// Per-lane view of the cell currently handled by this lane group.
-template <int D>
-struct CellView {
-  int c[D];         // cell coordinates
-  int valid;        // group has a cell this round
-};
-
 template <int D, int FAM>
 __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
   using C = Cfg<D, FAM>;
@@ -353,8 +301,11 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
   double* acc = smem + C::OFF_ACC;
   double* wbuf = smem + C::OFF_W;  // wbuf + (m-1)*EMAX for m = 1..D-1 (gsylv)
   double* dblk = smem + C::OFF_D;  // D diag blocks (+ Tc block for gsylv)
-  unsigned short* clist = reinterpret_cast<unsigned short*>(smem + C::DOUBLES);
-  const int tid = threadIdx.x, lane = tid & 31;
+  double* seig = smem + C::OFF_EIG;
+  // slot table of the (D-1)-mode cell grid: packed cell coordinates (5 bits
+  // per mode) in the low bits, coordinate sum in bits 26..31.
+  unsigned* slots = reinterpret_cast<unsigned*>(smem + C::DOUBLES);
+  const int tid = threadIdx.x;
 
   for (;;) {
     if (tid == 0) s_tile = atomicAdd(a.counter, 1);
@@ -362,50 +313,52 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
     const int qi = s_tile;
     if (qi >= a.ntiles) break;
 
-    // ---- tile geometry + Schur cells (thread 0) ---------------------------
-    if (tid == 0) {
-      const int64_t lt = a.order[qi];
-      tg.lt = lt;
-      int64_t rem = lt, gb = 0;
-      int E = 1, H = 0, ncell = 1, kp = 0;
-      for (int m = 0; m < D; ++m) {
-        const int tm = static_cast<int>(rem % a.ntiles_mode[m]);
+    // ---- tile geometry: host-built per-mode tables, loaded in parallel ------
+    if (tid < D) {
+      int64_t rem = a.order[qi];
+      int tm = 0;
+      for (int m = 0; m <= tid; ++m) {
+        tm = static_cast<int>(rem % a.ntiles_mode[m]);
         rem /= a.ntiles_mode[m];
-        tg.tco[m] = tm;
-        const int st = a.bnd[m][tm];
-        const int ex = a.bnd[m][tm + 1] - st;
-        tg.start[m] = st;
-        tg.ext[m] = ex;
+      }
+      const TileMode& src = a.tmode[tid][tm];
+      tg.tco[tid] = tm;
+      tg.start[tid] = src.start;
+      tg.ext[tid] = src.ext;
+      tg.nc[tid] = src.nc;
+      tg.pidx[tid] = src.pair;  // temporarily: pair flag
+      for (int k = 0; k < src.nc; ++k) {
+        tg.cs[tid][k] = src.cs[k];
+        tg.cz[tid][k] = src.cz[k];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int64_t lt = 0, mul = 1, gb = 0;
+      int E = 1, H = 0, kp = 0, S = 1;
+      for (int m = 0; m < D; ++m) {
+        lt += tg.tco[m] * mul;
+        mul *= a.ntiles_mode[m];
         tg.tstride[m] = E;
-        E *= ex;
-        gb += static_cast<int64_t>(st) * a.stride[m];
-        int nc = 0;
-        bool pair = false;
-        for (int r = 0; r < ex;) {
-          const int sz = (a.blk[m][st + r] == 1) ? 2 : 1;
-          tg.cs[m][nc] = static_cast<unsigned char>(r);
-          tg.cz[m][nc] = static_cast<unsigned char>(sz);
-          pair |= (sz == 2);
-          ++nc;
-          r += sz;
-        }
-        tg.nc[m] = nc;
-        ncell *= nc;
-        H += nc - 1;
+        E *= tg.ext[m];
+        gb += static_cast<int64_t>(tg.start[m]) * a.stride[m];
+        H += tg.nc[m] - 1;
+        if (m < D - 1) S *= tg.nc[m];
+        const bool pair = tg.pidx[m] != 0;
         tg.pidx[m] = pair ? kp : -1;
         if (pair) tg.pm[kp++] = m;
       }
+      tg.lt = lt;
       tg.E = E;
       tg.gbase = gb;
-      tg.ncell = ncell;
       tg.H = H;
       tg.kp = kp;
-      for (int h = 0; h <= H + 1; ++h) tg.hoff[h] = 0;
+      tg.ncell = S;  // slots of the (D-1)-mode grid
     }
     __syncthreads();
     const int E = tg.E;
 
-    // ---- gather B~_t, stage diagonal blocks, zero W partials ---------------
+    // ---- gather B~_t, stage diagonal blocks + eigen data, slot table ---------
     for (int l = tid; l < E; l += kThreads) {
       int rem = l;
       int64_t off = tg.gbase;
@@ -420,6 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
     cp_async_commit();
     for (int m = 0; m < D; ++m) {
       const int em = tg.ext[m], st = tg.start[m], nm = a.dims[m];
+      for (int e = tid; e < em * kEigStride; e += kThreads)
+        seig[m * C::MPAD * kEigStride + e] = a.eig[m][static_cast<int64_t>(st) * kEigStride + e];
       for (int e = tid; e < em * em; e += kThreads) {
         const int i = e % em, j = e / em;
         dblk[m * C::DBLK + e] = a.T[m][(st + i) + static_cast<int64_t>(st + j) * nm];
@@ -433,50 +388,62 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
       }
       for (int e = tid; e < C::NWB * E; e += kThreads) wbuf[(e / E) * C::EMAX + (e % E)] = 0.0;
     }
-    // Hyperplane histogram of the cells.
-    for (int cid = tid; cid < tg.ncell; cid += kThreads) {
-      int rem = cid, h = 0;
+    for (int sl = tid; sl < tg.ncell; sl += kThreads) {
+      int rem = sl;
+      unsigned packed = 0, sum = 0;
 #pragma unroll
-      for (int v = 0; v < D; ++v) {
-        h += rem % tg.nc[v];
+      for (int v = 0; v < D - 1; ++v) {
+        const int cv = rem % tg.nc[v];
         rem /= tg.nc[v];
+        packed |= static_cast<unsigned>(cv) << (5 * v);
+        sum += cv;
       }
-      atomicAdd(&tg.hoff[h + 1], 1);
+      slots[sl] = packed | (sum << 26);
     }
     cp_async_wait_all();
     __syncthreads();
-    if (tid == 0) {
-      for (int h = 0; h <= tg.H; ++h) {
-        tg.hoff[h + 1] += tg.hoff[h];
-        tg.cursor[h] = tg.hoff[h];
-      }
-    }
-    __syncthreads();
-    for (int cid = tid; cid < tg.ncell; cid += kThreads) {
-      int rem = cid, h = 0;
-#pragma unroll
-      for (int v = 0; v < D; ++v) {
-        h += rem % tg.nc[v];
-        rem /= tg.nc[v];
-      }
-      clist[atomicAdd(&tg.cursor[h], 1)] = static_cast<unsigned short>(cid);
-    }
 
     // ---- left-looking off-diagonal updates (DMMA) --------------------------
-    if (FAM == 0) {
-      for (int m = 0; m < D; ++m)
-        update_pass<D, FAM>(a, tg, smem, acc, m, a.T[m], a.X, nullptr, nullptr, 1, -1.0);
-    } else {
-      // mode 0: acc -= S[t0, later] x_0 X  +  Tc[t0, later] x_0 V
-      update_pass<D, FAM>(a, tg, smem, acc, 0, a.T[0], a.X, a.Tc, a.W[1], 2, -1.0);
-      // tails: W'_m = sum_{later s} A_m[t_m, s] x_m W_{m+1}   (W_D == X)
-      for (int m = 1; m < D; ++m)
-        update_pass<D, FAM>(a, tg, smem, wbuf + (m - 1) * C::EMAX, m, a.T[m],
-                            m == D - 1 ? a.X : a.W[m + 1], nullptr, nullptr, 1, 1.0);
+    // Far tiles (t_m+2 ..) of every mode first: they finished hyperplanes
+    // ago; then the nearest neighbours, which are the last to be released.
+    for (int part = 0; part < 2; ++part) {
+      int64_t mul = 1;
+      for (int m = 0; m < D; ++m) {
+        const int tm = tg.tco[m], pm = a.ntiles_mode[m];
+        const int* bm = a.bnd[m];
+        int k_lo = 0, k_hi = 0, wt = -1;
+        if (part == 0 && tm + 2 < pm) {
+          k_lo = bm[tm + 2];
+          k_hi = a.dims[m];
+          wt = tm + 2;
+        } else if (part == 1 && tm + 1 < pm) {
+          k_lo = bm[tm + 1];
+          k_hi = bm[tm + 2];
+          wt = tm + 1;
+        }
+        if (wt >= 0) {
+          const int64_t wtile = tg.lt + static_cast<int64_t>(wt - tm) * mul;
+          if (FAM == 0) {
+            update_pass<D, FAM>(a, tg, smem, acc, m, k_lo, k_hi, wtile, a.T[m], a.X, nullptr,
+                                nullptr, 1, -1.0);
+          } else if (m == 0) {
+            // acc -= S[t0, later] x_0 X  +  Tc[t0, later] x_0 V
+            update_pass<D, FAM>(a, tg, smem, acc, 0, k_lo, k_hi, wtile, a.T[0], a.X, a.Tc,
+                                a.W[1], 2, -1.0);
+          } else {
+            // W'_m += A_m[t_m, later] x_m W_{m+1}   (W_D == X)
+            update_pass<D, FAM>(a, tg, smem, wbuf + (m - 1) * C::EMAX, m, k_lo, k_hi, wtile,
+                                a.T[m], m == D - 1 ? a.X : a.W[m + 1], nullptr, nullptr, 1, 1.0);
+          }
+        }
+        mul *= pm;
+      }
     }
     __syncthreads();
 
     // ---- in-tile wavefront over Schur cells --------------------------------
+    // Hyperplane h = sum_m c_m from high to low.  Lane groups map onto the
+    // slots of the (D-1)-mode cell grid; the last coordinate follows from h.
     {
       const int kp = tg.kp;
       const int LB = kp < 5 ? kp : 5;
@@ -484,25 +451,27 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
       const int NG = kThreads / G;
       const int gid = tid / G, lig = tid & (G - 1);
       const int U = 1 << (kp > 5 ? kp - 5 : 0);
-      for (int h = tg.H; h >= 0; --h) {
-        const int cbeg = tg.hoff[h], ccount = tg.hoff[h + 1] - cbeg;
-        const int rounds = (ccount + NG - 1) / NG;
+      const int nlast = tg.nc[D - 1];
+      const int rounds = (tg.ncell + NG - 1) / NG;
+      for (int h = (a.dbg & 1) ? -1 : tg.H; h >= 0; --h) {
         for (int rd = 0; rd < rounds; ++rd) {
           const int slot = rd * NG + gid;
-          const bool gvalid = slot < ccount;
           int c[D];
+          bool gvalid = slot < tg.ncell;
           {
-            int rem = gvalid ? clist[cbeg + slot] : 0;
+            const unsigned pk = gvalid ? slots[slot] : 0u;
 #pragma unroll
-            for (int v = 0; v < D; ++v) {
-              c[v] = rem % tg.nc[v];
-              rem /= tg.nc[v];
-            }
+            for (int v = 0; v < D - 1; ++v) c[v] = (pk >> (5 * v)) & 31;
+            const int cl = h - static_cast<int>(pk >> 26);
+            gvalid = gvalid && cl >= 0 && cl < nlast;
+            c[D - 1] = gvalid ? cl : 0;
           }
+          if (!__any_sync(0xffffffffu, gvalid)) continue;  // warp-uniform skip
           // Unknowns of this lane.
           int off[C::UMAX];
           bool present[C::UMAX];
           int loc[C::UMAX][D];  // tile-local coordinates
+          int bitv[C::UMAX][D];
 #pragma unroll
           for (int u = 0; u < C::UMAX; ++u) {
             const int bits = lig | (u << LB);
@@ -510,39 +479,54 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
             int o = 0;
 #pragma unroll
             for (int v = 0; v < D; ++v) {
-              const int b = tg.pidx[v] >= 0 ? (bits >> tg.pidx[v]) & 1 : 0;
+              const int pj = tg.pidx[v];
+              const int b = pj >= 0 ? (bits >> pj) & 1 : 0;
               const int cz = tg.cz[v][c[v]];
               if (b && cz == 1) pres = false;
               const int iv = tg.cs[v][c[v]] + (cz == 2 ? b : 0);
               loc[u][v] = iv;
+              bitv[u][v] = b;
               o += iv * tg.tstride[v];
             }
             present[u] = pres;
             off[u] = o;
           }
-          // Eigen data of each pair mode's block for this cell.
-          // Residuals (left-looking in-tile dots) -------------------------
+          // In-tile left-looking dot products along mode v on buffer `src`
+          // (independent accumulators per mode and parity for ILP).
+          auto dot_mode = [&](int u, int v, const double* blk, const double* src) -> double {
+            const int em = tg.ext[v];
+            const int iv = loc[u][v];
+            const int jend = tg.cs[v][c[v]] + tg.cz[v][c[v]];
+            const int ts = tg.tstride[v];
+            const double* drow = blk + iv;
+            const double* sp = src + off[u] - iv * ts;
+            double s0 = 0.0, s1 = 0.0;
+            int j = jend;
+            for (; j + 1 < em; j += 2) {
+              s0 = fma(drow[j * em], sp[j * ts], s0);
+              s1 = fma(drow[(j + 1) * em], sp[(j + 1) * ts], s1);
+            }
+            if (j < em) s0 = fma(drow[j * em], sp[j * ts], s0);
+            return s0 + s1;
+          };
           double r[C::UMAX];
           if (FAM == 0) {
 #pragma unroll
             for (int u = 0; u < C::UMAX; ++u) {
               double s = 0.0;
               if (present[u]) {
+                double sv[D];
+#pragma unroll
+                for (int v = 0; v < D; ++v)
+                  sv[v] = (a.dbg & 2) ? 0.0 : dot_mode(u, v, dblk + v * C::DBLK, acc);
                 s = acc[off[u]];
 #pragma unroll
-                for (int v = 0; v < D; ++v) {
-                  const int em = tg.ext[v];
-                  const int iv = loc[u][v];
-                  const int jend = tg.cs[v][c[v]] + tg.cz[v][c[v]];
-                  const double* Dv = dblk + v * C::DBLK;
-                  const int ts = tg.tstride[v];
-                  for (int j = jend; j < em; ++j) s -= Dv[iv + j * em] * acc[off[u] + (j - iv) * ts];
-                }
+                for (int v = 0; v < D; ++v) s -= sv[v];
               }
               r[u] = s;
             }
           }
-          // gsylv: tail partials P_m, chain R, mode-0 residual.
+          // gsylv: tail partials P_m (external + in-tile later cells).
           double P[C::UMAX][D];
           if (FAM == 1) {
 #pragma unroll
@@ -551,25 +535,16 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
               for (int v = 1; v < D; ++v) {
                 double s = 0.0;
                 if (present[u]) {
-                  s = wbuf[(v - 1) * C::EMAX + off[u]];
                   const double* srcb = (v == D - 1) ? acc : wbuf + v * C::EMAX;
-                  const int em = tg.ext[v];
-                  const int iv = loc[u][v];
-                  const int jend = tg.cs[v][c[v]] + tg.cz[v][c[v]];
-                  const double* Dv = dblk + v * C::DBLK;
-                  const int ts = tg.tstride[v];
-                  for (int j = jend; j < em; ++j)
-                    s += Dv[iv + j * em] * srcb[off[u] + (j - iv) * ts];
+                  s = wbuf[(v - 1) * C::EMAX + off[u]] + dot_mode(u, v, dblk + v * C::DBLK, srcb);
                 }
                 P[u][v] = s;
               }
             }
           }
-          // helpers -----------------------------------------------------------
-          auto bit_of = [&](int u, int j) { return ((lig | (u << LB)) >> j) & 1; };
-          // y <- A_v,cc x_v y with the cell's diagonal block of `blk` (tile-local,
-          // ld e_v).  Shuffles are issued whenever v is a pair mode of the tile
-          // (tile-uniform), so lane groups holding 1x1 cells stay converged.
+          // y <- A_v,cc x_v y with the cell's diagonal block of `blk`.
+          // Shuffles are issued whenever v is a pair mode of the tile
+          // (tile-uniform), so groups holding 1x1 cells stay converged.
           auto cell_mode_apply = [&](double (&y)[C::UMAX], int v, const double* blk) {
             const int em = tg.ext[v];
             const int i0 = tg.cs[v][c[v]];
@@ -581,10 +556,8 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
                 const double a00 = blk[i0 + i0 * em], a01 = blk[i0 + (i0 + 1) * em];
                 const double a10 = blk[(i0 + 1) + i0 * em], a11 = blk[(i0 + 1) + (i0 + 1) * em];
 #pragma unroll
-                for (int u = 0; u < C::UMAX; ++u) {
-                  const int b = bit_of(u, j);
-                  y[u] = b == 0 ? a00 * y[u] + a01 * py[u] : a10 * py[u] + a11 * y[u];
-                }
+                for (int u = 0; u < C::UMAX; ++u)
+                  y[u] = bitv[u][v] == 0 ? a00 * y[u] + a01 * py[u] : a10 * py[u] + a11 * y[u];
                 return;
               }
             }
@@ -592,53 +565,120 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
 #pragma unroll
             for (int u = 0; u < C::UMAX; ++u) y[u] *= d0;
           };
-          // Complex butterfly with eigen data (inv: V^{-1}, else V) of pair mode v.
-          auto eig_apply = [&](Cplx (&z)[C::UMAX], int v, bool inv) {
+          // ---- closed-form cell solve in the real normal form -------------------
+          // Every 2x2 diagonal block is W (alpha I + beta J) W^{-1} with real W
+          // (J = [[0,1],[-1,0]]), or W diag(l0, l1) W^{-1} for a real pair.  In
+          // the W basis, J is diagonalised by the FIXED butterfly
+          //   zeta+ = (x0 - i x1)/2 (eigenvalue +i),  zeta- = (x0 + i x1)/2 (-i),
+          // so the cell operator sum_v A_v,cc becomes diagonal with entries
+          // s + i*omega (s, omega real sums over the modes).
+          // wd layout (kEigStride doubles at a block's first row):
+          //   [0] alpha|l0  [1] l1  [2] beta  [3] kind (0 1x1, 1 complex, 2 real)
+          //   [4..7] W^{-1} (row-major)  [8..11] W (row-major)
+          auto wd_of = [&](int v) -> const double* {
+            return seig + (v * C::MPAD + tg.cs[v][c[v]]) * kEigStride;
+          };
+          // real 2x2 transform of mode v's pair (M row-major at wd + off4)
+          auto pair_real = [&](double (&x)[C::UMAX], int v, int off4) {
+            const int j = tg.pidx[v];
+            if (j < 0) return;
+            double px[C::UMAX];
+            partner_r<C::UMAX>(x, px, j, LB);
+            if (tg.cz[v][c[v]] != 2) return;
+            const double* M = wd_of(v) + off4;
+#pragma unroll
+            for (int u = 0; u < C::UMAX; ++u)
+              x[u] = bitv[u][v] == 0 ? M[0] * x[u] + M[1] * px[u] : M[2] * px[u] + M[3] * x[u];
+          };
+          auto pair_fwd = [&](Cplx (&z)[C::UMAX], int v) {
             const int j = tg.pidx[v];
             if (j < 0) return;
             Cplx pz[C::UMAX];
             partner_c<C::UMAX>(z, pz, j, LB);
-            if (tg.cz[v][c[v]] != 2) return;
-            const double* ed = a.eig[v] + static_cast<int64_t>(tg.start[v] + tg.cs[v][c[v]]) * kEigStride;
-            const double* M = ed + (inv ? 4 : 12);
-            const Cplx m00{M[0], M[1]}, m01{M[2], M[3]}, m10{M[4], M[5]}, m11{M[6], M[7]};
+            if (tg.cz[v][c[v]] != 2 || wd_of(v)[3] != 1.0) return;
 #pragma unroll
             for (int u = 0; u < C::UMAX; ++u) {
-              const int b = bit_of(u, j);
-              z[u] = b == 0 ? cadd(cmul(m00, z[u]), cmul(m01, pz[u]))
-                            : cadd(cmul(m10, pz[u]), cmul(m11, z[u]));
+              // b=0: (z0 - i z1)/2 ; b=1: (z0 + i z1)/2 with z0 = partner
+              const Cplx o = z[u], p = pz[u];
+              z[u] = bitv[u][v] == 0 ? Cplx{0.5 * (o.re + p.im), 0.5 * (o.im - p.re)}
+                                     : Cplx{0.5 * (p.re - o.im), 0.5 * (p.im + o.re)};
             }
           };
+          auto pair_inv = [&](Cplx (&z)[C::UMAX], int v) {
+            const int j = tg.pidx[v];
+            if (j < 0) return;
+            Cplx pz[C::UMAX];
+            partner_c<C::UMAX>(z, pz, j, LB);
+            if (tg.cz[v][c[v]] != 2 || wd_of(v)[3] != 1.0) return;
+#pragma unroll
+            for (int u = 0; u < C::UMAX; ++u) {
+              // x0 = zeta+ + zeta- ; x1 = i (zeta+ - zeta-)
+              const Cplx o = z[u], p = pz[u];
+              z[u] = bitv[u][v] == 0 ? Cplx{o.re + p.re, o.im + p.im}
+                                     : Cplx{o.im - p.im, p.re - o.re};
+            }
+          };
+          // eigenvalue of mode v's cell block for unknown u (in the W basis)
           auto lam_of = [&](int u, int v) -> Cplx {
-            // eigenvalue of mode v's cell block for this unknown's bit
             const int i0 = tg.cs[v][c[v]];
             if (tg.cz[v][c[v]] == 2) {
-              const int j = tg.pidx[v];
-              const double* ed = a.eig[v] + static_cast<int64_t>(tg.start[v] + i0) * kEigStride;
-              const int b = bit_of(u, j);
-              return Cplx{ed[2 * b], ed[2 * b + 1]};
+              const double* w = wd_of(v);
+              const int b = bitv[u][v];
+              if (w[3] == 1.0) return Cplx{w[0], b ? -w[2] : w[2]};
+              return Cplx{b ? w[1] : w[0], 0.0};
             }
             return Cplx{dblk[v * C::DBLK + i0 + i0 * tg.ext[v]], 0.0};
           };
 
-          // Closed-form cell solve: y = cellop^{-1} rhs (real in, real out).
           bool singular = false;
+          // y = cellop^{-1} rhs (real in, real out).
           auto cell_solve = [&](const double (&rhs)[C::UMAX], double (&y)[C::UMAX]) {
+            if (FAM == 0 && kp == 0) {  // all-1x1 tile: one real division
+#pragma unroll
+              for (int u = 0; u < C::UMAX; ++u) {
+                double mu = 0.0;
+#pragma unroll
+                for (int v = 0; v < D; ++v) {
+                  const int i0 = tg.cs[v][c[v]];
+                  mu += dblk[v * C::DBLK + i0 + i0 * tg.ext[v]];
+                }
+                if (fabs(mu) <= a.tiny) {
+                  singular = singular || present[u];
+                  mu = 1.0;
+                }
+                y[u] = present[u] ? rhs[u] / mu : 0.0;
+              }
+              return;
+            }
+            const int v_first = (FAM == 0) ? 0 : 1;
+            double x[C::UMAX];
+#pragma unroll
+            for (int u = 0; u < C::UMAX; ++u) x[u] = rhs[u];
+#pragma unroll
+            for (int v = v_first; v < D; ++v) pair_real(x, v, 4);  // W^{-1}
             Cplx z[C::UMAX];
 #pragma unroll
-            for (int u = 0; u < C::UMAX; ++u) z[u] = Cplx{rhs[u], 0.0};
-            const int v_first = (FAM == 0) ? 0 : 1;
-            for (int v = v_first; v < D; ++v) eig_apply(z, v, true);
+            for (int u = 0; u < C::UMAX; ++u) z[u] = Cplx{x[u], 0.0};
+#pragma unroll
+            for (int v = v_first; v < D; ++v) pair_fwd(z, v);
             if (FAM == 0) {
 #pragma unroll
               for (int u = 0; u < C::UMAX; ++u) {
-                Cplx mu{0.0, 0.0};
-                for (int v = 0; v < D; ++v) mu = cadd(mu, lam_of(u, v));
-                if (fabs(mu.re) + fabs(mu.im) <= a.tiny) {
-                  singular = singular || present[u];
-                  mu = Cplx{1.0, 0.0};
+                double sr = 0.0, si = 0.0;
+#pragma unroll
+                for (int v = 0; v < D; ++v) {
+                  const Cplx l = lam_of(u, v);
+                  sr += l.re;
+                  si += l.im;
                 }
-                z[u] = cdiv(z[u], mu);
+                const double den = sr * sr + si * si;
+                if (den <= a.tiny * a.tiny) {
+                  singular = singular || present[u];
+                  z[u] = Cplx{0.0, 0.0};
+                } else {
+                  const double inv = 1.0 / den;
+                  z[u] = Cplx{(z[u].re * sr + z[u].im * si) * inv, (z[u].im * sr - z[u].re * si) * inv};
+                }
               }
             } else {
               // mode-0 pencil unit (S_cc + kappa Tc_cc) per tail eigen-index
@@ -652,6 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
 #pragma unroll
               for (int u = 0; u < C::UMAX; ++u) {
                 Cplx kappa{1.0, 0.0};
+#pragma unroll
                 for (int v = 1; v < D; ++v) kappa = cmul(kappa, lam_of(u, v));
                 auto ent = [&](int r_, int c_) {
                   return cadd(Cplx{Sb[(i0 + r_) + (i0 + c_) * e0], 0.0},
@@ -671,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
                     singular = singular || present[u];
                     det = Cplx{1.0, 0.0};
                   }
-                  const int b = bit_of(u, j0);
+                  const int b = bitv[u][0];
                   // x0 = (m11 r0 - m01 r1)/det ; x1 = (m00 r1 - m10 r0)/det
                   const Cplx r0 = b == 0 ? z[u] : pz[u];
                   const Cplx r1 = b == 0 ? pz[u] : z[u];
@@ -681,9 +722,14 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
                 }
               }
             }
-            for (int v = D - 1; v >= v_first; --v) eig_apply(z, v, false);
 #pragma unroll
-            for (int u = 0; u < C::UMAX; ++u) y[u] = present[u] ? z[u].re : 0.0;
+            for (int v = D - 1; v >= v_first; --v) pair_inv(z, v);
+#pragma unroll
+            for (int u = 0; u < C::UMAX; ++u) x[u] = z[u].re;
+#pragma unroll
+            for (int v = v_first; v < D; ++v) pair_real(x, v, 8);  // W
+#pragma unroll
+            for (int u = 0; u < C::UMAX; ++u) y[u] = present[u] ? x[u] : 0.0;
           };
           // Cell operator applied to y (real): Laplace sum_v y x_v D_v,cc;
           // gsylv y x_0 S_cc + (y x_tails A_cc) x_0 Tc_cc.
@@ -726,32 +772,27 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
             for (int u = 0; u < C::UMAX; ++u) {
               double s = 0.0;
               if (present[u]) {
-                s = acc[off[u]] - R[u];
-                const int e0 = tg.ext[0];
-                const int i0 = loc[u][0];
-                const int jend = tg.cs[0][c[0]] + tg.cz[0][c[0]];
-                const double* Sb = dblk;
-                const double* Tb = dblk + D * C::DBLK;
-                const double* Vb = wbuf;  // W_1 == V
-                for (int j = jend; j < e0; ++j) {
-                  const int o2 = off[u] + (j - i0);
-                  s -= Sb[i0 + j * e0] * acc[o2] + Tb[i0 + j * e0] * Vb[o2];
-                }
+                s = acc[off[u]] - R[u] - dot_mode(u, 0, dblk, acc) -
+                    dot_mode(u, 0, dblk + D * C::DBLK, wbuf);  // W_1 == V
               }
               r[u] = s;
             }
           }
 
-          double y[C::UMAX], res[C::UMAX], dy[C::UMAX];
+          double y[C::UMAX];
           cell_solve(r, y);
-          cell_op(y, res);
+          if (a.refine) {  // plan-uniform: some 2x2 eigenbasis is ill-conditioned
+            double res[C::UMAX], dy[C::UMAX];
+            cell_op(y, res);
 #pragma unroll
-          for (int u = 0; u < C::UMAX; ++u) res[u] = present[u] ? r[u] - res[u] : 0.0;
-          cell_solve(res, dy);
+            for (int u = 0; u < C::UMAX; ++u) res[u] = present[u] ? r[u] - res[u] : 0.0;
+            cell_solve(res, dy);
 #pragma unroll
-          for (int u = 0; u < C::UMAX; ++u) y[u] += dy[u];
+            for (int u = 0; u < C::UMAX; ++u) y[u] += dy[u];
+          }
 
-          if (singular && gvalid) atomicMin(a.status, static_cast<int>(tg.lt < 0x7f7f7f7e ? tg.lt : 0x7f7f7f7e));
+          if (singular && gvalid)
+            atomicMin(a.status, static_cast<int>(tg.lt < 0x7f7f7f7e ? tg.lt : 0x7f7f7f7e));
 #pragma unroll
           for (int u = 0; u < C::UMAX; ++u)
             if (present[u]) acc[off[u]] = y[u];
@@ -796,21 +837,24 @@ __global__ void __launch_bounds__(kThreads, 1) solve_kernel(SolveArgs a) {
       st_release(a.flags + tg.lt, a.epoch);
     }
   }
-  (void)lane;
 }
 
 template <int D, int FAM>
 cudaError_t launch_t(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
   using C = Cfg<D, FAM>;
   auto k = solve_kernel<D, FAM>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
-  if (e != cudaSuccess) return e;
-  int dev = 0, nsm = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, C::BYTES);
-  if (e != cudaSuccess) return e;
-  if (occ < 1) occ = 1;
+  // One-time per process: smem opt-in and the persistent grid size.
+  static int nsm = 0, occ = 0;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, C::BYTES);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > a.ntiles) grid = a.ntiles;
   if (grid < 1) grid = 1;

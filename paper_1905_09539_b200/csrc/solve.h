@@ -6,7 +6,17 @@
 namespace tsg {
 
 constexpr int kMaxOrder = 8;
-constexpr int kEigStride = 20;  // doubles of eigen data per Schur-block start row
+constexpr int kEigStride = 12;  // doubles of normal-form data per Schur-block start row
+
+constexpr int kMaxCells = 32;   // Schur cells per mode inside one tile
+
+// Host-built geometry of tile index t along one mode: global start, extent,
+// and its 1x1/2x2 Schur cells (start offset inside the tile, size).
+struct TileMode {
+  int start;
+  unsigned char ext, nc, pair, pad;
+  unsigned char cs[kMaxCells], cz[kMaxCells];
+};
 
 // Reduced Laplace-like / gsylv equation on a tiled tensor, solved in place
 // by one persistent dataflow kernel (see solve.cu for the algorithm).
@@ -21,7 +31,7 @@ struct SolveArgs {
   double* W[kMaxOrder];
   const double* T[kMaxOrder];   // quasi-triangular coefficients (device, col-major)
   const double* Tc;             // gsylv: upper-triangular C factor (mode 0)
-  const int8_t* blk[kMaxOrder]; // per row: 0 = 1x1, 1 = first row of 2x2, 2 = second
+  const TileMode* tmode[kMaxOrder];  // per mode: ntiles_mode entries
   const double* eig[kMaxOrder]; // per row: kEigStride doubles (valid at block starts)
   int ntiles_mode[kMaxOrder];
   const int* bnd[kMaxOrder];    // tile boundaries per mode (ntiles_mode+1)
@@ -32,6 +42,8 @@ struct SolveArgs {
   int* status;                  // first singular cell linear index (or INT_MAX)
   int epoch;
   double tiny;                  // |cell eigenvalue| <= tiny -> singular
+  int refine;                   // 1: one refinement step per base cell
+  int dbg;                      // ablation mask (development only; 0 in production)
 };
 
 struct SolveLaunchInfo {

@@ -20,6 +20,9 @@ class Context:
         if rc != 0:
             raise gpu_error(f"tsg_create failed ({rc})")
 
+    def stream_ptr(self) -> int:
+        return int(lib().tsg_ctx_stream(self.h) or 0)
+
     def error(self) -> str:
         return lib().tsg_last_error(self.h).decode()
 

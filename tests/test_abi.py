@@ -1,0 +1,84 @@
+"""CPU: the C-ABI library loads and exports every symbol include/tsylv_gpu.h
+declares; host-only entry points (RandomStream, Schur/QZ setup, screen,
+argument validation) work without a GPU."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle.restate as O
+from conftest import ROOT, rel_diff
+
+HDR = os.path.join(ROOT, "include", "tsylv_gpu.h")
+G = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1905_09539_b200._lib import TSG_SYMBOLS, lib
+    L = lib()
+    declared = set(re.findall(r"\b(tsg_[a-z_]+)\s*\(", open(HDR).read()))
+    assert declared, "no declarations parsed"
+    assert declared == set(TSG_SYMBOLS)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.tsg_abi_version() == 1
+
+
+def test_random_stream_bit_exact():
+    import paper_1905_09539_b200 as T
+    for seed in (1, 42, 987654321):
+        rs = T.RandomStream(seed)
+        assert np.array_equal(np.array([rs.uniform() for _ in range(16)]), G[f"rng{seed}_uniform"])
+        assert np.array_equal(np.array([rs.normal() for _ in range(33)]), G[f"rng{seed}_normal"])
+
+
+@pytest.mark.parametrize("name,kind", [("c1", 1), ("c2", 2), ("c3", 2), ("c4", 2), ("c5", 5)])
+def test_make_problem_bit_exact(name, kind):
+    import paper_1905_09539_b200 as T
+    dims = tuple(int(v) for v in G[f"{name}_dims"])
+    p = T.make_problem(kind, dims, seed=1)
+    for m, a in enumerate(p.coeffs):
+        assert np.array_equal(a, G[f"{name}_A{m}"])
+    assert np.array_equal(p.rhs, G[f"{name}_rhs"])
+    if kind == 5:
+        assert np.array_equal(p.c, G[f"{name}_C"])
+
+
+def test_host_schur_and_qz_contracts():
+    import paper_1905_09539_b200 as T
+    rs = O.RandomStream(3)
+    a = O.randn_matrix(rs, 9, 9)
+    c = O.randn_matrix(rs, 9, 9)
+    u, t = T.schur(a)
+    assert O.is_upper_quasi_triangular(t)
+    assert np.abs(u @ t @ u.T - a).max() < 100 * O.U * 9 * np.abs(a).max()
+    assert np.abs(u.T @ u - np.eye(9)).max() < 1e-13
+    q, z, s, tt = T.qz(a, c)
+    assert O.is_upper_quasi_triangular(s) and np.all(np.tril(tt, -1) == 0)
+    assert np.abs(q @ s @ z.T - a).max() < 1e-12 and np.abs(q @ tt @ z.T - c).max() < 1e-12
+
+
+def test_dimension_errors_are_raised_before_the_gpu():
+    import paper_1905_09539_b200 as T
+    with pytest.raises(T.dimension_error):
+        T.solve_laplace(T.LaplaceProblem([np.eye(3)], np.zeros((3,))))
+    with pytest.raises(T.dimension_error):
+        T.solve_laplace(T.LaplaceProblem([np.eye(3), np.eye(4)], np.zeros((3, 5), order="F")))
+    with pytest.raises(T.dimension_error):
+        T.solve_gsylv(T.GSylvProblem([np.eye(3), np.eye(2)], np.eye(2), np.zeros((3, 2))))
+
+
+def test_solvability_screen_host():
+    import ctypes
+    from paper_1905_09539_b200._lib import lib
+    from paper_1905_09539_b200.api import _ptrs, _f
+    t = [_f(np.diag([1.0, 2])), _f(np.diag([10.0, 20])), _f(np.diag([-21.0, 100]))]
+    pp, keep = _ptrs(t)
+    mn = ctypes.c_double()
+    wit = (ctypes.c_int * 3)()
+    ok = ctypes.c_int()
+    err = ctypes.create_string_buffer(256)
+    rc = lib().tsylv_check_solvable_laplace(3, (ctypes.c_int * 3)(2, 2, 2), pp, 0.0,
+                                            ctypes.byref(mn), wit, ctypes.byref(ok), err, 256)
+    assert rc == 0 and ok.value == 0 and list(wit) == [0, 1, 0] and mn.value == 0.0
