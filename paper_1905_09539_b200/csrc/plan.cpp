@@ -63,11 +63,14 @@ struct tsg_plan {
   std::vector<int64_t> stride;
   int64_t N = 0;
   // device factors
-  std::vector<DevBuf> T, Fwd, FwdT, Bwd, BwdT, eig;  // per mode
+  std::vector<DevBuf> T, Fwd, FwdT, Bwd, BwdT, eig, pdat;  // per mode
   DevBuf Tc;
   std::vector<tsg::TileMode*> tmode;
   std::vector<int*> bnd;
   int* order = nullptr;
+  unsigned long long* ocoord = nullptr;
+  int fast = 0;  // 1: solve_lap_kernel, 3: solve_lap3_kernel (Laplace, good eigenbases)
+  int lt3 = 3;   // log2 tile extent of solve_lap3
   int* flags = nullptr;
   int* counter = nullptr;   // [0] = queue head, [1] = status
   int64_t ntiles = 0;
@@ -91,6 +94,7 @@ struct tsg_plan {
     for (auto* b : bnd)
       if (b) cudaFree(b);
     if (order) cudaFree(order);
+    if (ocoord) cudaFree(ocoord);
     if (flags) cudaFree(flags);
     if (counter) cudaFree(counter);
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -158,13 +162,17 @@ std::vector<int8_t> block_codes(const double* t, int n) {
 // alpha + i beta; a real pair is W diag(l0, l1) W^{-1}.  1x1 rows store t_ii.
 // Returns false for a defective 2x2 block (equal real eigenvalues).
 bool normal_form(const double* t, int n, const std::vector<int8_t>& code, std::vector<double>& e,
-                 double* max_cond) {
+                 std::vector<double>& pdv, double* max_cond) {
   e.assign(static_cast<size_t>(n) * tsg::kEigStride, 0.0);
+  pdv.assign(static_cast<size_t>(n) * tsg::kPStride, 0.0);
   for (int i = 0; i < n; ++i) {
     double* w = e.data() + static_cast<size_t>(i) * tsg::kEigStride;
+    double* pr = pdv.data() + static_cast<size_t>(i) * tsg::kPStride;
     if (code[i] == 0) {
       w[0] = w[1] = at(t, n, i, i);
       w[4] = w[7] = w[8] = w[11] = 1.0;
+      pr[0] = at(t, n, i, i);
+      pr[4] = pr[10] = pr[12] = pr[18] = 1.0;  // P = Pinv = I
       continue;
     }
     if (code[i] != 1) continue;
@@ -208,6 +216,37 @@ bool normal_form(const double* t, int n, const std::vector<int8_t>& code, std::v
     }
     const double ni = std::sqrt(Wi[0] * Wi[0] + Wi[1] * Wi[1] + Wi[2] * Wi[2] + Wi[3] * Wi[3]);
     if (max_cond) *max_cond = std::max(*max_cond, nw * ni);
+    // Eigenbasis P (columns = eigenvectors), Pinv and eigenvalues, complex.
+    using Cx = std::complex<double>;
+    Cx P[4], Pi[4], L0, L1;
+    if (w[3] == 1.0) {
+      // P = W E, E = [[1, 1], [i, -i]];  Pinv = E^{-1} W^{-1}, E^{-1} = 1/2 [[1, -i], [1, i]]
+      const Cx I(0.0, 1.0);
+      P[0] = W[0] + I * W[1];
+      P[1] = W[0] - I * W[1];
+      P[2] = W[2] + I * W[3];
+      P[3] = W[2] - I * W[3];
+      Pi[0] = 0.5 * (Wi[0] - I * Wi[2]);
+      Pi[1] = 0.5 * (Wi[1] - I * Wi[3]);
+      Pi[2] = 0.5 * (Wi[0] + I * Wi[2]);
+      Pi[3] = 0.5 * (Wi[1] + I * Wi[3]);
+      L0 = Cx(w[0], w[2]);
+      L1 = Cx(w[0], -w[2]);
+    } else {
+      for (int k = 0; k < 4; ++k) {
+        P[k] = W[k];
+        Pi[k] = Wi[k];
+      }
+      L0 = w[0];
+      L1 = w[1];
+    }
+    pr[0] = L0.real(), pr[1] = L0.imag(), pr[2] = L1.real(), pr[3] = L1.imag();
+    for (int k = 0; k < 4; ++k) {
+      pr[4 + 2 * k] = P[k].real();
+      pr[5 + 2 * k] = P[k].imag();
+      pr[12 + 2 * k] = Pi[k].real();
+      pr[13 + 2 * k] = Pi[k].imag();
+    }
   }
   return true;
 }
@@ -231,9 +270,10 @@ std::vector<double> transpose(const double* a, int n) {
 }
 
 // Per-mode tile extents under the kernel caps, honouring n_min / opts.tile.
-std::vector<int> choose_tiles(int family, const std::vector<int>& dims, const tsg_opts& o) {
+std::vector<int> choose_tiles(int family, const std::vector<int>& dims, const tsg_opts& o,
+                              const tsg::TileCaps caps) {
+  (void)family;
   const int d = static_cast<int>(dims.size());
-  const tsg::TileCaps caps = tsg::solve_caps(family, d);
   std::vector<int> b(d);
   for (int m = 0; m < d; ++m) {
     int t = caps.emax;
@@ -357,6 +397,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   pl->Bwd.resize(d);
   pl->BwdT.resize(d);
   pl->eig.resize(d);
+  pl->pdat.resize(d);
   pl->tmode.assign(d, nullptr);
   pl->bnd.assign(d, nullptr);
 
@@ -367,11 +408,12 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     const size_t nn = static_cast<size_t>(n) * n;
     TSG_CU(upload_mat(pl->T[m], T[m], nn));
     codes[m] = block_codes(T[m], n);
-    std::vector<double> nf;
-    if (!normal_form(T[m], n, codes[m], nf, &pl->max_cond))
+    std::vector<double> nf, pdv;
+    if (!normal_form(T[m], n, codes[m], nf, pdv, &pl->max_cond))
       return fail(ctx, TSG_EDIM, "coefficient " + std::to_string(m) +
                                      " has a defective 2x2 diagonal block (equal real eigenvalues)");
     TSG_CU(upload_mat(pl->eig[m], nf.data(), nf.size()));
+    TSG_CU(upload_mat(pl->pdat[m], pdv.data(), pdv.size()));
     scale += fro(T[m], nn);
     if (!reduced_only) {
       // forward: A = U^T (mode 0), At = U (m > 0); back: A = U, At = U^T.
@@ -395,8 +437,18 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   pl->refine = pl->max_cond > 1e3 ? 1 : 0;
   if (const char* e = std::getenv("TSG_REFINE")) pl->refine = std::atoi(e);
 
+  // Kernel choice: the fast Laplace path needs well-conditioned eigenbases
+  // (no refinement step); gsylv and the rest use the generic kernel.
+  pl->fast = (family == 0 && !pl->refine) ? (d == 3 ? 3 : 1) : 0;
+  if (const char* e = std::getenv("TSG_FAST")) pl->fast = std::atoi(e);
+  if (pl->fast == 3 && d != 3) pl->fast = 1;
+  if (family != 0) pl->fast = 0;
+  pl->lt3 = 3;
+  if (const char* e = std::getenv("TSG_LT")) pl->lt3 = std::atoi(e) == 4 ? 4 : 3;
   // Tiles.
-  pl->tile_ext = choose_tiles(family, pl->dims, o);
+  pl->tile_ext = choose_tiles(family, pl->dims, o,
+                              pl->fast == 3 ? tsg::solve_lap3_caps(pl->lt3)
+                                            : (pl->fast ? tsg::solve_lap_caps(d) : tsg::solve_caps(family, d)));
   pl->ntiles_mode.resize(d);
   pl->ntiles = 1;
   std::vector<std::vector<int>> bds(d);
@@ -420,6 +472,11 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         tmd.cs[nc] = static_cast<unsigned char>(r);
         tmd.cz[nc] = static_cast<unsigned char>(sz);
         if (sz == 2) tmd.pair = 1;
+        for (int q = r; q < r + sz; ++q) {
+          tmd.cellof[q] = static_cast<unsigned char>(nc);
+          tmd.cend[q] = static_cast<unsigned char>(r + sz);
+        }
+        tmd.cplx[r] = sz == 2 ? 1 : 0;
         ++nc;
         r += sz;
       }
@@ -428,6 +485,8 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     TSG_CU(upload(&pl->tmode[m], tms));
   }
   if (pl->ntiles > INT_MAX / 2) return fail(ctx, TSG_EDIM, "too many tiles");
+  for (int m = 0; m < d; ++m)
+    if (pl->ntiles_mode[m] > 1024) return fail(ctx, TSG_EDIM, "more than 1024 tiles along a mode");
   // Topological order: hyperplane sum_m t_m descending.
   {
     std::vector<int> hp(pl->ntiles), ord(pl->ntiles);
@@ -443,6 +502,17 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     }
     std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return hp[x] > hp[y]; });
     TSG_CU(upload(&pl->order, ord));
+    std::vector<unsigned long long> oc(pl->ntiles);
+    for (int64_t q = 0; q < pl->ntiles; ++q) {
+      int64_t r = ord[q];
+      unsigned long long pk = 0;
+      for (int m = 0; m < d; ++m) {
+        pk |= static_cast<unsigned long long>(r % pl->ntiles_mode[m]) << (10 * m);
+        r /= pl->ntiles_mode[m];
+      }
+      oc[q] = pk;
+    }
+    TSG_CU(upload(&pl->ocoord, oc));
   }
   TSG_CU(cudaMalloc(&pl->flags, pl->ntiles * sizeof(int)));
   TSG_CU(cudaMalloc(&pl->counter, 2 * sizeof(int)));
@@ -750,6 +820,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     a.T[m] = pl->T[m].p;
     a.tmode[m] = pl->tmode[m];
     a.eig[m] = pl->eig[m].p;
+    a.pdat[m] = pl->pdat[m].p;
     a.ntiles_mode[m] = pl->ntiles_mode[m];
     a.bnd[m] = pl->bnd[m];
     if (pl->family == 1 && m >= 1) a.W[m] = pl->wchain[m].p;
@@ -758,6 +829,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   a.X = work;
   a.ntiles = pl->ntiles;
   a.order = pl->order;
+  a.ocoord = pl->ocoord;
   a.flags = pl->flags;
   a.counter = pl->counter;
   a.status = pl->counter + 1;
@@ -765,8 +837,28 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   a.tiny = pl->tiny;
   a.refine = pl->refine;
   if (const char* e = std::getenv("TSG_DBG")) a.dbg = std::atoi(e);
-  TSG_CU(tsg::launch_solve(a, st, &pl->solve_info));
+  static unsigned long long* prof = nullptr;
+  const bool want_prof = std::getenv("TSG_PROF") != nullptr;
+  if (want_prof) {
+    if (!prof) cudaMalloc(&prof, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
+    a.prof = prof;
+  }
+  if (pl->fast == 3)
+    TSG_CU(tsg::launch_solve_lap3(pl->lt3, a, st, &pl->solve_info));
+  else if (pl->fast)
+    TSG_CU(tsg::launch_solve_lap(a, st, &pl->solve_info));
+  else
+    TSG_CU(tsg::launch_solve(a, st, &pl->solve_info));
   ++pl->launches;
+  if (want_prof) {
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const double nt = h[8] ? static_cast<double>(h[8]) : 1.0;
+    std::fprintf(stderr, "[tsg prof] tiles=%.0f cycles/tile: setup %.0f stage %.0f update %.0f That+fwdT %.0f wave %.0f backT %.0f scatter %.0f | idle/queue %.0f\n",
+                 nt, h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt, h[6] / nt, h[7] / nt);
+  }
   if (std::getenv("TSG_VERBOSE"))
     std::fprintf(stderr, "[tsg] solve grid=%d block=%d smem=%d ctas/sm=%d tiles=%lld refine=%d cond=%.3g\n",
                  pl->solve_info.grid, pl->solve_info.block, pl->solve_info.smem_bytes,

@@ -7,6 +7,7 @@ namespace tsg {
 
 constexpr int kMaxOrder = 8;
 constexpr int kEigStride = 12;  // doubles of normal-form data per Schur-block start row
+constexpr int kPStride = 20;    // doubles of eigenbasis (P, Pinv, lambda) data per block row
 
 constexpr int kMaxCells = 32;   // Schur cells per mode inside one tile
 
@@ -16,6 +17,9 @@ struct TileMode {
   int start;
   unsigned char ext, nc, pair, pad;
   unsigned char cs[kMaxCells], cz[kMaxCells];
+  unsigned char cellof[kMaxCells];  // tile row -> cell index
+  unsigned char cend[kMaxCells];    // tile row -> first row after its cell
+  unsigned char cplx[kMaxCells];    // 1 on the first row of a 2x2 block
 };
 
 // Reduced Laplace-like / gsylv equation on a tiled tensor, solved in place
@@ -37,6 +41,8 @@ struct SolveArgs {
   const int* bnd[kMaxOrder];    // tile boundaries per mode (ntiles_mode+1)
   int64_t ntiles;
   const int* order;             // topological order of linear tile ids
+  const unsigned long long* ocoord;  // packed tile coordinates of order[] (10 bits/mode)
+  const double* pdat[kMaxOrder];     // per row: kPStride doubles (fast Laplace path)
   int* flags;                   // per tile: epoch when solved
   int* counter;                 // work queue head (zeroed before launch)
   int* status;                  // first singular cell linear index (or INT_MAX)
@@ -44,6 +50,7 @@ struct SolveArgs {
   double tiny;                  // |cell eigenvalue| <= tiny -> singular
   int refine;                   // 1: one refinement step per base cell
   int dbg;                      // ablation mask (development only; 0 in production)
+  unsigned long long* prof;     // optional per-phase cycle counters (development)
 };
 
 struct SolveLaunchInfo {
@@ -58,5 +65,13 @@ struct TileCaps {
 TileCaps solve_caps(int family, int d);
 
 cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
+
+// Order-3 Laplace fast path (solve_lap3.cu): padded 16^3 tiles.
+TileCaps solve_lap3_caps(int lt);  // lt = log2 tile extent (3 or 4)
+cudaError_t launch_solve_lap3(int lt, const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
+
+// Fast Laplace path (solve_lap.cu): small tiles, eigenbasis base cells.
+TileCaps solve_lap_caps(int d);
+cudaError_t launch_solve_lap(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
 
 }  // namespace tsg

@@ -1,0 +1,558 @@
+// Order-3 Laplace fast path: the dataflow solve specialised for d = 3 with a
+// compile-time padded 16x16x16 tile (C1, C2, C4 of BASELINE.json).
+//
+// Per tile (one 256-thread CTA, two CTAs per SM):
+//   1. host-packed tile coordinates -> per-mode tables (start, extent, Schur
+//      cells, row->cell maps) in one round trip; B~_t, the three diagonal
+//      blocks T_m[t,t] and the eigenbasis data are fetched with cp.async
+//      (padding rows zero-filled), so all index math is shifts and masks;
+//   2. left-looking updates  acc -= T_m[t, later] x_m X(later)  on DMMA with
+//      fragments loaded straight from L2 (each B element feeds exactly one
+//      8-row DMMA block, so shared-memory staging would buy nothing): the far
+//      tiles of all modes first (released >= 2 hyperplanes ago), then the
+//      three nearest neighbours;
+//   3. the tile moves into the eigenbasis of its diagonal Schur blocks
+//      (block-diagonal P_m^{-1} per mode, see solve_lap.cu), where the base
+//      cells decouple and the wavefront over cell hyperplanes solves every
+//      unknown independently (complex), then back with P_m;
+//   4. scatter X_t and release its flag.
+// Reference: lap_rec / lap_base (laplace.hpp:99-153), block_back_substitution
+// (kernels.hpp:179-261), mode_multiply update (laplace.hpp:147).
+#include <climits>
+#include <cstdint>
+
+#include "common.cuh"
+#include "solve.h"
+#include "solve_common.cuh"
+
+namespace tsg {
+namespace {
+
+// LT = log2 of the padded tile extent: 3 (8^3 tiles, 128 threads) or
+// 4 (16^3 tiles, 256 threads).
+template <int LT>
+struct L3C {
+  static constexpr int E = 1 << LT;
+  static constexpr int T = E * E * E;
+  static constexpr int THREADS = LT == 3 ? 128 : 256;
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int MB = E / 8;               // 8-row DMMA blocks along the mode
+  static constexpr int NBW = E * E / 8 / WARPS;  // 8-col DMMA blocks per warp
+  // shared memory layout (doubles)
+  static constexpr int OFF_XR = 0;
+  static constexpr int OFF_XI = OFF_XR + T;
+  static constexpr int OFF_DH = OFF_XI + T;            // That_m: 3 x (re, im) x E x E
+  static constexpr int OFF_DB = OFF_DH + 3 * 2 * E * E;  // T_m[t,t]: 3 x E x E
+  static constexpr int OFF_PD = OFF_DB + 3 * E * E;      // eigenbasis rows: 3 x E x kPStride
+  static constexpr int OFF_LAM = OFF_PD + 3 * E * kPStride;
+  static constexpr int DOUBLES = OFF_LAM + 3 * 2 * E;
+  static constexpr int BYTES = DOUBLES * 8;
+};
+
+struct L3Geom {
+  int64_t lt;
+  int64_t gbase;
+  int start[3], ext[3], tco[3];
+  int nc[3], H, kp;
+  unsigned char cs[3][16], cz[3][16], cellof[3][16], cend[3][16], cplx[3][16];
+};
+
+// tile-local padded offset of (i0, i1, i2)
+template <int LT>
+TSG_DEVINL int l3off(int i0, int i1, int i2) { return i0 | (i1 << LT) | (i2 << (2 * LT)); }
+
+// ---- left-looking update along mode M over global rows [k_lo, k_hi) --------
+// xr[row i of mode M, cross-section n] -= sum_k T_M[start+i, k] X(..k..)
+// Warp w owns cross-section columns [32w, 32w+32) (4 DMMA col blocks) and
+// both 8-row blocks.  Fragments come straight from global memory (L2).
+template <int LT, int M>
+TSG_DEVINL void l3_update(const SolveArgs& a, const L3Geom& tg, double* xr, int k_lo, int k_hi) {
+  using C = L3C<LT>;
+  constexpr int E = C::E, MB = C::MB, NBW = C::NBW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  constexpr int VA = (M == 0) ? 1 : 0, VB = (M == 2) ? 1 : 2;  // the other two modes
+  const int nm = a.dims[M];
+  const double* __restrict__ Tm = a.T[M];
+  const double* __restrict__ X = a.X;
+  const int64_t sM = a.stride[M];
+  // B fragment columns of this lane: n = 8*NBW*warp + 8*jb + gq;
+  // cross-section n = ia + E*ib over modes (VA, VB).
+  int64_t boff[NBW];
+  bool bok[NBW];
+#pragma unroll
+  for (int jb = 0; jb < NBW; ++jb) {
+    const int n = 8 * NBW * warp + 8 * jb + gq;
+    const int ia = n & (E - 1), ib = n >> LT;
+    bok[jb] = ia < tg.ext[VA] && ib < tg.ext[VB];
+    boff[jb] = bok[jb] ? static_cast<int64_t>(tg.start[VA] + ia) * a.stride[VA] +
+                             static_cast<int64_t>(tg.start[VB] + ib) * a.stride[VB]
+                       : 0;
+  }
+  const int row0 = tg.start[M];
+  const int em = tg.ext[M];
+  bool aok[MB];
+#pragma unroll
+  for (int ib = 0; ib < MB; ++ib) aok[ib] = gq + 8 * ib < em;
+  double c[MB][NBW][2];
+#pragma unroll
+  for (int ib = 0; ib < MB; ++ib)
+#pragma unroll
+    for (int jb = 0; jb < NBW; ++jb) c[ib][jb][0] = c[ib][jb][1] = 0.0;
+
+  // Per-lane pointers at row k_lo + tq.  Padded rows/columns read in-bounds
+  // garbage that only reaches padded outputs (never scattered); only the
+  // K tail is masked.
+  const double* pa[MB];
+  const double* pb[NBW];
+#pragma unroll
+  for (int ib = 0; ib < MB; ++ib) {
+    const int row = aok[ib] ? row0 + gq + 8 * ib : row0;
+    pa[ib] = Tm + static_cast<int64_t>(k_lo + tq) * nm + row;
+  }
+#pragma unroll
+  for (int jb = 0; jb < NBW; ++jb) pb[jb] = X + boff[jb] + static_cast<int64_t>(k_lo + tq) * sM;
+  const int64_t sa = 4 * static_cast<int64_t>(nm), sb = 4 * sM;
+  constexpr int U = 4;  // k4-steps per batch (16 rows)
+  const int kr = k_hi - k_lo;
+  const int nfull = kr >> 4;
+  for (int bt = 0; bt < nfull; ++bt) {
+    double af[U][MB], bf[U][NBW];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int ib = 0; ib < MB; ++ib) {
+        af[u][ib] = __ldg(pa[ib]);
+        pa[ib] += sa;
+      }
+#pragma unroll
+      for (int jb = 0; jb < NBW; ++jb) {
+        bf[u][jb] = ld_cg(pb[jb]);
+        pb[jb] += sb;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int ib = 0; ib < MB; ++ib)
+#pragma unroll
+        for (int jb = 0; jb < NBW; ++jb) dmma(c[ib][jb][0], c[ib][jb][1], af[u][ib], bf[u][jb]);
+  }
+  const int rem = kr & 15;
+  if (rem) {
+    double af[U][MB], bf[U][NBW];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool kok = 4 * u + tq < rem;
+#pragma unroll
+      for (int ib = 0; ib < MB; ++ib) {
+        af[u][ib] = kok ? __ldg(pa[ib]) : 0.0;
+        pa[ib] += sa;
+      }
+#pragma unroll
+      for (int jb = 0; jb < NBW; ++jb) {
+        bf[u][jb] = kok ? ld_cg(pb[jb]) : 0.0;
+        pb[jb] += sb;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (4 * u >= rem) break;
+#pragma unroll
+      for (int ib = 0; ib < MB; ++ib)
+#pragma unroll
+        for (int jb = 0; jb < NBW; ++jb) dmma(c[ib][jb][0], c[ib][jb][1], af[u][ib], bf[u][jb]);
+    }
+  }
+  // xr -= c   (rows i = 8*ib + gq, cols n = 8*NBW*warp + 8*jb + 2*tq + h)
+#pragma unroll
+  for (int ib = 0; ib < MB; ++ib)
+#pragma unroll
+    for (int jb = 0; jb < NBW; ++jb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 8 * ib + gq, n = 8 * NBW * warp + 8 * jb + 2 * tq + h;
+        const int ia = n & (E - 1), ib2 = n >> LT;
+        int l;
+        if (M == 0) l = l3off<LT>(i, ia, ib2);
+        else if (M == 1) l = l3off<LT>(ia, i, ib2);
+        else l = l3off<LT>(ia, ib2, i);
+        xr[l] -= c[ib][jb][h];
+      }
+}
+
+TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile) {
+  const int* f = a.flags + tile;
+  while (ld_acquire(f) < a.epoch) __nanosleep(32);
+}
+
+template <int LT>
+__global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2) solve_lap3_kernel(SolveArgs a) {
+  using C = L3C<LT>;
+  constexpr int E = C::E, L3_T = C::T, L3_THREADS = C::THREADS;
+  constexpr int EE = E * E, MSK = E - 1;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ L3Geom tg;
+  __shared__ int s_tile;
+  double* xr = smem + C::OFF_XR;
+  double* xi = smem + C::OFF_XI;
+  double* dh = smem + C::OFF_DH;
+  double* db = smem + C::OFF_DB;
+  double* pd = smem + C::OFF_PD;
+  double* lam = smem + C::OFF_LAM;
+  const int tid = threadIdx.x;
+  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tmark = clock64();
+  auto mark = [&](int k) {
+    if (a.prof) {
+      const long long t = clock64();
+      ph[k] += static_cast<unsigned long long>(t - tmark);
+      tmark = t;
+    }
+  };
+
+  for (;;) {
+    mark(7);
+    if (tid == 0) s_tile = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int qi = s_tile;
+    if (qi >= a.ntiles) break;
+    mark(0);
+
+    // ---- geometry (host-built tables) ---------------------------------------
+    if (tid < 3) {
+      const unsigned long long pk = a.ocoord[qi];
+      const int tm = static_cast<int>((pk >> (10 * tid)) & 1023);
+      const TileMode& src = a.tmode[tid][tm];
+      tg.tco[tid] = tm;
+      tg.start[tid] = src.start;
+      tg.ext[tid] = src.ext;
+      tg.nc[tid] = src.nc;
+      for (int k = 0; k < 16; ++k) {
+        tg.cs[tid][k] = src.cs[k];
+        tg.cz[tid][k] = src.cz[k];
+        tg.cellof[tid][k] = src.cellof[k];
+        tg.cend[tid][k] = src.cend[k];
+        tg.cplx[tid][k] = src.cplx[k];
+      }
+      if (tid == 0) tg.lt = a.order[qi];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      tg.gbase = static_cast<int64_t>(tg.start[0]) * a.stride[0] +
+                 static_cast<int64_t>(tg.start[1]) * a.stride[1] +
+                 static_cast<int64_t>(tg.start[2]) * a.stride[2];
+      tg.H = tg.nc[0] + tg.nc[1] + tg.nc[2] - 3;
+      int kp = 0;
+      for (int m = 0; m < 3; ++m)
+        for (int k = 0; k < tg.nc[m]; ++k) kp |= (tg.cz[m][k] == 2) ? (1 << m) : 0;
+      tg.kp = kp;
+    }
+    __syncthreads();
+    const int e0 = tg.ext[0], e1 = tg.ext[1], e2 = tg.ext[2];
+
+    // ---- gather B~_t (padded, zero-filled) + diag blocks + eigenbasis rows ----
+    for (int l = tid; l < L3_T; l += L3_THREADS) {
+      const int i0 = l & MSK, i1 = (l >> LT) & MSK, i2 = l >> (2 * LT);
+      const bool ok = i0 < e0 && i1 < e1 && i2 < e2;
+      const double* src = ok ? a.X + tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2] : a.X;
+      cp_async8(xr + l, src, ok ? 8 : 0);
+    }
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int em = tg.ext[m], st = tg.start[m], nm = a.dims[m];
+      for (int e = tid; e < EE; e += L3_THREADS) {
+        const int i = e & MSK, j = e >> LT;
+        const bool ok = i < em && j < em;
+        cp_async8(db + m * EE + e, ok ? a.T[m] + (st + i) + static_cast<int64_t>(st + j) * nm : a.T[m],
+                  ok ? 8 : 0);
+      }
+      for (int e = tid; e < E * kPStride; e += L3_THREADS) {
+        const bool ok = e < em * kPStride;
+        cp_async8(pd + m * E * kPStride + e,
+                  ok ? a.pdat[m] + static_cast<int64_t>(st) * kPStride + e : a.pdat[m], ok ? 8 : 0);
+      }
+    }
+    cp_async_commit();
+
+    // ---- left-looking updates, far tiles of every mode (DMMA from L2) ---------
+    // (these only read global memory and registers; the xr RMW happens after
+    //  the staged tile has landed)
+    int64_t mul[3] = {1, a.ntiles_mode[0], static_cast<int64_t>(a.ntiles_mode[0]) * a.ntiles_mode[1]};
+    cp_async_wait_all();
+    __syncthreads();
+    mark(1);
+    for (int part = 0; part < 2; ++part) {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int tm = tg.tco[m], pmt = a.ntiles_mode[m];
+        const int* bm = a.bnd[m];
+        int k_lo = 0, k_hi = 0, wt = -1;
+        if (part == 0 && tm + 2 < pmt) {
+          k_lo = bm[tm + 2];
+          k_hi = a.dims[m];
+          wt = tm + 2;
+        } else if (part == 1 && tm + 1 < pmt) {
+          k_lo = bm[tm + 1];
+          k_hi = bm[tm + 2];
+          wt = tm + 1;
+        }
+        if (wt < 0 || (a.dbg & 4)) continue;  // uniform
+        if (tid == 0) wait_flag(a, tg.lt + (wt - tm) * mul[m]);
+        __syncthreads();
+        if (m == 0) l3_update<LT, 0>(a, tg, xr, k_lo, k_hi);
+        else if (m == 1) l3_update<LT, 1>(a, tg, xr, k_lo, k_hi);
+        else l3_update<LT, 2>(a, tg, xr, k_lo, k_hi);
+      }
+    }
+
+    mark(2);
+    // ---- That_m = Pinv D_m P on later-cell entries; lambda_m -----------------
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int em = tg.ext[m];
+      const double* dm = db + m * EE;
+      const double* pm = pd + m * E * kPStride;
+      for (int e = tid; e < EE; e += L3_THREADS) {
+        const int i = e & MSK, j = e >> LT;
+        double re = 0.0, im = 0.0;
+        if (i < em && j < em && j >= tg.cend[m][i]) {
+          const int I0 = tg.cs[m][tg.cellof[m][i]], Iz = tg.cz[m][tg.cellof[m][i]];
+          const int J0 = tg.cs[m][tg.cellof[m][j]], Jz = tg.cz[m][tg.cellof[m][j]];
+          const double* pi = pm + I0 * kPStride + 12;
+          const double* pj = pm + J0 * kPStride + 4;
+          for (int aa = 0; aa < Iz; ++aa) {
+            const double wr = Iz == 2 ? pi[((i - I0) * 2 + aa) * 2] : 1.0;
+            const double wi = Iz == 2 ? pi[((i - I0) * 2 + aa) * 2 + 1] : 0.0;
+            for (int bb = 0; bb < Jz; ++bb) {
+              const double d = dm[(I0 + aa) + (J0 + bb) * E];
+              const double vr = Jz == 2 ? pj[(bb * 2 + (j - J0)) * 2] : 1.0;
+              const double vi = Jz == 2 ? pj[(bb * 2 + (j - J0)) * 2 + 1] : 0.0;
+              re += d * (wr * vr - wi * vi);
+              im += d * (wr * vi + wi * vr);
+            }
+          }
+        }
+        dh[m * 2 * EE + i + E * j] = re;
+        dh[m * 2 * EE + EE + i + E * j] = im;
+      }
+      if (tid < E) {
+        const int i = tid;
+        double lr = 0.0, li = 0.0;
+        if (i < em) {
+          const int I0 = tg.cs[m][tg.cellof[m][i]];
+          const double* p = pm + I0 * kPStride + (i - I0) * 2;
+          lr = p[0];
+          li = p[1];
+        }
+        lam[m * 2 * E + i] = lr;
+        lam[m * 2 * E + E + i] = li;
+      }
+    }
+    for (int l = tid; l < L3_T; l += L3_THREADS) xi[l] = 0.0;
+    __syncthreads();
+
+    // ---- into the eigenbasis (pair modes) -------------------------------------
+    const int kp = tg.kp;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      if (!(kp & (1 << m))) continue;  // uniform
+      const double* pm = pd + m * E * kPStride;
+      // work item: (row i of mode m, cross-section n)
+      for (int w = tid; w < L3_T; w += L3_THREADS) {
+        const int i = w & MSK, n = w >> LT;
+        if (!tg.cplx[m][i]) continue;  // first row of a 2x2 block
+        const int na = n & MSK, nb = n >> LT;
+        int l, st;
+        if (m == 0) l = l3off<LT>(i, na, nb), st = 1;
+        else if (m == 1) l = l3off<LT>(na, i, nb), st = E;
+        else l = l3off<LT>(na, nb, i), st = EE;
+        const double* pi = pm + i * kPStride + 12;
+        const int l2 = l + st;
+        const double ar = xr[l], ai = xi[l], br = xr[l2], bi = xi[l2];
+        xr[l] = pi[0] * ar - pi[1] * ai + pi[2] * br - pi[3] * bi;
+        xi[l] = pi[0] * ai + pi[1] * ar + pi[2] * bi + pi[3] * br;
+        xr[l2] = pi[4] * ar - pi[5] * ai + pi[6] * br - pi[7] * bi;
+        xi[l2] = pi[4] * ai + pi[5] * ar + pi[6] * bi + pi[7] * br;
+      }
+      __syncthreads();
+    }
+
+    mark(3);
+    // ---- wavefront over cell hyperplanes --------------------------------------
+    // lanes: (slot over the (c0, c1) cell grid) x (unknown inside the cell).
+    // Modes 0 and 1 of a lane are fixed for the whole tile; only the mode-2
+    // cell c2 = h - c0 - c1 moves with the hyperplane.
+    // lanes: (row i0, row i1, row bit b2 of a mode-2 pair); the mode-2 cell
+    // c2 = h - cell(i0) - cell(i1) moves with the hyperplane.
+    const int nc2 = tg.nc[2];
+    const int p2 = (kp & 4) ? 1 : 0;
+    constexpr int LPT = (2 * EE + L3_THREADS - 1) / L3_THREADS;  // lanes per thread
+    int lc01[LPT], lb2[LPT], loff[LPT], lce0[LPT], lce1[LPT], li0[LPT], li1[LPT];
+    double llr[LPT], lli[LPT];
+    bool lok[LPT];
+#pragma unroll
+    for (int q = 0; q < LPT; ++q) {
+      const int L = tid + q * L3_THREADS;
+      const int rest = L >> p2;
+      const int i0 = rest & (E - 1), i1 = (rest >> LT) & (E - 1);
+      lok[q] = rest < EE && i0 < tg.ext[0] && i1 < tg.ext[1];
+      lc01[q] = tg.cellof[0][i0] + tg.cellof[1][i1];
+      lb2[q] = L & p2;
+      li0[q] = i0;
+      li1[q] = i1;
+      loff[q] = i0 + E * i1;
+      lce0[q] = tg.cend[0][i0];
+      lce1[q] = tg.cend[1][i1];
+      llr[q] = lam[i0] + lam[2 * E + i1];
+      lli[q] = lam[E + i0] + lam[3 * E + i1];
+    }
+    bool singular = false;
+    const int e0w = tg.ext[0], e1w = tg.ext[1], e2w = tg.ext[2];
+    for (int h = tg.H; h >= 0; --h) {
+#pragma unroll
+      for (int q = 0; q < LPT; ++q) {
+        const int c2 = h - lc01[q];
+        if (!lok[q] || c2 < 0 || c2 >= nc2) continue;
+        int i2 = tg.cs[2][c2];
+        if (lb2[q]) {
+          if (tg.cz[2][c2] != 2) continue;
+          i2 += 1;
+        }
+        const int off = loff[q] + EE * i2;
+        double rr = xr[off], ri = xi[off];
+        // dots along the three modes: sum_j That_m[i_m, j] xhat(u | m -> j)
+        const int ii[3] = {li0[q], li1[q], i2};
+        const int jb0[3] = {lce0[q], lce1[q], tg.cs[2][c2] + tg.cz[2][c2]};
+        const int ee[3] = {e0w, e1w, e2w};
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          const int st = (m == 0) ? 1 : (m == 1 ? E : EE);
+          const int i = ii[m];
+          const double* drp = dh + m * 2 * EE + i;
+          const double* xrp = xr + off - i * st;
+          const double* xip = xi + off - i * st;
+          double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
+          int j = jb0[m];
+          const int em = ee[m];
+          for (; j + 1 < em; j += 2) {
+            const double cr = drp[E * j], ci = drp[EE + E * j];
+            const double yr = xrp[j * st], yi = xip[j * st];
+            const double cr2 = drp[E * (j + 1)], ci2 = drp[EE + E * (j + 1)];
+            const double yr2 = xrp[(j + 1) * st], yi2 = xip[(j + 1) * st];
+            ar0 = fma(cr, yr, ar0);
+            ar0 = fma(-ci, yi, ar0);
+            ai0 = fma(cr, yi, ai0);
+            ai0 = fma(ci, yr, ai0);
+            ar1 = fma(cr2, yr2, ar1);
+            ar1 = fma(-ci2, yi2, ar1);
+            ai1 = fma(cr2, yi2, ai1);
+            ai1 = fma(ci2, yr2, ai1);
+          }
+          if (j < em) {
+            const double cr = drp[E * j], ci = drp[EE + E * j];
+            const double yr = xrp[j * st], yi = xip[j * st];
+            ar0 = fma(cr, yr, ar0);
+            ar0 = fma(-ci, yi, ar0);
+            ai0 = fma(cr, yi, ai0);
+            ai0 = fma(ci, yr, ai0);
+          }
+          rr -= ar0 + ar1;
+          ri -= ai0 + ai1;
+        }
+        const double mur = llr[q] + lam[4 * E + i2], mui = lli[q] + lam[5 * E + i2];
+        const double den = mur * mur + mui * mui;
+        if (!(den > a.tiny * a.tiny)) {
+          singular = true;
+          xr[off] = 0.0;
+          xi[off] = 0.0;
+        } else {
+          const double inv = 1.0 / den;
+          xr[off] = (rr * mur + ri * mui) * inv;
+          xi[off] = (ri * mur - rr * mui) * inv;
+        }
+      }
+      __syncthreads();
+    }
+    if (singular)
+      atomicMin(a.status, static_cast<int>(tg.lt < 0x7f7f7f7e ? tg.lt : 0x7f7f7f7e));
+
+    mark(4);
+    // ---- back to the Schur basis -------------------------------------------------
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      if (!(kp & (1 << m))) continue;
+      const double* pm = pd + m * E * kPStride;
+      for (int w = tid; w < L3_T; w += L3_THREADS) {
+        const int i = w & MSK, n = w >> LT;
+        if (!tg.cplx[m][i]) continue;
+        const int na = n & MSK, nb = n >> LT;
+        int l, st;
+        if (m == 0) l = l3off<LT>(i, na, nb), st = 1;
+        else if (m == 1) l = l3off<LT>(na, i, nb), st = E;
+        else l = l3off<LT>(na, nb, i), st = EE;
+        const double* p = pm + i * kPStride + 4;
+        const int l2 = l + st;
+        const double ar = xr[l], ai = xi[l], br = xr[l2], bi = xi[l2];
+        xr[l] = p[0] * ar - p[1] * ai + p[2] * br - p[3] * bi;
+        xi[l] = p[0] * ai + p[1] * ar + p[2] * bi + p[3] * br;
+        xr[l2] = p[4] * ar - p[5] * ai + p[6] * br - p[7] * bi;
+        xi[l2] = p[4] * ai + p[5] * ar + p[6] * bi + p[7] * br;
+      }
+      __syncthreads();
+    }
+
+    mark(5);
+    // ---- scatter X_t, release --------------------------------------------------
+    for (int l = tid; l < L3_T; l += L3_THREADS) {
+      const int i0 = l & MSK, i1 = (l >> LT) & MSK, i2 = l >> (2 * LT);
+      if (i0 < e0 && i1 < e1 && i2 < e2)
+        a.X[tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2]] = xr[l];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(a.flags + tg.lt, a.epoch);
+    }
+    mark(6);
+    if (a.prof && tid == 0) atomicAdd(a.prof + 8, 1ull);
+  }
+  if (a.prof && tid == 0)
+    for (int k = 0; k < 8; ++k) atomicAdd(a.prof + k, ph[k]);
+}
+
+template <int LT>
+cudaError_t launch_l3(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
+  using C = L3C<LT>;
+  static int nsm = 0, occ = 0;
+  auto k = solve_lap3_kernel<LT>;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, C::THREADS, C::BYTES);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = static_cast<int64_t>(nsm) * occ;
+  if (grid > a.ntiles) grid = a.ntiles;
+  if (info) *info = SolveLaunchInfo{static_cast<int>(grid), C::THREADS, C::BYTES, occ};
+  k<<<static_cast<unsigned>(grid), C::THREADS, C::BYTES, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+TileCaps solve_lap3_caps(int lt) {
+  const int e = 1 << lt;
+  return TileCaps{e, e * e * e, e * e};
+}
+
+cudaError_t launch_solve_lap3(int lt, const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
+  if (a.ntiles <= 0) return cudaSuccess;
+  return lt == 3 ? launch_l3<3>(a, st, info) : launch_l3<4>(a, st, info);
+}
+
+}  // namespace tsg
