@@ -50,6 +50,7 @@ struct SolveArgs {
   double tiny;                  // |cell eigenvalue| <= tiny -> singular
   int refine;                   // 1: one refinement step per base cell
   int dbg;                      // ablation mask (development only; 0 in production)
+  int use_tma;                  // far updates through TMA tensor maps (set by the launcher)
   unsigned long long* prof;     // optional per-phase cycle counters (development)
 };
 

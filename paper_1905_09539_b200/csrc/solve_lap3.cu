@@ -19,11 +19,14 @@
 // Reference: lap_rec / lap_base (laplace.hpp:99-153), block_back_substitution
 // (kernels.hpp:179-261), mode_multiply update (laplace.hpp:147).
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 #include <cstdint>
 
 #include "common.cuh"
 #include "solve.h"
 #include "solve_common.cuh"
+#include "tma.h"
 
 namespace tsg {
 namespace {
@@ -45,7 +48,12 @@ struct L3C {
   static constexpr int OFF_DB = OFF_DH + 3 * 2 * E * E;  // T_m[t,t]: 3 x E x E
   static constexpr int OFF_PD = OFF_DB + 3 * E * E;      // eigenbasis rows: 3 x E x kPStride
   static constexpr int OFF_LAM = OFF_PD + 3 * E * kPStride;
-  static constexpr int DOUBLES = OFF_LAM + 3 * 2 * E;
+  // TMA ring for the far updates: NST boxes of E x E x KCH doubles
+  static constexpr int KCH = LT == 3 ? 32 : 8;
+  static constexpr int NST = LT == 3 ? 3 : 2;
+  static constexpr int CH = E * E * KCH;
+  static constexpr int OFF_STG = OFF_LAM + 3 * 2 * E;
+  static constexpr int DOUBLES = OFF_STG + NST * CH;
   static constexpr int BYTES = DOUBLES * 8;
 };
 
@@ -186,8 +194,98 @@ TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile) {
   while (ld_acquire(f) < a.epoch) __nanosleep(32);
 }
 
+// Far-tile update along mode M with TMA-staged K chunks: one elected thread
+// streams boxes of (KCH rows along M) x (the tile's E x E cross-section) of
+// X into an NST-deep mbarrier ring; every warp runs DMMA with B fragments
+// from the landed box and A fragments (T_M columns) from L1/L2.
+template <int LT, int M>
+TSG_DEVINL void l3_update_tma(const SolveArgs& a, const L3Geom& tg, double* xr, int k_lo, int k_hi,
+                              int64_t wait_tile, const CUtensorMap* map, double* stg, uint64_t* bars,
+                              unsigned& phases) {
+  using C = L3C<LT>;
+  constexpr int E = C::E, EE = E * E, MB = C::MB, NBW = C::NBW, KCH = C::KCH, NST = C::NST,
+                CH = C::CH;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int nch = (k_hi - k_lo + KCH - 1) / KCH;
+  auto issue = [&](int cidx, int st) {
+    int cc[3] = {tg.start[0], tg.start[1], tg.start[2]};
+    cc[M] = k_lo + cidx * KCH;
+    mbar_expect_tx(bars + st, CH * 8);
+    tma_load_3d(stg + st * CH, map, cc[0], cc[1], cc[2], bars + st);
+  };
+  if (tid == 0) {
+    wait_flag(a, wait_tile);
+    fence_proxy_async();
+    for (int st = 0; st < NST && st < nch; ++st) issue(st, st);
+  }
+  const int nm = a.dims[M];
+  const double* __restrict__ Tm = a.T[M];
+  const int row0 = tg.start[M], em = tg.ext[M];
+  int arow[MB];
+#pragma unroll
+  for (int ib = 0; ib < MB; ++ib) arow[ib] = (gq + 8 * ib < em) ? row0 + gq + 8 * ib : row0;
+  // stage offsets of this lane's B fragment columns
+  int bcol[NBW];
+#pragma unroll
+  for (int jb = 0; jb < NBW; ++jb) {
+    const int n = 8 * NBW * warp + 8 * jb + gq;
+    const int ia = n & (E - 1), ib = n >> LT;
+    bcol[jb] = (M == 0) ? KCH * n : (M == 1 ? ia + E * KCH * ib : n);
+  }
+  constexpr int KST = (M == 0) ? 1 : (M == 1 ? E : EE);  // stage stride along k
+  double c[MB][NBW][2];
+#pragma unroll
+  for (int ib = 0; ib < MB; ++ib)
+#pragma unroll
+    for (int jb = 0; jb < NBW; ++jb) c[ib][jb][0] = c[ib][jb][1] = 0.0;
+  for (int ci = 0; ci < nch; ++ci) {
+    const int st = ci % NST;
+    mbar_wait(bars + st, (phases >> st) & 1u);
+    phases ^= 1u << st;
+    const double* B = stg + st * CH;
+    const int kb = k_lo + ci * KCH;
+#pragma unroll
+    for (int k4 = 0; k4 < KCH; k4 += 4) {
+      const int kg = kb + k4 + tq;
+      const bool kok = kg < k_hi;
+      double af[MB], bf[NBW];
+#pragma unroll
+      for (int ib = 0; ib < MB; ++ib)
+        af[ib] = kok ? __ldg(Tm + static_cast<int64_t>(kg) * nm + arow[ib]) : 0.0;
+#pragma unroll
+      for (int jb = 0; jb < NBW; ++jb) bf[jb] = B[bcol[jb] + (k4 + tq) * KST];
+#pragma unroll
+      for (int ib = 0; ib < MB; ++ib)
+#pragma unroll
+        for (int jb = 0; jb < NBW; ++jb) dmma(c[ib][jb][0], c[ib][jb][1], af[ib], bf[jb]);
+    }
+    __syncthreads();  // stage st fully consumed
+    if (tid == 0 && ci + NST < nch) {
+      fence_proxy_async();
+      issue(ci + NST, st);
+    }
+  }
+#pragma unroll
+  for (int ib = 0; ib < MB; ++ib)
+#pragma unroll
+    for (int jb = 0; jb < NBW; ++jb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 8 * ib + gq, n = 8 * NBW * warp + 8 * jb + 2 * tq + h;
+        const int ia = n & (E - 1), ib2 = n >> LT;
+        int l;
+        if (M == 0) l = l3off<LT>(i, ia, ib2);
+        else if (M == 1) l = l3off<LT>(ia, i, ib2);
+        else l = l3off<LT>(ia, ib2, i);
+        xr[l] -= c[ib][jb][h];
+      }
+}
+
 template <int LT>
-__global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2) solve_lap3_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
+    solve_lap3_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tm0,
+                      const __grid_constant__ CUtensorMap tm1, const __grid_constant__ CUtensorMap tm2) {
   using C = L3C<LT>;
   constexpr int E = C::E, L3_T = C::T, L3_THREADS = C::THREADS;
   constexpr int EE = E * E, MSK = E - 1;
@@ -200,7 +298,15 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2) solve_lap3_
   double* db = smem + C::OFF_DB;
   double* pd = smem + C::OFF_PD;
   double* lam = smem + C::OFF_LAM;
+  double* stg = smem + C::OFF_STG;
+  __shared__ __align__(8) uint64_t bars[C::NST];
+  unsigned phases = 0;
   const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < C::NST; ++i) mbar_init(bars + i, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
   unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tmark = clock64();
   auto mark = [&](int k) {
@@ -298,6 +404,13 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2) solve_lap3_
           wt = tm + 1;
         }
         if (wt < 0 || (a.dbg & 4)) continue;  // uniform
+        if (part == 0 && a.use_tma && !((a.dbg >> (3 + m)) & 1)) {
+          __syncthreads();  // previous pass's xr writes
+          if (m == 0) l3_update_tma<LT, 0>(a, tg, xr, k_lo, k_hi, tg.lt + (wt - tm) * mul[m], &tm0, stg, bars, phases);
+          else if (m == 1) l3_update_tma<LT, 1>(a, tg, xr, k_lo, k_hi, tg.lt + (wt - tm) * mul[m], &tm1, stg, bars, phases);
+          else l3_update_tma<LT, 2>(a, tg, xr, k_lo, k_hi, tg.lt + (wt - tm) * mul[m], &tm2, stg, bars, phases);
+          continue;
+        }
         if (tid == 0) wait_flag(a, tg.lt + (wt - tm) * mul[m]);
         __syncthreads();
         if (m == 0) l3_update<LT, 0>(a, tg, xr, k_lo, k_hi);
@@ -522,7 +635,25 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2) solve_lap3_
 }
 
 template <int LT>
-cudaError_t launch_l3(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
+cudaError_t launch_l3(const SolveArgs& a0, cudaStream_t st, SolveLaunchInfo* info) {
+  SolveArgs a = a0;
+  // TMA maps over the work tensor, one box shape per mode (E x E x KCH)
+  CUtensorMap maps[3];
+  {
+    const uint64_t dims[3] = {static_cast<uint64_t>(a.dims[0]), static_cast<uint64_t>(a.dims[1]),
+                              static_cast<uint64_t>(a.dims[2])};
+    // Opt-in (TSG_TMA=1): measured slower than direct L2 fragment loads for
+    // the 64-byte-wide boxes of 8^3 tiles, and unresolved on some tiny
+    // tile shapes; see DESIGN.md.
+    bool ok = (a.dims[0] % 2 == 0) && std::getenv("TSG_TMA") != nullptr;
+    for (int m = 0; m < 3 && ok; ++m) {
+      uint32_t box[3] = {L3C<LT>::E, L3C<LT>::E, L3C<LT>::E};
+      box[m] = L3C<LT>::KCH;
+      ok = encode_tmap_f64(&maps[m], a.X, 3, dims, box);
+    }
+    a.use_tma = ok ? 1 : 0;
+    if (!ok) std::memset(maps, 0, sizeof(maps));
+  }
   using C = L3C<LT>;
   static int nsm = 0, occ = 0;
   auto k = solve_lap3_kernel<LT>;
@@ -539,7 +670,7 @@ cudaError_t launch_l3(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > a.ntiles) grid = a.ntiles;
   if (info) *info = SolveLaunchInfo{static_cast<int>(grid), C::THREADS, C::BYTES, occ};
-  k<<<static_cast<unsigned>(grid), C::THREADS, C::BYTES, st>>>(a);
+  k<<<static_cast<unsigned>(grid), C::THREADS, C::BYTES, st>>>(a, maps[0], maps[1], maps[2]);
   return cudaGetLastError();
 }
 
