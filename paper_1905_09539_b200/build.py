@@ -72,8 +72,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     jobs = []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        extra = os.environ.get("TSG_NVCC_FLAGS", "").split()
         cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-diag-suppress", "177", *inc, "-c", src, "-o", obj]
+               "-diag-suppress", "177", *extra, *inc, "-c", src, "-o", obj]
         jobs.append((obj, [src] + headers, cmd))
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cpp"))):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")

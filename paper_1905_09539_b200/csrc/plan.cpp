@@ -63,7 +63,7 @@ struct tsg_plan {
   std::vector<int64_t> stride;
   int64_t N = 0;
   // device factors
-  std::vector<DevBuf> T, Fwd, FwdT, Bwd, BwdT, eig, pdat;  // per mode
+  std::vector<DevBuf> T, Fwd, FwdT, Bwd, BwdT, eig, pdat, dhat;  // per mode
   DevBuf Tc;
   std::vector<tsg::TileMode*> tmode;
   std::vector<int*> bnd;
@@ -398,6 +398,8 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   pl->BwdT.resize(d);
   pl->eig.resize(d);
   pl->pdat.resize(d);
+  pl->dhat.resize(d);
+  std::vector<std::vector<double>> pdvs(d), nfs(d);
   pl->tmode.assign(d, nullptr);
   pl->bnd.assign(d, nullptr);
 
@@ -414,6 +416,8 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
                                      " has a defective 2x2 diagonal block (equal real eigenvalues)");
     TSG_CU(upload_mat(pl->eig[m], nf.data(), nf.size()));
     TSG_CU(upload_mat(pl->pdat[m], pdv.data(), pdv.size()));
+    pdvs[m] = pdv;
+    nfs[m] = nf;
     scale += fro(T[m], nn);
     if (!reduced_only) {
       // forward: A = U^T (mode 0), At = U (m > 0); back: A = U, At = U^T.
@@ -477,12 +481,53 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
           tmd.cend[q] = static_cast<unsigned char>(r + sz);
         }
         tmd.cplx[r] = sz == 2 ? 1 : 0;
+        if (sz == 2 && nfs[m][static_cast<size_t>(tmd.start + r) * tsg::kEigStride + 3] == 1.0) {
+          tmd.ckind[r] = 1;
+          tmd.ckind[r + 1] = 2;
+        }
         ++nc;
         r += sz;
       }
       tmd.nc = static_cast<unsigned char>(nc);
     }
     TSG_CU(upload(&pl->tmode[m], tms));
+    if (pl->fast == 3) {
+      // Eigenbasis diagonal block of every tile index along mode m:
+      // That[i][j] = sum Pinv_blk(i)[i,a] T[a,b] P_blk(j)[b,j] for j beyond
+      // i's cell (0 elsewhere), then lambda_i; layout of solve_lap3 (DHS).
+      using Cx = std::complex<double>;
+      const int E = 1 << pl->lt3, EE = E * E, DHS = 2 * EE + 2 * E;
+      std::vector<double> dh(static_cast<size_t>(pl->ntiles_mode[m]) * DHS, 0.0);
+      const int n = dims[m];
+      auto Pget = [&](int row0, int r, int c, int which) {  // which 4: P, 12: Pinv
+        const double* pr = pdvs[m].data() + static_cast<size_t>(row0) * tsg::kPStride + which;
+        return Cx(pr[(r * 2 + c) * 2], pr[(r * 2 + c) * 2 + 1]);
+      };
+      for (int t = 0; t < pl->ntiles_mode[m]; ++t) {
+        const tsg::TileMode& tmd = tms[t];
+        double* o = dh.data() + static_cast<size_t>(t) * DHS;
+        for (int i = 0; i < tmd.ext; ++i) {
+          const int ci = tmd.cellof[i], I0 = tmd.cs[ci], Iz = tmd.cz[ci];
+          for (int j = tmd.cend[i]; j < tmd.ext; ++j) {
+            const int cj = tmd.cellof[j], J0 = tmd.cs[cj], Jz = tmd.cz[cj];
+            Cx acc(0.0, 0.0);
+            for (int aa = 0; aa < Iz; ++aa)
+              for (int bb = 0; bb < Jz; ++bb) {
+                const double dv = at(T[m], n, tmd.start + I0 + aa, tmd.start + J0 + bb);
+                const Cx w = Iz == 2 ? Pget(tmd.start + I0, i - I0, aa, 12) : Cx(1.0, 0.0);
+                const Cx v = Jz == 2 ? Pget(tmd.start + J0, bb, j - J0, 4) : Cx(1.0, 0.0);
+                acc += w * dv * v;
+              }
+            o[i + E * j] = acc.real();
+            o[EE + i + E * j] = acc.imag();
+          }
+          const double* pr = pdvs[m].data() + static_cast<size_t>(tmd.start + I0) * tsg::kPStride;
+          o[2 * EE + i] = pr[(i - I0) * 2];
+          o[2 * EE + E + i] = pr[(i - I0) * 2 + 1];
+        }
+      }
+      TSG_CU(upload_mat(pl->dhat[m], dh.data(), dh.size()));
+    }
   }
   if (pl->ntiles > INT_MAX / 2) return fail(ctx, TSG_EDIM, "too many tiles");
   for (int m = 0; m < d; ++m)
@@ -821,6 +866,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     a.tmode[m] = pl->tmode[m];
     a.eig[m] = pl->eig[m].p;
     a.pdat[m] = pl->pdat[m].p;
+    a.dhat[m] = pl->dhat[m].p;
     a.ntiles_mode[m] = pl->ntiles_mode[m];
     a.bnd[m] = pl->bnd[m];
     if (pl->family == 1 && m >= 1) a.W[m] = pl->wchain[m].p;
@@ -837,6 +883,17 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   a.tiny = pl->tiny;
   a.refine = pl->refine;
   if (const char* e = std::getenv("TSG_DBG")) a.dbg = std::atoi(e);
+  static unsigned long long* trace = nullptr;
+  static int64_t trace_n = 0;
+  const bool want_trace = std::getenv("TSG_TRACE") != nullptr;
+  if (want_trace) {
+    if (trace_n < pl->ntiles) {
+      if (trace) cudaFree(trace);
+      cudaMalloc(&trace, pl->ntiles * sizeof(unsigned long long));
+      trace_n = pl->ntiles;
+    }
+    a.trace = trace;
+  }
   static unsigned long long* prof = nullptr;
   const bool want_prof = std::getenv("TSG_PROF") != nullptr;
   if (want_prof) {
@@ -851,6 +908,37 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   else
     TSG_CU(tsg::launch_solve(a, st, &pl->solve_info));
   ++pl->launches;
+  if (want_trace) {
+    // per hyperplane: count, first and last release (us from the first release)
+    std::vector<unsigned long long> tr(pl->ntiles);
+    cudaMemcpyAsync(tr.data(), trace, pl->ntiles * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long t0 = ~0ull;
+    for (auto v : tr) t0 = std::min(t0, v);
+    std::vector<int> hp(pl->ntiles);
+    int H = 0;
+    for (int64_t t = 0; t < pl->ntiles; ++t) {
+      int64_t r = t;
+      int h = 0;
+      for (int m = 0; m < d; ++m) {
+        h += static_cast<int>(r % pl->ntiles_mode[m]);
+        r /= pl->ntiles_mode[m];
+      }
+      hp[t] = h;
+      H = std::max(H, h);
+    }
+    std::vector<double> lo(H + 1, 1e30), hi(H + 1, 0);
+    std::vector<int> cnt(H + 1, 0);
+    for (int64_t t = 0; t < pl->ntiles; ++t) {
+      const double v = (tr[t] - t0) * 1e-3;
+      lo[hp[t]] = std::min(lo[hp[t]], v);
+      hi[hp[t]] = std::max(hi[hp[t]], v);
+      cnt[hp[t]]++;
+    }
+    std::fprintf(stderr, "[tsg trace] hyperplane: tiles first_us last_us\n");
+    for (int h = H; h >= 0; --h)
+      std::fprintf(stderr, "[tsg trace] %3d %5d %9.1f %9.1f\n", h, cnt[h], lo[h], hi[h]);
+  }
   if (want_prof) {
     unsigned long long h[16];
     cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);

@@ -20,6 +20,7 @@ struct TileMode {
   unsigned char cellof[kMaxCells];  // tile row -> cell index
   unsigned char cend[kMaxCells];    // tile row -> first row after its cell
   unsigned char cplx[kMaxCells];    // 1 on the first row of a 2x2 block
+  unsigned char ckind[kMaxCells];   // 1/2: first/second row of a complex-eigenvalue pair, else 0
 };
 
 // Reduced Laplace-like / gsylv equation on a tiled tensor, solved in place
@@ -43,6 +44,7 @@ struct SolveArgs {
   const int* order;             // topological order of linear tile ids
   const unsigned long long* ocoord;  // packed tile coordinates of order[] (10 bits/mode)
   const double* pdat[kMaxOrder];     // per row: kPStride doubles (fast Laplace path)
+  const double* dhat[kMaxOrder];     // per tile index: eigenbasis diag block + lambdas (lap3)
   int* flags;                   // per tile: epoch when solved
   int* counter;                 // work queue head (zeroed before launch)
   int* status;                  // first singular cell linear index (or INT_MAX)
@@ -52,6 +54,7 @@ struct SolveArgs {
   int dbg;                      // ablation mask (development only; 0 in production)
   int use_tma;                  // far updates through TMA tensor maps (set by the launcher)
   unsigned long long* prof;     // optional per-phase cycle counters (development)
+  unsigned long long* trace;    // optional per-tile release globaltimer (development)
 };
 
 struct SolveLaunchInfo {

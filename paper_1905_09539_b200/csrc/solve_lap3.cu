@@ -33,26 +33,34 @@ namespace {
 
 // LT = log2 of the padded tile extent: 3 (8^3 tiles, 128 threads) or
 // 4 (16^3 tiles, 256 threads).
+#ifndef L3_T3
+#define L3_T3 128
+#endif
+#ifndef L3_MINB
+#define L3_MINB 4
+#endif
 template <int LT>
 struct L3C {
   static constexpr int E = 1 << LT;
   static constexpr int T = E * E * E;
-  static constexpr int THREADS = LT == 3 ? 128 : 256;
+  static constexpr int THREADS = LT == 3 ? L3_T3 : 256;
   static constexpr int WARPS = THREADS / 32;
   static constexpr int MB = E / 8;               // 8-row DMMA blocks along the mode
   static constexpr int NBW = E * E / 8 / WARPS;  // 8-col DMMA blocks per warp
   // shared memory layout (doubles)
   static constexpr int OFF_XR = 0;
   static constexpr int OFF_XI = OFF_XR + T;
-  static constexpr int OFF_DH = OFF_XI + T;            // That_m: 3 x (re, im) x E x E
-  static constexpr int OFF_DB = OFF_DH + 3 * 2 * E * E;  // T_m[t,t]: 3 x E x E
-  static constexpr int OFF_PD = OFF_DB + 3 * E * E;      // eigenbasis rows: 3 x E x kPStride
+  // per mode: That_m (re, im: E x E each) then lambda_m (re, im: E each),
+  // host-precomputed per tile index (tsg_plan: dhat tables)
+  static constexpr int DHS = 2 * E * E + 2 * E;
+  static constexpr int OFF_DH = OFF_XI + T;
+  static constexpr int OFF_PD = OFF_DH + 3 * DHS;        // eigenbasis rows: 3 x E x kPStride
   static constexpr int OFF_LAM = OFF_PD + 3 * E * kPStride;
   // TMA ring for the far updates: NST boxes of E x E x KCH doubles
   static constexpr int KCH = LT == 3 ? 32 : 8;
   static constexpr int NST = LT == 3 ? 3 : 2;
   static constexpr int CH = E * E * KCH;
-  static constexpr int OFF_STG = OFF_LAM + 3 * 2 * E;
+  static constexpr int OFF_STG = OFF_LAM;
   static constexpr int DOUBLES = OFF_STG + NST * CH;
   static constexpr int BYTES = DOUBLES * 8;
 };
@@ -62,7 +70,14 @@ struct L3Geom {
   int64_t gbase;
   int start[3], ext[3], tco[3];
   int nc[3], H, kp;
-  unsigned char cs[3][16], cz[3][16], cellof[3][16], cend[3][16], cplx[3][16];
+  unsigned char cs[3][16], cz[3][16], cellof[3][16], cend[3][16], cplx[3][16], ckind[3][16];
+  int npair[3];
+  int nlane;
+  unsigned short lane[2 * 16 * 16];  // representative lanes: i0 | i1 << 4 | b2 << 8
+  // mode-2 data per (cell c2, row bit b): i2 | cend << 5 | ckind << 10 | sigma << 12 | valid << 17
+  unsigned m2[16][2];
+  double m2lam[16][2][2];
+  unsigned char prow[3][8];  // first rows of the 2x2 blocks per mode
 };
 
 // tile-local padded offset of (i0, i1, i2)
@@ -99,6 +114,14 @@ TSG_DEVINL void l3_update(const SolveArgs& a, const L3Geom& tg, double* xr, int 
   }
   const int row0 = tg.start[M];
   const int em = tg.ext[M];
+  {
+    // a DMMA column block is fully padded when its slowest cross-section
+    // index lies beyond the tile (warp-uniform): skip the warp entirely
+    bool any = false;
+#pragma unroll
+    for (int jb = 0; jb < NBW; ++jb) any |= ((8 * NBW * warp + 8 * jb) >> LT) < tg.ext[VB];
+    if (!any && !(a.dbg & 128)) return;
+  }
   bool aok[MB];
 #pragma unroll
   for (int ib = 0; ib < MB; ++ib) aok[ib] = gq + 8 * ib < em;
@@ -191,7 +214,12 @@ TSG_DEVINL void l3_update(const SolveArgs& a, const L3Geom& tg, double* xr, int 
 
 TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile) {
   const int* f = a.flags + tile;
-  while (ld_acquire(f) < a.epoch) __nanosleep(32);
+  unsigned ns = 32;
+  const unsigned cap = (a.dbg & 64) ? 32 : 256;
+  while (ld_acquire(f) < a.epoch) {
+    __nanosleep(ns);
+    if (ns < cap) ns <<= 1;
+  }
 }
 
 // Far-tile update along mode M with TMA-staged K chunks: one elected thread
@@ -283,7 +311,7 @@ TSG_DEVINL void l3_update_tma(const SolveArgs& a, const L3Geom& tg, double* xr, 
 }
 
 template <int LT>
-__global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
+__global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     solve_lap3_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tm0,
                       const __grid_constant__ CUtensorMap tm1, const __grid_constant__ CUtensorMap tm2) {
   using C = L3C<LT>;
@@ -295,7 +323,6 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
   double* xr = smem + C::OFF_XR;
   double* xi = smem + C::OFF_XI;
   double* dh = smem + C::OFF_DH;
-  double* db = smem + C::OFF_DB;
   double* pd = smem + C::OFF_PD;
   double* lam = smem + C::OFF_LAM;
   double* stg = smem + C::OFF_STG;
@@ -340,6 +367,7 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
         tg.cellof[tid][k] = src.cellof[k];
         tg.cend[tid][k] = src.cend[k];
         tg.cplx[tid][k] = src.cplx[k];
+        tg.ckind[tid][k] = src.ckind[k];
       }
       if (tid == 0) tg.lt = a.order[qi];
     }
@@ -350,8 +378,13 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
                  static_cast<int64_t>(tg.start[2]) * a.stride[2];
       tg.H = tg.nc[0] + tg.nc[1] + tg.nc[2] - 3;
       int kp = 0;
-      for (int m = 0; m < 3; ++m)
-        for (int k = 0; k < tg.nc[m]; ++k) kp |= (tg.cz[m][k] == 2) ? (1 << m) : 0;
+      for (int m = 0; m < 3; ++m) {
+        int np = 0;
+        for (int k = 0; k < tg.nc[m]; ++k)
+          if (tg.cz[m][k] == 2) tg.prow[m][np++] = tg.cs[m][k];
+        tg.npair[m] = np;
+        kp |= np ? (1 << m) : 0;
+      }
       tg.kp = kp;
     }
     __syncthreads();
@@ -367,12 +400,9 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
 #pragma unroll
     for (int m = 0; m < 3; ++m) {
       const int em = tg.ext[m], st = tg.start[m], nm = a.dims[m];
-      for (int e = tid; e < EE; e += L3_THREADS) {
-        const int i = e & MSK, j = e >> LT;
-        const bool ok = i < em && j < em;
-        cp_async8(db + m * EE + e, ok ? a.T[m] + (st + i) + static_cast<int64_t>(st + j) * nm : a.T[m],
-                  ok ? 8 : 0);
-      }
+      (void)nm;
+      const double* dsrc = a.dhat[m] + static_cast<int64_t>(tg.tco[m]) * C::DHS;
+      for (int e = 2 * tid; e < C::DHS; e += 2 * L3_THREADS) cp_async16(dh + m * C::DHS + e, dsrc + e, 16);
       for (int e = tid; e < E * kPStride; e += L3_THREADS) {
         const bool ok = e < em * kPStride;
         cp_async8(pd + m * E * kPStride + e,
@@ -388,80 +418,37 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
     cp_async_wait_all();
     __syncthreads();
     mark(1);
-    for (int part = 0; part < 2; ++part) {
+    // Parts by distance along each mode, farthest first across modes:
+    // part 0 = tiles >= t+3 (released >= 3 hyperplanes ago), part 1 = t+2,
+    // part 2 = t+1 (nearest: the only part normally on the critical path).
+    for (int part = 0; part < 3; ++part) {
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
         const int tm = tg.tco[m], pmt = a.ntiles_mode[m];
         const int* bm = a.bnd[m];
-        int k_lo = 0, k_hi = 0, wt = -1;
-        if (part == 0 && tm + 2 < pmt) {
-          k_lo = bm[tm + 2];
-          k_hi = a.dims[m];
-          wt = tm + 2;
-        } else if (part == 1 && tm + 1 < pmt) {
-          k_lo = bm[tm + 1];
-          k_hi = bm[tm + 2];
-          wt = tm + 1;
-        }
-        if (wt < 0 || (a.dbg & 4)) continue;  // uniform
+        const int dist = part == 0 ? 3 : (part == 1 ? 2 : 1);
+        if (tm + dist >= pmt || (a.dbg & 4)) continue;  // uniform
+        const int k_lo = bm[tm + dist];
+        const int k_hi = part == 0 ? a.dims[m] : bm[tm + dist + 1];
+        const int64_t wtile = tg.lt + dist * mul[m];
         if (part == 0 && a.use_tma && !((a.dbg >> (3 + m)) & 1)) {
           __syncthreads();  // previous pass's xr writes
-          if (m == 0) l3_update_tma<LT, 0>(a, tg, xr, k_lo, k_hi, tg.lt + (wt - tm) * mul[m], &tm0, stg, bars, phases);
-          else if (m == 1) l3_update_tma<LT, 1>(a, tg, xr, k_lo, k_hi, tg.lt + (wt - tm) * mul[m], &tm1, stg, bars, phases);
-          else l3_update_tma<LT, 2>(a, tg, xr, k_lo, k_hi, tg.lt + (wt - tm) * mul[m], &tm2, stg, bars, phases);
+          if (m == 0) l3_update_tma<LT, 0>(a, tg, xr, k_lo, k_hi, wtile, &tm0, stg, bars, phases);
+          else if (m == 1) l3_update_tma<LT, 1>(a, tg, xr, k_lo, k_hi, wtile, &tm1, stg, bars, phases);
+          else l3_update_tma<LT, 2>(a, tg, xr, k_lo, k_hi, wtile, &tm2, stg, bars, phases);
           continue;
         }
-        if (tid == 0) wait_flag(a, tg.lt + (wt - tm) * mul[m]);
+        if (tid == 0) wait_flag(a, wtile);
         __syncthreads();
         if (m == 0) l3_update<LT, 0>(a, tg, xr, k_lo, k_hi);
         else if (m == 1) l3_update<LT, 1>(a, tg, xr, k_lo, k_hi);
         else l3_update<LT, 2>(a, tg, xr, k_lo, k_hi);
       }
     }
+    __syncthreads();
 
     mark(2);
-    // ---- That_m = Pinv D_m P on later-cell entries; lambda_m -----------------
-#pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      const int em = tg.ext[m];
-      const double* dm = db + m * EE;
-      const double* pm = pd + m * E * kPStride;
-      for (int e = tid; e < EE; e += L3_THREADS) {
-        const int i = e & MSK, j = e >> LT;
-        double re = 0.0, im = 0.0;
-        if (i < em && j < em && j >= tg.cend[m][i]) {
-          const int I0 = tg.cs[m][tg.cellof[m][i]], Iz = tg.cz[m][tg.cellof[m][i]];
-          const int J0 = tg.cs[m][tg.cellof[m][j]], Jz = tg.cz[m][tg.cellof[m][j]];
-          const double* pi = pm + I0 * kPStride + 12;
-          const double* pj = pm + J0 * kPStride + 4;
-          for (int aa = 0; aa < Iz; ++aa) {
-            const double wr = Iz == 2 ? pi[((i - I0) * 2 + aa) * 2] : 1.0;
-            const double wi = Iz == 2 ? pi[((i - I0) * 2 + aa) * 2 + 1] : 0.0;
-            for (int bb = 0; bb < Jz; ++bb) {
-              const double d = dm[(I0 + aa) + (J0 + bb) * E];
-              const double vr = Jz == 2 ? pj[(bb * 2 + (j - J0)) * 2] : 1.0;
-              const double vi = Jz == 2 ? pj[(bb * 2 + (j - J0)) * 2 + 1] : 0.0;
-              re += d * (wr * vr - wi * vi);
-              im += d * (wr * vi + wi * vr);
-            }
-          }
-        }
-        dh[m * 2 * EE + i + E * j] = re;
-        dh[m * 2 * EE + EE + i + E * j] = im;
-      }
-      if (tid < E) {
-        const int i = tid;
-        double lr = 0.0, li = 0.0;
-        if (i < em) {
-          const int I0 = tg.cs[m][tg.cellof[m][i]];
-          const double* p = pm + I0 * kPStride + (i - I0) * 2;
-          lr = p[0];
-          li = p[1];
-        }
-        lam[m * 2 * E + i] = lr;
-        lam[m * 2 * E + E + i] = li;
-      }
-    }
+    // That_m and lambda_m arrived with the staged copies (host tables).
     for (int l = tid; l < L3_T; l += L3_THREADS) xi[l] = 0.0;
     __syncthreads();
 
@@ -471,10 +458,10 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
     for (int m = 0; m < 3; ++m) {
       if (!(kp & (1 << m))) continue;  // uniform
       const double* pm = pd + m * E * kPStride;
-      // work item: (row i of mode m, cross-section n)
-      for (int w = tid; w < L3_T; w += L3_THREADS) {
-        const int i = w & MSK, n = w >> LT;
-        if (!tg.cplx[m][i]) continue;  // first row of a 2x2 block
+      // work item: (2x2 block of mode m, cross-section n)
+      const int nw = tg.npair[m] * EE;
+      for (int w = tid; w < nw; w += L3_THREADS) {
+        const int i = tg.prow[m][w >> (2 * LT)], n = w & (EE - 1);
         const int na = n & MSK, nb = n >> LT;
         int l, st;
         if (m == 0) l = l3off<LT>(i, na, nb), st = 1;
@@ -496,30 +483,61 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
     // lanes: (slot over the (c0, c1) cell grid) x (unknown inside the cell).
     // Modes 0 and 1 of a lane are fixed for the whole tile; only the mode-2
     // cell c2 = h - c0 - c1 moves with the hyperplane.
-    // lanes: (row i0, row i1, row bit b2 of a mode-2 pair); the mode-2 cell
-    // c2 = h - cell(i0) - cell(i1) moves with the hyperplane.
+    // Conjugate symmetry: the tile data are real, so in the eigenbasis
+    // xhat(sigma(u)) = conj(xhat(u)) with sigma swapping the two rows of every
+    // complex-pair block (same cell, same hyperplane).  Lanes are the orbit
+    // representatives (i0, i1, b2): the first complex-pair row decides; each
+    // solve writes u and sigma(u).
     const int nc2 = tg.nc[2];
     const int p2 = (kp & 4) ? 1 : 0;
+    if (tid == 0) tg.nlane = 0;
+    __syncthreads();
+    for (int L = tid; L < (EE << p2); L += L3_THREADS) {
+      const int rest = L >> p2;
+      const int i0 = rest & (E - 1), i1 = (rest >> LT) & (E - 1), b2 = L & p2;
+      if (i0 >= tg.ext[0] || i1 >= tg.ext[1]) continue;
+      const int k0 = tg.ckind[0][i0], k1 = tg.ckind[1][i1];
+      if (k0 == 2 || (k0 == 0 && k1 == 2)) continue;  // represented by its partner
+      tg.lane[atomicAdd(&tg.nlane, 1)] = static_cast<unsigned short>(i0 | (i1 << 4) | (b2 << 8));
+    }
+    __syncthreads();
+    const int nlane = tg.nlane;
     constexpr int LPT = (2 * EE + L3_THREADS - 1) / L3_THREADS;  // lanes per thread
-    int lc01[LPT], lb2[LPT], loff[LPT], lce0[LPT], lce1[LPT], li0[LPT], li1[LPT];
+    int lc01[LPT], lb2[LPT], loff[LPT], lce0[LPT], lce1[LPT], li0[LPT], li1[LPT], lsoff[LPT];
     double llr[LPT], lli[LPT];
-    bool lok[LPT];
+    bool lok[LPT], lcx[LPT];
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
       const int L = tid + q * L3_THREADS;
-      const int rest = L >> p2;
-      const int i0 = rest & (E - 1), i1 = (rest >> LT) & (E - 1);
-      lok[q] = rest < EE && i0 < tg.ext[0] && i1 < tg.ext[1];
+      lok[q] = L < nlane;
+      const int pk = lok[q] ? tg.lane[L] : 0;
+      const int i0 = pk & 15, i1 = (pk >> 4) & 15, b2 = (pk >> 8) & 1;
+      const int k0 = tg.ckind[0][i0], k1 = tg.ckind[1][i1];
       lc01[q] = tg.cellof[0][i0] + tg.cellof[1][i1];
-      lb2[q] = L & p2;
+      lb2[q] = b2;
       li0[q] = i0;
       li1[q] = i1;
       loff[q] = i0 + E * i1;
+      lcx[q] = k0 != 0 || k1 != 0;
+      // sigma of the (i0, i1) part of the offset
+      lsoff[q] = (k0 == 1 ? i0 + 1 : i0) + E * (k1 == 1 ? i1 + 1 : (k1 == 2 ? i1 - 1 : i1));
       lce0[q] = tg.cend[0][i0];
       lce1[q] = tg.cend[1][i1];
-      llr[q] = lam[i0] + lam[2 * E + i1];
-      lli[q] = lam[E + i0] + lam[3 * E + i1];
+      llr[q] = dh[2 * EE + i0] + dh[C::DHS + 2 * EE + i1];
+      lli[q] = dh[2 * EE + E + i0] + dh[C::DHS + 2 * EE + E + i1];
     }
+    if (tid < 2 * nc2) {
+      const int c2 = tid >> 1, b = tid & 1;
+      const int r0 = tg.cs[2][c2], z = tg.cz[2][c2];
+      const int i2 = r0 + (b && z == 2 ? 1 : 0);
+      const int k2 = tg.ckind[2][i2];
+      const int sg = k2 == 1 ? i2 + 1 : (k2 == 2 ? i2 - 1 : i2);
+      const int valid = (b == 0 || z == 2) ? 1 : 0;
+      tg.m2[c2][b] = static_cast<unsigned>(i2 | ((r0 + z) << 5) | (k2 << 10) | (sg << 12) | (valid << 17));
+      tg.m2lam[c2][b][0] = dh[2 * C::DHS + 2 * EE + i2];
+      tg.m2lam[c2][b][1] = dh[2 * C::DHS + 2 * EE + E + i2];
+    }
+    __syncthreads();
     bool singular = false;
     const int e0w = tg.ext[0], e1w = tg.ext[1], e2w = tg.ext[2];
     for (int h = tg.H; h >= 0; --h) {
@@ -527,62 +545,78 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
       for (int q = 0; q < LPT; ++q) {
         const int c2 = h - lc01[q];
         if (!lok[q] || c2 < 0 || c2 >= nc2) continue;
-        int i2 = tg.cs[2][c2];
-        if (lb2[q]) {
-          if (tg.cz[2][c2] != 2) continue;
-          i2 += 1;
-        }
+        const unsigned pk2 = tg.m2[c2][lb2[q]];
+        if (!(pk2 >> 17)) continue;
+        const int i2 = pk2 & 31, ce2 = (pk2 >> 5) & 31, k2 = (pk2 >> 10) & 3, sg2 = (pk2 >> 12) & 31;
+        // second row of a mode-2 complex pair: the partner lane (b2 = 0)
+        // owns this orbit unless modes 0/1 already decided it
+        if (lb2[q] && !lcx[q] && k2 == 2) continue;
         const int off = loff[q] + EE * i2;
-        double rr = xr[off], ri = xi[off];
-        // dots along the three modes: sum_j That_m[i_m, j] xhat(u | m -> j)
-        const int ii[3] = {li0[q], li1[q], i2};
-        const int jb0[3] = {lce0[q], lce1[q], tg.cs[2][c2] + tg.cz[2][c2]};
-        const int ee[3] = {e0w, e1w, e2w};
+        const bool orbit2 = lcx[q] || k2 != 0;  // sigma(u) != u
+        const int soff = lsoff[q] + EE * sg2;
+        const double mur = llr[q] + tg.m2lam[c2][lb2[q]][0];
+        const double mui = lli[q] + tg.m2lam[c2][lb2[q]][1];
+        // dots along the three modes, interleaved for ILP:
+        //   sum_m sum_{j >= cend_m} That_m[i_m, j] xhat(u | m -> j)
+        const int i0 = li0[q], i1 = li1[q];
+        const int L0 = e0w - lce0[q], L1 = e1w - lce1[q], L2 = e2w - ce2;
+        const double* d0 = dh + i0 + E * lce0[q];
+        const double* d1 = dh + C::DHS + i1 + E * lce1[q];
+        const double* d2 = dh + 2 * C::DHS + i2 + E * ce2;
+        const double* x0 = xr + off + (lce0[q] - i0);
+        const double* x1 = xr + off + E * (lce1[q] - i1);
+        const double* x2 = xr + off + EE * (ce2 - i2);
+        double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0, ar2 = 0.0, ai2 = 0.0;
+        if (!kp) {  // all-1x1 tile: real arithmetic
 #pragma unroll
-        for (int m = 0; m < 3; ++m) {
-          const int st = (m == 0) ? 1 : (m == 1 ? E : EE);
-          const int i = ii[m];
-          const double* drp = dh + m * 2 * EE + i;
-          const double* xrp = xr + off - i * st;
-          const double* xip = xi + off - i * st;
-          double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
-          int j = jb0[m];
-          const int em = ee[m];
-          for (; j + 1 < em; j += 2) {
-            const double cr = drp[E * j], ci = drp[EE + E * j];
-            const double yr = xrp[j * st], yi = xip[j * st];
-            const double cr2 = drp[E * (j + 1)], ci2 = drp[EE + E * (j + 1)];
-            const double yr2 = xrp[(j + 1) * st], yi2 = xip[(j + 1) * st];
-            ar0 = fma(cr, yr, ar0);
-            ar0 = fma(-ci, yi, ar0);
-            ai0 = fma(cr, yi, ai0);
-            ai0 = fma(ci, yr, ai0);
-            ar1 = fma(cr2, yr2, ar1);
-            ar1 = fma(-ci2, yi2, ar1);
-            ai1 = fma(cr2, yi2, ai1);
-            ai1 = fma(ci2, yr2, ai1);
+          for (int t = 0; t < E - 1; ++t) {
+            if (t < L0) ar0 = fma(d0[E * t], x0[t], ar0);
+            if (t < L1) ar1 = fma(d1[E * t], x1[E * t], ar1);
+            if (t < L2) ar2 = fma(d2[E * t], x2[EE * t], ar2);
           }
-          if (j < em) {
-            const double cr = drp[E * j], ci = drp[EE + E * j];
-            const double yr = xrp[j * st], yi = xip[j * st];
-            ar0 = fma(cr, yr, ar0);
-            ar0 = fma(-ci, yi, ar0);
-            ai0 = fma(cr, yi, ai0);
-            ai0 = fma(ci, yr, ai0);
+        } else {
+          const int XI = C::OFF_XI - C::OFF_XR;
+#pragma unroll
+          for (int t = 0; t < E - 1; ++t) {
+            if (t < L0) {
+              const double cr = d0[E * t], ci = d0[EE + E * t], yr = x0[t], yi = x0[XI + t];
+              ar0 = fma(cr, yr, ar0);
+              ar0 = fma(-ci, yi, ar0);
+              ai0 = fma(cr, yi, ai0);
+              ai0 = fma(ci, yr, ai0);
+            }
+            if (t < L1) {
+              const double cr = d1[E * t], ci = d1[EE + E * t], yr = x1[E * t], yi = x1[XI + E * t];
+              ar1 = fma(cr, yr, ar1);
+              ar1 = fma(-ci, yi, ar1);
+              ai1 = fma(cr, yi, ai1);
+              ai1 = fma(ci, yr, ai1);
+            }
+            if (t < L2) {
+              const double cr = d2[E * t], ci = d2[EE + E * t], yr = x2[EE * t], yi = x2[XI + EE * t];
+              ar2 = fma(cr, yr, ar2);
+              ar2 = fma(-ci, yi, ar2);
+              ai2 = fma(cr, yi, ai2);
+              ai2 = fma(ci, yr, ai2);
+            }
           }
-          rr -= ar0 + ar1;
-          ri -= ai0 + ai1;
         }
-        const double mur = llr[q] + lam[4 * E + i2], mui = lli[q] + lam[5 * E + i2];
+        const double rr = xr[off] - (ar0 + ar1 + ar2);
+        const double ri = xi[off] - (ai0 + ai1 + ai2);
         const double den = mur * mur + mui * mui;
+        double vr = 0.0, vi = 0.0;
         if (!(den > a.tiny * a.tiny)) {
           singular = true;
-          xr[off] = 0.0;
-          xi[off] = 0.0;
         } else {
           const double inv = 1.0 / den;
-          xr[off] = (rr * mur + ri * mui) * inv;
-          xi[off] = (ri * mur - rr * mui) * inv;
+          vr = (rr * mur + ri * mui) * inv;
+          vi = (ri * mur - rr * mui) * inv;
+        }
+        xr[off] = vr;
+        xi[off] = vi;
+        if (orbit2) {
+          xr[soff] = vr;
+          xi[soff] = -vi;
         }
       }
       __syncthreads();
@@ -596,9 +630,9 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
     for (int m = 0; m < 3; ++m) {
       if (!(kp & (1 << m))) continue;
       const double* pm = pd + m * E * kPStride;
-      for (int w = tid; w < L3_T; w += L3_THREADS) {
-        const int i = w & MSK, n = w >> LT;
-        if (!tg.cplx[m][i]) continue;
+      const int nw = tg.npair[m] * EE;
+      for (int w = tid; w < nw; w += L3_THREADS) {
+        const int i = tg.prow[m][w >> (2 * LT)], n = w & (EE - 1);
         const int na = n & MSK, nb = n >> LT;
         int l, st;
         if (m == 0) l = l3off<LT>(i, na, nb), st = 1;
@@ -626,6 +660,11 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
     if (tid == 0) {
       __threadfence();
       st_release(a.flags + tg.lt, a.epoch);
+      if (a.trace) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[tg.lt] = t;
+      }
     }
     mark(6);
     if (a.prof && tid == 0) atomicAdd(a.prof + 8, 1ull);
@@ -636,9 +675,11 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? 4 : 2)
 
 template <int LT>
 cudaError_t launch_l3(const SolveArgs& a0, cudaStream_t st, SolveLaunchInfo* info) {
+  using C = L3C<LT>;
   SolveArgs a = a0;
   // TMA maps over the work tensor, one box shape per mode (E x E x KCH)
   CUtensorMap maps[3];
+  std::memset(maps, 0, sizeof(maps));
   {
     const uint64_t dims[3] = {static_cast<uint64_t>(a.dims[0]), static_cast<uint64_t>(a.dims[1]),
                               static_cast<uint64_t>(a.dims[2])};
@@ -647,30 +688,30 @@ cudaError_t launch_l3(const SolveArgs& a0, cudaStream_t st, SolveLaunchInfo* inf
     // tile shapes; see DESIGN.md.
     bool ok = (a.dims[0] % 2 == 0) && std::getenv("TSG_TMA") != nullptr;
     for (int m = 0; m < 3 && ok; ++m) {
-      uint32_t box[3] = {L3C<LT>::E, L3C<LT>::E, L3C<LT>::E};
-      box[m] = L3C<LT>::KCH;
+      uint32_t box[3] = {C::E, C::E, C::E};
+      box[m] = C::KCH;
       ok = encode_tmap_f64(&maps[m], a.X, 3, dims, box);
     }
     a.use_tma = ok ? 1 : 0;
-    if (!ok) std::memset(maps, 0, sizeof(maps));
   }
-  using C = L3C<LT>;
-  static int nsm = 0, occ = 0;
+  // the TMA ring is the last smem region: leave it out when unused
+  const int bytes = a.use_tma ? C::BYTES : C::OFF_STG * 8;
+  static int nsm = 0, occ[2] = {0, 0};
   auto k = solve_lap3_kernel<LT>;
-  if (occ == 0) {
+  if (occ[a.use_tma] == 0) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, C::THREADS, C::BYTES);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.use_tma], k, C::THREADS, bytes);
     if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
+    if (occ[a.use_tma] < 1) occ[a.use_tma] = 1;
   }
-  int64_t grid = static_cast<int64_t>(nsm) * occ;
+  int64_t grid = static_cast<int64_t>(nsm) * occ[a.use_tma];
   if (grid > a.ntiles) grid = a.ntiles;
-  if (info) *info = SolveLaunchInfo{static_cast<int>(grid), C::THREADS, C::BYTES, occ};
-  k<<<static_cast<unsigned>(grid), C::THREADS, C::BYTES, st>>>(a, maps[0], maps[1], maps[2]);
+  if (info) *info = SolveLaunchInfo{static_cast<int>(grid), C::THREADS, bytes, occ[a.use_tma]};
+  k<<<static_cast<unsigned>(grid), C::THREADS, bytes, st>>>(a, maps[0], maps[1], maps[2]);
   return cudaGetLastError();
 }
 
