@@ -20,6 +20,7 @@
 // distinct 8-byte bank pairs (conflict-free LDS.64).
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm.h"
@@ -29,7 +30,10 @@ namespace tsg {
 namespace {
 
 constexpr int BK = 16;
-constexpr int kStages = 3;
+#ifndef TSG_GEMM_STAGES
+#define TSG_GEMM_STAGES 3
+#endif
+constexpr int kStages = TSG_GEMM_STAGES;
 
 template <int BM, int BN>
 struct GemmSmem {
@@ -42,11 +46,11 @@ struct GemmSmem {
 };
 
 template <int BM, int BN, int WM, int WN, bool VEC>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 dgemm_nn_kernel(GemmArgs g) {
   using S = GemmSmem<BM, BN>;
   constexpr int NWM = BM / WM;              // warps along M
-  static_assert((BM / WM) * (BN / WN) == 8, "8 warps");
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
   constexpr int FM = WM / 8, FN = WN / 8;   // 8x8 fragments per warp
   extern __shared__ __align__(16) double smem[];
 
@@ -73,7 +77,7 @@ dgemm_nn_kernel(GemmArgs g) {
     if (VEC) {
       // A: BK columns of BM contiguous doubles -> 16-byte chunks.
       constexpr int ACH = BK * BM / 2;
-      for (int c = tid; c < ACH; c += 256) {
+      for (int c = tid; c < ACH; c += NT) {
         const int kk = c / (BM / 2), mm = (c % (BM / 2)) * 2;
         const int gm = m0 + mm, gk = k0 + kk;
         int bytes = 0;
@@ -86,7 +90,7 @@ dgemm_nn_kernel(GemmArgs g) {
       }
       // B: BN columns of BK contiguous doubles.
       constexpr int BCH = BN * BK / 2;
-      for (int c = tid; c < BCH; c += 256) {
+      for (int c = tid; c < BCH; c += NT) {
         const int nn = c / (BK / 2), kk = (c % (BK / 2)) * 2;
         const int gn = n0 + nn, gk = k0 + kk;
         int bytes = 0;
@@ -98,14 +102,14 @@ dgemm_nn_kernel(GemmArgs g) {
         cp_async16(sb + nn * S::LDB + kk, src, bytes);
       }
     } else {
-      for (int c = tid; c < BK * BM; c += 256) {
+      for (int c = tid; c < BK * BM; c += NT) {
         const int kk = c / BM, mm = c % BM;
         const int gm = m0 + mm, gk = k0 + kk;
         const bool ok = gk < g.K && gm < g.M;
         cp_async8(sa + kk * S::LDA + mm,
                   ok ? A + static_cast<int64_t>(gk) * g.lda + gm : A, ok ? 8 : 0);
       }
-      for (int c = tid; c < BN * BK; c += 256) {
+      for (int c = tid; c < BN * BK; c += NT) {
         const int nn = c / BK, kk = c % BK;
         const int gn = n0 + nn, gk = k0 + kk;
         const bool ok = gn < g.N && gk < g.K;
@@ -190,7 +194,7 @@ cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
       attr = true;
     }
-    k<<<static_cast<unsigned>(tiles), 256, S::BYTES, st>>>(g);
+    k<<<static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, st>>>(g);
   } else {
     auto k = dgemm_nn_kernel<BM, BN, WM, WN, false>;
     static bool attr = false;
@@ -198,7 +202,7 @@ cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
       attr = true;
     }
-    k<<<static_cast<unsigned>(tiles), 256, S::BYTES, st>>>(g);
+    k<<<static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, st>>>(g);
   }
   return cudaGetLastError();
 }
@@ -207,8 +211,23 @@ cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
 
 cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
-  // Tile choice: the big dimension gets the 128 side; small-N slabs
-  // (middle-mode transforms with n_m <= 64) use a 64-wide N tile.
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = std::getenv("TSG_GEMM_CFG");
+    cfg = e ? std::atoi(e) : 0;
+  }
+  if (cfg == 1 && g.M >= 128 && g.N >= 64) return launch_cfg<128, 64, 32, 32>(g, st);   // 8 warps, 2 CTA/SM
+  if (cfg == 2 && g.M >= 128 && g.N >= 128) return launch_cfg<128, 128, 32, 32>(g, st); // 16 warps
+  if (cfg == 3 && g.M >= 128 && g.N >= 128) return launch_cfg<128, 128, 32, 64>(g, st); // 8 warps 32x64
+  if (cfg == 4 && g.M >= 64 && g.N >= 128) return launch_cfg<64, 128, 32, 32>(g, st);   // 8 warps
+  if (cfg == 5 && g.M >= 128 && g.N >= 128) return launch_cfg<128, 128, 64, 64>(g, st); // 4 warps
+  if (cfg == 6 && g.M >= 64 && g.N >= 64) return launch_cfg<64, 64, 32, 32>(g, st);      // 4 warps
+  if (cfg == 7 && g.M >= 128 && g.N >= 64) return launch_cfg<128, 64, 64, 16>(g, st);    // 8 warps
+  // Default: 64x64 CTA tiles of four 32x32-DMMA warps (up to 4 CTAs/SM);
+  // measured best on the C2/C4 transforms (29-32 TF/s vs 24-25 for 128x128
+  // with one CTA per SM, profiles/r01_gemm_configs.log).
+  if (g.M >= 64 && g.N >= 64) return launch_cfg<64, 64, 32, 32>(g, st);
+  // Small-N slabs (middle-mode transforms with n_m < 64) / small-M.
   if (g.N <= 64 && g.M >= 128) return launch_cfg<128, 64, 32, 32>(g, st);
   if (g.M <= 64 && g.N >= 128) return launch_cfg<64, 128, 32, 32>(g, st);
   if (g.M <= 64 && g.N <= 64) return launch_cfg<64, 64, 32, 16>(g, st);
