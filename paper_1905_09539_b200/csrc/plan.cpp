@@ -63,7 +63,7 @@ struct tsg_plan {
   std::vector<int64_t> stride;
   int64_t N = 0;
   // device factors
-  std::vector<DevBuf> T, Fwd, FwdT, Bwd, BwdT, eig, pdat, dhat;  // per mode
+  std::vector<DevBuf> T, Fwd, FwdT, Bwd, BwdT, eig, pdat, dhat, vhat;  // per mode
   DevBuf Tc;
   std::vector<tsg::TileMode*> tmode;
   std::vector<int*> bnd;
@@ -312,6 +312,109 @@ std::vector<int> tile_bounds(int n, int b, const std::vector<int8_t>& code) {
   return bd;
 }
 
+// Eigenvectors of every tile's diagonal block, for the lap3 diagonalised
+// tiles.  In the eigenbasis of its 2x2 cells the block is upper triangular
+// (That, diagonal lambda; dh tables above), so its eigenvectors Vh are unit
+// upper triangular by back substitution:
+//   Vh[i][k] = sum_{j >= cend(i)} That[i][j] Vh[j][k] / (lambda_k - lambda_i).
+// V = P_tile Vh (columns scaled to unit norm), V^{-1} = Vh^{-1} P_tile^{-1},
+// all in long double.  vcond = ||V||_F ||V^{-1}||_F / ext (1 for a normal
+// block; inf when two eigenvalues coincide).
+void tile_eigvecs(std::vector<tsg::TileMode>& tms, const std::vector<double>& dh,
+                  const std::vector<double>& pdv, std::vector<double>& vh) {
+  using Cx = std::complex<long double>;
+  constexpr int E = 8, EE = 64, DHS = 2 * EE + 2 * E, VHS = tsg::kVhStride;
+  vh.assign(tms.size() * VHS, 0.0);
+  for (size_t t = 0; t < tms.size(); ++t) {
+    tsg::TileMode& tm = tms[t];
+    const int ex = tm.ext;
+    const double* o = dh.data() + t * DHS;
+    double* out = vh.data() + t * VHS;
+    Cx Th[E][E] = {}, lam[E], P[E][E] = {}, Pi[E][E] = {};
+    for (int i = 0; i < ex; ++i) {
+      lam[i] = Cx(o[2 * EE + i], o[2 * EE + E + i]);
+      for (int j = tm.cend[i]; j < ex; ++j) Th[i][j] = Cx(o[i + E * j], o[EE + i + E * j]);
+    }
+    for (int c = 0; c < tm.nc; ++c) {
+      const int r0 = tm.cs[c], z = tm.cz[c];
+      if (z == 1) {
+        P[r0][r0] = Pi[r0][r0] = 1.0L;
+        continue;
+      }
+      const double* pr = pdv.data() + static_cast<size_t>(tm.start + r0) * tsg::kPStride;
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+          P[r0 + a][r0 + b] = Cx(pr[4 + (a * 2 + b) * 2], pr[5 + (a * 2 + b) * 2]);
+          Pi[r0 + a][r0 + b] = Cx(pr[12 + (a * 2 + b) * 2], pr[13 + (a * 2 + b) * 2]);
+        }
+    }
+    Cx Vh[E][E] = {}, W[E][E] = {};
+    bool ok = true;
+    for (int k = 0; k < ex && ok; ++k) {
+      Vh[k][k] = 1.0L;
+      for (int i = k - 1; i >= 0; --i) {
+        Cx s = 0.0L;
+        for (int j = tm.cend[i]; j <= k; ++j) s += Th[i][j] * Vh[j][k];
+        const Cx dl = lam[k] - lam[i];
+        if (std::abs(s) == 0.0L) continue;
+        if (std::abs(dl) == 0.0L) {
+          ok = false;
+          break;
+        }
+        Vh[i][k] = s / dl;
+      }
+    }
+    for (int c = 0; c < ex && ok; ++c) {  // W = Vh^{-1}
+      W[c][c] = 1.0L;
+      for (int i = c - 1; i >= 0; --i) {
+        Cx s = 0.0L;
+        for (int j = i + 1; j <= c; ++j) s += Vh[i][j] * W[j][c];
+        W[i][c] = -s;
+      }
+    }
+    Cx V[E][E] = {}, Vi[E][E] = {};
+    long double nv = 0, ni = 0;
+    if (ok) {
+      for (int i = 0; i < ex; ++i)
+        for (int k = 0; k < ex; ++k)
+          for (int j = 0; j < ex; ++j) {
+            V[i][k] += P[i][j] * Vh[j][k];
+            Vi[i][k] += W[i][j] * Pi[j][k];
+          }
+      for (int k = 0; k < ex; ++k) {  // unit columns of V, matching rows of V^{-1}
+        long double cn = 0;
+        for (int i = 0; i < ex; ++i) cn += std::norm(V[i][k]);
+        cn = std::sqrt(cn);
+        for (int i = 0; i < ex; ++i) {
+          V[i][k] /= cn;
+          Vi[k][i] *= cn;
+        }
+      }
+      for (int i = 0; i < ex; ++i)
+        for (int k = 0; k < ex; ++k) {
+          nv += std::norm(V[i][k]);
+          ni += std::norm(Vi[i][k]);
+        }
+    }
+    const long double vc = ok ? std::sqrt(nv * ni) / ex : 0.0L;
+    tm.vcond = ok && std::isfinite(static_cast<double>(vc)) ? static_cast<float>(vc)
+                                                           : std::numeric_limits<float>::infinity();
+    for (int i = 0; i < E; ++i) {
+      for (int k = 0; k < E; ++k) {
+        const bool in = i < ex && k < ex;
+        const Cx vi = in ? Vi[i][k] : Cx(i == k ? 1.0L : 0.0L);
+        const Cx v = in ? V[i][k] : Cx(i == k ? 1.0L : 0.0L);
+        out[i * E + k] = static_cast<double>(vi.real());
+        out[EE + i * E + k] = static_cast<double>(vi.imag());
+        out[2 * EE + i * E + k] = static_cast<double>(v.real());
+        out[3 * EE + i * E + k] = static_cast<double>(v.imag());
+      }
+      out[4 * EE + i] = i < ex ? static_cast<double>(lam[i].real()) : 1.0;
+      out[4 * EE + E + i] = i < ex ? static_cast<double>(lam[i].imag()) : 0.0;
+    }
+  }
+}
+
 int capture_or_run(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool graph);
 
 }  // namespace
@@ -399,6 +502,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   pl->eig.resize(d);
   pl->pdat.resize(d);
   pl->dhat.resize(d);
+  pl->vhat.resize(d);
   std::vector<std::vector<double>> pdvs(d), nfs(d);
   pl->tmode.assign(d, nullptr);
   pl->bnd.assign(d, nullptr);
@@ -490,7 +594,6 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       }
       tmd.nc = static_cast<unsigned char>(nc);
     }
-    TSG_CU(upload(&pl->tmode[m], tms));
     if (pl->fast == 3) {
       // Eigenbasis diagonal block of every tile index along mode m:
       // That[i][j] = sum Pinv_blk(i)[i,a] T[a,b] P_blk(j)[b,j] for j beyond
@@ -527,7 +630,13 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         }
       }
       TSG_CU(upload_mat(pl->dhat[m], dh.data(), dh.size()));
+      if (pl->lt3 == 3) {
+        std::vector<double> vh;
+        tile_eigvecs(tms, dh, pdvs[m], vh);
+        TSG_CU(upload_mat(pl->vhat[m], vh.data(), vh.size()));
+      }
     }
+    TSG_CU(upload(&pl->tmode[m], tms));
   }
   if (pl->ntiles > INT_MAX / 2) return fail(ctx, TSG_EDIM, "too many tiles");
   for (int m = 0; m < d; ++m)
@@ -867,6 +976,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     a.eig[m] = pl->eig[m].p;
     a.pdat[m] = pl->pdat[m].p;
     a.dhat[m] = pl->dhat[m].p;
+    a.vhat[m] = pl->vhat[m].p;
     a.ntiles_mode[m] = pl->ntiles_mode[m];
     a.bnd[m] = pl->bnd[m];
     if (pl->family == 1 && m >= 1) a.W[m] = pl->wchain[m].p;

@@ -21,7 +21,15 @@ struct TileMode {
   unsigned char cend[kMaxCells];    // tile row -> first row after its cell
   unsigned char cplx[kMaxCells];    // 1 on the first row of a 2x2 block
   unsigned char ckind[kMaxCells];   // 1/2: first/second row of a complex-eigenvalue pair, else 0
+  float vcond;                      // lap3: ||V||_F ||V^-1||_F / ext of the block's eigenvectors
 };
+
+// lap3 diagonalised tiles: per tile index along a mode, V^{-1} (re, im),
+// V (re, im) as 8x8 row-major (identity-padded) and lambda (re, im).
+constexpr int kVhStride = 4 * 64 + 2 * 8;
+// A tile is diagonalised when the product of its three vcond values is at
+// most this (the eigenvector transforms then cost <= ~kDiagCond ulps).
+constexpr float kDiagCond = 1000.0f;
 
 // Reduced Laplace-like / gsylv equation on a tiled tensor, solved in place
 // by one persistent dataflow kernel (see solve.cu for the algorithm).
@@ -45,6 +53,7 @@ struct SolveArgs {
   const unsigned long long* ocoord;  // packed tile coordinates of order[] (10 bits/mode)
   const double* pdat[kMaxOrder];     // per row: kPStride doubles (fast Laplace path)
   const double* dhat[kMaxOrder];     // per tile index: eigenbasis diag block + lambdas (lap3)
+  const double* vhat[kMaxOrder];     // per tile index: eigenvectors of the diag block (lap3)
   int* flags;                   // per tile: epoch when solved
   int* counter;                 // work queue head (zeroed before launch)
   int* status;                  // first singular cell linear index (or INT_MAX)
@@ -52,7 +61,6 @@ struct SolveArgs {
   double tiny;                  // |cell eigenvalue| <= tiny -> singular
   int refine;                   // 1: one refinement step per base cell
   int dbg;                      // ablation mask (development only; 0 in production)
-  int use_tma;                  // far updates through TMA tensor maps (set by the launcher)
   unsigned long long* prof;     // optional per-phase cycle counters (development)
   unsigned long long* trace;    // optional per-tile release globaltimer (development)
 };

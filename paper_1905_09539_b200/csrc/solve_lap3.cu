@@ -26,7 +26,6 @@
 #include "common.cuh"
 #include "solve.h"
 #include "solve_common.cuh"
-#include "tma.h"
 
 namespace tsg {
 namespace {
@@ -56,12 +55,12 @@ struct L3C {
   static constexpr int OFF_DH = OFF_XI + T;
   static constexpr int OFF_PD = OFF_DH + 3 * DHS;        // eigenbasis rows: 3 x E x kPStride
   static constexpr int OFF_LAM = OFF_PD + 3 * E * kPStride;
-  // TMA ring for the far updates: NST boxes of E x E x KCH doubles
-  static constexpr int KCH = LT == 3 ? 32 : 8;
-  static constexpr int NST = LT == 3 ? 3 : 2;
-  static constexpr int CH = E * E * KCH;
-  static constexpr int OFF_STG = OFF_LAM;
-  static constexpr int DOUBLES = OFF_STG + NST * CH;
+  static_assert(LT != 3 || 3 * kVhStride <= OFF_LAM - OFF_DH, "vh aliases dh + pd");
+  // K-split far updates (LT = 3): warps 1..WARPS-1 accumulate their partial
+  // tile products in private buffers, warp 0 directly into xr
+  static constexpr bool KSPLIT = LT == 3;
+  static constexpr int OFF_RED = OFF_LAM;
+  static constexpr int DOUBLES = OFF_RED + (KSPLIT ? (WARPS - 1) * T : 0);
   static constexpr int BYTES = DOUBLES * 8;
 };
 
@@ -69,7 +68,8 @@ struct L3Geom {
   int64_t lt;
   int64_t gbase;
   int start[3], ext[3], tco[3];
-  int nc[3], H, kp;
+  int nc[3], H, kp, diag;
+  float vc[3];
   unsigned char cs[3][16], cz[3][16], cellof[3][16], cend[3][16], cplx[3][16], ckind[3][16];
   int npair[3];
   int nlane;
@@ -222,98 +222,185 @@ TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile) {
   }
 }
 
-// Far-tile update along mode M with TMA-staged K chunks: one elected thread
-// streams boxes of (KCH rows along M) x (the tile's E x E cross-section) of
-// X into an NST-deep mbarrier ring; every warp runs DMMA with B fragments
-// from the landed box and A fragments (T_M columns) from L1/L2.
+// ---- far updates of all three modes in one pass, K split across warps ------
+// The k4-steps of the three far ranges (rows >= bnd[t_m + 3] of each mode)
+// are concatenated and cut into WARPS equal slices.  A warp accumulates the
+// whole E x E^2 product of its current mode in registers (one 8-row block,
+// all E column blocks) and, at a mode change or the end of its slice, folds
+// it into xr (warp 0, subtracting) or its private buffer (adding; folded
+// into xr after the near updates).  Every warp thus walks a quarter of the
+// K range instead of all of it: 4x fewer dependent L2 round trips per tile
+// than splitting the columns.
+#ifndef L3_UB
+#define L3_UB 3
+#endif
 template <int LT, int M>
-TSG_DEVINL void l3_update_tma(const SolveArgs& a, const L3Geom& tg, double* xr, int k_lo, int k_hi,
-                              int64_t wait_tile, const CUtensorMap* map, double* stg, uint64_t* bars,
-                              unsigned& phases) {
-  using C = L3C<LT>;
-  constexpr int E = C::E, EE = E * E, MB = C::MB, NBW = C::NBW, KCH = C::KCH, NST = C::NST,
-                CH = C::CH;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, int k_lo, int k_hi, double* dst,
+                           bool sub) {
+  constexpr int E = L3C<LT>::E, UB = L3_UB;
+  static_assert(E == 8, "one 8-row DMMA block per mode");
+  const int lane = threadIdx.x & 31;
   const int gq = lane >> 2, tq = lane & 3;
-  const int nch = (k_hi - k_lo + KCH - 1) / KCH;
-  auto issue = [&](int cidx, int st) {
-    int cc[3] = {tg.start[0], tg.start[1], tg.start[2]};
-    cc[M] = k_lo + cidx * KCH;
-    mbar_expect_tx(bars + st, CH * 8);
-    tma_load_3d(stg + st * CH, map, cc[0], cc[1], cc[2], bars + st);
-  };
-  if (tid == 0) {
-    wait_flag(a, wait_tile);
-    fence_proxy_async();
-    for (int st = 0; st < NST && st < nch; ++st) issue(st, st);
-  }
+  constexpr int VA = (M == 0) ? 1 : 0, VB = (M == 2) ? 1 : 2;  // the other two modes
   const int nm = a.dims[M];
-  const double* __restrict__ Tm = a.T[M];
-  const int row0 = tg.start[M], em = tg.ext[M];
-  int arow[MB];
+  const int ea = tg.ext[VA], eb = tg.ext[VB], em = tg.ext[M];
+  // B column n = 8 jb + gq  <->  cross-section (VA = gq, VB = jb)
+  const int64_t SJ = a.stride[VB];
+  const int ia = gq < ea ? gq : ea - 1;  // padded lanes re-read a valid column
+  const int64_t base = static_cast<int64_t>(tg.start[VA] + ia) * a.stride[VA] +
+                       static_cast<int64_t>(tg.start[VB]) * SJ;
+  const int row = tg.start[M] + (gq < em ? gq : em - 1);
+  const double* pa = a.T[M] + static_cast<int64_t>(k_lo + tq) * nm + row;
+  const double* pb = a.X + base + static_cast<int64_t>(k_lo + tq) * a.stride[M];
+  const int64_t sa = 4 * static_cast<int64_t>(nm), sb = 4 * a.stride[M];
+  double c[E][2];
 #pragma unroll
-  for (int ib = 0; ib < MB; ++ib) arow[ib] = (gq + 8 * ib < em) ? row0 + gq + 8 * ib : row0;
-  // stage offsets of this lane's B fragment columns
-  int bcol[NBW];
+  for (int jb = 0; jb < E; ++jb) c[jb][0] = c[jb][1] = 0.0;
+  const int nfs = (k_hi - k_lo) >> 2;  // k4-steps with all four rows valid
+  const int nb = nfs / UB;
+  for (int bt = 0; bt < nb; ++bt) {
+    double af[UB], bf[UB][E];
 #pragma unroll
-  for (int jb = 0; jb < NBW; ++jb) {
-    const int n = 8 * NBW * warp + 8 * jb + gq;
-    const int ia = n & (E - 1), ib = n >> LT;
-    bcol[jb] = (M == 0) ? KCH * n : (M == 1 ? ia + E * KCH * ib : n);
-  }
-  constexpr int KST = (M == 0) ? 1 : (M == 1 ? E : EE);  // stage stride along k
-  double c[MB][NBW][2];
+    for (int u = 0; u < UB; ++u) {
+      af[u] = __ldg(pa);
+      pa += sa;
 #pragma unroll
-  for (int ib = 0; ib < MB; ++ib)
-#pragma unroll
-    for (int jb = 0; jb < NBW; ++jb) c[ib][jb][0] = c[ib][jb][1] = 0.0;
-  for (int ci = 0; ci < nch; ++ci) {
-    const int st = ci % NST;
-    mbar_wait(bars + st, (phases >> st) & 1u);
-    phases ^= 1u << st;
-    const double* B = stg + st * CH;
-    const int kb = k_lo + ci * KCH;
-#pragma unroll
-    for (int k4 = 0; k4 < KCH; k4 += 4) {
-      const int kg = kb + k4 + tq;
-      const bool kok = kg < k_hi;
-      double af[MB], bf[NBW];
-#pragma unroll
-      for (int ib = 0; ib < MB; ++ib)
-        af[ib] = kok ? __ldg(Tm + static_cast<int64_t>(kg) * nm + arow[ib]) : 0.0;
-#pragma unroll
-      for (int jb = 0; jb < NBW; ++jb) bf[jb] = B[bcol[jb] + (k4 + tq) * KST];
-#pragma unroll
-      for (int ib = 0; ib < MB; ++ib)
-#pragma unroll
-        for (int jb = 0; jb < NBW; ++jb) dmma(c[ib][jb][0], c[ib][jb][1], af[ib], bf[jb]);
+      for (int jb = 0; jb < E; ++jb) bf[u][jb] = jb < eb ? ld_cg(pb + jb * SJ) : 0.0;
+      pb += sb;
     }
-    __syncthreads();  // stage st fully consumed
-    if (tid == 0 && ci + NST < nch) {
-      fence_proxy_async();
-      issue(ci + NST, st);
-    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u)
+#pragma unroll
+      for (int jb = 0; jb < E; ++jb)
+        if (jb < eb) dmma(c[jb][0], c[jb][1], af[u], bf[u][jb]);
   }
+  // remaining steps (the last one possibly partial), masked per row
+  for (int k = k_lo + 4 * nb * UB; k < k_hi; k += 4) {
+    const bool kok = k + tq < k_hi;
+    const double av = kok ? __ldg(pa) : 0.0;
+    double bv[E];
 #pragma unroll
-  for (int ib = 0; ib < MB; ++ib)
+    for (int jb = 0; jb < E; ++jb) bv[jb] = (kok && jb < eb) ? ld_cg(pb + jb * SJ) : 0.0;
+    pa += sa;
+    pb += sb;
 #pragma unroll
-    for (int jb = 0; jb < NBW; ++jb)
+    for (int jb = 0; jb < E; ++jb)
+      if (jb < eb) dmma(c[jb][0], c[jb][1], av, bv[jb]);
+  }
+  // fold: row i = gq of mode M, cross-section (VA = 2 tq + h, VB = jb)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = 8 * ib + gq, n = 8 * NBW * warp + 8 * jb + 2 * tq + h;
-        const int ia = n & (E - 1), ib2 = n >> LT;
-        int l;
-        if (M == 0) l = l3off<LT>(i, ia, ib2);
-        else if (M == 1) l = l3off<LT>(ia, i, ib2);
-        else l = l3off<LT>(ia, ib2, i);
-        xr[l] -= c[ib][jb][h];
+  for (int jb = 0; jb < E; ++jb)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = gq, va = 2 * tq + h;
+      int l;
+      if (M == 0) l = l3off<LT>(i, va, jb);
+      else if (M == 1) l = l3off<LT>(va, i, jb);
+      else l = l3off<LT>(va, jb, i);
+      dst[l] += sub ? -c[jb][h] : c[jb][h];
+    }
+}
+
+template <int LT>
+TSG_DEVINL void l3_far_ksplit(const SolveArgs& a, const L3Geom& tg, double* xr, double* red,
+                              const int* klo, const int* khi) {
+  using C = L3C<LT>;
+  const int warp = threadIdx.x >> 5;
+  int s[3], S = 0;
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    s[m] = (khi[m] - klo[m] + 3) >> 2;
+    S += s[m];
+  }
+  if (S == 0) return;
+  const int w0 = (S * warp) / C::WARPS, w1 = (S * (warp + 1)) / C::WARPS;
+  double* dst = warp == 0 ? xr : red + (warp - 1) * C::T;
+  const bool sub = warp == 0;
+  int off = 0;
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    const int lo = w0 > off ? w0 : off, hi = w1 < off + s[m] ? w1 : off + s[m];
+    if (lo < hi) {
+      const int kl = klo[m] + 4 * (lo - off);
+      const int kh = min(khi[m], klo[m] + 4 * (hi - off));
+      if (m == 0) l3_far_seg<LT, 0>(a, tg, kl, kh, dst, sub);
+      else if (m == 1) l3_far_seg<LT, 1>(a, tg, kl, kh, dst, sub);
+      else l3_far_seg<LT, 2>(a, tg, kl, kh, dst, sub);
+    }
+    off += s[m];
+  }
+}
+
+// ---- diagonalised tiles ------------------------------------------------------
+// When the eigenvector bases V_m of the tile's three diagonal blocks are well
+// conditioned (host vcond tables), the in-tile Kronecker-sum solve is
+//   x^ = x x_0 V0^-1 x_1 V1^-1 x_2 V2^-1,  x^ /= l0_i + l1_j + l2_k,
+//   x  = x^ x_0 V0 x_1 V1 x_2 V2
+// i.e. six complex 8x8 mode products on DMMA (real input for the first, real
+// output for the last) and no wavefront.  Warp w owns cross-section column
+// blocks 2w and 2w+1; the matrix is row-major (8 x 8) in shared memory.
+template <int M>
+TSG_DEVINL int l3d_addr(int i, int n) {  // tile offset of mode-M row i, cross-section column n
+  if (M == 0) return i + 8 * n;
+  if (M == 1) return (n & 7) + 8 * i + 64 * (n >> 3);
+  return n + 64 * i;
+}
+
+template <int M, bool CIN, bool COUT, bool DIV>
+TSG_DEVINL bool l3d_mode(const double* sr, const double* si, double* dr, double* di, const double* Ar,
+                         const double* Ai, const double* vh, const int* ext, double tiny) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  double cr[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, ci[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    const int k = 4 * ks + t;
+    const double ar = Ar[8 * g + k], ai = Ai[8 * g + k];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int n = 8 * (2 * warp + q) + g;
+      const double br = sr[l3d_addr<M>(k, n)];
+      dmma(cr[q][0], cr[q][1], ar, br);
+      if (COUT) dmma(ci[q][0], ci[q][1], ai, br);
+      if (CIN) {
+        const double bi = si[l3d_addr<M>(k, n)];
+        dmma(cr[q][0], cr[q][1], -ai, bi);
+        if (COUT) dmma(ci[q][0], ci[q][1], ar, bi);
       }
+    }
+  }
+  bool sing = false;
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int n = 8 * (2 * warp + q) + 2 * t + h;
+      double vr = cr[q][h], vi = ci[q][h];
+      if (DIV) {  // M == 2: rows are i2, columns (i0, i1)
+        const int i0 = n & 7, i1 = n >> 3;
+        const double mr = vh[4 * 64 + i0] + vh[kVhStride + 4 * 64 + i1] + vh[2 * kVhStride + 4 * 64 + g];
+        const double mi = vh[4 * 64 + 8 + i0] + vh[kVhStride + 4 * 64 + 8 + i1] +
+                          vh[2 * kVhStride + 4 * 64 + 8 + g];
+        const double den = mr * mr + mi * mi;
+        if (!(den > tiny * tiny)) {
+          if (i0 < ext[0] && i1 < ext[1] && g < ext[2]) sing = true;
+          vr = vi = 0.0;
+        } else {
+          const double inv = 1.0 / den;
+          const double r = (cr[q][h] * mr + ci[q][h] * mi) * inv;
+          vi = (ci[q][h] * mr - cr[q][h] * mi) * inv;
+          vr = r;
+        }
+      }
+      dr[l3d_addr<M>(g, n)] = vr;
+      if (COUT) di[l3d_addr<M>(g, n)] = vi;
+    }
+  return sing;
 }
 
 template <int LT>
 __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
-    solve_lap3_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tm0,
-                      const __grid_constant__ CUtensorMap tm1, const __grid_constant__ CUtensorMap tm2) {
+    solve_lap3_kernel(SolveArgs a) {
   using C = L3C<LT>;
   constexpr int E = C::E, L3_T = C::T, L3_THREADS = C::THREADS;
   constexpr int EE = E * E, MSK = E - 1;
@@ -325,15 +412,8 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
   double* dh = smem + C::OFF_DH;
   double* pd = smem + C::OFF_PD;
   double* lam = smem + C::OFF_LAM;
-  double* stg = smem + C::OFF_STG;
-  __shared__ __align__(8) uint64_t bars[C::NST];
-  unsigned phases = 0;
+  double* red = smem + C::OFF_RED;
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int i = 0; i < C::NST; ++i) mbar_init(bars + i, 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
   unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tmark = clock64();
   auto mark = [&](int k) {
@@ -361,6 +441,7 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
       tg.start[tid] = src.start;
       tg.ext[tid] = src.ext;
       tg.nc[tid] = src.nc;
+      tg.vc[tid] = src.vcond;
       for (int k = 0; k < 16; ++k) {
         tg.cs[tid][k] = src.cs[k];
         tg.cz[tid][k] = src.cz[k];
@@ -386,6 +467,8 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
         kp |= np ? (1 << m) : 0;
       }
       tg.kp = kp;
+      tg.diag = LT == 3 && a.vhat[0] != nullptr && !(a.dbg & 1024) &&
+                tg.vc[0] * tg.vc[1] * tg.vc[2] <= kDiagCond;
     }
     __syncthreads();
     const int e0 = tg.ext[0], e1 = tg.ext[1], e2 = tg.ext[2];
@@ -397,16 +480,26 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
       const double* src = ok ? a.X + tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2] : a.X;
       cp_async8(xr + l, src, ok ? 8 : 0);
     }
+    if (tg.diag) {  // eigenvector bases (V^-1, V, lambda) of the three modes
+      double* vh = dh;  // aliases the That / eigenbasis-row regions
 #pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      const int em = tg.ext[m], st = tg.start[m], nm = a.dims[m];
-      (void)nm;
-      const double* dsrc = a.dhat[m] + static_cast<int64_t>(tg.tco[m]) * C::DHS;
-      for (int e = 2 * tid; e < C::DHS; e += 2 * L3_THREADS) cp_async16(dh + m * C::DHS + e, dsrc + e, 16);
-      for (int e = tid; e < E * kPStride; e += L3_THREADS) {
-        const bool ok = e < em * kPStride;
-        cp_async8(pd + m * E * kPStride + e,
-                  ok ? a.pdat[m] + static_cast<int64_t>(st) * kPStride + e : a.pdat[m], ok ? 8 : 0);
+      for (int m = 0; m < 3; ++m) {
+        const double* vsrc = a.vhat[m] + static_cast<int64_t>(tg.tco[m]) * kVhStride;
+        for (int e = 2 * tid; e < kVhStride; e += 2 * L3_THREADS)
+          cp_async16(vh + m * kVhStride + e, vsrc + e, 16);
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int em = tg.ext[m], st = tg.start[m];
+        const double* dsrc = a.dhat[m] + static_cast<int64_t>(tg.tco[m]) * C::DHS;
+        for (int e = 2 * tid; e < C::DHS; e += 2 * L3_THREADS)
+          cp_async16(dh + m * C::DHS + e, dsrc + e, 16);
+        for (int e = tid; e < E * kPStride; e += L3_THREADS) {
+          const bool ok = e < em * kPStride;
+          cp_async8(pd + m * E * kPStride + e,
+                    ok ? a.pdat[m] + static_cast<int64_t>(st) * kPStride + e : a.pdat[m], ok ? 8 : 0);
+        }
       }
     }
     cp_async_commit();
@@ -421,7 +514,21 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     // Parts by distance along each mode, farthest first across modes:
     // part 0 = tiles >= t+3 (released >= 3 hyperplanes ago), part 1 = t+2,
     // part 2 = t+1 (nearest: the only part normally on the critical path).
-    for (int part = 0; part < 3; ++part) {
+    if constexpr (C::KSPLIT) {
+      for (int l = tid; l < (C::WARPS - 1) * L3_T; l += L3_THREADS) red[l] = 0.0;
+      int klo[3], khi[3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int tm = tg.tco[m];
+        const bool has = tm + 3 < a.ntiles_mode[m] && !(a.dbg & 4);
+        klo[m] = has ? a.bnd[m][tm + 3] : 0;
+        khi[m] = has ? a.dims[m] : 0;
+        if (has && tid == 0) wait_flag(a, tg.lt + 3 * mul[m]);
+      }
+      __syncthreads();
+      l3_far_ksplit<LT>(a, tg, xr, red, klo, khi);
+    }
+    for (int part = C::KSPLIT ? 1 : 0; part < 3; ++part) {
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
         const int tm = tg.tco[m], pmt = a.ntiles_mode[m];
@@ -431,13 +538,6 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
         const int k_lo = bm[tm + dist];
         const int k_hi = part == 0 ? a.dims[m] : bm[tm + dist + 1];
         const int64_t wtile = tg.lt + dist * mul[m];
-        if (part == 0 && a.use_tma && !((a.dbg >> (3 + m)) & 1)) {
-          __syncthreads();  // previous pass's xr writes
-          if (m == 0) l3_update_tma<LT, 0>(a, tg, xr, k_lo, k_hi, wtile, &tm0, stg, bars, phases);
-          else if (m == 1) l3_update_tma<LT, 1>(a, tg, xr, k_lo, k_hi, wtile, &tm1, stg, bars, phases);
-          else l3_update_tma<LT, 2>(a, tg, xr, k_lo, k_hi, wtile, &tm2, stg, bars, phases);
-          continue;
-        }
         if (tid == 0) wait_flag(a, wtile);
         __syncthreads();
         if (m == 0) l3_update<LT, 0>(a, tg, xr, k_lo, k_hi);
@@ -449,9 +549,44 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
 
     mark(2);
     // That_m and lambda_m arrived with the staged copies (host tables).
-    for (int l = tid; l < L3_T; l += L3_THREADS) xi[l] = 0.0;
+    for (int l = tid; l < L3_T; l += L3_THREADS) {
+      xi[l] = 0.0;
+      if constexpr (C::KSPLIT) {
+        double r = 0.0;
+#pragma unroll
+        for (int w = 0; w < C::WARPS - 1; ++w) r += red[w * L3_T + l];
+        xr[l] -= r;
+      }
+    }
     __syncthreads();
 
+    if constexpr (LT == 3) {
+      if (tg.diag) {
+        const double* vh = dh;
+        double* yr = red;
+        double* yi = red + L3_T;
+        const int* ex = tg.ext;
+        constexpr int VS = kVhStride, RE = 0, IM = 64, VR = 128, VI = 192;
+        bool sing = false;
+        l3d_mode<0, false, true, false>(xr, nullptr, yr, yi, vh + RE, vh + IM, vh, ex, a.tiny);
+        __syncthreads();
+        l3d_mode<1, true, true, false>(yr, yi, xr, xi, vh + VS + RE, vh + VS + IM, vh, ex, a.tiny);
+        __syncthreads();
+        sing |= l3d_mode<2, true, true, true>(xr, xi, yr, yi, vh + 2 * VS + RE, vh + 2 * VS + IM, vh, ex,
+                                              a.tiny);
+        __syncthreads();
+        l3d_mode<2, true, true, false>(yr, yi, xr, xi, vh + 2 * VS + VR, vh + 2 * VS + VI, vh, ex, a.tiny);
+        __syncthreads();
+        l3d_mode<1, true, true, false>(xr, xi, yr, yi, vh + VS + VR, vh + VS + VI, vh, ex, a.tiny);
+        __syncthreads();
+        l3d_mode<0, true, false, false>(yr, yi, xr, nullptr, vh + VR, vh + VI, vh, ex, a.tiny);
+        if (sing) atomicMin(a.status, static_cast<int>(tg.lt < 0x7f7f7f7e ? tg.lt : 0x7f7f7f7e));
+        __syncthreads();
+        mark(5);
+        goto scatter;
+      }
+    }
+    {
     // ---- into the eigenbasis (pair modes) -------------------------------------
     const int kp = tg.kp;
 #pragma unroll
@@ -650,6 +785,8 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     }
 
     mark(5);
+    }
+  scatter:
     // ---- scatter X_t, release --------------------------------------------------
     for (int l = tid; l < L3_T; l += L3_THREADS) {
       const int i0 = l & MSK, i1 = (l >> LT) & MSK, i2 = l >> (2 * LT);
@@ -677,41 +814,23 @@ template <int LT>
 cudaError_t launch_l3(const SolveArgs& a0, cudaStream_t st, SolveLaunchInfo* info) {
   using C = L3C<LT>;
   SolveArgs a = a0;
-  // TMA maps over the work tensor, one box shape per mode (E x E x KCH)
-  CUtensorMap maps[3];
-  std::memset(maps, 0, sizeof(maps));
-  {
-    const uint64_t dims[3] = {static_cast<uint64_t>(a.dims[0]), static_cast<uint64_t>(a.dims[1]),
-                              static_cast<uint64_t>(a.dims[2])};
-    // Opt-in (TSG_TMA=1): measured slower than direct L2 fragment loads for
-    // the 64-byte-wide boxes of 8^3 tiles, and unresolved on some tiny
-    // tile shapes; see DESIGN.md.
-    bool ok = (a.dims[0] % 2 == 0) && std::getenv("TSG_TMA") != nullptr;
-    for (int m = 0; m < 3 && ok; ++m) {
-      uint32_t box[3] = {C::E, C::E, C::E};
-      box[m] = C::KCH;
-      ok = encode_tmap_f64(&maps[m], a.X, 3, dims, box);
-    }
-    a.use_tma = ok ? 1 : 0;
-  }
-  // the TMA ring is the last smem region: leave it out when unused
-  const int bytes = a.use_tma ? C::BYTES : C::OFF_STG * 8;
-  static int nsm = 0, occ[2] = {0, 0};
+  const int bytes = C::BYTES;
+  static int nsm = 0, occ = 0;
   auto k = solve_lap3_kernel<LT>;
-  if (occ[a.use_tma] == 0) {
+  if (occ == 0) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[a.use_tma], k, C::THREADS, bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, C::THREADS, bytes);
     if (e != cudaSuccess) return e;
-    if (occ[a.use_tma] < 1) occ[a.use_tma] = 1;
+    if (occ < 1) occ = 1;
   }
-  int64_t grid = static_cast<int64_t>(nsm) * occ[a.use_tma];
+  int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > a.ntiles) grid = a.ntiles;
-  if (info) *info = SolveLaunchInfo{static_cast<int>(grid), C::THREADS, bytes, occ[a.use_tma]};
-  k<<<static_cast<unsigned>(grid), C::THREADS, bytes, st>>>(a, maps[0], maps[1], maps[2]);
+  if (info) *info = SolveLaunchInfo{static_cast<int>(grid), C::THREADS, bytes, occ};
+  k<<<static_cast<unsigned>(grid), C::THREADS, bytes, st>>>(a);
   return cudaGetLastError();
 }
 
