@@ -1054,7 +1054,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     const double nt = h[8] ? static_cast<double>(h[8]) : 1.0;
-    std::fprintf(stderr, "[tsg prof] tiles=%.0f cycles/tile: setup %.0f stage %.0f update %.0f That+fwdT %.0f wave %.0f backT %.0f scatter %.0f | idle/queue %.0f\n",
+    std::fprintf(stderr, "[tsg prof] tiles=%.0f cycles/tile: setup %.0f stage %.0f update(near) %.0f farwait|That+fwdT %.0f far|wave %.0f diag|backT %.0f scatter %.0f | idle/queue %.0f\n",
                  nt, h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt, h[6] / nt, h[7] / nt);
   }
   if (std::getenv("TSG_VERBOSE"))

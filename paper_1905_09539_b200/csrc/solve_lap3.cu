@@ -56,11 +56,12 @@ struct L3C {
   static constexpr int OFF_PD = OFF_DH + 3 * DHS;        // eigenbasis rows: 3 x E x kPStride
   static constexpr int OFF_LAM = OFF_PD + 3 * E * kPStride;
   static_assert(LT != 3 || 3 * kVhStride <= OFF_LAM - OFF_DH, "vh aliases dh + pd");
-  // K-split far updates (LT = 3): warps 1..WARPS-1 accumulate their partial
-  // tile products in private buffers, warp 0 directly into xr
+  // K-split updates (LT = 3): every warp accumulates its partial tile
+  // products in a private buffer (reused as the complex work tile of the
+  // diagonalised solve)
   static constexpr bool KSPLIT = LT == 3;
   static constexpr int OFF_RED = OFF_LAM;
-  static constexpr int DOUBLES = OFF_RED + (KSPLIT ? (WARPS - 1) * T : 0);
+  static constexpr int DOUBLES = OFF_RED + (KSPLIT ? WARPS * T : 0);
   static constexpr int BYTES = DOUBLES * 8;
 };
 
@@ -216,6 +217,7 @@ TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile) {
   const int* f = a.flags + tile;
   unsigned ns = 32;
   const unsigned cap = (a.dbg & 64) ? 32 : 256;
+  if (a.dbg & 512) return;  // timing ablation only: results are wrong
   while (ld_acquire(f) < a.epoch) {
     __nanosleep(ns);
     if (ns < cap) ns <<= 1;
@@ -302,8 +304,8 @@ TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, int k_lo, int k
 }
 
 template <int LT>
-TSG_DEVINL void l3_far_ksplit(const SolveArgs& a, const L3Geom& tg, double* xr, double* red,
-                              const int* klo, const int* khi) {
+TSG_DEVINL void l3_far_ksplit(const SolveArgs& a, const L3Geom& tg, double* red, const int* klo,
+                              const int* khi) {
   using C = L3C<LT>;
   const int warp = threadIdx.x >> 5;
   int s[3], S = 0;
@@ -314,8 +316,8 @@ TSG_DEVINL void l3_far_ksplit(const SolveArgs& a, const L3Geom& tg, double* xr, 
   }
   if (S == 0) return;
   const int w0 = (S * warp) / C::WARPS, w1 = (S * (warp + 1)) / C::WARPS;
-  double* dst = warp == 0 ? xr : red + (warp - 1) * C::T;
-  const bool sub = warp == 0;
+  double* dst = red + warp * C::T;
+  const bool sub = false;
   int off = 0;
 #pragma unroll
   for (int m = 0; m < 3; ++m) {
@@ -504,18 +506,20 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     }
     cp_async_commit();
 
-    // ---- left-looking updates, far tiles of every mode (DMMA from L2) ---------
-    // (these only read global memory and registers; the xr RMW happens after
-    //  the staged tile has landed)
+    // ---- left-looking updates ---------------------------------------------------
     int64_t mul[3] = {1, a.ntiles_mode[0], static_cast<int64_t>(a.ntiles_mode[0]) * a.ntiles_mode[1]};
-    cp_async_wait_all();
-    __syncthreads();
-    mark(1);
-    // Parts by distance along each mode, farthest first across modes:
-    // part 0 = tiles >= t+3 (released >= 3 hyperplanes ago), part 1 = t+2,
-    // part 2 = t+1 (nearest: the only part normally on the critical path).
     if constexpr (C::KSPLIT) {
-      for (int l = tid; l < (C::WARPS - 1) * L3_T; l += L3_THREADS) red[l] = 0.0;
+      // Two K-split passes over all three modes, each one batch of DMMA
+      // fragment loads per warp and slice (see l3_far_ksplit); the staged
+      // copies land meanwhile (the passes only read global memory and fold
+      // into the per-warp buffers):
+      //   far  = rows of tiles >= t+3 (released >= 3 hyperplanes ago),
+      //   near = rows of tiles t+1, t+2 (after the t+1 flags).
+      {
+        double* mine = red + (tid >> 5) * L3_T;
+        for (int l = tid & 31; l < L3_T; l += 32) mine[l] = 0.0;
+        __syncwarp();
+      }
       int klo[3], khi[3];
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
@@ -526,39 +530,59 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
         if (has && tid == 0) wait_flag(a, tg.lt + 3 * mul[m]);
       }
       __syncthreads();
-      l3_far_ksplit<LT>(a, tg, xr, red, klo, khi);
-    }
-    for (int part = C::KSPLIT ? 1 : 0; part < 3; ++part) {
+      mark(3);
+      l3_far_ksplit<LT>(a, tg, red, klo, khi);
+      mark(4);
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
-        const int tm = tg.tco[m], pmt = a.ntiles_mode[m];
-        const int* bm = a.bnd[m];
-        const int dist = part == 0 ? 3 : (part == 1 ? 2 : 1);
-        if (tm + dist >= pmt || (a.dbg & 4)) continue;  // uniform
-        const int k_lo = bm[tm + dist];
-        const int k_hi = part == 0 ? a.dims[m] : bm[tm + dist + 1];
-        const int64_t wtile = tg.lt + dist * mul[m];
-        if (tid == 0) wait_flag(a, wtile);
-        __syncthreads();
-        if (m == 0) l3_update<LT, 0>(a, tg, xr, k_lo, k_hi);
-        else if (m == 1) l3_update<LT, 1>(a, tg, xr, k_lo, k_hi);
-        else l3_update<LT, 2>(a, tg, xr, k_lo, k_hi);
+        const int tm = tg.tco[m];
+        const bool has = tm + 1 < a.ntiles_mode[m] && !(a.dbg & 4);
+        klo[m] = has ? a.bnd[m][tm + 1] : 0;
+        khi[m] = has ? (tm + 3 < a.ntiles_mode[m] ? a.bnd[m][tm + 3] : a.dims[m]) : 0;
+        if (has && tid == 0) wait_flag(a, tg.lt + mul[m]);
       }
-    }
-    __syncthreads();
-
-    mark(2);
-    // That_m and lambda_m arrived with the staged copies (host tables).
-    for (int l = tid; l < L3_T; l += L3_THREADS) {
-      xi[l] = 0.0;
-      if constexpr (C::KSPLIT) {
+      __syncthreads();
+      mark(2);
+      l3_far_ksplit<LT>(a, tg, red, klo, khi);
+      cp_async_wait_all();
+      __syncthreads();
+      mark(1);
+      for (int l = tid; l < L3_T; l += L3_THREADS) {
         double r = 0.0;
 #pragma unroll
-        for (int w = 0; w < C::WARPS - 1; ++w) r += red[w * L3_T + l];
+        for (int w = 0; w < C::WARPS; ++w) r += red[w * L3_T + l];
         xr[l] -= r;
+        if (!tg.diag) xi[l] = 0.0;
       }
+      __syncthreads();
+    } else {
+      cp_async_wait_all();
+      __syncthreads();
+      mark(1);
+      // parts by distance along each mode, farthest first across modes:
+      // part 0 = tiles >= t+3, part 1 = t+2, part 2 = t+1
+      for (int part = 0; part < 3; ++part) {
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          const int tm = tg.tco[m], pmt = a.ntiles_mode[m];
+          const int* bm = a.bnd[m];
+          const int dist = part == 0 ? 3 : (part == 1 ? 2 : 1);
+          if (tm + dist >= pmt || (a.dbg & 4)) continue;  // uniform
+          const int k_lo = bm[tm + dist];
+          const int k_hi = part == 0 ? a.dims[m] : bm[tm + dist + 1];
+          const int64_t wtile = tg.lt + dist * mul[m];
+          if (tid == 0) wait_flag(a, wtile);
+          __syncthreads();
+          if (m == 0) l3_update<LT, 0>(a, tg, xr, k_lo, k_hi);
+          else if (m == 1) l3_update<LT, 1>(a, tg, xr, k_lo, k_hi);
+          else l3_update<LT, 2>(a, tg, xr, k_lo, k_hi);
+        }
+      }
+      __syncthreads();
+      mark(2);
+      for (int l = tid; l < L3_T; l += L3_THREADS) xi[l] = 0.0;
+      __syncthreads();
     }
-    __syncthreads();
 
     if constexpr (LT == 3) {
       if (tg.diag) {
