@@ -133,6 +133,47 @@ int tsg_residual(tsg_ctx* ctx, int family, int d, const int* dims,
                  const double* X, int inputs_on_device, double* out);
 
 /* ABI version (bumped on any signature change). */
+
+/* ---- Slab-sharded multi-GPU solve (Laplace-like, d = 3) ---------------------
+ * Replaces nothing in the reference (a CPU library); implements the
+ * multi-GPU plan of SURVEY.md §8(e) behind the same algorithm as
+ * tsg_laplace_solve.  The tensor is cut into `nranks` slabs along its LAST
+ * mode (tile-aligned, never inside a 2x2 Schur block; a slab is a contiguous
+ * piece of the column-major tensor).  One process per GPU owns one slab:
+ *   forward_local   B_r x_m U_m^T, m < d-1          -> send buffer (padded)
+ *   (caller)        all-gather of the send buffers   -> gather buffer (NCCL)
+ *   forward_split   gather x_{d-1} U_{d-1}^T[R_r,:]  -> own slab of B~
+ *   solve           one dataflow kernel per GPU over all slabs: tiles and
+ *                   flags of the other ranks are read through CUDA IPC peer
+ *                   mappings over NVLink (system-scope acquire/release)
+ *   back_local / (caller) all-gather / back_split    -> X_r
+ * Emulated mode (emulate = 1): one process holds all slabs on one GPU, the
+ * gather buffer doubles as the send buffers and `solve` runs one kernel over
+ * every slab (validates the sharded path on a single device); B and X are
+ * then the whole tensor.  Every step is enqueued on `stream` (cudaStream_t,
+ * NULL = context stream) without host synchronisation. */
+typedef struct tsg_dplan tsg_dplan;
+#define TSG_IPC_BYTES 128
+/* Slab row bounds (nranks + 1 entries) of a mode of extent n with
+ * quasi-triangular factor T, for base tiles of extent `tile`. */
+int tsg_slab_bounds(int n, const double* T, int tile, int nranks, int* bounds);
+int tsg_dplan_create(tsg_ctx* ctx, int rank, int nranks, int emulate, int d, const int* dims,
+                     const double* const* T, const double* const* U, const tsg_opts* opts,
+                     tsg_dplan** out);
+void tsg_dplan_destroy(tsg_dplan* dp);
+/* slab bounds (nranks + 1), elements of this rank's slab, of one send slot */
+int tsg_dplan_info(const tsg_dplan* dp, int* bounds, int64_t* slab_elems, int64_t* send_elems);
+int tsg_dplan_buffers(tsg_dplan* dp, double** send, double** gather);
+int tsg_dplan_ipc_export(tsg_dplan* dp, void* handles);
+int tsg_dplan_ipc_import(tsg_dplan* dp, const void* all_handles);
+int tsg_dplan_forward_local(tsg_dplan* dp, const double* B, void* stream);
+int tsg_dplan_forward_split(tsg_dplan* dp, void* stream);
+int tsg_dplan_solve(tsg_dplan* dp, void* stream);
+int tsg_dplan_back_local(tsg_dplan* dp, void* stream);
+int tsg_dplan_back_split(tsg_dplan* dp, double* X, void* stream);
+/* Synchronises the stream; TSG_ESINGULAR when a zero pivot was seen. */
+int tsg_dplan_status(tsg_dplan* dp, void* stream);
+
 int tsg_abi_version(void);
 
 #ifdef __cplusplus

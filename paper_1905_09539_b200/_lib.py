@@ -39,6 +39,10 @@ TSG_SYMBOLS = [
     "tsg_laplace_reduced", "tsg_gsylv_solve", "tsg_gsylv_reduced", "tsg_plan_create",
     "tsg_plan_execute", "tsg_plan_destroy", "tsg_plan_info", "tsg_mode_multiply",
     "tsg_residual", "tsg_abi_version",
+    "tsg_slab_bounds", "tsg_dplan_create", "tsg_dplan_destroy", "tsg_dplan_info",
+    "tsg_dplan_buffers", "tsg_dplan_ipc_export", "tsg_dplan_ipc_import",
+    "tsg_dplan_forward_local", "tsg_dplan_forward_split", "tsg_dplan_solve",
+    "tsg_dplan_back_local", "tsg_dplan_back_split", "tsg_dplan_status",
 ]
 
 
@@ -59,6 +63,20 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tsg_plan_destroy": (None, [P]),
         "tsg_plan_info": (I, [P, ctypes.POINTER(ctypes.c_int64), c_int_p, c_dbl_p]),
         "tsg_residual": (I, [P, I, I, c_int_p, c_dbl_pp, P, P, P, I, c_dbl_p]),
+        "tsg_slab_bounds": (I, [I, c_dbl_p, I, I, c_int_p]),
+        "tsg_dplan_create": (I, [P, I, I, I, I, c_int_p, c_dbl_pp, c_dbl_pp, ctypes.POINTER(TsgOpts),
+                                 ctypes.POINTER(P)]),
+        "tsg_dplan_destroy": (None, [P]),
+        "tsg_dplan_info": (I, [P, c_int_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+        "tsg_dplan_buffers": (I, [P, ctypes.POINTER(P), ctypes.POINTER(P)]),
+        "tsg_dplan_ipc_export": (I, [P, P]),
+        "tsg_dplan_ipc_import": (I, [P, P]),
+        "tsg_dplan_forward_local": (I, [P, P, P]),
+        "tsg_dplan_forward_split": (I, [P, P]),
+        "tsg_dplan_solve": (I, [P, P]),
+        "tsg_dplan_back_local": (I, [P, P]),
+        "tsg_dplan_back_split": (I, [P, P, P]),
+        "tsg_dplan_status": (I, [P, P]),
         "tsylv_solve_laplace": (I, [I, c_int_p, c_dbl_pp, c_dbl_p, I, I, I, c_dbl_p, c_dbl_p, E, I]),
         "tsylv_solve_gsylv": (I, [I, c_int_p, c_dbl_pp, c_dbl_p, c_dbl_p, I, I, I, c_dbl_p,
                                   c_dbl_p, E, I]),

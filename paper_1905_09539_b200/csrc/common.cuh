@@ -52,6 +52,21 @@ TSG_DEVINL int ld_acquire(const int* p) {
 TSG_DEVINL void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+// System scope (tiles and flags shared with peer GPUs over NVLink).
+TSG_DEVINL int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+TSG_DEVINL void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// Uncached (volatile) load for peer-written tiles.
+TSG_DEVINL double ld_volatile(const double* p) {
+  double v;
+  asm volatile("ld.volatile.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  return v;
+}
 TSG_DEVINL double ld_cg(const double* p) {
   double v;
   asm volatile("ld.global.cg.f64 %0, [%1];\n" : "=d"(v) : "l"(p));

@@ -31,91 +31,37 @@
 #include "solve.h"
 #include "util.h"
 
-struct tsg_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  std::string err;
-  cudaEvent_t ev[8] = {};
-};
+#include "plan_impl.h"
 
-struct DevBuf {
-  double* p = nullptr;
-  size_t n = 0;
-  void reset() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-  cudaError_t ensure(size_t count) {
-    if (count <= n) return cudaSuccess;
-    reset();
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double));
-    if (e == cudaSuccess) n = count;
-    return e;
-  }
-  ~DevBuf() { reset(); }
-};
-
-struct tsg_plan {
-  tsg_ctx* ctx = nullptr;
-  int family = 0, d = 0, reduced_only = 0;
-  std::vector<int> dims;
-  std::vector<int64_t> stride;
-  int64_t N = 0;
-  // device factors
-  std::vector<DevBuf> T, Fwd, FwdT, Bwd, BwdT, eig, pdat, dhat, vhat;  // per mode
-  DevBuf Tc;
-  std::vector<tsg::TileMode*> tmode;
-  std::vector<int*> bnd;
-  int* order = nullptr;
-  unsigned long long* ocoord = nullptr;
-  int fast = 0;  // 1: solve_lap_kernel, 3: solve_lap3_kernel (Laplace, good eigenbases)
-  int lt3 = 3;   // log2 tile extent of solve_lap3
-  int* flags = nullptr;
-  int* counter = nullptr;   // [0] = queue head, [1] = status
-  int64_t ntiles = 0;
-  std::vector<int> ntiles_mode, tile_ext;
-  // work buffers
-  DevBuf xdev, w1, w2;
-  std::vector<DevBuf> wchain;  // gsylv W_m, m = 1..d-1
-  double flops_alg = 0, flops_exec = 0;
-  double tiny = 0;
-  double max_cond = 0;  // worst 2x2 eigenbasis condition (Frobenius)
-  int refine = 0;
-  tsg::SolveLaunchInfo solve_info{};
-  // graph cache
-  cudaGraphExec_t gexec = nullptr;
-  const double* g_in = nullptr;
-  double* g_out = nullptr;
-  int launches = 0;
-  ~tsg_plan() {
-    for (auto* b : tmode)
-      if (b) cudaFree(b);
-    for (auto* b : bnd)
-      if (b) cudaFree(b);
-    if (order) cudaFree(order);
-    if (ocoord) cudaFree(ocoord);
-    if (flags) cudaFree(flags);
-    if (counter) cudaFree(counter);
-    if (gexec) cudaGraphExecDestroy(gexec);
-  }
-};
-
-namespace {
-
-constexpr int kNoStatus = 0x7f7f7f7f;  // memset(0x7f) pattern: no singular cell
+namespace tsg_impl {
 
 int fail(tsg_ctx* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
   return code;
 }
 
-#define TSG_CU(call)                                                                 \
-  do {                                                                               \
-    cudaError_t _e = (call);                                                         \
-    if (_e != cudaSuccess)                                                           \
-      return fail(ctx, TSG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
-  } while (0)
+cudaError_t upload_mat(DevBuf& b, const double* h, size_t n) {
+  cudaError_t e = b.ensure(n);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(b.p, h, n * sizeof(double), cudaMemcpyHostToDevice);
+}
+
+std::vector<double> transpose(const double* a, int n) {
+  std::vector<double> t(static_cast<size_t>(n) * n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) t[j + static_cast<size_t>(i) * n] = a[i + static_cast<size_t>(j) * n];
+  return t;
+}
+
+}  // namespace tsg_impl
+
+namespace {
+
+constexpr int kNoStatus = 0x7f7f7f7f;  // memset(0x7f) pattern: no singular cell
+
+using tsg_impl::fail;
+using tsg_impl::transpose;
+using tsg_impl::upload_mat;
 
 double at(const double* a, int n, int i, int j) { return a[i + static_cast<size_t>(j) * n]; }
 
@@ -256,17 +202,6 @@ cudaError_t upload(T** dst, const std::vector<T>& v) {
   cudaError_t e = cudaMalloc(dst, std::max<size_t>(v.size(), 1) * sizeof(T));
   if (e != cudaSuccess) return e;
   return cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
-}
-cudaError_t upload_mat(DevBuf& b, const double* h, size_t n) {
-  cudaError_t e = b.ensure(n);
-  if (e != cudaSuccess) return e;
-  return cudaMemcpy(b.p, h, n * sizeof(double), cudaMemcpyHostToDevice);
-}
-std::vector<double> transpose(const double* a, int n) {
-  std::vector<double> t(static_cast<size_t>(n) * n);
-  for (int j = 0; j < n; ++j)
-    for (int i = 0; i < n; ++i) t[j + static_cast<size_t>(i) * n] = a[i + static_cast<size_t>(j) * n];
-  return t;
 }
 
 // Per-mode tile extents under the kernel caps, honouring n_min / opts.tile.
@@ -418,6 +353,12 @@ void tile_eigvecs(std::vector<tsg::TileMode>& tms, const std::vector<double>& dh
 int capture_or_run(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool graph);
 
 }  // namespace
+
+namespace tsg_impl {
+std::vector<int> tile_bounds_of(const double* T, int n, int b) {
+  return tile_bounds(n, b, block_codes(T, n));
+}
+}  // namespace tsg_impl
 
 extern "C" {
 
@@ -638,6 +579,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     }
     TSG_CU(upload(&pl->tmode[m], tms));
   }
+  pl->bds_h = bds;
   if (pl->ntiles > INT_MAX / 2) return fail(ctx, TSG_EDIM, "too many tiles");
   for (int m = 0; m < d; ++m)
     if (pl->ntiles_mode[m] > 1024) return fail(ctx, TSG_EDIM, "more than 1024 tiles along a mode");
@@ -656,6 +598,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     }
     std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return hp[x] > hp[y]; });
     TSG_CU(upload(&pl->order, ord));
+    pl->order_h = ord;
     std::vector<unsigned long long> oc(pl->ntiles);
     for (int64_t q = 0; q < pl->ntiles; ++q) {
       int64_t r = ord[q];
@@ -935,6 +878,48 @@ int tsg_gsylv_reduced(tsg_ctx* ctx, int d, const int* dims, const double* S, con
 
 }  // extern "C"
 
+namespace tsg_impl {
+
+void fill_solve_args(const tsg_plan* pl, double* work, tsg::SolveArgs& a) {
+  const int d = pl->d;
+  a.family = pl->family;
+  a.d = d;
+  for (int m = 0; m < d; ++m) {
+    a.dims[m] = pl->dims[m];
+    a.stride[m] = pl->stride[m];
+    a.T[m] = pl->T[m].p;
+    a.tmode[m] = pl->tmode[m];
+    a.eig[m] = pl->eig[m].p;
+    a.pdat[m] = pl->pdat[m].p;
+    a.dhat[m] = pl->dhat[m].p;
+    a.vhat[m] = pl->vhat[m].p;
+    a.ntiles_mode[m] = pl->ntiles_mode[m];
+    a.bnd[m] = pl->bnd[m];
+    if (pl->family == 1 && m >= 1) a.W[m] = pl->wchain[m].p;
+  }
+  a.Tc = pl->family == 1 ? pl->Tc.p : nullptr;
+  a.X = work;
+  a.ntiles = pl->ntiles;
+  a.order = pl->order;
+  a.ocoord = pl->ocoord;
+  a.tiny = pl->tiny;
+  a.refine = pl->refine;
+  // one slab: the whole tensor
+  a.nslab = 1;
+  a.sys = 0;
+  a.slo[0] = 0;
+  a.slo[1] = pl->dims[d - 1];
+  a.xs[0] = work;
+}
+
+cudaError_t launch_plan_solve(tsg_plan* pl, const tsg::SolveArgs& a, cudaStream_t st) {
+  if (pl->fast == 3) return tsg::launch_solve_lap3(pl->lt3, a, st, &pl->solve_info);
+  if (pl->fast) return tsg::launch_solve_lap(a, st, &pl->solve_info);
+  return tsg::launch_solve(a, st, &pl->solve_info);
+}
+
+}  // namespace tsg_impl
+
 namespace {
 
 // Enqueue the whole pipeline on `st` (fwd transforms, solve, back transforms).
@@ -966,27 +951,9 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   TSG_CU(cudaMemsetAsync(pl->counter, 0, sizeof(int), st));
   TSG_CU(cudaMemsetAsync(pl->counter + 1, 0x7f, sizeof(int), st));  // kNoStatus
   tsg::SolveArgs a{};
-  a.family = pl->family;
-  a.d = d;
-  for (int m = 0; m < d; ++m) {
-    a.dims[m] = pl->dims[m];
-    a.stride[m] = pl->stride[m];
-    a.T[m] = pl->T[m].p;
-    a.tmode[m] = pl->tmode[m];
-    a.eig[m] = pl->eig[m].p;
-    a.pdat[m] = pl->pdat[m].p;
-    a.dhat[m] = pl->dhat[m].p;
-    a.vhat[m] = pl->vhat[m].p;
-    a.ntiles_mode[m] = pl->ntiles_mode[m];
-    a.bnd[m] = pl->bnd[m];
-    if (pl->family == 1 && m >= 1) a.W[m] = pl->wchain[m].p;
-  }
-  a.Tc = pl->family == 1 ? pl->Tc.p : nullptr;
-  a.X = work;
-  a.ntiles = pl->ntiles;
-  a.order = pl->order;
-  a.ocoord = pl->ocoord;
+  tsg_impl::fill_solve_args(pl, work, a);
   a.flags = pl->flags;
+  a.fs[0] = pl->flags;
   a.counter = pl->counter;
   a.status = pl->counter + 1;
   a.epoch = 1;
@@ -1011,12 +978,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
     a.prof = prof;
   }
-  if (pl->fast == 3)
-    TSG_CU(tsg::launch_solve_lap3(pl->lt3, a, st, &pl->solve_info));
-  else if (pl->fast)
-    TSG_CU(tsg::launch_solve_lap(a, st, &pl->solve_info));
-  else
-    TSG_CU(tsg::launch_solve(a, st, &pl->solve_info));
+  TSG_CU(tsg_impl::launch_plan_solve(pl, a, st));
   ++pl->launches;
   if (want_trace) {
     // per hyperplane: count, first and last release (us from the first release)

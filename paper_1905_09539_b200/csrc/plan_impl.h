@@ -1,0 +1,106 @@
+// Internal declarations shared by plan.cpp (single-GPU plans) and dist.cpp
+// (slab-sharded multi-GPU plans).  Not part of the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tsylv_gpu.h"
+#include "solve.h"
+
+struct tsg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  cudaEvent_t ev[8] = {};
+};
+
+struct DevBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  cudaError_t ensure(size_t count) {
+    if (count <= n) return cudaSuccess;
+    reset();
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  ~DevBuf() { reset(); }
+};
+
+struct tsg_plan {
+  tsg_ctx* ctx = nullptr;
+  int family = 0, d = 0, reduced_only = 0;
+  std::vector<int> dims;
+  std::vector<int64_t> stride;
+  int64_t N = 0;
+  // device factors
+  std::vector<DevBuf> T, Fwd, FwdT, Bwd, BwdT, eig, pdat, dhat, vhat;  // per mode
+  DevBuf Tc;
+  std::vector<tsg::TileMode*> tmode;
+  std::vector<int*> bnd;
+  int* order = nullptr;
+  unsigned long long* ocoord = nullptr;
+  int fast = 0;  // 1: solve_lap_kernel, 3: solve_lap3_kernel (Laplace, good eigenbases)
+  int lt3 = 3;   // log2 tile extent of solve_lap3
+  int* flags = nullptr;
+  int* counter = nullptr;   // [0] = queue head, [1] = status
+  int64_t ntiles = 0;
+  std::vector<std::vector<int>> bds_h;  // host tile boundaries per mode
+  std::vector<int> order_h;             // host topological order (linear tile ids)
+  std::vector<int> ntiles_mode, tile_ext;
+  // work buffers
+  DevBuf xdev, w1, w2;
+  std::vector<DevBuf> wchain;  // gsylv W_m, m = 1..d-1
+  double flops_alg = 0, flops_exec = 0;
+  double tiny = 0;
+  double max_cond = 0;  // worst 2x2 eigenbasis condition (Frobenius)
+  int refine = 0;
+  tsg::SolveLaunchInfo solve_info{};
+  // graph cache
+  cudaGraphExec_t gexec = nullptr;
+  const double* g_in = nullptr;
+  double* g_out = nullptr;
+  int launches = 0;
+  ~tsg_plan() {
+    for (auto* b : tmode)
+      if (b) cudaFree(b);
+    for (auto* b : bnd)
+      if (b) cudaFree(b);
+    if (order) cudaFree(order);
+    if (ocoord) cudaFree(ocoord);
+    if (flags) cudaFree(flags);
+    if (counter) cudaFree(counter);
+    if (gexec) cudaGraphExecDestroy(gexec);
+  }
+};
+
+
+namespace tsg_impl {
+
+int fail(tsg_ctx* ctx, int code, const std::string& msg);
+cudaError_t upload_mat(DevBuf& b, const double* h, size_t n);
+std::vector<double> transpose(const double* a, int n);
+// Solve arguments of a plan over work tensor `work` (everything except the
+// queue, flags and status fields).
+void fill_solve_args(const tsg_plan* pl, double* work, tsg::SolveArgs& a);
+// Launch the plan's dataflow kernel with fully populated arguments.
+cudaError_t launch_plan_solve(tsg_plan* pl, const tsg::SolveArgs& a, cudaStream_t st);
+// Tile boundaries of a mode (2x2 Schur blocks never split).
+std::vector<int> tile_bounds_of(const double* T, int n, int b);
+
+}  // namespace tsg_impl
+
+#define TSG_CU(call)                                                                 \
+  do {                                                                               \
+    cudaError_t _e = (call);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return tsg_impl::fail(ctx, TSG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)

@@ -10,6 +10,7 @@ constexpr int kEigStride = 12;  // doubles of normal-form data per Schur-block s
 constexpr int kPStride = 20;    // doubles of eigenbasis (P, Pinv, lambda) data per block row
 
 constexpr int kMaxCells = 32;   // Schur cells per mode inside one tile
+constexpr int kMaxSlabs = 8;    // slabs (ranks) along the last mode, sharded solves
 
 // Host-built geometry of tile index t along one mode: global start, extent,
 // and its 1x1/2x2 Schur cells (start offset inside the tile, size).
@@ -63,6 +64,15 @@ struct SolveArgs {
   int dbg;                      // ablation mask (development only; 0 in production)
   unsigned long long* prof;     // optional per-phase cycle counters (development)
   unsigned long long* trace;    // optional per-tile release globaltimer (development)
+  // Slabs along the last mode (lap3 only; nslab = 1 and xs[0] = X otherwise).
+  // Element offset(i) of the global tensor lives at xs[q] + offset(i) for
+  // the slab q = slab_of(i_{d-1}); xs[q] are virtual bases (slab pointer
+  // minus slo[q] * stride[d-1]), peer-mapped on multi-GPU runs.
+  int nslab;
+  int sys;                      // 1: flags and tiles shared across GPUs (system scope)
+  int slo[kMaxSlabs + 1];       // slab row bounds along mode d-1 (tile-aligned)
+  double* xs[kMaxSlabs];
+  int* fs[kMaxSlabs];           // tile flags of the slab owner (indexed by linear tile id)
 };
 
 struct SolveLaunchInfo {

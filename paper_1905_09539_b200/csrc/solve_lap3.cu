@@ -69,7 +69,8 @@ struct L3Geom {
   int64_t lt;
   int64_t gbase;
   int start[3], ext[3], tco[3];
-  int nc[3], H, kp, diag;
+  int nc[3], H, kp, diag, own;
+  double* xb;  // (virtual) base of the slab holding the tile
   float vc[3];
   unsigned char cs[3][16], cz[3][16], cellof[3][16], cend[3][16], cplx[3][16], ckind[3][16];
   int npair[3];
@@ -213,11 +214,25 @@ TSG_DEVINL void l3_update(const SolveArgs& a, const L3Geom& tg, double* xr, int 
       }
 }
 
-TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile) {
-  const int* f = a.flags + tile;
+// slab (owner) of row `row` along the last mode
+TSG_DEVINL int slab_of(const SolveArgs& a, int row) {
+  int q = 0;
+  while (q + 1 < a.nslab && row >= a.slo[q + 1]) ++q;
+  return q;
+}
+
+TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile, int owner) {
+  if (a.dbg & 512) return;  // timing ablation only: results are wrong
+  const int* f = a.fs[owner] + tile;
   unsigned ns = 32;
   const unsigned cap = (a.dbg & 64) ? 32 : 256;
-  if (a.dbg & 512) return;  // timing ablation only: results are wrong
+  if (a.sys) {
+    while (ld_acquire_sys(f) < a.epoch) {
+      __nanosleep(ns);
+      if (ns < cap) ns <<= 1;
+    }
+    return;
+  }
   while (ld_acquire(f) < a.epoch) {
     __nanosleep(ns);
     if (ns < cap) ns <<= 1;
@@ -236,9 +251,9 @@ TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile) {
 #ifndef L3_UB
 #define L3_UB 3
 #endif
-template <int LT, int M>
-TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, int k_lo, int k_hi, double* dst,
-                           bool sub) {
+template <int LT, int M, bool VOL>
+TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, const double* xb, int k_lo, int k_hi,
+                           double* dst, bool sub) {
   constexpr int E = L3C<LT>::E, UB = L3_UB;
   static_assert(E == 8, "one 8-row DMMA block per mode");
   const int lane = threadIdx.x & 31;
@@ -253,7 +268,7 @@ TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, int k_lo, int k
                        static_cast<int64_t>(tg.start[VB]) * SJ;
   const int row = tg.start[M] + (gq < em ? gq : em - 1);
   const double* pa = a.T[M] + static_cast<int64_t>(k_lo + tq) * nm + row;
-  const double* pb = a.X + base + static_cast<int64_t>(k_lo + tq) * a.stride[M];
+  const double* pb = xb + base + static_cast<int64_t>(k_lo + tq) * a.stride[M];
   const int64_t sa = 4 * static_cast<int64_t>(nm), sb = 4 * a.stride[M];
   double c[E][2];
 #pragma unroll
@@ -267,7 +282,7 @@ TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, int k_lo, int k
       af[u] = __ldg(pa);
       pa += sa;
 #pragma unroll
-      for (int jb = 0; jb < E; ++jb) bf[u][jb] = jb < eb ? ld_cg(pb + jb * SJ) : 0.0;
+      for (int jb = 0; jb < E; ++jb) bf[u][jb] = jb < eb ? (VOL ? ld_volatile(pb + jb * SJ) : ld_cg(pb + jb * SJ)) : 0.0;
       pb += sb;
     }
 #pragma unroll
@@ -282,7 +297,8 @@ TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, int k_lo, int k
     const double av = kok ? __ldg(pa) : 0.0;
     double bv[E];
 #pragma unroll
-    for (int jb = 0; jb < E; ++jb) bv[jb] = (kok && jb < eb) ? ld_cg(pb + jb * SJ) : 0.0;
+    for (int jb = 0; jb < E; ++jb)
+      bv[jb] = (kok && jb < eb) ? (VOL ? ld_volatile(pb + jb * SJ) : ld_cg(pb + jb * SJ)) : 0.0;
     pa += sa;
     pb += sb;
 #pragma unroll
@@ -303,34 +319,53 @@ TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, int k_lo, int k
     }
 }
 
+// One K range of the updates: rows [k_lo, k_hi) of mode m, read through the
+// (virtual) base of the slab that holds them.
+struct KSeg {
+  int m, k_lo, k_hi, remote;
+  const double* xb;
+};
+
 template <int LT>
-TSG_DEVINL void l3_far_ksplit(const SolveArgs& a, const L3Geom& tg, double* red, const int* klo,
-                              const int* khi) {
+TSG_DEVINL void l3_far_ksplit(const SolveArgs& a, const L3Geom& tg, double* red, const KSeg* seg,
+                              int nseg) {
   using C = L3C<LT>;
   const int warp = threadIdx.x >> 5;
-  int s[3], S = 0;
-#pragma unroll
-  for (int m = 0; m < 3; ++m) {
-    s[m] = (khi[m] - klo[m] + 3) >> 2;
-    S += s[m];
-  }
+  int S = 0;
+  for (int i = 0; i < nseg; ++i) S += (seg[i].k_hi - seg[i].k_lo + 3) >> 2;
   if (S == 0) return;
   const int w0 = (S * warp) / C::WARPS, w1 = (S * (warp + 1)) / C::WARPS;
   double* dst = red + warp * C::T;
-  const bool sub = false;
   int off = 0;
-#pragma unroll
-  for (int m = 0; m < 3; ++m) {
-    const int lo = w0 > off ? w0 : off, hi = w1 < off + s[m] ? w1 : off + s[m];
+  for (int i = 0; i < nseg; ++i) {
+    const int si = (seg[i].k_hi - seg[i].k_lo + 3) >> 2;
+    const int lo = w0 > off ? w0 : off, hi = w1 < off + si ? w1 : off + si;
     if (lo < hi) {
-      const int kl = klo[m] + 4 * (lo - off);
-      const int kh = min(khi[m], klo[m] + 4 * (hi - off));
-      if (m == 0) l3_far_seg<LT, 0>(a, tg, kl, kh, dst, sub);
-      else if (m == 1) l3_far_seg<LT, 1>(a, tg, kl, kh, dst, sub);
-      else l3_far_seg<LT, 2>(a, tg, kl, kh, dst, sub);
+      const int kl = seg[i].k_lo + 4 * (lo - off);
+      const int kh = min(seg[i].k_hi, seg[i].k_lo + 4 * (hi - off));
+      const double* xb = seg[i].xb;
+      if (seg[i].m == 0) l3_far_seg<LT, 0, false>(a, tg, xb, kl, kh, dst, false);
+      else if (seg[i].m == 1) l3_far_seg<LT, 1, false>(a, tg, xb, kl, kh, dst, false);
+      else if (seg[i].remote) l3_far_seg<LT, 2, true>(a, tg, xb, kl, kh, dst, false);
+      else l3_far_seg<LT, 2, false>(a, tg, xb, kl, kh, dst, false);
     }
-    off += s[m];
+    off += si;
   }
+}
+
+// Update segments for rows [lo_m, hi_m) of each mode: modes 0, 1 read the
+// tile's own slab; mode 2 is cut at slab boundaries.
+TSG_DEVINL int l3_segments(const SolveArgs& a, int own, const int* lo, const int* hi, KSeg* seg) {
+  int n = 0;
+  for (int m = 0; m < 2; ++m)
+    if (hi[m] > lo[m]) seg[n++] = KSeg{m, lo[m], hi[m], 0, a.xs[own]};
+  if (hi[2] > lo[2]) {
+    for (int q = slab_of(a, lo[2]); q < a.nslab && a.slo[q] < hi[2]; ++q) {
+      const int kl = max(lo[2], a.slo[q]), kh = min(hi[2], a.slo[q + 1]);
+      if (kh > kl) seg[n++] = KSeg{2, kl, kh, (a.sys && q != own) ? 1 : 0, a.xs[q]};
+    }
+  }
+  return n;
 }
 
 // ---- diagonalised tiles ------------------------------------------------------
@@ -409,6 +444,8 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
   extern __shared__ __align__(16) double smem[];
   __shared__ L3Geom tg;
   __shared__ int s_tile;
+  __shared__ KSeg s_seg[2 + kMaxSlabs];
+  __shared__ int s_nseg;
   double* xr = smem + C::OFF_XR;
   double* xi = smem + C::OFF_XI;
   double* dh = smem + C::OFF_DH;
@@ -456,6 +493,8 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     }
     __syncthreads();
     if (tid == 0) {
+      tg.own = slab_of(a, tg.start[2]);
+      tg.xb = a.xs[tg.own];
       tg.gbase = static_cast<int64_t>(tg.start[0]) * a.stride[0] +
                  static_cast<int64_t>(tg.start[1]) * a.stride[1] +
                  static_cast<int64_t>(tg.start[2]) * a.stride[2];
@@ -479,7 +518,7 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     for (int l = tid; l < L3_T; l += L3_THREADS) {
       const int i0 = l & MSK, i1 = (l >> LT) & MSK, i2 = l >> (2 * LT);
       const bool ok = i0 < e0 && i1 < e1 && i2 < e2;
-      const double* src = ok ? a.X + tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2] : a.X;
+      const double* src = ok ? tg.xb + tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2] : a.xs[0] + a.slo[0] * a.stride[2];
       cp_async8(xr + l, src, ok ? 8 : 0);
     }
     if (tg.diag) {  // eigenvector bases (V^-1, V, lambda) of the three modes
@@ -520,30 +559,36 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
         for (int l = tid & 31; l < L3_T; l += 32) mine[l] = 0.0;
         __syncwarp();
       }
-      int klo[3], khi[3];
-#pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const int tm = tg.tco[m];
-        const bool has = tm + 3 < a.ntiles_mode[m] && !(a.dbg & 4);
-        klo[m] = has ? a.bnd[m][tm + 3] : 0;
-        khi[m] = has ? a.dims[m] : 0;
-        if (has && tid == 0) wait_flag(a, tg.lt + 3 * mul[m]);
+      if (tid == 0) {  // far: rows of tiles >= t+3
+        int lo[3], hi[3];
+        for (int m = 0; m < 3; ++m) {
+          const int tm = tg.tco[m];
+          const bool has = tm + 3 < a.ntiles_mode[m] && !(a.dbg & 4);
+          lo[m] = has ? a.bnd[m][tm + 3] : 0;
+          hi[m] = has ? a.dims[m] : 0;
+          if (has) wait_flag(a, tg.lt + 3 * mul[m], m == 2 ? slab_of(a, lo[2]) : tg.own);
+        }
+        s_nseg = l3_segments(a, tg.own, lo, hi, s_seg);
       }
       __syncthreads();
       mark(3);
-      l3_far_ksplit<LT>(a, tg, red, klo, khi);
+      l3_far_ksplit<LT>(a, tg, red, s_seg, s_nseg);
       mark(4);
-#pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const int tm = tg.tco[m];
-        const bool has = tm + 1 < a.ntiles_mode[m] && !(a.dbg & 4);
-        klo[m] = has ? a.bnd[m][tm + 1] : 0;
-        khi[m] = has ? (tm + 3 < a.ntiles_mode[m] ? a.bnd[m][tm + 3] : a.dims[m]) : 0;
-        if (has && tid == 0) wait_flag(a, tg.lt + mul[m]);
+      __syncthreads();  // s_seg reuse
+      if (tid == 0) {  // near: rows of tiles t+1, t+2
+        int lo[3], hi[3];
+        for (int m = 0; m < 3; ++m) {
+          const int tm = tg.tco[m];
+          const bool has = tm + 1 < a.ntiles_mode[m] && !(a.dbg & 4);
+          lo[m] = has ? a.bnd[m][tm + 1] : 0;
+          hi[m] = has ? (tm + 3 < a.ntiles_mode[m] ? a.bnd[m][tm + 3] : a.dims[m]) : 0;
+          if (has) wait_flag(a, tg.lt + mul[m], m == 2 ? slab_of(a, lo[2]) : tg.own);
+        }
+        s_nseg = l3_segments(a, tg.own, lo, hi, s_seg);
       }
       __syncthreads();
       mark(2);
-      l3_far_ksplit<LT>(a, tg, red, klo, khi);
+      l3_far_ksplit<LT>(a, tg, red, s_seg, s_nseg);
       cp_async_wait_all();
       __syncthreads();
       mark(1);
@@ -571,7 +616,7 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
           const int k_lo = bm[tm + dist];
           const int k_hi = part == 0 ? a.dims[m] : bm[tm + dist + 1];
           const int64_t wtile = tg.lt + dist * mul[m];
-          if (tid == 0) wait_flag(a, wtile);
+          if (tid == 0) wait_flag(a, wtile, 0);
           __syncthreads();
           if (m == 0) l3_update<LT, 0>(a, tg, xr, k_lo, k_hi);
           else if (m == 1) l3_update<LT, 1>(a, tg, xr, k_lo, k_hi);
@@ -815,12 +860,17 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     for (int l = tid; l < L3_T; l += L3_THREADS) {
       const int i0 = l & MSK, i1 = (l >> LT) & MSK, i2 = l >> (2 * LT);
       if (i0 < e0 && i1 < e1 && i2 < e2)
-        a.X[tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2]] = xr[l];
+        tg.xb[tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2]] = xr[l];
     }
     __syncthreads();
     if (tid == 0) {
-      __threadfence();
-      st_release(a.flags + tg.lt, a.epoch);
+      if (a.sys) {
+        __threadfence_system();
+        st_release_sys(a.fs[tg.own] + tg.lt, a.epoch);
+      } else {
+        __threadfence();
+        st_release(a.fs[tg.own] + tg.lt, a.epoch);
+      }
       if (a.trace) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
