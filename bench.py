@@ -17,10 +17,14 @@ back transforms X = X~ x_m U_m — on synthetic seeded inputs
   cpu_baseline : the reference solver itself (oracle/_ref, built from the
           unmodified reference headers) on the host cores, rank 0 at N=1
 
-Multi-GPU (N>1, torchrun): each rank solves its own replica of the
-configuration (weak scaling, no data-path collective yet — slab sharding is
-the next step).  `--impl reference` times the reference CPU
-solver (rank 0 only; other ranks exit 0).
+Multi-GPU (N>1, torchrun, NCCL): the order-3 Laplace configurations (C1, C2,
+C4) run ONE problem sharded into N slabs along the last mode (strong
+scaling): slab-local transforms, NCCL all-gathers for the last-mode
+transforms, and the dataflow solve over peer-mapped slabs (CUDA IPC, NVLink),
+see paper_1905_09539_b200/dist.py.  C3 (d=6) and C5 (gsylv) are not sharded
+yet and run one replica per GPU (weak scaling).  `--sharded` forces the
+sharded path at N=1 (plumbing check).  `--impl reference` times the reference
+CPU solver (rank 0 only; other ranks exit 0).
 """
 from __future__ import annotations
 
@@ -340,6 +344,133 @@ def run_ours(a, rank, world, local):
         dist.destroy_process_group()
 
 
+def run_sharded(a, rank, world, local):
+    """One problem, `world` slabs along the last mode (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1905_09539_b200 as T
+    from paper_1905_09539_b200.dist import DeviceSlabs, ShardedLaplace
+    from paper_1905_09539_b200.plan import Context
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    kind, dims, desc = CONFIGS[a.config]
+    N = int(np.prod(dims))
+    p = T.make_problem(kind, dims, seed=1)  # the same problem on every rank
+    fs = [T.schur(c) for c in p.coeffs]      # shared host setup
+    ctx = Context(local)
+    be = DeviceSlabs(ctx, rank, world, [f[1] for f in fs], [f[0] for f in fs])
+    sl = ShardedLaplace(be)
+    lo, hi = be.bounds[rank], be.bounds[rank + 1]
+    b_host = torch.from_numpy(np.ascontiguousarray(p.rhs[..., lo:hi].reshape(-1, order="F"))).pin_memory()
+    x_host = torch.empty_like(b_host).pin_memory()
+    b = b_host.to(dev)
+    x = torch.empty_like(b)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
+    sp = ctx.stream_ptr()
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        be.forward_local(b, sp)
+        sl._all_gather()
+        be.forward_split(sp)
+        if ev is not None:
+            ev[1].record(stream)
+        be.solve(sp)
+        if ev is not None:
+            ev[2].record(stream)
+        be.back_local(sp)
+        sl._all_gather()
+        be.back_split(x, sp)
+        if ev is not None:
+            ev[3].record(stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(a.warmup, 3)):
+            step()
+        be.status(sp)
+        dist.barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local)
+        clocks.start()
+        time.sleep(0.2)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.steps)]
+        for i in range(a.steps):
+            step(evs[i])
+        stream.synchronize()
+        clk = clocks.stop()
+        ms = evs[0][0].elapsed_time(evs[-1][3]) / a.steps
+        t_fwd = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
+        t_solve = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
+        t_back = statistics.median(e[2].elapsed_time(e[3]) for e in evs)
+        be.status(sp)
+        # end to end: pinned host slab in, solution slab out, every step
+        dist.barrier()
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(a.steps):
+            b.copy_(b_host, non_blocking=True)
+            step()
+            x_host.copy_(x, non_blocking=True)
+        f1.record(stream)
+        f1.synchronize()
+        ms_e2e = f0.elapsed_time(f1) / a.steps
+        t = torch.tensor([ms, ms_e2e, t_fwd, t_solve, t_back], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_e2e, t_fwd, t_solve, t_back = (float(v) for v in t)
+        # gather X to rank 0 through the padded send/gather buffers
+        be.send.zero_()
+        be.send[: x.numel()].copy_(x)
+        sl._all_gather()
+        torch.cuda.synchronize()
+    res = None
+    if rank == 0:
+        g = be.gather.cpu().numpy()
+        parts = []
+        for q in range(world):
+            rows = be.bounds[q + 1] - be.bounds[q]
+            seg = g[q * be.send_elems:q * be.send_elems + rows * int(np.prod(dims[:-1]))]
+            parts.append(seg.reshape(tuple(dims[:-1]) + (rows,), order="F"))
+        xs = np.concatenate(parts, axis=len(dims) - 1)
+        res = T.residual(p, xs)
+        tr_f, solve_f = flops_alg(kind, dims)
+        line = {
+            "metric": METRIC, "value": N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded RandomStream, BASELINE.json distributions)",
+            "config": {"workload": a.config, "desc": desc, "dims": list(dims), "unknowns": N,
+                       "l2": "inputs larger than L2 (8N bytes per tensor > 126 MB L2)",
+                       "parallelism": f"{world} slabs along mode {len(dims) - 1} "
+                                      f"(rows {be.bounds}); NCCL all-gather for the last-mode "
+                                      "transforms, peer-mapped dataflow solve",
+                       "schur_setup": "host LAPACK dgees, outside the timed region"},
+            "phases_ms": {"forward_transforms+allgather": t_fwd, "reduced_solve": t_solve,
+                          "back_transforms+allgather": t_back},
+            "fp64_tflops_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12,
+            "frac_fp64_peak_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12 / PEAK_FP64_TFLOPS / world,
+            "residual": res,
+            "roofline": {"bound": "tensor", "achieved": solve_f / (t_solve * 1e-3) / 1e12 / world,
+                         "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
+                         "frac": solve_f / (t_solve * 1e-3) / 1e12 / world / PEAK_FP64_TFLOPS,
+                         "traffic": None,
+                         "kernel": "solve_lap3_kernel (sharded dataflow solve), per GPU",
+                         "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak_probe.log"},
+            "e2e": {"value": N / (ms_e2e * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N, "ms_per_step": ms_e2e},
+            "gpu_launches": 7 * a.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    del sl, be
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -348,10 +479,18 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="sharded path even at N=1")
     a = ap.parse_args()
     rank, world, local = dist_env()
     if a.impl == "reference":
         run_reference(a, rank)
+    elif (world > 1 or a.sharded) and CONFIGS[a.config][0] != 5 and len(CONFIGS[a.config][1]) == 3:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        run_sharded(a, rank, world, local)
     else:
         run_ours(a, rank, world, local)
 

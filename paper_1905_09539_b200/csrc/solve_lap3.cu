@@ -221,12 +221,12 @@ TSG_DEVINL int slab_of(const SolveArgs& a, int row) {
   return q;
 }
 
-TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile, int owner) {
+TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile, int owner, int own) {
   if (a.dbg & 512) return;  // timing ablation only: results are wrong
   const int* f = a.fs[owner] + tile;
   unsigned ns = 32;
   const unsigned cap = (a.dbg & 64) ? 32 : 256;
-  if (a.sys) {
+  if (a.sys && owner != own) {  // released by a peer GPU
     while (ld_acquire_sys(f) < a.epoch) {
       __nanosleep(ns);
       if (ns < cap) ns <<= 1;
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
           const bool has = tm + 3 < a.ntiles_mode[m] && !(a.dbg & 4);
           lo[m] = has ? a.bnd[m][tm + 3] : 0;
           hi[m] = has ? a.dims[m] : 0;
-          if (has) wait_flag(a, tg.lt + 3 * mul[m], m == 2 ? slab_of(a, lo[2]) : tg.own);
+          if (has) wait_flag(a, tg.lt + 3 * mul[m], m == 2 ? slab_of(a, lo[2]) : tg.own, tg.own);
         }
         s_nseg = l3_segments(a, tg.own, lo, hi, s_seg);
       }
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
           const bool has = tm + 1 < a.ntiles_mode[m] && !(a.dbg & 4);
           lo[m] = has ? a.bnd[m][tm + 1] : 0;
           hi[m] = has ? (tm + 3 < a.ntiles_mode[m] ? a.bnd[m][tm + 3] : a.dims[m]) : 0;
-          if (has) wait_flag(a, tg.lt + mul[m], m == 2 ? slab_of(a, lo[2]) : tg.own);
+          if (has) wait_flag(a, tg.lt + mul[m], m == 2 ? slab_of(a, lo[2]) : tg.own, tg.own);
         }
         s_nseg = l3_segments(a, tg.own, lo, hi, s_seg);
       }
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
           const int k_lo = bm[tm + dist];
           const int k_hi = part == 0 ? a.dims[m] : bm[tm + dist + 1];
           const int64_t wtile = tg.lt + dist * mul[m];
-          if (tid == 0) wait_flag(a, wtile, 0);
+          if (tid == 0) wait_flag(a, wtile, 0, 0);
           __syncthreads();
           if (m == 0) l3_update<LT, 0>(a, tg, xr, k_lo, k_hi);
           else if (m == 1) l3_update<LT, 1>(a, tg, xr, k_lo, k_hi);
@@ -864,7 +864,7 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     }
     __syncthreads();
     if (tid == 0) {
-      if (a.sys) {
+      if (a.sys && tg.own > 0) {  // read by the lower slabs' GPUs
         __threadfence_system();
         st_release_sys(a.fs[tg.own] + tg.lt, a.epoch);
       } else {

@@ -102,9 +102,9 @@ class DeviceSlabs:
         self._check(lib().tsg_dplan_ipc_import(self.h, allh), "ipc_import")
 
     # ---- steps (enqueued on `stream`, a cudaStream_t as int) ----
-    def forward_local(self, b_ptr: int, stream: int) -> None:
-        self._check(lib().tsg_dplan_forward_local(self.h, ctypes.c_void_p(b_ptr), ctypes.c_void_p(stream)),
-                    "forward_local")
+    def forward_local(self, b, stream: int) -> None:
+        self._check(lib().tsg_dplan_forward_local(self.h, ctypes.c_void_p(b.data_ptr()),
+                                                  ctypes.c_void_p(stream)), "forward_local")
 
     def forward_split(self, stream: int) -> None:
         self._check(lib().tsg_dplan_forward_split(self.h, ctypes.c_void_p(stream)), "forward_split")
@@ -115,9 +115,9 @@ class DeviceSlabs:
     def back_local(self, stream: int) -> None:
         self._check(lib().tsg_dplan_back_local(self.h, ctypes.c_void_p(stream)), "back_local")
 
-    def back_split(self, x_ptr: int, stream: int) -> None:
-        self._check(lib().tsg_dplan_back_split(self.h, ctypes.c_void_p(x_ptr), ctypes.c_void_p(stream)),
-                    "back_split")
+    def back_split(self, x, stream: int) -> None:
+        self._check(lib().tsg_dplan_back_split(self.h, ctypes.c_void_p(x.data_ptr()),
+                                               ctypes.c_void_p(stream)), "back_split")
 
     def status(self, stream: int) -> None:
         self._check(lib().tsg_dplan_status(self.h, ctypes.c_void_p(stream)), "status")
@@ -161,10 +161,10 @@ class ShardedLaplace:
         dist.all_gather_into_tensor(self.be.gather, self.be.send, group=self.group)
 
     def solve(self, b, x, stream: int = 0, check: bool = False):
-        """b, x: this rank's slab (the whole tensor when emulated), device
-        tensors / buffers exposing data_ptr(); enqueued on `stream`."""
+        """b, x: this rank's slab (the whole tensor when emulated) as flat
+        column-major tensors on the backend's device; enqueued on `stream`."""
         be = self.be
-        be.forward_local(b.data_ptr(), stream)
+        be.forward_local(b, stream)
         if not self.emulate:
             self._all_gather()
         be.forward_split(stream)
@@ -172,7 +172,7 @@ class ShardedLaplace:
         be.back_local(stream)
         if not self.emulate:
             self._all_gather()
-        be.back_split(x.data_ptr(), stream)
+        be.back_split(x, stream)
         if check:
             be.status(stream)
         return x
