@@ -534,6 +534,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         r += sz;
       }
       tmd.nc = static_cast<unsigned char>(nc);
+      tmd.far_lo = t + 3 < pl->ntiles_mode[m] ? bds[m][t + 3] : dims[m];
     }
     if (pl->fast == 3) {
       // Eigenbasis diagonal block of every tile index along mode m:

@@ -14,7 +14,7 @@ constexpr int kMaxSlabs = 8;    // slabs (ranks) along the last mode, sharded so
 
 // Host-built geometry of tile index t along one mode: global start, extent,
 // and its 1x1/2x2 Schur cells (start offset inside the tile, size).
-struct TileMode {
+struct alignas(16) TileMode {
   int start;
   unsigned char ext, nc, pair, pad;
   unsigned char cs[kMaxCells], cz[kMaxCells];
@@ -23,6 +23,7 @@ struct TileMode {
   unsigned char cplx[kMaxCells];    // 1 on the first row of a 2x2 block
   unsigned char ckind[kMaxCells];   // 1/2: first/second row of a complex-eigenvalue pair, else 0
   float vcond;                      // lap3: ||V||_F ||V^-1||_F / ext of the block's eigenvectors
+  int far_lo;                       // first row of tile t+3 (the mode extent when there is none)
 };
 
 // lap3 diagonalised tiles: per tile index along a mode, V^{-1} (re, im),

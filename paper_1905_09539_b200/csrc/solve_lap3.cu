@@ -239,6 +239,18 @@ TSG_DEVINL void wait_flag(const SolveArgs& a, int64_t tile, int owner, int own) 
   }
 }
 
+// single-tensor (one GPU, one slab) flag wait
+TSG_DEVINL void wait_flag1(const SolveArgs& a, int64_t tile) {
+  if (a.dbg & 512) return;  // timing ablation only: results are wrong
+  const int* f = a.flags + tile;
+  unsigned ns = 32;
+  const unsigned cap = (a.dbg & 64) ? 32 : 256;
+  while (ld_acquire(f) < a.epoch) {
+    __nanosleep(ns);
+    if (ns < cap) ns <<= 1;
+  }
+}
+
 // ---- far updates of all three modes in one pass, K split across warps ------
 // The k4-steps of the three far ranges (rows >= bnd[t_m + 3] of each mode)
 // are concatenated and cut into WARPS equal slices.  A warp accumulates the
@@ -317,6 +329,37 @@ TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, const double* x
       else l = l3off<LT>(va, jb, i);
       dst[l] += sub ? -c[jb][h] : c[jb][h];
     }
+}
+
+// Single-tensor variant: one K range per mode (rows [klo_m, khi_m)), the
+// mode loop unrolled at compile time.
+template <int LT>
+TSG_DEVINL void l3_ksplit1(const SolveArgs& a, const L3Geom& tg, double* red, const int* klo,
+                           const int* khi) {
+  using C = L3C<LT>;
+  const int warp = threadIdx.x >> 5;
+  int s[3], S = 0;
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    s[m] = (khi[m] - klo[m] + 3) >> 2;
+    S += s[m];
+  }
+  if (S == 0) return;
+  const int w0 = (S * warp) / C::WARPS, w1 = (S * (warp + 1)) / C::WARPS;
+  double* dst = red + warp * C::T;
+  int off = 0;
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    const int lo = w0 > off ? w0 : off, hi = w1 < off + s[m] ? w1 : off + s[m];
+    if (lo < hi) {
+      const int kl = klo[m] + 4 * (lo - off);
+      const int kh = min(khi[m], klo[m] + 4 * (hi - off));
+      if (m == 0) l3_far_seg<LT, 0, false>(a, tg, a.X, kl, kh, dst, false);
+      else if (m == 1) l3_far_seg<LT, 1, false>(a, tg, a.X, kl, kh, dst, false);
+      else l3_far_seg<LT, 2, false>(a, tg, a.X, kl, kh, dst, false);
+    }
+    off += s[m];
+  }
 }
 
 // One K range of the updates: rows [k_lo, k_hi) of mode m, read through the
@@ -435,7 +478,10 @@ TSG_DEVINL bool l3d_mode(const double* sr, const double* si, double* dr, double*
   return sing;
 }
 
-template <int LT>
+// DIST = the tensor is split into slabs (multi-GPU or emulated, tsg_dplan):
+// per-slab bases, owner-aware flags and segment lists; the single-tensor
+// instantiation keeps the plain addressing.
+template <int LT, bool DIST>
 __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     solve_lap3_kernel(SolveArgs a) {
   using C = L3C<LT>;
@@ -444,8 +490,8 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
   extern __shared__ __align__(16) double smem[];
   __shared__ L3Geom tg;
   __shared__ int s_tile;
-  __shared__ KSeg s_seg[2 + kMaxSlabs];
-  __shared__ int s_nseg;
+  __shared__ KSeg s_seg[2][2 + kMaxSlabs];  // far / near pass segments (DIST)
+  __shared__ int s_nseg[2];
   double* xr = smem + C::OFF_XR;
   double* xi = smem + C::OFF_XI;
   double* dh = smem + C::OFF_DH;
@@ -493,8 +539,10 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     }
     __syncthreads();
     if (tid == 0) {
-      tg.own = slab_of(a, tg.start[2]);
-      tg.xb = a.xs[tg.own];
+      if constexpr (DIST) {
+        tg.own = slab_of(a, tg.start[2]);
+        tg.xb = a.xs[tg.own];
+      }
       tg.gbase = static_cast<int64_t>(tg.start[0]) * a.stride[0] +
                  static_cast<int64_t>(tg.start[1]) * a.stride[1] +
                  static_cast<int64_t>(tg.start[2]) * a.stride[2];
@@ -518,7 +566,8 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     for (int l = tid; l < L3_T; l += L3_THREADS) {
       const int i0 = l & MSK, i1 = (l >> LT) & MSK, i2 = l >> (2 * LT);
       const bool ok = i0 < e0 && i1 < e1 && i2 < e2;
-      const double* src = ok ? tg.xb + tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2] : a.xs[0] + a.slo[0] * a.stride[2];
+      const double* xb = DIST ? tg.xb : a.X;
+      const double* src = ok ? xb + tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2] : a.X;
       cp_async8(xr + l, src, ok ? 8 : 0);
     }
     if (tg.diag) {  // eigenvector bases (V^-1, V, lambda) of the three modes
@@ -559,6 +608,32 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
         for (int l = tid & 31; l < L3_T; l += 32) mine[l] = 0.0;
         __syncwarp();
       }
+      if constexpr (!DIST) {
+        int klo[3], khi[3];
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          const int tm = tg.tco[m];
+          const bool has = tm + 3 < a.ntiles_mode[m] && !(a.dbg & 4);
+          klo[m] = has ? a.bnd[m][tm + 3] : 0;
+          khi[m] = has ? a.dims[m] : 0;
+          if (has && tid == 0) wait_flag1(a, tg.lt + 3 * mul[m]);
+        }
+        __syncthreads();
+        mark(3);
+        l3_ksplit1<LT>(a, tg, red, klo, khi);
+        mark(4);
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          const int tm = tg.tco[m];
+          const bool has = tm + 1 < a.ntiles_mode[m] && !(a.dbg & 4);
+          klo[m] = has ? a.bnd[m][tm + 1] : 0;
+          khi[m] = has ? (tm + 3 < a.ntiles_mode[m] ? a.bnd[m][tm + 3] : a.dims[m]) : 0;
+          if (has && tid == 0) wait_flag1(a, tg.lt + mul[m]);
+        }
+        __syncthreads();
+        mark(2);
+        l3_ksplit1<LT>(a, tg, red, klo, khi);
+      } else {
       if (tid == 0) {  // far: rows of tiles >= t+3
         int lo[3], hi[3];
         for (int m = 0; m < 3; ++m) {
@@ -568,13 +643,12 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
           hi[m] = has ? a.dims[m] : 0;
           if (has) wait_flag(a, tg.lt + 3 * mul[m], m == 2 ? slab_of(a, lo[2]) : tg.own, tg.own);
         }
-        s_nseg = l3_segments(a, tg.own, lo, hi, s_seg);
+        s_nseg[0] = l3_segments(a, tg.own, lo, hi, s_seg[0]);
       }
       __syncthreads();
       mark(3);
-      l3_far_ksplit<LT>(a, tg, red, s_seg, s_nseg);
+      l3_far_ksplit<LT>(a, tg, red, s_seg[0], s_nseg[0]);
       mark(4);
-      __syncthreads();  // s_seg reuse
       if (tid == 0) {  // near: rows of tiles t+1, t+2
         int lo[3], hi[3];
         for (int m = 0; m < 3; ++m) {
@@ -584,11 +658,12 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
           hi[m] = has ? (tm + 3 < a.ntiles_mode[m] ? a.bnd[m][tm + 3] : a.dims[m]) : 0;
           if (has) wait_flag(a, tg.lt + mul[m], m == 2 ? slab_of(a, lo[2]) : tg.own, tg.own);
         }
-        s_nseg = l3_segments(a, tg.own, lo, hi, s_seg);
+        s_nseg[1] = l3_segments(a, tg.own, lo, hi, s_seg[1]);
       }
       __syncthreads();
       mark(2);
-      l3_far_ksplit<LT>(a, tg, red, s_seg, s_nseg);
+      l3_far_ksplit<LT>(a, tg, red, s_seg[1], s_nseg[1]);
+      }
       cp_async_wait_all();
       __syncthreads();
       mark(1);
@@ -616,7 +691,7 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
           const int k_lo = bm[tm + dist];
           const int k_hi = part == 0 ? a.dims[m] : bm[tm + dist + 1];
           const int64_t wtile = tg.lt + dist * mul[m];
-          if (tid == 0) wait_flag(a, wtile, 0, 0);
+          if (tid == 0) wait_flag1(a, wtile);
           __syncthreads();
           if (m == 0) l3_update<LT, 0>(a, tg, xr, k_lo, k_hi);
           else if (m == 1) l3_update<LT, 1>(a, tg, xr, k_lo, k_hi);
@@ -860,16 +935,16 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     for (int l = tid; l < L3_T; l += L3_THREADS) {
       const int i0 = l & MSK, i1 = (l >> LT) & MSK, i2 = l >> (2 * LT);
       if (i0 < e0 && i1 < e1 && i2 < e2)
-        tg.xb[tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2]] = xr[l];
+        (DIST ? tg.xb : a.X)[tg.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2]] = xr[l];
     }
     __syncthreads();
     if (tid == 0) {
-      if (a.sys && tg.own > 0) {  // read by the lower slabs' GPUs
+      if (DIST && a.sys && tg.own > 0) {  // read by the lower slabs' GPUs
         __threadfence_system();
         st_release_sys(a.fs[tg.own] + tg.lt, a.epoch);
       } else {
         __threadfence();
-        st_release(a.fs[tg.own] + tg.lt, a.epoch);
+        st_release((DIST ? a.fs[tg.own] : a.flags) + tg.lt, a.epoch);
       }
       if (a.trace) {
         unsigned long long t;
@@ -889,8 +964,10 @@ cudaError_t launch_l3(const SolveArgs& a0, cudaStream_t st, SolveLaunchInfo* inf
   using C = L3C<LT>;
   SolveArgs a = a0;
   const int bytes = C::BYTES;
-  static int nsm = 0, occ = 0;
-  auto k = solve_lap3_kernel<LT>;
+  const bool dist = LT == 3 && (a.nslab > 1 || a.sys);
+  auto k = dist ? solve_lap3_kernel<LT, LT == 3> : solve_lap3_kernel<LT, false>;
+  static int nsm = 0, occs[2] = {0, 0};
+  int& occ = occs[dist ? 1 : 0];
   if (occ == 0) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
     if (e != cudaSuccess) return e;
