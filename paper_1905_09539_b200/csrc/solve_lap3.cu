@@ -260,8 +260,11 @@ TSG_DEVINL void wait_flag1(const SolveArgs& a, int64_t tile) {
 // into xr after the near updates).  Every warp thus walks a quarter of the
 // K range instead of all of it: 4x fewer dependent L2 round trips per tile
 // than splitting the columns.
+#ifndef L3_PARWAIT
+#define L3_PARWAIT 1
+#endif
 #ifndef L3_UB
-#define L3_UB 3
+#define L3_UB 2
 #endif
 template <int LT, int M, bool VOL>
 TSG_DEVINL void l3_far_seg(const SolveArgs& a, const L3Geom& tg, const double* xb, int k_lo, int k_hi,
@@ -622,14 +625,37 @@ __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
         mark(3);
         l3_ksplit1<LT>(a, tg, red, klo, khi);
         mark(4);
+#if L3_PARWAIT
+        int64_t wt[3];
+#endif
 #pragma unroll
         for (int m = 0; m < 3; ++m) {
           const int tm = tg.tco[m];
           const bool has = tm + 1 < a.ntiles_mode[m] && !(a.dbg & 4);
           klo[m] = has ? a.bnd[m][tm + 1] : 0;
           khi[m] = has ? (tm + 3 < a.ntiles_mode[m] ? a.bnd[m][tm + 3] : a.dims[m]) : 0;
+#if L3_PARWAIT
+          wt[m] = has ? tg.lt + mul[m] : -1;
+#else
           if (has && tid == 0) wait_flag1(a, tg.lt + mul[m]);
+#endif
         }
+#if L3_PARWAIT
+        if (tid == 0 && !(a.dbg & 512)) {
+          bool ok[3] = {wt[0] < 0, wt[1] < 0, wt[2] < 0};
+          unsigned ns = 32;
+          while (!(ok[0] && ok[1] && ok[2])) {
+            int v[3];
+#pragma unroll
+            for (int m = 0; m < 3; ++m) v[m] = ok[m] ? 0 : ld_acquire(a.flags + wt[m]);
+#pragma unroll
+            for (int m = 0; m < 3; ++m) ok[m] = ok[m] || v[m] >= a.epoch;
+            if (ok[0] && ok[1] && ok[2]) break;
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+          }
+        }
+#endif
         __syncthreads();
         mark(2);
         l3_ksplit1<LT>(a, tg, red, klo, khi);
