@@ -134,7 +134,9 @@ int tsg_dplan_create(tsg_ctx* ctx, int rank, int nranks, int emulate, int d, con
   dp->d = d;
   dp->dims.assign(dims, dims + d);
   for (int m = 0; m < d - 1; ++m) dp->plane *= dims[m];
+  tsg_impl::g_force_lap3 = true;
   int rc = tsg_plan_create(ctx, 0, d, dims, T, nullptr, nullptr, nullptr, 1, opts, &dp->pl);
+  tsg_impl::g_force_lap3 = false;
   if (rc != TSG_OK) return rc;
   tsg_plan* pl = dp->pl;
   if (pl->fast != 3 || pl->lt3 != 3)

@@ -35,6 +35,8 @@
 
 namespace tsg_impl {
 
+thread_local bool g_force_lap3 = false;
+
 int fail(tsg_ctx* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
   return code;
@@ -255,10 +257,11 @@ std::vector<int> tile_bounds(int n, int b, const std::vector<int8_t>& code) {
 // V = P_tile Vh (columns scaled to unit norm), V^{-1} = Vh^{-1} P_tile^{-1},
 // all in long double.  vcond = ||V||_F ||V^{-1}||_F / ext (1 for a normal
 // block; inf when two eigenvalues coincide).
+template <int E>
 void tile_eigvecs(std::vector<tsg::TileMode>& tms, const std::vector<double>& dh,
                   const std::vector<double>& pdv, std::vector<double>& vh) {
   using Cx = std::complex<long double>;
-  constexpr int E = 8, EE = 64, DHS = 2 * EE + 2 * E, VHS = tsg::kVhStride;
+  constexpr int EE = E * E, DHS = 2 * EE + 2 * E, VHS = 4 * EE + 2 * E;
   vh.assign(tms.size() * VHS, 0.0);
   for (size_t t = 0; t < tms.size(); ++t) {
     tsg::TileMode& tm = tms[t];
@@ -494,24 +497,26 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   if (family != 0) pl->fast = 0;
   pl->lt3 = 3;
   if (const char* e = std::getenv("TSG_LT")) pl->lt3 = std::atoi(e) == 4 ? 4 : 3;
-  // Tiles.
-  pl->tile_ext = choose_tiles(family, pl->dims, o,
-                              pl->fast == 3 ? tsg::solve_lap3_caps(pl->lt3)
-                                            : (pl->fast ? tsg::solve_lap_caps(d) : tsg::solve_caps(family, d)));
-  pl->ntiles_mode.resize(d);
-  pl->ntiles = 1;
-  std::vector<std::vector<int>> bds(d);
-  for (int m = 0; m < d; ++m) {
-    bds[m] = tile_bounds(dims[m], pl->tile_ext[m], codes[m]);
-    pl->ntiles_mode[m] = static_cast<int>(bds[m].size()) - 1;
-    pl->ntiles *= pl->ntiles_mode[m];
-    TSG_CU(upload(&pl->bnd[m], bds[m]));
-    std::vector<tsg::TileMode> tms(pl->ntiles_mode[m]);
-    for (int t = 0; t < pl->ntiles_mode[m]; ++t) {
-      tsg::TileMode& tmd = tms[t];
+  // Tiles (host tables first; the 16^3 TMA kernel is taken when every tile's
+  // eigenvector bases are well conditioned, else the 8^3 kernel).
+  struct ModeTables {
+    std::vector<int> bd;
+    std::vector<tsg::TileMode> tms;
+    std::vector<double> dh, vh;
+    float maxvc = 0.0f;
+  };
+  std::vector<ModeTables> mts(d);
+  auto build_mode = [&](int m, int lt, bool diag16) -> int {
+    ModeTables& mt = mts[m];
+    mt = ModeTables{};
+    mt.bd = tile_bounds(dims[m], pl->tile_ext[m], codes[m]);
+    const int ntm = static_cast<int>(mt.bd.size()) - 1;
+    mt.tms.resize(ntm);
+    for (int t = 0; t < ntm; ++t) {
+      tsg::TileMode& tmd = mt.tms[t];
       std::memset(&tmd, 0, sizeof(tmd));
-      tmd.start = bds[m][t];
-      const int ex = bds[m][t + 1] - bds[m][t];
+      tmd.start = mt.bd[t];
+      const int ex = mt.bd[t + 1] - mt.bd[t];
       if (ex > 255) return fail(ctx, TSG_EDIM, "tile extent too large");
       tmd.ext = static_cast<unsigned char>(ex);
       int nc = 0;
@@ -534,22 +539,23 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         r += sz;
       }
       tmd.nc = static_cast<unsigned char>(nc);
-      tmd.far_lo = t + 3 < pl->ntiles_mode[m] ? bds[m][t + 3] : dims[m];
+      tmd.far_lo = t + 3 < ntm ? mt.bd[t + 3] : dims[m];
     }
     if (pl->fast == 3) {
       // Eigenbasis diagonal block of every tile index along mode m:
       // That[i][j] = sum Pinv_blk(i)[i,a] T[a,b] P_blk(j)[b,j] for j beyond
       // i's cell (0 elsewhere), then lambda_i; layout of solve_lap3 (DHS).
       using Cx = std::complex<double>;
-      const int E = 1 << pl->lt3, EE = E * E, DHS = 2 * EE + 2 * E;
-      std::vector<double> dh(static_cast<size_t>(pl->ntiles_mode[m]) * DHS, 0.0);
+      const int E = 1 << lt, EE = E * E, DHS = 2 * EE + 2 * E;
+      std::vector<double>& dh = mt.dh;
+      dh.assign(static_cast<size_t>(ntm) * DHS, 0.0);
       const int n = dims[m];
       auto Pget = [&](int row0, int r, int c, int which) {  // which 4: P, 12: Pinv
         const double* pr = pdvs[m].data() + static_cast<size_t>(row0) * tsg::kPStride + which;
         return Cx(pr[(r * 2 + c) * 2], pr[(r * 2 + c) * 2 + 1]);
       };
-      for (int t = 0; t < pl->ntiles_mode[m]; ++t) {
-        const tsg::TileMode& tmd = tms[t];
+      for (int t = 0; t < ntm; ++t) {
+        const tsg::TileMode& tmd = mt.tms[t];
         double* o = dh.data() + static_cast<size_t>(t) * DHS;
         for (int i = 0; i < tmd.ext; ++i) {
           const int ci = tmd.cellof[i], I0 = tmd.cs[ci], Iz = tmd.cz[ci];
@@ -571,14 +577,50 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
           o[2 * EE + E + i] = pr[(i - I0) * 2 + 1];
         }
       }
-      TSG_CU(upload_mat(pl->dhat[m], dh.data(), dh.size()));
-      if (pl->lt3 == 3) {
-        std::vector<double> vh;
-        tile_eigvecs(tms, dh, pdvs[m], vh);
-        TSG_CU(upload_mat(pl->vhat[m], vh.data(), vh.size()));
-      }
+      if (lt == 3) tile_eigvecs<8>(mt.tms, dh, pdvs[m], mt.vh);
+      else if (diag16) tile_eigvecs<16>(mt.tms, dh, pdvs[m], mt.vh);
+      for (const auto& tm : mt.tms) mt.maxvc = std::max(mt.maxvc, tm.vcond);
     }
-    TSG_CU(upload(&pl->tmode[m], tms));
+    return TSG_OK;
+  };
+  const char* e16 = std::getenv("TSG_LAP16");
+  const bool want16 = pl->fast == 3 && d == 3 && !tsg_impl::g_force_lap3 && !std::getenv("TSG_LT") &&
+                      (e16 ? std::atoi(e16) != 0
+                           : (dims[0] >= 64 && dims[1] >= 64 && dims[2] >= 64 && pl->N >= (int64_t{1} << 23))) &&
+                      dims[0] % 2 == 0;  // TMA: 16-byte row strides
+  if (want16) {
+    pl->tile_ext = choose_tiles(family, pl->dims, o, tsg::solve_lap16_caps());
+    double prod = 1.0;
+    for (int m = 0; m < d; ++m) {
+      const int rc = build_mode(m, 4, true);
+      if (rc != TSG_OK) return rc;
+      prod *= mts[m].maxvc;
+    }
+    if (prod <= tsg::kDiagCond) {
+      pl->use16 = true;
+      pl->lt3 = 4;
+    }
+  }
+  if (!pl->use16) {
+    pl->tile_ext = choose_tiles(family, pl->dims, o,
+                                pl->fast == 3 ? tsg::solve_lap3_caps(pl->lt3)
+                                              : (pl->fast ? tsg::solve_lap_caps(d) : tsg::solve_caps(family, d)));
+    for (int m = 0; m < d; ++m) {
+      const int rc = build_mode(m, pl->lt3, false);
+      if (rc != TSG_OK) return rc;
+    }
+  }
+  pl->ntiles_mode.resize(d);
+  pl->ntiles = 1;
+  std::vector<std::vector<int>> bds(d);
+  for (int m = 0; m < d; ++m) {
+    bds[m] = mts[m].bd;
+    pl->ntiles_mode[m] = static_cast<int>(bds[m].size()) - 1;
+    pl->ntiles *= pl->ntiles_mode[m];
+    TSG_CU(upload(&pl->bnd[m], bds[m]));
+    if (!mts[m].dh.empty()) TSG_CU(upload_mat(pl->dhat[m], mts[m].dh.data(), mts[m].dh.size()));
+    if (!mts[m].vh.empty()) TSG_CU(upload_mat(pl->vhat[m], mts[m].vh.data(), mts[m].vh.size()));
+    TSG_CU(upload(&pl->tmode[m], mts[m].tms));
   }
   pl->bds_h = bds;
   if (pl->ntiles > INT_MAX / 2) return fail(ctx, TSG_EDIM, "too many tiles");
@@ -914,6 +956,7 @@ void fill_solve_args(const tsg_plan* pl, double* work, tsg::SolveArgs& a) {
 }
 
 cudaError_t launch_plan_solve(tsg_plan* pl, const tsg::SolveArgs& a, cudaStream_t st) {
+  if (pl->use16) return tsg::launch_solve_lap16(a, st, &pl->solve_info);
   if (pl->fast == 3) return tsg::launch_solve_lap3(pl->lt3, a, st, &pl->solve_info);
   if (pl->fast) return tsg::launch_solve_lap(a, st, &pl->solve_info);
   return tsg::launch_solve(a, st, &pl->solve_info);

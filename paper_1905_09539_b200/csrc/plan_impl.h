@@ -50,6 +50,7 @@ struct tsg_plan {
   unsigned long long* ocoord = nullptr;
   int fast = 0;  // 1: solve_lap_kernel, 3: solve_lap3_kernel (Laplace, good eigenbases)
   int lt3 = 3;   // log2 tile extent of solve_lap3
+  bool use16 = false;  // 16^3 TMA kernel (solve_lap16.cu)
   int* flags = nullptr;
   int* counter = nullptr;   // [0] = queue head, [1] = status
   int64_t ntiles = 0;
@@ -84,6 +85,9 @@ struct tsg_plan {
 
 
 namespace tsg_impl {
+
+// set while tsg_dplan_create builds its plan (the sharded solve runs the 8^3 kernel)
+extern thread_local bool g_force_lap3;
 
 int fail(tsg_ctx* ctx, int code, const std::string& msg);
 cudaError_t upload_mat(DevBuf& b, const double* h, size_t n);

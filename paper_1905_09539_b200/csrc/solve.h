@@ -29,6 +29,7 @@ struct alignas(16) TileMode {
 // lap3 diagonalised tiles: per tile index along a mode, V^{-1} (re, im),
 // V (re, im) as 8x8 row-major (identity-padded) and lambda (re, im).
 constexpr int kVhStride = 4 * 64 + 2 * 8;
+constexpr int kVhStride16 = 4 * 256 + 2 * 16;
 // A tile is diagonalised when the product of its three vcond values is at
 // most this (the eigenvector transforms then cost <= ~kDiagCond ulps).
 constexpr float kDiagCond = 1000.0f;
@@ -92,6 +93,11 @@ cudaError_t launch_solve(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* i
 // Order-3 Laplace fast path (solve_lap3.cu): padded 16^3 tiles.
 TileCaps solve_lap3_caps(int lt);  // lt = log2 tile extent (3 or 4)
 cudaError_t launch_solve_lap3(int lt, const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
+
+// Order-3 Laplace, 16^3 tiles, TMA-staged updates, diagonalised base case
+// (solve_lap16.cu; plans whose tiles are all diagonalisable).
+TileCaps solve_lap16_caps();
+cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
 
 // Fast Laplace path (solve_lap.cu): small tiles, eigenbasis base cells.
 TileCaps solve_lap_caps(int d);

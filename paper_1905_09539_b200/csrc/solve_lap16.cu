@@ -1,0 +1,419 @@
+// Order-3 Laplace solve over 16^3 tiles with TMA-staged operands (C2, C4).
+//
+// Same dataflow as solve_lap3.cu (tiles in topological hyperplane order from
+// an atomic queue, left-looking updates from later tiles, release flags),
+// rebuilt around the two costs that bound the 8^3 kernel:
+//   * update traffic: every B element loaded for the left-looking update
+//     feeds one row block per tile extent, so 16-row tiles halve the L2
+//     traffic of sum_m T_m[t, later] x_m X(later) (24 N vs 48 N doubles);
+//   * memory-level parallelism: one producer warp streams the update
+//     operand as 16x16x16 boxes of X (cp.async.bulk.tensor, 32 KB each)
+//     into a two-stage mbarrier ring, so the eight consumer warps only issue
+//     DMMA and shared-memory fragment loads (no register-bound load batches).
+// The base case is the diagonalised tile of solve_lap3.cu at E = 16:
+//   x^ = x x_0 V0^-1 x_1 V1^-1 x_2 V2^-1, x^ /= l0 + l1 + l2, x = x^ x_m V_m,
+// twenty real 16x16x256 DMMA GEMMs (the first and last real-only), using the
+// ring as the complex work tile.  Plans choose this kernel only when every
+// tile's eigenvector bases are well conditioned (tsg_plan: vcond product).
+// One CTA (8 consumer + 1 producer warps) per SM.
+// Reference: lap_rec / lap_base (laplace.hpp:99-153), mode_multiply update
+// (laplace.hpp:147), block_back_substitution (kernels.hpp:179-261).
+#include <cstdint>
+
+#include "common.cuh"
+#include "solve.h"
+#include "tma.h"
+
+namespace tsg {
+namespace {
+
+constexpr int E = 16, EE = 256, TT = 4096;
+constexpr int CW = 8;                 // consumer warps
+constexpr int THREADS = (CW + 1) * 32;
+#ifndef L16_NST
+#define L16_NST 2
+#endif
+#ifndef L16_BY
+#define L16_BY 17
+#endif
+#ifndef L16_BX
+#define L16_BX 20
+#endif
+constexpr int NSR = L16_NST;          // ring stages in the ring region
+constexpr int NST = NSR + 1;          // + xi (free while the updates stream)
+constexpr int VHS = kVhStride16;
+// Shared tile layout = the TMA box layout: (x0, x1, x2) at x0 + S1 x1 + S2 x2.
+// Boxes are 20 x 17 x 16: the inner start coordinate of an FP64 box must be
+// even (16-byte aligned), so a box starts at c0 & ~1 and the 16 used
+// elements sit at offset o = c0 & 1; the padded strides (20, 340 doubles)
+// make every DMMA fragment load of the three modes bank-conflict free.
+constexpr int BX = L16_BX, BY = L16_BY, BZ = 16;
+constexpr int S1 = BX, S2 = BX * BY, TD = BX * BY * BZ;
+constexpr int OFF_XR = 0, OFF_XI = TD, OFF_VH = 2 * TD, OFF_RING = OFF_VH + 3 * VHS;
+constexpr int DOUBLES = OFF_RING + NSR * TD;
+constexpr int BYTES = DOUBLES * 8;
+constexpr unsigned BOX_BYTES = TD * 8;
+static_assert((OFF_RING * 8) % 128 == 0 && (TD * 8) % 128 == 0, "TMA destinations 128-byte aligned");
+static_assert(NSR >= 2, "the ring doubles as the complex work tile (yr, yi)");
+
+struct G16 {
+  int64_t lt, gbase;
+  int start[3], ext[3], tco[3];
+  int nlo[3], flo[3];  // first rows of tiles t+1 and t+2 per mode (n_m when absent)
+  int nch;             // chunks of this tile
+};
+
+TSG_DEVINL void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+TSG_DEVINL void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+TSG_DEVINL void consumers_sync() { asm volatile("bar.sync 1, %0;\n" ::"n"(CW * 32) : "memory"); }
+
+// tile offset of mode-M row i, cross-section column n (the other two modes,
+// first one fastest); also the layout of a 16^3 TMA box along mode M
+template <int M>
+TSG_DEVINL int addr16(int i, int n) {
+  if (M == 0) return i + S1 * (n & (E - 1)) + S2 * (n >> 4);
+  if (M == 1) return (n & (E - 1)) + S1 * i + S2 * (n >> 4);
+  return (n & (E - 1)) + S1 * (n >> 4) + S2 * i;
+}
+
+// chunk c of the tile: mode, first row, end row (far ranges first, then the
+// near tiles t+1), identical on the producer and the consumers
+struct Chunk {
+  int m, k, kh, first;  // first: first chunk of its (mode, far/near) group
+};
+TSG_DEVINL Chunk chunk_of(const G16& g, const int* dims, int c) {
+#pragma unroll
+  for (int part = 0; part < 2; ++part)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int lo = part == 0 ? g.flo[m] : g.nlo[m];
+      const int hi = part == 0 ? dims[m] : g.flo[m];
+      const int n = hi > lo ? (hi - lo + E - 1) / E : 0;
+      if (c < n) return Chunk{m + 3 * part, lo + E * c, hi, c == 0};
+      c -= n;
+    }
+  return Chunk{0, 0, 0, 0};
+}
+
+// acc[rb][cb] += T_M[rows, k..k+15] * box(k, cols) for this warp's 4 column
+// blocks (cross-section columns 32 w .. 32 w + 31), both 8-row blocks
+// A fragments of a chunk: T_M[tile rows, k..k+15] (rows beyond the tensor
+// clamp, columns >= kh give 0)
+TSG_DEVINL void chunk_afrag(const SolveArgs& a, const G16& g, int m, int k, int kh, double (&af)[4][2]) {
+  const int lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int n = a.dims[m];
+  const double* Tm = a.T[m];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb) {
+      const int kk = k + 4 * ks + tq;
+      int row = g.start[m] + 8 * rb + gq;
+      row = row < n ? row : n - 1;
+      af[ks][rb] = kk < kh ? __ldg(Tm + row + static_cast<int64_t>(kk) * n) : 0.0;
+    }
+}
+
+// acc[rb][cb] += A(16 rows x 16 k) * box(k, cols) for this warp's 4 column
+// blocks (cross-section columns 32 w .. 32 w + 31), both 8-row blocks
+template <int M>
+TSG_DEVINL void chunk_dmma(const double* box, const double (&af)[4][2], double (&acc)[2][4][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) {
+      const double b = box[addr16<M>(4 * ks + tq, 8 * (4 * warp + cb) + gq)];
+#pragma unroll
+      for (int rb = 0; rb < 2; ++rb) dmma(acc[rb][cb][0], acc[rb][cb][1], af[ks][rb], b);
+    }
+}
+
+template <int M>
+TSG_DEVINL void flush16(double* xr, const double (&acc)[2][4][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) xr[addr16<M>(8 * rb + gq, 8 * (4 * warp + cb) + 2 * tq + h)] -= acc[rb][cb][h];
+}
+
+// one complex 16x16 mode product over the tile (out of place), optional
+// fused division by mu = l0 + l1 + l2 (mode 2 only)
+template <int M, bool CIN, bool COUT, bool DIV>
+TSG_DEVINL bool cmode16(const double* sr, const double* si, double* dr, double* di, const double* Ar,
+                        const double* Ai, const double* vh, const int* ext, double tiny) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  double cr[2][4][2], ci[2][4][2];
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) cr[rb][cb][0] = cr[rb][cb][1] = ci[rb][cb][0] = ci[rb][cb][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k = 4 * ks + tq;
+    double ar[2], ai[2];
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb) {
+      ar[rb] = Ar[E * (8 * rb + gq) + k];
+      ai[rb] = Ai[E * (8 * rb + gq) + k];
+    }
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) {
+      const int n = 8 * (4 * warp + cb) + gq;
+      const double br = sr[addr16<M>(k, n)];
+      const double bi = CIN ? si[addr16<M>(k, n)] : 0.0;
+#pragma unroll
+      for (int rb = 0; rb < 2; ++rb) {
+        dmma(cr[rb][cb][0], cr[rb][cb][1], ar[rb], br);
+        if (COUT) dmma(ci[rb][cb][0], ci[rb][cb][1], ai[rb], br);
+        if (CIN) {
+          dmma(cr[rb][cb][0], cr[rb][cb][1], -ai[rb], bi);
+          if (COUT) dmma(ci[rb][cb][0], ci[rb][cb][1], ar[rb], bi);
+        }
+      }
+    }
+  }
+  bool sing = false;
+#pragma unroll
+  for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = 8 * rb + gq, n = 8 * (4 * warp + cb) + 2 * tq + h;
+        double vr = cr[rb][cb][h], vi = ci[rb][cb][h];
+        if (DIV) {  // M == 2: rows i2, columns (i0, i1)
+          const int i0 = n & (E - 1), i1 = n >> 4;
+          const double mr = vh[4 * EE + i0] + vh[VHS + 4 * EE + i1] + vh[2 * VHS + 4 * EE + row];
+          const double mi = vh[4 * EE + E + i0] + vh[VHS + 4 * EE + E + i1] + vh[2 * VHS + 4 * EE + E + row];
+          const double den = mr * mr + mi * mi;
+          if (!(den > tiny * tiny)) {
+            if (i0 < ext[0] && i1 < ext[1] && row < ext[2]) sing = true;
+            vr = vi = 0.0;
+          } else {
+            const double inv = 1.0 / den;
+            const double r = (cr[rb][cb][h] * mr + ci[rb][cb][h] * mi) * inv;
+            vi = (ci[rb][cb][h] * mr - cr[rb][cb][h] * mi) * inv;
+            vr = r;
+          }
+        }
+        dr[addr16<M>(row, n)] = vr;
+        if (COUT) di[addr16<M>(row, n)] = vi;
+      }
+  return sing;
+}
+
+TSG_DEVINL void wait_tile(const SolveArgs& a, int64_t tile) {
+  const int* f = a.flags + tile;
+  unsigned ns = 32;
+  while (ld_acquire(f) < a.epoch) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    solve_lap16_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tmx) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ G16 g;
+  __shared__ int s_tile;
+  __shared__ __align__(8) uint64_t full[NST], empty[NST], bar_x, bar_v;
+  double* xr = smem + OFF_XR;
+  double* xi = smem + OFF_XI;
+  double* vh = smem + OFF_VH;
+  double* ring = smem + OFF_RING;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, CW);
+    }
+    mbar_init(&bar_x, 1);
+    mbar_init(&bar_v, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  unsigned gch = 0;   // chunks consumed/produced so far (ring phases)
+  unsigned tphase = 0;  // tiles processed (bar_x / bar_v phases)
+  const int64_t mul[3] = {1, a.ntiles_mode[0], static_cast<int64_t>(a.ntiles_mode[0]) * a.ntiles_mode[1]};
+
+  for (;; ++tphase) {
+    if (tid == 0) s_tile = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int qi = s_tile;
+    if (qi >= a.ntiles) break;
+    if (tid < 3) {
+      const unsigned long long pk = a.ocoord[qi];
+      const int tm = static_cast<int>((pk >> (10 * tid)) & 1023);
+      const TileMode& src = a.tmode[tid][tm];
+      g.tco[tid] = tm;
+      g.start[tid] = src.start;
+      g.ext[tid] = src.ext;
+      const int p = a.ntiles_mode[tid];
+      g.nlo[tid] = tm + 1 < p ? a.bnd[tid][tm + 1] : a.dims[tid];
+      g.flo[tid] = tm + 2 < p ? a.bnd[tid][tm + 2] : a.dims[tid];
+      if (tid == 0) g.lt = a.order[qi];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      g.gbase = static_cast<int64_t>(g.start[0]) + static_cast<int64_t>(g.start[1]) * a.stride[1] +
+                static_cast<int64_t>(g.start[2]) * a.stride[2];
+      int nch = 0;
+      for (int m = 0; m < 3; ++m) {
+        nch += a.dims[m] > g.flo[m] ? (a.dims[m] - g.flo[m] + E - 1) / E : 0;
+        nch += g.flo[m] > g.nlo[m] ? (g.flo[m] - g.nlo[m] + E - 1) / E : 0;
+      }
+      g.nch = (a.dbg & 4) ? 0 : nch;
+    }
+    __syncthreads();
+    const int nch = g.nch;
+
+    if (warp == CW) {
+      // ---------------- producer: B~ tile, eigenvector bases, update boxes ----
+      if ((tid & 31) == 0) {
+        if (!(a.dbg & 32768)) {
+          mbar_expect_tx(&bar_x, BOX_BYTES);
+          tma_load_3d(xr, &tmx, g.start[0] & ~1, g.start[1], g.start[2], &bar_x);
+        }
+        if (!(a.dbg & 16384)) {
+          mbar_expect_tx(&bar_v, 3 * VHS * 8);
+          for (int m = 0; m < 3; ++m)
+            bulk_g2s(vh + m * VHS, a.vhat[m] + static_cast<int64_t>(g.tco[m]) * VHS, VHS * 8, &bar_v);
+        }
+        for (int c = 0; c < nch; ++c, ++gch) {
+          const Chunk ch = chunk_of(g, a.dims, c);
+          const int m = ch.m % 3;
+          if (ch.first) {  // far: tile t+2 along m; near: tile t+1
+            wait_tile(a, g.lt + (ch.m < 3 ? 2 : 1) * mul[m]);
+            fence_proxy_async();
+          }
+          const int s = gch % NST;
+          if (gch >= NST) mbar_wait(empty + s, ((gch / NST) - 1) & 1);
+          int cc[3] = {g.start[0], g.start[1], g.start[2]};
+          cc[m] = ch.k;
+          mbar_expect_tx(full + s, BOX_BYTES);
+          tma_load_3d(s < NSR ? ring + s * TD : xi, &tmx, cc[0] & ~1, cc[1], cc[2], full + s);
+        }
+      } else {
+        gch += nch;
+      }
+      gch = __shfl_sync(0xffffffffu, gch, 0);
+    } else {
+      // ---------------- consumers --------------------------------------------
+      double acc[3][2][4][2];
+#pragma unroll
+      for (int m = 0; m < 3; ++m)
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) acc[m][rb][cb][0] = acc[m][rb][cb][1] = 0.0;
+      double af[4][2], an[4][2];
+      Chunk ch = chunk_of(g, a.dims, 0);
+      if (nch > 0) chunk_afrag(a, g, ch.m % 3, ch.k, ch.kh, af);
+      for (int c = 0; c < nch; ++c, ++gch) {
+        const Chunk cn = chunk_of(g, a.dims, c + 1);
+        if (c + 1 < nch) chunk_afrag(a, g, cn.m % 3, cn.k, cn.kh, an);  // next chunk's A, in flight
+        const int s = gch % NST;
+        mbar_wait(full + s, (gch / NST) & 1);
+        const int m = ch.m % 3;
+        const double* box = (s < NSR ? ring + s * TD : xi) + ((m == 0 ? ch.k : g.start[0]) & 1);
+        if (m == 0) chunk_dmma<0>(box, af, acc[0]);
+        else if (m == 1) chunk_dmma<1>(box, af, acc[1]);
+        else chunk_dmma<2>(box, af, acc[2]);
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(empty + s);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) af[ks][0] = an[ks][0], af[ks][1] = an[ks][1];
+        ch = cn;
+      }
+      if (!(a.dbg & 32768)) mbar_wait(&bar_x, tphase & 1);  // B~ tile landed
+      double* xo = xr + (g.start[0] & 1);  // the B~ box starts at an even row
+      flush16<0>(xo, acc[0]);
+      consumers_sync();
+      flush16<1>(xo, acc[1]);
+      consumers_sync();
+      flush16<2>(xo, acc[2]);
+      consumers_sync();
+      // ---- diagonalised base case (ring = complex work tile) ----
+      if (!(a.dbg & 16384)) mbar_wait(&bar_v, tphase & 1);
+      if (a.dbg & 2048) goto scatter16;
+      {
+      double* yr = ring;
+      double* yi = ring + TD;
+      const int* ex = g.ext;
+      constexpr int RE = 0, IM = EE, VR = 2 * EE, VI = 3 * EE;
+      bool sing = false;
+      cmode16<0, false, true, false>(xo, nullptr, yr, yi, vh + RE, vh + IM, vh, ex, a.tiny);
+      consumers_sync();
+      cmode16<1, true, true, false>(yr, yi, xr, xi, vh + VHS + RE, vh + VHS + IM, vh, ex, a.tiny);
+      consumers_sync();
+      sing |= cmode16<2, true, true, true>(xr, xi, yr, yi, vh + 2 * VHS + RE, vh + 2 * VHS + IM, vh, ex,
+                                           a.tiny);
+      consumers_sync();
+      cmode16<2, true, true, false>(yr, yi, xr, xi, vh + 2 * VHS + VR, vh + 2 * VHS + VI, vh, ex, a.tiny);
+      consumers_sync();
+      cmode16<1, true, true, false>(xr, xi, yr, yi, vh + VHS + VR, vh + VHS + VI, vh, ex, a.tiny);
+      consumers_sync();
+      cmode16<0, true, false, false>(yr, yi, xr, nullptr, vh + VR, vh + VI, vh, ex, a.tiny);
+      if (sing) atomicMin(a.status, static_cast<int>(g.lt < 0x7f7f7f7e ? g.lt : 0x7f7f7f7e));
+      consumers_sync();
+      }
+    scatter16:
+      // ---- scatter X_t, release ----
+      const int e0 = g.ext[0], e1 = g.ext[1], e2 = g.ext[2];
+      for (int l = tid; l < TT; l += CW * 32) {
+        const int i0 = l & (E - 1), i1 = (l >> 4) & (E - 1), i2 = l >> 8;
+        if (i0 < e0 && i1 < e1 && i2 < e2)
+          a.X[g.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2]] = xr[i0 + S1 * i1 + S2 * i2];
+      }
+      consumers_sync();
+      if (tid == 0) {
+        __threadfence();
+        st_release(a.flags + g.lt, a.epoch);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+TileCaps solve_lap16_caps() { return TileCaps{E, TT, EE}; }
+
+cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
+  if (a.ntiles <= 0) return cudaSuccess;
+  CUtensorMap map;
+  const uint64_t dims[3] = {static_cast<uint64_t>(a.dims[0]), static_cast<uint64_t>(a.dims[1]),
+                            static_cast<uint64_t>(a.dims[2])};
+  const uint32_t box[3] = {BX, BY, BZ};
+  if (!encode_tmap_f64(&map, a.X, 3, dims, box)) return cudaErrorInvalidValue;
+  static int nsm = 0;
+  if (nsm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(solve_lap16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BYTES);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t grid = nsm;
+  if (grid > a.ntiles) grid = a.ntiles;
+  if (info) *info = SolveLaunchInfo{static_cast<int>(grid), THREADS, BYTES, 1};
+  solve_lap16_kernel<<<static_cast<unsigned>(grid), THREADS, BYTES, st>>>(a, map);
+  return cudaGetLastError();
+}
+
+}  // namespace tsg

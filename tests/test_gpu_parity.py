@@ -162,3 +162,17 @@ def test_solve_gsylv_baseline_shape(gpu, ref, dims):
     rep = gpu.solve_gsylv(p)
     assert rel_diff(rep.solution, want) < REL
     assert rep.residual < RES
+
+
+# 16^3-tile TMA kernel (solve_lap16.cu): chosen by default from 2^23 unknowns;
+# forced here on small shapes (odd tile starts along mode 0, partial boxes at
+# the tensor edges, several tiles per CTA).
+@pytest.mark.parametrize("kind,dims", [(2, (64, 64, 64)), (2, (96, 66, 80)), (1, (64, 48, 80)), (2, (128, 64, 70))])
+def test_lap16_kernel_matches_reference(gpu, ref, kind, dims, monkeypatch):
+    monkeypatch.setenv("TSG_LAP16", "1")
+    p = gpu.make_problem(kind, dims, seed=5)
+    want, _ = ref.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
+    rep = gpu.solve_laplace(p, gpu.SolverConfig(strategy=gpu.Strategy.recursion_only,
+                                                arithmetic=gpu.Arithmetic.real_quasitriangular))
+    assert rel_diff(rep.solution, want) < REL
+    assert ref.residual_laplace(p.coeffs, p.rhs, rep.solution) < RES
