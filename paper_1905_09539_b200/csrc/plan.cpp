@@ -257,11 +257,13 @@ std::vector<int> tile_bounds(int n, int b, const std::vector<int8_t>& code) {
 // V = P_tile Vh (columns scaled to unit norm), V^{-1} = Vh^{-1} P_tile^{-1},
 // all in long double.  vcond = ||V||_F ||V^{-1}||_F / ext (1 for a normal
 // block; inf when two eigenvalues coincide).
-template <int E>
+// REAL = true: the real block-diagonalising basis instead (see below),
+// layout Vr^-1 | Vr (row-major) | alpha | beta, 2 E^2 + 2 E doubles.
+template <int E, bool REAL = false>
 void tile_eigvecs(std::vector<tsg::TileMode>& tms, const std::vector<double>& dh,
                   const std::vector<double>& pdv, std::vector<double>& vh) {
   using Cx = std::complex<long double>;
-  constexpr int EE = E * E, DHS = 2 * EE + 2 * E, VHS = 4 * EE + 2 * E;
+  constexpr int EE = E * E, DHS = 2 * EE + 2 * E, VHS = REAL ? 2 * EE + 2 * E : 4 * EE + 2 * E;
   vh.assign(tms.size() * VHS, 0.0);
   for (size_t t = 0; t < tms.size(); ++t) {
     tsg::TileMode& tm = tms[t];
@@ -337,6 +339,76 @@ void tile_eigvecs(std::vector<tsg::TileMode>& tms, const std::vector<double>& dh
     const long double vc = ok ? std::sqrt(nv * ni) / ex : 0.0L;
     tm.vcond = ok && std::isfinite(static_cast<double>(vc)) ? static_cast<float>(vc)
                                                            : std::numeric_limits<float>::infinity();
+    if constexpr (REAL) {
+      // Real block-diagonalising basis: a real eigenvalue keeps its (phase-
+      // normalised, real) eigenvector; a complex pair alpha +- i beta of cell
+      // rows (r, r+1) takes [Re v_r, Im v_r], for which
+      // D [Re v, Im v] = [Re v, Im v] [[alpha, beta], [-beta, alpha]].
+      long double Vr[E][E] = {}, Vri[E][E] = {};
+      bool okr = ok;
+      for (int c = 0; c < tm.nc && okr; ++c) {
+        const int r0 = tm.cs[c];
+        if (tm.cz[c] == 1) {
+          int im = 0;
+          for (int i = 1; i < ex; ++i)
+            if (std::abs(V[i][r0]) > std::abs(V[im][r0])) im = i;
+          const Cx ph = V[im][r0] / std::abs(V[im][r0]);
+          for (int i = 0; i < ex; ++i) Vr[i][r0] = (V[i][r0] / ph).real();
+        } else {
+          for (int i = 0; i < ex; ++i) {
+            Vr[i][r0] = V[i][r0].real();
+            Vr[i][r0 + 1] = V[i][r0].imag();
+          }
+        }
+      }
+      // Vri = Vr^{-1} (Gauss-Jordan, partial pivoting, long double)
+      if (okr) {
+        long double Aug[E][2 * E] = {};
+        for (int i = 0; i < ex; ++i) {
+          for (int k = 0; k < ex; ++k) Aug[i][k] = Vr[i][k];
+          Aug[i][ex + i] = 1.0L;
+        }
+        for (int col = 0; col < ex && okr; ++col) {
+          int pv = col;
+          for (int i = col + 1; i < ex; ++i)
+            if (std::fabs(Aug[i][col]) > std::fabs(Aug[pv][col])) pv = i;
+          if (Aug[pv][col] == 0.0L) {
+            okr = false;
+            break;
+          }
+          if (pv != col)
+            for (int k = 0; k < 2 * ex; ++k) std::swap(Aug[pv][k], Aug[col][k]);
+          const long double inv = 1.0L / Aug[col][col];
+          for (int k = 0; k < 2 * ex; ++k) Aug[col][k] *= inv;
+          for (int i = 0; i < ex; ++i) {
+            if (i == col || Aug[i][col] == 0.0L) continue;
+            const long double f = Aug[i][col];
+            for (int k = 0; k < 2 * ex; ++k) Aug[i][k] -= f * Aug[col][k];
+          }
+        }
+        for (int i = 0; i < ex; ++i)
+          for (int k = 0; k < ex; ++k) Vri[i][k] = Aug[i][ex + k];
+      }
+      long double nr = 0, nri = 0;
+      for (int i = 0; i < ex; ++i)
+        for (int k = 0; k < ex; ++k) {
+          nr += Vr[i][k] * Vr[i][k];
+          nri += Vri[i][k] * Vri[i][k];
+        }
+      const long double vcr = okr ? std::sqrt(nr * nri) / ex : 0.0L;
+      tm.vcond = okr && std::isfinite(static_cast<double>(vcr)) ? static_cast<float>(vcr)
+                                                               : std::numeric_limits<float>::infinity();
+      for (int i = 0; i < E; ++i) {
+        for (int k = 0; k < E; ++k) {
+          const bool in = i < ex && k < ex;
+          out[i * E + k] = in ? static_cast<double>(Vri[i][k]) : (i == k ? 1.0 : 0.0);
+          out[EE + i * E + k] = in ? static_cast<double>(Vr[i][k]) : (i == k ? 1.0 : 0.0);
+        }
+        out[2 * EE + i] = i < ex ? static_cast<double>(lam[i].real()) : 1.0;
+        out[2 * EE + E + i] = i < ex ? static_cast<double>(lam[i].imag()) : 0.0;
+      }
+      continue;
+    }
     for (int i = 0; i < E; ++i) {
       for (int k = 0; k < E; ++k) {
         const bool in = i < ex && k < ex;
@@ -578,7 +650,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         }
       }
       if (lt == 3) tile_eigvecs<8>(mt.tms, dh, pdvs[m], mt.vh);
-      else if (diag16) tile_eigvecs<16>(mt.tms, dh, pdvs[m], mt.vh);
+      else if (diag16) tile_eigvecs<16, true>(mt.tms, dh, pdvs[m], mt.vh);
       for (const auto& tm : mt.tms) mt.maxvc = std::max(mt.maxvc, tm.vcond);
     }
     return TSG_OK;
@@ -1060,6 +1132,10 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     const double nt = h[8] ? static_cast<double>(h[8]) : 1.0;
+    if (pl->use16)
+      std::fprintf(stderr, "[tsg prof16] tiles=%.0f cycles/tile (consumer 0): claim+geom %.0f first-box %.0f chunks %.0f flush %.0f diag %.0f scatter+rel %.0f | producer: flag waits %.0f ring waits+issue %.0f\n",
+                   nt, h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt, h[6] / nt, h[7] / nt);
+    else
     std::fprintf(stderr, "[tsg prof] tiles=%.0f cycles/tile: setup %.0f stage %.0f update(near) %.0f farwait|That+fwdT %.0f far|wave %.0f diag|backT %.0f scatter %.0f | idle/queue %.0f\n",
                  nt, h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt, h[6] / nt, h[7] / nt);
   }

@@ -29,7 +29,7 @@ struct alignas(16) TileMode {
 // lap3 diagonalised tiles: per tile index along a mode, V^{-1} (re, im),
 // V (re, im) as 8x8 row-major (identity-padded) and lambda (re, im).
 constexpr int kVhStride = 4 * 64 + 2 * 8;
-constexpr int kVhStride16 = 4 * 256 + 2 * 16;
+constexpr int kVhStride16 = 2 * 256 + 2 * 16;  // real block-diagonal basis (lap16)
 // A tile is diagonalised when the product of its three vcond values is at
 // most this (the eigenvector transforms then cost <= ~kDiagCond ulps).
 constexpr float kDiagCond = 1000.0f;

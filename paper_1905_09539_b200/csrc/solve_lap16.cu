@@ -10,11 +10,14 @@
 //     operand as 16x16x16 boxes of X (cp.async.bulk.tensor, 32 KB each)
 //     into a two-stage mbarrier ring, so the eight consumer warps only issue
 //     DMMA and shared-memory fragment loads (no register-bound load batches).
-// The base case is the diagonalised tile of solve_lap3.cu at E = 16:
-//   x^ = x x_0 V0^-1 x_1 V1^-1 x_2 V2^-1, x^ /= l0 + l1 + l2, x = x^ x_m V_m,
-// twenty real 16x16x256 DMMA GEMMs (the first and last real-only), using the
-// ring as the complex work tile.  Plans choose this kernel only when every
-// tile's eigenvector bases are well conditioned (tsg_plan: vcond product).
+// The base case block-diagonalises the tile over the reals: with V_m the real
+// eigenvector basis of the tile's diagonal Schur block (1x1 cells keep their
+// eigenvector, 2x2 cells take [Re v, Im v]),
+//   y = x x_0 V0^-1 x_1 V1^-1 x_2 V2^-1,  cell solves (<= 8 unknowns each,
+//   closed form, cell_solve16),  x = y x_m V_m:
+// six real 16x16x256 DMMA GEMMs, using the ring as the work tile.  Plans
+// choose this kernel only when every tile's bases are well conditioned
+// (tsg_plan: vcond product <= kDiagCond).
 // One CTA (8 consumer + 1 producer warps) per SM.
 // Reference: lap_rec / lap_base (laplace.hpp:99-153), mode_multiply update
 // (laplace.hpp:147), block_back_substitution (kernels.hpp:179-261).
@@ -61,6 +64,8 @@ struct G16 {
   int start[3], ext[3], tco[3];
   int nlo[3], flo[3];  // first rows of tiles t+1 and t+2 per mode (n_m when absent)
   int nch;             // chunks of this tile
+  int nc[3];           // Schur cells (1x1 / 2x2) of the tile's diagonal blocks
+  unsigned char cs[3][16], cz[3][16];
 };
 
 TSG_DEVINL void mbar_arrive(uint64_t* bar) {
@@ -218,6 +223,94 @@ TSG_DEVINL bool cmode16(const double* sr, const double* si, double* dr, double* 
   return sing;
 }
 
+// Block-diagonal Kronecker-sum solve of the transformed tile, in place: with
+// V_m^-1 D_m V_m = B_m (1x1 alpha, 2x2 [[alpha, beta], [-beta, alpha]]) the
+// system sum_m B_m x_m Y = R decouples into cells (one Schur cell per mode,
+// <= 8 unknowns); on a cell, the pair modes are diagonalised by the fixed
+// butterfly E = [[1, 1], [i, -i]] (eigenvalues alpha +- i beta), so
+//   y = Re( E (x) E (x) E  diag(1 / mu)  E^-1 (x) E^-1 (x) E^-1  r ),
+//   mu = sum_m alpha_m + i s_m beta_m.
+TSG_DEVINL bool cell_solve16(double* y, const G16& g, const double* vh, double tiny) {
+  const int nc0 = g.nc[0], nc1 = g.nc[1], nc2 = g.nc[2];
+  const int ncell = nc0 * nc1 * nc2;
+  bool sing = false;
+  for (int q = threadIdx.x; q < ncell; q += CW * 32) {
+    const int c[3] = {q % nc0, (q / nc0) % nc1, q / (nc0 * nc1)};
+    int r[3], z[3];
+    double al[3], be[3];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      r[m] = g.cs[m][c[m]];
+      z[m] = g.cz[m][c[m]];
+      al[m] = vh[m * VHS + 2 * EE + r[m]];
+      be[m] = z[m] == 2 ? vh[m * VHS + 2 * EE + E + r[m]] : 0.0;
+    }
+    const bool valid = r[0] < g.ext[0] && r[1] < g.ext[1] && r[2] < g.ext[2];
+    double zr[8], zi[8];
+#pragma unroll
+    for (int idx = 0; idx < 8; ++idx) {
+      const int a0 = idx & 1, a1 = (idx >> 1) & 1, a2 = idx >> 2;
+      const bool in = a0 < z[0] && a1 < z[1] && a2 < z[2];
+      zr[idx] = in ? y[(r[0] + a0) + S1 * (r[1] + a1) + S2 * (r[2] + a2)] : 0.0;
+      zi[idx] = 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      if (z[m] != 2) continue;
+      const int bit = 1 << m;
+#pragma unroll
+      for (int idx = 0; idx < 8; ++idx) {
+        if (idx & bit) continue;
+        const double ur = zr[idx], ui = zi[idx], vr = zr[idx | bit], vi = zi[idx | bit];
+        zr[idx] = 0.5 * (ur + vi);
+        zi[idx] = 0.5 * (ui - vr);
+        zr[idx | bit] = 0.5 * (ur - vi);
+        zi[idx | bit] = 0.5 * (ui + vr);
+      }
+    }
+#pragma unroll
+    for (int idx = 0; idx < 8; ++idx) {
+      double mr = 0.0, mi = 0.0;
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        mr += al[m];
+        mi += ((idx >> m) & 1) ? -be[m] : be[m];
+      }
+      const double den = mr * mr + mi * mi;
+      if (!(den > tiny * tiny)) {
+        if (valid) sing = true;
+        zr[idx] = zi[idx] = 0.0;
+      } else {
+        const double inv = 1.0 / den;
+        const double nr = (zr[idx] * mr + zi[idx] * mi) * inv;
+        zi[idx] = (zi[idx] * mr - zr[idx] * mi) * inv;
+        zr[idx] = nr;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      if (z[m] != 2) continue;
+      const int bit = 1 << m;
+#pragma unroll
+      for (int idx = 0; idx < 8; ++idx) {
+        if (idx & bit) continue;
+        const double ur = zr[idx], ui = zi[idx], vr = zr[idx | bit], vi = zi[idx | bit];
+        zr[idx] = ur + vr;            // u + v
+        zi[idx] = ui + vi;
+        zr[idx | bit] = vi - ui;      // i (u - v)
+        zi[idx | bit] = ur - vr;
+      }
+    }
+#pragma unroll
+    for (int idx = 0; idx < 8; ++idx) {
+      const int a0 = idx & 1, a1 = (idx >> 1) & 1, a2 = idx >> 2;
+      if (a0 < z[0] && a1 < z[1] && a2 < z[2])
+        y[(r[0] + a0) + S1 * (r[1] + a1) + S2 * (r[2] + a2)] = zr[idx];
+    }
+  }
+  return sing;
+}
+
 TSG_DEVINL void wait_tile(const SolveArgs& a, int64_t tile) {
   const int* f = a.flags + tile;
   unsigned ns = 32;
@@ -252,7 +345,20 @@ __global__ void __launch_bounds__(THREADS, 1)
   unsigned tphase = 0;  // tiles processed (bar_x / bar_v phases)
   const int64_t mul[3] = {1, a.ntiles_mode[0], static_cast<int64_t>(a.ntiles_mode[0]) * a.ntiles_mode[1]};
 
+  // optional per-phase cycle counters of consumer thread 0 (TSG_PROF):
+  // 0 claim+geometry, 1 first box wait, 2 update chunks, 3 flush, 4 diag,
+  // 5 scatter+release; producer thread: 6 flag waits, 7 ring waits
+  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tmark = clock64();
+  auto mark = [&](int k) {
+    if (a.prof) {
+      const long long t = clock64();
+      ph[k] += static_cast<unsigned long long>(t - tmark);
+      tmark = t;
+    }
+  };
   for (;; ++tphase) {
+    mark(5);
     if (tid == 0) s_tile = atomicAdd(a.counter, 1);
     __syncthreads();
     const int qi = s_tile;
@@ -264,6 +370,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       g.tco[tid] = tm;
       g.start[tid] = src.start;
       g.ext[tid] = src.ext;
+      g.nc[tid] = src.nc;
+      for (int k = 0; k < 16; ++k) {
+        g.cs[tid][k] = src.cs[k];
+        g.cz[tid][k] = src.cz[k];
+      }
       const int p = a.ntiles_mode[tid];
       g.nlo[tid] = tm + 1 < p ? a.bnd[tid][tm + 1] : a.dims[tid];
       g.flo[tid] = tm + 2 < p ? a.bnd[tid][tm + 2] : a.dims[tid];
@@ -299,8 +410,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           const Chunk ch = chunk_of(g, a.dims, c);
           const int m = ch.m % 3;
           if (ch.first) {  // far: tile t+2 along m; near: tile t+1
+            mark(7);
             wait_tile(a, g.lt + (ch.m < 3 ? 2 : 1) * mul[m]);
             fence_proxy_async();
+            mark(6);
           }
           const int s = gch % NST;
           if (gch >= NST) mbar_wait(empty + s, ((gch / NST) - 1) & 1);
@@ -322,6 +435,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int rb = 0; rb < 2; ++rb)
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb) acc[m][rb][cb][0] = acc[m][rb][cb][1] = 0.0;
+      mark(0);
       double af[4][2], an[4][2];
       Chunk ch = chunk_of(g, a.dims, 0);
       if (nch > 0) chunk_afrag(a, g, ch.m % 3, ch.k, ch.kh, af);
@@ -330,6 +444,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (c + 1 < nch) chunk_afrag(a, g, cn.m % 3, cn.k, cn.kh, an);  // next chunk's A, in flight
         const int s = gch % NST;
         mbar_wait(full + s, (gch / NST) & 1);
+        if (c == 0) mark(1);
         const int m = ch.m % 3;
         const double* box = (s < NSR ? ring + s * TD : xi) + ((m == 0 ? ch.k : g.start[0]) & 1);
         if (m == 0) chunk_dmma<0>(box, af, acc[0]);
@@ -341,6 +456,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int ks = 0; ks < 4; ++ks) af[ks][0] = an[ks][0], af[ks][1] = an[ks][1];
         ch = cn;
       }
+      mark(2);
       if (!(a.dbg & 32768)) mbar_wait(&bar_x, tphase & 1);  // B~ tile landed
       double* xo = xr + (g.start[0] & 1);  // the B~ box starts at an even row
       flush16<0>(xo, acc[0]);
@@ -350,30 +466,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       flush16<2>(xo, acc[2]);
       consumers_sync();
       // ---- diagonalised base case (ring = complex work tile) ----
+      mark(3);
       if (!(a.dbg & 16384)) mbar_wait(&bar_v, tphase & 1);
       if (a.dbg & 2048) goto scatter16;
       {
-      double* yr = ring;
-      double* yi = ring + TD;
+      // ---- real block-diagonalised base case (ring = work tile) ----
+      double* y = ring;
       const int* ex = g.ext;
-      constexpr int RE = 0, IM = EE, VR = 2 * EE, VI = 3 * EE;
-      bool sing = false;
-      cmode16<0, false, true, false>(xo, nullptr, yr, yi, vh + RE, vh + IM, vh, ex, a.tiny);
+      constexpr int VRI = 0, VRR = EE;
+      cmode16<0, false, false, false>(xo, nullptr, y, nullptr, vh + VRI, vh + VRI, vh, ex, a.tiny);
       consumers_sync();
-      cmode16<1, true, true, false>(yr, yi, xr, xi, vh + VHS + RE, vh + VHS + IM, vh, ex, a.tiny);
+      cmode16<1, false, false, false>(y, nullptr, xr, nullptr, vh + VHS + VRI, vh + VHS + VRI, vh, ex, a.tiny);
       consumers_sync();
-      sing |= cmode16<2, true, true, true>(xr, xi, yr, yi, vh + 2 * VHS + RE, vh + 2 * VHS + IM, vh, ex,
-                                           a.tiny);
+      cmode16<2, false, false, false>(xr, nullptr, y, nullptr, vh + 2 * VHS + VRI, vh + 2 * VHS + VRI, vh, ex,
+                                      a.tiny);
       consumers_sync();
-      cmode16<2, true, true, false>(yr, yi, xr, xi, vh + 2 * VHS + VR, vh + 2 * VHS + VI, vh, ex, a.tiny);
+      const bool sing = cell_solve16(y, g, vh, a.tiny);
       consumers_sync();
-      cmode16<1, true, true, false>(xr, xi, yr, yi, vh + VHS + VR, vh + VHS + VI, vh, ex, a.tiny);
+      cmode16<0, false, false, false>(y, nullptr, xr, nullptr, vh + VRR, vh + VRR, vh, ex, a.tiny);
       consumers_sync();
-      cmode16<0, true, false, false>(yr, yi, xr, nullptr, vh + VR, vh + VI, vh, ex, a.tiny);
+      cmode16<1, false, false, false>(xr, nullptr, y, nullptr, vh + VHS + VRR, vh + VHS + VRR, vh, ex, a.tiny);
+      consumers_sync();
+      cmode16<2, false, false, false>(y, nullptr, xr, nullptr, vh + 2 * VHS + VRR, vh + 2 * VHS + VRR, vh, ex,
+                                      a.tiny);
       if (sing) atomicMin(a.status, static_cast<int>(g.lt < 0x7f7f7f7e ? g.lt : 0x7f7f7f7e));
       consumers_sync();
       }
     scatter16:
+      mark(4);
       // ---- scatter X_t, release ----
       const int e0 = g.ext[0], e1 = g.ext[1], e2 = g.ext[2];
       for (int l = tid; l < TT; l += CW * 32) {
@@ -387,6 +507,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         st_release(a.flags + g.lt, a.epoch);
       }
     }
+  }
+  if (a.prof && (tid == 0 || tid == CW * 32)) {
+    for (int k = 0; k < 8; ++k) atomicAdd(a.prof + k, ph[k]);
+    if (tid == 0) atomicAdd(a.prof + 8, static_cast<unsigned long long>(tphase));
   }
 }
 
