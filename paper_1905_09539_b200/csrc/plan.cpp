@@ -613,7 +613,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       tmd.nc = static_cast<unsigned char>(nc);
       tmd.far_lo = t + 3 < ntm ? mt.bd[t + 3] : dims[m];
     }
-    if (pl->fast == 3) {
+    if (pl->fast == 3 || pl->fast == 5) {
       // Eigenbasis diagonal block of every tile index along mode m:
       // That[i][j] = sum Pinv_blk(i)[i,a] T[a,b] P_blk(j)[b,j] for j beyond
       // i's cell (0 elsewhere), then lambda_i; layout of solve_lap3 (DHS).
@@ -673,7 +673,31 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       pl->lt3 = 4;
     }
   }
-  if (!pl->use16) {
+  // order >= 4 Laplace: the diagonalised small-tile kernel when its padded
+  // tiles fit (<= 512 unknowns) and every tile's bases are well conditioned
+  const char* ed = std::getenv("TSG_LAPD");
+  if (!pl->use16 && pl->fast == 1 && d >= 4 && (ed ? std::atoi(ed) != 0 : true)) {
+    pl->fast = 5;
+    pl->tile_ext = choose_tiles(family, pl->dims, o, tsg::solve_lapd_caps());
+    double prod = 1.0;
+    int lsum = 0;
+    pl->tlog.assign(d, 0);
+    pl->tsh.assign(d, 0);
+    for (int m = 0; m < d; ++m) {
+      const int rc = build_mode(m, 3, false);
+      if (rc != TSG_OK) return rc;
+      prod *= mts[m].maxvc;
+      int mx = 1;
+      for (const auto& tm : mts[m].tms) mx = std::max(mx, static_cast<int>(tm.ext));
+      int lg = 0;
+      while ((1 << lg) < mx) ++lg;
+      pl->tsh[m] = lsum;
+      pl->tlog[m] = lg;
+      lsum += lg;
+    }
+    if (!(prod <= tsg::kDiagCond) || lsum > 9) pl->fast = 1;
+  }
+  if (!pl->use16 && pl->fast != 5) {
     pl->tile_ext = choose_tiles(family, pl->dims, o,
                                 pl->fast == 3 ? tsg::solve_lap3_caps(pl->lt3)
                                               : (pl->fast ? tsg::solve_lap_caps(d) : tsg::solve_caps(family, d)));
@@ -1019,6 +1043,10 @@ void fill_solve_args(const tsg_plan* pl, double* work, tsg::SolveArgs& a) {
   a.ocoord = pl->ocoord;
   a.tiny = pl->tiny;
   a.refine = pl->refine;
+  for (size_t m = 0; m < pl->tlog.size(); ++m) {
+    a.tlog[m] = pl->tlog[m];
+    a.tsh[m] = pl->tsh[m];
+  }
   // one slab: the whole tensor
   a.nslab = 1;
   a.sys = 0;
@@ -1029,6 +1057,7 @@ void fill_solve_args(const tsg_plan* pl, double* work, tsg::SolveArgs& a) {
 
 cudaError_t launch_plan_solve(tsg_plan* pl, const tsg::SolveArgs& a, cudaStream_t st) {
   if (pl->use16) return tsg::launch_solve_lap16(a, st, &pl->solve_info);
+  if (pl->fast == 5) return tsg::launch_solve_lapd(a, st, &pl->solve_info);
   if (pl->fast == 3) return tsg::launch_solve_lap3(pl->lt3, a, st, &pl->solve_info);
   if (pl->fast) return tsg::launch_solve_lap(a, st, &pl->solve_info);
   return tsg::launch_solve(a, st, &pl->solve_info);

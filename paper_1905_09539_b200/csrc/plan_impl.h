@@ -51,6 +51,7 @@ struct tsg_plan {
   int fast = 0;  // 1: solve_lap_kernel, 3: solve_lap3_kernel (Laplace, good eigenbases)
   int lt3 = 3;   // log2 tile extent of solve_lap3
   bool use16 = false;  // 16^3 TMA kernel (solve_lap16.cu)
+  std::vector<int> tlog, tsh;  // solve_lapd padded tile layout
   int* flags = nullptr;
   int* counter = nullptr;   // [0] = queue head, [1] = status
   int64_t ntiles = 0;

@@ -70,6 +70,8 @@ struct SolveArgs {
   // Element offset(i) of the global tensor lives at xs[q] + offset(i) for
   // the slab q = slab_of(i_{d-1}); xs[q] are virtual bases (slab pointer
   // minus slo[q] * stride[d-1]), peer-mapped on multi-GPU runs.
+  int tlog[kMaxOrder];          // solve_lapd: log2 padded tile extent per mode
+  int tsh[kMaxOrder];           // solve_lapd: bit offset of mode m in the tile index
   int nslab;
   int sys;                      // 1: flags and tiles shared across GPUs (system scope)
   int slo[kMaxSlabs + 1];       // slab row bounds along mode d-1 (tile-aligned)
@@ -98,6 +100,11 @@ cudaError_t launch_solve_lap3(int lt, const SolveArgs& a, cudaStream_t st, Solve
 // (solve_lap16.cu; plans whose tiles are all diagonalisable).
 TileCaps solve_lap16_caps();
 cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
+
+// Higher-order Laplace (solve_lapd.cu, d = 4..6): small padded tiles,
+// DMMA updates, diagonalised base case.
+TileCaps solve_lapd_caps();
+cudaError_t launch_solve_lapd(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
 
 // Fast Laplace path (solve_lap.cu): small tiles, eigenbasis base cells.
 TileCaps solve_lap_caps(int d);

@@ -1,0 +1,327 @@
+// Higher-order Laplace-like solve (d = 4..6, e.g. C3 = 24^6): the dataflow
+// of solve_lap3.cu on small d-dimensional tiles (padded extents 2/4/8,
+// at most 512 unknowns), four CTAs of 128 threads per SM.
+//
+// Per tile:
+//   1. gather B~_t (cp.async, padded power-of-two layout) and the complex
+//      eigenvector bases of its d diagonal Schur blocks (host tables, the
+//      same 8x8 identity-padded V^-1 | V | lambda records as solve_lap3);
+//   2. left-looking updates in two passes (tiles >= t+2 first, then the t+1
+//      neighbours after their flags): for every mode the tile's cross-section
+//      is split over the warps in 8-column blocks and
+//        Y(cross, rows) -= X(cross, k) T_m(rows, k)^T
+//      runs on DMMA with X as the A operand (so a small tile extent e_m only
+//      pads the N side of the 8x8x4 product; each X element is loaded once);
+//   3. diagonalised base case: x^ = x x_m V_m^-1 (all modes), divide by
+//      sum_m lambda_m, x = x^ x_m V_m, one thread per fibre (P_m <= 8);
+//   4. scatter, release.
+// Reference: lap_rec / lap_base (laplace.hpp:99-153), the merged-mode base
+// case laplace_merged (laplace.hpp:202-244), mode_multiply (laplace.hpp:147).
+#include <cstdint>
+
+#include "common.cuh"
+#include "solve.h"
+
+namespace tsg {
+namespace {
+
+constexpr int THREADS = 128, WARPS = 4, EP = 512;
+constexpr int VHS = kVhStride;  // 8x8 complex records (tile_eigvecs<8>)
+constexpr int NBMAX = EP / 2 / 8 / WARPS;  // 8-column blocks per warp, P_m >= 2
+
+template <int D>
+struct GD {
+  int64_t lt, gbase;
+  int start[D], ext[D], tco[D];
+};
+
+TSG_DEVINL void waitp(const SolveArgs& a, int64_t tile) {
+  const int* f = a.flags + tile;
+  unsigned ns = 32;
+  while (ld_acquire(f) < a.epoch) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
+
+// cross-section column n of mode m -> tile-local offset (mode m row 0) and
+// the clamped global offset of its fibre start (without mode m's start)
+template <int D>
+TSG_DEVINL void cross_of(const SolveArgs& a, const GD<D>& g, int m, int n, int& lt, int64_t& go) {
+  lt = 0;
+  go = 0;
+  int rem = n;
+#pragma unroll
+  for (int v = 0; v < D; ++v) {
+    if (v == m) continue;
+    const int lp = a.tlog[v];
+    const int iv = rem & ((1 << lp) - 1);
+    rem >>= lp;
+    lt += iv << a.tsh[v];
+    const int ic = iv < g.ext[v] ? iv : g.ext[v] - 1;
+    go += static_cast<int64_t>(g.start[v] + ic) * a.stride[v];
+  }
+}
+
+// xr -= sum_k X(cross, k) T_m(rows, k) over rows k in [klo, khi) of mode m
+// (cross-section of ep >> log2 P_m columns, 8-column blocks dealt to the
+// warps, NBMAX blocks per warp and round)
+template <int D>
+TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int ep, int m, int klo, int khi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int lpm = a.tlog[m], shm = a.tsh[m];
+  const int cross = ep >> lpm;
+  const int nblk = (cross + 7) >> 3;
+  const int nm = a.dims[m];
+  const int64_t sm = a.stride[m];
+  const double* Tm = a.T[m];
+  const int row = g.start[m] + gq;  // B fragment: T_m[row][k], rows beyond the tile give 0
+  const bool rok = gq < g.ext[m];
+  for (int base = warp; base < nblk; base += WARPS * NBMAX) {
+    int ltc[NBMAX];
+    int64_t goc[NBMAX];
+    bool cok[NBMAX];
+    double acc[NBMAX][2];
+#pragma unroll
+    for (int j = 0; j < NBMAX; ++j) {
+      const int b = base + WARPS * j;
+      acc[j][0] = acc[j][1] = 0.0;
+      ltc[j] = 0;
+      goc[j] = 0;
+      cok[j] = b < nblk && 8 * b + gq < cross;
+      if (cok[j]) cross_of<D>(a, g, m, 8 * b + gq, ltc[j], goc[j]);
+    }
+    for (int k0 = klo; k0 < khi; k0 += 4) {
+      const int k = k0 + tq;
+      const bool kok = k < khi;
+      const double bt = (kok && rok) ? __ldg(Tm + row + static_cast<int64_t>(k) * nm) : 0.0;
+      double av[NBMAX];
+#pragma unroll
+      for (int j = 0; j < NBMAX; ++j)
+        av[j] = (cok[j] && kok) ? ld_cg(a.X + goc[j] + static_cast<int64_t>(k) * sm) : 0.0;
+#pragma unroll
+      for (int j = 0; j < NBMAX; ++j)
+        if (base + WARPS * j < nblk) dmma(acc[j][0], acc[j][1], av[j], bt);
+    }
+    // C[g][2t+h]: cross column 8b + g, row 2t + h of mode m
+#pragma unroll
+    for (int j = 0; j < NBMAX; ++j) {
+      if (!cok[j]) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 2 * tq + h;
+        if (r < (1 << lpm)) xr[ltc[j] + (r << shm)] -= acc[j][h];
+      }
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
+  __shared__ __align__(16) double xr[EP];
+  __shared__ __align__(16) double xi[EP];
+  __shared__ __align__(16) double vh[D * VHS];
+  __shared__ GD<D> g;
+  __shared__ int s_tile;
+  const int tid = threadIdx.x;
+  int ep = 1;
+#pragma unroll
+  for (int m = 0; m < D; ++m) ep <<= a.tlog[m];
+
+  for (;;) {
+    if (tid == 0) s_tile = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int qi = s_tile;
+    if (qi >= a.ntiles) break;
+    if (tid < D) {
+      const unsigned long long pk = a.ocoord[qi];
+      const int tm = static_cast<int>((pk >> (10 * tid)) & 1023);
+      const TileMode& src = a.tmode[tid][tm];
+      g.tco[tid] = tm;
+      g.start[tid] = src.start;
+      g.ext[tid] = src.ext;
+      if (tid == 0) g.lt = a.order[qi];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int64_t gb = 0;
+      for (int m = 0; m < D; ++m) gb += static_cast<int64_t>(g.start[m]) * a.stride[m];
+      g.gbase = gb;
+    }
+    __syncthreads();
+
+    // ---- gather B~_t and the eigenvector bases ----
+    for (int l = tid; l < ep; l += THREADS) {
+      int64_t off = g.gbase;
+      bool ok = true;
+#pragma unroll
+      for (int v = 0; v < D; ++v) {
+        const int iv = (l >> a.tsh[v]) & ((1 << a.tlog[v]) - 1);
+        ok &= iv < g.ext[v];
+        off += static_cast<int64_t>(iv) * a.stride[v];
+      }
+      cp_async8(xr + l, ok ? a.X + off : a.X, ok ? 8 : 0);
+      xi[l] = 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+      const double* src = a.vhat[m] + static_cast<int64_t>(g.tco[m]) * VHS;
+      for (int e = 2 * tid; e < VHS; e += 2 * THREADS) cp_async16(vh + m * VHS + e, src + e, 16);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+
+    // ---- left-looking updates: far (tiles >= t+2), then near (t+1) ----
+    int64_t mul = 1;
+    int64_t muls[D];
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+      muls[m] = mul;
+      mul *= a.ntiles_mode[m];
+    }
+    for (int part = 0; part < 2 && !(a.dbg & 4); ++part) {
+      if (tid == 0) {
+        for (int m = 0; m < D; ++m) {
+          const int tm = g.tco[m], d0 = part == 0 ? 2 : 1;
+          if (tm + d0 < a.ntiles_mode[m]) waitp(a, g.lt + d0 * muls[m]);
+        }
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int m = 0; m < D; ++m) {
+        const int tm = g.tco[m], p = a.ntiles_mode[m];
+        int klo, khi;
+        if (part == 0) {
+          klo = tm + 2 < p ? a.bnd[m][tm + 2] : 0;
+          khi = tm + 2 < p ? a.dims[m] : 0;
+        } else {
+          klo = tm + 1 < p ? a.bnd[m][tm + 1] : 0;
+          khi = tm + 1 < p ? (tm + 2 < p ? a.bnd[m][tm + 2] : a.dims[m]) : 0;
+        }
+        if (khi > klo) update_mode<D>(a, g, xr, ep, m, klo, khi);
+        __syncthreads();
+      }
+    }
+
+    // ---- diagonalised base case (complex, one thread per fibre) ----
+    for (int pass = 0; pass < 2; ++pass) {  // 0: x V^-1 on every mode, 1: x V
+#pragma unroll 1
+      for (int m = 0; m < D; ++m) {
+        const int lpm = a.tlog[m], pm = 1 << lpm, shm = a.tsh[m];
+        const double* Vr = vh + m * VHS + (pass == 0 ? 0 : 128);
+        const double* Vi = Vr + 64;
+        for (int f = tid; f < (ep >> lpm); f += THREADS) {
+          int lt0;
+          int64_t dummy;
+          cross_of<D>(a, g, m, f, lt0, dummy);
+          double zr[8], zi[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+            if (r < pm) {
+              zr[r] = xr[lt0 + (r << shm)];
+              zi[r] = xi[lt0 + (r << shm)];
+            }
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            if (r >= pm) continue;
+            double sr = 0.0, si = 0.0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              if (c >= pm) continue;
+              const double ar = Vr[8 * r + c], ai = Vi[8 * r + c];
+              sr = fma(ar, zr[c], fma(-ai, zi[c], sr));
+              si = fma(ar, zi[c], fma(ai, zr[c], si));
+            }
+            xr[lt0 + (r << shm)] = sr;
+            xi[lt0 + (r << shm)] = si;
+          }
+        }
+        __syncthreads();
+      }
+      if (pass == 0) {
+        bool sing = false;
+        for (int l = tid; l < ep; l += THREADS) {
+          double mr = 0.0, mi = 0.0;
+          bool valid = true;
+#pragma unroll
+          for (int v = 0; v < D; ++v) {
+            const int iv = (l >> a.tsh[v]) & ((1 << a.tlog[v]) - 1);
+            valid &= iv < g.ext[v];
+            mr += vh[v * VHS + 256 + iv];
+            mi += vh[v * VHS + 264 + iv];
+          }
+          const double den = mr * mr + mi * mi;
+          if (!(den > a.tiny * a.tiny)) {
+            if (valid) sing = true;
+            xr[l] = xi[l] = 0.0;
+          } else {
+            const double inv = 1.0 / den, pr = xr[l], pi = xi[l];
+            xr[l] = (pr * mr + pi * mi) * inv;
+            xi[l] = (pi * mr - pr * mi) * inv;
+          }
+        }
+        if (sing) atomicMin(a.status, static_cast<int>(g.lt < 0x7f7f7f7e ? g.lt : 0x7f7f7f7e));
+        __syncthreads();
+      }
+    }
+
+    // ---- scatter X_t (real part), release ----
+    for (int l = tid; l < ep; l += THREADS) {
+      int64_t off = g.gbase;
+      bool ok = true;
+#pragma unroll
+      for (int v = 0; v < D; ++v) {
+        const int iv = (l >> a.tsh[v]) & ((1 << a.tlog[v]) - 1);
+        ok &= iv < g.ext[v];
+        off += static_cast<int64_t>(iv) * a.stride[v];
+      }
+      if (ok) a.X[off] = xr[l];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(a.flags + g.lt, a.epoch);
+    }
+  }
+}
+
+template <int D>
+cudaError_t launch_d(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
+  static int nsm = 0, occ = 0;
+  auto k = solve_lapd_kernel<D>;
+  if (occ == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, THREADS, 0);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  int64_t grid = static_cast<int64_t>(nsm) * occ;
+  if (grid > a.ntiles) grid = a.ntiles;
+  if (info) *info = SolveLaunchInfo{static_cast<int>(grid), THREADS, 0, occ};
+  k<<<static_cast<unsigned>(grid), THREADS, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+TileCaps solve_lapd_caps() { return TileCaps{8, EP, EP / 2}; }
+
+cudaError_t launch_solve_lapd(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
+  if (a.ntiles <= 0) return cudaSuccess;
+  switch (a.d) {
+    case 4:
+      return launch_d<4>(a, st, info);
+    case 5:
+      return launch_d<5>(a, st, info);
+    case 6:
+      return launch_d<6>(a, st, info);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace tsg
