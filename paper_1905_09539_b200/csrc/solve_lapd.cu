@@ -128,8 +128,21 @@ __global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
   int ep = 1;
 #pragma unroll
   for (int m = 0; m < D; ++m) ep <<= a.tlog[m];
+  // optional cycle counters (TSG_PROF): 0 claim+geometry, 1 gather, 2 far
+  // updates, 3 near updates (incl. flag waits), 4 base case, 5 scatter
+  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tmark = clock64();
+  auto mark = [&](int k) {
+    if (a.prof) {
+      const long long t = clock64();
+      ph[k] += static_cast<unsigned long long>(t - tmark);
+      tmark = t;
+    }
+  };
+  int ntl = 0;
 
-  for (;;) {
+  for (;; ++ntl) {
+    mark(5);
     if (tid == 0) s_tile = atomicAdd(a.counter, 1);
     __syncthreads();
     const int qi = s_tile;
@@ -151,6 +164,7 @@ __global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
     }
     __syncthreads();
 
+    mark(0);
     // ---- gather B~_t and the eigenvector bases ----
     for (int l = tid; l < ep; l += THREADS) {
       int64_t off = g.gbase;
@@ -172,6 +186,7 @@ __global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
+    mark(1);
 
     // ---- left-looking updates: far (tiles >= t+2), then near (t+1) ----
     int64_t mul = 1;
@@ -203,6 +218,7 @@ __global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
         if (khi > klo) update_mode<D>(a, g, xr, ep, m, klo, khi);
         __syncthreads();
       }
+      mark(2 + part);
     }
 
     // ---- diagonalised base case (complex, one thread per fibre) ----
@@ -267,6 +283,7 @@ __global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
       }
     }
 
+    mark(4);
     // ---- scatter X_t (real part), release ----
     for (int l = tid; l < ep; l += THREADS) {
       int64_t off = g.gbase;
@@ -284,6 +301,10 @@ __global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
       __threadfence();
       st_release(a.flags + g.lt, a.epoch);
     }
+  }
+  if (a.prof && tid == 0) {
+    for (int k = 0; k < 8; ++k) atomicAdd(a.prof + k, ph[k]);
+    atomicAdd(a.prof + 8, static_cast<unsigned long long>(ntl));
   }
 }
 
