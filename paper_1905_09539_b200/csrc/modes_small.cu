@@ -1,0 +1,173 @@
+// Fused transforms of small modes (n <= 48): Y = X x_a A x_b B for two
+// consecutive modes a, b = a + 1 (or one mode, B = null) in ONE pass over
+// HBM.  For C3 (24^6) the per-mode DGEMM is HBM-bound at n/8 = 3 FLOP/B with
+// badly padded 64-wide tiles; pairing the modes halves the passes and the
+// per-fibre products run from shared memory.
+//
+// Block = (c inner indices) x (n_a x n_b group) x (o outer indices), staged
+// in shared memory in that order (inner fastest): c consecutive indices of
+// the contiguous prefix (modes < a) when a > 0, else o consecutive indices
+// of the suffix (modes > b), so every block is a few contiguous runs.  Each
+// thread owns whole fibres along the mode being applied (in place, the
+// fibre lives in registers), with the n x n matrices in shared memory.
+// Reference: mode_multiply (tensor.hpp:187-231) at laplace.hpp:282/297.
+#include <cstdint>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace tsg {
+namespace {
+
+constexpr int THREADS = 256;
+
+struct PairArgs {
+  const double* X;
+  double* Y;
+  const double* A;  // n_a x n_a, column-major (Y = X x_a A: y_i = sum_k A(i,k) x_k)
+  const double* B;  // n_b x n_b or null
+  int na, nb;       // nb = 1 when B is null
+  int c, o;         // block inner / outer extents
+  int64_t P, Q;     // prefix (modes < a) and suffix (modes > b) sizes
+  int64_t nblk;     // blocks
+  int bsz;          // doubles per block = c * na * nb * o
+};
+
+// y[f, i] = sum_k M(i, k) x[f, k] for the fibres of the block along a
+// coordinate of extent N and stride st (in the block): fibre index f
+// enumerates (lo < st) x (hi) with element offset lo + st * (k + N * hi).
+template <int N>
+TSG_DEVINL void fibres(double* blk, const double* M, int st, int nf) {
+  for (int f = threadIdx.x; f < nf; f += THREADS) {
+    const int lo = f % st, hi = f / st;
+    double* p = blk + lo + static_cast<int64_t>(st) * N * hi;
+    double x[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) x[k] = p[st * k];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < N; ++k) s = fma(M[i + N * k], x[k], s);
+      p[st * i] = s;
+    }
+  }
+}
+
+template <int NA, int NB>
+__global__ void __launch_bounds__(THREADS) pair_kernel(PairArgs g) {
+  extern __shared__ __align__(16) double sm[];
+  double* ma = sm;
+  double* mb = sm + NA * NA;
+  double* blk = mb + (NB > 1 ? NB * NB : 0);
+  for (int e = threadIdx.x; e < NA * NA; e += THREADS) ma[e] = g.A[e];
+  if (NB > 1)
+    for (int e = threadIdx.x; e < NB * NB; e += THREADS) mb[e] = g.B[e];
+  const int c = g.c, o = g.o;
+  const int grp = NA * NB;
+  for (int64_t bk = blockIdx.x; bk < g.nblk; bk += gridDim.x) {
+    // block bk -> (prefix chunk pc, suffix chunk sc)
+    const int64_t npc = g.P / c;
+    const int64_t pc = bk % npc, sc = bk / npc;
+    const int64_t base = pc * c + sc * static_cast<int64_t>(o) * g.P * grp;
+    __syncthreads();  // previous block written back
+    // gather: element (ic, gi, io) at base + ic + P * (gi + grp * io)
+    for (int e = threadIdx.x; e < g.bsz; e += THREADS) {
+      const int ic = e % c, rest = e / c;
+      const int gi = rest % grp, io = rest / grp;
+      blk[e] = g.X[base + ic + g.P * (gi + static_cast<int64_t>(grp) * io)];
+    }
+    __syncthreads();
+    fibres<NA>(blk, ma, c, g.bsz / NA);  // mode a: stride c in the block
+    if (NB > 1) {
+      __syncthreads();
+      fibres<NB>(blk, mb, c * NA, g.bsz / NB);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < g.bsz; e += THREADS) {
+      const int ic = e % c, rest = e / c;
+      const int gi = rest % grp, io = rest / grp;
+      g.Y[base + ic + g.P * (gi + static_cast<int64_t>(grp) * io)] = blk[e];
+    }
+  }
+}
+
+template <int NA, int NB>
+cudaError_t launch_pair(const PairArgs& g, cudaStream_t st) {
+  const int smem = (NA * NA + (NB > 1 ? NB * NB : 0) + g.bsz) * 8;
+  auto k = pair_kernel<NA, NB>;
+  static int nsm = 0, occ = 0, last_smem = -1;
+  if (last_smem != smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, THREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    last_smem = smem;
+  }
+  int64_t grid = static_cast<int64_t>(nsm) * occ;
+  if (grid > g.nblk) grid = g.nblk;
+  k<<<static_cast<unsigned>(grid), THREADS, smem, st>>>(g);
+  return cudaGetLastError();
+}
+
+template <int NA>
+cudaError_t dispatch_b(const PairArgs& g, cudaStream_t st) {
+  switch (g.nb) {
+    case 1: return launch_pair<NA, 1>(g, st);
+    case 16: return launch_pair<NA, 16>(g, st);
+    case 24: return launch_pair<NA, 24>(g, st);
+    case 32: return launch_pair<NA, 32>(g, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+bool small_mode_ok(int n) { return n == 16 || n == 24 || n == 32; }
+
+cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, int a, bool pair,
+                            const double* A, const double* B, cudaStream_t st, double* flops) {
+  const int b = pair ? a + 1 : a;
+  if (a < 0 || b >= d || !small_mode_ok(dims[a]) || (pair && !small_mode_ok(dims[b])))
+    return cudaErrorInvalidValue;
+  PairArgs g{};
+  g.X = X;
+  g.Y = Y;
+  g.A = A;
+  g.B = pair ? B : nullptr;
+  g.na = dims[a];
+  g.nb = pair ? dims[b] : 1;
+  g.P = 1;
+  g.Q = 1;
+  for (int v = 0; v < a; ++v) g.P *= dims[v];
+  for (int v = b + 1; v < d; ++v) g.Q *= dims[v];
+  const int grp = g.na * g.nb;
+  // ~8-9K doubles per block: inner chunk from the prefix, else outer batch
+  const int target = 9216;
+  g.c = 1;
+  g.o = 1;
+  if (g.P > 1) {
+    int c = 1;
+    while (c * 2 * grp <= target && g.P % (c * 2) == 0) c *= 2;
+    g.c = c;
+  } else {
+    int o = 1;
+    while (o * 2 * grp <= target && g.Q % (o * 2) == 0) o *= 2;
+    g.o = o;
+  }
+  g.bsz = g.c * grp * g.o;
+  g.nblk = (g.P / g.c) * (g.Q / g.o);
+  if (flops) *flops += 2.0 * static_cast<double>(g.P) * g.Q * grp * (g.na + g.nb - (pair ? 0 : 1));
+  switch (g.na) {
+    case 16: return dispatch_b<16>(g, st);
+    case 24: return dispatch_b<24>(g, st);
+    case 32: return dispatch_b<32>(g, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace tsg

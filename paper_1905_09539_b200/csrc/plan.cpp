@@ -1065,6 +1065,52 @@ cudaError_t launch_plan_solve(tsg_plan* pl, const tsg::SolveArgs& a, cudaStream_
 
 }  // namespace tsg_impl
 
+// All-mode transform in -> target (ping-pong through `other`): per-mode DMMA
+// GEMMs, except consecutive small modes (n in {16, 24, 32}), which go
+// through the fused shared-memory pass two at a time (modes_small.cu).
+cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double* other, bool fwd,
+                          cudaStream_t st) {
+  const int d = pl->d;
+  struct Pass {
+    int m;
+    int kind;  // 0 GEMM, 1 small single, 2 small pair
+  };
+  std::vector<Pass> ps;
+  static const bool small_on = [] {
+    const char* e = std::getenv("TSG_SMALLMODES");
+    return !e || std::atoi(e) != 0;
+  }();
+  for (int m = 0; m < d;) {
+    const bool sm = small_on && tsg::small_mode_ok(pl->dims[m]);
+    if (sm && m + 1 < d && tsg::small_mode_ok(pl->dims[m + 1])) {
+      ps.push_back({m, 2});
+      m += 2;
+    } else {
+      ps.push_back({m, sm ? 1 : 0});
+      m += 1;
+    }
+  }
+  const int k = static_cast<int>(ps.size());
+  const double* src = in;
+  for (int i = 0; i < k; ++i) {
+    double* dst = ((k - 1 - i) % 2 == 0) ? target : other;
+    const int m = ps[i].m;
+    const double* A = fwd ? pl->Fwd[m].p : pl->Bwd[m].p;
+    const double* At = fwd ? pl->FwdT[m].p : pl->BwdT[m].p;
+    cudaError_t e;
+    if (ps[i].kind == 0) {
+      e = tsg::mode_product(src, dst, d, pl->dims.data(), m, A, At, pl->dims[m], 1.0, 0.0, st);
+    } else {
+      const double* B = ps[i].kind == 2 ? (fwd ? pl->Fwd[m + 1].p : pl->Bwd[m + 1].p) : nullptr;
+      e = tsg::mode_pair_small(src, dst, d, pl->dims.data(), m, ps[i].kind == 2, A, B, st);
+    }
+    if (e != cudaSuccess) return e;
+    ++pl->launches;
+    src = dst;
+  }
+  return cudaSuccess;
+}
+
 namespace {
 
 // Enqueue the whole pipeline on `st` (fwd transforms, solve, back transforms).
@@ -1076,14 +1122,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   double* work = nullptr;
   // Forward transforms: outputs alternate w2/w1 and end in w1.
   if (!pl->reduced_only) {
-    const double* src = in;
-    for (int m = 0; m < d; ++m) {
-      double* dst = ((d - 1 - m) % 2 == 0) ? pl->w1.p : pl->w2.p;
-      TSG_CU(tsg::mode_product(src, dst, d, pl->dims.data(), m, pl->Fwd[m].p, pl->FwdT[m].p,
-                               pl->dims[m], 1.0, 0.0, st));
-      ++pl->launches;
-      src = dst;
-    }
+    TSG_CU(transform_all(pl, in, pl->w1.p, pl->w2.p, true, st));
     work = pl->w1.p;
   } else {
     work = out;
@@ -1178,16 +1217,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
                  pl->max_cond);
   if (timing) TSG_CU(cudaEventRecord(ev[3], st));
   // Back transforms: outputs alternate (w2, out) and end in `out`.
-  if (!pl->reduced_only) {
-    const double* src = work;
-    for (int m = 0; m < d; ++m) {
-      double* dst = ((d - 1 - m) % 2 == 0) ? out : pl->w2.p;
-      TSG_CU(tsg::mode_product(src, dst, d, pl->dims.data(), m, pl->Bwd[m].p, pl->BwdT[m].p,
-                               pl->dims[m], 1.0, 0.0, st));
-      ++pl->launches;
-      src = dst;
-    }
-  }
+  if (!pl->reduced_only) TSG_CU(transform_all(pl, work, out, pl->w2.p, false, st));
   if (timing) TSG_CU(cudaEventRecord(ev[4], st));
   return TSG_OK;
 }

@@ -22,6 +22,10 @@
 #include "common.cuh"
 #include "solve.h"
 
+#ifndef LAPD_PROF
+#define LAPD_PROF 0
+#endif
+
 namespace tsg {
 namespace {
 
@@ -130,6 +134,8 @@ __global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
   for (int m = 0; m < D; ++m) ep <<= a.tlog[m];
   // optional cycle counters (TSG_PROF): 0 claim+geometry, 1 gather, 2 far
   // updates, 3 near updates (incl. flag waits), 4 base case, 5 scatter
+  // (compiled in with -DLAPD_PROF=1 only: the counters cost registers)
+#if LAPD_PROF
   unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tmark = clock64();
   auto mark = [&](int k) {
@@ -139,9 +145,16 @@ __global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
       tmark = t;
     }
   };
+#else
+  auto mark = [](int) {};
+#endif
+#if LAPD_PROF
   int ntl = 0;
-
-  for (;; ++ntl) {
+#endif
+  for (;;) {
+#if LAPD_PROF
+    ++ntl;
+#endif
     mark(5);
     if (tid == 0) s_tile = atomicAdd(a.counter, 1);
     __syncthreads();
@@ -302,10 +315,12 @@ __global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
       st_release(a.flags + g.lt, a.epoch);
     }
   }
+#if LAPD_PROF
   if (a.prof && tid == 0) {
     for (int k = 0; k < 8; ++k) atomicAdd(a.prof + k, ph[k]);
     atomicAdd(a.prof + 8, static_cast<unsigned long long>(ntl));
   }
+#endif
 }
 
 template <int D>

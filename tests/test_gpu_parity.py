@@ -176,3 +176,15 @@ def test_lap16_kernel_matches_reference(gpu, ref, kind, dims, monkeypatch):
                                                 arithmetic=gpu.Arithmetic.real_quasitriangular))
     assert rel_diff(rep.solution, want) < REL
     assert ref.residual_laplace(p.coeffs, p.rhs, rep.solution) < RES
+
+
+# Fused small-mode transforms (modes_small.cu): consecutive extents in
+# {16, 24, 32} are transformed two modes per HBM pass.
+@pytest.mark.parametrize("dims", [(16, 24, 32), (24, 24, 24, 16), (32, 16, 24, 24, 16), (7, 24, 24, 16)])
+def test_small_mode_transforms(gpu, ref, dims):
+    p = gpu.make_problem(2, dims, seed=6)
+    want, _ = ref.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
+    rep = gpu.solve_laplace(p, gpu.SolverConfig(strategy=gpu.Strategy.recursion_only,
+                                                arithmetic=gpu.Arithmetic.real_quasitriangular))
+    assert rel_diff(rep.solution, want) < REL
+    assert ref.residual_laplace(p.coeffs, p.rhs, rep.solution) < RES
