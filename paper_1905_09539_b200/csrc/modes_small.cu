@@ -27,7 +27,8 @@ struct PairArgs {
   const double* A;  // n_a x n_a, column-major (Y = X x_a A: y_i = sum_k A(i,k) x_k)
   const double* B;  // n_b x n_b or null
   int na, nb;       // nb = 1 when B is null
-  int c, o;         // block inner / outer extents
+  int c, o;         // block inner / outer extents (c a power of two)
+  int lc;           // log2 c
   int64_t P, Q;     // prefix (modes < a) and suffix (modes > b) sizes
   int64_t nblk;     // blocks
   int bsz;          // doubles per block = c * na * nb * o
@@ -36,21 +37,42 @@ struct PairArgs {
 // y[f, i] = sum_k M(i, k) x[f, k] for the fibres of the block along a
 // coordinate of extent N and stride st (in the block): fibre index f
 // enumerates (lo < st) x (hi) with element offset lo + st * (k + N * hi).
+// DMMA: M (N x N, registers) is the A operand, each warp takes whole
+// 8-fibre blocks (B operand from shared memory) and writes them back in
+// place once all their rows are read.
 template <int N>
 TSG_DEVINL void fibres(double* blk, const double* M, int st, int nf) {
-  for (int f = threadIdx.x; f < nf; f += THREADS) {
-    const int lo = f % st, hi = f / st;
-    double* p = blk + lo + static_cast<int64_t>(st) * N * hi;
-    double x[N];
+  constexpr int RB = N / 8, KS = N / 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  double af[RB][KS];
 #pragma unroll
-    for (int k = 0; k < N; ++k) x[k] = p[st * k];
+  for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double s = 0.0;
+    for (int ks = 0; ks < KS; ++ks) af[rb][ks] = M[(8 * rb + gq) + N * (4 * ks + tq)];
+  for (int fb = warp; fb < (nf >> 3); fb += THREADS / 32) {
+    // fibre of this lane as B column: f = 8 fb + gq; as C column: 8 fb + 2 tq + h
+    const int fB = 8 * fb + gq;
+    const double* pB = blk + (fB % st) + static_cast<int64_t>(st) * N * (fB / st);
+    double bf[KS];
 #pragma unroll
-      for (int k = 0; k < N; ++k) s = fma(M[i + N * k], x[k], s);
-      p[st * i] = s;
+    for (int ks = 0; ks < KS; ++ks) bf[ks] = pB[st * (4 * ks + tq)];
+    double c[RB][2];
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb) c[rb][0] = c[rb][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) dmma(c[rb][0], c[rb][1], af[rb][ks], bf[ks]);
+    __syncwarp();  // every row of the warp's 8 fibres has been read
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int fC = 8 * fb + 2 * tq + h;
+      double* pC = blk + (fC % st) + static_cast<int64_t>(st) * N * (fC / st);
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) pC[st * (8 * rb + gq)] = c[rb][h];
     }
+    __syncwarp();
   }
 }
 
@@ -64,30 +86,30 @@ __global__ void __launch_bounds__(THREADS) pair_kernel(PairArgs g) {
   if (NB > 1)
     for (int e = threadIdx.x; e < NB * NB; e += THREADS) mb[e] = g.B[e];
   const int c = g.c, o = g.o;
-  const int grp = NA * NB;
+  constexpr int GRP = NA * NB;
   for (int64_t bk = blockIdx.x; bk < g.nblk; bk += gridDim.x) {
     // block bk -> (prefix chunk pc, suffix chunk sc)
     const int64_t npc = g.P / c;
     const int64_t pc = bk % npc, sc = bk / npc;
-    const int64_t base = pc * c + sc * static_cast<int64_t>(o) * g.P * grp;
+    const int64_t base = pc * c + sc * static_cast<int64_t>(o) * g.P * GRP;
     __syncthreads();  // previous block written back
     // gather: element (ic, gi, io) at base + ic + P * (gi + grp * io)
     for (int e = threadIdx.x; e < g.bsz; e += THREADS) {
-      const int ic = e % c, rest = e / c;
-      const int gi = rest % grp, io = rest / grp;
-      blk[e] = g.X[base + ic + g.P * (gi + static_cast<int64_t>(grp) * io)];
+      const int ic = e & (c - 1), rest = e >> g.lc;
+      const int gi = rest % GRP, io = rest / GRP;
+      blk[e] = g.X[base + ic + g.P * (gi + static_cast<int64_t>(GRP) * io)];
     }
     __syncthreads();
     fibres<NA>(blk, ma, c, g.bsz / NA);  // mode a: stride c in the block
-    if (NB > 1) {
+    if constexpr (NB > 1) {
       __syncthreads();
       fibres<NB>(blk, mb, c * NA, g.bsz / NB);
     }
     __syncthreads();
     for (int e = threadIdx.x; e < g.bsz; e += THREADS) {
-      const int ic = e % c, rest = e / c;
-      const int gi = rest % grp, io = rest / grp;
-      g.Y[base + ic + g.P * (gi + static_cast<int64_t>(grp) * io)] = blk[e];
+      const int ic = e & (c - 1), rest = e >> g.lc;
+      const int gi = rest % GRP, io = rest / GRP;
+      g.Y[base + ic + g.P * (gi + static_cast<int64_t>(GRP) * io)] = blk[e];
     }
   }
 }
@@ -160,6 +182,8 @@ cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, 
     g.o = o;
   }
   g.bsz = g.c * grp * g.o;
+  g.lc = 0;
+  while ((1 << g.lc) < g.c) ++g.lc;
   g.nblk = (g.P / g.c) * (g.Q / g.o);
   if (flops) *flops += 2.0 * static_cast<double>(g.P) * g.Q * grp * (g.na + g.nb - (pair ? 0 : 1));
   switch (g.na) {
