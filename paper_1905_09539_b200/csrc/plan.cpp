@@ -613,7 +613,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       tmd.nc = static_cast<unsigned char>(nc);
       tmd.far_lo = t + 3 < ntm ? mt.bd[t + 3] : dims[m];
     }
-    if (pl->fast == 3 || pl->fast == 5) {
+    if (pl->fast == 3 || pl->fast == 5 || pl->fast == 6) {
       // Eigenbasis diagonal block of every tile index along mode m:
       // That[i][j] = sum Pinv_blk(i)[i,a] T[a,b] P_blk(j)[b,j] for j beyond
       // i's cell (0 elsewhere), then lambda_i; layout of solve_lap3 (DHS).
@@ -697,7 +697,31 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     }
     if (!(prod <= tsg::kDiagCond) || lsum > 9) pl->fast = 1;
   }
-  if (!pl->use16 && pl->fast != 5) {
+  // gsylv d = 3..5: the small-tile kernel when the tail tiles' bases are
+  // well conditioned (mode 0 is solved by back substitution, no basis)
+  const char* eg = std::getenv("TSG_GSYD");
+  if (family == 1 && d >= 3 && d <= 5 && (eg ? std::atoi(eg) != 0 : true)) {
+    pl->fast = 6;
+    pl->tile_ext = choose_tiles(family, pl->dims, o, tsg::solve_gsyd_caps());
+    double prod = 1.0;
+    int lsum = 0;
+    pl->tlog.assign(d, 0);
+    pl->tsh.assign(d, 0);
+    for (int m = 0; m < d; ++m) {
+      const int rc = build_mode(m, 3, false);
+      if (rc != TSG_OK) return rc;
+      if (m > 0) prod *= mts[m].maxvc;
+      int mx = 1;
+      for (const auto& tm : mts[m].tms) mx = std::max(mx, static_cast<int>(tm.ext));
+      int lg = 0;
+      while ((1 << lg) < mx) ++lg;
+      pl->tsh[m] = lsum;
+      pl->tlog[m] = lg;
+      lsum += lg;
+    }
+    if (!(prod <= tsg::kDiagCond) || lsum > 9) pl->fast = 0;
+  }
+  if (!pl->use16 && pl->fast != 5 && pl->fast != 6) {
     pl->tile_ext = choose_tiles(family, pl->dims, o,
                                 pl->fast == 3 ? tsg::solve_lap3_caps(pl->lt3)
                                               : (pl->fast ? tsg::solve_lap_caps(d) : tsg::solve_caps(family, d)));
@@ -1058,6 +1082,7 @@ void fill_solve_args(const tsg_plan* pl, double* work, tsg::SolveArgs& a) {
 cudaError_t launch_plan_solve(tsg_plan* pl, const tsg::SolveArgs& a, cudaStream_t st) {
   if (pl->use16) return tsg::launch_solve_lap16(a, st, &pl->solve_info);
   if (pl->fast == 5) return tsg::launch_solve_lapd(a, st, &pl->solve_info);
+  if (pl->fast == 6) return tsg::launch_solve_gsyd(a, st, &pl->solve_info);
   if (pl->fast == 3) return tsg::launch_solve_lap3(pl->lt3, a, st, &pl->solve_info);
   if (pl->fast) return tsg::launch_solve_lap(a, st, &pl->solve_info);
   return tsg::launch_solve(a, st, &pl->solve_info);

@@ -106,6 +106,11 @@ cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchI
 TileCaps solve_lapd_caps();
 cudaError_t launch_solve_lapd(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
 
+// gsylv d = 3..5 (solve_gsyd.cu): small tiles, DMMA chain updates, tail
+// eigenbasis + mode-0 pencil back substitution.
+TileCaps solve_gsyd_caps();
+cudaError_t launch_solve_gsyd(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
+
 // Fast Laplace path (solve_lap.cu): small tiles, eigenbasis base cells.
 TileCaps solve_lap_caps(int d);
 cudaError_t launch_solve_lap(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
