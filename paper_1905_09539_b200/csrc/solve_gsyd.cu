@@ -181,7 +181,10 @@ TSG_DEVINL void cmode(const SolveArgs& a, const GG<D>& g, double* xr, double* xi
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS, 4) solve_gsyd_kernel(SolveArgs a) {
+#ifndef GSYD_MINB
+#define GSYD_MINB 3
+#endif
+__global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArgs a) {
   __shared__ __align__(16) double xr[EP];
   __shared__ __align__(16) double xi[EP];
   __shared__ __align__(16) double lb[D - 1][EP];  // L_m -> W_m (m = 1..D-1)
