@@ -695,7 +695,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       pl->tlog[m] = lg;
       lsum += lg;
     }
-    if (!(prod <= tsg::kDiagCond) || lsum > 9) pl->fast = 1;
+    if (!(prod <= tsg::kDiagCond) || (1 << lsum) > tsg::solve_lapd_caps().Emax) pl->fast = 1;
   }
   // gsylv d = 3..5: the small-tile kernel when the tail tiles' bases are
   // well conditioned (mode 0 is solved by back substitution, no basis)

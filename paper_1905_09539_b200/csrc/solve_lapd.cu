@@ -29,7 +29,10 @@
 namespace tsg {
 namespace {
 
-constexpr int THREADS = 128, WARPS = 4, EP = 512;
+#ifndef LAPD_EP
+#define LAPD_EP 512
+#endif
+constexpr int EP = LAPD_EP, THREADS = EP / 4, WARPS = THREADS / 32;
 constexpr int VHS = kVhStride;  // 8x8 complex records (tile_eigvecs<8>)
 constexpr int NBMAX = EP / 2 / 8 / WARPS;  // 8-column blocks per warp, P_m >= 2
 
@@ -122,7 +125,7 @@ TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int 
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS, 4) solve_lapd_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArgs a) {
   __shared__ __align__(16) double xr[EP];
   __shared__ __align__(16) double xi[EP];
   __shared__ __align__(16) double vh[D * VHS];
