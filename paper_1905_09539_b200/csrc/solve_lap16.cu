@@ -505,6 +505,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (tid == 0) {
         __threadfence();
         st_release(a.flags + g.lt, a.epoch);
+        if (a.trace) {
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+          a.trace[g.lt] = tt;
+        }
       }
     }
   }
