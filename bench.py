@@ -142,17 +142,19 @@ def build_plan(T, ctx, kind, p):
     return Plan(ctx, 0, [f[1] for f in fs], [f[0] for f in fs])
 
 
-def traffic_from_profiles(config: str):
-    """ncu dram bytes per launch of the dominant kernel, if a capture was
-    summarised into profiles/ncu_traffic.json (written from an ncu --set full
-    report of this config)."""
+def traffic_from_profiles(config: str, kernel: str):
+    """ncu dram bytes (read + write) per launch of `kernel` ("solve" or
+    "dgemm"), if an ncu --set full capture of this config was summarised into
+    profiles/ncu_traffic.json (tools/ncu_summary.py)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get(config)
+            d = json.load(f).get(config)
     except (OSError, ValueError):
         return None
+    if isinstance(d, dict):
+        return d.get(kernel)
+    return d if kernel == "solve" else None
 
 
 def cpu_reference_solve(kind, dims, seed=1):
@@ -293,13 +295,13 @@ def run_ours(a, rank, world, local):
     # (2d launches per step); achieved = algorithmic FLOP per launch / launch time
     d = len(dims)
     if t_solve >= t_fwd + t_back:
-        dom = {"kernel": "solve_kernel (reduced dataflow solve, K2+K3)",
+        dom = {"kernel": "solve kernel (reduced dataflow solve, K2+K3)", "ncu": "solve",
                "achieved": solve_f / (t_solve * 1e-3) / 1e12, "launch_ms": t_solve}
     else:
-        dom = {"kernel": "dgemm_nn_kernel (mode transforms, K1)",
+        dom = {"kernel": "dgemm_nn_kernel (mode transforms, K1)", "ncu": "dgemm",
                "achieved": tr_f / ((t_fwd + t_back) * 1e-3) / 1e12,
                "launch_ms": (t_fwd + t_back) / (2 * d)}
-    traffic = traffic_from_profiles(a.config)
+    traffic = traffic_from_profiles(a.config, dom["ncu"])
     roofline = {"bound": "tensor", "achieved": dom["achieved"], "peak": PEAK_FP64_TFLOPS,
                 "unit": "TFLOP/s", "frac": dom["achieved"] / PEAK_FP64_TFLOPS,
                 "traffic": traffic, "kernel": dom["kernel"],

@@ -55,8 +55,10 @@ def main():
                     lines.append(f"   {k:70s} {d[k]}")
             try:
                 t = to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"])
-                if "solve" in d["kernel"] and traffic is None:
-                    traffic = t
+                kind = "solve" if "solve" in d["kernel"] else ("dgemm" if "dgemm" in d["kernel"] else None)
+                if kind:
+                    traffic = traffic or {}
+                    traffic.setdefault(kind, t)
             except (KeyError, ValueError):
                 pass
     open(out_txt, "w").write("\n".join(lines) + "\n")
