@@ -188,3 +188,14 @@ def test_small_mode_transforms(gpu, ref, dims):
                                                 arithmetic=gpu.Arithmetic.real_quasitriangular))
     assert rel_diff(rep.solution, want) < REL
     assert ref.residual_laplace(p.coeffs, p.rhs, rep.solution) < RES
+
+
+# Degenerate extents: modes of extent 1 and order-2 problems.
+@pytest.mark.parametrize("dims", [(1, 6, 5), (7, 1, 1), (1, 1), (1, 9), (5, 1, 4, 1), (100, 37)])
+def test_degenerate_extents(gpu, ref, dims):
+    p = gpu.make_problem(2, dims, seed=8)
+    want, _ = ref.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
+    rep = gpu.solve_laplace(p, gpu.SolverConfig(strategy=gpu.Strategy.recursion_only,
+                                                arithmetic=gpu.Arithmetic.real_quasitriangular))
+    assert rel_diff(rep.solution, want) < REL
+    assert rep.residual < RES
