@@ -69,10 +69,12 @@ TSG_DEVINL void cross_g(const SolveArgs& a, const GG<D>& g, int m, int n, int& l
   }
 }
 
-// dst += sign * sum_k src(cross, k) Tm(rows, k) over rows k in [klo, khi)
-template <int D>
-TSG_DEVINL void update_src(const SolveArgs& a, const GG<D>& g, double* dst, double sign, int ep, int m,
-                           int klo, int khi, const double* Tm, const double* src) {
+// dst += sign * sum_k src(cross, k) Tm(rows, k) over rows k in [klo, khi).
+// NB 8-column blocks per warp and round, UB k4-steps of loads in flight
+// (NB * UB <= 16 fragment loads per batch).
+template <int D, int NB, int UB>
+TSG_DEVINL void update_nb(const SolveArgs& a, const GG<D>& g, double* dst, double sign, int ep, int m,
+                          int klo, int khi, const double* Tm, const double* src) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int lpm = a.tlog[m], shm = a.tsh[m];
@@ -82,13 +84,13 @@ TSG_DEVINL void update_src(const SolveArgs& a, const GG<D>& g, double* dst, doub
   const int64_t sm = a.stride[m];
   const int row = g.start[m] + gq;
   const bool rok = gq < g.ext[m];
-  for (int base = warp; base < nblk; base += WARPS * NBMAX) {
-    int ltc[NBMAX];
-    int64_t goc[NBMAX];
-    bool cok[NBMAX];
-    double acc[NBMAX][2];
+  for (int base = warp; base < nblk; base += WARPS * NB) {
+    int ltc[NB];
+    int64_t goc[NB];
+    bool cok[NB];
+    double acc[NB][2];
 #pragma unroll
-    for (int j = 0; j < NBMAX; ++j) {
+    for (int j = 0; j < NB; ++j) {
       const int b = base + WARPS * j;
       acc[j][0] = acc[j][1] = 0.0;
       ltc[j] = 0;
@@ -96,20 +98,25 @@ TSG_DEVINL void update_src(const SolveArgs& a, const GG<D>& g, double* dst, doub
       cok[j] = b < nblk && 8 * b + gq < cross;
       if (cok[j]) cross_g<D>(a, g, m, 8 * b + gq, ltc[j], goc[j]);
     }
-    for (int k0 = klo; k0 < khi; k0 += 4) {
-      const int k = k0 + tq;
-      const bool kok = k < khi;
-      const double bt = (kok && rok) ? __ldg(Tm + row + static_cast<int64_t>(k) * nm) : 0.0;
-      double av[NBMAX];
+    for (int k0 = klo; k0 < khi; k0 += 4 * UB) {
+      double bt[UB], av[UB][NB];
 #pragma unroll
-      for (int j = 0; j < NBMAX; ++j)
-        av[j] = (cok[j] && kok) ? ld_cg(src + goc[j] + static_cast<int64_t>(k) * sm) : 0.0;
+      for (int u = 0; u < UB; ++u) {
+        const int k = k0 + 4 * u + tq;
+        const bool kok = k < khi;
+        bt[u] = (kok && rok) ? __ldg(Tm + row + static_cast<int64_t>(k) * nm) : 0.0;
 #pragma unroll
-      for (int j = 0; j < NBMAX; ++j)
-        if (base + WARPS * j < nblk) dmma(acc[j][0], acc[j][1], av[j], bt);
+        for (int j = 0; j < NB; ++j)
+          av[u][j] = (cok[j] && kok) ? ld_cg(src + goc[j] + static_cast<int64_t>(k) * sm) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (base + WARPS * j < nblk) dmma(acc[j][0], acc[j][1], av[u][j], bt[u]);
     }
 #pragma unroll
-    for (int j = 0; j < NBMAX; ++j) {
+    for (int j = 0; j < NB; ++j) {
       if (!cok[j]) continue;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -118,6 +125,15 @@ TSG_DEVINL void update_src(const SolveArgs& a, const GG<D>& g, double* dst, doub
       }
     }
   }
+}
+
+template <int D>
+TSG_DEVINL void update_src(const SolveArgs& a, const GG<D>& g, double* dst, double sign, int ep, int m,
+                           int klo, int khi, const double* Tm, const double* src) {
+  const int nblk = ((ep >> a.tlog[m]) + 7) >> 3;
+  if (nblk <= 2 * WARPS) update_nb<D, 2, 8>(a, g, dst, sign, ep, m, klo, khi, Tm, src);
+  else if (nblk <= 4 * WARPS) update_nb<D, 4, 4>(a, g, dst, sign, ep, m, klo, khi, Tm, src);
+  else update_nb<D, 8, 2>(a, g, dst, sign, ep, m, klo, khi, Tm, src);
 }
 
 // buf(fibre along m) = M (P x P, row-major stride 8) * buf(fibre) [+ add(fibre)]
