@@ -113,6 +113,13 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims,
 int tsg_plan_execute(tsg_plan* plan, const double* B, double* X,
                      int inputs_on_device, tsg_report* rep);
 void tsg_plan_destroy(tsg_plan* plan);
+/* Solve nrhs right-hand sides from HOST buffers B[i] into X[i] (pinned
+ * memory recommended) with the copies overlapped: the host->device copy of
+ * B[i+1] and the device->host copy of X[i-1] run on copy streams while
+ * solve i runs (two device staging slots).  Synchronous on return;
+ * rep->t_total_ms covers the whole batch (first copy to last copy). */
+int tsg_plan_execute_stream(tsg_plan* plan, int nrhs, const double* const* B, double* const* X,
+                            tsg_report* rep);
 /* Number of tiles / dataflow steps of the plan's reduced solve. */
 int tsg_plan_info(const tsg_plan* plan, int64_t* n_tiles, int* tile_extents,
                   double* flops_alg);

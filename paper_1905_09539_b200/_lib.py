@@ -37,7 +37,8 @@ TSG_SYMBOLS = [
     "tsg_default_opts", "tsg_create", "tsg_destroy", "tsg_last_error", "tsg_ctx_stream",
     "tsg_laplace_solve",
     "tsg_laplace_reduced", "tsg_gsylv_solve", "tsg_gsylv_reduced", "tsg_plan_create",
-    "tsg_plan_execute", "tsg_plan_destroy", "tsg_plan_info", "tsg_mode_multiply",
+    "tsg_plan_execute", "tsg_plan_execute_stream", "tsg_plan_destroy", "tsg_plan_info",
+    "tsg_mode_multiply",
     "tsg_residual", "tsg_abi_version",
     "tsg_slab_bounds", "tsg_dplan_create", "tsg_dplan_destroy", "tsg_dplan_info",
     "tsg_dplan_buffers", "tsg_dplan_ipc_export", "tsg_dplan_ipc_import",
@@ -60,6 +61,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tsg_plan_create": (I, [P, I, I, c_int_p, c_dbl_pp, c_dbl_pp, c_dbl_p, c_dbl_p, I,
                                 ctypes.POINTER(TsgOpts), ctypes.POINTER(P)]),
         "tsg_plan_execute": (I, [P, P, P, I, ctypes.POINTER(TsgReport)]),
+        "tsg_plan_execute_stream": (I, [P, I, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(TsgReport)]),
         "tsg_plan_destroy": (None, [P]),
         "tsg_plan_info": (I, [P, ctypes.POINTER(ctypes.c_int64), c_int_p, c_dbl_p]),
         "tsg_residual": (I, [P, I, I, c_int_p, c_dbl_pp, P, P, P, I, c_dbl_p]),

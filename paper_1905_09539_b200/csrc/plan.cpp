@@ -426,6 +426,7 @@ void tile_eigvecs(std::vector<tsg::TileMode>& tms, const std::vector<double>& dh
 }
 
 int capture_or_run(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool graph);
+int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool timing);
 
 }  // namespace
 
@@ -879,6 +880,81 @@ int tsg_plan_execute(tsg_plan* pl, const double* B, double* X, int inputs_on_dev
   if (hstat[1] != kNoStatus)
     return fail(ctx, TSG_ESINGULAR,
                 "reduced solve: numerically singular base cell in tile " + std::to_string(hstat[1]));
+  return TSG_OK;
+}
+
+int tsg_plan_execute_stream(tsg_plan* pl, int nrhs, const double* const* B, double* const* X,
+                            tsg_report* rep) {
+  if (!pl || nrhs < 0 || (nrhs > 0 && (!B || !X))) return TSG_EINVAL;
+  tsg_ctx* ctx = pl->ctx;
+  TSG_CU(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const size_t bytes = static_cast<size_t>(pl->N) * sizeof(double);
+  for (int s = 0; s < 2; ++s) {
+    TSG_CU(pl->sin[s].ensure(pl->N));
+    TSG_CU(pl->sout[s].ensure(pl->N));
+  }
+  cudaStream_t cin = nullptr, cout = nullptr;
+  TSG_CU(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
+  TSG_CU(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
+  cudaEvent_t in_ready[2], solved[2], out_free[2], t0, t1;
+  for (int s = 0; s < 2; ++s) {
+    TSG_CU(cudaEventCreateWithFlags(&in_ready[s], cudaEventDisableTiming));
+    TSG_CU(cudaEventCreateWithFlags(&solved[s], cudaEventDisableTiming));
+    TSG_CU(cudaEventCreateWithFlags(&out_free[s], cudaEventDisableTiming));
+  }
+  TSG_CU(cudaEventCreate(&t0));
+  TSG_CU(cudaEventCreate(&t1));
+  TSG_CU(cudaEventRecord(t0, st));
+  TSG_CU(cudaStreamWaitEvent(cin, t0, 0));
+  DevBuf stat;  // status word of every solve (singular cells), checked at the end
+  TSG_CU(stat.ensure((static_cast<size_t>(std::max(nrhs, 1)) + 1) / 2));
+  int* dstat = reinterpret_cast<int*>(stat.p);
+  for (int i = 0; i < nrhs; ++i) {
+    const int s = i & 1;
+    // slot s input is free once solve i-2 finished
+    if (i >= 2) TSG_CU(cudaStreamWaitEvent(cin, solved[s], 0));
+    TSG_CU(cudaMemcpyAsync(pl->sin[s].p, B[i], bytes, cudaMemcpyHostToDevice, cin));
+    TSG_CU(cudaEventRecord(in_ready[s], cin));
+    TSG_CU(cudaStreamWaitEvent(st, in_ready[s], 0));
+    if (i >= 2) TSG_CU(cudaStreamWaitEvent(st, out_free[s], 0));  // D2H of i-2 drained sout[s]
+    const int rc = enqueue(pl, pl->sin[s].p, pl->sout[s].p, st, false);
+    if (rc != TSG_OK) return rc;
+    TSG_CU(cudaMemcpyAsync(dstat + i, pl->counter + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    TSG_CU(cudaEventRecord(solved[s], st));
+    TSG_CU(cudaStreamWaitEvent(cout, solved[s], 0));
+    TSG_CU(cudaMemcpyAsync(X[i], pl->sout[s].p, bytes, cudaMemcpyDeviceToHost, cout));
+    TSG_CU(cudaEventRecord(out_free[s], cout));
+  }
+  TSG_CU(cudaEventRecord(t1, cout));
+  std::vector<int> hs(static_cast<size_t>(nrhs));
+  if (nrhs > 0) TSG_CU(cudaMemcpyAsync(hs.data(), dstat, nrhs * sizeof(int), cudaMemcpyDeviceToHost, st));
+  TSG_CU(cudaStreamSynchronize(cout));
+  TSG_CU(cudaStreamSynchronize(st));
+  int hstat[2] = {0, kNoStatus};
+  for (int v : hs)
+    if (v != kNoStatus && hstat[1] == kNoStatus) hstat[1] = v;
+  if (rep) {
+    float t = 0;
+    std::memset(rep, 0, sizeof(*rep));
+    cudaEventElapsedTime(&t, t0, t1);
+    rep->t_total_ms = t;
+    rep->flops_alg = pl->flops_alg * nrhs;
+    rep->flops_exec = pl->flops_exec * nrhs;
+    rep->zero_pivot_index = hstat[1] == kNoStatus ? -1 : hstat[1];
+    rep->kernel_launches = pl->launches * nrhs;
+  }
+  for (int s = 0; s < 2; ++s) {
+    cudaEventDestroy(in_ready[s]);
+    cudaEventDestroy(solved[s]);
+    cudaEventDestroy(out_free[s]);
+  }
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaStreamDestroy(cin);
+  cudaStreamDestroy(cout);
+  if (hstat[1] != kNoStatus)
+    return fail(ctx, TSG_ESINGULAR, "reduced solve: numerically singular base cell in tile " + std::to_string(hstat[1]));
   return TSG_OK;
 }
 

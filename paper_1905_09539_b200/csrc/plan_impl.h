@@ -60,6 +60,7 @@ struct tsg_plan {
   std::vector<int> ntiles_mode, tile_ext;
   // work buffers
   DevBuf xdev, w1, w2;
+  DevBuf sin[2], sout[2];  // tsg_plan_execute_stream staging (double-buffered)
   std::vector<DevBuf> wchain;  // gsylv W_m, m = 1..d-1
   double flops_alg = 0, flops_exec = 0;
   double tiny = 0;

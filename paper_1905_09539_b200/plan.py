@@ -92,6 +92,21 @@ class Plan:
             raise gpu_error(f"tsg_plan_execute failed ({rc}): {self.ctx.error()}")
         return rep
 
+    def execute_stream(self, b_ptrs: list, x_ptrs: list) -> TsgReport:
+        """Solve len(b_ptrs) right-hand sides from HOST buffers (raw pointers,
+        pinned memory recommended) with copy/compute overlap
+        (tsg_plan_execute_stream)."""
+        n = len(b_ptrs)
+        if len(x_ptrs) != n:
+            raise ValueError("execute_stream: as many outputs as inputs")
+        bp = (ctypes.c_void_p * max(n, 1))(*[ctypes.c_void_p(int(p)) for p in b_ptrs])
+        xp = (ctypes.c_void_p * max(n, 1))(*[ctypes.c_void_p(int(p)) for p in x_ptrs])
+        rep = TsgReport()
+        rc = lib().tsg_plan_execute_stream(self.h, n, bp, xp, ctypes.byref(rep))
+        if rc != 0:
+            raise gpu_error(f"tsg_plan_execute_stream failed ({rc}): {self.ctx.error()}")
+        return rep
+
     def close(self):
         if self.h:
             lib().tsg_plan_destroy(self.h)
