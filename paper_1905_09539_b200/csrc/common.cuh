@@ -15,11 +15,21 @@ namespace tsg {
 
 // D = A(8x4, row) * B(4x8, col) + C(8x8).  Fragment ownership per lane
 // (g = lane>>2, t = lane&3):  a = A[g][t], b = B[t][g], c = C[g][2t..2t+1].
+#ifndef TSG_DMMA_VOLATILE
+#define TSG_DMMA_VOLATILE 1
+#endif
 TSG_DEVINL void dmma(double& c0, double& c1, double a, double b) {
+#if TSG_DMMA_VOLATILE
   asm volatile(
       "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
+#else
+  // no side effects: let the compiler schedule the products freely
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+#endif
 }
 
 TSG_DEVINL uint32_t smem_u32(const void* p) {

@@ -45,8 +45,12 @@ struct GemmSmem {
   static constexpr int BYTES = kStages * STAGE * 8;
 };
 
-template <int BM, int BN, int WM, int WN, bool VEC>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+#ifndef TSG_GEMM_MINB
+#define TSG_GEMM_MINB 1
+#endif
+template <int BM, int BN, int WM, int WN, bool VEC, bool FAST = false>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
+                                  (FAST && (BM / WM) * (BN / WN) == 4) ? 4 : TSG_GEMM_MINB)
 dgemm_nn_kernel(GemmArgs g) {
   using S = GemmSmem<BM, BN>;
   constexpr int NWM = BM / WM;              // warps along M
@@ -119,6 +123,46 @@ dgemm_nn_kernel(GemmArgs g) {
     }
   };
 
+  // Interior tiles (no M/N edge, K a multiple of BK, 16-byte aligned): the
+  // per-thread copy sources are fixed pointers advanced by BK per k-tile.
+  constexpr int ACH = BK * BM / 2, BCH = BN * BK / 2;
+  constexpr int NA = (ACH + NT - 1) / NT, NB = (BCH + NT - 1) / NT;
+  // FAST instantiations are launched only when every tile is interior
+  constexpr bool interior = FAST;
+  // 32-bit per-thread source offsets (the operands' tile panels are small)
+  const double* A0 = A + m0;
+  const double* B0 = B + static_cast<int64_t>(n0) * g.ldb;
+  int ga[NA], gb[NB], oa[NA], ob[NB];
+  if constexpr (FAST) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const int c = tid + i * NT;
+      const int kk = c / (BM / 2), mm = (c % (BM / 2)) * 2;
+      ga[i] = kk * static_cast<int>(g.lda) + mm;
+      oa[i] = kk * S::LDA + mm;
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int c = tid + i * NT;
+      const int nn = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+      gb[i] = nn * static_cast<int>(g.ldb) + kk;
+      ob[i] = nn * S::LDB + kk;
+    }
+  }
+  const int64_t astep = static_cast<int64_t>(BK) * g.lda;
+  auto load_fast = [&](int stage, int kt) {
+    double* sa = smem + stage * S::STAGE;
+    double* sb = sa + S::A_ELEMS;
+    const double* ak = A0 + kt * astep;
+    const double* bk = B0 + kt * BK;
+#pragma unroll
+    for (int i = 0; i < NA; ++i)
+      if (ACH % NT == 0 || tid + i * NT < ACH) cp_async16(sa + oa[i], ak + ga[i], 16);
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (BCH % NT == 0 || tid + i * NT < BCH) cp_async16(sb + ob[i], bk + gb[i], 16);
+  };
+
   double acc[FM][FN][2];
 #pragma unroll
   for (int i = 0; i < FM; ++i)
@@ -128,7 +172,10 @@ dgemm_nn_kernel(GemmArgs g) {
   const int nk = (g.K + BK - 1) / BK;
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
-    if (s < nk) load_stage(s, s * BK);
+    if (s < nk) {
+      if constexpr (interior) load_fast(s, s);
+      else load_stage(s, s * BK);
+    }
     cp_async_commit();
   }
 
@@ -137,7 +184,10 @@ dgemm_nn_kernel(GemmArgs g) {
     __syncthreads();
     {
       const int nxt = kt + kStages - 1;
-      if (nxt < nk) load_stage(nxt % kStages, nxt * BK);
+      if (nxt < nk) {
+        if constexpr (interior) load_fast(nxt % kStages, nxt);
+        else load_stage(nxt % kStages, nxt * BK);
+      }
       cp_async_commit();
     }
     const double* sa = smem + (kt % kStages) * S::STAGE;
@@ -187,7 +237,17 @@ cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
   const bool vec = (g.lda % 2 == 0) && (g.ldb % 2 == 0) && (g.sA % 2 == 0) && (g.sB % 2 == 0) &&
                    ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0);
-  if (vec) {
+  const bool all_interior = vec && g.M % BM == 0 && g.N % BN == 0 && g.K % BK == 0 &&
+                            g.lda * BK < (int64_t{1} << 30) && g.ldb * BN < (int64_t{1} << 30);
+  if (all_interior) {
+    auto k = dgemm_nn_kernel<BM, BN, WM, WN, true, true>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
+      attr = true;
+    }
+    k<<<static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, st>>>(g);
+  } else if (vec) {
     auto k = dgemm_nn_kernel<BM, BN, WM, WN, true>;
     static bool attr = false;
     if (!attr) {
