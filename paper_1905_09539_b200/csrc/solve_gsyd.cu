@@ -290,9 +290,13 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
         mul *= a.ntiles_mode[m];
       }
     }
-    for (int part = 0; part < 2 && !(a.dbg & 4); ++part) {
+#ifndef GSYD_ONEPASS
+#define GSYD_ONEPASS 1
+#endif
+    constexpr int NPART = GSYD_ONEPASS ? 1 : 2;
+    for (int part = 0; part < NPART && !(a.dbg & 4); ++part) {
       if (tid == 0) {
-        const int d0 = part == 0 ? 2 : 1;
+        const int d0 = (part == 0 && !GSYD_ONEPASS) ? 2 : 1;
         for (int m = 0; m < D; ++m)
           if (g.tco[m] + d0 < a.ntiles_mode[m]) waitg(a, g.lt + d0 * muls[m]);
       }
@@ -301,7 +305,10 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
       for (int m = 0; m < D; ++m) {
         const int tm = g.tco[m], p = a.ntiles_mode[m];
         int klo, khi;
-        if (part == 0) {
+        if (GSYD_ONEPASS) {
+          klo = tm + 1 < p ? a.bnd[m][tm + 1] : 0;
+          khi = tm + 1 < p ? a.dims[m] : 0;
+        } else if (part == 0) {
           klo = tm + 2 < p ? a.bnd[m][tm + 2] : 0;
           khi = tm + 2 < p ? a.dims[m] : 0;
         } else {

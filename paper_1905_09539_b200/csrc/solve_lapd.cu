@@ -212,10 +212,17 @@ __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArg
       muls[m] = mul;
       mul *= a.ntiles_mode[m];
     }
-    for (int part = 0; part < 2 && !(a.dbg & 4); ++part) {
+#ifndef LAPD_ONEPASS
+#define LAPD_ONEPASS 1
+#endif
+    // LAPD_ONEPASS: wait for the t+1 flags and stream each mode's whole
+    // range at once (half the update rounds; no overlap of the far rows with
+    // the wait, which rarely matters on the wide hyperplanes of d = 6)
+    constexpr int NPART = LAPD_ONEPASS ? 1 : 2;
+    for (int part = 0; part < NPART && !(a.dbg & 4); ++part) {
       if (tid == 0) {
         for (int m = 0; m < D; ++m) {
-          const int tm = g.tco[m], d0 = part == 0 ? 2 : 1;
+          const int tm = g.tco[m], d0 = (part == 0 && !LAPD_ONEPASS) ? 2 : 1;
           if (tm + d0 < a.ntiles_mode[m]) waitp(a, g.lt + d0 * muls[m]);
         }
       }
@@ -224,7 +231,10 @@ __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArg
       for (int m = 0; m < D; ++m) {
         const int tm = g.tco[m], p = a.ntiles_mode[m];
         int klo, khi;
-        if (part == 0) {
+        if (LAPD_ONEPASS) {
+          klo = tm + 1 < p ? a.bnd[m][tm + 1] : 0;
+          khi = tm + 1 < p ? a.dims[m] : 0;
+        } else if (part == 0) {
           klo = tm + 2 < p ? a.bnd[m][tm + 2] : 0;
           khi = tm + 2 < p ? a.dims[m] : 0;
         } else {
