@@ -310,7 +310,9 @@ def run_ours(a, rank, world, local):
         line = {
             "metric": METRIC, "value": world * N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True,
+            # N > 1 for C1/C2/C4 runs the same problem sharded (run_sharded): strong
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded RandomStream, BASELINE.json distributions)",
             "config": {"workload": a.config, "desc": desc, "dims": list(dims),
                        "unknowns": N, "l2": "inputs larger than L2 (8N bytes per tensor, "
