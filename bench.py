@@ -198,7 +198,7 @@ def run_reference(a, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
         "steps": a.steps, "warmup": min(a.warmup, 1), "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded RandomStream, BASELINE.json distributions)",
         "config": {"workload": a.config, "desc": desc, "dims": list(dims),
                    "reference_config": cfg_name},
