@@ -22,6 +22,7 @@
 // Reference: lap_rec / lap_base (laplace.hpp:99-153), mode_multiply update
 // (laplace.hpp:147), block_back_substitution (kernels.hpp:179-261).
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "solve.h"
@@ -64,6 +65,7 @@ struct G16 {
   int start[3], ext[3], tco[3];
   int nlo[3], flo[3];  // first rows of tiles t+1 and t+2 per mode (n_m when absent)
   int nch;             // chunks of this tile
+  int done;            // decoupled kernel: no more tiles
   int nc[3];           // Schur cells (1x1 / 2x2) of the tile's diagonal blocks
   unsigned char cs[3][16], cz[3][16];
 };
@@ -519,6 +521,211 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Decoupled variant: the producer warp runs one tile ahead of the consumers.
+// It claims the next tile, publishes its geometry through a two-slot queue
+// (mbarriers), loads its bases into the other half of a double-buffered
+// table region and streams its first update boxes while the consumers are
+// still in the previous tile's base case and scatter; the B~ tile goes into
+// xr once the consumers signal that the previous tile has been scattered.
+// The base case works in xr and the xi region (so the two-stage ring is
+// never touched by the consumers outside the update phase).
+// ---------------------------------------------------------------------------
+constexpr int D_OFF_VH = 2 * TD, D_OFF_RING = D_OFF_VH + 6 * VHS;
+constexpr int D_BYTES = (D_OFF_RING + 2 * TD) * 8;
+static_assert((D_OFF_RING * 8) % 128 == 0, "TMA destinations 128-byte aligned");
+
+TSG_DEVINL void fill_geometry(const SolveArgs& a, G16& g, int q, int lane) {
+  if (lane < 3) {
+    const unsigned long long pk = a.ocoord[q];
+    const int tm = static_cast<int>((pk >> (10 * lane)) & 1023);
+    const TileMode& src = a.tmode[lane][tm];
+    g.tco[lane] = tm;
+    g.start[lane] = src.start;
+    g.ext[lane] = src.ext;
+    g.nc[lane] = src.nc;
+    for (int k = 0; k < 16; ++k) {
+      g.cs[lane][k] = src.cs[k];
+      g.cz[lane][k] = src.cz[k];
+    }
+    const int p = a.ntiles_mode[lane];
+    g.nlo[lane] = tm + 1 < p ? a.bnd[lane][tm + 1] : a.dims[lane];
+    g.flo[lane] = tm + 2 < p ? a.bnd[lane][tm + 2] : a.dims[lane];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    g.lt = a.order[q];
+    g.gbase = static_cast<int64_t>(g.start[0]) + static_cast<int64_t>(g.start[1]) * a.stride[1] +
+              static_cast<int64_t>(g.start[2]) * a.stride[2];
+    int nch = 0;
+    for (int m = 0; m < 3; ++m) {
+      nch += a.dims[m] > g.flo[m] ? (a.dims[m] - g.flo[m] + E - 1) / E : 0;
+      nch += g.flo[m] > g.nlo[m] ? (g.flo[m] - g.nlo[m] + E - 1) / E : 0;
+    }
+    g.nch = (a.dbg & 4) ? 0 : nch;
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    solve_lap16d_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tmx) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ G16 gq[2];
+  __shared__ __align__(8) uint64_t full[2], empty[2], bar_x, bar_v[2], info_full[2], info_empty[2], xr_free;
+  double* xr = smem;
+  double* yb = smem + TD;
+  double* vhb = smem + D_OFF_VH;
+  double* ring = smem + D_OFF_RING;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, CW);
+      mbar_init(bar_v + s, 1);
+      mbar_init(info_full + s, 1);
+      mbar_init(info_empty + s, 1);
+    }
+    mbar_init(&bar_x, 1);
+    mbar_init(&xr_free, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t mul[3] = {1, a.ntiles_mode[0], static_cast<int64_t>(a.ntiles_mode[0]) * a.ntiles_mode[1]};
+
+  if (warp == CW) {
+    // ---------------- producer warp ----------------
+    unsigned gch = 0;
+    for (int it = 0;; ++it) {
+      const int slot = it & 1;
+      if (it >= 2) mbar_wait(&info_empty[slot], ((it >> 1) - 1) & 1);
+      G16& g = gq[slot];
+      int q = 0;
+      if (lane == 0) q = atomicAdd(a.counter, 1);
+      q = __shfl_sync(0xffffffffu, q, 0);
+      const bool done = q >= a.ntiles;
+      if (!done) fill_geometry(a, g, q, lane);
+      if (lane == 0) g.done = done ? 1 : 0;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&info_full[slot]);
+      if (done) break;
+      if (lane == 0) {
+        double* vh = vhb + slot * 3 * VHS;
+        mbar_expect_tx(&bar_v[slot], 3 * VHS * 8);
+        for (int m = 0; m < 3; ++m)
+          bulk_g2s(vh + m * VHS, a.vhat[m] + static_cast<int64_t>(g.tco[m]) * VHS, VHS * 8, &bar_v[slot]);
+        const int nch = g.nch;
+        bool bx = false;
+        auto issue_bx = [&]() {
+          if (it >= 1) mbar_wait(&xr_free, (it - 1) & 1);  // previous tile scattered
+          mbar_expect_tx(&bar_x, BOX_BYTES);
+          tma_load_3d(xr, &tmx, g.start[0] & ~1, g.start[1], g.start[2], &bar_x);
+          bx = true;
+        };
+        if (nch == 0) issue_bx();
+        for (int c = 0; c < nch; ++c, ++gch) {
+          const Chunk ch = chunk_of(g, a.dims, c);
+          const int m = ch.m % 3;
+          if (ch.first) {
+            wait_tile(a, g.lt + (ch.m < 3 ? 2 : 1) * mul[m]);
+            fence_proxy_async();
+          }
+          const int s = gch & 1;
+          if (gch >= 2) mbar_wait(empty + s, ((gch >> 1) - 1) & 1);
+          int cc[3] = {g.start[0], g.start[1], g.start[2]};
+          cc[m] = ch.k;
+          mbar_expect_tx(full + s, BOX_BYTES);
+          tma_load_3d(ring + s * TD, &tmx, cc[0] & ~1, cc[1], cc[2], full + s);
+          if (!bx && (c == 1 || c + 1 == nch)) issue_bx();  // two boxes in flight first
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- consumers ----------------
+    unsigned gch = 0;
+    for (int it = 0;; ++it) {
+      const int slot = it & 1;
+      mbar_wait(&info_full[slot], (it >> 1) & 1);
+      const G16& g = gq[slot];
+      if (g.done) break;
+      const int nch = g.nch;
+      double acc[3][2][4][2];
+#pragma unroll
+      for (int m = 0; m < 3; ++m)
+#pragma unroll
+        for (int rb = 0; rb < 2; ++rb)
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) acc[m][rb][cb][0] = acc[m][rb][cb][1] = 0.0;
+      double af[4][2], an[4][2];
+      Chunk ch = chunk_of(g, a.dims, 0);
+      if (nch > 0) chunk_afrag(a, g, ch.m % 3, ch.k, ch.kh, af);
+      for (int c = 0; c < nch; ++c, ++gch) {
+        const Chunk cn = chunk_of(g, a.dims, c + 1);
+        if (c + 1 < nch) chunk_afrag(a, g, cn.m % 3, cn.k, cn.kh, an);
+        const int s = gch & 1;
+        mbar_wait(full + s, (gch >> 1) & 1);
+        const int m = ch.m % 3;
+        const double* box = ring + s * TD + ((m == 0 ? ch.k : g.start[0]) & 1);
+        if (m == 0) chunk_dmma<0>(box, af, acc[0]);
+        else if (m == 1) chunk_dmma<1>(box, af, acc[1]);
+        else chunk_dmma<2>(box, af, acc[2]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) af[ks][0] = an[ks][0], af[ks][1] = an[ks][1];
+        ch = cn;
+      }
+      mbar_wait(&bar_x, it & 1);
+      double* xo = xr + (g.start[0] & 1);
+      flush16<0>(xo, acc[0]);
+      consumers_sync();
+      flush16<1>(xo, acc[1]);
+      consumers_sync();
+      flush16<2>(xo, acc[2]);
+      consumers_sync();
+      mbar_wait(&bar_v[slot], (it >> 1) & 1);
+      const double* vh = vhb + slot * 3 * VHS;
+      const int* ex = g.ext;
+      constexpr int VRI = 0, VRR = EE;
+      cmode16<0, false, false, false>(xo, nullptr, yb, nullptr, vh + VRI, vh + VRI, vh, ex, a.tiny);
+      consumers_sync();
+      cmode16<1, false, false, false>(yb, nullptr, xr, nullptr, vh + VHS + VRI, vh + VHS + VRI, vh, ex, a.tiny);
+      consumers_sync();
+      cmode16<2, false, false, false>(xr, nullptr, yb, nullptr, vh + 2 * VHS + VRI, vh + 2 * VHS + VRI, vh, ex,
+                                      a.tiny);
+      consumers_sync();
+      const bool sing = cell_solve16(yb, g, vh, a.tiny);
+      consumers_sync();
+      cmode16<0, false, false, false>(yb, nullptr, xr, nullptr, vh + VRR, vh + VRR, vh, ex, a.tiny);
+      consumers_sync();
+      cmode16<1, false, false, false>(xr, nullptr, yb, nullptr, vh + VHS + VRR, vh + VHS + VRR, vh, ex, a.tiny);
+      consumers_sync();
+      cmode16<2, false, false, false>(yb, nullptr, xr, nullptr, vh + 2 * VHS + VRR, vh + 2 * VHS + VRR, vh, ex,
+                                      a.tiny);
+      if (sing) atomicMin(a.status, static_cast<int>(g.lt < 0x7f7f7f7e ? g.lt : 0x7f7f7f7e));
+      consumers_sync();
+      const int e0 = g.ext[0], e1 = g.ext[1], e2 = g.ext[2];
+      for (int l = tid; l < TT; l += CW * 32) {
+        const int i0 = l & (E - 1), i1 = (l >> 4) & (E - 1), i2 = l >> 8;
+        if (i0 < e0 && i1 < e1 && i2 < e2)
+          a.X[g.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2]] = xr[i0 + S1 * i1 + S2 * i2];
+      }
+      fence_proxy_async();  // this thread's generic xr / xi accesses before the next TMA into them
+      consumers_sync();
+      if (tid == 0) {
+        __threadfence();
+        st_release(a.flags + g.lt, a.epoch);
+        if (a.trace) {
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+          a.trace[g.lt] = tt;
+        }
+        mbar_arrive(&xr_free);
+        mbar_arrive(&info_empty[slot]);
+      }
+    }
+  }
+}
+
 }  // namespace
 
 TileCaps solve_lap16_caps() { return TileCaps{E, TT, EE}; }
@@ -530,6 +737,24 @@ cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchI
                             static_cast<uint64_t>(a.dims[2])};
   const uint32_t box[3] = {BX, BY, BZ};
   if (!encode_tmap_f64(&map, a.X, 3, dims, box)) return cudaErrorInvalidValue;
+#ifndef L16_DEC
+#define L16_DEC 1
+#endif
+  if (L16_DEC || std::getenv("TSG_L16DEC")) {
+    static int nsm2 = 0;
+    if (nsm2 == 0) {
+      cudaError_t e = cudaFuncSetAttribute(solve_lap16d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D_BYTES);
+      if (e != cudaSuccess) return e;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm2, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int64_t grid = nsm2;
+    if (grid > a.ntiles) grid = a.ntiles;
+    if (info) *info = SolveLaunchInfo{static_cast<int>(grid), THREADS, D_BYTES, 1};
+    solve_lap16d_kernel<<<static_cast<unsigned>(grid), THREADS, D_BYTES, st>>>(a, map);
+    return cudaGetLastError();
+  }
   static int nsm = 0;
   if (nsm == 0) {
     cudaError_t e = cudaFuncSetAttribute(solve_lap16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BYTES);
