@@ -531,8 +531,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 // The base case works in xr and the xi region (so the two-stage ring is
 // never touched by the consumers outside the update phase).
 // ---------------------------------------------------------------------------
+#ifndef L16_DNS
+#define L16_DNS 2
+#endif
+constexpr int DNS = L16_DNS;  // ring stages of the decoupled kernel
 constexpr int D_OFF_VH = 2 * TD, D_OFF_RING = D_OFF_VH + 6 * VHS;
-constexpr int D_BYTES = (D_OFF_RING + 2 * TD) * 8;
+constexpr int D_BYTES = (D_OFF_RING + DNS * TD) * 8;
 static_assert((D_OFF_RING * 8) % 128 == 0, "TMA destinations 128-byte aligned");
 
 TSG_DEVINL void fill_geometry(const SolveArgs& a, G16& g, int q, int lane) {
@@ -570,16 +574,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     solve_lap16d_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tmx) {
   extern __shared__ __align__(128) double smem[];
   __shared__ G16 gq[2];
-  __shared__ __align__(8) uint64_t full[2], empty[2], bar_x, bar_v[2], info_full[2], info_empty[2], xr_free;
+  __shared__ __align__(8) uint64_t full[DNS], empty[DNS], bar_x, bar_v[2], info_full[2], info_empty[2], xr_free;
   double* xr = smem;
   double* yb = smem + TD;
   double* vhb = smem + D_OFF_VH;
   double* ring = smem + D_OFF_RING;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < DNS; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, CW);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(bar_v + s, 1);
       mbar_init(info_full + s, 1);
       mbar_init(info_empty + s, 1);
@@ -628,13 +634,13 @@ __global__ void __launch_bounds__(THREADS, 1)
             wait_tile(a, g.lt + (ch.m < 3 ? 2 : 1) * mul[m]);
             fence_proxy_async();
           }
-          const int s = gch & 1;
-          if (gch >= 2) mbar_wait(empty + s, ((gch >> 1) - 1) & 1);
+          const int s = gch % DNS;
+          if (gch >= DNS) mbar_wait(empty + s, ((gch / DNS) - 1) & 1);
           int cc[3] = {g.start[0], g.start[1], g.start[2]};
           cc[m] = ch.k;
           mbar_expect_tx(full + s, BOX_BYTES);
           tma_load_3d(ring + s * TD, &tmx, cc[0] & ~1, cc[1], cc[2], full + s);
-          if (!bx && (c == 1 || c + 1 == nch)) issue_bx();  // two boxes in flight first
+          if (!bx && (c == DNS - 1 || c + 1 == nch)) issue_bx();  // ring filled first
         }
       }
       __syncwarp();
@@ -661,8 +667,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int c = 0; c < nch; ++c, ++gch) {
         const Chunk cn = chunk_of(g, a.dims, c + 1);
         if (c + 1 < nch) chunk_afrag(a, g, cn.m % 3, cn.k, cn.kh, an);
-        const int s = gch & 1;
-        mbar_wait(full + s, (gch >> 1) & 1);
+        const int s = gch % DNS;
+        mbar_wait(full + s, (gch / DNS) & 1);
         const int m = ch.m % 3;
         const double* box = ring + s * TD + ((m == 0 ? ch.k : g.start[0]) & 1);
         if (m == 0) chunk_dmma<0>(box, af, acc[0]);
