@@ -34,7 +34,6 @@ namespace {
 #endif
 constexpr int EP = LAPD_EP, THREADS = EP / 4, WARPS = THREADS / 32;
 constexpr int VHS = kVhStride;  // 8x8 complex records (tile_eigvecs<8>)
-constexpr int NBMAX = EP / 2 / 8 / WARPS;  // 8-column blocks per warp, P_m >= 2
 
 template <int D>
 struct GD {
@@ -73,8 +72,8 @@ TSG_DEVINL void cross_of(const SolveArgs& a, const GD<D>& g, int m, int n, int& 
 // xr -= sum_k X(cross, k) T_m(rows, k) over rows k in [klo, khi) of mode m
 // (cross-section of ep >> log2 P_m columns, 8-column blocks dealt to the
 // warps, NBMAX blocks per warp and round)
-template <int D>
-TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int ep, int m, int klo, int khi) {
+template <int D, int NB, int UB>
+TSG_DEVINL void update_nb(const SolveArgs& a, const GD<D>& g, double* xr, int ep, int m, int klo, int khi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int lpm = a.tlog[m], shm = a.tsh[m];
@@ -85,13 +84,13 @@ TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int 
   const double* Tm = a.T[m];
   const int row = g.start[m] + gq;  // B fragment: T_m[row][k], rows beyond the tile give 0
   const bool rok = gq < g.ext[m];
-  for (int base = warp; base < nblk; base += WARPS * NBMAX) {
-    int ltc[NBMAX];
-    int64_t goc[NBMAX];
-    bool cok[NBMAX];
-    double acc[NBMAX][2];
+  for (int base = warp; base < nblk; base += WARPS * NB) {
+    int ltc[NB];
+    int64_t goc[NB];
+    bool cok[NB];
+    double acc[NB][2];
 #pragma unroll
-    for (int j = 0; j < NBMAX; ++j) {
+    for (int j = 0; j < NB; ++j) {
       const int b = base + WARPS * j;
       acc[j][0] = acc[j][1] = 0.0;
       ltc[j] = 0;
@@ -99,21 +98,26 @@ TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int 
       cok[j] = b < nblk && 8 * b + gq < cross;
       if (cok[j]) cross_of<D>(a, g, m, 8 * b + gq, ltc[j], goc[j]);
     }
-    for (int k0 = klo; k0 < khi; k0 += 4) {
-      const int k = k0 + tq;
-      const bool kok = k < khi;
-      const double bt = (kok && rok) ? __ldg(Tm + row + static_cast<int64_t>(k) * nm) : 0.0;
-      double av[NBMAX];
+    for (int k0 = klo; k0 < khi; k0 += 4 * UB) {
+      double bt[UB], av[UB][NB];
 #pragma unroll
-      for (int j = 0; j < NBMAX; ++j)
-        av[j] = (cok[j] && kok) ? ld_cg(a.X + goc[j] + static_cast<int64_t>(k) * sm) : 0.0;
+      for (int u = 0; u < UB; ++u) {
+        const int k = k0 + 4 * u + tq;
+        const bool kok = k < khi;
+        bt[u] = (kok && rok) ? __ldg(Tm + row + static_cast<int64_t>(k) * nm) : 0.0;
 #pragma unroll
-      for (int j = 0; j < NBMAX; ++j)
-        if (base + WARPS * j < nblk) dmma(acc[j][0], acc[j][1], av[j], bt);
+        for (int j = 0; j < NB; ++j)
+          av[u][j] = (cok[j] && kok) ? ld_cg(a.X + goc[j] + static_cast<int64_t>(k) * sm) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (base + WARPS * j < nblk) dmma(acc[j][0], acc[j][1], av[u][j], bt[u]);
     }
     // C[g][2t+h]: cross column 8b + g, row 2t + h of mode m
 #pragma unroll
-    for (int j = 0; j < NBMAX; ++j) {
+    for (int j = 0; j < NB; ++j) {
       if (!cok[j]) continue;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -122,6 +126,20 @@ TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int 
       }
     }
   }
+}
+
+#ifndef LAPD_NB
+#define LAPD_NB 4
+#endif
+#ifndef LAPD_UBK
+#define LAPD_UBK 4
+#endif
+// xr -= sum_k X(cross, k) T_m(rows, k) over rows k in [klo, khi) of mode m
+// (cross-section of ep >> log2 P_m columns in 8-column blocks dealt to the
+// warps, LAPD_NB blocks per round and LAPD_UBK k4-steps per load batch)
+template <int D>
+TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int ep, int m, int klo, int khi) {
+  update_nb<D, LAPD_NB, LAPD_UBK>(a, g, xr, ep, m, klo, khi);
 }
 
 template <int D>
