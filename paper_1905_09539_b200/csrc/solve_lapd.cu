@@ -72,6 +72,50 @@ TSG_DEVINL void cross_of(const SolveArgs& a, const GD<D>& g, int m, int n, int& 
 // xr -= sum_k X(cross, k) T_m(rows, k) over rows k in [klo, khi) of mode m
 // (cross-section of ep >> log2 P_m columns, 8-column blocks dealt to the
 // warps, NBMAX blocks per warp and round)
+// tile-local offset of the first element of fibre f along mode m
+template <int D>
+TSG_DEVINL int fibre_lt(const SolveArgs& a, int m, int f) {
+  int lt = 0, rem = f;
+#pragma unroll
+  for (int v = 0; v < D; ++v) {
+    if (v == m) continue;
+    const int lp = a.tlog[v];
+    lt += (rem & ((1 << lp) - 1)) << a.tsh[v];
+    rem >>= lp;
+  }
+  return lt;
+}
+
+// (xr, xi) fibres along mode m (padded extent P) times the 8x8-record
+// complex matrix (re at Vr, im at Vr + 64; the tile's P x P block)
+template <int D, int P>
+TSG_DEVINL void fibre_cmode(const SolveArgs& a, const GD<D>& g, double* xr, double* xi, const double* Vr,
+                            int ep, int m) {
+  const double* Vi = Vr + 64;
+  const int shm = a.tsh[m];
+  for (int f = threadIdx.x; f < ep / P; f += THREADS) {
+    const int lt0 = fibre_lt<D>(a, m, f);
+    double zr[P], zi[P];
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      zr[r] = xr[lt0 + (r << shm)];
+      zi[r] = xi[lt0 + (r << shm)];
+    }
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      double sr = 0.0, si = 0.0;
+#pragma unroll
+      for (int c = 0; c < P; ++c) {
+        const double ar = Vr[8 * r + c], ai = Vi[8 * r + c];
+        sr = fma(ar, zr[c], fma(-ai, zi[c], sr));
+        si = fma(ar, zi[c], fma(ai, zr[c], si));
+      }
+      xr[lt0 + (r << shm)] = sr;
+      xi[lt0 + (r << shm)] = si;
+    }
+  }
+}
+
 template <int D, int NB, int UB>
 TSG_DEVINL void update_nb(const SolveArgs& a, const GD<D>& g, double* xr, int ep, int m, int klo, int khi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -269,34 +313,12 @@ __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArg
     for (int pass = 0; pass < 2; ++pass) {  // 0: x V^-1 on every mode, 1: x V
 #pragma unroll 1
       for (int m = 0; m < D; ++m) {
-        const int lpm = a.tlog[m], pm = 1 << lpm, shm = a.tsh[m];
         const double* Vr = vh + m * VHS + (pass == 0 ? 0 : 128);
-        const double* Vi = Vr + 64;
-        for (int f = tid; f < (ep >> lpm); f += THREADS) {
-          int lt0;
-          int64_t dummy;
-          cross_of<D>(a, g, m, f, lt0, dummy);
-          double zr[8], zi[8];
-#pragma unroll
-          for (int r = 0; r < 8; ++r)
-            if (r < pm) {
-              zr[r] = xr[lt0 + (r << shm)];
-              zi[r] = xi[lt0 + (r << shm)];
-            }
-#pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            if (r >= pm) continue;
-            double sr = 0.0, si = 0.0;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              if (c >= pm) continue;
-              const double ar = Vr[8 * r + c], ai = Vi[8 * r + c];
-              sr = fma(ar, zr[c], fma(-ai, zi[c], sr));
-              si = fma(ar, zi[c], fma(ai, zr[c], si));
-            }
-            xr[lt0 + (r << shm)] = sr;
-            xi[lt0 + (r << shm)] = si;
-          }
+        switch (a.tlog[m]) {
+          case 0: fibre_cmode<D, 1>(a, g, xr, xi, Vr, ep, m); break;
+          case 1: fibre_cmode<D, 2>(a, g, xr, xi, Vr, ep, m); break;
+          case 2: fibre_cmode<D, 4>(a, g, xr, xi, Vr, ep, m); break;
+          default: fibre_cmode<D, 8>(a, g, xr, xi, Vr, ep, m); break;
         }
         __syncthreads();
       }
