@@ -136,56 +136,71 @@ TSG_DEVINL void update_src(const SolveArgs& a, const GG<D>& g, double* dst, doub
   else update_nb<D, 8, 2>(a, g, dst, sign, ep, m, klo, khi, Tm, src);
 }
 
-// buf(fibre along m) = M (P x P, row-major stride 8) * buf(fibre) [+ add(fibre)]
+// tile-local offset of the first element of fibre f along mode m
 template <int D>
-TSG_DEVINL void rmode(const SolveArgs& a, const GG<D>& g, double* buf, const double* add, const double* M,
-                      int ep, int m, double sign = 1.0) {
-  const int lpm = a.tlog[m], pm = 1 << lpm, shm = a.tsh[m];
-  for (int f = threadIdx.x; f < (ep >> lpm); f += THREADS) {
-    int lt0;
-    int64_t dummy;
-    cross_g<D>(a, g, m, f, lt0, dummy);
-    double x[8];
+TSG_DEVINL int fibre_lt(const SolveArgs& a, int m, int f) {
+  int lt = 0, rem = f;
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < pm) x[r] = buf[lt0 + (r << shm)];
+  for (int v = 0; v < D; ++v) {
+    if (v == m) continue;
+    const int lp = a.tlog[v];
+    lt += (rem & ((1 << lp) - 1)) << a.tsh[v];
+    rem >>= lp;
+  }
+  return lt;
+}
+
+// buf(fibre along m) = add(fibre) + sign * M (P x P of a row-major stride-8
+// block) buf(fibre), P the padded extent of mode m (compile time)
+template <int D, int P>
+TSG_DEVINL void rmode_p(const SolveArgs& a, double* buf, const double* add, const double* M, int ep, int m,
+                        double sign) {
+  const int shm = a.tsh[m];
+  for (int f = threadIdx.x; f < ep / P; f += THREADS) {
+    const int lt0 = fibre_lt<D>(a, m, f);
+    double x[P];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      if (r >= pm) continue;
+    for (int r = 0; r < P; ++r) x[r] = buf[lt0 + (r << shm)];
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
       double s = 0.0;
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < pm) s = fma(M[8 * r + c], x[c], s);
+      for (int c = 0; c < P; ++c) s = fma(M[8 * r + c], x[c], s);
       const int l = lt0 + (r << shm);
       buf[l] = (add ? add[l] : 0.0) + sign * s;
     }
   }
 }
 
-// complex mode product with an 8x8 table (re at Vr, im at Vr + 64)
 template <int D>
-TSG_DEVINL void cmode(const SolveArgs& a, const GG<D>& g, double* xr, double* xi, const double* Vr, int ep,
-                      int m) {
-  const int lpm = a.tlog[m], pm = 1 << lpm, shm = a.tsh[m];
+TSG_DEVINL void rmode(const SolveArgs& a, const GG<D>& g, double* buf, const double* add, const double* M,
+                      int ep, int m, double sign = 1.0) {
+  switch (a.tlog[m]) {
+    case 0: rmode_p<D, 1>(a, buf, add, M, ep, m, sign); break;
+    case 1: rmode_p<D, 2>(a, buf, add, M, ep, m, sign); break;
+    case 2: rmode_p<D, 4>(a, buf, add, M, ep, m, sign); break;
+    default: rmode_p<D, 8>(a, buf, add, M, ep, m, sign); break;
+  }
+}
+
+// complex mode product with an 8x8 table (re at Vr, im at Vr + 64)
+template <int D, int P>
+TSG_DEVINL void cmode_p(const SolveArgs& a, double* xr, double* xi, const double* Vr, int ep, int m) {
+  const int shm = a.tsh[m];
   const double* Vi = Vr + 64;
-  for (int f = threadIdx.x; f < (ep >> lpm); f += THREADS) {
-    int lt0;
-    int64_t dummy;
-    cross_g<D>(a, g, m, f, lt0, dummy);
-    double zr[8], zi[8];
+  for (int f = threadIdx.x; f < ep / P; f += THREADS) {
+    const int lt0 = fibre_lt<D>(a, m, f);
+    double zr[P], zi[P];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      if (r < pm) {
-        zr[r] = xr[lt0 + (r << shm)];
-        zi[r] = xi[lt0 + (r << shm)];
-      }
+    for (int r = 0; r < P; ++r) {
+      zr[r] = xr[lt0 + (r << shm)];
+      zi[r] = xi[lt0 + (r << shm)];
+    }
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      if (r >= pm) continue;
+    for (int r = 0; r < P; ++r) {
       double sr = 0.0, si = 0.0;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (c >= pm) continue;
+      for (int c = 0; c < P; ++c) {
         const double ar = Vr[8 * r + c], ai = Vi[8 * r + c];
         sr = fma(ar, zr[c], fma(-ai, zi[c], sr));
         si = fma(ar, zi[c], fma(ai, zr[c], si));
@@ -193,6 +208,17 @@ TSG_DEVINL void cmode(const SolveArgs& a, const GG<D>& g, double* xr, double* xi
       xr[lt0 + (r << shm)] = sr;
       xi[lt0 + (r << shm)] = si;
     }
+  }
+}
+
+template <int D>
+TSG_DEVINL void cmode(const SolveArgs& a, const GG<D>& g, double* xr, double* xi, const double* Vr, int ep,
+                      int m) {
+  switch (a.tlog[m]) {
+    case 0: cmode_p<D, 1>(a, xr, xi, Vr, ep, m); break;
+    case 1: cmode_p<D, 2>(a, xr, xi, Vr, ep, m); break;
+    case 2: cmode_p<D, 4>(a, xr, xi, Vr, ep, m); break;
+    default: cmode_p<D, 8>(a, xr, xi, Vr, ep, m); break;
   }
 }
 
