@@ -220,3 +220,42 @@ def test_plan_execute_stream_matches_single(gpu):
     assert rep.t_total_ms > 0
     for x, w in zip(xs, want):
         assert rel_diff(x, w) < 1e-15
+
+
+def _jordanish(n, lam, off, rng):
+    t = np.triu(rng.standard_normal((n, n))) * 0.3
+    t[np.arange(n), np.arange(n)] = lam
+    for i in range(n - 1):
+        t[i, i + 1] = off
+    return np.asfortranarray(t)
+
+
+# Defective (Jordan-like) diagonal blocks: the tiles' eigenvector bases do
+# not exist, so the plans fall back from the diagonalised tiles to the
+# wavefront base case (lap3) / the generic kernel; still nonsingular.
+@pytest.mark.parametrize("dims", [(24, 20, 18), (12, 10, 9, 8)])
+def test_laplace_defective_blocks_fallback(gpu, ref, dims):
+    rng = np.random.default_rng(11)
+    t = [_jordanish(n, 2.0 + 0.5 * m, 1.0, rng) for m, n in enumerate(dims)]
+    b = np.asfortranarray(rng.standard_normal(dims))
+    want = ref.laplace_recursive(t, b, 4)
+    got = gpu.laplace_recursive(t, b, 8)
+    assert rel_diff(got, want) < 1e-10
+
+
+# Ill-conditioned 2x2 Schur blocks (eigenbasis condition ~1e4): the plan
+# switches to the generic kernel with one refinement step per cell.
+def test_laplace_ill_conditioned_pairs_refine(gpu, ref):
+    rng = np.random.default_rng(12)
+    dims = (10, 12, 9)
+    t = []
+    for n in dims:
+        m = np.triu(rng.standard_normal((n, n))) * 0.2
+        m[np.arange(n), np.arange(n)] = 3.0 + rng.random(n)
+        m[0, 0] = m[1, 1] = 3.5
+        m[0, 1], m[1, 0] = 1e4, -1e-4  # eigenvalues 3.5 +- 1i, basis cond ~1e4
+        t.append(np.asfortranarray(m))
+    b = np.asfortranarray(rng.standard_normal(dims))
+    want = ref.laplace_recursive(t, b, 3)
+    got = gpu.laplace_recursive(t, b, 4)
+    assert rel_diff(got, want) < 1e-10
