@@ -29,7 +29,10 @@ namespace tsg {
 
 namespace {
 
-constexpr int BK = 16;
+#ifndef TSG_GEMM_BK
+#define TSG_GEMM_BK 16
+#endif
+constexpr int BK = TSG_GEMM_BK;
 #ifndef TSG_GEMM_STAGES
 #define TSG_GEMM_STAGES 3
 #endif
