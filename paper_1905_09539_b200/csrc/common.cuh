@@ -62,6 +62,9 @@ TSG_DEVINL int ld_acquire(const int* p) {
 TSG_DEVINL void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+// Programmatic dependent launch trigger: lets the next kernel in the stream
+// (a tile-flag-gated back transform) launch while this grid still runs.
+TSG_DEVINL void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 // System scope (tiles and flags shared with peer GPUs over NVLink).
 TSG_DEVINL int ld_acquire_sys(const int* p) {
   int v;

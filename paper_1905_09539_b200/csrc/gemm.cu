@@ -70,8 +70,20 @@ dgemm_nn_kernel(GemmArgs g) {
   const int64_t tiles_m = (g.M + BM - 1) / BM;
   const int64_t tiles_n = (g.N + BN - 1) / BN;
   const int64_t mt = bid % tiles_m;
-  const int64_t nt = (bid / tiles_m) % tiles_n;
+  int64_t nt = (bid / tiles_m) % tiles_n;
   const int64_t bt = bid / (tiles_m * tiles_n);
+  if (g.wflags) {
+    // Gated back transform: the solve releases the last columns first.
+    nt = tiles_n - 1 - nt;
+    const int c0 = static_cast<int>(nt * BN) / kWaitCols;
+    const int c1 = min(g.wgroups, static_cast<int>((nt * BN + BN + kWaitCols - 1) / kWaitCols));
+    for (int i = g.woff[c0] + tid; i < g.woff[c1]; i += NT) {
+      const int* f = g.wflags + g.wids[i];
+      while (ld_acquire(f) != g.wepoch) __nanosleep(256);
+    }
+    __threadfence();
+    __syncthreads();
+  }
   const int m0 = static_cast<int>(mt * BM), n0 = static_cast<int>(nt * BN);
 
   const double* __restrict__ A = g.A + bt * g.sA;
@@ -231,6 +243,28 @@ dgemm_nn_kernel(GemmArgs g) {
   }
 }
 
+template <typename K>
+void launch_k(K k, unsigned grid, int threads, int smem, const GemmArgs& g, cudaStream_t st) {
+  if (!g.pdl) {
+    k<<<grid, threads, smem, st>>>(g);
+    return;
+  }
+  // Programmatic dependent launch: the grid may start once every CTA of the
+  // preceding solve kernel has started (griddepcontrol.launch_dependents);
+  // its CTAs fill the SMs the solve releases and gate on tile flags.
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, g);
+}
+
 template <int BM, int BN, int WM, int WN>
 cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
   using S = GemmSmem<BM, BN>;
@@ -249,7 +283,7 @@ cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
       attr = true;
     }
-    k<<<static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, st>>>(g);
+    launch_k(k, static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, g, st);
   } else if (vec) {
     auto k = dgemm_nn_kernel<BM, BN, WM, WN, true>;
     static bool attr = false;
@@ -257,7 +291,7 @@ cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
       attr = true;
     }
-    k<<<static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, st>>>(g);
+    launch_k(k, static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, g, st);
   } else {
     auto k = dgemm_nn_kernel<BM, BN, WM, WN, false>;
     static bool attr = false;
@@ -265,7 +299,7 @@ cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
       attr = true;
     }
-    k<<<static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, st>>>(g);
+    launch_k(k, static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, g, st);
   }
   return cudaGetLastError();
 }
@@ -303,7 +337,7 @@ namespace tsg {
 
 cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int mode,
                          const double* A, const double* At, int r, double alpha, double beta,
-                         cudaStream_t st, double* flops) {
+                         cudaStream_t st, double* flops, const GemmArgs* gate) {
   int64_t P = 1, Q = 1;
   for (int v = 0; v < mode; ++v) P *= dims[v];
   for (int v = mode + 1; v < d; ++v) Q *= dims[v];
@@ -325,6 +359,14 @@ cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int
     g.sA = g.sB = g.sC = 0;
     g.batch = 1;
     if (Q > 0x7fffffffLL) return cudaErrorInvalidValue;
+    if (gate) {
+      g.wflags = gate->wflags;
+      g.woff = gate->woff;
+      g.wids = gate->wids;
+      g.wepoch = gate->wepoch;
+      g.wgroups = gate->wgroups;
+      g.pdl = gate->pdl;
+    }
   } else {
     // per slab q: Y_q (P x r) = X_q (P x n) * A^T (n x r)  (tensor.hpp:211-229)
     if (P > 0x7fffffffLL) return cudaErrorInvalidValue;

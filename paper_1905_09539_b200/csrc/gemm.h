@@ -17,7 +17,21 @@ struct GemmArgs {
   int64_t sA, sB, sC;
   int64_t batch;
   double alpha, beta;
+  // Optional tile-flag gate (back transform overlapped with the solve): the
+  // CTA owning columns [n0, n0+BN) of a mode-0 product first waits until
+  // wflags[wids[i]] == wepoch for i in [woff[n0/64], woff[ceil((n0+BN)/64)]);
+  // n-tiles are then issued last-column first, and with pdl the kernel is
+  // launched as a programmatic dependent of the preceding solve kernel.
+  const int* wflags = nullptr;
+  const int* woff = nullptr;
+  const int* wids = nullptr;
+  int wepoch = 0;
+  int wgroups = 0;  // number of 64-column groups (entries of woff minus one)
+  int pdl = 0;
 };
+
+// Column granularity of the GemmArgs tile-flag gate.
+constexpr int kWaitCols = 64;
 
 cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st);
 
@@ -26,7 +40,8 @@ cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st);
 // used for mode > 0).  Y has dims[mode] replaced by r.
 cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int mode,
                          const double* A, const double* At, int r, double alpha, double beta,
-                         cudaStream_t st, double* flops = nullptr);
+                         cudaStream_t st, double* flops = nullptr,
+                         const GemmArgs* gate = nullptr);
 
 // Fused small-mode transform (modes_small.cu): Y = X x_a A (x_{a+1} B when
 // pair), one HBM pass; extents 16, 24, 32 only (small_mode_ok).

@@ -54,6 +54,12 @@ struct tsg_plan {
   std::vector<int> tlog, tsh;  // solve_lapd padded tile layout
   int* flags = nullptr;
   int* counter = nullptr;   // [0] = queue head, [1] = status
+  // Back transform mode 0 gated on tile flags and launched as a programmatic
+  // dependent of the solve (overlaps the solve's drain): per 64-column group
+  // of X_(0), the linear ids of the tiles (0, t_1, .., t_{d-1}) it reads.
+  int* gate_off = nullptr;
+  int* gate_ids = nullptr;
+  int gate_groups = 0;
   int64_t ntiles = 0;
   std::vector<std::vector<int>> bds_h;  // host tile boundaries per mode
   std::vector<int> order_h;             // host topological order (linear tile ids)
@@ -81,6 +87,8 @@ struct tsg_plan {
     if (ocoord) cudaFree(ocoord);
     if (flags) cudaFree(flags);
     if (counter) cudaFree(counter);
+    if (gate_off) cudaFree(gate_off);
+    if (gate_ids) cudaFree(gate_ids);
     if (gexec) cudaGraphExecDestroy(gexec);
   }
 };

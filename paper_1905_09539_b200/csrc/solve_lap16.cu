@@ -324,6 +324,7 @@ TSG_DEVINL void wait_tile(const SolveArgs& a, int64_t tile) {
 
 __global__ void __launch_bounds__(THREADS, 1)
     solve_lap16_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tmx) {
+  pdl_trigger();
   extern __shared__ __align__(128) double smem[];
   __shared__ G16 g;
   __shared__ int s_tile;
@@ -572,6 +573,7 @@ TSG_DEVINL void fill_geometry(const SolveArgs& a, G16& g, int q, int lane) {
 
 __global__ void __launch_bounds__(THREADS, 1)
     solve_lap16d_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tmx) {
+  pdl_trigger();
   extern __shared__ __align__(128) double smem[];
   __shared__ G16 gq[2];
   __shared__ __align__(8) uint64_t full[DNS], empty[DNS], bar_x, bar_v[2], info_full[2], info_empty[2], xr_free;

@@ -487,6 +487,7 @@ TSG_DEVINL bool l3d_mode(const double* sr, const double* si, double* dr, double*
 template <int LT, bool DIST>
 __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     solve_lap3_kernel(SolveArgs a) {
+  pdl_trigger();
   using C = L3C<LT>;
   constexpr int E = C::E, L3_T = C::T, L3_THREADS = C::THREADS;
   constexpr int EE = E * E, MSK = E - 1;

@@ -188,6 +188,7 @@ TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int 
 
 template <int D>
 __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArgs a) {
+  pdl_trigger();
   __shared__ __align__(16) double xr[EP];
   __shared__ __align__(16) double xi[EP];
   __shared__ __align__(16) double vh[D * VHS];

@@ -259,3 +259,37 @@ def test_laplace_ill_conditioned_pairs_refine(gpu, ref):
     want = ref.laplace_recursive(t, b, 3)
     got = gpu.laplace_recursive(t, b, 4)
     assert rel_diff(got, want) < 1e-10
+
+
+# The back transform's mode-0 GEMM is gated on tile flags and launched as a
+# programmatic dependent of the solve (plan.cpp gate_*); with TSG_GATE=0 it
+# runs after the solve.  Same arithmetic in the same order -> bit-identical.
+_GATE_SCRIPT = r"""
+import hashlib, os, sys
+import numpy as np
+sys.path.insert(0, os.getcwd())
+import paper_1905_09539_b200 as T
+cfg = T.SolverConfig(strategy=T.Strategy.recursion_only, arithmetic=T.Arithmetic.real_quasitriangular)
+out = []
+for dims, seed in [((70, 45, 33), 1), ((96, 66, 80), 2), ((40, 9, 8, 7), 3)]:
+    p = T.make_problem(2, dims, seed=seed)
+    x = np.ascontiguousarray(T.solve_laplace(p, cfg).solution)
+    out.append(hashlib.sha256(x.tobytes()).hexdigest()[:16])
+print(" ".join(out))
+"""
+
+
+def test_gated_back_transform_bitexact():
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for g in ("0", "1"):
+        env = dict(os.environ, TSG_GATE=g, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", _GATE_SCRIPT], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[g] = r.stdout.strip().splitlines()[-1]
+    assert res["0"] == res["1"], res
