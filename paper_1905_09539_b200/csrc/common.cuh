@@ -7,6 +7,7 @@
 // with cp.async (LDGSTS) multi-stage pipelines.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 #define TSG_DEVINL __device__ __forceinline__
@@ -65,6 +66,28 @@ TSG_DEVINL void st_release(int* p, int v) {
 // Programmatic dependent launch trigger: lets the next kernel in the stream
 // (a tile-flag-gated back transform) launch while this grid still runs.
 TSG_DEVINL void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+// Wait for the preceding grid's completion and memory flush when this grid was
+// launched as a programmatic dependent (returns at once otherwise).
+TSG_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+// Host: launch `k` as a programmatic dependent of the previous kernel in `st`
+// (it may start once every CTA of that kernel has called pdl_trigger(); the
+// kernel must call pdl_wait() before touching the predecessor's outputs).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 // System scope (tiles and flags shared with peer GPUs over NVLink).
 TSG_DEVINL int ld_acquire_sys(const int* p) {
   int v;

@@ -72,6 +72,11 @@ dgemm_nn_kernel(GemmArgs g) {
   const int64_t mt = bid % tiles_m;
   int64_t nt = (bid / tiles_m) % tiles_n;
   const int64_t bt = bid / (tiles_m * tiles_n);
+  // Programmatic launches: wait for the producer of A/B (except the gated
+  // back transform, which waits on tile flags instead), then let the next
+  // kernel's CTAs be scheduled as this grid drains.
+  if (!g.wflags) pdl_wait();
+  pdl_trigger();
   if (g.wflags) {
     // Gated back transform: the solve releases the last columns first.
     nt = tiles_n - 1 - nt;
@@ -249,20 +254,7 @@ void launch_k(K k, unsigned grid, int threads, int smem, const GemmArgs& g, cuda
     k<<<grid, threads, smem, st>>>(g);
     return;
   }
-  // Programmatic dependent launch: the grid may start once every CTA of the
-  // preceding solve kernel has started (griddepcontrol.launch_dependents);
-  // its CTAs fill the SMs the solve releases and gate on tile flags.
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k, g);
+  launch_pdl(k, grid, threads, smem, st, g);
 }
 
 template <int BM, int BN, int WM, int WN>
@@ -365,7 +357,6 @@ cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int
       g.wids = gate->wids;
       g.wepoch = gate->wepoch;
       g.wgroups = gate->wgroups;
-      g.pdl = gate->pdl;
     }
   } else {
     // per slab q: Y_q (P x r) = X_q (P x n) * A^T (n x r)  (tensor.hpp:211-229)
@@ -384,6 +375,7 @@ cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int
     g.sC = P * r;
     g.batch = Q;
   }
+  if (gate) g.pdl = gate->pdl;
   if (flops) *flops += 2.0 * static_cast<double>(P) * Q * n * r;
   return dgemm_nn(g, st);
 }

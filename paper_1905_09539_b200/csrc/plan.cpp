@@ -1247,8 +1247,14 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
     const double* At = fwd ? pl->FwdT[m].p : pl->BwdT[m].p;
     cudaError_t e;
     if (ps[i].kind == 0) {
+      // GEMM after GEMM: programmatic launch (the next pass's CTAs are
+      // scheduled while this one drains; pdl_wait() orders the data).
+      tsg::GemmArgs chain{};
+      chain.pdl = 1;
+      const tsg::GemmArgs* opt = (i == 0 && m == 0) ? gate0
+                                 : (i > 0 && ps[i - 1].kind == 0) ? &chain : nullptr;
       e = tsg::mode_product(src, dst, d, pl->dims.data(), m, A, At, pl->dims[m], 1.0, 0.0, st,
-                            nullptr, i == 0 && m == 0 ? gate0 : nullptr);
+                            nullptr, opt);
     } else {
       const double* B = ps[i].kind == 2 ? (fwd ? pl->Fwd[m + 1].p : pl->Bwd[m + 1].p) : nullptr;
       e = tsg::mode_pair_small(src, dst, d, pl->dims.data(), m, ps[i].kind == 2, A, B, st);
@@ -1273,6 +1279,11 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   cudaEvent_t* ev = ctx->ev;
   pl->launches = 0;
   double* work = nullptr;
+  // Solve state reset first, so the forward GEMMs and the solve follow each
+  // other directly (programmatic launches).
+  TSG_CU(cudaMemsetAsync(pl->flags, 0, pl->ntiles * sizeof(int), st));
+  TSG_CU(cudaMemsetAsync(pl->counter, 0, sizeof(int), st));
+  TSG_CU(cudaMemsetAsync(pl->counter + 1, 0x7f, sizeof(int), st));  // kNoStatus
   // Forward transforms: outputs alternate w2/w1 and end in w1.
   if (!pl->reduced_only) {
     TSG_CU(transform_all(pl, in, pl->w1.p, pl->w2.p, true, st));
@@ -1284,9 +1295,6 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   }
   if (timing) TSG_CU(cudaEventRecord(ev[2], st));
   // Reduced solve.
-  TSG_CU(cudaMemsetAsync(pl->flags, 0, pl->ntiles * sizeof(int), st));
-  TSG_CU(cudaMemsetAsync(pl->counter, 0, sizeof(int), st));
-  TSG_CU(cudaMemsetAsync(pl->counter + 1, 0x7f, sizeof(int), st));  // kNoStatus
   tsg::SolveArgs a{};
   tsg_impl::fill_solve_args(pl, work, a);
   a.flags = pl->flags;

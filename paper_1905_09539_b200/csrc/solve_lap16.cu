@@ -324,6 +324,7 @@ TSG_DEVINL void wait_tile(const SolveArgs& a, int64_t tile) {
 
 __global__ void __launch_bounds__(THREADS, 1)
     solve_lap16_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tmx) {
+  pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) double smem[];
   __shared__ G16 g;
@@ -573,6 +574,7 @@ TSG_DEVINL void fill_geometry(const SolveArgs& a, G16& g, int q, int lane) {
 
 __global__ void __launch_bounds__(THREADS, 1)
     solve_lap16d_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tmx) {
+  pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) double smem[];
   __shared__ G16 gq[2];
@@ -760,8 +762,8 @@ cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchI
     int64_t grid = nsm2;
     if (grid > a.ntiles) grid = a.ntiles;
     if (info) *info = SolveLaunchInfo{static_cast<int>(grid), THREADS, D_BYTES, 1};
-    solve_lap16d_kernel<<<static_cast<unsigned>(grid), THREADS, D_BYTES, st>>>(a, map);
-    return cudaGetLastError();
+    cudaError_t le = launch_pdl(solve_lap16d_kernel, static_cast<unsigned>(grid), THREADS, D_BYTES, st, a, map);
+    return le != cudaSuccess ? le : cudaGetLastError();
   }
   static int nsm = 0;
   if (nsm == 0) {
@@ -774,8 +776,8 @@ cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchI
   int64_t grid = nsm;
   if (grid > a.ntiles) grid = a.ntiles;
   if (info) *info = SolveLaunchInfo{static_cast<int>(grid), THREADS, BYTES, 1};
-  solve_lap16_kernel<<<static_cast<unsigned>(grid), THREADS, BYTES, st>>>(a, map);
-  return cudaGetLastError();
+  cudaError_t le = launch_pdl(solve_lap16_kernel, static_cast<unsigned>(grid), THREADS, BYTES, st, a, map);
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 }  // namespace tsg

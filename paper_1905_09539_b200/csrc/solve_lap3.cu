@@ -487,6 +487,7 @@ TSG_DEVINL bool l3d_mode(const double* sr, const double* si, double* dr, double*
 template <int LT, bool DIST>
 __global__ void __launch_bounds__(L3C<LT>::THREADS, LT == 3 ? L3_MINB : 2)
     solve_lap3_kernel(SolveArgs a) {
+  pdl_wait();
   pdl_trigger();
   using C = L3C<LT>;
   constexpr int E = C::E, L3_T = C::T, L3_THREADS = C::THREADS;
@@ -1008,8 +1009,8 @@ cudaError_t launch_l3(const SolveArgs& a0, cudaStream_t st, SolveLaunchInfo* inf
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > a.ntiles) grid = a.ntiles;
   if (info) *info = SolveLaunchInfo{static_cast<int>(grid), C::THREADS, bytes, occ};
-  k<<<static_cast<unsigned>(grid), C::THREADS, bytes, st>>>(a);
-  return cudaGetLastError();
+  cudaError_t le = launch_pdl(k, static_cast<unsigned>(grid), C::THREADS, bytes, st, a);
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 }  // namespace

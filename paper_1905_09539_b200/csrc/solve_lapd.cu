@@ -188,6 +188,7 @@ TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int 
 
 template <int D>
 __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArgs a) {
+  pdl_wait();
   pdl_trigger();
   __shared__ __align__(16) double xr[EP];
   __shared__ __align__(16) double xi[EP];
@@ -392,8 +393,8 @@ cudaError_t launch_d(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info)
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > a.ntiles) grid = a.ntiles;
   if (info) *info = SolveLaunchInfo{static_cast<int>(grid), THREADS, 0, occ};
-  k<<<static_cast<unsigned>(grid), THREADS, 0, st>>>(a);
-  return cudaGetLastError();
+  cudaError_t le = launch_pdl(k, static_cast<unsigned>(grid), THREADS, 0, st, a);
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 }  // namespace
