@@ -44,7 +44,7 @@ cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int
                          const GemmArgs* gate = nullptr);
 
 // Fused small-mode transform (modes_small.cu): Y = X x_a A (x_{a+1} B when
-// pair), one HBM pass; extents 16, 24, 32 only (small_mode_ok).
+// pair), one HBM pass; extents 16, 24, 32, 40 only (small_mode_ok).
 bool small_mode_ok(int n);
 cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, int a, bool pair,
                             const double* A, const double* B, cudaStream_t st, double* flops = nullptr);

@@ -43,13 +43,19 @@ struct PairArgs {
 template <int N>
 TSG_DEVINL void fibres(double* blk, const double* M, int st, int nf) {
   constexpr int RB = N / 8, KS = N / 4;
+  // N <= 32: the matrix fragments live in registers; larger N reads them
+  // from shared memory per k-step (conflict-free: N = 8 mod 32 for 40)
+  constexpr bool REG = N <= 32;
+  constexpr int KR = REG ? KS : 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
-  double af[RB][KS];
+  double af[RB][KR];
+  if constexpr (REG) {
 #pragma unroll
-  for (int rb = 0; rb < RB; ++rb)
+    for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) af[rb][ks] = M[(8 * rb + gq) + N * (4 * ks + tq)];
+      for (int ks = 0; ks < KS; ++ks) af[rb][ks] = M[(8 * rb + gq) + N * (4 * ks + tq)];
+  }
   for (int fb = warp; fb < (nf >> 3); fb += THREADS / 32) {
     // fibre of this lane as B column: f = 8 fb + gq; as C column: 8 fb + 2 tq + h
     const int fB = 8 * fb + gq;
@@ -63,7 +69,10 @@ TSG_DEVINL void fibres(double* blk, const double* M, int st, int nf) {
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-      for (int rb = 0; rb < RB; ++rb) dmma(c[rb][0], c[rb][1], af[rb][ks], bf[ks]);
+      for (int rb = 0; rb < RB; ++rb) {
+        if constexpr (REG) dmma(c[rb][0], c[rb][1], af[rb][ks], bf[ks]);
+        else dmma(c[rb][0], c[rb][1], M[(8 * rb + gq) + N * (4 * ks + tq)], bf[ks]);
+      }
     __syncwarp();  // every row of the warp's 8 fibres has been read
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -143,13 +152,14 @@ cudaError_t dispatch_b(const PairArgs& g, cudaStream_t st) {
     case 16: return launch_pair<NA, 16>(g, st);
     case 24: return launch_pair<NA, 24>(g, st);
     case 32: return launch_pair<NA, 32>(g, st);
+    case 40: return launch_pair<NA, 40>(g, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 }  // namespace
 
-bool small_mode_ok(int n) { return n == 16 || n == 24 || n == 32; }
+bool small_mode_ok(int n) { return n == 16 || n == 24 || n == 32 || n == 40; }
 
 cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, int a, bool pair,
                             const double* A, const double* B, cudaStream_t st, double* flops) {
@@ -190,6 +200,7 @@ cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, 
     case 16: return dispatch_b<16>(g, st);
     case 24: return dispatch_b<24>(g, st);
     case 32: return dispatch_b<32>(g, st);
+    case 40: return dispatch_b<40>(g, st);
     default: return cudaErrorInvalidValue;
   }
 }

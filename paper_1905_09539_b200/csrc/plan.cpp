@@ -1213,7 +1213,7 @@ cudaError_t launch_plan_solve(tsg_plan* pl, const tsg::SolveArgs& a, cudaStream_
 }  // namespace tsg_impl
 
 // All-mode transform in -> target (ping-pong through `other`): per-mode DMMA
-// GEMMs, except consecutive small modes (n in {16, 24, 32}), which go
+// GEMMs, except consecutive small modes (n in {16, 24, 32, 40}), which go
 // through the fused shared-memory pass two at a time (modes_small.cu).
 cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double* other, bool fwd,
                           cudaStream_t st, const tsg::GemmArgs* gate0 = nullptr,

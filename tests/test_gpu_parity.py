@@ -155,7 +155,7 @@ def test_solve_gsylv_pipeline(gpu, ref, dims):
     assert rep.residual < RES
 
 
-@pytest.mark.parametrize("dims", [(40, 8, 8, 8), (60, 12, 12, 12)])
+@pytest.mark.parametrize("dims", [(40, 8, 8, 8), (60, 12, 12, 12), (30, 40, 40, 40)])
 def test_solve_gsylv_baseline_shape(gpu, ref, dims):
     p = gpu.make_problem(5, dims, seed=1)
     want, info = ref.solve_gsylv(p.coeffs, p.c, p.rhs)
@@ -179,8 +179,9 @@ def test_lap16_kernel_matches_reference(gpu, ref, kind, dims, monkeypatch):
 
 
 # Fused small-mode transforms (modes_small.cu): consecutive extents in
-# {16, 24, 32} are transformed two modes per HBM pass.
-@pytest.mark.parametrize("dims", [(16, 24, 32), (24, 24, 24, 16), (32, 16, 24, 24, 16), (7, 24, 24, 16)])
+# {16, 24, 32, 40} are transformed two modes per HBM pass.
+@pytest.mark.parametrize("dims", [(16, 24, 32), (24, 24, 24, 16), (32, 16, 24, 24, 16), (7, 24, 24, 16),
+                                  (40, 40, 24), (7, 40, 40, 16), (9, 16, 40)])
 def test_small_mode_transforms(gpu, ref, dims):
     p = gpu.make_problem(2, dims, seed=6)
     want, _ = ref.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
