@@ -50,40 +50,17 @@ TSG_DEVINL void waitp(const SolveArgs& a, int64_t tile) {
   }
 }
 
-// cross-section column n of mode m -> tile-local offset (mode m row 0) and
-// the clamped global offset of its fibre start (without mode m's start)
-template <int D>
-TSG_DEVINL void cross_of(const SolveArgs& a, const GD<D>& g, int m, int n, int& lt, int64_t& go) {
-  lt = 0;
-  go = 0;
-  int rem = n;
-#pragma unroll
-  for (int v = 0; v < D; ++v) {
-    if (v == m) continue;
-    const int lp = a.tlog[v];
-    const int iv = rem & ((1 << lp) - 1);
-    rem >>= lp;
-    lt += iv << a.tsh[v];
-    const int ic = iv < g.ext[v] ? iv : g.ext[v] - 1;
-    go += static_cast<int64_t>(g.start[v] + ic) * a.stride[v];
-  }
-}
-
 // xr -= sum_k X(cross, k) T_m(rows, k) over rows k in [klo, khi) of mode m
 // (cross-section of ep >> log2 P_m columns, 8-column blocks dealt to the
 // warps, NBMAX blocks per warp and round)
-// tile-local offset of the first element of fibre f along mode m
+// tile-local offset of the first element of fibre f along mode m: the
+// tile index is the concatenation of the modes' bit fields (mode 0 lowest),
+// so dropping mode m's field from a fibre index = inserting tlog[m] zero
+// bits at tsh[m]
 template <int D>
 TSG_DEVINL int fibre_lt(const SolveArgs& a, int m, int f) {
-  int lt = 0, rem = f;
-#pragma unroll
-  for (int v = 0; v < D; ++v) {
-    if (v == m) continue;
-    const int lp = a.tlog[v];
-    lt += (rem & ((1 << lp) - 1)) << a.tsh[v];
-    rem >>= lp;
-  }
-  return lt;
+  const int sh = a.tsh[m];
+  return (f & ((1 << sh) - 1)) | ((f >> sh) << (sh + a.tlog[m]));
 }
 
 // (xr, xi) fibres along mode m (padded extent P) times the 8x8-record
@@ -117,7 +94,8 @@ TSG_DEVINL void fibre_cmode(const SolveArgs& a, const GD<D>& g, double* xr, doub
 }
 
 template <int D, int NB, int UB>
-TSG_DEVINL void update_nb(const SolveArgs& a, const GD<D>& g, double* xr, int ep, int m, int klo, int khi) {
+TSG_DEVINL void update_nb(const SolveArgs& a, const GD<D>& g, double* xr, const int64_t* goff, int ep, int m,
+                          int klo, int khi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int lpm = a.tlog[m], shm = a.tsh[m];
@@ -125,39 +103,47 @@ TSG_DEVINL void update_nb(const SolveArgs& a, const GD<D>& g, double* xr, int ep
   const int nblk = (cross + 7) >> 3;
   const int nm = a.dims[m];
   const int64_t sm = a.stride[m];
-  const double* Tm = a.T[m];
   const int row = g.start[m] + gq;  // B fragment: T_m[row][k], rows beyond the tile give 0
   const bool rok = gq < g.ext[m];
+  // X(cross n, k) = X[goff[lt(n)] + (k - start_m) * stride_m]; padded cross
+  // columns (goff < 0) are skipped
+  const int64_t kofs = static_cast<int64_t>(klo + tq - g.start[m]) * sm;
+  const int64_t s4 = 4 * sm;
+  const double* pt0 = a.T[m] + row + static_cast<int64_t>(klo + tq) * nm;
+  const int64_t t4 = 4 * static_cast<int64_t>(nm);
   for (int base = warp; base < nblk; base += WARPS * NB) {
     int ltc[NB];
-    int64_t goc[NB];
+    const double* px[NB];
     bool cok[NB];
     double acc[NB][2];
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       const int b = base + WARPS * j;
+      const int n = 8 * b + gq;
       acc[j][0] = acc[j][1] = 0.0;
-      ltc[j] = 0;
-      goc[j] = 0;
-      cok[j] = b < nblk && 8 * b + gq < cross;
-      if (cok[j]) cross_of<D>(a, g, m, 8 * b + gq, ltc[j], goc[j]);
+      ltc[j] = (n & ((1 << shm) - 1)) | ((n >> shm) << (shm + lpm));
+      const int64_t go = (b < nblk && n < cross) ? goff[ltc[j]] : -1;
+      cok[j] = go >= 0;
+      px[j] = a.X + (cok[j] ? go + kofs : 0);
     }
+    const double* pt = pt0;
     for (int k0 = klo; k0 < khi; k0 += 4 * UB) {
       double bt[UB], av[UB][NB];
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
-        const int k = k0 + 4 * u + tq;
-        const bool kok = k < khi;
-        bt[u] = (kok && rok) ? __ldg(Tm + row + static_cast<int64_t>(k) * nm) : 0.0;
+        const bool kok = k0 + 4 * u + tq < khi;
+        bt[u] = (kok && rok) ? __ldg(pt + u * t4) : 0.0;
 #pragma unroll
-        for (int j = 0; j < NB; ++j)
-          av[u][j] = (cok[j] && kok) ? ld_cg(a.X + goc[j] + static_cast<int64_t>(k) * sm) : 0.0;
+        for (int j = 0; j < NB; ++j) av[u][j] = (cok[j] && kok) ? ld_cg(px[j] + u * s4) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < UB; ++u)
 #pragma unroll
         for (int j = 0; j < NB; ++j)
           if (base + WARPS * j < nblk) dmma(acc[j][0], acc[j][1], av[u][j], bt[u]);
+      pt += UB * t4;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) px[j] += UB * s4;
     }
     // C[g][2t+h]: cross column 8b + g, row 2t + h of mode m
 #pragma unroll
@@ -182,8 +168,9 @@ TSG_DEVINL void update_nb(const SolveArgs& a, const GD<D>& g, double* xr, int ep
 // (cross-section of ep >> log2 P_m columns in 8-column blocks dealt to the
 // warps, LAPD_NB blocks per round and LAPD_UBK k4-steps per load batch)
 template <int D>
-TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, int ep, int m, int klo, int khi) {
-  update_nb<D, LAPD_NB, LAPD_UBK>(a, g, xr, ep, m, klo, khi);
+TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, const int64_t* goff, int ep, int m,
+                            int klo, int khi) {
+  update_nb<D, LAPD_NB, LAPD_UBK>(a, g, xr, goff, ep, m, klo, khi);
 }
 
 template <int D>
@@ -193,6 +180,7 @@ __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArg
   __shared__ __align__(16) double xr[EP];
   __shared__ __align__(16) double xi[EP];
   __shared__ __align__(16) double vh[D * VHS];
+  __shared__ int64_t goff[EP];  // global offset of each tile element (-1: padding)
   __shared__ GD<D> g;
   __shared__ int s_tile;
   const int tid = threadIdx.x;
@@ -257,6 +245,7 @@ __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArg
       }
       cp_async8(xr + l, ok ? a.X + off : a.X, ok ? 8 : 0);
       xi[l] = 0.0;
+      goff[l] = ok ? off : -1;
     }
 #pragma unroll
     for (int m = 0; m < D; ++m) {
@@ -305,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArg
           klo = tm + 1 < p ? a.bnd[m][tm + 1] : 0;
           khi = tm + 1 < p ? (tm + 2 < p ? a.bnd[m][tm + 2] : a.dims[m]) : 0;
         }
-        if (khi > klo) update_mode<D>(a, g, xr, ep, m, klo, khi);
+        if (khi > klo) update_mode<D>(a, g, xr, goff, ep, m, klo, khi);
         __syncthreads();
       }
       mark(2 + part);
@@ -354,15 +343,8 @@ __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArg
     mark(4);
     // ---- scatter X_t (real part), release ----
     for (int l = tid; l < ep; l += THREADS) {
-      int64_t off = g.gbase;
-      bool ok = true;
-#pragma unroll
-      for (int v = 0; v < D; ++v) {
-        const int iv = (l >> a.tsh[v]) & ((1 << a.tlog[v]) - 1);
-        ok &= iv < g.ext[v];
-        off += static_cast<int64_t>(iv) * a.stride[v];
-      }
-      if (ok) a.X[off] = xr[l];
+      const int64_t off = goff[l];
+      if (off >= 0) a.X[off] = xr[l];
     }
     __syncthreads();
     if (tid == 0) {
