@@ -52,29 +52,12 @@ TSG_DEVINL void waitg(const SolveArgs& a, int64_t tile) {
   }
 }
 
-template <int D>
-TSG_DEVINL void cross_g(const SolveArgs& a, const GG<D>& g, int m, int n, int& lt, int64_t& go) {
-  lt = 0;
-  go = 0;
-  int rem = n;
-#pragma unroll
-  for (int v = 0; v < D; ++v) {
-    if (v == m) continue;
-    const int lp = a.tlog[v];
-    const int iv = rem & ((1 << lp) - 1);
-    rem >>= lp;
-    lt += iv << a.tsh[v];
-    const int ic = iv < g.ext[v] ? iv : g.ext[v] - 1;
-    go += static_cast<int64_t>(g.start[v] + ic) * a.stride[v];
-  }
-}
-
 // dst += sign * sum_k src(cross, k) Tm(rows, k) over rows k in [klo, khi).
 // NB 8-column blocks per warp and round, UB k4-steps of loads in flight
 // (NB * UB <= 16 fragment loads per batch).
 template <int D, int NB, int UB>
-TSG_DEVINL void update_nb(const SolveArgs& a, const GG<D>& g, double* dst, double sign, int ep, int m,
-                          int klo, int khi, const double* Tm, const double* src) {
+TSG_DEVINL void update_nb(const SolveArgs& a, const GG<D>& g, double* dst, const int64_t* goff, double sign, int ep,
+                          int m, int klo, int khi, const double* Tm, const double* src) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int lpm = a.tlog[m], shm = a.tsh[m];
@@ -84,36 +67,45 @@ TSG_DEVINL void update_nb(const SolveArgs& a, const GG<D>& g, double* dst, doubl
   const int64_t sm = a.stride[m];
   const int row = g.start[m] + gq;
   const bool rok = gq < g.ext[m];
+  // src(cross n, k) = src[goff[lt(n)] + (k - start_m) * stride_m] (goff < 0:
+  // padded cross column, skipped); lt(n) inserts mode m's zero bit field
+  const int64_t kofs = static_cast<int64_t>(klo + tq - g.start[m]) * sm;
+  const int64_t s4 = 4 * sm;
+  const double* pt0 = Tm + row + static_cast<int64_t>(klo + tq) * nm;
+  const int64_t t4 = 4 * static_cast<int64_t>(nm);
   for (int base = warp; base < nblk; base += WARPS * NB) {
     int ltc[NB];
-    int64_t goc[NB];
+    const double* px[NB];
     bool cok[NB];
     double acc[NB][2];
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       const int b = base + WARPS * j;
+      const int n = 8 * b + gq;
       acc[j][0] = acc[j][1] = 0.0;
-      ltc[j] = 0;
-      goc[j] = 0;
-      cok[j] = b < nblk && 8 * b + gq < cross;
-      if (cok[j]) cross_g<D>(a, g, m, 8 * b + gq, ltc[j], goc[j]);
+      ltc[j] = (n & ((1 << shm) - 1)) | ((n >> shm) << (shm + lpm));
+      const int64_t go = (b < nblk && n < cross) ? goff[ltc[j]] : -1;
+      cok[j] = go >= 0;
+      px[j] = src + (cok[j] ? go + kofs : 0);
     }
+    const double* pt = pt0;
     for (int k0 = klo; k0 < khi; k0 += 4 * UB) {
       double bt[UB], av[UB][NB];
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
-        const int k = k0 + 4 * u + tq;
-        const bool kok = k < khi;
-        bt[u] = (kok && rok) ? __ldg(Tm + row + static_cast<int64_t>(k) * nm) : 0.0;
+        const bool kok = k0 + 4 * u + tq < khi;
+        bt[u] = (kok && rok) ? __ldg(pt + u * t4) : 0.0;
 #pragma unroll
-        for (int j = 0; j < NB; ++j)
-          av[u][j] = (cok[j] && kok) ? ld_cg(src + goc[j] + static_cast<int64_t>(k) * sm) : 0.0;
+        for (int j = 0; j < NB; ++j) av[u][j] = (cok[j] && kok) ? ld_cg(px[j] + u * s4) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < UB; ++u)
 #pragma unroll
         for (int j = 0; j < NB; ++j)
           if (base + WARPS * j < nblk) dmma(acc[j][0], acc[j][1], av[u][j], bt[u]);
+      pt += UB * t4;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) px[j] += UB * s4;
     }
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
@@ -128,26 +120,20 @@ TSG_DEVINL void update_nb(const SolveArgs& a, const GG<D>& g, double* dst, doubl
 }
 
 template <int D>
-TSG_DEVINL void update_src(const SolveArgs& a, const GG<D>& g, double* dst, double sign, int ep, int m,
-                           int klo, int khi, const double* Tm, const double* src) {
+TSG_DEVINL void update_src(const SolveArgs& a, const GG<D>& g, double* dst, const int64_t* goff, double sign,
+                           int ep, int m, int klo, int khi, const double* Tm, const double* src) {
   const int nblk = ((ep >> a.tlog[m]) + 7) >> 3;
-  if (nblk <= 2 * WARPS) update_nb<D, 2, 8>(a, g, dst, sign, ep, m, klo, khi, Tm, src);
-  else if (nblk <= 4 * WARPS) update_nb<D, 4, 4>(a, g, dst, sign, ep, m, klo, khi, Tm, src);
-  else update_nb<D, 8, 2>(a, g, dst, sign, ep, m, klo, khi, Tm, src);
+  if (nblk <= 2 * WARPS) update_nb<D, 2, 8>(a, g, dst, goff, sign, ep, m, klo, khi, Tm, src);
+  else if (nblk <= 4 * WARPS) update_nb<D, 4, 4>(a, g, dst, goff, sign, ep, m, klo, khi, Tm, src);
+  else update_nb<D, 8, 2>(a, g, dst, goff, sign, ep, m, klo, khi, Tm, src);
 }
 
-// tile-local offset of the first element of fibre f along mode m
+// tile-local offset of the first element of fibre f along mode m (the
+// tile index concatenates the modes' bit fields: insert mode m's zero field)
 template <int D>
 TSG_DEVINL int fibre_lt(const SolveArgs& a, int m, int f) {
-  int lt = 0, rem = f;
-#pragma unroll
-  for (int v = 0; v < D; ++v) {
-    if (v == m) continue;
-    const int lp = a.tlog[v];
-    lt += (rem & ((1 << lp) - 1)) << a.tsh[v];
-    rem >>= lp;
-  }
-  return lt;
+  const int sh = a.tsh[m];
+  return (f & ((1 << sh) - 1)) | ((f >> sh) << (sh + a.tlog[m]));
 }
 
 // buf(fibre along m) = add(fibre) + sign * M (P x P of a row-major stride-8
@@ -233,6 +219,7 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
   __shared__ __align__(16) double rb[EP];         // R chain
   __shared__ __align__(16) double vh[(D - 1) * VHS];
   __shared__ double blk[D + 1][64];                // S_tt, A_m,tt (m >= 1), Tc_tt: 8x8 row-major
+  __shared__ int64_t goff[EP];                     // global offset per tile element (-1: padding)
   __shared__ GG<D> g;
   __shared__ int s_tile;
   const int tid = threadIdx.x;
@@ -282,6 +269,7 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
       }
       cp_async8(xr + l, ok ? a.X + off : a.X, ok ? 8 : 0);
       xi[l] = 0.0;
+      goff[l] = ok ? off : -1;
 #pragma unroll
       for (int m = 0; m < D - 1; ++m) lb[m][l] = 0.0;
     }
@@ -343,10 +331,10 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
         }
         if (khi <= klo) continue;
         if (m == 0) {
-          update_src<D>(a, g, xr, -1.0, ep, 0, klo, khi, a.T[0], a.X);
-          update_src<D>(a, g, xr, -1.0, ep, 0, klo, khi, a.Tc, a.W[1]);
+          update_src<D>(a, g, xr, goff, -1.0, ep, 0, klo, khi, a.T[0], a.X);
+          update_src<D>(a, g, xr, goff, -1.0, ep, 0, klo, khi, a.Tc, a.W[1]);
         } else {
-          update_src<D>(a, g, lb[m - 1], 1.0, ep, m, klo, khi, a.T[m], m == D - 1 ? a.X : a.W[m + 1]);
+          update_src<D>(a, g, lb[m - 1], goff, 1.0, ep, m, klo, khi, a.T[m], m == D - 1 ? a.X : a.W[m + 1]);
         }
       }
       __syncthreads();
@@ -378,9 +366,7 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
     {
       const int lp0 = a.tlog[0];
       for (int f = tid; f < (ep >> lp0); f += THREADS) {  // fibres along mode 0
-        int lt0;
-        int64_t dummy;
-        cross_g<D>(a, g, 0, f, lt0, dummy);
+        const int lt0 = f << lp0;
         // z = prod_m lambda_m(j_m) over the tail coordinates of the fibre
         double zr = 1.0, zi = 0.0;
         bool valid = true;
@@ -486,15 +472,8 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
 
     // ---- scatter X_t and W_m(t), release ----
     for (int l = tid; l < ep; l += THREADS) {
-      int64_t off = g.gbase;
-      bool ok = true;
-#pragma unroll
-      for (int v = 0; v < D; ++v) {
-        const int iv = (l >> a.tsh[v]) & ((1 << a.tlog[v]) - 1);
-        ok &= iv < g.ext[v];
-        off += static_cast<int64_t>(iv) * a.stride[v];
-      }
-      if (ok) {
+      const int64_t off = goff[l];
+      if (off >= 0) {
         a.X[off] = xr[l];
 #pragma unroll
         for (int m = 1; m < D; ++m) a.W[m][off] = lb[m - 1][l];
