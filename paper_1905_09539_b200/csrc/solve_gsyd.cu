@@ -309,10 +309,9 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
 #endif
     constexpr int NPART = GSYD_ONEPASS ? 1 : 2;
     for (int part = 0; part < NPART && !(a.dbg & 4); ++part) {
-      if (tid == 0) {
-        const int d0 = (part == 0 && !GSYD_ONEPASS) ? 2 : 1;
-        for (int m = 0; m < D; ++m)
-          if (g.tco[m] + d0 < a.ntiles_mode[m]) waitg(a, g.lt + d0 * muls[m]);
+      if (tid < D) {  // one thread per mode: the D flag round trips overlap
+        const int d0 = (part == 0 && !GSYD_ONEPASS) ? 2 : 1, m = tid;
+        if (g.tco[m] + d0 < a.ntiles_mode[m]) waitg(a, g.lt + d0 * muls[m]);
       }
       __syncthreads();
 #pragma unroll 1

@@ -174,7 +174,10 @@ TSG_DEVINL void update_mode(const SolveArgs& a, const GD<D>& g, double* xr, cons
 }
 
 template <int D>
-__global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArgs a) {
+#ifndef LAPD_MINB
+#define LAPD_MINB (2048 / EP + 1)  // 5 CTAs/SM at EP = 512 (96 registers)
+#endif
+__global__ void __launch_bounds__(THREADS, LAPD_MINB) solve_lapd_kernel(SolveArgs a) {
   pdl_wait();
   pdl_trigger();
   __shared__ __align__(16) double xr[EP];
@@ -273,11 +276,10 @@ __global__ void __launch_bounds__(THREADS, 2048 / EP) solve_lapd_kernel(SolveArg
     // the wait, which rarely matters on the wide hyperplanes of d = 6)
     constexpr int NPART = LAPD_ONEPASS ? 1 : 2;
     for (int part = 0; part < NPART && !(a.dbg & 4); ++part) {
-      if (tid == 0) {
-        for (int m = 0; m < D; ++m) {
-          const int tm = g.tco[m], d0 = (part == 0 && !LAPD_ONEPASS) ? 2 : 1;
-          if (tm + d0 < a.ntiles_mode[m]) waitp(a, g.lt + d0 * muls[m]);
-        }
+      if (tid < D) {  // one thread per mode: the D flag round trips overlap
+        const int m = tid;
+        const int tm = g.tco[m], d0 = (part == 0 && !LAPD_ONEPASS) ? 2 : 1;
+        if (tm + d0 < a.ntiles_mode[m]) waitp(a, g.lt + d0 * muls[m]);
       }
       __syncthreads();
 #pragma unroll 1
