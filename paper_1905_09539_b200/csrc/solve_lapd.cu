@@ -159,7 +159,7 @@ TSG_DEVINL void update_nb(const SolveArgs& a, const GD<D>& g, double* xr, const 
 }
 
 #ifndef LAPD_NB
-#define LAPD_NB 4
+#define LAPD_NB 2
 #endif
 #ifndef LAPD_UBK
 #define LAPD_UBK 4
