@@ -196,6 +196,9 @@ TSG_DEVINL bool cmode16(const double* sr, const double* si, double* dr, double* 
     }
   }
   bool sing = false;
+  // every element of the warp's 32 cross-section columns is read (above)
+  // and written (below) by this warp only: in place needs just this
+  __syncwarp();
 #pragma unroll
   for (int rb = 0; rb < 2; ++rb)
 #pragma unroll
@@ -530,14 +533,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 // table region and streams its first update boxes while the consumers are
 // still in the previous tile's base case and scatter; the B~ tile goes into
 // xr once the consumers signal that the previous tile has been scattered.
-// The base case works in xr and the xi region (so the two-stage ring is
-// never touched by the consumers outside the update phase).
+// The base case works in place in xr (each warp reads and writes only its
+// own cross-section columns of a mode product), which frees the former work
+// tile for a third ring stage (the ring is never touched by the consumers
+// outside the update phase).
 // ---------------------------------------------------------------------------
 #ifndef L16_DNS
-#define L16_DNS 2
+#define L16_DNS 3
 #endif
 constexpr int DNS = L16_DNS;  // ring stages of the decoupled kernel
-constexpr int D_OFF_VH = 2 * TD, D_OFF_RING = D_OFF_VH + 6 * VHS;
+// xr (the tile, base case in place), double-buffered bases, the ring
+constexpr int D_OFF_VH = TD, D_OFF_RING = D_OFF_VH + 6 * VHS;
 constexpr int D_BYTES = (D_OFF_RING + DNS * TD) * 8;
 static_assert((D_OFF_RING * 8) % 128 == 0, "TMA destinations 128-byte aligned");
 
@@ -580,7 +586,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ G16 gq[2];
   __shared__ __align__(8) uint64_t full[DNS], empty[DNS], bar_x, bar_v[2], info_full[2], info_empty[2], xr_free;
   double* xr = smem;
-  double* yb = smem + TD;
   double* vhb = smem + D_OFF_VH;
   double* ring = smem + D_OFF_RING;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -696,20 +701,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       const double* vh = vhb + slot * 3 * VHS;
       const int* ex = g.ext;
       constexpr int VRI = 0, VRR = EE;
-      cmode16<0, false, false, false>(xo, nullptr, yb, nullptr, vh + VRI, vh + VRI, vh, ex, a.tiny);
+      cmode16<0, false, false, false>(xo, nullptr, xo, nullptr, vh + VRI, vh + VRI, vh, ex, a.tiny);
       consumers_sync();
-      cmode16<1, false, false, false>(yb, nullptr, xr, nullptr, vh + VHS + VRI, vh + VHS + VRI, vh, ex, a.tiny);
+      cmode16<1, false, false, false>(xo, nullptr, xo, nullptr, vh + VHS + VRI, vh + VHS + VRI, vh, ex, a.tiny);
       consumers_sync();
-      cmode16<2, false, false, false>(xr, nullptr, yb, nullptr, vh + 2 * VHS + VRI, vh + 2 * VHS + VRI, vh, ex,
+      cmode16<2, false, false, false>(xo, nullptr, xo, nullptr, vh + 2 * VHS + VRI, vh + 2 * VHS + VRI, vh, ex,
                                       a.tiny);
       consumers_sync();
-      const bool sing = cell_solve16(yb, g, vh, a.tiny);
+      const bool sing = cell_solve16(xo, g, vh, a.tiny);
       consumers_sync();
-      cmode16<0, false, false, false>(yb, nullptr, xr, nullptr, vh + VRR, vh + VRR, vh, ex, a.tiny);
+      cmode16<0, false, false, false>(xo, nullptr, xo, nullptr, vh + VRR, vh + VRR, vh, ex, a.tiny);
       consumers_sync();
-      cmode16<1, false, false, false>(xr, nullptr, yb, nullptr, vh + VHS + VRR, vh + VHS + VRR, vh, ex, a.tiny);
+      cmode16<1, false, false, false>(xo, nullptr, xo, nullptr, vh + VHS + VRR, vh + VHS + VRR, vh, ex, a.tiny);
       consumers_sync();
-      cmode16<2, false, false, false>(yb, nullptr, xr, nullptr, vh + 2 * VHS + VRR, vh + 2 * VHS + VRR, vh, ex,
+      cmode16<2, false, false, false>(xo, nullptr, xo, nullptr, vh + 2 * VHS + VRR, vh + 2 * VHS + VRR, vh, ex,
                                       a.tiny);
       if (sing) atomicMin(a.status, static_cast<int>(g.lt < 0x7f7f7f7e ? g.lt : 0x7f7f7f7e));
       consumers_sync();
@@ -717,7 +722,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int l = tid; l < TT; l += CW * 32) {
         const int i0 = l & (E - 1), i1 = (l >> 4) & (E - 1), i2 = l >> 8;
         if (i0 < e0 && i1 < e1 && i2 < e2)
-          a.X[g.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2]] = xr[i0 + S1 * i1 + S2 * i2];
+          a.X[g.gbase + i0 + i1 * a.stride[1] + i2 * a.stride[2]] = xo[i0 + S1 * i1 + S2 * i2];
       }
       fence_proxy_async();  // this thread's generic xr / xi accesses before the next TMA into them
       consumers_sync();
