@@ -68,7 +68,7 @@ def main():
             js = json.load(open(path))
         except (OSError, ValueError):
             js = {}
-        js[config] = traffic
+        js.setdefault(config, {}).update(traffic)
         json.dump(js, open(path, "w"), indent=1)
     print("\n".join(lines))
 
