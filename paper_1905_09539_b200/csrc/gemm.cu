@@ -71,12 +71,24 @@ dgemm_nn_kernel(GemmArgs g) {
   const int64_t tiles_n = (g.N + BN - 1) / BN;
   const int64_t mt = bid % tiles_m;
   int64_t nt = (bid / tiles_m) % tiles_n;
-  const int64_t bt = bid / (tiles_m * tiles_n);
+  int64_t bt = bid / (tiles_m * tiles_n);
   // Programmatic launches: wait for the producer of A/B (except the gated
-  // back transform, which waits on tile flags instead), then let the next
+  // transforms, which acquire tile / slab flags instead), then let the next
   // kernel's CTAs be scheduled as this grid drains.
-  if (!g.wflags) pdl_wait();
+  if (!g.wflags && !g.pflags) pdl_wait();
   pdl_trigger();
+  if (g.pflags) {
+    if (g.pdesc) bt = g.batch - 1 - bt;
+    const int c0 = static_cast<int>(bt * g.pcpb / g.pbn);
+    const int c1 = static_cast<int>(((bt + 1) * g.pcpb - 1) / g.pbn);
+    const int cnt = (c1 - c0 + 1) * g.ptm;
+    for (int i = tid; i < cnt; i += NT) {
+      const int* f = g.pflags + (i % g.ptm) + static_cast<int64_t>(c0 + i / g.ptm) * g.ptm;
+      while (ld_acquire(f) != g.pepoch) __nanosleep(128);
+    }
+    __threadfence();
+    __syncthreads();
+  }
   if (g.wflags) {
     // Gated back transform: the solve releases the last columns first.
     nt = tiles_n - 1 - nt;
@@ -246,6 +258,13 @@ dgemm_nn_kernel(GemmArgs g) {
       }
     }
   }
+  if (g.dflags) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(g.dflags + mt + nt * tiles_m, g.depoch);
+    }
+  }
 }
 
 template <typename K>
@@ -297,6 +316,19 @@ cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
 }
 
 }  // namespace
+
+void gemm_tile_shape(int M, int N, int* bm, int* bn) {
+  // mirrors the default dispatch of dgemm_nn below
+  if (const char* e = std::getenv("TSG_GEMM_CFG"); e && std::atoi(e) != 0) {
+    *bm = *bn = 0;
+    return;
+  }
+  if (M >= 64 && N >= 64) *bm = 64, *bn = 64;
+  else if (N <= 64 && M >= 128) *bm = 128, *bn = 64;
+  else if (M <= 64 && N >= 128) *bm = 64, *bn = 128;
+  else if (M <= 64 && N <= 64) *bm = 64, *bn = 64;
+  else *bm = 128, *bn = 128;
+}
 
 cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
@@ -375,7 +407,20 @@ cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int
     g.sC = P * r;
     g.batch = Q;
   }
-  if (gate) g.pdl = gate->pdl;
+  if (gate) {
+    g.pdl = gate->pdl;
+    if (g.batch == 1) {
+      g.dflags = gate->dflags;
+      g.depoch = gate->depoch;
+    } else {
+      g.pflags = gate->pflags;
+      g.pepoch = gate->pepoch;
+      g.ptm = gate->ptm;
+      g.pbn = gate->pbn;
+      g.pcpb = gate->pcpb;
+      g.pdesc = gate->pdesc;
+    }
+  }
   if (flops) *flops += 2.0 * static_cast<double>(P) * Q * n * r;
   return dgemm_nn(g, st);
 }

@@ -28,7 +28,22 @@ struct GemmArgs {
   int wepoch = 0;
   int wgroups = 0;  // number of 64-column groups (entries of woff minus one)
   int pdl = 0;
+  // Producer side of a slab-wise chain (mode-0 product feeding mode 1,
+  // batch 1): each CTA releases dflags[mt + nt * tiles_m] = depoch after
+  // its stores.
+  int* dflags = nullptr;
+  int depoch = 0;
+  // Consumer side (batched mode-1 product): batch q reads producer columns
+  // [q * pcpb, (q + 1) * pcpb), i.e. producer tiles (all ptm m-tiles) x
+  // (n-tiles of width pbn over those columns); the CTA acquires their flags
+  // (== pepoch) instead of waiting for the whole producer grid.  pdesc:
+  // batches are issued last first (the producer finishes those first).
+  const int* pflags = nullptr;
+  int pepoch = 0, ptm = 0, pbn = 0, pcpb = 0, pdesc = 0;
 };
+
+// CTA tile (BM x BN) dgemm_nn uses for an M x N product (0 x 0: unknown).
+void gemm_tile_shape(int M, int N, int* bm, int* bn);
 
 // Column granularity of the GemmArgs tile-flag gate.
 constexpr int kWaitCols = 64;

@@ -822,6 +822,22 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       TSG_CU(upload(&pl->gate_ids, ids));
       pl->gate_groups = static_cast<int>(G);
     }
+    // Slab chain mode 0 -> mode 1 (both GEMM passes, mode 1 batched)
+    const bool two_gemm = !(small_on && (tsg::small_mode_ok(dims[0]) || tsg::small_mode_ok(dims[1])));
+    if (!pl->reduced_only && d >= 3 && two_gemm && pl->N / (static_cast<int64_t>(dims[0]) * dims[1]) > 1) {
+      int bm = 0, bn = 0;
+      const int64_t Q0 = pl->N / dims[0];
+      tsg::gemm_tile_shape(dims[0], static_cast<int>(Q0), &bm, &bn);
+      if (bm > 0 && bn > 0 && Q0 < INT_MAX) {
+        pl->s_tm = (dims[0] + bm - 1) / bm;
+        pl->s_bn = bn;
+        pl->sdone_n = pl->s_tm * static_cast<int>((Q0 + bn - 1) / bn);
+        for (auto*& f : pl->sdone) {
+          TSG_CU(cudaMalloc(&f, pl->sdone_n * sizeof(int)));
+          TSG_CU(cudaMemset(f, 0, pl->sdone_n * sizeof(int)));
+        }
+      }
+    }
   }
 
   // Executed FLOP of the solve: left-looking updates per tile and pass.
@@ -1239,6 +1255,12 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
     }
   }
   const int k = static_cast<int>(ps.size());
+  // slab chain: mode-1 CTAs start on the slabs the mode-0 GEMM has finished
+  // (TSG_SCHAIN=0, read per call, turns it off)
+  const char* sc_env = std::getenv("TSG_SCHAIN");
+  const bool schain = pl->sdone[0] && k >= 2 && ps[0].m == 0 && ps[0].kind == 0 && ps[1].m == 1 &&
+                      ps[1].kind == 0 && !(sc_env && std::atoi(sc_env) == 0);
+  int* sdone = pl->sdone[fwd ? 0 : 1];
   const double* src = in;
   for (int i = 0; i < k; ++i) {
     double* dst = ((k - 1 - i) % 2 == 0) ? target : other;
@@ -1250,9 +1272,20 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
       // GEMM after GEMM: programmatic launch (the next pass's CTAs are
       // scheduled while this one drains; pdl_wait() orders the data).
       tsg::GemmArgs chain{};
-      chain.pdl = 1;
-      const tsg::GemmArgs* opt = (i == 0 && m == 0) ? gate0
-                                 : (i > 0 && ps[i - 1].kind == 0) ? &chain : nullptr;
+      if (i == 0 && gate0) chain = *gate0;
+      chain.pdl = (i == 0 && gate0) || (i > 0 && ps[i - 1].kind == 0) ? 1 : 0;
+      if (schain && i == 0) {
+        chain.dflags = sdone;
+        chain.depoch = pl->chain_epoch;
+      } else if (schain && i == 1) {
+        chain.pflags = sdone;
+        chain.pepoch = pl->chain_epoch;
+        chain.ptm = pl->s_tm;
+        chain.pbn = pl->s_bn;
+        chain.pcpb = pl->dims[1];
+        chain.pdesc = gate0 && gate0->wflags ? 1 : 0;  // gated mode 0 runs last columns first
+      }
+      const tsg::GemmArgs* opt = &chain;
       e = tsg::mode_product(src, dst, d, pl->dims.data(), m, A, At, pl->dims[m], 1.0, 0.0, st,
                             nullptr, opt);
     } else {
@@ -1261,7 +1294,7 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
     }
     if (e != cudaSuccess) return e;
     ++pl->launches;
-    if (i == 0 && after0) {
+    if (i == (schain ? 1 : 0) && after0) {
       e = cudaEventRecord(after0, st);
       if (e != cudaSuccess) return e;
     }
@@ -1278,6 +1311,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   const int d = pl->d;
   cudaEvent_t* ev = ctx->ev;
   pl->launches = 0;
+  ++pl->chain_epoch;
   double* work = nullptr;
   // Solve state reset first, so the forward GEMMs and the solve follow each
   // other directly (programmatic launches).
