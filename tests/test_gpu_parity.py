@@ -263,8 +263,10 @@ def test_laplace_ill_conditioned_pairs_refine(gpu, ref):
 
 
 # The back transform's mode-0 GEMM is gated on tile flags and launched as a
-# programmatic dependent of the solve (plan.cpp gate_*); with TSG_GATE=0 it
-# runs after the solve.  Same arithmetic in the same order -> bit-identical.
+# programmatic dependent of the solve (plan.cpp gate_*), and the mode-1
+# transform GEMMs start per slab on the mode-0 GEMM's done flags; with
+# TSG_GATE=0 TSG_SCHAIN=0 every kernel waits for its predecessor.  Same
+# arithmetic in the same order -> bit-identical.
 _GATE_SCRIPT = r"""
 import hashlib, os, sys
 import numpy as np
@@ -272,10 +274,13 @@ sys.path.insert(0, os.getcwd())
 import paper_1905_09539_b200 as T
 cfg = T.SolverConfig(strategy=T.Strategy.recursion_only, arithmetic=T.Arithmetic.real_quasitriangular)
 out = []
-for dims, seed in [((70, 45, 33), 1), ((96, 66, 80), 2), ((40, 9, 8, 7), 3)]:
+for dims, seed in [((70, 45, 33), 1), ((96, 66, 80), 2), ((40, 9, 8, 7), 3), ((72, 70, 3), 4)]:
     p = T.make_problem(2, dims, seed=seed)
     x = np.ascontiguousarray(T.solve_laplace(p, cfg).solution)
     out.append(hashlib.sha256(x.tobytes()).hexdigest()[:16])
+p = T.make_problem(5, (30, 70, 66), seed=5)  # gsylv: same transform chain
+x = np.ascontiguousarray(T.solve_gsylv(p).solution)
+out.append(hashlib.sha256(x.tobytes()).hexdigest()[:16])
 print(" ".join(out))
 """
 
@@ -288,7 +293,9 @@ def test_gated_back_transform_bitexact():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
     for g in ("0", "1"):
-        env = dict(os.environ, TSG_GATE=g, PYTHONPATH=root)
+        # "0": back transform after the solve and no slab chain between the
+        # mode-0 / mode-1 transform GEMMs; "1": both overlaps on (default)
+        env = dict(os.environ, TSG_GATE=g, TSG_SCHAIN=g, PYTHONPATH=root)
         r = subprocess.run([sys.executable, "-c", _GATE_SCRIPT], cwd=root, env=env,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
