@@ -1398,6 +1398,9 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     if (pl->fast == 5)
       std::fprintf(stderr, "[tsg profd] tiles=%.0f cycles/tile: claim+geom %.0f gather %.0f far %.0f near %.0f base %.0f scatter+rel %.0f\n",
                    nt, h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt);
+    else if (pl->use16 && tsg::lap16_decoupled())
+      std::fprintf(stderr, "[tsg prof16d] tiles=%.0f cycles/tile (consumer 0): wait tile info %.0f chunks (incl. ring waits) %.0f B~ box wait %.0f flush %.0f bases wait %.0f base case %.0f scatter+release %.0f\n",
+                   nt, h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt, h[6] / nt);
     else if (pl->use16)
       std::fprintf(stderr, "[tsg prof16] tiles=%.0f cycles/tile (consumer 0): claim+geom %.0f first-box %.0f chunks %.0f flush %.0f diag %.0f scatter+rel %.0f | producer: flag waits %.0f ring waits+issue %.0f\n",
                    nt, h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt, h[6] / nt, h[7] / nt);

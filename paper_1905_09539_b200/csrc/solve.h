@@ -100,6 +100,8 @@ cudaError_t launch_solve_lap3(int lt, const SolveArgs& a, cudaStream_t st, Solve
 // (solve_lap16.cu; plans whose tiles are all diagonalisable).
 TileCaps solve_lap16_caps();
 cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
+// true when launch_solve_lap16 runs the decoupled kernel (solve_lap16d_kernel)
+bool lap16_decoupled();
 
 // Higher-order Laplace (solve_lapd.cu, d = 4..6): small padded tiles,
 // DMMA updates, diagonalised base case.

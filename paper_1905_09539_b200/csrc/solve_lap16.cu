@@ -31,6 +31,10 @@
 namespace tsg {
 namespace {
 
+#ifndef L16_PROF
+#define L16_PROF 0
+#endif
+
 constexpr int E = 16, EE = 256, TT = 4096;
 constexpr int CW = 8;                 // consumer warps
 constexpr int THREADS = (CW + 1) * 32;
@@ -635,7 +639,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma_load_3d(xr, &tmx, g.start[0] & ~1, g.start[1], g.start[2], &bar_x);
           bx = true;
         };
-        if (nch == 0) issue_bx();
+        // B~ box: at once when the previous tile is already scattered (ramp
+        // regimes: the consumers idle), else after the ring is filled
+        if (nch == 0 || it == 0 || mbar_test(&xr_free, (it - 1) & 1)) issue_bx();
         for (int c = 0; c < nch; ++c, ++gch) {
           const Chunk ch = chunk_of(g, a.dims, c);
           const int m = ch.m % 3;
@@ -657,11 +663,32 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     // ---------------- consumers ----------------
     unsigned gch = 0;
+    // -DL16_PROF=1 + TSG_PROF: consumer thread 0 accumulates cycles per
+    // phase (compiled out by default: the counters cost registers)
+#if L16_PROF
+    const bool prof = a.prof != nullptr && tid == 0;
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tm0 = clock64();
+    auto mark = [&](int k) {
+      if (prof) {
+        const long long t = clock64();
+        ph[k] += static_cast<unsigned long long>(t - tm0);
+        tm0 = t;
+      }
+    };
+    int ntl = 0;
+#else
+    auto mark = [](int) {};
+#endif
     for (int it = 0;; ++it) {
       const int slot = it & 1;
       mbar_wait(&info_full[slot], (it >> 1) & 1);
       const G16& g = gq[slot];
+      mark(0);
       if (g.done) break;
+#if L16_PROF
+      ++ntl;
+#endif
       const int nch = g.nch;
       double acc[3][2][4][2];
 #pragma unroll
@@ -689,7 +716,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int ks = 0; ks < 4; ++ks) af[ks][0] = an[ks][0], af[ks][1] = an[ks][1];
         ch = cn;
       }
+      mark(1);
       mbar_wait(&bar_x, it & 1);
+      mark(2);
       double* xo = xr + (g.start[0] & 1);
       flush16<0>(xo, acc[0]);
       consumers_sync();
@@ -697,7 +726,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       consumers_sync();
       flush16<2>(xo, acc[2]);
       consumers_sync();
+      mark(3);
       mbar_wait(&bar_v[slot], (it >> 1) & 1);
+      mark(4);
       const double* vh = vhb + slot * 3 * VHS;
       const int* ex = g.ext;
       constexpr int VRI = 0, VRR = EE;
@@ -718,6 +749,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                       a.tiny);
       if (sing) atomicMin(a.status, static_cast<int>(g.lt < 0x7f7f7f7e ? g.lt : 0x7f7f7f7e));
       consumers_sync();
+      mark(5);
       const int e0 = g.ext[0], e1 = g.ext[1], e2 = g.ext[2];
       for (int l = tid; l < TT; l += CW * 32) {
         const int i0 = l & (E - 1), i1 = (l >> 4) & (E - 1), i2 = l >> 8;
@@ -737,13 +769,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_arrive(&xr_free);
         mbar_arrive(&info_empty[slot]);
       }
+      mark(6);
     }
+#if L16_PROF
+    if (prof) {
+      for (int k = 0; k < 7; ++k) atomicAdd(a.prof + k, ph[k]);
+      atomicAdd(a.prof + 8, static_cast<unsigned long long>(ntl));
+    }
+#endif
   }
 }
 
 }  // namespace
 
 TileCaps solve_lap16_caps() { return TileCaps{E, TT, EE}; }
+
+#ifndef L16_DEC
+#define L16_DEC 1
+#endif
+bool lap16_decoupled() { return L16_DEC || std::getenv("TSG_L16DEC"); }
 
 cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
   if (a.ntiles <= 0) return cudaSuccess;
@@ -752,10 +796,7 @@ cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchI
                             static_cast<uint64_t>(a.dims[2])};
   const uint32_t box[3] = {BX, BY, BZ};
   if (!encode_tmap_f64(&map, a.X, 3, dims, box)) return cudaErrorInvalidValue;
-#ifndef L16_DEC
-#define L16_DEC 1
-#endif
-  if (L16_DEC || std::getenv("TSG_L16DEC")) {
+  if (lap16_decoupled()) {
     static int nsm2 = 0;
     if (nsm2 == 0) {
       cudaError_t e = cudaFuncSetAttribute(solve_lap16d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D_BYTES);
