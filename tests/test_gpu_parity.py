@@ -274,7 +274,8 @@ sys.path.insert(0, os.getcwd())
 import paper_1905_09539_b200 as T
 cfg = T.SolverConfig(strategy=T.Strategy.recursion_only, arithmetic=T.Arithmetic.real_quasitriangular)
 out = []
-for dims, seed in [((70, 45, 33), 1), ((96, 66, 80), 2), ((40, 9, 8, 7), 3), ((72, 70, 3), 4)]:
+for dims, seed in [((70, 45, 33), 1), ((96, 66, 80), 2), ((40, 9, 8, 7), 3), ((72, 70, 3), 4),
+                   ((70, 5, 300), 6), ((50, 80, 30), 7)]:
     p = T.make_problem(2, dims, seed=seed)
     x = np.ascontiguousarray(T.solve_laplace(p, cfg).solution)
     out.append(hashlib.sha256(x.tobytes()).hexdigest()[:16])
