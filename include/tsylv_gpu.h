@@ -1,7 +1,7 @@
 /* tsylv_gpu.h — C-ABI of the B200-native Schur-basis solve.
  *
  * This is the drop-in boundary below the reference's C++ solver entry points
- * (proj/include/tsylv/*.hpp).  No C++ or torch types cross it: plain
+ * (proj/include/tsylv/ headers).  No C++ or torch types cross it: plain
  * pointers, int extents, column-major FP64 buffers (mode 0 fastest, the
  * layout of tsylv::Tensor, tensor.hpp:19-27).  Each entry point names the
  * reference interface it replaces.
@@ -102,7 +102,7 @@ int tsg_gsylv_reduced(tsg_ctx* ctx, int d, const int* dims, const double* S,
                       tsg_report* rep);
 
 /* ---- Plans: set up once (factors uploaded, tiles/schedule built), execute
- * many times.  The bench times tsg_plan_execute with inputs resident.
+ * many times.  The bench times tsg_plan_enqueue with inputs resident.
  * family: 0 Laplace (Tc/S/Q/Z unused), 1 gsylv.  For gsylv, T[0]=S,
  * U[0]=Q and the extra pointers Tc, Z are used.  reduced_only=1 skips
  * both transforms (U/Q/Z may be NULL). */
@@ -112,6 +112,13 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims,
                     const tsg_opts* opts, tsg_plan** out);
 int tsg_plan_execute(tsg_plan* plan, const double* B, double* X,
                      int inputs_on_device, tsg_report* rep);
+/* Asynchronous device-resident solve: enqueue the whole pipeline for B -> X
+ * (device pointers) on the context stream and return at once, so repeated
+ * solves run back to back without host round trips.  No singularity check
+ * and no timings: tsg_plan_sync waits for every enqueued solve and reports
+ * the zero pivot of the most recent one (rep may be NULL). */
+int tsg_plan_enqueue(tsg_plan* plan, const double* B, double* X);
+int tsg_plan_sync(tsg_plan* plan, tsg_report* rep);
 void tsg_plan_destroy(tsg_plan* plan);
 /* Solve nrhs right-hand sides from HOST buffers B[i] into X[i] (pinned
  * memory recommended) with the copies overlapped: the host->device copy of

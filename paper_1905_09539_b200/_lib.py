@@ -38,6 +38,7 @@ TSG_SYMBOLS = [
     "tsg_laplace_solve",
     "tsg_laplace_reduced", "tsg_gsylv_solve", "tsg_gsylv_reduced", "tsg_plan_create",
     "tsg_plan_execute", "tsg_plan_execute_stream", "tsg_plan_destroy", "tsg_plan_info",
+    "tsg_plan_enqueue", "tsg_plan_sync",
     "tsg_mode_multiply",
     "tsg_residual", "tsg_abi_version",
     "tsg_slab_bounds", "tsg_dplan_create", "tsg_dplan_destroy", "tsg_dplan_info",
@@ -63,6 +64,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tsg_plan_execute": (I, [P, P, P, I, ctypes.POINTER(TsgReport)]),
         "tsg_plan_execute_stream": (I, [P, I, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(TsgReport)]),
         "tsg_plan_destroy": (None, [P]),
+        "tsg_plan_enqueue": (I, [P, P, P]),
+        "tsg_plan_sync": (I, [P, ctypes.POINTER(TsgReport)]),
         "tsg_plan_info": (I, [P, ctypes.POINTER(ctypes.c_int64), c_int_p, c_dbl_p]),
         "tsg_residual": (I, [P, I, I, c_int_p, c_dbl_pp, P, P, P, I, c_dbl_p]),
         "tsg_slab_bounds": (I, [I, c_dbl_p, I, I, c_int_p]),

@@ -892,6 +892,30 @@ int tsg_plan_info(const tsg_plan* pl, int64_t* n_tiles, int* tile_extents, doubl
   return TSG_OK;
 }
 
+int tsg_plan_enqueue(tsg_plan* pl, const double* B, double* X) {
+  if (!pl || !B || !X) return TSG_EINVAL;
+  tsg_ctx* ctx = pl->ctx;
+  TSG_CU(cudaSetDevice(ctx->device));
+  return enqueue(pl, B, X, pl->ctx->stream, false);
+}
+
+int tsg_plan_sync(tsg_plan* pl, tsg_report* rep) {
+  if (!pl) return TSG_EINVAL;
+  tsg_ctx* ctx = pl->ctx;
+  TSG_CU(cudaSetDevice(ctx->device));
+  int hstat[2] = {0, kNoStatus};
+  TSG_CU(cudaMemcpyAsync(hstat, pl->counter, sizeof(hstat), cudaMemcpyDeviceToHost, pl->ctx->stream));
+  TSG_CU(cudaStreamSynchronize(pl->ctx->stream));
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->flops_alg = pl->flops_alg;
+    rep->flops_exec = pl->flops_exec;
+    rep->zero_pivot_index = hstat[1] == kNoStatus ? -1 : hstat[1];
+    rep->kernel_launches = pl->launches;
+  }
+  return TSG_OK;
+}
+
 int tsg_plan_execute(tsg_plan* pl, const double* B, double* X, int inputs_on_device,
                      tsg_report* rep) {
   if (!pl) return TSG_EINVAL;

@@ -84,6 +84,20 @@ class Plan:
             raise gpu_error(f"tsg_plan_execute failed ({rc}): {self.ctx.error()}")
         return rep
 
+    def enqueue_device(self, b_ptr: int, x_ptr: int) -> None:
+        """Asynchronous solve on the context stream (tsg_plan_enqueue)."""
+        rc = lib().tsg_plan_enqueue(self.h, ctypes.c_void_p(b_ptr), ctypes.c_void_p(x_ptr))
+        if rc != 0:
+            raise gpu_error(f"tsg_plan_enqueue failed ({rc}): {self.ctx.error()}")
+
+    def sync(self) -> TsgReport:
+        """Wait for every enqueued solve (tsg_plan_sync); zero pivot of the last."""
+        rep = TsgReport()
+        rc = lib().tsg_plan_sync(self.h, ctypes.byref(rep))
+        if rc != 0:
+            raise gpu_error(f"tsg_plan_sync failed ({rc}): {self.ctx.error()}")
+        return rep
+
     def execute_host(self, b: np.ndarray, x: np.ndarray) -> TsgReport:
         rep = TsgReport()
         rc = lib().tsg_plan_execute(self.h, b.ctypes.data_as(ctypes.c_void_p),

@@ -223,6 +223,32 @@ def test_plan_execute_stream_matches_single(gpu):
         assert rel_diff(x, w) < 1e-15
 
 
+def test_plan_enqueue_back_to_back(gpu):
+    """tsg_plan_enqueue: several asynchronous device-resident solves into
+    different outputs, then tsg_plan_sync; each matches the synchronous
+    execution bit for bit (C2-like shape on the 16^3 kernel and a small one)."""
+    import torch
+    from paper_1905_09539_b200.plan import Context, Plan
+    for dims in [(40, 36, 44), (96, 66, 80)]:
+        p = gpu.make_problem(2, dims, seed=10)
+        fs = [gpu.schur(a) for a in p.coeffs]
+        pl = Plan(Context(0), 0, [f[1] for f in fs], [f[0] for f in fs])
+        rng = np.random.default_rng(4)
+        bs = [torch.from_numpy(rng.standard_normal(int(np.prod(dims)))).cuda() for _ in range(4)]
+        want = []
+        for b in bs:
+            x = torch.empty_like(b)
+            pl.execute_device(b.data_ptr(), x.data_ptr())
+            want.append(x.cpu().numpy())
+        xs = [torch.zeros_like(b) for b in bs]
+        for b, x in zip(bs, xs):
+            pl.enqueue_device(b.data_ptr(), x.data_ptr())
+        rep = pl.sync()
+        assert rep.zero_pivot_index == -1
+        for x, w in zip(xs, want):
+            assert np.array_equal(x.cpu().numpy(), w)
+
+
 def _jordanish(n, lam, off, rng):
     t = np.triu(rng.standard_normal((n, n))) * 0.3
     t[np.arange(n), np.arange(n)] = lam
