@@ -48,33 +48,20 @@ struct GemmSmem {
   static constexpr int BYTES = kStages * STAGE * 8;
 };
 
-#ifndef TSG_GEMM_MINB
-#define TSG_GEMM_MINB 1
-#endif
-template <int BM, int BN, int WM, int WN, bool VEC, bool FAST = false>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
-                                  (FAST && (BM / WM) * (BN / WN) == 4) ? 4 : TSG_GEMM_MINB)
-dgemm_nn_kernel(GemmArgs g) {
-  using S = GemmSmem<BM, BN>;
-  constexpr int NWM = BM / WM;              // warps along M
-  constexpr int NT = (BM / WM) * (BN / WN) * 32;
-  constexpr int FM = WM / 8, FN = WN / 8;   // 8x8 fragments per warp
-  extern __shared__ __align__(16) double smem[];
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % NWM, wn = warp / NWM;
-  const int gq = lane >> 2, tq = lane & 3;
-
-  // Flattened grid: m-tile fastest (B-panel reuse in L2), then n-tile, batch.
+// Tile of this CTA and the cross-kernel waits every GEMM kernel shares.
+// Flattened grid: m-tile fastest (B-panel reuse in L2), then n-tile, batch.
+// Programmatic launches wait for the producer of A/B (pdl_wait), except the
+// gated transforms, which acquire tile / slab flags instead; every grid
+// then lets the next kernel's CTAs be scheduled as it drains.
+template <int BM, int BN, int NT>
+TSG_DEVINL void gemm_prologue(const GemmArgs& g, int tid, int64_t& mt, int64_t& nt, int64_t& bt,
+                              int64_t& tiles_m) {
   const int64_t bid = blockIdx.x;
-  const int64_t tiles_m = (g.M + BM - 1) / BM;
+  tiles_m = (g.M + BM - 1) / BM;
   const int64_t tiles_n = (g.N + BN - 1) / BN;
-  const int64_t mt = bid % tiles_m;
-  int64_t nt = (bid / tiles_m) % tiles_n;
-  int64_t bt = bid / (tiles_m * tiles_n);
-  // Programmatic launches: wait for the producer of A/B (except the gated
-  // transforms, which acquire tile / slab flags instead), then let the next
-  // kernel's CTAs be scheduled as this grid drains.
+  mt = bid % tiles_m;
+  nt = (bid / tiles_m) % tiles_n;
+  bt = bid / (tiles_m * tiles_n);
   if (!g.wflags && !g.pflags) pdl_wait();
   pdl_trigger();
   if (g.pflags) {
@@ -101,6 +88,38 @@ dgemm_nn_kernel(GemmArgs g) {
     __threadfence();
     __syncthreads();
   }
+}
+
+// Done flag of a producer CTA tile (slab chain), after all its stores.
+TSG_DEVINL void gemm_done(const GemmArgs& g, int tid, int64_t mt, int64_t nt, int64_t tiles_m) {
+  if (g.dflags) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(g.dflags + mt + nt * tiles_m, g.depoch);
+    }
+  }
+}
+
+#ifndef TSG_GEMM_MINB
+#define TSG_GEMM_MINB 1
+#endif
+template <int BM, int BN, int WM, int WN, bool VEC, bool FAST = false>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32,
+                                  (FAST && (BM / WM) * (BN / WN) == 4) ? 4 : TSG_GEMM_MINB)
+dgemm_nn_kernel(GemmArgs g) {
+  using S = GemmSmem<BM, BN>;
+  constexpr int NWM = BM / WM;              // warps along M
+  constexpr int NT = (BM / WM) * (BN / WN) * 32;
+  constexpr int FM = WM / 8, FN = WN / 8;   // 8x8 fragments per warp
+  extern __shared__ __align__(16) double smem[];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % NWM, wn = warp / NWM;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  int64_t mt, nt, bt, tiles_m;
+  gemm_prologue<BM, BN, NT>(g, tid, mt, nt, bt, tiles_m);
   const int m0 = static_cast<int>(mt * BM), n0 = static_cast<int>(nt * BN);
 
   const double* __restrict__ A = g.A + bt * g.sA;
@@ -258,13 +277,7 @@ dgemm_nn_kernel(GemmArgs g) {
       }
     }
   }
-  if (g.dflags) {
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release(g.dflags + mt + nt * tiles_m, g.depoch);
-    }
-  }
+  gemm_done(g, tid, mt, nt, tiles_m);
 }
 
 template <typename K>
