@@ -720,20 +720,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&bar_x, it & 1);
       mark(2);
       double* xo = xr + (g.start[0] & 1);
-      flush16<0>(xo, acc[0]);
-      consumers_sync();
-      flush16<1>(xo, acc[1]);
-      consumers_sync();
+      // Warp w owns the cross-section columns [32 w, 32 w + 32) of every
+      // mode; for modes 0 and 1 these are the whole slab i2 in {2w, 2w+1},
+      // so mode-0 and mode-1 passes of the same warp need no CTA barrier
+      // between them (mode 2, the cell solve and the scatter do).
       flush16<2>(xo, acc[2]);
       consumers_sync();
+      flush16<0>(xo, acc[0]);
+      __syncwarp();
+      flush16<1>(xo, acc[1]);
       mark(3);
       mbar_wait(&bar_v[slot], (it >> 1) & 1);
       mark(4);
       const double* vh = vhb + slot * 3 * VHS;
       const int* ex = g.ext;
       constexpr int VRI = 0, VRR = EE;
+      __syncwarp();
       cmode16<0, false, false, false>(xo, nullptr, xo, nullptr, vh + VRI, vh + VRI, vh, ex, a.tiny);
-      consumers_sync();
+      __syncwarp();
       cmode16<1, false, false, false>(xo, nullptr, xo, nullptr, vh + VHS + VRI, vh + VHS + VRI, vh, ex, a.tiny);
       consumers_sync();
       cmode16<2, false, false, false>(xo, nullptr, xo, nullptr, vh + 2 * VHS + VRI, vh + 2 * VHS + VRI, vh, ex,
@@ -741,12 +745,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       consumers_sync();
       const bool sing = cell_solve16(xo, g, vh, a.tiny);
       consumers_sync();
-      cmode16<0, false, false, false>(xo, nullptr, xo, nullptr, vh + VRR, vh + VRR, vh, ex, a.tiny);
-      consumers_sync();
-      cmode16<1, false, false, false>(xo, nullptr, xo, nullptr, vh + VHS + VRR, vh + VHS + VRR, vh, ex, a.tiny);
-      consumers_sync();
+      // back to the Schur basis: mode 2 first, then the warp-local modes 0, 1
       cmode16<2, false, false, false>(xo, nullptr, xo, nullptr, vh + 2 * VHS + VRR, vh + 2 * VHS + VRR, vh, ex,
                                       a.tiny);
+      consumers_sync();
+      cmode16<0, false, false, false>(xo, nullptr, xo, nullptr, vh + VRR, vh + VRR, vh, ex, a.tiny);
+      __syncwarp();
+      cmode16<1, false, false, false>(xo, nullptr, xo, nullptr, vh + VHS + VRR, vh + VHS + VRR, vh, ex, a.tiny);
       if (sing) atomicMin(a.status, static_cast<int>(g.lt < 0x7f7f7f7e ? g.lt : 0x7f7f7f7e));
       consumers_sync();
       mark(5);
