@@ -832,10 +832,9 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         pl->s_tm = (dims[0] + bm - 1) / bm;
         pl->s_bn = bn;
         pl->sdone_n = pl->s_tm * static_cast<int>((Q0 + bn - 1) / bn);
-        for (auto*& f : pl->sdone) {
-          TSG_CU(cudaMalloc(&f, pl->sdone_n * sizeof(int)));
-          TSG_CU(cudaMemset(f, 0, pl->sdone_n * sizeof(int)));
-        }
+        // one allocation for both directions (reset by one memset per solve)
+        TSG_CU(cudaMalloc(&pl->sdone[0], 2 * static_cast<size_t>(pl->sdone_n) * sizeof(int)));
+        pl->sdone[1] = pl->sdone[0] + pl->sdone_n;
       }
     }
   }
@@ -1300,10 +1299,10 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
       chain.pdl = (i == 0 && gate0) || (i > 0 && ps[i - 1].kind == 0) ? 1 : 0;
       if (schain && i == 0) {
         chain.dflags = sdone;
-        chain.depoch = pl->chain_epoch;
+        chain.depoch = 1;
       } else if (schain && i == 1) {
         chain.pflags = sdone;
-        chain.pepoch = pl->chain_epoch;
+        chain.pepoch = 1;
         chain.ptm = pl->s_tm;
         chain.pbn = pl->s_bn;
         chain.pcpb = pl->dims[1];
@@ -1335,13 +1334,13 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   const int d = pl->d;
   cudaEvent_t* ev = ctx->ev;
   pl->launches = 0;
-  ++pl->chain_epoch;
   double* work = nullptr;
   // Solve state reset first, so the forward GEMMs and the solve follow each
   // other directly (programmatic launches).
   TSG_CU(cudaMemsetAsync(pl->flags, 0, pl->ntiles * sizeof(int), st));
   TSG_CU(cudaMemsetAsync(pl->counter, 0, sizeof(int), st));
   TSG_CU(cudaMemsetAsync(pl->counter + 1, 0x7f, sizeof(int), st));  // kNoStatus
+  if (pl->sdone[0]) TSG_CU(cudaMemsetAsync(pl->sdone[0], 0, 2 * static_cast<size_t>(pl->sdone_n) * sizeof(int), st));
   // Forward transforms: outputs alternate w2/w1 and end in w1.
   if (!pl->reduced_only) {
     TSG_CU(transform_all(pl, in, pl->w1.p, pl->w2.p, true, st));

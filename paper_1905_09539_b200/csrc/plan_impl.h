@@ -62,9 +62,9 @@ struct tsg_plan {
   int gate_groups = 0;
   // Slab chain between the mode-0 and mode-1 transform GEMMs (fwd, back):
   // done flags of the mode-0 GEMM's CTA tiles (s_tm m-tiles, width s_bn),
-  // compared against a per-execution epoch (no reset).
+  // one allocation (sdone[1] = sdone[0] + sdone_n) reset at every solve.
   int* sdone[2] = {nullptr, nullptr};
-  int sdone_n = 0, s_tm = 0, s_bn = 0, chain_epoch = 0;
+  int sdone_n = 0, s_tm = 0, s_bn = 0;
   int64_t ntiles = 0;
   std::vector<std::vector<int>> bds_h;  // host tile boundaries per mode
   std::vector<int> order_h;             // host topological order (linear tile ids)
@@ -94,8 +94,7 @@ struct tsg_plan {
     if (counter) cudaFree(counter);
     if (gate_off) cudaFree(gate_off);
     if (gate_ids) cudaFree(gate_ids);
-    for (auto* f : sdone)
-      if (f) cudaFree(f);
+    if (sdone[0]) cudaFree(sdone[0]);
     if (gexec) cudaGraphExecDestroy(gexec);
   }
 };
