@@ -1337,10 +1337,8 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   double* work = nullptr;
   // Solve state reset first, so the forward GEMMs and the solve follow each
   // other directly (programmatic launches).
-  TSG_CU(cudaMemsetAsync(pl->flags, 0, pl->ntiles * sizeof(int), st));
-  TSG_CU(cudaMemsetAsync(pl->counter, 0, sizeof(int), st));
-  TSG_CU(cudaMemsetAsync(pl->counter + 1, 0x7f, sizeof(int), st));  // kNoStatus
-  if (pl->sdone[0]) TSG_CU(cudaMemsetAsync(pl->sdone[0], 0, 2 * static_cast<size_t>(pl->sdone_n) * sizeof(int), st));
+  TSG_CU(tsg::reset_state(pl->flags, pl->ntiles, pl->counter, kNoStatus, pl->sdone[0],
+                          2 * static_cast<int64_t>(pl->sdone_n), st));
   // Forward transforms: outputs alternate w2/w1 and end in w1.
   if (!pl->reduced_only) {
     TSG_CU(transform_all(pl, in, pl->w1.p, pl->w2.p, true, st));

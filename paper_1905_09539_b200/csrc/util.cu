@@ -1,5 +1,6 @@
 // Small device utilities: squared Frobenius norms and fused r -= t, used by
 // the device residual (tsg_residual; reference oracle.hpp:231-268).
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -39,7 +40,26 @@ int grid_for(int64_t n) {
   return static_cast<int>(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
 }
 
+__global__ void reset_kernel(int* flags, int64_t nf, int* counter, int status, int* extra, int64_t ne) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t i = i0; i < nf; i += stride) flags[i] = 0;
+  for (int64_t i = i0; i < ne; i += stride) extra[i] = 0;
+  if (i0 == 0) {
+    counter[0] = 0;
+    counter[1] = status;
+  }
+}
+
 }  // namespace
+
+cudaError_t reset_state(int* flags, int64_t nf, int* counter, int status, int* extra, int64_t ne,
+                        cudaStream_t st) {
+  const int64_t n = nf > ne ? nf : ne;
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256 + 1, 1184));
+  reset_kernel<<<blocks, 256, 0, st>>>(flags, nf, counter, status, extra, extra ? ne : 0);
+  return cudaGetLastError();
+}
 
 cudaError_t sumsq(const double* x, int64_t n, double* out_dev, cudaStream_t st) {
   sumsq_kernel<<<grid_for(n), 256, 0, st>>>(x, n, out_dev);

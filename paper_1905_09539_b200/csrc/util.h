@@ -7,4 +7,8 @@ namespace tsg {
 cudaError_t sumsq(const double* x, int64_t n, double* out_dev, cudaStream_t st);
 // y += a * x
 cudaError_t axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st);
+// Per-solve state reset in one launch: flags[0..nf) = 0, counter[0] = 0,
+// counter[1] = status (no singular cell), extra[0..ne) = 0 (may be null).
+cudaError_t reset_state(int* flags, int64_t nf, int* counter, int status, int* extra, int64_t ne,
+                        cudaStream_t st);
 }  // namespace tsg
