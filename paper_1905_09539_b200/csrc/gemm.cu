@@ -56,13 +56,13 @@ struct GemmSmem {
 template <int BM, int BN, int NT>
 TSG_DEVINL void gemm_prologue(const GemmArgs& g, int tid, int64_t& mt, int64_t& nt, int64_t& bt,
                               int64_t& tiles_m) {
-  const int64_t bid = blockIdx.x;
+  const int64_t bid = g.drev ? static_cast<int64_t>(gridDim.x) - 1 - blockIdx.x : blockIdx.x;
   tiles_m = (g.M + BM - 1) / BM;
   const int64_t tiles_n = (g.N + BN - 1) / BN;
   mt = bid % tiles_m;
   nt = (bid / tiles_m) % tiles_n;
   bt = bid / (tiles_m * tiles_n);
-  if (!g.wflags && !g.pflags) pdl_wait();
+  if (!g.wflags && !g.pflags && !g.nowait) pdl_wait();
   pdl_trigger();
   if (g.pflags) {
     if (g.pdesc) bt = g.batch - 1 - bt;
@@ -422,9 +422,11 @@ cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int
   }
   if (gate) {
     g.pdl = gate->pdl;
+    g.nowait = gate->nowait;
     if (g.batch == 1) {
       g.dflags = gate->dflags;
       g.depoch = gate->depoch;
+      g.drev = gate->drev;
     } else {
       g.pflags = gate->pflags;
       g.pepoch = gate->pepoch;

@@ -40,6 +40,9 @@ struct GemmArgs {
   // batches are issued last first (the producer finishes those first).
   const int* pflags = nullptr;
   int pepoch = 0, ptm = 0, pbn = 0, pcpb = 0, pdesc = 0;
+  // nowait: a programmatic launch whose inputs are complete by construction
+  // (skip griddepcontrol.wait); drev: issue the CTA tiles last first.
+  int nowait = 0, drev = 0;
 };
 
 // CTA tile (BM x BN) dgemm_nn uses for an M x N product (0 x 0: unknown).

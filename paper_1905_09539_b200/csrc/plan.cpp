@@ -832,10 +832,57 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         pl->s_tm = (dims[0] + bm - 1) / bm;
         pl->s_bn = bn;
         pl->sdone_n = pl->s_tm * static_cast<int>((Q0 + bn - 1) / bn);
-        // one allocation for both directions (reset by one memset per solve)
-        TSG_CU(cudaMalloc(&pl->sdone[0], 2 * static_cast<size_t>(pl->sdone_n) * sizeof(int)));
-        pl->sdone[1] = pl->sdone[0] + pl->sdone_n;
       }
+    }
+    // Trailing cube (TSG_CUBE = tiles per mode, default 4, 0 = off)
+    {
+      const char* ce = std::getenv("TSG_CUBE");
+      const int L1 = ce ? std::atoi(ce) : 4;
+      const char* cg = std::getenv("TSG_CUBE_GRID");
+      bool ok = L1 > 0 && family == 0 && !pl->reduced_only && d == 3 && pl->use16 && tsg::lap16_decoupled() &&
+                !(small_on && tsg::small_mode_ok(dims[2]));
+      for (int m = 0; ok && m < d; ++m) ok = pl->ntiles_mode[m] >= L1 + 3;
+      int bm = 0, bn = 0;
+      if (ok) tsg::gemm_tile_shape(dims[0] * dims[1], dims[2], &bm, &bn);
+      if (ok && bm > 0 && bn > 0) {
+        pl->cube = L1;
+        pl->cube_grid = cg ? std::max(1, std::atoi(cg)) : 12;
+        pl->fg_bm = bm;
+        pl->fg_bn = bn;
+        pl->fg_tm = (dims[0] * dims[1] + bm - 1) / bm;
+        pl->fdone_n = pl->fg_tm * ((dims[2] + bn - 1) / bn);
+        std::vector<int> o1, o2;
+        std::vector<unsigned long long> c1, c2;
+        for (int64_t q = 0; q < pl->ntiles; ++q) {
+          int64_t r = pl->order_h[q];
+          bool in = true;
+          unsigned long long pk = 0;
+          for (int m = 0; m < d; ++m) {
+            const int t = static_cast<int>(r % pl->ntiles_mode[m]);
+            r /= pl->ntiles_mode[m];
+            in = in && t >= pl->ntiles_mode[m] - L1;
+            pk |= static_cast<unsigned long long>(t) << (10 * m);
+          }
+          (in ? o1 : o2).push_back(pl->order_h[q]);
+          (in ? c1 : c2).push_back(pk);
+        }
+        TSG_CU(upload(&pl->order1, o1));
+        TSG_CU(upload(&pl->order2, o2));
+        TSG_CU(upload(&pl->ocoord1, c1));
+        TSG_CU(upload(&pl->ocoord2, c2));
+        pl->ntiles1 = static_cast<int64_t>(o1.size());
+        pl->ntiles2 = static_cast<int64_t>(o2.size());
+      }
+    }
+    // one allocation for the per-solve auxiliary flags (reset with the tile flags)
+    pl->aux_n = 2 * static_cast<int64_t>(pl->sdone_n) + pl->fdone_n + (pl->cube ? 1 : 0);
+    if (pl->aux_n > 0) {
+      TSG_CU(cudaMalloc(&pl->aux, pl->aux_n * sizeof(int)));
+      if (pl->sdone_n) {
+        pl->sdone[0] = pl->aux;
+        pl->sdone[1] = pl->aux + pl->sdone_n;
+      }
+      if (pl->cube) pl->fdone = pl->aux + 2 * static_cast<int64_t>(pl->sdone_n);
     }
   }
 
@@ -1256,7 +1303,8 @@ cudaError_t launch_plan_solve(tsg_plan* pl, const tsg::SolveArgs& a, cudaStream_
 // through the fused shared-memory pass two at a time (modes_small.cu).
 cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double* other, bool fwd,
                           cudaStream_t st, const tsg::GemmArgs* gate0 = nullptr,
-                          cudaEvent_t after0 = nullptr) {
+                          cudaEvent_t after0 = nullptr, int i_lo = 0, int i_hi = -1,
+                          const tsg::GemmArgs* last = nullptr) {
   const int d = pl->d;
   struct Pass {
     int m;
@@ -1284,8 +1332,10 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
   const bool schain = pl->sdone[0] && k >= 2 && ps[0].m == 0 && ps[0].kind == 0 && ps[1].m == 1 &&
                       ps[1].kind == 0 && !(sc_env && std::atoi(sc_env) == 0);
   int* sdone = pl->sdone[fwd ? 0 : 1];
-  const double* src = in;
-  for (int i = 0; i < k; ++i) {
+  if (i_hi < 0 || i_hi > k) i_hi = k;
+  // pass i reads the previous pass's output (ping-pong ending in target)
+  const double* src = i_lo == 0 ? in : (((k - i_lo) % 2 == 0) ? target : other);
+  for (int i = i_lo; i < i_hi; ++i) {
     double* dst = ((k - 1 - i) % 2 == 0) ? target : other;
     const int m = ps[i].m;
     const double* A = fwd ? pl->Fwd[m].p : pl->Bwd[m].p;
@@ -1307,6 +1357,13 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
         chain.pbn = pl->s_bn;
         chain.pcpb = pl->dims[1];
         chain.pdesc = gate0 && gate0->wflags ? 1 : 0;  // gated mode 0 runs last columns first
+      }
+      if (last && i == k - 1) {  // the last forward GEMM feeding the trailing cube
+        chain.pdl = last->pdl;
+        chain.nowait = last->nowait;
+        chain.dflags = last->dflags;
+        chain.depoch = last->depoch;
+        chain.drev = last->drev;
       }
       const tsg::GemmArgs* opt = &chain;
       e = tsg::mode_product(src, dst, d, pl->dims.data(), m, A, At, pl->dims[m], 1.0, 0.0, st,
@@ -1337,10 +1394,48 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   double* work = nullptr;
   // Solve state reset first, so the forward GEMMs and the solve follow each
   // other directly (programmatic launches).
-  TSG_CU(tsg::reset_state(pl->flags, pl->ntiles, pl->counter, kNoStatus, pl->sdone[0],
-                          2 * static_cast<int64_t>(pl->sdone_n), st));
+  TSG_CU(tsg::reset_state(pl->flags, pl->ntiles, pl->counter, kNoStatus, pl->aux, pl->aux_n, st));
+  const bool want_trace = std::getenv("TSG_TRACE") != nullptr;
+  const bool want_prof = std::getenv("TSG_PROF") != nullptr;
+  // TSG_GATE=0 (read per call) runs every kernel after its predecessor: the
+  // back transform after the solve, no trailing cube (bench kernel timing).
+  const char* gate_env = std::getenv("TSG_GATE");
+  const bool gate_off = gate_env && std::atoi(gate_env) == 0;
+  const bool cubed = pl->cube > 0 && !want_trace && !want_prof && !gate_off;
   // Forward transforms: outputs alternate w2/w1 and end in w1.
-  if (!pl->reduced_only) {
+  if (!pl->reduced_only && cubed) {
+    // all passes but the last; then the cube grid (resident on a few SMs,
+    // waiting per tile on the last GEMM's done flags); then the last GEMM
+    // as its programmatic dependent (inputs complete: no griddepcontrol.wait)
+    TSG_CU(transform_all(pl, in, pl->w1.p, pl->w2.p, true, st, nullptr, nullptr, 0, 2));
+    if (timing) TSG_CU(cudaEventRecord(ev[2], st));
+    work = pl->w1.p;
+    tsg::SolveArgs c{};
+    tsg_impl::fill_solve_args(pl, work, c);
+    c.flags = pl->flags;
+    c.fs[0] = pl->flags;
+    c.counter = pl->fdone + pl->fdone_n;
+    c.status = pl->counter + 1;
+    c.epoch = 1;
+    c.order = pl->order1;
+    c.ocoord = pl->ocoord1;
+    c.ntiles = pl->ntiles1;
+    c.gflags = pl->fdone;
+    c.gepoch = 1;
+    c.gbm = pl->fg_bm;
+    c.gbn = pl->fg_bn;
+    c.gtm = pl->fg_tm;
+    c.max_grid = pl->cube_grid;
+    TSG_CU(tsg::launch_solve_lap16(c, st, nullptr));
+    ++pl->launches;
+    tsg::GemmArgs lastg{};
+    lastg.pdl = 1;
+    lastg.nowait = 1;
+    lastg.dflags = pl->fdone;
+    lastg.depoch = 1;
+    lastg.drev = 1;
+    TSG_CU(transform_all(pl, in, pl->w1.p, pl->w2.p, true, st, nullptr, nullptr, 2, 3, &lastg));
+  } else if (!pl->reduced_only) {
     TSG_CU(transform_all(pl, in, pl->w1.p, pl->w2.p, true, st));
     work = pl->w1.p;
   } else {
@@ -1348,7 +1443,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     if (in != out)
       TSG_CU(cudaMemcpyAsync(out, in, pl->N * sizeof(double), cudaMemcpyDeviceToDevice, st));
   }
-  if (timing) TSG_CU(cudaEventRecord(ev[2], st));
+  if (timing && !cubed) TSG_CU(cudaEventRecord(ev[2], st));
   // Reduced solve.
   tsg::SolveArgs a{};
   tsg_impl::fill_solve_args(pl, work, a);
@@ -1357,12 +1452,30 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   a.counter = pl->counter;
   a.status = pl->counter + 1;
   a.epoch = 1;
+  if (cubed) {  // the cube's tiles are the first grid's
+    a.order = pl->order2;
+    a.ocoord = pl->ocoord2;
+    a.ntiles = pl->ntiles2;
+    // programmatic dependent of the last forward GEMM: CTAs take the SMs its
+    // last wave frees and start on the tiles whose right-hand side is done
+    static const bool main_gate = [] {
+      const char* e = std::getenv("TSG_CUBE_MAINGATE");
+      return !e || std::atoi(e) != 0;
+    }();
+    if (main_gate) {
+      a.gflags = pl->fdone;
+      a.gepoch = 1;
+      a.gbm = pl->fg_bm;
+      a.gbn = pl->fg_bn;
+      a.gtm = pl->fg_tm;
+      a.gate_pdl = 1;
+    }
+  }
   a.tiny = pl->tiny;
   a.refine = pl->refine;
   if (const char* e = std::getenv("TSG_DBG")) a.dbg = std::atoi(e);
   static unsigned long long* trace = nullptr;
   static int64_t trace_n = 0;
-  const bool want_trace = std::getenv("TSG_TRACE") != nullptr;
   if (want_trace) {
     if (trace_n < pl->ntiles) {
       if (trace) cudaFree(trace);
@@ -1372,7 +1485,6 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     a.trace = trace;
   }
   static unsigned long long* prof = nullptr;
-  const bool want_prof = std::getenv("TSG_PROF") != nullptr;
   if (want_prof) {
     if (!prof) cudaMalloc(&prof, 16 * sizeof(unsigned long long));
     cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
@@ -1439,9 +1551,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   // so the solve/back split point moves after it.
   // TSG_GATE=0 (read per call) runs the back transform after the solve, so
   // the bench can time the solve kernel alone.
-  const char* gate_env = std::getenv("TSG_GATE");
-  const bool gated = pl->gate_groups > 0 && !want_trace && !want_prof &&
-                     !(gate_env && std::atoi(gate_env) == 0);
+  const bool gated = pl->gate_groups > 0 && !want_trace && !want_prof && !gate_off;
   if (timing && !gated) TSG_CU(cudaEventRecord(ev[3], st));
   if (!pl->reduced_only) {
     tsg::GemmArgs gate{};

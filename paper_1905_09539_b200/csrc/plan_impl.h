@@ -65,6 +65,21 @@ struct tsg_plan {
   // one allocation (sdone[1] = sdone[0] + sdone_n) reset at every solve.
   int* sdone[2] = {nullptr, nullptr};
   int sdone_n = 0, s_tm = 0, s_bn = 0;
+  // Trailing cube (lap16d): the last `cube` tiles of every mode are solved
+  // by a small first grid (cube_grid CTAs, own queue) that runs beside the
+  // last forward GEMM, gated per tile on that GEMM's done flags (fdone);
+  // the main grid takes the other tiles.  aux = [sdone fwd | sdone back |
+  // fdone | cube queue head], reset with the tile flags at every solve.
+  int cube = 0, cube_grid = 0;
+  int* order1 = nullptr;
+  int* order2 = nullptr;
+  unsigned long long* ocoord1 = nullptr;
+  unsigned long long* ocoord2 = nullptr;
+  int64_t ntiles1 = 0, ntiles2 = 0;
+  int* fdone = nullptr;
+  int fdone_n = 0, fg_bm = 0, fg_bn = 0, fg_tm = 0;
+  int* aux = nullptr;
+  int64_t aux_n = 0;
   int64_t ntiles = 0;
   std::vector<std::vector<int>> bds_h;  // host tile boundaries per mode
   std::vector<int> order_h;             // host topological order (linear tile ids)
@@ -94,7 +109,10 @@ struct tsg_plan {
     if (counter) cudaFree(counter);
     if (gate_off) cudaFree(gate_off);
     if (gate_ids) cudaFree(gate_ids);
-    if (sdone[0]) cudaFree(sdone[0]);
+    if (aux) cudaFree(aux);
+    for (void* q : {static_cast<void*>(order1), static_cast<void*>(order2), static_cast<void*>(ocoord1),
+                    static_cast<void*>(ocoord2)})
+      if (q) cudaFree(q);
     if (gexec) cudaGraphExecDestroy(gexec);
   }
 };

@@ -77,6 +77,14 @@ struct SolveArgs {
   int slo[kMaxSlabs + 1];       // slab row bounds along mode d-1 (tile-aligned)
   double* xs[kMaxSlabs];
   int* fs[kMaxSlabs];           // tile flags of the slab owner (indexed by linear tile id)
+  // Forward gate (lap16d): the last forward GEMM (mode 2: rows i0 + n0 i1,
+  // columns i2) releases each gbm x gbn output tile as gflags[mt + nt * gtm]
+  // = gepoch; a tile loads its right-hand side once the GEMM tiles covering
+  // it are released (null: the whole forward pass precedes the launch).
+  const int* gflags;
+  int gepoch, gbm, gbn, gtm;
+  int max_grid;                 // > 0: at most this many CTAs (lap16d)
+  int gate_pdl;                 // with gflags: launch as a programmatic dependent of the gating GEMM
 };
 
 struct SolveLaunchInfo {

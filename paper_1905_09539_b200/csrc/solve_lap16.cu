@@ -584,7 +584,8 @@ TSG_DEVINL void fill_geometry(const SolveArgs& a, G16& g, int q, int lane) {
 
 __global__ void __launch_bounds__(THREADS, 1)
     solve_lap16d_kernel(SolveArgs a, const __grid_constant__ CUtensorMap tmx) {
-  pdl_wait();
+  // with the forward gate, right-hand sides are awaited per tile instead
+  if (!a.gflags) pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) double smem[];
   __shared__ G16 gq[2];
@@ -626,6 +627,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&info_full[slot]);
       if (done) break;
+      if (a.gflags) {
+        // forward gate: the GEMM tiles holding this tile's right-hand side
+        // (rows i0 + n0 i1 for i1 in the tile, one lane per i1)
+        if (lane < g.ext[1]) {
+          const int r0 = g.start[0] + a.dims[0] * (g.start[1] + lane);
+          const int mlo = r0 / a.gbm, mhi = (r0 + g.ext[0] - 1) / a.gbm;
+          const int nlo = g.start[2] / a.gbn, nhi = (g.start[2] + g.ext[2] - 1) / a.gbn;
+          for (int nt = nlo; nt <= nhi; ++nt)
+            for (int mt = mlo; mt <= mhi; ++mt) {
+              const int* f = a.gflags + mt + nt * a.gtm;
+              while (ld_acquire(f) != a.gepoch) __nanosleep(64);
+            }
+        }
+        __syncwarp();
+        fence_proxy_async();
+      }
       if (lane == 0) {
         double* vh = vhb + slot * 3 * VHS;
         mbar_expect_tx(&bar_v[slot], 3 * VHS * 8);
@@ -812,7 +829,12 @@ cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchI
     }
     int64_t grid = nsm2;
     if (grid > a.ntiles) grid = a.ntiles;
+    if (a.max_grid > 0 && grid > a.max_grid) grid = a.max_grid;
     if (info) *info = SolveLaunchInfo{static_cast<int>(grid), THREADS, D_BYTES, 1};
+    if (a.gflags && !a.gate_pdl) {  // gated on the NEXT kernel's output: plain launch
+      solve_lap16d_kernel<<<static_cast<unsigned>(grid), THREADS, D_BYTES, st>>>(a, map);
+      return cudaGetLastError();
+    }
     cudaError_t le = launch_pdl(solve_lap16d_kernel, static_cast<unsigned>(grid), THREADS, D_BYTES, st, a, map);
     return le != cudaSuccess ? le : cudaGetLastError();
   }

@@ -328,3 +328,38 @@ def test_gated_back_transform_bitexact():
         assert r.returncode == 0, r.stderr[-2000:]
         res[g] = r.stdout.strip().splitlines()[-1]
     assert res["0"] == res["1"], res
+
+
+_CUBE_SCRIPT = r"""
+import hashlib, os, sys
+import numpy as np
+sys.path.insert(0, os.getcwd())
+import paper_1905_09539_b200 as T
+cfg = T.SolverConfig(strategy=T.Strategy.recursion_only, arithmetic=T.Arithmetic.real_quasitriangular)
+out = []
+for dims, seed in [((128, 128, 128), 1), ((160, 144, 136), 2)]:
+    p = T.make_problem(2, dims, seed=seed)
+    x = np.ascontiguousarray(T.solve_laplace(p, cfg).solution)
+    out.append(hashlib.sha256(x.tobytes()).hexdigest()[:16])
+print(" ".join(out))
+"""
+
+
+# Trailing cube (plan.cpp cube_*): the last tiles of every mode solved by a
+# small first grid beside the last forward GEMM, gated per tile on its done
+# flags, the main grid gated likewise; forced here on the 16^3 kernel with a
+# 2-tile cube.  Same tile operations -> bit-identical to the plain order.
+def test_trailing_cube_bitexact():
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for c in ("0", "2"):
+        env = dict(os.environ, TSG_LAP16="1", TSG_CUBE=c, TSG_CUBE_GRID="3", PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", _CUBE_SCRIPT], cwd=root, env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[c] = r.stdout.strip().splitlines()[-1]
+    assert res["0"] == res["2"], res
