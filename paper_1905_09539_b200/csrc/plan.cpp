@@ -834,10 +834,10 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         pl->sdone_n = pl->s_tm * static_cast<int>((Q0 + bn - 1) / bn);
       }
     }
-    // Trailing cube (TSG_CUBE = tiles per mode, default 4, 0 = off)
+    // Trailing cube (TSG_CUBE = tiles per mode, default 6, 0 = off; TSG_CUBE_GRID CTAs, default 16)
     {
       const char* ce = std::getenv("TSG_CUBE");
-      const int L1 = ce ? std::atoi(ce) : 4;
+      const int L1 = ce ? std::atoi(ce) : 6;
       const char* cg = std::getenv("TSG_CUBE_GRID");
       bool ok = L1 > 0 && family == 0 && !pl->reduced_only && d == 3 && pl->use16 && tsg::lap16_decoupled() &&
                 !(small_on && tsg::small_mode_ok(dims[2]));
@@ -846,7 +846,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       if (ok) tsg::gemm_tile_shape(dims[0] * dims[1], dims[2], &bm, &bn);
       if (ok && bm > 0 && bn > 0) {
         pl->cube = L1;
-        pl->cube_grid = cg ? std::max(1, std::atoi(cg)) : 12;
+        pl->cube_grid = cg ? std::max(1, std::atoi(cg)) : 16;
         pl->fg_bm = bm;
         pl->fg_bn = bn;
         pl->fg_tm = (dims[0] * dims[1] + bm - 1) / bm;
