@@ -844,7 +844,9 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       for (int m = 0; ok && m < d; ++m) ok = pl->ntiles_mode[m] >= L1 + 3;
       int bm = 0, bn = 0;
       if (ok) tsg::gemm_tile_shape(dims[0] * dims[1], dims[2], &bm, &bn);
-      if (ok && bm > 0 && bn > 0) {
+      int nsm = 0;
+      if (ok) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
+      if (ok && bm > 0 && bn > 0 && nsm >= 4 * (cg ? std::max(1, std::atoi(cg)) : 16)) {
         pl->cube = L1;
         pl->cube_grid = cg ? std::max(1, std::atoi(cg)) : 16;
         pl->fg_bm = bm;
@@ -1401,7 +1403,15 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   // back transform after the solve, no trailing cube (bench kernel timing).
   const char* gate_env = std::getenv("TSG_GATE");
   const bool gate_off = gate_env && std::atoi(gate_env) == 0;
-  const bool cubed = pl->cube > 0 && !want_trace && !want_prof && !gate_off;
+  // The cube grid waits on the NEXT kernel (the last forward GEMM): only
+  // with concurrent kernels.  Serialising tools (Nsight Compute / Systems,
+  // compute-sanitizer, CUDA_LAUNCH_BLOCKING=1) run without it.
+  static const bool serialized = [] {
+    const char* lb = std::getenv("CUDA_LAUNCH_BLOCKING");
+    return (lb && std::atoi(lb) != 0) || std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") ||
+           std::getenv("NV_TPS_LAUNCH_TOKEN") || std::getenv("CUDA_INJECTION64_PATH");
+  }();
+  const bool cubed = pl->cube > 0 && !want_trace && !want_prof && !gate_off && !serialized;
   // Forward transforms: outputs alternate w2/w1 and end in w1.
   if (!pl->reduced_only && cubed) {
     // all passes but the last; then the cube grid (resident on a few SMs,
