@@ -32,6 +32,7 @@ struct PairArgs {
   int64_t P, Q;     // prefix (modes < a) and suffix (modes > b) sizes
   int64_t nblk;     // blocks
   int bsz;          // doubles per block = c * na * nb * o
+  int vec;          // 16-byte chunks (runs of even length at even offsets)
 };
 
 // y[f, i] = sum_k M(i, k) x[f, k] for the fibres of the block along a
@@ -85,29 +86,53 @@ TSG_DEVINL void fibres(double* blk, const double* M, int st, int nf) {
   }
 }
 
+// Double-buffered: while the fibres of block b are multiplied in shared
+// memory, block b + grid streams into the other buffer (cp.async, 16-byte
+// chunks when the block's contiguous runs allow), so HBM traffic overlaps
+// the DMMA work; results go back with 16-byte stores.
 template <int NA, int NB>
 __global__ void __launch_bounds__(THREADS) pair_kernel(PairArgs g) {
   extern __shared__ __align__(16) double sm[];
   double* ma = sm;
   double* mb = sm + NA * NA;
-  double* blk = mb + (NB > 1 ? NB * NB : 0);
+  double* buf0 = mb + (NB > 1 ? NB * NB : 0);
   for (int e = threadIdx.x; e < NA * NA; e += THREADS) ma[e] = g.A[e];
   if (NB > 1)
     for (int e = threadIdx.x; e < NB * NB; e += THREADS) mb[e] = g.B[e];
   const int c = g.c, o = g.o;
   constexpr int GRP = NA * NB;
-  for (int64_t bk = blockIdx.x; bk < g.nblk; bk += gridDim.x) {
-    // block bk -> (prefix chunk pc, suffix chunk sc)
-    const int64_t npc = g.P / c;
+  const int64_t npc = g.P / c;
+  // element e of a block: (ic, gi, io) at base + ic + P * (gi + GRP * io);
+  // runs of c consecutive elements are contiguous, as is the whole block
+  // when P == 1, so pairs (e, e + 1) with e even are 16-byte chunks
+  const bool vec = g.vec != 0;
+  auto base_of = [&](int64_t bk) {
     const int64_t pc = bk % npc, sc = bk / npc;
-    const int64_t base = pc * c + sc * static_cast<int64_t>(o) * g.P * GRP;
-    __syncthreads();  // previous block written back
-    // gather: element (ic, gi, io) at base + ic + P * (gi + grp * io)
-    for (int e = threadIdx.x; e < g.bsz; e += THREADS) {
-      const int ic = e & (c - 1), rest = e >> g.lc;
-      const int gi = rest % GRP, io = rest / GRP;
-      blk[e] = g.X[base + ic + g.P * (gi + static_cast<int64_t>(GRP) * io)];
+    return pc * c + sc * static_cast<int64_t>(o) * g.P * GRP;
+  };
+  auto off_of = [&](int e) {
+    const int ic = e & (c - 1), rest = e >> g.lc;
+    const int gi = rest % GRP, io = rest / GRP;
+    return ic + g.P * (gi + static_cast<int64_t>(GRP) * io);
+  };
+  auto gather = [&](int64_t bk, double* blk) {
+    const int64_t base = base_of(bk);
+    if (vec) {
+      for (int e = 2 * threadIdx.x; e < g.bsz; e += 2 * THREADS) cp_async16(blk + e, g.X + base + off_of(e), 16);
+    } else {
+      for (int e = threadIdx.x; e < g.bsz; e += THREADS) cp_async8(blk + e, g.X + base + off_of(e), 8);
     }
+    cp_async_commit();
+  };
+  int64_t bk = blockIdx.x;
+  if (bk < g.nblk) gather(bk, buf0);
+  for (int it = 0; bk < g.nblk; bk += gridDim.x, ++it) {
+    double* blk = buf0 + (it & 1) * g.bsz;
+    double* nxt = buf0 + ((it + 1) & 1) * g.bsz;
+    const int64_t bn = bk + gridDim.x;
+    if (bn < g.nblk) gather(bn, nxt);  // the other buffer was scattered last round
+    else cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
     fibres<NA>(blk, ma, c, g.bsz / NA);  // mode a: stride c in the block
     if constexpr (NB > 1) {
@@ -115,17 +140,21 @@ __global__ void __launch_bounds__(THREADS) pair_kernel(PairArgs g) {
       fibres<NB>(blk, mb, c * NA, g.bsz / NB);
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < g.bsz; e += THREADS) {
-      const int ic = e & (c - 1), rest = e >> g.lc;
-      const int gi = rest % GRP, io = rest / GRP;
-      g.Y[base + ic + g.P * (gi + static_cast<int64_t>(GRP) * io)] = blk[e];
+    const int64_t base = base_of(bk);
+    if (vec) {
+      for (int e = 2 * threadIdx.x; e < g.bsz; e += 2 * THREADS)
+        *reinterpret_cast<double2*>(g.Y + base + off_of(e)) = *reinterpret_cast<const double2*>(blk + e);
+    } else {
+      for (int e = threadIdx.x; e < g.bsz; e += THREADS) g.Y[base + off_of(e)] = blk[e];
     }
+    __syncthreads();  // blk is the next round's prefetch target
   }
+  cp_async_wait_all();
 }
 
 template <int NA, int NB>
 cudaError_t launch_pair(const PairArgs& g, cudaStream_t st) {
-  const int smem = (NA * NA + (NB > 1 ? NB * NB : 0) + g.bsz) * 8;
+  const int smem = (NA * NA + (NB > 1 ? NB * NB : 0) + 2 * g.bsz) * 8;
   auto k = pair_kernel<NA, NB>;
   static int nsm = 0, occ = 0, last_smem = -1;
   if (last_smem != smem) {
@@ -179,7 +208,7 @@ cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, 
   for (int v = b + 1; v < d; ++v) g.Q *= dims[v];
   const int grp = g.na * g.nb;
   // ~8-9K doubles per block: inner chunk from the prefix, else outer batch
-  const int target = 9216;
+  const int target = 4608;  // two buffers of ~36 KB: 2-3 CTAs per SM
   g.c = 1;
   g.o = 1;
   if (g.P > 1) {
@@ -195,6 +224,8 @@ cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, 
   g.lc = 0;
   while ((1 << g.lc) < g.c) ++g.lc;
   g.nblk = (g.P / g.c) * (g.Q / g.o);
+  g.vec = ((g.c % 2 == 0 && g.P % 2 == 0) || (g.c == 1 && g.P == 1 && grp % 2 == 0)) &&
+          (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
   if (flops) *flops += 2.0 * static_cast<double>(g.P) * g.Q * grp * (g.na + g.nb - (pair ? 0 : 1));
   switch (g.na) {
     case 16: return dispatch_b<16>(g, st);
