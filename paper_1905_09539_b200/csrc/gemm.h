@@ -64,6 +64,9 @@ cudaError_t mode_product(const double* X, double* Y, int d, const int* dims, int
 // Fused small-mode transform (modes_small.cu): Y = X x_a A (x_{a+1} B when
 // pair), one HBM pass; extents 16, 24, 32, 40 only (small_mode_ok).
 bool small_mode_ok(int n);
+// The fused pass over mode a (and a + 1 when pair) is available for this
+// shape (extents as above and whole 8-fibre blocks per shared-memory block).
+bool small_pass_ok(int d, const int* dims, int a, bool pair);
 cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, int a, bool pair,
                             const double* A, const double* B, cudaStream_t st, double* flops = nullptr);
 

@@ -190,6 +190,41 @@ cudaError_t dispatch_b(const PairArgs& g, cudaStream_t st) {
 
 bool small_mode_ok(int n) { return n == 16 || n == 24 || n == 32 || n == 40; }
 
+namespace {
+// Block shape of a fused pass: c | P (inner chunk of the prefix), o | Q
+// (outer batch), powers of two, ~4.6K doubles per block.  The fibre
+// products work on whole 8-fibre blocks, so the fibres per block along
+// mode a (c * nb * o) and mode b (c * na * o) must be multiples of 8: pairs
+// always are (extents 16..40); a single mode may need o > 1 (odd prefix) and
+// is unsupported when neither P nor Q supplies the factor (GEMM then).
+bool pass_shape(int64_t P, int64_t Q, int na, int nb, int* c_out, int* o_out) {
+  const int grp = na * nb;
+  const int target = 4608;  // two buffers of ~36 KB: 2-3 CTAs per SM
+  int c = 1, o = 1;
+  if (P > 1) {
+    while (c * 2 * grp <= target && P % (c * 2) == 0) c *= 2;
+  } else {
+    while (o * 2 * grp <= target && Q % (o * 2) == 0) o *= 2;
+  }
+  auto ok = [&] { return (c * nb * o) % 8 == 0 && (nb == 1 || (c * na * o) % 8 == 0); };
+  while (!ok() && Q % (o * 2) == 0 && c * grp * o * 2 <= 2 * target) o *= 2;
+  if (!ok()) return false;
+  *c_out = c;
+  *o_out = o;
+  return true;
+}
+}  // namespace
+
+bool small_pass_ok(int d, const int* dims, int a, bool pair) {
+  const int b = pair ? a + 1 : a;
+  if (a < 0 || b >= d || !small_mode_ok(dims[a]) || (pair && !small_mode_ok(dims[b]))) return false;
+  int64_t P = 1, Q = 1;
+  for (int v = 0; v < a; ++v) P *= dims[v];
+  for (int v = b + 1; v < d; ++v) Q *= dims[v];
+  int c, o;
+  return pass_shape(P, Q, dims[a], pair ? dims[b] : 1, &c, &o);
+}
+
 cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, int a, bool pair,
                             const double* A, const double* B, cudaStream_t st, double* flops) {
   const int b = pair ? a + 1 : a;
@@ -207,19 +242,7 @@ cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, 
   for (int v = 0; v < a; ++v) g.P *= dims[v];
   for (int v = b + 1; v < d; ++v) g.Q *= dims[v];
   const int grp = g.na * g.nb;
-  // ~8-9K doubles per block: inner chunk from the prefix, else outer batch
-  const int target = 4608;  // two buffers of ~36 KB: 2-3 CTAs per SM
-  g.c = 1;
-  g.o = 1;
-  if (g.P > 1) {
-    int c = 1;
-    while (c * 2 * grp <= target && g.P % (c * 2) == 0) c *= 2;
-    g.c = c;
-  } else {
-    int o = 1;
-    while (o * 2 * grp <= target && g.Q % (o * 2) == 0) o *= 2;
-    g.o = o;
-  }
+  if (!pass_shape(g.P, g.Q, g.na, g.nb, &g.c, &g.o)) return cudaErrorNotSupported;
   g.bsz = g.c * grp * g.o;
   g.lc = 0;
   while ((1 << g.lc) < g.c) ++g.lc;

@@ -839,8 +839,10 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       const char* ce = std::getenv("TSG_CUBE");
       const int L1 = ce ? std::atoi(ce) : 6;
       const char* cg = std::getenv("TSG_CUBE_GRID");
+      // three GEMM forward passes (enqueue splits them 2 + 1 around the cube grid)
       bool ok = L1 > 0 && family == 0 && !pl->reduced_only && d == 3 && pl->use16 && tsg::lap16_decoupled() &&
-                !(small_on && tsg::small_mode_ok(dims[2]));
+                !(small_on && (tsg::small_mode_ok(dims[0]) || tsg::small_mode_ok(dims[1]) ||
+                               tsg::small_mode_ok(dims[2])));
       for (int m = 0; ok && m < d; ++m) ok = pl->ntiles_mode[m] >= L1 + 3;
       int bm = 0, bn = 0;
       if (ok) tsg::gemm_tile_shape(dims[0] * dims[1], dims[2], &bm, &bn);
@@ -1318,12 +1320,12 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
     return !e || std::atoi(e) != 0;
   }();
   for (int m = 0; m < d;) {
-    const bool sm = small_on && tsg::small_mode_ok(pl->dims[m]);
-    if (sm && m + 1 < d && tsg::small_mode_ok(pl->dims[m + 1])) {
+    const int* dm = pl->dims.data();
+    if (small_on && m + 1 < d && tsg::small_pass_ok(d, dm, m, true)) {
       ps.push_back({m, 2});
       m += 2;
     } else {
-      ps.push_back({m, sm ? 1 : 0});
+      ps.push_back({m, small_on && tsg::small_pass_ok(d, dm, m, false) ? 1 : 0});
       m += 1;
     }
   }

@@ -181,7 +181,10 @@ def test_lap16_kernel_matches_reference(gpu, ref, kind, dims, monkeypatch):
 # Fused small-mode transforms (modes_small.cu): consecutive extents in
 # {16, 24, 32, 40} are transformed two modes per HBM pass.
 @pytest.mark.parametrize("dims", [(16, 24, 32), (24, 24, 24, 16), (32, 16, 24, 24, 16), (7, 24, 24, 16),
-                                  (40, 40, 24), (7, 40, 40, 16), (9, 16, 40)])
+                                  (40, 40, 24), (7, 40, 40, 16), (9, 16, 40),
+                                  # single small modes behind an odd prefix: blocks widen along the
+                                  # suffix to whole 8-fibre groups, or the mode falls back to a GEMM
+                                  (79, 32, 21), (5, 40, 3), (3, 16)])
 def test_small_mode_transforms(gpu, ref, dims):
     p = gpu.make_problem(2, dims, seed=6)
     want, _ = ref.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
