@@ -17,7 +17,15 @@ RES = 1e-12
 
 
 def _shapes():
-    rng = np.random.default_rng(2026)
+    # TSG_FUZZ_SEEDS=k runs k seeded draws (default one)
+    import os
+    out = []
+    for seed in range(2026, 2026 + int(os.environ.get("TSG_FUZZ_SEEDS", "1"))):
+        out += _draw(np.random.default_rng(seed))
+    return out
+
+
+def _draw(rng):
     out = []
     for _ in range(4):  # lap3 / generic order 3
         out.append((2, tuple(int(v) for v in rng.integers(20, 90, 3)), {}))
@@ -29,6 +37,18 @@ def _shapes():
     out.append((2, (24, 40, 16, 11), {}))  # small-mode pairs
     out.append((5, (37, 9, 9, 9), {}))     # gsylv
     out.append((5, (50, 24, 24), {}))
+    # small extents (fused transform passes) mixed with odd ones, any position
+    small = [16, 24, 32, 40]
+    for _ in range(10):
+        d = int(rng.integers(2, 5))
+        dims = [int(rng.choice(small)) if rng.random() < 0.5 else int(rng.integers(3, 30)) for _ in range(d)]
+        if int(np.prod(dims)) > 400_000:
+            dims[-1] = 3
+        out.append((2, tuple(dims), {}))
+    for _ in range(3):
+        n0 = int(rng.integers(5, 40))
+        nt = int(rng.choice(small + [7, 9]))
+        out.append((5, (n0, nt, nt), {}))
     return out
 
 
