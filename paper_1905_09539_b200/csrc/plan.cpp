@@ -523,6 +523,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   std::vector<std::vector<double>> pdvs(d), nfs(d);
   pl->tmode.assign(d, nullptr);
   pl->bnd.assign(d, nullptr);
+  pl->rowtile.assign(d, nullptr);
 
   double scale = 0;
   std::vector<std::vector<int8_t>> codes(d);
@@ -739,6 +740,12 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     pl->ntiles_mode[m] = static_cast<int>(bds[m].size()) - 1;
     pl->ntiles *= pl->ntiles_mode[m];
     TSG_CU(upload(&pl->bnd[m], bds[m]));
+    {
+      std::vector<int> rt(dims[m], 0);
+      for (int t = 0; t + 1 < static_cast<int>(bds[m].size()); ++t)
+        for (int i = bds[m][t]; i < bds[m][t + 1]; ++i) rt[i] = t;
+      TSG_CU(upload(&pl->rowtile[m], rt));
+    }
     if (!mts[m].dh.empty()) TSG_CU(upload_mat(pl->dhat[m], mts[m].dh.data(), mts[m].dh.size()));
     if (!mts[m].vh.empty()) TSG_CU(upload_mat(pl->vhat[m], mts[m].vh.data(), mts[m].vh.size()));
     TSG_CU(upload(&pl->tmode[m], mts[m].tms));
@@ -1270,6 +1277,7 @@ void fill_solve_args(const tsg_plan* pl, double* work, tsg::SolveArgs& a) {
     a.vhat[m] = pl->vhat[m].p;
     a.ntiles_mode[m] = pl->ntiles_mode[m];
     a.bnd[m] = pl->bnd[m];
+    a.rowtile[m] = pl->rowtile[m];
     if (pl->family == 1 && m >= 1) a.W[m] = pl->wchain[m].p;
   }
   a.Tc = pl->family == 1 ? pl->Tc.p : nullptr;

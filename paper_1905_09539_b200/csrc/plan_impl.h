@@ -46,6 +46,7 @@ struct tsg_plan {
   DevBuf Tc;
   std::vector<tsg::TileMode*> tmode;
   std::vector<int*> bnd;
+  std::vector<int*> rowtile;  // per mode: tile index of every row
   int* order = nullptr;
   unsigned long long* ocoord = nullptr;
   int fast = 0;  // 1: solve_lap_kernel, 3: solve_lap3_kernel (Laplace, good eigenbases)
@@ -102,6 +103,8 @@ struct tsg_plan {
     for (auto* b : tmode)
       if (b) cudaFree(b);
     for (auto* b : bnd)
+      if (b) cudaFree(b);
+    for (auto* b : rowtile)
       if (b) cudaFree(b);
     if (order) cudaFree(order);
     if (ocoord) cudaFree(ocoord);

@@ -51,6 +51,7 @@ struct SolveArgs {
   const double* eig[kMaxOrder]; // per row: kEigStride doubles (valid at block starts)
   int ntiles_mode[kMaxOrder];
   const int* bnd[kMaxOrder];    // tile boundaries per mode (ntiles_mode+1)
+  const int* rowtile[kMaxOrder];  // per mode: tile index of every row
   int64_t ntiles;
   const int* order;             // topological order of linear tile ids
   const unsigned long long* ocoord;  // packed tile coordinates of order[] (10 bits/mode)

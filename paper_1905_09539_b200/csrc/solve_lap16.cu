@@ -96,7 +96,10 @@ TSG_DEVINL int addr16(int i, int n) {
 }
 
 // chunk c of the tile: mode, first row, end row (far ranges first, then the
-// near tiles t+1), identical on the producer and the consumers
+// near tiles t+1), identical on the producer and the consumers.  Far ranges
+// (tiles >= t+2) run top down, so the chunks of long-finished tiles go first
+// and the t+2 rows, released last, come at the end of the group (the
+// producer waits per chunk on the tile holding its first row).
 struct Chunk {
   int m, k, kh, first;  // first: first chunk of its (mode, far/near) group
 };
@@ -108,7 +111,13 @@ TSG_DEVINL Chunk chunk_of(const G16& g, const int* dims, int c) {
       const int lo = part == 0 ? g.flo[m] : g.nlo[m];
       const int hi = part == 0 ? dims[m] : g.flo[m];
       const int n = hi > lo ? (hi - lo + E - 1) / E : 0;
-      if (c < n) return Chunk{m + 3 * part, lo + E * c, hi, c == 0};
+      if (c < n) {
+        if (part == 0) {
+          const int k = lo + E * (n - 1 - c);
+          return Chunk{m, k, min(k + E, hi), c == 0};
+        }
+        return Chunk{m + 3, lo + E * c, hi, c == 0};
+      }
       c -= n;
     }
   return Chunk{0, 0, 0, 0};
@@ -643,11 +652,36 @@ __global__ void __launch_bounds__(THREADS, 1)
         __syncwarp();
         fence_proxy_async();
       }
-      if (lane == 0) {
+      if (lane == 0) {  // the tile's bases first (no dependency)
         double* vh = vhb + slot * 3 * VHS;
         mbar_expect_tx(&bar_v[slot], 3 * VHS * 8);
         for (int m = 0; m < 3; ++m)
           bulk_g2s(vh + m * VHS, a.vhat[m] + static_cast<int64_t>(g.tco[m]) * VHS, VHS * 8, &bar_v[slot]);
+      }
+      // far groups: which tiles above t+1 are already released?  lanes
+      // 10 m + j read the flag of tile t + (2 + j) e_m; released tiles along
+      // a mode form a suffix, so the lowest offset with every offset above
+      // it released confirms all those tiles (rdy[m]: lowest confirmed tile
+      // index along m; ten released offsets confirm everything from t+2 up)
+      int rdy[3];
+      {
+        const int pm = lane / 10, off = 2 + lane % 10;
+        bool okf = true;
+        if (pm < 3 && g.tco[pm] + off < a.ntiles_mode[pm])
+          okf = ld_acquire(a.flags + g.lt + off * mul[pm]) >= a.epoch;
+        const unsigned bal = __ballot_sync(0xffffffffu, okf);
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          const unsigned bits = (bal >> (10 * m)) & 0x3ffu;  // bit j: offset 2 + j
+          int o = 12;                                      // lowest offset of the released suffix
+          while (o > 2 && ((bits >> (o - 3)) & 1u)) --o;
+          rdy[m] = o == 12 ? a.ntiles_mode[m] : g.tco[m] + o;
+          if (bits == 0x3ffu) rdy[m] = g.tco[m] + 2;
+        }
+        __syncwarp();
+        fence_proxy_async();
+      }
+      if (lane == 0) {
         const int nch = g.nch;
         bool bx = false;
         auto issue_bx = [&]() {
@@ -662,8 +696,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < nch; ++c, ++gch) {
           const Chunk ch = chunk_of(g, a.dims, c);
           const int m = ch.m % 3;
-          if (ch.first) {
-            wait_tile(a, g.lt + (ch.m < 3 ? 2 : 1) * mul[m]);
+          if (ch.m < 3) {  // far chunk: the tile holding its first row
+            const int tk = a.rowtile[m][ch.k];
+            if (tk < rdy[m]) {
+              wait_tile(a, g.lt + (tk - g.tco[m]) * mul[m]);
+              fence_proxy_async();
+              rdy[m] = tk;
+            }
+          } else if (ch.first) {
+            wait_tile(a, g.lt + mul[m]);
             fence_proxy_async();
           }
           const int s = gch % DNS;
