@@ -1497,12 +1497,14 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   static unsigned long long* trace = nullptr;
   static int64_t trace_n = 0;
   if (want_trace) {
-    if (trace_n < pl->ntiles) {
+    if (trace_n < 4 * pl->ntiles) {
       if (trace) cudaFree(trace);
-      cudaMalloc(&trace, pl->ntiles * sizeof(unsigned long long));
-      trace_n = pl->ntiles;
+      cudaMalloc(&trace, 4 * pl->ntiles * sizeof(unsigned long long));
+      trace_n = 4 * pl->ntiles;
     }
+    cudaMemsetAsync(trace, 0, 4 * pl->ntiles * sizeof(unsigned long long), st);
     a.trace = trace;
+    a.ntiles_total = pl->ntiles;
   }
   static unsigned long long* prof = nullptr;
   if (want_prof) {
@@ -1514,9 +1516,10 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   ++pl->launches;
   if (want_trace) {
     // per hyperplane: count, first and last release (us from the first release)
-    std::vector<unsigned long long> tr(pl->ntiles);
-    cudaMemcpyAsync(tr.data(), trace, pl->ntiles * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+    std::vector<unsigned long long> tr(pl->ntiles), tr4(4 * pl->ntiles);
+    cudaMemcpyAsync(tr4.data(), trace, 4 * pl->ntiles * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
+    std::copy(tr4.begin(), tr4.begin() + pl->ntiles, tr.begin());
     unsigned long long t0 = ~0ull;
     for (auto v : tr) t0 = std::min(t0, v);
     std::vector<int> hp(pl->ntiles);
@@ -1542,6 +1545,22 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     std::fprintf(stderr, "[tsg trace] hyperplane: tiles first_us last_us\n");
     for (int h = H; h >= 0; --h)
       std::fprintf(stderr, "[tsg trace] %3d %5d %9.1f %9.1f\n", h, cnt[h], lo[h], hi[h]);
+    if (tr4[pl->ntiles] | tr4[pl->ntiles + 1]) {  // -DL16_TRACE2=1 build: per-tile phases
+      std::vector<double> c2f(H + 1, 0), f2d(H + 1, 0), d2r(H + 1, 0), cl(H + 1, 0);
+      for (int64_t t = 0; t < pl->ntiles; ++t) {
+        const double rel = tr[t], cla = tr4[pl->ntiles + t], far = tr4[2 * pl->ntiles + t],
+                     dn = tr4[3 * pl->ntiles + t];
+        const double f = far > 0 ? far : cla;
+        c2f[hp[t]] += (f - cla) * 1e-3;
+        f2d[hp[t]] += (dn - f) * 1e-3;
+        d2r[hp[t]] += (rel - dn) * 1e-3;
+        cl[hp[t]] += (cla - t0) * 1e-3;
+      }
+      std::fprintf(stderr, "[tsg trace2] hp tiles claim_us claim->far_done far_done->chunks_done chunks_done->release (avg us)\n");
+      for (int h = H; h >= 0; --h)
+        std::fprintf(stderr, "[tsg trace2] %3d %5d %9.1f %9.1f %9.1f %9.1f\n", h, cnt[h], cl[h] / cnt[h],
+                     c2f[h] / cnt[h], f2d[h] / cnt[h], d2r[h] / cnt[h]);
+    }
   }
   if (want_prof) {
     unsigned long long h[16];

@@ -86,6 +86,7 @@ struct SolveArgs {
   int gepoch, gbm, gbn, gtm;
   int max_grid;                 // > 0: at most this many CTAs (lap16d)
   int gate_pdl;                 // with gflags: launch as a programmatic dependent of the gating GEMM
+  int64_t ntiles_total;         // all tiles of the plan (trace layout; development)
 };
 
 struct SolveLaunchInfo {

@@ -34,6 +34,9 @@ namespace {
 #ifndef L16_PROF
 #define L16_PROF 0
 #endif
+#ifndef L16_TRACE2
+#define L16_TRACE2 0  // development: claim / far-done / chunks-done times per tile (TSG_TRACE)
+#endif
 
 constexpr int E = 16, EE = 256, TT = 4096;
 constexpr int CW = 8;                 // consumer warps
@@ -633,6 +636,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool done = q >= a.ntiles;
       if (!done) fill_geometry(a, g, q, lane);
       if (lane == 0) g.done = done ? 1 : 0;
+#if L16_TRACE2
+      if (lane == 0 && !done && a.trace) {
+        unsigned long long tt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+        a.trace[a.ntiles_total + g.lt] = tt;  // claimed
+      }
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&info_full[slot]);
       if (done) break;
@@ -762,6 +772,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const Chunk cn = chunk_of(g, a.dims, c + 1);
         if (c + 1 < nch) chunk_afrag(a, g, cn.m % 3, cn.k, cn.kh, an);
         const int s = gch % DNS;
+#if L16_TRACE2
+        if (tid == 0 && a.trace && ch.m >= 3 && (c == 0 || chunk_of(g, a.dims, c - 1).m < 3)) {
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+          a.trace[2 * a.ntiles_total + g.lt] = tt;  // far groups done
+        }
+#endif
         mbar_wait(full + s, (gch / DNS) & 1);
         const int m = ch.m % 3;
         const double* box = ring + s * TD + ((m == 0 ? ch.k : g.start[0]) & 1);
@@ -775,6 +792,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         ch = cn;
       }
       mark(1);
+#if L16_TRACE2
+      if (tid == 0 && a.trace) {
+        unsigned long long tt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+        a.trace[3 * a.ntiles_total + g.lt] = tt;  // all chunks done
+      }
+#endif
       mbar_wait(&bar_x, it & 1);
       mark(2);
       double* xo = xr + (g.start[0] & 1);
