@@ -661,7 +661,8 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   const bool want16 = pl->fast == 3 && d == 3 && !tsg_impl::g_force_lap3 && !std::getenv("TSG_LT") &&
                       (e16 ? std::atoi(e16) != 0
                            : (dims[0] >= 64 && dims[1] >= 64 && dims[2] >= 64 && pl->N >= (int64_t{1} << 23))) &&
-                      dims[0] % 2 == 0;  // TMA: 16-byte row strides
+                      dims[0] % 2 == 0 &&  // TMA: 16-byte row strides
+                      dims[0] <= 1024 && dims[1] <= 1024 && dims[2] <= 1024;  // per-tile chunk list
   if (want16) {
     pl->tile_ext = choose_tiles(family, pl->dims, o, tsg::solve_lap16_caps());
     double prod = 1.0;

@@ -75,6 +75,7 @@ struct G16 {
   int done;            // decoupled kernel: no more tiles
   int nc[3];           // Schur cells (1x1 / 2x2) of the tile's diagonal blocks
   unsigned char cs[3][16], cz[3][16];
+  unsigned ck[208];    // decoupled kernel: the tile's chunk list (pack_chunk), n_m <= 1024
 };
 
 TSG_DEVINL void mbar_arrive(uint64_t* bar) {
@@ -124,6 +125,17 @@ TSG_DEVINL Chunk chunk_of(const G16& g, const int* dims, int c) {
       c -= n;
     }
   return Chunk{0, 0, 0, 0};
+}
+
+// chunk list entries: mode group (3 bits), first row, end row (12 bits
+// each), first-of-group flag; built once per tile by the producer warp
+TSG_DEVINL unsigned pack_chunk(const Chunk& c) {
+  return static_cast<unsigned>(c.m) | (static_cast<unsigned>(c.k) << 3) | (static_cast<unsigned>(c.kh) << 15) |
+         (static_cast<unsigned>(c.first) << 27);
+}
+TSG_DEVINL Chunk unpack_chunk(unsigned v) {
+  return Chunk{static_cast<int>(v & 7u), static_cast<int>((v >> 3) & 4095u), static_cast<int>((v >> 15) & 4095u),
+               static_cast<int>(v >> 27)};
 }
 
 // acc[rb][cb] += T_M[rows, k..k+15] * box(k, cols) for this warp's 4 column
@@ -592,6 +604,9 @@ TSG_DEVINL void fill_geometry(const SolveArgs& a, G16& g, int q, int lane) {
     }
     g.nch = (a.dbg & 4) ? 0 : nch;
   }
+  __syncwarp();
+  for (int c = lane; c < g.nch; c += 32) g.ck[c] = pack_chunk(chunk_of(g, a.dims, c));
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -704,7 +719,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // regimes: the consumers idle), else after the ring is filled
         if (nch == 0 || it == 0 || mbar_test(&xr_free, (it - 1) & 1)) issue_bx();
         for (int c = 0; c < nch; ++c, ++gch) {
-          const Chunk ch = chunk_of(g, a.dims, c);
+          const Chunk ch = unpack_chunk(g.ck[c]);
           const int m = ch.m % 3;
           if (ch.m < 3) {  // far chunk: the tile holding its first row
             const int tk = a.rowtile[m][ch.k];
@@ -766,14 +781,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int cb = 0; cb < 4; ++cb) acc[m][rb][cb][0] = acc[m][rb][cb][1] = 0.0;
       double af[4][2], an[4][2];
-      Chunk ch = chunk_of(g, a.dims, 0);
+      Chunk ch = nch > 0 ? unpack_chunk(g.ck[0]) : Chunk{0, 0, 0, 0};
       if (nch > 0) chunk_afrag(a, g, ch.m % 3, ch.k, ch.kh, af);
       for (int c = 0; c < nch; ++c, ++gch) {
-        const Chunk cn = chunk_of(g, a.dims, c + 1);
+        const Chunk cn = c + 1 < nch ? unpack_chunk(g.ck[c + 1]) : Chunk{0, 0, 0, 0};
         if (c + 1 < nch) chunk_afrag(a, g, cn.m % 3, cn.k, cn.kh, an);
         const int s = gch % DNS;
 #if L16_TRACE2
-        if (tid == 0 && a.trace && ch.m >= 3 && (c == 0 || chunk_of(g, a.dims, c - 1).m < 3)) {
+        if (tid == 0 && a.trace && ch.m >= 3 && (c == 0 || unpack_chunk(g.ck[c - 1]).m < 3)) {
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           a.trace[2 * a.ntiles_total + g.lt] = tt;  // far groups done
