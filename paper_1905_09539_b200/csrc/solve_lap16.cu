@@ -34,6 +34,9 @@ namespace {
 #ifndef L16_PROF
 #define L16_PROF 0
 #endif
+#ifndef L16_ORDER_AB
+#define L16_ORDER_AB 1  // decoupled kernel: far chunks of tiles >= t+3 first, then the t+2 rows of every mode
+#endif
 #ifndef L16_TRACE2
 #define L16_TRACE2 0  // development: claim / far-done / chunks-done times per tile (TSG_TRACE)
 #endif
@@ -605,7 +608,28 @@ TSG_DEVINL void fill_geometry(const SolveArgs& a, G16& g, int q, int lane) {
     g.nch = (a.dbg & 4) ? 0 : nch;
   }
   __syncwarp();
+#if L16_ORDER_AB
+  // far chunks of tiles >= t+3 (top down, mode after mode), then the lowest
+  // far chunk of every mode (tile t+2's rows, released last), then near
+  if (lane == 0) {
+    int n[3], c = 0;
+    for (int m = 0; m < 3; ++m) n[m] = a.dims[m] > g.flo[m] ? (a.dims[m] - g.flo[m] + E - 1) / E : 0;
+    for (int m = 0; m < 3; ++m)
+      for (int j = n[m] - 1; j >= 1; --j) {
+        const int k = g.flo[m] + E * j;
+        g.ck[c++] = pack_chunk(Chunk{m, k, min(k + E, a.dims[m]), 0});
+      }
+    for (int m = 0; m < 3; ++m)
+      if (n[m] > 0) g.ck[c++] = pack_chunk(Chunk{m, g.flo[m], min(g.flo[m] + E, a.dims[m]), 0});
+    for (int m = 0; m < 3; ++m) {
+      const int lo = g.nlo[m], hi = g.flo[m];
+      const int nn = hi > lo ? (hi - lo + E - 1) / E : 0;
+      for (int j = 0; j < nn; ++j) g.ck[c++] = pack_chunk(Chunk{m + 3, lo + E * j, hi, j == 0});
+    }
+  }
+#else
   for (int c = lane; c < g.nch; c += 32) g.ck[c] = pack_chunk(chunk_of(g, a.dims, c));
+#endif
   __syncwarp();
 }
 
