@@ -7,17 +7,19 @@
 //     feeds one row block per tile extent, so 16-row tiles halve the L2
 //     traffic of sum_m T_m[t, later] x_m X(later) (24 N vs 48 N doubles);
 //   * memory-level parallelism: one producer warp streams the update
-//     operand as 16x16x16 boxes of X (cp.async.bulk.tensor, 32 KB each)
-//     into a two-stage mbarrier ring, so the eight consumer warps only issue
-//     DMMA and shared-memory fragment loads (no register-bound load batches).
+//     operand as 16x16x16 boxes of X (cp.async.bulk.tensor, padded to
+//     20x17x16 = 43.5 KB for conflict-free fragment loads) through an
+//     mbarrier ring (two stages here, three in the decoupled kernel below,
+//     which is the default), so the eight consumer warps only issue DMMA and
+//     shared-memory fragment loads (no register-bound load batches).
 // The base case block-diagonalises the tile over the reals: with V_m the real
 // eigenvector basis of the tile's diagonal Schur block (1x1 cells keep their
 // eigenvector, 2x2 cells take [Re v, Im v]),
 //   y = x x_0 V0^-1 x_1 V1^-1 x_2 V2^-1,  cell solves (<= 8 unknowns each,
 //   closed form, cell_solve16),  x = y x_m V_m:
-// six real 16x16x256 DMMA GEMMs, using the ring as the work tile.  Plans
-// choose this kernel only when every tile's bases are well conditioned
-// (tsg_plan: vcond product <= kDiagCond).
+// six real 16x16x256 DMMA GEMMs (this kernel: the ring as the work tile;
+// the decoupled kernel: in place).  Plans choose these kernels only when every
+// tile's bases are well conditioned (tsg_plan: vcond product <= kDiagCond).
 // One CTA (8 consumer + 1 producer warps) per SM.
 // Reference: lap_rec / lap_base (laplace.hpp:99-153), mode_multiply update
 // (laplace.hpp:147), block_back_substitution (kernels.hpp:179-261).
@@ -567,7 +569,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 // The base case works in place in xr (each warp reads and writes only its
 // own cross-section columns of a mode product), which frees the former work
 // tile for a third ring stage (the ring is never touched by the consumers
-// outside the update phase).
+// outside the update phase).  The producer also builds the tile's chunk list
+// once (G16::ck: far tiles >= t+3 of every mode top down, then the t+2 rows,
+// then the near groups), checks the far tiles' flags in one batched poll and
+// waits per chunk only on tiles not yet released; with the forward gate
+// (trailing cube, SolveArgs::gflags) it first acquires the last forward
+// GEMM's tiles under the tile's right-hand side.
 // ---------------------------------------------------------------------------
 #ifndef L16_DNS
 #define L16_DNS 3
