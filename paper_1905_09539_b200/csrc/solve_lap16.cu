@@ -765,10 +765,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           const int s = gch % DNS;
           if (gch >= DNS) mbar_wait(empty + s, ((gch / DNS) - 1) & 1);
-          int cc[3] = {g.start[0], g.start[1], g.start[2]};
-          cc[m] = ch.k;
+          // box origin: the chunk's first row along m, the tile's start elsewhere
+          const int c0 = m == 0 ? ch.k : g.start[0], c1 = m == 1 ? ch.k : g.start[1],
+                    c2 = m == 2 ? ch.k : g.start[2];
           mbar_expect_tx(full + s, BOX_BYTES);
-          tma_load_3d(ring + s * TD, &tmx, cc[0] & ~1, cc[1], cc[2], full + s);
+          tma_load_3d(ring + s * TD, &tmx, c0 & ~1, c1, c2, full + s);
           if (!bx && (c == DNS - 1 || c + 1 == nch)) issue_bx();  // ring filled first
         }
       }
