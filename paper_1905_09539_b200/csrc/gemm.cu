@@ -343,8 +343,33 @@ void gemm_tile_shape(int M, int N, int* bm, int* bn) {
   else *bm = 128, *bn = 128;
 }
 
+// Shared-memory attributes of every kernel the default dispatch can pick,
+// set once up front: a cudaFuncSetAttribute between two launches of a
+// programmatic-dependent pair (first use of an instantiation) serialises
+// them, and the trailing-cube grid waits on its dependent GEMM.
+template <int BM, int BN, int WM, int WN>
+void set_attrs() {
+  const int bytes = GemmSmem<BM, BN>::BYTES;
+  cudaFuncSetAttribute(dgemm_nn_kernel<BM, BN, WM, WN, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(dgemm_nn_kernel<BM, BN, WM, WN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(dgemm_nn_kernel<BM, BN, WM, WN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+void gemm_prepare() {
+  static const bool done = [] {
+    set_attrs<64, 64, 32, 32>();
+    set_attrs<128, 64, 32, 32>();
+    set_attrs<64, 128, 32, 32>();
+    set_attrs<64, 64, 32, 16>();
+    set_attrs<128, 128, 64, 32>();
+    return true;
+  }();
+  (void)done;
+}
+
 cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
+  gemm_prepare();
   static int cfg = -1;
   if (cfg < 0) {
     const char* e = std::getenv("TSG_GEMM_CFG");

@@ -842,6 +842,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         pl->sdone_n = pl->s_tm * static_cast<int>((Q0 + bn - 1) / bn);
       }
     }
+    tsg::gemm_prepare();  // kernel attributes before any launch chain (see gemm.cu)
     // Trailing cube (TSG_CUBE = tiles per mode, default 6, 0 = off; TSG_CUBE_GRID CTAs, default 16)
     {
       const char* ce = std::getenv("TSG_CUBE");
@@ -1021,6 +1022,8 @@ int tsg_plan_execute(tsg_plan* pl, const double* B, double* X, int inputs_on_dev
     rep->zero_pivot_index = hstat[1] == kNoStatus ? -1 : hstat[1];
     rep->kernel_launches = pl->launches;
   }
+  if (hstat[1] == tsg::kGateTimeout)
+    return fail(ctx, TSG_ECUDA, "reduced solve: forward gate timed out (serialised launches)");
   if (hstat[1] != kNoStatus)
     return fail(ctx, TSG_ESINGULAR,
                 "reduced solve: numerically singular base cell in tile " + std::to_string(hstat[1]));
@@ -1097,6 +1100,8 @@ int tsg_plan_execute_stream(tsg_plan* pl, int nrhs, const double* const* B, doub
   cudaEventDestroy(t1);
   cudaStreamDestroy(cin);
   cudaStreamDestroy(cout);
+  if (hstat[1] == tsg::kGateTimeout)
+    return fail(ctx, TSG_ECUDA, "reduced solve: forward gate timed out (serialised launches)");
   if (hstat[1] != kNoStatus)
     return fail(ctx, TSG_ESINGULAR, "reduced solve: numerically singular base cell in tile " + std::to_string(hstat[1]));
   return TSG_OK;
@@ -1447,6 +1452,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     c.gbn = pl->fg_bn;
     c.gtm = pl->fg_tm;
     c.max_grid = pl->cube_grid;
+    if (const char* e = std::getenv("TSG_DBG")) c.dbg = std::atoi(e);
     TSG_CU(tsg::launch_solve_lap16(c, st, nullptr));
     ++pl->launches;
     tsg::GemmArgs lastg{};
@@ -1605,6 +1611,19 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
                          gated && timing ? ev[3] : nullptr));
   }
   if (timing) TSG_CU(cudaEventRecord(ev[4], st));
+  if (cubed && std::getenv("TSG_DBG_FDONE")) {  // development: unreleased forward-gate tiles
+    std::vector<int> fd(pl->fdone_n);
+    cudaMemcpyAsync(fd.data(), pl->fdone, pl->fdone_n * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    int nun = 0;
+    for (int i = 0; i < pl->fdone_n; ++i)
+      if (fd[i] != 1) {
+        if (nun < 12) std::fprintf(stderr, "[tsg dbg] fdone[%d] (mt %d nt %d) = %d\n", i, i % pl->fg_tm, i / pl->fg_tm, fd[i]);
+        ++nun;
+      }
+    std::fprintf(stderr, "[tsg dbg] fdone unreleased %d of %d (tm %d, bm %d, bn %d)\n", nun, pl->fdone_n, pl->fg_tm,
+                 pl->fg_bm, pl->fg_bn);
+  }
   return TSG_OK;
 }
 

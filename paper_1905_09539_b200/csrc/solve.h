@@ -89,6 +89,9 @@ struct SolveArgs {
   int64_t ntiles_total;         // all tiles of the plan (trace layout; development)
 };
 
+// SolveArgs::status value of a forward gate that never opened (lap16d).
+constexpr int kGateTimeout = 0x7e000000;
+
 struct SolveLaunchInfo {
   int grid, block, smem_bytes, ctas_per_sm;
 };

@@ -702,7 +702,16 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int nt = nlo; nt <= nhi; ++nt)
             for (int mt = mlo; mt <= mhi; ++mt) {
               const int* f = a.gflags + mt + nt * a.gtm;
-              while (ld_acquire(f) != a.gepoch) __nanosleep(64);
+              // bounded: the gating GEMM must run beside this grid; if it
+              // cannot (serialised launches), fail the solve instead of hanging
+              long long spins = 0;
+              while (ld_acquire(f) != a.gepoch) {
+                __nanosleep(64);
+                if (++spins > ((a.dbg & 32768) ? 2000000LL : (1LL << 26))) {
+                  atomicExch(a.status, kGateTimeout);
+                  break;
+                }
+              }
             }
         }
         __syncwarp();

@@ -226,6 +226,40 @@ def test_plan_execute_stream_matches_single(gpu):
         assert rel_diff(x, w) < 1e-15
 
 
+def test_plan_stream_and_enqueue_with_cube(gpu, monkeypatch):
+    """The host-streaming and asynchronous entry points on a plan with every
+    overlap active (16^3 kernel forced, a 2-tile trailing cube, back-transform
+    gate, slab chain) give the synchronous solve's bits."""
+    import torch
+    from paper_1905_09539_b200.plan import Context, Plan
+    monkeypatch.setenv("TSG_LAP16", "1")
+    monkeypatch.setenv("TSG_CUBE", "2")
+    monkeypatch.setenv("TSG_CUBE_GRID", "4")
+    dims = (144, 136, 128)
+    p = gpu.make_problem(2, dims, seed=12)
+    fs = [gpu.schur(a) for a in p.coeffs]
+    pl = Plan(Context(0), 0, [f[1] for f in fs], [f[0] for f in fs])
+    rng = np.random.default_rng(5)
+    bs = [np.asfortranarray(rng.standard_normal(dims)) for _ in range(3)]
+    want = []
+    for b in bs:
+        x = np.zeros_like(b)
+        pl.execute_host(b, x)
+        want.append(x)
+    xs = [np.zeros_like(b) for b in bs]
+    pl.execute_stream([b.ctypes.data for b in bs], [x.ctypes.data for x in xs])
+    for x, w in zip(xs, want):
+        assert np.array_equal(x, w)
+    bd = [torch.from_numpy(np.ascontiguousarray(b.reshape(-1, order="F"))).cuda() for b in bs]
+    xd = [torch.zeros_like(b) for b in bd]
+    for b, x in zip(bd, xd):
+        pl.enqueue_device(b.data_ptr(), x.data_ptr())
+    assert pl.sync().zero_pivot_index == -1
+    for x, w in zip(xd, want):
+        assert np.array_equal(x.cpu().numpy(), w.reshape(-1, order="F"))
+    assert rel_diff(want[0], gpu.solve_laplace(gpu.LaplaceProblem(p.coeffs, bs[0])).solution) < REL
+
+
 def test_plan_enqueue_back_to_back(gpu):
     """tsg_plan_enqueue: several asynchronous device-resident solves into
     different outputs, then tsg_plan_sync; each matches the synchronous
