@@ -1,3 +1,8 @@
+"""One solve through a plan (host buffers: `host`, or the streaming entry
+point: `stream`) for a given shape, printing the time: used under `timeout`
+to probe the overlap machinery for hangs, e.g.
+  TSG_LAP16=1 TSG_CUBE=2 TSG_CUBE_GRID=4 timeout 30 python tools/cube_dbg.py host 144,136,128
+(development)."""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np
@@ -16,4 +21,3 @@ if step == "host":
 elif step == "stream":
     pl.execute_stream([b.ctypes.data], [x.ctypes.data])
 print(step, dims, "ok", time.time() - t, flush=True)
-rep = pl.execute_device  # noqa
