@@ -64,12 +64,15 @@ TSG_DEVINL int fibre_lt(const SolveArgs& a, int m, int f) {
 }
 
 // (xr, xi) fibres along mode m (padded extent P) times the 8x8-record
-// complex matrix (re at Vr, im at Vr + 64; the tile's P x P block)
-template <int D, int P>
-TSG_DEVINL void fibre_cmode(const SolveArgs& a, const GD<D>& g, double* xr, double* xi, const double* Vr,
-                            int ep, int m) {
+// complex matrix (re at Vr, im at Vr + 64; the tile's P x P block).  DIV:
+// then divide every element by mu = sum_v lambda_v(i_v) (the last forward
+// pass; returns true when a valid element has |mu| <= tiny)
+template <int D, int P, bool DIV = false>
+TSG_DEVINL bool fibre_cmode(const SolveArgs& a, const GD<D>& g, double* xr, double* xi, const double* Vr,
+                            int ep, int m, const double* vh = nullptr) {
   const double* Vi = Vr + 64;
   const int shm = a.tsh[m];
+  bool sing = false;
   for (int f = threadIdx.x; f < ep / P; f += THREADS) {
     const int lt0 = fibre_lt<D>(a, m, f);
     double zr[P], zi[P];
@@ -77,6 +80,19 @@ TSG_DEVINL void fibre_cmode(const SolveArgs& a, const GD<D>& g, double* xr, doub
     for (int r = 0; r < P; ++r) {
       zr[r] = xr[lt0 + (r << shm)];
       zi[r] = xi[lt0 + (r << shm)];
+    }
+    // DIV: the eigenvalue sum of the fibre's other modes, once per fibre
+    double br = 0.0, bi = 0.0;
+    bool bvalid = true;
+    if constexpr (DIV) {
+#pragma unroll
+      for (int v = 0; v < D; ++v) {
+        if (v == m) continue;
+        const int iv = (lt0 >> a.tsh[v]) & ((1 << a.tlog[v]) - 1);
+        bvalid &= iv < g.ext[v];
+        br += vh[v * VHS + 256 + iv];
+        bi += vh[v * VHS + 264 + iv];
+      }
     }
 #pragma unroll
     for (int r = 0; r < P; ++r) {
@@ -87,10 +103,23 @@ TSG_DEVINL void fibre_cmode(const SolveArgs& a, const GD<D>& g, double* xr, doub
         sr = fma(ar, zr[c], fma(-ai, zi[c], sr));
         si = fma(ar, zi[c], fma(ai, zr[c], si));
       }
+      if constexpr (DIV) {
+        const double mr = br + vh[m * VHS + 256 + r], mi = bi + vh[m * VHS + 264 + r];
+        const double den = mr * mr + mi * mi;
+        if (!(den > a.tiny * a.tiny)) {
+          if (bvalid && r < g.ext[m]) sing = true;
+          sr = si = 0.0;
+        } else {
+          const double inv = 1.0 / den, pr = sr, pi = si;
+          sr = (pr * mr + pi * mi) * inv;
+          si = (pi * mr - pr * mi) * inv;
+        }
+      }
       xr[lt0 + (r << shm)] = sr;
       xi[lt0 + (r << shm)] = si;
     }
   }
+  return sing;
 }
 
 template <int D, int NB, int UB>
@@ -307,37 +336,23 @@ __global__ void __launch_bounds__(THREADS, LAPD_MINB) solve_lapd_kernel(SolveArg
 #pragma unroll 1
       for (int m = 0; m < D; ++m) {
         const double* Vr = vh + m * VHS + (pass == 0 ? 0 : 128);
-        switch (a.tlog[m]) {
-          case 0: fibre_cmode<D, 1>(a, g, xr, xi, Vr, ep, m); break;
-          case 1: fibre_cmode<D, 2>(a, g, xr, xi, Vr, ep, m); break;
-          case 2: fibre_cmode<D, 4>(a, g, xr, xi, Vr, ep, m); break;
-          default: fibre_cmode<D, 8>(a, g, xr, xi, Vr, ep, m); break;
-        }
-        __syncthreads();
-      }
-      if (pass == 0) {
-        bool sing = false;
-        for (int l = tid; l < ep; l += THREADS) {
-          double mr = 0.0, mi = 0.0;
-          bool valid = true;
-#pragma unroll
-          for (int v = 0; v < D; ++v) {
-            const int iv = (l >> a.tsh[v]) & ((1 << a.tlog[v]) - 1);
-            valid &= iv < g.ext[v];
-            mr += vh[v * VHS + 256 + iv];
-            mi += vh[v * VHS + 264 + iv];
+        if (pass == 0 && m == D - 1) {  // last forward pass: division by mu fused
+          bool sing = false;
+          switch (a.tlog[m]) {
+            case 0: sing = fibre_cmode<D, 1, true>(a, g, xr, xi, Vr, ep, m, vh); break;
+            case 1: sing = fibre_cmode<D, 2, true>(a, g, xr, xi, Vr, ep, m, vh); break;
+            case 2: sing = fibre_cmode<D, 4, true>(a, g, xr, xi, Vr, ep, m, vh); break;
+            default: sing = fibre_cmode<D, 8, true>(a, g, xr, xi, Vr, ep, m, vh); break;
           }
-          const double den = mr * mr + mi * mi;
-          if (!(den > a.tiny * a.tiny)) {
-            if (valid) sing = true;
-            xr[l] = xi[l] = 0.0;
-          } else {
-            const double inv = 1.0 / den, pr = xr[l], pi = xi[l];
-            xr[l] = (pr * mr + pi * mi) * inv;
-            xi[l] = (pi * mr - pr * mi) * inv;
+          if (sing) atomicMin(a.status, static_cast<int>(g.lt < 0x7f7f7f7e ? g.lt : 0x7f7f7f7e));
+        } else {
+          switch (a.tlog[m]) {
+            case 0: fibre_cmode<D, 1>(a, g, xr, xi, Vr, ep, m); break;
+            case 1: fibre_cmode<D, 2>(a, g, xr, xi, Vr, ep, m); break;
+            case 2: fibre_cmode<D, 4>(a, g, xr, xi, Vr, ep, m); break;
+            default: fibre_cmode<D, 8>(a, g, xr, xi, Vr, ep, m); break;
           }
         }
-        if (sing) atomicMin(a.status, static_cast<int>(g.lt < 0x7f7f7f7e ? g.lt : 0x7f7f7f7e));
         __syncthreads();
       }
     }
