@@ -140,13 +140,15 @@ TSG_DEVINL int fibre_lt(const SolveArgs& a, int m, int f) {
 // block) buf(fibre), P the padded extent of mode m (compile time)
 template <int D, int P>
 TSG_DEVINL void rmode_p(const SolveArgs& a, double* buf, const double* add, const double* M, int ep, int m,
-                        double sign) {
+                        double sign, const double* src = nullptr) {
+  // buf(fibre) = add(fibre) + sign M src(fibre), src = buf when null
   const int shm = a.tsh[m];
+  const double* in = src ? src : buf;
   for (int f = threadIdx.x; f < ep / P; f += THREADS) {
     const int lt0 = fibre_lt<D>(a, m, f);
     double x[P];
 #pragma unroll
-    for (int r = 0; r < P; ++r) x[r] = buf[lt0 + (r << shm)];
+    for (int r = 0; r < P; ++r) x[r] = in[lt0 + (r << shm)];
 #pragma unroll
     for (int r = 0; r < P; ++r) {
       double s = 0.0;
@@ -160,12 +162,12 @@ TSG_DEVINL void rmode_p(const SolveArgs& a, double* buf, const double* add, cons
 
 template <int D>
 TSG_DEVINL void rmode(const SolveArgs& a, const GG<D>& g, double* buf, const double* add, const double* M,
-                      int ep, int m, double sign = 1.0) {
+                      int ep, int m, double sign = 1.0, const double* src = nullptr) {
   switch (a.tlog[m]) {
-    case 0: rmode_p<D, 1>(a, buf, add, M, ep, m, sign); break;
-    case 1: rmode_p<D, 2>(a, buf, add, M, ep, m, sign); break;
-    case 2: rmode_p<D, 4>(a, buf, add, M, ep, m, sign); break;
-    default: rmode_p<D, 8>(a, buf, add, M, ep, m, sign); break;
+    case 0: rmode_p<D, 1>(a, buf, add, M, ep, m, sign, src); break;
+    case 1: rmode_p<D, 2>(a, buf, add, M, ep, m, sign, src); break;
+    case 2: rmode_p<D, 4>(a, buf, add, M, ep, m, sign, src); break;
+    default: rmode_p<D, 8>(a, buf, add, M, ep, m, sign, src); break;
   }
 }
 
@@ -459,13 +461,10 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
     }
 
     // ---- W chain: W_{d-1} = A_{d-1} X + L_{d-1}, W_m = A_m W_{m+1} + L_m ----
-    for (int l = tid; l < ep; l += THREADS) rb[l] = xr[l];
-    __syncthreads();
+    // in place in the chain buffers: lb[m-1] = L_m + A_m W_{m+1}, W_d = X (xr)
 #pragma unroll 1
     for (int m = D - 1; m >= 1; --m) {
-      rmode<D>(a, g, rb, lb[m - 1], blk[m], ep, m);  // rb = A_m rb + L_m = W_m
-      __syncthreads();
-      for (int l = tid; l < ep; l += THREADS) lb[m - 1][l] = rb[l];
+      rmode<D>(a, g, lb[m - 1], lb[m - 1], blk[m], ep, m, 1.0, m == D - 1 ? xr : lb[m]);
       __syncthreads();
     }
 
