@@ -342,11 +342,9 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
     }
 
     // ---- R = A_1 (A_2 (... L_{d-1}) + L_2) + L_1; rhs -= Tc_tt R ----
-    for (int l = tid; l < ep; l += THREADS) rb[l] = lb[D - 2][l];
-    __syncthreads();
 #pragma unroll 1
-    for (int m = D - 2; m >= 1; --m) {
-      rmode<D>(a, g, rb, lb[m - 1], blk[m], ep, m);
+    for (int m = D - 2; m >= 1; --m) {  // the first step reads L_{d-1} in place
+      rmode<D>(a, g, rb, lb[m - 1], blk[m], ep, m, 1.0, m == D - 2 ? lb[D - 2] : nullptr);
       __syncthreads();
     }
     rmode<D>(a, g, rb, xr, blk[D], ep, 0, -1.0);  // rb = xr - Tc_tt R
