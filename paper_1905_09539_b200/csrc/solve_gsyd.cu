@@ -351,14 +351,10 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
     __syncthreads();
 
     // ---- base case: tail eigenbasis, mode-0 pencil back substitution ----
-    for (int l = tid; l < ep; l += THREADS) {
-      xr[l] = rb[l];
-      xi[l] = 0.0;
-    }
-    __syncthreads();
+    // works on rb (= B~ - Tc_tt R) and xi (zeroed by the gather) in place
 #pragma unroll 1
     for (int m = 1; m < D; ++m) {
-      cmode<D>(a, g, xr, xi, vh + (m - 1) * VHS, ep, m);
+      cmode<D>(a, g, rb, xi, vh + (m - 1) * VHS, ep, m);
       __syncthreads();
     }
     bool sing = false;
@@ -383,7 +379,7 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
 #pragma unroll
         for (int r = 0; r < 8; ++r)
           if (r < e0) {
-            br[r] = xr[lt0 + r];
+            br[r] = rb[lt0 + r];
             bi[r] = xi[lt0 + r];
           }
         // back substitution over the Schur cells of S (last row first; all
@@ -445,7 +441,7 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
 #pragma unroll
         for (int r = 0; r < 8; ++r)
           if (r < e0) {
-            xr[lt0 + r] = br[r];
+            rb[lt0 + r] = br[r];
             xi[lt0 + r] = bi[r];
           }
       }
@@ -454,15 +450,15 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
     __syncthreads();
 #pragma unroll 1
     for (int m = 1; m < D; ++m) {
-      cmode<D>(a, g, xr, xi, vh + (m - 1) * VHS + 128, ep, m);
+      cmode<D>(a, g, rb, xi, vh + (m - 1) * VHS + 128, ep, m);
       __syncthreads();
     }
 
     // ---- W chain: W_{d-1} = A_{d-1} X + L_{d-1}, W_m = A_m W_{m+1} + L_m ----
-    // in place in the chain buffers: lb[m-1] = L_m + A_m W_{m+1}, W_d = X (xr)
+    // in place in the chain buffers: lb[m-1] = L_m + A_m W_{m+1}, W_d = X (rb)
 #pragma unroll 1
     for (int m = D - 1; m >= 1; --m) {
-      rmode<D>(a, g, lb[m - 1], lb[m - 1], blk[m], ep, m, 1.0, m == D - 1 ? xr : lb[m]);
+      rmode<D>(a, g, lb[m - 1], lb[m - 1], blk[m], ep, m, 1.0, m == D - 1 ? rb : lb[m]);
       __syncthreads();
     }
 
@@ -470,7 +466,7 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
     for (int l = tid; l < ep; l += THREADS) {
       const int64_t off = goff[l];
       if (off >= 0) {
-        a.X[off] = xr[l];
+        a.X[off] = rb[l];
 #pragma unroll
         for (int m = 1; m < D; ++m) a.W[m][off] = lb[m - 1][l];
       }
