@@ -207,7 +207,7 @@ bool pass_shape(int64_t P, int64_t Q, int na, int nb, int* c_out, int* o_out) {
     while (o * 2 * grp <= target && Q % (o * 2) == 0) o *= 2;
   }
   auto ok = [&] { return (c * nb * o) % 8 == 0 && (nb == 1 || (c * na * o) % 8 == 0); };
-  while (!ok() && Q % (o * 2) == 0 && c * grp * o * 2 <= 2 * target) o *= 2;
+  while (!ok() && Q % (o * 2) == 0 && c * grp * o * 2 <= target) o *= 2;  // stay within the block budget
   if (!ok()) return false;
   *c_out = c;
   *o_out = o;
