@@ -1,8 +1,10 @@
 """Benchmark of the B200 Schur-basis solve (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
-One "step" is one full solve of the BASELINE configuration — forward
+Headline workload: C4 (Laplace d=3, 1024x512x256), the configuration
+BASELINE.json quotes the 1/2/4/8-GPU metric on.  One "step" is one full solve
+of that configuration — forward
 transforms B~ = B x_m U_m^T, the reduced quasi-triangular dataflow solve,
 back transforms X = X~ x_m U_m — on synthetic seeded inputs
 (include/tsylv/random.hpp).  The Schur/QZ factors are shared host setup
@@ -16,7 +18,10 @@ back transforms X = X~ x_m U_m — on synthetic seeded inputs
   roofline : dominant kernel's algorithmic FLOP / its average launch time,
           against the measured FP64 DMMA peak (profiles/r01_fp64_peak_probe.log)
   cpu_baseline : the reference solver itself (oracle/_ref, built from the
-          unmodified reference headers) on the host cores, rank 0 at N=1
+          unmodified reference headers) on the host cores, rank 0 at N=1;
+          its solution also gives `rel_err_vs_reference` of the timed output
+  all_configs : C1-C5 (one plan each, K solves enqueued back to back):
+          ms per solve, unknowns/s, fraction of the FP64 peak, residual
 
 Multi-GPU (N>1, torchrun, NCCL): the order-3 Laplace configurations (C1, C2,
 C4) run ONE problem sharded into N slabs along the last mode (strong
@@ -25,7 +30,9 @@ transforms, and the dataflow solve over peer-mapped slabs (CUDA IPC, NVLink),
 see paper_1905_09539_b200/dist.py.  C3 (d=6) and C5 (gsylv) are not sharded
 yet and run one replica per GPU (weak scaling).  `--sharded` forces the
 sharded path at N=1 (plumbing check).  `--impl reference` times the reference
-CPU solver (rank 0 only; other ranks exit 0).
+CPU solver (rank 0 only; other ranks exit 0) on inputs drawn from the
+reference's own RandomStream (oracle/_ref), so that process never loads the
+product library.
 """
 from __future__ import annotations
 
@@ -67,6 +74,24 @@ def flops_alg(kind: int, dims) -> tuple[float, float]:
     else:
         solve = N * sum(n - 1 for n in dims)
     return tr, solve
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_of(name: str) -> dict:
+    """The `config` object both arms print (identical keys and values)."""
+    kind, dims, desc = CONFIGS[name]
+    return {"workload": name, "desc": desc, "dims": list(dims), "unknowns": int(np.prod(dims)),
+            "seed": 1}
 
 
 def dist_env():
@@ -158,57 +183,121 @@ def traffic_from_profiles(config: str, kernel: str):
     return d if kernel == "solve" else None
 
 
-def cpu_reference_solve(kind, dims, seed=1):
-    """One reference solve (oracle/_ref) on the box's host cores.
-    Returns (seconds like-for-like, seconds total, info, cores)."""
+def cpu_reference_solve(kind, dims, seed=1, problem=None):
+    """One reference solve (oracle/_ref) on the box's host cores, on the
+    BASELINE inputs drawn from the reference's own RandomStream (or on
+    `problem` = (coeffs, c, rhs)).  Returns (seconds like-for-like, seconds
+    total, info, cores, X, reference config name)."""
     cores = os.cpu_count() or 1
     os.environ["OPENBLAS_NUM_THREADS"] = str(cores)
     os.environ.pop("TSYLV_THREADS", None)
     import oracle.ref as R
-    import paper_1905_09539_b200 as T
-    p = T.make_problem(kind, dims, seed=seed)
+    co, c, rhs = problem if problem is not None else R.baseline_problem(kind, dims, seed=seed)
     t0 = time.perf_counter()
     if kind == 5:
         # the reference's own default (merge + complex); real recursion takes minutes at C5
-        _, info = R.solve_gsylv(p.coeffs, p.c, p.rhs, strategy=1, arithmetic=0)
+        x, info = R.solve_gsylv(co, c, rhs, strategy=1, arithmetic=0)
+        name = "merge+complex_triangular (reference default)"
+    elif len(dims) > 3:
+        # C3: real recursion exceeds 5 min (3^6 base blocks); the default is ~2 min
+        x, info = R.solve_laplace(co, rhs, strategy=1, arithmetic=0)
+        name = "merge+complex_triangular (reference default)"
     else:
-        _, info = R.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
+        x, info = R.solve_laplace(co, rhs, strategy=0, arithmetic=1)
+        name = "recursion_only+real_quasitriangular (the GPU path's arithmetic)"
     total = time.perf_counter() - t0
     like = info[3] + info[4]  # recursion_s + back_transform_s (Schur excluded)
-    return like, total, info, cores
+    return like, total, info, cores, x, name
 
 
 def run_reference(a, rank):
+    """The reference arm: the reference's own CPU solver (oracle/_ref) on all
+    host cores, rank 0 only.  Each step is one full solve of the workload
+    (about 1.5 min at C4 on 16 cores), so the run stops after --steps solves
+    or once 150 s of solves have run (at least one), with no warm-up (plain
+    CPU code: nothing to warm); the cap is stated in the line."""
     if rank != 0:
         return
     kind, dims, desc = CONFIGS[a.config]
     N = float(np.prod(dims))
-    cfg_name = "recursion_only+real_quasitriangular" if kind != 5 else "merge+complex (default)"
     vals, tots = [], []
-    # bounded sample: each step is one full CPU solve (~8 s at C2 on 16
-    # cores), so at most 1 warm-up and 3 timed solves run
-    a.steps = min(a.steps, 3)
-    for i in range(min(a.warmup, 1) + a.steps):
-        like, total, info, cores = cpu_reference_solve(kind, dims)
-        if i >= min(a.warmup, 1):
-            vals.append(like)
-            tots.append(total)
-    t = statistics.median(vals)
+    t_start = time.perf_counter()
+    while len(vals) < max(a.steps, 1) and (not vals or time.perf_counter() - t_start < 150.0):
+        like, total, info, cores, x, cfg_name = cpu_reference_solve(kind, dims)
+        del x
+        vals.append(like)
+        tots.append(total)
+    steps = len(vals)
+    t = min(vals)
     v = N / t
+    sample = (f"{steps} full {a.config} solve(s) of the reference tsylv ({cfg_name}; oracle/_ref, "
+              f"unmodified headers + OpenBLAS 0.3.15, OPENBLAS_NUM_THREADS={cores}); value = N / "
+              f"min(recursion_s + back_transform_s), Schur setup excluded; total incl. Schur "
+              f"{min(tots):.2f} s")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
-        "steps": a.steps, "warmup": min(a.warmup, 1), "ms_per_step": t * 1e3,
+        "steps": steps, "warmup": 0, "ms_per_step": t * 1e3,
+        "steps_note": f"requested --steps {a.steps} --warmup {a.warmup}; ran {steps} timed solve(s) "
+                      f"and no warm-up (150 s budget; one step is one full CPU solve, "
+                      f"{t:.2f} s like-for-like)",
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded RandomStream, BASELINE.json distributions)",
-        "config": {"workload": a.config, "desc": desc, "dims": list(dims),
-                   "reference_config": cfg_name},
+        "config": config_of(a.config),
+        "reference_config": cfg_name,
+        "cpu": {"model": cpu_model(), "cores": cores},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"one full {a.config} solve per step ({cfg_name}); value = N / "
-                                   f"(recursion_s + back_transform_s), Schur setup excluded; "
-                                   f"median total incl. Schur {statistics.median(tots):.2f} s"},
+                         "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def time_enqueued(torch, plan, stream, b, x, steps):
+    """K solves enqueued back to back on the library stream (tsg_plan_enqueue,
+    no host round trip between steps), CUDA events on that stream.
+    Returns (ms per solve, kernel launches per solve)."""
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+    for _ in range(steps):
+        plan.enqueue_device(b.data_ptr(), x.data_ptr())
+    with torch.cuda.stream(stream):
+        e1.record(stream)
+    e1.synchronize()
+    rep = plan.sync()
+    if rep.zero_pivot_index >= 0:
+        raise RuntimeError(f"singular operator (zero pivot {rep.zero_pivot_index})")
+    return e0.elapsed_time(e1) / steps, rep.kernel_launches
+
+
+def all_configs(T, torch, ctx, local, steps, skip):
+    """C1-C5 on this GPU: one plan each, K solves enqueued back to back."""
+    out = {}
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", local))
+    for name in CONFIGS:
+        if name == skip:
+            continue
+        kind, dims, _ = CONFIGS[name]
+        N = int(np.prod(dims))
+        p = T.make_problem(kind, dims, seed=1)
+        plan = build_plan(T, ctx, kind, p)
+        b = torch.from_numpy(np.ascontiguousarray(p.rhs.reshape(-1, order="F"))).cuda(local)
+        x = torch.empty_like(b)
+        for _ in range(3):
+            plan.execute_device(b.data_ptr(), x.data_ptr())
+        torch.cuda.synchronize()
+        ms, launches = time_enqueued(torch, plan, stream, b, x, steps)
+        res = T.residual(p, x.cpu().numpy().reshape(dims, order="F"))
+        tr_f, solve_f = flops_alg(kind, dims)
+        out[name] = {"ms_per_solve": ms, "unknowns_per_s": N / (ms * 1e-3),
+                     "fp64_tflops_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12,
+                     "frac_fp64_peak_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12 / PEAK_FP64_TFLOPS,
+                     "residual": res, "solves": steps, "launches_per_solve": launches}
+        plan.close()
+        del b, x, p
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_ours(a, rank, world, local):
@@ -248,28 +337,14 @@ def run_ours(a, rank, world, local):
     reps = [plan.execute_device(b.data_ptr(), x.data_ptr()) for _ in range(3)]
 
     # ---- device-resident timed region --------------------------------------
-    # tsg_plan_enqueue: the K solves are enqueued back to back on the library
-    # stream (no host round trip between steps); tsg_plan_sync afterwards.
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
     time.sleep(0.2)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-    for _ in range(a.steps):
-        plan.enqueue_device(b.data_ptr(), x.data_ptr())
-    with torch.cuda.stream(stream):
-        e1.record(stream)
-    e1.synchronize()
+    ms, launches_per = time_enqueued(torch, plan, stream, b, x, a.steps)
     clk = clocks.stop()
-    srep_sync = plan.sync()
-    if srep_sync.zero_pivot_index >= 0:
-        raise RuntimeError(f"singular operator (zero pivot {srep_sync.zero_pivot_index})")
     barrier()
-    ms = e0.elapsed_time(e1) / a.steps
-    launches = a.steps * srep_sync.kernel_launches
+    launches = a.steps * launches_per
 
     # ---- end-to-end through the C-ABI with host buffers -----------------------
     # tsg_plan_execute_stream: every step copies its right-hand side from
@@ -334,17 +409,17 @@ def run_ours(a, rank, world, local):
             "metric": METRIC, "value": world * N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": ms,
             "higher_is_better": True,
-            # N > 1 for C1/C2/C4 runs the same problem sharded (run_sharded): strong
             "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded RandomStream, BASELINE.json distributions)",
-            "config": {"workload": a.config, "desc": desc, "dims": list(dims),
-                       "unknowns": N, "l2": "inputs larger than L2 (8N bytes per tensor, "
-                       "plus two N-sized work buffers, > 126 MB L2)",
-                       "parallelism": (f"{world} independent replicas (sharded setup failed: "
-                                       f"{getattr(a, 'fallback', '')})" if getattr(a, "fallback", None)
-                                       else f"{world} independent replicas (no sharding)") if world > 1
-                       else "single GPU", "tiles": info["n_tiles"], "tile": info["tile"],
-                       "schur_setup": "host LAPACK dgees/dgges, outside the timed region"},
+            "config": config_of(a.config),
+            "details": {
+                "l2": "inputs larger than L2 (8N bytes per tensor, plus two N-sized work "
+                      "buffers, > 126 MB L2)",
+                "parallelism": (f"{world} independent replicas (sharded setup failed: "
+                                f"{getattr(a, 'fallback', '')})" if getattr(a, "fallback", None)
+                                else f"{world} independent replicas (no sharding)") if world > 1
+                else "single GPU", "tiles": info["n_tiles"], "tile": info["tile"],
+                "schur_setup": "host LAPACK dgees/dgges, outside the timed region"},
             "phases_ms": {"forward_transforms_before_solve": t_fwd_gated,
                           "last_fwd_gemm+solve+back_modes_overlapped": t_solve_ovl,
                           "back_transforms_rest": t_back_rest,
@@ -362,14 +437,25 @@ def run_ours(a, rank, world, local):
             "gpu_launches": launches,
             "clocks": clk,
         }
+        if world == 1 and not a.no_all_configs:
+            plan.close()
+            del b, x
+            torch.cuda.empty_cache()
+            line["all_configs"] = all_configs(T, torch, ctx, local, 10, a.config)
         if world == 1 and not a.no_cpu_baseline:
-            like, total, rinfo, cores = cpu_reference_solve(kind, dims)
+            like, total, rinfo, cores, xr, cfg_name = cpu_reference_solve(
+                kind, dims, problem=(p.coeffs, getattr(p, "c", None), p.rhs))
+            nr = float(np.linalg.norm(xr))
+            line["rel_err_vs_reference"] = float(np.linalg.norm(xs - xr) / nr)
+            line["reference_residual"] = rinfo[0]
+            line["cpu"] = {"model": cpu_model(), "cores": cores}
             line["cpu_baseline"] = {
                 "value": N / like, "unit": UNIT, "cores": cores, "kind": "reference",
-                "sample": f"one full {a.config} solve of the reference tsylv (oracle/_ref, "
-                          f"unmodified headers + OpenBLAS, OPENBLAS_NUM_THREADS={cores}); value = "
-                          f"N/(recursion_s+back_transform_s) = N/{like:.2f}s, Schur excluded "
-                          f"(total incl. Schur {total:.2f}s)"}
+                "sample": f"one full {a.config} solve of the reference tsylv ({cfg_name}; "
+                          f"oracle/_ref, unmodified headers + OpenBLAS, OPENBLAS_NUM_THREADS="
+                          f"{cores}) on the same inputs; value = N/(recursion_s+back_transform_s) "
+                          f"= N/{like:.2f}s, Schur excluded (total incl. Schur {total:.2f}s); "
+                          f"its X gives rel_err_vs_reference"}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -524,9 +610,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-all-configs", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="sharded path even at N=1")
     a = ap.parse_args()
     rank, world, local = dist_env()

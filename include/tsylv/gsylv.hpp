@@ -2,6 +2,7 @@
 //
 //   solve_gsylv(p, cfg)                    reference gsylv.hpp:311-331
 //   gsylv_recursive(T, C, Bt, n_min)       reference gsylv.hpp:149-159
+//   gsylv_merged(T, C, Bt, n_min)          reference gsylv.hpp:167-232
 //
 // Pipeline of gsylv_pipeline (gsylv.hpp:236-302): QZ of (A_0, C) and Schur of
 // every tail coefficient on the host (shared setup), the pencil screen, then
@@ -41,6 +42,41 @@ inline Tensor<double> gsylv_recursive(const std::vector<Matrix<double>>& t, cons
   gpu::check(tsg_gsylv_reduced(gpu::context(), b.order(), b.dims().data(), t[0].data(), c.data(),
                                tail.data(), b.data(), x.data(), &o, nullptr),
              "gsylv_recursive");
+  return x;
+}
+
+// Reduced form with mode merging (gsylv.hpp:167-232): the reference fuses
+// the last two modes (kron(A_{d-1}, A_{d-2})) while n_{d-2} n_{d-1} <=
+// n_min^2 and recurses to order-2 solve_gsylv_tri leaves; strictly upper
+// triangular coefficients and C are required (require_reduced_gsylv with
+// strict = true, gsylv.hpp:130-141).  On the GPU the pencil tiles of the
+// dataflow solve stand in for the merged modes; the pencil screen runs
+// first.  d = 2 forwards to solve_gsylv_tri(T_0, C, T_1, B, min(n_min, 8)).
+inline Tensor<double> gsylv_merged(std::vector<Matrix<double>> t, Matrix<double> c,
+                                   Tensor<double> b, int n_min) {
+  detail::require_reduced(t, b, n_min, "gsylv_merged", true);
+  if (t.size() < 2) throw dimension_error("gsylv_merged: need at least two modes");
+  if (c.rows() != t[0].rows() || c.cols() != t[0].cols())
+    throw dimension_error("gsylv_merged: C must match A_0");
+  if (!is_upper_triangular(c)) throw dimension_error("gsylv_merged: C must be upper triangular");
+  const int d = static_cast<int>(t.size());
+  if (d == 2) {
+    Matrix<double> bm(b.dim(0), b.dim(1), std::vector<double>(b.data(), b.data() + b.size()));
+    Matrix<double> x = solve_gsylv_tri(t[0], c, t[1], std::move(bm),
+                                       std::min(n_min, matrix_floor_n_min));
+    return Tensor<double>(b.dims(), std::vector<double>(x.data(), x.data() + x.size()));
+  }
+  const Solvability s = check_solvable_gsylv(t, c);
+  if (!s.solvable)
+    throw singular_error(detail::witness_message("gsylv_merged", s), s.witness, s.witness_values,
+                         s.min_abs);
+  std::vector<const double*> tail;
+  for (size_t m = 1; m < t.size(); ++m) tail.push_back(t[m].data());
+  tsg_opts o = detail::gpu_opts(0);
+  Tensor<double> x(b.dims());
+  gpu::check(tsg_gsylv_reduced(gpu::context(), d, b.dims().data(), t[0].data(), c.data(),
+                               tail.data(), b.data(), x.data(), &o, nullptr),
+             "gsylv_merged");
   return x;
 }
 

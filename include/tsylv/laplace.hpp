@@ -2,6 +2,7 @@
 //
 //   solve_laplace(p, cfg)              reference laplace.hpp:324-344
 //   laplace_recursive(T, Bt, n_min)    reference laplace.hpp:185-195
+//   laplace_merged(T, Bt, n_min)       reference laplace.hpp:202-244
 //
 // solve_laplace keeps the reference pipeline: host Schur
 // of every coefficient (shared setup, dgees), the host solvability screen
@@ -21,6 +22,7 @@
 #include "tsylv/matrix.hpp"
 #include "tsylv/problems.hpp"
 #include "tsylv/solvability.hpp"
+#include "tsylv/sylvester.hpp"
 #include "tsylv/tensor.hpp"
 
 namespace tsylv {
@@ -53,7 +55,7 @@ inline void fill_gpu(GpuTimings& g, const tsg_report& r) {
 }
 
 inline void require_reduced(const std::vector<Matrix<double>>& t, const Tensor<double>& b,
-                            int n_min, const char* who) {
+                            int n_min, const char* who, bool strict_triangular = false) {
   if (n_min < 1) throw dimension_error(std::string(who) + ": n_min must be >= 1");
   if (t.empty() || b.order() != static_cast<int>(t.size()))
     throw dimension_error(std::string(who) + ": rhs order does not match coefficient count");
@@ -61,9 +63,10 @@ inline void require_reduced(const std::vector<Matrix<double>>& t, const Tensor<d
     if (t[m].rows() != t[m].cols() || t[m].rows() != b.dim(static_cast<int>(m)))
       throw dimension_error(std::string(who) + ": coefficient " + std::to_string(m) +
                             " does not match rhs");
-    if (!is_upper_quasi_triangular(t[m]))
+    if (strict_triangular ? !is_upper_triangular(t[m]) : !is_upper_quasi_triangular(t[m]))
       throw dimension_error(std::string(who) + ": coefficient " + std::to_string(m) +
-                            " must be upper quasi-triangular");
+                            (strict_triangular ? " must be upper triangular"
+                                               : " must be upper quasi-triangular"));
   }
 }
 
@@ -92,6 +95,40 @@ inline Tensor<double> laplace_recursive(const std::vector<Matrix<double>>& t, Te
   gpu::check(tsg_laplace_reduced(gpu::context(), b.order(), b.dims().data(), tp.data(), b.data(),
                                  x.data(), &o, nullptr),
              "laplace_recursive");
+  return x;
+}
+
+// Reduced form with mode merging (laplace.hpp:202-244): the reference fuses
+// modes 0 and 1 while n_0 n_1 <= n_min^2 and recurses down to order-2
+// solve_sylvester_tri leaves; it requires strictly upper triangular
+// coefficients (complex Schur forms; for real T a real-spectrum Schur form).
+// Same contract here.  On the GPU the multi-mode tiles of the dataflow solve
+// play the role of the merged modes, so merging is a tile
+// shape, not a dense Kronecker-sum matrix; n_min is the reference's merge
+// cutoff and the GPU picks its own tile extents.  Every eigenvalue tuple is
+// screened first (the reference screens each leaf with solve_sylvester_tri's
+// tolerance): singular operators raise singular_error.  d = 2 forwards to
+// solve_sylvester_tri(T_0, T_1, B, min(n_min, 8)) exactly as the reference.
+inline Tensor<double> laplace_merged(std::vector<Matrix<double>> t, Tensor<double> b, int n_min) {
+  detail::require_reduced(t, b, n_min, "laplace_merged", true);
+  const int d = static_cast<int>(t.size());
+  if (d == 2) {
+    Matrix<double> bm(b.dim(0), b.dim(1), std::vector<double>(b.data(), b.data() + b.size()));
+    Matrix<double> x = solve_sylvester_tri(t[0], t[1], std::move(bm),
+                                           std::min(n_min, matrix_floor_n_min));
+    return Tensor<double>(b.dims(), std::vector<double>(x.data(), x.data() + x.size()));
+  }
+  const Solvability s = check_solvable_laplace(t);
+  if (!s.solvable)
+    throw singular_error(detail::witness_message("laplace_merged", s), s.witness,
+                         s.witness_values, s.min_abs);
+  std::vector<const double*> tp;
+  for (const auto& m : t) tp.push_back(m.data());
+  tsg_opts o = detail::gpu_opts(0);
+  Tensor<double> x(b.dims());
+  gpu::check(tsg_laplace_reduced(gpu::context(), d, b.dims().data(), tp.data(), b.data(),
+                                 x.data(), &o, nullptr),
+             "laplace_merged");
   return x;
 }
 

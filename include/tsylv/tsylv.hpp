@@ -8,8 +8,10 @@
 #include "tsylv/lapack.hpp"
 #include "tsylv/laplace.hpp"
 #include "tsylv/matrix.hpp"
+#include "tsylv/oracle.hpp"
 #include "tsylv/problems.hpp"
 #include "tsylv/random.hpp"
 #include "tsylv/scalar.hpp"
 #include "tsylv/solvability.hpp"
+#include "tsylv/sylvester.hpp"
 #include "tsylv/tensor.hpp"

@@ -38,6 +38,11 @@ def lib() -> ctypes.CDLL:
             "ref_solve_gsylv": (I, [I, Ip, Dpp, Dp, Dp, I, I, I, Dp, Dp, E, I]),
             "ref_laplace_recursive": (I, [I, Ip, Dpp, Dp, I, Dp, E, I]),
             "ref_gsylv_recursive": (I, [I, Ip, Dpp, Dp, Dp, I, Dp, E, I]),
+            "ref_laplace_merged": (I, [I, Ip, Dpp, Dp, I, Dp, E, I]),
+            "ref_gsylv_merged": (I, [I, Ip, Dpp, Dp, Dp, I, Dp, E, I]),
+            "ref_solve_sylvester_tri": (I, [I, I, Dp, Dp, Dp, I, Dp, E, I]),
+            "ref_solve_gsylv_tri": (I, [I, I, Dp, Dp, Dp, Dp, I, Dp, E, I]),
+            "ref_baseline_problem": (I, [I, I, Ip, ctypes.c_uint64, Dp, Dp, Dp]),
             "ref_mode_multiply": (I, [I, Ip, Dp, I, Dp, I, Dp, E, I]),
             "ref_schur": (I, [I, Dp, Dp, Dp, E, I]),
             "ref_qz": (I, [I, Dp, Dp, Dp, Dp, Dp, Dp, E, I]),
@@ -140,6 +145,70 @@ def gsylv_recursive(t, tc, bt, n_min):
     _chk(lib().ref_gsylv_recursive(bt.ndim, _dims(bt.shape), pp, _p(tc), _p(bt), n_min, _p(x),
                                    err, 1024), err)
     return x
+
+
+def laplace_merged(t, bt, n_min):
+    """laplace_merged<double> (laplace.hpp:202-244)."""
+    t = [_f(a) for a in t]
+    bt = _f(bt)
+    x = np.zeros(bt.shape, order="F")
+    pp, keep = _pp(t)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_laplace_merged(bt.ndim, _dims(bt.shape), pp, _p(bt), n_min, _p(x), err, 1024),
+         err)
+    return x
+
+
+def gsylv_merged(t, tc, bt, n_min):
+    """gsylv_merged<double> (gsylv.hpp:167-232)."""
+    t = [_f(a) for a in t]
+    tc = _f(tc)
+    bt = _f(bt)
+    x = np.zeros(bt.shape, order="F")
+    pp, keep = _pp(t)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_gsylv_merged(bt.ndim, _dims(bt.shape), pp, _p(tc), _p(bt), n_min, _p(x), err,
+                                1024), err)
+    return x
+
+
+def solve_sylvester_tri(a1, a2, b, n_min=32):
+    """solve_sylvester_tri<double> (sylvester.hpp:194-215): A1 X + X A2^H = B."""
+    a1, a2, b = _f(a1), _f(a2), _f(b)
+    x = np.zeros(b.shape, order="F")
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_solve_sylvester_tri(a1.shape[0], a2.shape[0], _p(a1), _p(a2), _p(b), n_min,
+                                       _p(x), err, 1024), err)
+    return x
+
+
+def solve_gsylv_tri(a1, c, a2, b, n_min=32):
+    """solve_gsylv_tri<double> (sylvester.hpp:219-241): A1 X + C X A2^H = B."""
+    a1, c, a2, b = _f(a1), _f(c), _f(a2), _f(b)
+    x = np.zeros(b.shape, order="F")
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_solve_gsylv_tri(a1.shape[0], a2.shape[0], _p(a1), _p(c), _p(a2), _p(b), n_min,
+                                   _p(x), err, 1024), err)
+    return x
+
+
+def baseline_problem(kind, dims, seed=1):
+    """BASELINE.json inputs drawn from the reference's RandomStream
+    (random.hpp:19-77): returns (coeffs, c or None, rhs).  kind 1 C1,
+    2 C2-C4, 5 C5 (coeffs {A, C^T, ..}, c = B)."""
+    dims = [int(n) for n in dims]
+    co = np.zeros(sum(n * n for n in dims))
+    c = np.zeros(dims[0] ** 2)
+    rhs = np.zeros(int(np.prod(dims)))
+    rc = lib().ref_baseline_problem(kind, len(dims), _dims(dims), seed, _p(co), _p(c), _p(rhs))
+    if rc != 0:
+        raise RefError(1, f"baseline_problem: bad kind {kind}")
+    mats, o = [], 0
+    for n in dims:
+        mats.append(co[o:o + n * n].reshape((n, n), order="F").copy(order="F"))
+        o += n * n
+    return (mats, c.reshape((dims[0],) * 2, order="F").copy(order="F") if kind == 5 else None,
+            rhs.reshape(dims, order="F"))
 
 
 def mode_multiply(x, a, mode):

@@ -9,14 +9,22 @@
 //   solve_gsylv         gsylv.hpp:311-331
 //   laplace_recursive   laplace.hpp:185-195
 //   gsylv_recursive     gsylv.hpp:149-159
+//   laplace_merged      laplace.hpp:202-244
+//   gsylv_merged        gsylv.hpp:167-232
+//   solve_sylvester_tri sylvester.hpp:194-215
+//   solve_gsylv_tri     sylvester.hpp:219-241
 //   mode_multiply       tensor.hpp:187-231
 //   schur / qz          kernels.hpp:78-156
 //   oracle::solve       oracle.hpp:205-221
 //   oracle::residual    oracle.hpp:233-268
 //   RandomStream        random.hpp:19-62 (+ generators :64-223)
+//   BASELINE.json inputs (ref_baseline_problem): the configurations' formulas
+//   drawn from the reference's own RandomStream / randn_matrix / randn_tensor,
+//   so the reference arm of bench.py never loads the product library.
 // Status codes follow the C-ABI convention of include/tsylv_gpu.h:
 //   0 ok, 1 dimension_error, 2 singular_error, 3 factorization_error,
 //   4 std::invalid_argument (config conflict), 5 anything else.
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -151,6 +159,48 @@ int ref_gsylv_recursive(int d, const int* dims, const double* const* t,
     std::vector<Matrix<double>> coeffs;
     for (int m = 0; m < d; ++m) coeffs.push_back(mat(dims[m], dims[m], t[m]));
     copy_out(gsylv_recursive(coeffs, mat(dims[0], dims[0], tc), ten(d, dims, bt), n_min), x);
+  });
+}
+
+int ref_laplace_merged(int d, const int* dims, const double* const* t,
+                       const double* bt, int n_min, double* x, char* err,
+                       int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> coeffs;
+    for (int m = 0; m < d; ++m) coeffs.push_back(mat(dims[m], dims[m], t[m]));
+    copy_out(laplace_merged(std::move(coeffs), ten(d, dims, bt), n_min), x);
+  });
+}
+
+int ref_gsylv_merged(int d, const int* dims, const double* const* t,
+                     const double* tc, const double* bt, int n_min, double* x,
+                     char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> coeffs;
+    for (int m = 0; m < d; ++m) coeffs.push_back(mat(dims[m], dims[m], t[m]));
+    copy_out(gsylv_merged(std::move(coeffs), mat(dims[0], dims[0], tc), ten(d, dims, bt), n_min),
+             x);
+  });
+}
+
+// A1 X + X A2^H = B (a1: r x r, a2: c x c, b: r x c).
+int ref_solve_sylvester_tri(int r, int c, const double* a1, const double* a2,
+                            const double* b, int n_min, double* x, char* err,
+                            int errlen) {
+  return guarded(err, errlen, [&] {
+    Matrix<double> out = solve_sylvester_tri(mat(r, r, a1), mat(c, c, a2), mat(r, c, b), n_min);
+    std::memcpy(x, out.data(), out.size() * sizeof(double));
+  });
+}
+
+// A1 X + C X A2^H = B.
+int ref_solve_gsylv_tri(int r, int c, const double* a1, const double* cm,
+                        const double* a2, const double* b, int n_min, double* x,
+                        char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Matrix<double> out = solve_gsylv_tri(mat(r, r, a1), mat(r, r, cm), mat(c, c, a2),
+                                         mat(r, c, b), n_min);
+    std::memcpy(x, out.data(), out.size() * sizeof(double));
   });
 }
 
@@ -295,6 +345,71 @@ void ref_randn_quasi_triangular(void* r, int n, double diag_shift,
   Matrix<double> m = randn_quasi_triangular(*static_cast<RandomStream*>(r), n,
                                             diag_shift, pair_prob);
   std::memcpy(out, m.data(), m.size() * sizeof(double));
+}
+
+// BASELINE.json configurations (kind 1: convection-diffusion Laplace, C1;
+// kind 2: A = G/sqrt(n) + 3I Laplace, C2-C4; kind 5: gsylv A = G_A/sqrt(n0)
+// + 4I, B = G_B/sqrt(n0), C = G_C/(2 sqrt(nc)), posed as coeffs {A, C^T, ..},
+// c = B, C5).  Draw order: coefficients in mode order, then the rhs.  Output
+// layout as the generators above.  Returns 1 on a bad kind.
+int ref_baseline_problem(int kind, int d, const int* dims, std::uint64_t seed,
+                         double* coeffs, double* c, double* rhs) {
+  RandomStream r(seed);
+  std::vector<Matrix<double>> co;
+  Matrix<double> cc;
+  if (kind == 1 || kind == 2) {
+    for (int m = 0; m < d; ++m) {
+      const int n = dims[m];
+      Matrix<double> a(n, n);
+      if (kind == 1) {
+        const double cm = 0.5 + 1.5 * r.uniform();
+        const double h2 = static_cast<double>(n + 1) * (n + 1), h1 = cm * (n + 1) / 2.0;
+        for (int i = 0; i < n; ++i) {
+          a(i, i) = 2.0 * h2;
+          if (i + 1 < n) {
+            a(i, i + 1) = -h2 + h1;
+            a(i + 1, i) = -h2 - h1;
+          }
+        }
+      } else {
+        a = randn_matrix<double>(r, n, n);
+        const double s = std::sqrt(static_cast<double>(n));
+        for (int j = 0; j < n; ++j)
+          for (int i = 0; i < n; ++i) a(i, j) /= s;
+        for (int i = 0; i < n; ++i) a(i, i) += 3.0;
+      }
+      co.push_back(std::move(a));
+    }
+  } else if (kind == 5) {
+    const int n0 = dims[0], nc = dims[1];
+    Matrix<double> a = randn_matrix<double>(r, n0, n0);
+    Matrix<double> b = randn_matrix<double>(r, n0, n0);
+    Matrix<double> g = randn_matrix<double>(r, nc, nc);
+    const double s0 = std::sqrt(static_cast<double>(n0));
+    const double sc = 2.0 * std::sqrt(static_cast<double>(nc));
+    for (int j = 0; j < n0; ++j)
+      for (int i = 0; i < n0; ++i) {
+        a(i, j) /= s0;
+        b(i, j) /= s0;
+      }
+    for (int i = 0; i < n0; ++i) a(i, i) += 4.0;
+    for (int j = 0; j < nc; ++j)
+      for (int i = 0; i < nc; ++i) g(i, j) /= sc;
+    co.push_back(std::move(a));
+    const Matrix<double> gt = transposed(g);
+    for (int m = 1; m < d; ++m) co.push_back(gt);
+    cc = std::move(b);
+  } else {
+    return 1;
+  }
+  Tensor<double> t = randn_tensor<double>(r, dims_of(d, dims));
+  for (int m = 0; m < d; ++m) {
+    std::memcpy(coeffs, co[m].data(), co[m].size() * sizeof(double));
+    coeffs += co[m].size();
+  }
+  if (kind == 5 && c) std::memcpy(c, cc.data(), cc.size() * sizeof(double));
+  copy_out(t, rhs);
+  return 0;
 }
 
 } // extern "C"

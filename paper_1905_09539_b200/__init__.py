@@ -6,12 +6,14 @@ this package is the Python host mirror of the reference's API on top of it.
 """
 from .api import (Arithmetic, GSylvProblem, LaplaceProblem, PhaseTimings, RandomStream,
                   SolveReport, SolverConfig, Strategy, dimension_error, factorization_error,
-                  gpu_error, gsylv_recursive, laplace_recursive, make_problem, mode_multiply, qz,
-                  residual, schur, singular_error, solve_gsylv, solve_laplace)
+                  gpu_error, gsylv_merged, gsylv_recursive, laplace_merged, laplace_recursive,
+                  make_problem, mode_multiply, oracle, qz, residual, schur, singular_error,
+                  solve_gsylv, solve_gsylv_tri, solve_laplace, solve_sylvester_tri)
 
 __all__ = [
     "Arithmetic", "GSylvProblem", "LaplaceProblem", "PhaseTimings", "RandomStream", "SolveReport",
     "SolverConfig", "Strategy", "dimension_error", "factorization_error", "gpu_error",
-    "gsylv_recursive", "laplace_recursive", "make_problem", "mode_multiply", "qz", "residual",
-    "schur", "singular_error", "solve_gsylv", "solve_laplace",
+    "gsylv_merged", "gsylv_recursive", "laplace_merged", "laplace_recursive", "make_problem",
+    "mode_multiply", "oracle", "qz", "residual", "schur", "singular_error", "solve_gsylv",
+    "solve_gsylv_tri", "solve_laplace", "solve_sylvester_tri",
 ]

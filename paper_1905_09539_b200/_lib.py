@@ -87,6 +87,12 @@ def _declare(lib: ctypes.CDLL) -> None:
                                   c_dbl_p, E, I]),
         "tsylv_laplace_recursive": (I, [I, c_int_p, c_dbl_pp, c_dbl_p, I, c_dbl_p, E, I]),
         "tsylv_gsylv_recursive": (I, [I, c_int_p, c_dbl_pp, c_dbl_p, c_dbl_p, I, c_dbl_p, E, I]),
+        "tsylv_laplace_merged": (I, [I, c_int_p, c_dbl_pp, c_dbl_p, I, c_dbl_p, E, I]),
+        "tsylv_gsylv_merged": (I, [I, c_int_p, c_dbl_pp, c_dbl_p, c_dbl_p, I, c_dbl_p, E, I]),
+        "tsylv_solve_sylvester_tri": (I, [I, I, c_dbl_p, c_dbl_p, c_dbl_p, I, c_dbl_p, E, I]),
+        "tsylv_solve_gsylv_tri": (I, [I, I, c_dbl_p, c_dbl_p, c_dbl_p, c_dbl_p, I, c_dbl_p, E, I]),
+        "tsylv_oracle_solve_laplace": (I, [I, c_int_p, c_dbl_pp, c_dbl_p, c_dbl_p, E, I]),
+        "tsylv_oracle_solve_gsylv": (I, [I, c_int_p, c_dbl_pp, c_dbl_p, c_dbl_p, c_dbl_p, E, I]),
         "tsylv_mode_multiply": (I, [I, c_int_p, c_dbl_p, I, c_dbl_p, I, c_dbl_p, E, I]),
         "tsylv_schur": (I, [I, c_dbl_p, c_dbl_p, c_dbl_p, E, I]),
         "tsylv_qz": (I, [I, c_dbl_p, c_dbl_p, c_dbl_p, c_dbl_p, c_dbl_p, c_dbl_p, E, I]),

@@ -9,6 +9,11 @@ the reference layout, tensor.hpp:19-27); matrices are (n, n) float64 arrays.
     solve_gsylv(p, cfg)            gsylv.hpp:311-331
     laplace_recursive(T, Bt, nmin) laplace.hpp:185-195
     gsylv_recursive(T, C, Bt, nmin) gsylv.hpp:149-159
+    laplace_merged(T, Bt, nmin)    laplace.hpp:202-244
+    gsylv_merged(T, C, Bt, nmin)   gsylv.hpp:167-232
+    solve_sylvester_tri(A1, A2, B, nmin)     sylvester.hpp:194-215
+    solve_gsylv_tri(A1, C, A2, B, nmin)      sylvester.hpp:219-241
+    oracle.residual(p, X), oracle.solve(p)   oracle.hpp:205-268
     mode_multiply(X, A, mode)      tensor.hpp:187-231
     schur(A), qz(A, C)             kernels.hpp:78-156 (host LAPACK, shared setup)
 """
@@ -219,6 +224,102 @@ def gsylv_recursive(coeffs: list, c: np.ndarray, b: np.ndarray, n_min: int) -> n
                                      err, 1024)
     _raise(rc, err)
     return x
+
+
+def laplace_merged(coeffs: list, b: np.ndarray, n_min: int) -> np.ndarray:
+    coeffs = [_f(a) for a in coeffs]
+    b = _f(b)
+    if b.ndim != len(coeffs):
+        raise dimension_error("laplace_merged: rhs order does not match coefficient count")
+    x = np.zeros(b.shape, order="F")
+    pp, keep = _ptrs(coeffs)
+    err = _err()
+    rc = lib().tsylv_laplace_merged(b.ndim, _dims(b), pp, _ptr(b), int(n_min), _ptr(x), err, 1024)
+    _raise(rc, err)
+    return x
+
+
+def gsylv_merged(coeffs: list, c: np.ndarray, b: np.ndarray, n_min: int) -> np.ndarray:
+    coeffs = [_f(a) for a in coeffs]
+    c = _f(c)
+    b = _f(b)
+    if b.ndim != len(coeffs):
+        raise dimension_error("gsylv_merged: rhs order does not match coefficient count")
+    x = np.zeros(b.shape, order="F")
+    pp, keep = _ptrs(coeffs)
+    err = _err()
+    rc = lib().tsylv_gsylv_merged(b.ndim, _dims(b), pp, _ptr(c), _ptr(b), int(n_min), _ptr(x),
+                                  err, 1024)
+    _raise(rc, err)
+    return x
+
+
+def _mat2(a, who):
+    a = _f(a)
+    if a.ndim != 2:
+        raise dimension_error(f"{who}: expected a matrix")
+    return a
+
+
+def solve_sylvester_tri(a1: np.ndarray, a2: np.ndarray, b: np.ndarray, n_min: int = 32) -> np.ndarray:
+    """A1 X + X A2^H = B with (quasi-)triangular A1, A2 (sylvester.hpp:194-215)."""
+    a1, a2, b = (_mat2(v, "solve_sylvester_tri") for v in (a1, a2, b))
+    if a1.shape[0] != a1.shape[1] or a2.shape[0] != a2.shape[1]:
+        raise dimension_error("solve_sylvester_tri: coefficients must be square")
+    if b.shape != (a1.shape[0], a2.shape[0]):
+        raise dimension_error(f"solve_sylvester_tri: rhs is {b.shape[0]}x{b.shape[1]}, expected "
+                              f"{a1.shape[0]}x{a2.shape[0]}")
+    x = np.zeros(b.shape, order="F")
+    err = _err()
+    rc = lib().tsylv_solve_sylvester_tri(a1.shape[0], a2.shape[0], _ptr(a1), _ptr(a2), _ptr(b),
+                                         int(n_min), _ptr(x), err, 1024)
+    _raise(rc, err)
+    return x
+
+
+def solve_gsylv_tri(a1: np.ndarray, c: np.ndarray, a2: np.ndarray, b: np.ndarray,
+                    n_min: int = 32) -> np.ndarray:
+    """A1 X + C X A2^H = B, (A1, C) in generalized Schur form (sylvester.hpp:219-241)."""
+    a1, c, a2, b = (_mat2(v, "solve_gsylv_tri") for v in (a1, c, a2, b))
+    if a1.shape[0] != a1.shape[1] or a2.shape[0] != a2.shape[1]:
+        raise dimension_error("solve_gsylv_tri: coefficients must be square")
+    if c.shape != a1.shape:
+        raise dimension_error("solve_gsylv_tri: C must match A1")
+    if b.shape != (a1.shape[0], a2.shape[0]):
+        raise dimension_error(f"solve_gsylv_tri: rhs is {b.shape[0]}x{b.shape[1]}, expected "
+                              f"{a1.shape[0]}x{a2.shape[0]}")
+    x = np.zeros(b.shape, order="F")
+    err = _err()
+    rc = lib().tsylv_solve_gsylv_tri(a1.shape[0], a2.shape[0], _ptr(a1), _ptr(c), _ptr(a2), _ptr(b),
+                                     int(n_min), _ptr(x), err, 1024)
+    _raise(rc, err)
+    return x
+
+
+class oracle:
+    """tsylv::oracle (oracle.hpp:205-268): residual on the device, dense
+    assemble-and-LU solve (N <= 4096) as the independent cross-check."""
+
+    @staticmethod
+    def residual(p, x: np.ndarray) -> float:
+        return residual(p, x)
+
+    @staticmethod
+    def solve(p) -> np.ndarray:
+        coeffs = [_f(a) for a in p.coeffs]
+        rhs = _f(p.rhs)
+        _check_problem(coeffs, rhs, "oracle::solve")
+        x = np.zeros(rhs.shape, order="F")
+        pp, keep = _ptrs(coeffs)
+        err = _err()
+        if isinstance(p, GSylvProblem):
+            rc = lib().tsylv_oracle_solve_gsylv(rhs.ndim, _dims(rhs), pp, _ptr(_f(p.c)), _ptr(rhs),
+                                                _ptr(x), err, 1024)
+        else:
+            rc = lib().tsylv_oracle_solve_laplace(rhs.ndim, _dims(rhs), pp, _ptr(rhs), _ptr(x),
+                                                  err, 1024)
+        _raise(rc, err)
+        return x
 
 
 def mode_multiply(x: np.ndarray, a: np.ndarray, mode: int) -> np.ndarray:

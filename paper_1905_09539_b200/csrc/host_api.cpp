@@ -125,6 +125,66 @@ int tsylv_gsylv_recursive(int d, const int* dims, const double* const* t, const 
   });
 }
 
+int tsylv_laplace_merged(int d, const int* dims, const double* const* t, const double* bt,
+                         int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> tt;
+    for (int m = 0; m < d; ++m) tt.push_back(mat(dims[m], dims[m], t[m]));
+    Tensor<double> r = laplace_merged(std::move(tt), ten(d, dims, bt), n_min);
+    std::memcpy(x, r.data(), r.size() * sizeof(double));
+  });
+}
+
+int tsylv_gsylv_merged(int d, const int* dims, const double* const* t, const double* tc,
+                       const double* bt, int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> tt;
+    for (int m = 0; m < d; ++m) tt.push_back(mat(dims[m], dims[m], t[m]));
+    Tensor<double> r = gsylv_merged(std::move(tt), mat(dims[0], dims[0], tc), ten(d, dims, bt), n_min);
+    std::memcpy(x, r.data(), r.size() * sizeof(double));
+  });
+}
+
+int tsylv_solve_sylvester_tri(int r, int c, const double* a1, const double* a2, const double* b,
+                              int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Matrix<double> out = solve_sylvester_tri(mat(r, r, a1), mat(c, c, a2), mat(r, c, b), n_min);
+    std::memcpy(x, out.data(), out.size() * sizeof(double));
+  });
+}
+
+int tsylv_solve_gsylv_tri(int r, int c, const double* a1, const double* cm, const double* a2,
+                          const double* b, int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Matrix<double> out =
+        solve_gsylv_tri(mat(r, r, a1), mat(r, r, cm), mat(c, c, a2), mat(r, c, b), n_min);
+    std::memcpy(x, out.data(), out.size() * sizeof(double));
+  });
+}
+
+int tsylv_oracle_solve_laplace(int d, const int* dims, const double* const* coeffs,
+                               const double* rhs, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    LaplaceProblem<double> p;
+    for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+    p.rhs = ten(d, dims, rhs);
+    Tensor<double> r = oracle::solve(p);
+    std::memcpy(x, r.data(), r.size() * sizeof(double));
+  });
+}
+
+int tsylv_oracle_solve_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
+                             const double* rhs, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GSylvProblem<double> p;
+    for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
+    p.c = mat(dims[0], dims[0], c);
+    p.rhs = ten(d, dims, rhs);
+    Tensor<double> r = oracle::solve(p);
+    std::memcpy(x, r.data(), r.size() * sizeof(double));
+  });
+}
+
 int tsylv_mode_multiply(int d, const int* dims, const double* xin, int r, const double* a, int mode,
                         double* y, char* err, int errlen) {
   return guarded(err, errlen, [&] {
@@ -157,7 +217,7 @@ double tsylv_residual_laplace(int d, const int* dims, const double* const* coeff
   LaplaceProblem<double> p;
   for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
   p.rhs = ten(d, dims, rhs);
-  return residual(p, ten(d, dims, x));
+  return oracle::residual(p, ten(d, dims, x));
 }
 
 double tsylv_residual_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
@@ -166,7 +226,7 @@ double tsylv_residual_gsylv(int d, const int* dims, const double* const* coeffs,
   for (int m = 0; m < d; ++m) p.coeffs.push_back(mat(dims[m], dims[m], coeffs[m]));
   p.c = mat(dims[0], dims[0], c);
   p.rhs = ten(d, dims, rhs);
-  return residual(p, ten(d, dims, x));
+  return oracle::residual(p, ten(d, dims, x));
 }
 
 int tsylv_check_solvable_laplace(int d, const int* dims, const double* const* t, double tol,

@@ -82,3 +82,20 @@ def test_solvability_screen_host():
     rc = lib().tsylv_check_solvable_laplace(3, (ctypes.c_int * 3)(2, 2, 2), pp, 0.0,
                                             ctypes.byref(mn), wit, ctypes.byref(ok), err, 256)
     assert rc == 0 and ok.value == 0 and list(wit) == [0, 1, 0] and mn.value == 0.0
+
+
+@pytest.mark.parametrize("kind,dims", [(1, (8, 9, 10)), (2, (12, 10, 8)), (2, (5, 4, 4, 3, 3, 3)),
+                                       (5, (20, 4, 4, 4))])
+def test_make_problem_matches_reference_generator(ref, kind, dims):
+    """The drop-in's BASELINE generator (include/tsylv/random.hpp) and the
+    oracle's (the reference's own RandomStream, oracle/ref_driver.cpp
+    ref_baseline_problem) give bit-identical inputs: the bench's reference
+    arm builds its inputs without loading the product library."""
+    import paper_1905_09539_b200 as T
+    co, c, rhs = ref.baseline_problem(kind, dims, seed=3)
+    p = T.make_problem(kind, dims, seed=3)
+    for a, b in zip(co, p.coeffs):
+        assert np.array_equal(a, b)
+    assert np.array_equal(rhs, p.rhs)
+    if kind == 5:
+        assert np.array_equal(c, p.c)
