@@ -99,3 +99,19 @@ def test_make_problem_matches_reference_generator(ref, kind, dims):
     assert np.array_equal(rhs, p.rhs)
     if kind == 5:
         assert np.array_equal(c, p.c)
+
+
+def test_oracle_dense_solve_host(ref):
+    """tsylv::oracle::solve (dense assemble + LU, host only) against the
+    reference's oracle::solve on the same problem, and its size cap."""
+    import paper_1905_09539_b200 as T
+    co, rhs = ref.RandomStream(31).laplace_problem([5, 4, 3])
+    assert rel_diff(T.oracle.solve(T.LaplaceProblem(co, rhs)), ref.dense_solve_laplace(co, rhs)) < 1e-12
+    co, c, rhs = ref.RandomStream(32).gsylv_problem([6, 3, 3])
+    assert rel_diff(T.oracle.solve(T.GSylvProblem(co, c, rhs)),
+                    ref.dense_solve_gsylv(co, c, rhs)) < 1e-12
+    with pytest.raises(T.dimension_error):
+        T.oracle.solve(T.LaplaceProblem([np.eye(17)] * 3, np.zeros((17, 17, 17), order="F")))
+    with pytest.raises(T.singular_error):
+        T.oracle.solve(T.LaplaceProblem([np.diag([1.0, 2.0]), np.diag([-1.0, 3.0])],
+                                        np.ones((2, 2), order="F")))
