@@ -290,7 +290,7 @@ def all_configs(T, torch, ctx, local, steps, skip):
         ms, launches = time_enqueued(torch, plan, stream, b, x, steps)
         res = T.residual(p, x.cpu().numpy().reshape(dims, order="F"))
         tr_f, solve_f = flops_alg(kind, dims)
-        out[name] = {"ms_per_solve": ms, "unknowns_per_s": N / (ms * 1e-3),
+        out[name] = {"ms_per_solve": ms, "reduced_solve": plan.describe(), "unknowns_per_s": N / (ms * 1e-3),
                      "fp64_tflops_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12,
                      "frac_fp64_peak_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12 / PEAK_FP64_TFLOPS,
                      "residual": res, "solves": steps, "launches_per_solve": launches}
@@ -419,6 +419,7 @@ def run_ours(a, rank, world, local):
                                 f"{getattr(a, 'fallback', '')})" if getattr(a, "fallback", None)
                                 else f"{world} independent replicas (no sharding)") if world > 1
                 else "single GPU", "tiles": info["n_tiles"], "tile": info["tile"],
+                "reduced_solve": plan.describe(),
                 "schur_setup": "host LAPACK dgees/dgges, outside the timed region"},
             "phases_ms": {"forward_transforms_before_solve": t_fwd_gated,
                           "last_fwd_gemm+solve+back_modes_overlapped": t_solve_ovl,

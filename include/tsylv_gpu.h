@@ -131,6 +131,11 @@ int tsg_plan_execute_stream(tsg_plan* plan, int nrhs, const double* const* B, do
 int tsg_plan_info(const tsg_plan* plan, int64_t* n_tiles, int* tile_extents,
                   double* flops_alg);
 
+/* Which reduced-solve kernel the plan runs, as a short text
+ * ("decoupled f=<mode> kappa=<prod>", "lap16", "lap3", "lapd", "gsyd",
+ * "generic"); returns the string length (truncated to len - 1). */
+int tsg_plan_describe(const tsg_plan* plan, char* buf, int len);
+
 /* ---- Mode product Y = X x_mode A  (tensor.hpp:187-231) -----------------
  * A is r x dims[mode] column-major; Y has dims with dims[mode] -> r. */
 int tsg_mode_multiply(tsg_ctx* ctx, int d, const int* dims, const double* X,

@@ -38,7 +38,7 @@ TSG_SYMBOLS = [
     "tsg_laplace_solve",
     "tsg_laplace_reduced", "tsg_gsylv_solve", "tsg_gsylv_reduced", "tsg_plan_create",
     "tsg_plan_execute", "tsg_plan_execute_stream", "tsg_plan_destroy", "tsg_plan_info",
-    "tsg_plan_enqueue", "tsg_plan_sync",
+    "tsg_plan_enqueue", "tsg_plan_sync", "tsg_plan_describe",
     "tsg_mode_multiply",
     "tsg_residual", "tsg_abi_version",
     "tsg_slab_bounds", "tsg_dplan_create", "tsg_dplan_destroy", "tsg_dplan_info",
@@ -67,6 +67,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tsg_plan_enqueue": (I, [P, P, P]),
         "tsg_plan_sync": (I, [P, ctypes.POINTER(TsgReport)]),
         "tsg_plan_info": (I, [P, ctypes.POINTER(ctypes.c_int64), c_int_p, c_dbl_p]),
+        "tsg_plan_describe": (I, [P, ctypes.c_char_p, I]),
         "tsg_residual": (I, [P, I, I, c_int_p, c_dbl_pp, P, P, P, I, c_dbl_p]),
         "tsg_slab_bounds": (I, [I, c_dbl_p, I, I, c_int_p]),
         "tsg_dplan_create": (I, [P, I, I, I, I, c_int_p, c_dbl_pp, c_dbl_pp, ctypes.POINTER(TsgOpts),

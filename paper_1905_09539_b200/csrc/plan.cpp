@@ -31,6 +31,7 @@
 #include "solve.h"
 #include "util.h"
 
+#include "decouple.h"
 #include "plan_impl.h"
 
 namespace tsg_impl {
@@ -426,6 +427,7 @@ void tile_eigvecs(std::vector<tsg::TileMode>& tms, const std::vector<double>& dh
 }
 
 int capture_or_run(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool graph);
+int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U);
 int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool timing);
 
 }  // namespace
@@ -558,6 +560,50 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     scale += fro(Tc, nn);
   }
   pl->tiny = 0.5 * std::numeric_limits<double>::epsilon() * scale;
+  {
+    const int rc = try_decouple(pl.get(), T, U);
+    if (rc != TSG_OK) return rc;
+  }
+  if (pl->decoupled) {
+    TSG_CU(cudaMalloc(&pl->flags, sizeof(int)));
+    TSG_CU(cudaMalloc(&pl->counter, 2 * sizeof(int)));
+    pl->ntiles = 1;
+    static const bool small_on = [] {
+      const char* e = std::getenv("TSG_SMALLMODES");
+      return !e || std::atoi(e) != 0;
+    }();
+    const bool two_gemm = !(small_on && (tsg::small_mode_ok(dims[0]) || tsg::small_mode_ok(dims[1])));
+    if (d >= 3 && two_gemm && pl->N / (static_cast<int64_t>(dims[0]) * dims[1]) > 1) {
+      int bm = 0, bn = 0;
+      const int64_t Q0 = pl->N / dims[0];
+      tsg::gemm_tile_shape(dims[0], static_cast<int>(Q0), &bm, &bn);
+      if (bm > 0 && bn > 0 && Q0 < INT_MAX) {
+        pl->s_tm = (dims[0] + bm - 1) / bm;
+        pl->s_bn = bn;
+        pl->sdone_n = pl->s_tm * static_cast<int>((Q0 + bn - 1) / bn);
+      }
+    }
+    tsg::gemm_prepare();
+    pl->aux_n = 2 * static_cast<int64_t>(pl->sdone_n);
+    if (pl->aux_n > 0) {
+      TSG_CU(cudaMalloc(&pl->aux, pl->aux_n * sizeof(int)));
+      pl->sdone[0] = pl->aux;
+      pl->sdone[1] = pl->aux + pl->sdone_n;
+    }
+    double sn = 0, snm1 = 0;
+    for (int m = 0; m < d; ++m) {
+      sn += dims[m];
+      snm1 += dims[m] - 1;
+    }
+    const double Nd = static_cast<double>(pl->N);
+    pl->flops_alg = Nd * snm1 + 4.0 * Nd * sn;
+    // complex back substitution: n_f^2 real FMA per pair of real fibres
+    pl->flops_exec = Nd * dims[pl->dec_f] + 4.0 * Nd * sn;
+    TSG_CU(pl->w1.ensure(pl->N));
+    TSG_CU(pl->w2.ensure(pl->N));
+    *out = pl.release();
+    return TSG_OK;
+  }
   // Closed-form base cells lose ~eps*cond(V); refine when some block's
   // eigenbasis is poorly conditioned (rare for LAPACK-standardised blocks).
   pl->refine = pl->max_cond > 1e3 ? 1 : 0;
@@ -949,6 +995,24 @@ int tsg_plan_info(const tsg_plan* pl, int64_t* n_tiles, int* tile_extents, doubl
     for (int m = 0; m < pl->d; ++m) tile_extents[m] = pl->tile_ext[m];
   if (flops_alg) *flops_alg = pl->flops_alg;
   return TSG_OK;
+}
+
+int tsg_plan_describe(const tsg_plan* pl, char* buf, int len) {
+  if (!pl) return -1;
+  char tmp[160];
+  if (pl->decoupled)
+    std::snprintf(tmp, sizeof(tmp), "decoupled f=%d kappa=%.3g", pl->dec_f, pl->dec_kappa);
+  else if (pl->use16)
+    std::snprintf(tmp, sizeof(tmp), "lap16");
+  else
+    std::snprintf(tmp, sizeof(tmp), "%s", pl->fast == 3 ? "lap3" : pl->fast == 5 ? "lapd" : pl->fast == 6 ? "gsyd"
+                                             : pl->fast == 1 ? "lap" : "generic");
+  const int n = static_cast<int>(std::strlen(tmp));
+  if (buf && len > 0) {
+    std::strncpy(buf, tmp, static_cast<size_t>(len - 1));
+    buf[len - 1] = 0;
+  }
+  return n;
 }
 
 int tsg_plan_enqueue(tsg_plan* pl, const double* B, double* X) {
@@ -1413,6 +1477,20 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   // Solve state reset first, so the forward GEMMs and the solve follow each
   // other directly (programmatic launches).
   TSG_CU(tsg::reset_state(pl->flags, pl->ntiles, pl->counter, kNoStatus, pl->aux, pl->aux_n, st));
+  if (pl->decoupled) {
+    TSG_CU(transform_all(pl, in, pl->w1.p, pl->w2.p, true, st));
+    if (timing) TSG_CU(cudaEventRecord(ev[2], st));
+    tsg::FibreArgs fa = pl->fib;
+    fa.X = pl->w1.p;
+    fa.counter = pl->counter;
+    fa.status = pl->counter + 1;
+    TSG_CU(tsg::launch_fibre_solve(fa, ctx->device, st, &pl->solve_info));
+    ++pl->launches;
+    if (timing) TSG_CU(cudaEventRecord(ev[3], st));
+    TSG_CU(transform_all(pl, pl->w1.p, out, pl->w2.p, false, st));
+    if (timing) TSG_CU(cudaEventRecord(ev[4], st));
+    return TSG_OK;
+  }
   const bool want_trace = std::getenv("TSG_TRACE") != nullptr;
   const bool want_prof = std::getenv("TSG_PROF") != nullptr;
   // TSG_GATE=0 (read per call) runs every kernel after its predecessor: the
@@ -1624,6 +1702,215 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     std::fprintf(stderr, "[tsg dbg] fdone unreleased %d of %d (tm %d, bm %d, bn %d)\n", nun, pl->fdone_n, pl->fg_tm,
                  pl->fg_bm, pl->fg_bn);
   }
+  return TSG_OK;
+}
+
+template <typename V>
+cudaError_t upload_owned(tsg_plan* pl, const V& v, const typename V::value_type** out) {
+  using E = typename V::value_type;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, std::max<size_t>(v.size(), 1) * sizeof(E));
+  if (e != cudaSuccess) return e;
+  pl->owned.push_back(p);
+  e = cudaMemcpy(p, v.data(), v.size() * sizeof(E), cudaMemcpyHostToDevice);
+  *out = static_cast<const E*>(p);
+  return e;
+}
+
+// Eigen-decoupled path: Laplace plans with transforms, every
+// mode but one free mode f > 0 with a well-conditioned real block-eigenbasis
+// (prod kappa_2 <= kDecoupleKappa).  TSG_DECOUPLE=0 turns it off,
+// TSG_DECOUPLE_NFMAX bounds n_f (default 1024).
+int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
+  tsg_ctx* ctx = pl->ctx;
+  const int d = pl->d;
+  const int* dims = pl->dims.data();
+  const char* env = std::getenv("TSG_DECOUPLE");
+  if (pl->family != 0 || pl->reduced_only || tsg_impl::g_force_lap3 || (env && std::atoi(env) == 0))
+    return TSG_OK;
+  if (d - 1 > tsg::kFibreMaxS) return TSG_OK;
+  const char* ne = std::getenv("TSG_DECOUPLE_NFMAX");
+  const int nfmax = ne ? std::atoi(ne) : 1024;
+  bool any = false;
+  for (int f = 1; f < d; ++f) any = any || dims[f] <= nfmax;
+  if (!any) return TSG_OK;
+  std::vector<tsg_impl::ModeEigen> me(d);
+  std::vector<int> ok(d);
+  for (int m = 0; m < d; ++m) ok[m] = tsg_impl::mode_eigen(T[m], dims[m], me[m]) ? 1 : 0;
+  int best = -1;
+  double best_prod = 0;
+  for (int f = 1; f < d; ++f) {
+    if (dims[f] > nfmax) continue;
+    double prod = 1;
+    for (int m = 0; m < d; ++m)
+      if (m != f) prod *= ok[m] ? me[m].kappa : 1e300;
+    if (!(prod <= tsg_impl::kDecoupleKappa)) continue;
+    const double kf = ok[f] ? me[f].kappa : 1e300;
+    if (best < 0 || dims[f] < dims[best] || (dims[f] == dims[best] && kf > (ok[best] ? me[best].kappa : 1e300))) {
+      best = f;
+      best_prod = prod;
+    }
+  }
+  if (best < 0) return TSG_OK;
+  const int f = best;
+  const int nf = dims[f];
+  {
+    const std::vector<int8_t> code = block_codes(T[f], nf);
+    for (int i = 0; i < nf; ++i)
+      if (code[i] == 1) {
+        const double p = at(T[f], nf, i, i), b = at(T[f], nf, i, i + 1), c = at(T[f], nf, i + 1, i),
+                     q = at(T[f], nf, i + 1, i + 1);
+        if (!(0.25 * (p - q) * (p - q) + b * c < 0)) return TSG_OK;  // not in standard form
+      }
+    int nsc = 0;
+    for (int m = 1; m < d; ++m) {
+      if (m == f) continue;
+      bool cx = false;
+      for (const auto& c : me[m].cells) cx = cx || c.size == 2;
+      nsc += cx ? 1 : 0;
+    }
+    const size_t tb = nf <= 64 ? static_cast<size_t>(nf) * nf * 8 : 0;
+    if (100 * 1024 <= tb + ((static_cast<size_t>(nf) * 8 + 4) << nsc) * 2) return TSG_OK;
+  }
+  tsg::FibreArgs& a = pl->fib;
+  a = tsg::FibreArgs{};
+  a.nf = nf;
+  a.sf = pl->stride[f];
+  {
+    std::vector<double> tt(static_cast<size_t>(nf) * nf), fc(4 * static_cast<size_t>(nf), 0.0);
+    for (int i = 0; i < nf; ++i)
+      for (int j = 0; j < nf; ++j) tt[static_cast<size_t>(i) * nf + j] = T[f][i + static_cast<size_t>(j) * nf];
+    const std::vector<int8_t> code = block_codes(T[f], nf);
+    for (int i = 0; i < nf; ++i) {
+      fc[4 * i] = code[i];
+      if (code[i] == 1) {
+        const double p = at(T[f], nf, i, i), b = at(T[f], nf, i, i + 1), c = at(T[f], nf, i + 1, i),
+                     q = at(T[f], nf, i + 1, i + 1);
+        const double disc = 0.25 * (p - q) * (p - q) + b * c;
+        const double re = 0.5 * (p + q), w = disc < 0 ? std::sqrt(-disc) : 0.0;
+        const double r2 = disc < 0 ? 0.0 : std::sqrt(disc);
+        // eigenvalues re +- i w (complex pair) or re +- r2 (real pair: stored as w = i r2
+        // is not representable; use the nearer-to-zero bound via re and r2 in the check)
+        fc[4 * i + 1] = fc[4 * i + 5] = re;
+        fc[4 * i + 2] = fc[4 * i + 6] = w;
+        fc[4 * i + 3] = fc[4 * i + 7] = r2;
+      }
+    }
+    TSG_CU(upload_owned(pl, tt, &a.Tt));
+    TSG_CU(upload_owned(pl, fc, &a.fcell));
+  }
+  // S modes other than 0, in mode order
+  int nsc = 0;
+  int64_t nblk_rest = 1;
+  for (int m = 1; m < d; ++m) {
+    if (m == f) continue;
+    const int s = a.ns++;
+    a.sstride[s] = pl->stride[m];
+    a.ncell[s] = static_cast<int>(me[m].cells.size());
+    TSG_CU(upload_owned(pl, me[m].cells, &a.cells[s]));
+    bool cx = false;
+    for (const auto& c : me[m].cells) cx = cx || c.size == 2;
+    nsc += cx ? 1 : 0;
+    nblk_rest *= a.ncell[s];
+  }
+  // mode-0 chunks of whole cells within the shared-memory budget: the
+  // register kernel for n_f <= 24 (three CTAs per SM), else the DMMA-blocked
+  // kernel (two CTAs per SM)
+  const bool small = nf <= 24;
+  int W = 0;
+  int ncell_s = 0;
+  for (int m = 1; m < d; ++m)
+    if (m != f) ncell_s += static_cast<int>(me[m].cells.size());
+  const int cell_smem = ncell_s <= 1024 ? ncell_s : 0;
+  if (small) {
+    // two block buffers (the next block streams in while one is solved)
+    const int NF = nf <= 8 ? 8 : nf <= 16 ? 16 : 24;
+    const long avail = (72 * 1024 - 2 * 128 * 32 - cell_smem * 24) / 8 - NF * NF - 3 * NF;
+    W = static_cast<int>(std::min<long>(avail / (2 * (static_cast<long>(nf) << nsc)), 128));
+  } else {
+    const size_t per_row = (static_cast<size_t>(nf) * 8 + 24) << nsc;
+    const size_t fixed = static_cast<size_t>(nf) * 16 * 8 + 128 * 32 + 16 + cell_smem * 24;
+    W = 108 * 1024 > fixed ? static_cast<int>(std::min<size_t>((108 * 1024 - fixed) / per_row, 128)) : 0;
+  }
+  if (W < 2) return TSG_OK;  // not admissible: the tile kernels keep the plan
+  std::vector<int> chunk{0}, cellrow0(dims[0]);
+  const auto& c0 = me[0].cells;
+  for (int c = 0; c < static_cast<int>(c0.size()); ++c) {
+    for (int r = c0[c].start; r < c0[c].start + c0[c].size; ++r) cellrow0[r] = c;
+    if (c0[c].start + c0[c].size - chunk.back() > W) chunk.push_back(c0[c].start);
+  }
+  chunk.push_back(dims[0]);
+  int wmax = 0;
+  for (size_t q = 0; q + 1 < chunk.size(); ++q) wmax = std::max(wmax, chunk[q + 1] - chunk[q]);
+  a.nchunk = static_cast<int>(chunk.size()) - 1;
+  TSG_CU(upload_owned(pl, chunk, &a.chunk_lo));
+  {
+    std::vector<int> u0{0};
+    std::vector<tsg::FibreUnit> units;
+    for (int q = 0; q < a.nchunk; ++q) {
+      int npb = 0;
+      for (int c = cellrow0[chunk[q]]; c < static_cast<int>(c0.size()) && c0[c].start < chunk[q + 1]; ++c) {
+        tsg::FibreUnit un{};
+        un.rl0 = c0[c].start - chunk[q];
+        un.pair0 = c0[c].size == 2 ? 1 : 0;
+        un.npair_before = npb;
+        un.sr = c0[c].re;
+        un.si = un.pair0 ? -c0[c].im : 0.0;
+        npb += un.pair0;
+        units.push_back(un);
+      }
+      u0.push_back(static_cast<int>(units.size()));
+    }
+    TSG_CU(upload_owned(pl, u0, &a.chunk_u0));
+    TSG_CU(upload_owned(pl, units, &a.units));
+  }
+  a.cell_smem = cell_smem;
+  TSG_CU(upload_owned(pl, cellrow0, &a.cellrow0));
+  TSG_CU(upload_owned(pl, c0, &a.cell0));
+  a.maxcol = wmax << nsc;
+  a.small = tsg::fibre_small_ok(nf, wmax) ? 1 : 0;
+  if (const char* e = std::getenv("TSG_FIBRE_SMALL")) a.small = a.small && std::atoi(e) != 0;
+  a.big = a.small ? 0 : 1;
+  if (const char* e = std::getenv("TSG_FIBRE_BIG")) a.big = a.big && std::atoi(e) != 0;
+  if (a.big) {
+    // row blocks of f: <= 8 rows, never splitting a 2x2 cell
+    const std::vector<int8_t> code = block_codes(T[f], nf);
+    std::vector<int> rb{0};
+    while (rb.back() < nf) {
+      int e = std::min(rb.back() + 8, nf);
+      if (e < nf && code[e] == 2) --e;
+      rb.push_back(e);
+    }
+    a.nrb = static_cast<int>(rb.size()) - 1;
+    TSG_CU(upload_owned(pl, rb, &a.rb));
+    a.pitch = tsg::fibre_pitch(a.maxcol);
+  }
+  a.nblocks = static_cast<int64_t>(a.nchunk) * nblk_rest;
+  // folded transforms of the S modes
+  for (int m = 0; m < d; ++m) {
+    if (m == f) continue;
+    const int n = dims[m];
+    const size_t nn = static_cast<size_t>(n) * n;
+    const std::vector<double> ut = transpose(U[m], n);
+    const std::vector<double> fw = tsg_impl::matmul(me[m].Pinv.data(), ut.data(), n);
+    const std::vector<double> bw = tsg_impl::matmul(U[m], me[m].P.data(), n);
+    const std::vector<double> fwt = transpose(fw.data(), n), bwt = transpose(bw.data(), n);
+    TSG_CU(upload_mat(pl->Fwd[m], fw.data(), nn));
+    TSG_CU(upload_mat(pl->FwdT[m], fwt.data(), nn));
+    TSG_CU(upload_mat(pl->Bwd[m], bw.data(), nn));
+    TSG_CU(upload_mat(pl->BwdT[m], bwt.data(), nn));
+  }
+  a.tiny = pl->tiny;
+  pl->decoupled = 1;
+  pl->dec_f = f;
+  pl->dec_kappa = best_prod;
+  pl->tile_ext.assign(d, 2);
+  pl->tile_ext[0] = wmax;
+  pl->tile_ext[f] = nf;
+  pl->ntiles_mode.assign(d, 1);
+  if (std::getenv("TSG_VERBOSE"))
+    std::fprintf(stderr, "[tsg] decoupled solve: free mode %d (n=%d), prod kappa %.3g, blocks %lld, maxcol %d\n",
+                 f, nf, best_prod, static_cast<long long>(a.nblocks), a.maxcol);
   return TSG_OK;
 }
 

@@ -94,6 +94,12 @@ struct tsg_plan {
   double max_cond = 0;  // worst 2x2 eigenbasis condition (Frobenius)
   int refine = 0;
   tsg::SolveLaunchInfo solve_info{};
+  // Eigen-decoupled fibre solve (decouple.cpp, solve_fibre.cu): modes other
+  // than `dec_f` are folded into their eigenbases by the transforms.
+  int decoupled = 0, dec_f = -1;
+  double dec_kappa = 0;
+  tsg::FibreArgs fib{};
+  std::vector<void*> owned;  // device tables of the fibre solve
   // graph cache
   cudaGraphExec_t gexec = nullptr;
   const double* g_in = nullptr;
@@ -117,6 +123,8 @@ struct tsg_plan {
                     static_cast<void*>(ocoord2)})
       if (q) cudaFree(q);
     if (gexec) cudaGraphExecDestroy(gexec);
+    for (void* q : owned)
+      if (q) cudaFree(q);
   }
 };
 

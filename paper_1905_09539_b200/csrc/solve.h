@@ -1,5 +1,6 @@
 // Host-side interface of the reduced-form dataflow solver (solve.cu).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -129,5 +130,62 @@ cudaError_t launch_solve_gsyd(const SolveArgs& a, cudaStream_t st, SolveLaunchIn
 // Fast Laplace path (solve_lap.cu): small tiles, eigenbasis base cells.
 TileCaps solve_lap_caps(int d);
 cudaError_t launch_solve_lap(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info);
+
+// ---- Eigen-decoupled fibre solve (solve_fibre.cu) ---------------------------
+// Modes s in S are moved into their real block-eigenbasis by the transforms
+// (T_s = P_s Lambda_s P_s^{-1}, Lambda_s = 1x1 lambda / 2x2 [[re, im], [-im, re]]
+// blocks), so the reduced operator is
+//     sum_{s in S} X x_s Lambda_s  +  X x_f T_f
+// and splits into independent units (one Schur cell per S mode) of 2^k
+// coupled fibres along the one free mode f (k = complex cells in the unit).
+// A butterfly over the unit's complex cells turns them into 2^(k-1) complex
+// fibres, each solving (T_f + sigma I) z = r by back substitution over the
+// 1x1/2x2 cells of T_f.  Mode 0 is in S (f > 0) and is cut into chunks of
+// whole cells; a block = one chunk x one cell of every other S mode x the
+// whole f extent.
+struct FibreCell {
+  int start, size;
+  double re, im;  // 1x1: lambda = re; 2x2: Lambda block [[re, im], [-im, re]]
+};
+constexpr int kFibreMaxS = 6;
+// Per mode-0 cell of a chunk (host-built, chunk_u0 indexes the chunk's first):
+// row offset in the chunk, 2x2 flag, pairs before it in the chunk, and its
+// contribution to the shift (re, -omega for a pair).
+struct alignas(16) FibreUnit {
+  int rl0, pair0, npair_before, pad;
+  double sr, si;
+};
+struct FibreArgs {
+  double* X;                 // in place: B^ on entry, X^ on exit
+  int nf;                    // extent of the free mode f
+  int64_t sf;                // its stride
+  const double* Tt;          // T_f row-major (Tt[i * nf + j] = T_f(i, j))
+  const double* fcell;       // per row of f: 4 doubles (code 0/1/2, a, omega, unused)
+  int nchunk;
+  const int* chunk_lo;       // nchunk + 1 mode-0 row bounds (whole cells)
+  const int* cellrow0;       // mode-0 row -> cell index
+  const FibreCell* cell0;    // mode-0 cells
+  const int* chunk_u0;       // nchunk + 1: first unit of every chunk
+  const FibreUnit* units;    // mode-0 cells as units, chunk by chunk
+  int cell_smem;             // > 0: cache the S' cell tables (this many) in shared memory
+  int ns;                    // other S modes
+  int64_t sstride[kFibreMaxS];
+  int ncell[kFibreMaxS];
+  const FibreCell* cells[kFibreMaxS];
+  int64_t nblocks;
+  int maxcol;                // largest block width (columns = chunk rows x 2^k')
+  int small;                 // 1: the register kernel (n_f <= 24, chunks <= 128 rows)
+  int big;                   // 1: the DMMA-blocked kernel (row blocks rb, shared pitch)
+  int pitch;                 // big: shared row pitch (= 4 mod 16 doubles)
+  int nrb;                   // big: row blocks of f (<= 8 rows, whole cells)
+  const int* rb;             // big: nrb + 1 row-block bounds
+  int* counter;              // block queue head (zeroed before launch)
+  int* status;               // first singular element offset (atomicMin)
+  double tiny;
+};
+cudaError_t launch_fibre_solve(const FibreArgs& a, int device, cudaStream_t st, SolveLaunchInfo* info);
+bool fibre_small_ok(int nf, int chunk_w);
+int fibre_pitch(int maxcol);
+size_t fibre_big_smem(int nf, int maxcol, int cell_smem);
 
 }  // namespace tsg

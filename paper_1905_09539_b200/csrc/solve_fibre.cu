@@ -1,0 +1,844 @@
+// Eigen-decoupled fibre solve (K5): the reduced solve once every mode but
+// one (f) has been moved into its real block-eigenbasis by the transforms.
+//
+// Operator on the transformed tensor (solve.h, FibreArgs):
+//     sum_{s in S} Y x_s Lambda_s + Y x_f T_f = R,
+// Lambda_s block diagonal (1x1 lambda, 2x2 [[a, w], [-w, a]]), T_f the
+// quasi-triangular Schur factor of mode f.  A unit = one cell of every S mode
+// = 2^k real fibres along f (k = its 2x2 cells).  Complex structure: for the
+// 2x2 cell of one S mode, z = y_0 + i y_1 turns [[a, w], [-w, a]] into the
+// scalar a - i w.  With several 2x2 cells the first one is the re/im pair
+// and every further cell t is diagonalised by the butterfly
+// (z_0, z_1) -> (z_0 + i z_1, z_0 - i z_1) (eigenvalues a_t - i w_t,
+// a_t + i w_t); the other half of the patterns are complex conjugates and
+// never formed.  Each of the 2^(k-1) complex fibres then solves
+//     (T_f + sigma I) z = r,  sigma = sum of its cells' eigenvalues,
+// by back substitution over the 1x1/2x2 cells of T_f (2x2: Cramer), and the
+// inverse butterfly restores the real fibres.  Everything runs in place in
+// shared memory: one HBM read of R and one write of X per element.
+//
+// Reference: the same equation the recursion laplace_recursive / lap_rec
+// (laplace.hpp:134-195) solves; the decoupling replaces the d-dimensional
+// dependency DAG by independent fibres.
+#include <climits>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "common.cuh"
+#include "solve.h"
+
+namespace tsg {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTsmemMax = 64;  // T_f staged in shared memory up to this extent
+
+struct Blk {
+  int64_t base;
+  int w, kb, r_lo, ncol, njob;
+  int64_t bstride[kFibreMaxS];
+  double bre[kFibreMaxS], bim[kFibreMaxS];
+  double sreal;
+};
+
+TSG_DEVINL int64_t goff(const Blk& B, int col, int i, int64_t sf) {
+  const int r = col % B.w, b = col / B.w;
+  int64_t o = B.base + r + static_cast<int64_t>(i) * sf;
+#pragma unroll
+  for (int t = 0; t < kFibreMaxS; ++t)
+    if (t < B.kb && ((b >> t) & 1)) o += B.bstride[t];
+  return o;
+}
+
+// In-place butterfly of every complex bit of the block, forward (inv = 0)
+// or inverse (inv = 1).  Quad (re0, im0, re1, im1) per (row, unit, bit).
+TSG_DEVINL void butterflies(const FibreArgs& a, const Blk& B, double* Y, bool inv) {
+  const int nf = a.nf, ncol = B.ncol;
+  for (int t = 0; t < B.kb; ++t) {
+    const int step = B.w << t;
+    for (int e = threadIdx.x; e < nf * ncol; e += blockDim.x) {
+      const int i = e / ncol, col = e - i * ncol;
+      const int rl = col % B.w, b = col / B.w;
+      if ((b >> t) & 1) continue;
+      const FibreCell c0 = a.cell0[a.cellrow0[B.r_lo + rl]];
+      int imo;
+      if (c0.size == 2) {
+        if (B.r_lo + rl != c0.start) continue;  // re row of the mode-0 pair
+        imo = 1;
+      } else {
+        if (t == 0 || (b & 1)) continue;  // bit 0 is the re/im pair itself
+        imo = B.w;
+      }
+      double* y = Y + static_cast<size_t>(i) * ncol;
+      const double re0 = y[col], im0 = y[col + imo];
+      const double re1 = y[col + step], im1 = y[col + step + imo];
+      if (!inv) {
+        y[col] = re0 - im1;
+        y[col + imo] = im0 + re1;
+        y[col + step] = re0 + im1;
+        y[col + step + imo] = im0 - re1;
+      } else {
+        y[col] = 0.5 * (re0 + re1);
+        y[col + imo] = 0.5 * (im0 + im1);
+        y[col + step] = 0.5 * (im0 - im1);
+        y[col + step + imo] = -0.5 * (re0 - re1);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Back substitution of one complex (or real, im < 0) fibre along f.
+TSG_DEVINL void solve_job(const FibreArgs& a, const double* T, double* Y, int ncol, int re, int im,
+                          double sr, double si, int64_t off_hint) {
+  const int nf = a.nf;
+  const bool cx = im >= 0;
+  for (int i = nf - 1; i >= 0;) {
+    const double* fc = a.fcell + 4 * i;
+    if (fc[0] == 2.0) {  // rows (i - 1, i): a 2x2 cell of T_f
+      const int i0 = i - 1;
+      double ar = Y[i0 * ncol + re], ai = cx ? Y[i0 * ncol + im] : 0.0;
+      double br = Y[i * ncol + re], bi = cx ? Y[i * ncol + im] : 0.0;
+      const double* t0 = T + static_cast<size_t>(i0) * nf;
+      const double* t1 = T + static_cast<size_t>(i) * nf;
+      for (int j = i + 1; j < nf; ++j) {
+        const double zr = Y[j * ncol + re], zi = cx ? Y[j * ncol + im] : 0.0;
+        ar = fma(-t0[j], zr, ar);
+        ai = fma(-t0[j], zi, ai);
+        br = fma(-t1[j], zr, br);
+        bi = fma(-t1[j], zi, bi);
+      }
+      // M = [[t00 + s, t01], [t10, t11 + s]] (complex s)
+      const double m00r = t0[i0] + sr, m11r = t1[i] + sr, m01 = t0[i], m10 = t1[i0];
+      const double detr = m00r * m11r - si * si - m01 * m10;
+      const double deti = si * (m00r + m11r);
+      // eigenvalues (a +- i w) + s of the cell: singular check
+      const double ea = fc[1] + sr, ew = fc[2];
+      const double e1 = hypot(ea, si + ew), e2 = hypot(ea, si - ew);
+      if (fmin(e1, e2) <= a.tiny)
+        atomicMin(a.status, static_cast<int>(off_hint < INT_MAX - 1 ? off_hint : INT_MAX - 1));
+      // za = (m11 ra - m01 rb) / det, zb = (m00 rb - m10 ra) / det
+      const double nar = m11r * ar - si * ai - m01 * br;
+      const double nai = m11r * ai + si * ar - m01 * bi;
+      const double nbr = m00r * br - si * bi - m10 * ar;
+      const double nbi = m00r * bi + si * br - m10 * ai;
+      const double dd = detr * detr + deti * deti;
+      const double ir = detr / dd, ii = -deti / dd;
+      Y[i0 * ncol + re] = nar * ir - nai * ii;
+      Y[i * ncol + re] = nbr * ir - nbi * ii;
+      if (cx) {
+        Y[i0 * ncol + im] = nar * ii + nai * ir;
+        Y[i * ncol + im] = nbr * ii + nbi * ir;
+      }
+      i -= 2;
+    } else {
+      double rr = Y[i * ncol + re], ri = cx ? Y[i * ncol + im] : 0.0;
+      const double* ti = T + static_cast<size_t>(i) * nf;
+      for (int j = i + 1; j < nf; ++j) {
+        rr = fma(-ti[j], Y[j * ncol + re], rr);
+        if (cx) ri = fma(-ti[j], Y[j * ncol + im], ri);
+      }
+      const double dr = ti[i] + sr, di = si;
+      const double dd = dr * dr + di * di;
+      if (sqrt(dd) <= a.tiny)
+        atomicMin(a.status, static_cast<int>(off_hint < INT_MAX - 1 ? off_hint : INT_MAX - 1));
+      Y[i * ncol + re] = (rr * dr + ri * di) / dd;
+      if (cx) Y[i * ncol + im] = (ri * dr - rr * di) / dd;
+      i -= 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) fibre_solve_kernel(const FibreArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int nf = a.nf;
+  const bool tsm = nf <= kTsmemMax;
+  double* sT = sm;
+  double* Y = sm + (tsm ? nf * nf : 0);
+  int* jobs = reinterpret_cast<int*>(Y + static_cast<size_t>(a.maxcol) * nf);
+  __shared__ Blk B;
+  __shared__ int64_t s_blk;
+  __shared__ int s_cnt;
+  pdl_wait();
+  if (tsm)
+    for (int e = threadIdx.x; e < nf * nf; e += blockDim.x) sT[e] = a.Tt[e];
+  const double* T = tsm ? sT : a.Tt;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_blk = atomicAdd(a.counter, 1);
+      s_cnt = 0;
+    }
+    __syncthreads();
+    const int64_t blk = s_blk;
+    if (blk >= a.nblocks) break;
+    if (threadIdx.x == 0) {
+      int64_t rest = blk / a.nchunk;
+      const int q = static_cast<int>(blk - rest * a.nchunk);
+      B.r_lo = a.chunk_lo[q];
+      B.w = a.chunk_lo[q + 1] - B.r_lo;
+      int64_t base = B.r_lo;
+      int kb = 0;
+      double sreal = 0.0;
+      for (int s = 0; s < a.ns; ++s) {
+        const int64_t nx = rest / a.ncell[s];
+        const int c = static_cast<int>(rest - nx * a.ncell[s]);
+        rest = nx;
+        const FibreCell fc = a.cells[s][c];
+        base += static_cast<int64_t>(fc.start) * a.sstride[s];
+        if (fc.size == 2) {
+          B.bstride[kb] = a.sstride[s];
+          B.bre[kb] = fc.re;
+          B.bim[kb] = fc.im;
+          ++kb;
+        } else {
+          sreal += fc.re;
+        }
+      }
+      B.base = base;
+      B.kb = kb;
+      B.sreal = sreal;
+      B.ncol = B.w << kb;
+    }
+    __syncthreads();
+    const int ncol = B.ncol, w = B.w;
+    // load: rows of w contiguous mode-0 elements
+    {
+      const int nb = 1 << B.kb;
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int row = warp; row < nf * nb; row += nw) {
+        const int i = row / nb, b = row - i * nb;
+        const double* src = a.X + goff(B, b * w, i, a.sf);
+        double* dst = Y + static_cast<size_t>(i) * ncol + b * w;
+        for (int r = lane; r < w; r += 32) dst[r] = src[r];
+      }
+    }
+    // job list (complex fibres: re column of each pattern; real units: the column)
+    for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
+      const int rl = col % w, b = col / w;
+      const FibreCell c0 = a.cell0[a.cellrow0[B.r_lo + rl]];
+      const bool job = c0.size == 2 ? (B.r_lo + rl == c0.start) : (B.kb == 0 || !(b & 1));
+      if (job) jobs[atomicAdd(&s_cnt, 1)] = col;
+    }
+    __syncthreads();
+    butterflies(a, B, Y, false);
+    const int njob = s_cnt;
+    for (int j = threadIdx.x; j < njob; j += blockDim.x) {
+      const int col = jobs[j];
+      const int rl = col % w, b = col / w;
+      const FibreCell c0 = a.cell0[a.cellrow0[B.r_lo + rl]];
+      double sr = B.sreal + c0.re, si = 0.0;
+      int im = -1;
+      if (c0.size == 2) {
+        si = -c0.im;
+        im = col + 1;
+      } else if (B.kb > 0) {
+        im = col + w;
+      }
+      for (int t = 0; t < B.kb; ++t) {
+        sr += B.bre[t];
+        si += ((b >> t) & 1) ? B.bim[t] : -B.bim[t];
+      }
+      solve_job(a, T, Y, ncol, col, im, sr, si, goff(B, col, 0, a.sf));
+    }
+    __syncthreads();
+    butterflies(a, B, Y, true);
+    {
+      const int nb = 1 << B.kb;
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int row = warp; row < nf * nb; row += nw) {
+        const int i = row / nb, b = row - i * nb;
+        double* dst = a.X + goff(B, b * w, i, a.sf);
+        const double* src = Y + static_cast<size_t>(i) * ncol + b * w;
+        for (int r = lane; r < w; r += 32) dst[r] = src[r];
+      }
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
+// ---- small free modes (n_f <= 32): units in registers -----------------------
+// Per block: units = the mode-0 cells of the chunk; unit u has 2^k columns
+// (k = 2x2 cells among its mode-0 cell and the block's S' cells), local
+// index l: bit 0 = the re/im pair, bit t >= 1 = the t-th further 2x2 cell.
+// Butterflies run per (unit, row) on the unit's 2^k values in registers; each
+// job (one complex fibre) keeps its n_f values in registers for the back
+// substitution against T_f in shared memory.
+constexpr int kMaxUnits = 128;
+constexpr int kSmallThreads = 128;  // 170 registers at n_f = 24: three CTAs per SM
+
+struct UnitTab {
+  int n;               // units in the block
+  int rl0[kMaxUnits];  // first chunk row
+  int k[kMaxUnits];    // complex bits (0..5)
+  int job0[kMaxUnits + 1];
+  double sr[kMaxUnits], si[kMaxUnits];  // mode-0 cell contribution to sigma (si: -omega for a pair)
+};
+
+TSG_DEVINL int ucol(int l, int rl0, int pair0, int w) {
+  return pair0 ? rl0 + (l & 1) + w * (l >> 1) : rl0 + w * l;
+}
+
+template <int K, bool INV>
+TSG_DEVINL void unit_bfly_k(double* y, int rl0, int pair0, int w) {
+  constexpr int NL = 1 << K;
+  double v[NL];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) v[l] = y[ucol(l, rl0, pair0, w)];
+#pragma unroll
+  for (int t = 1; t < K; ++t) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      if ((l & 1) || ((l >> t) & 1)) continue;
+      const int l1 = l | (1 << t);
+      const double re0 = v[l], im0 = v[l | 1], re1 = v[l1], im1 = v[l1 | 1];
+      if (!INV) {
+        v[l] = re0 - im1;
+        v[l | 1] = im0 + re1;
+        v[l1] = re0 + im1;
+        v[l1 | 1] = im0 - re1;
+      } else {
+        v[l] = 0.5 * (re0 + re1);
+        v[l | 1] = 0.5 * (im0 + im1);
+        v[l1] = 0.5 * (im0 - im1);
+        v[l1 | 1] = -0.5 * (re0 - re1);
+      }
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < NL; ++l) y[ucol(l, rl0, pair0, w)] = v[l];
+}
+
+template <bool INV>
+TSG_DEVINL void unit_butterfly(double* Y, int ncol, int i, int rl0, int k, int pair0, int w) {
+  double* y = Y + static_cast<size_t>(i) * ncol;
+  switch (k) {
+    case 2: unit_bfly_k<2, INV>(y, rl0, pair0, w); break;
+    case 3: unit_bfly_k<3, INV>(y, rl0, pair0, w); break;
+    case 4: unit_bfly_k<4, INV>(y, rl0, pair0, w); break;
+    case 5: unit_bfly_k<5, INV>(y, rl0, pair0, w); break;
+    default: break;
+  }
+}
+
+// Right-looking back substitution with the fibre in registers: once z_j
+// (or the 2x2 pair z_{j-1}, z_j) is final, its column of T_f is applied to
+// every row above.  All indices are compile-time (NF <= 24 stays in
+// registers at 128 per thread).
+template <int NF>
+TSG_DEVINL void solve_job_reg(const FibreArgs& a, const double* T, const double* fc, double* Y,
+                              int ncol, int re, int im, double sr, double si, int64_t off_hint) {
+  const int nf = a.nf;
+  const bool cx = im >= 0;
+  double zr[NF], zi[NF];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) {
+    zr[i] = i < nf ? Y[i * ncol + re] : 0.0;
+    zi[i] = (i < nf && cx) ? Y[i * ncol + im] : 0.0;
+  }
+  bool bad = false;
+#pragma unroll
+  for (int j = NF - 1; j >= 0; --j) {
+    if (j >= nf) continue;
+    const double code = fc[3 * j];
+    if (code == 1.0) continue;  // first row of a pair: solved with its second row
+    if (code == 2.0 && j >= 1) {
+      const double m00r = T[(j - 1) * NF + j - 1] + sr, m11r = T[j * NF + j] + sr;
+      const double m01 = T[(j - 1) * NF + j], m10 = T[j * NF + j - 1];
+      const double detr = m00r * m11r - si * si - m01 * m10, deti = si * (m00r + m11r);
+      const double ea = fc[3 * j + 1] + sr, ew = fc[3 * j + 2];
+      bad = bad || fmin(hypot(ea, si + ew), hypot(ea, si - ew)) <= a.tiny;
+      const double ar = zr[j - 1], ai = zi[j - 1], rr = zr[j], ri = zi[j];
+      const double nar = m11r * ar - si * ai - m01 * rr, nai = m11r * ai + si * ar - m01 * ri;
+      const double nbr = m00r * rr - si * ri - m10 * ar, nbi = m00r * ri + si * rr - m10 * ai;
+      const double dd = detr * detr + deti * deti, ir = detr / dd, ii = -deti / dd;
+      zr[j - 1] = nar * ir - nai * ii;
+      zi[j - 1] = nar * ii + nai * ir;
+      zr[j] = nbr * ir - nbi * ii;
+      zi[j] = nbr * ii + nbi * ir;
+#pragma unroll
+      for (int i = 0; i < NF; ++i) {
+        if (i < j - 1) {
+          const double t1 = T[i * NF + j], t0 = T[i * NF + j - 1];
+          zr[i] = fma(-t1, zr[j], fma(-t0, zr[j - 1], zr[i]));
+          zi[i] = fma(-t1, zi[j], fma(-t0, zi[j - 1], zi[i]));
+        }
+      }
+    } else {
+      const double dr = T[j * NF + j] + sr, dd = dr * dr + si * si;
+      bad = bad || sqrt(dd) <= a.tiny;
+      const double rr = zr[j], ri = zi[j];
+      zr[j] = (rr * dr + ri * si) / dd;
+      zi[j] = (ri * dr - rr * si) / dd;
+#pragma unroll
+      for (int i = 0; i < NF; ++i) {
+        if (i < j) {
+          const double t = T[i * NF + j];
+          zr[i] = fma(-t, zr[j], zr[i]);
+          zi[i] = fma(-t, zi[j], zi[i]);
+        }
+      }
+    }
+  }
+  if (bad) atomicMin(a.status, static_cast<int>(off_hint < INT_MAX - 1 ? off_hint : INT_MAX - 1));
+#pragma unroll
+  for (int i = 0; i < NF; ++i) {
+    if (i < nf) {
+      Y[i * ncol + re] = zr[i];
+      if (cx) Y[i * ncol + im] = zi[i];
+    }
+  }
+}
+
+// Block pipeline of the small kernel: while block n is solved, block n+1's
+// geometry is decoded from shared-memory cell tables and its data and unit
+// table stream in with cp.async (two buffers).
+struct SmallBuf {
+  Blk B;
+  int64_t blk;
+  int nunit;
+  int job0[kMaxUnits + 1];
+};
+
+TSG_DEVINL void decode_block(const FibreArgs& a, const FibreCell* scell, const int* soff, int64_t blk,
+                             Blk& B, int& nunit) {
+  int64_t rest = blk / a.nchunk;
+  const int q = static_cast<int>(blk - rest * a.nchunk);
+  B.r_lo = a.chunk_lo[q];
+  B.w = a.chunk_lo[q + 1] - B.r_lo;
+  B.njob = a.chunk_u0[q];  // first unit of the chunk (reused field)
+  nunit = a.chunk_u0[q + 1] - a.chunk_u0[q];
+  int64_t base = B.r_lo;
+  int kb = 0;
+  double sreal = 0.0;
+  for (int s = 0; s < a.ns; ++s) {
+    const int64_t nx = rest / a.ncell[s];
+    const int c = static_cast<int>(rest - nx * a.ncell[s]);
+    rest = nx;
+    const FibreCell fc = scell ? scell[soff[s] + c] : a.cells[s][c];
+    base += static_cast<int64_t>(fc.start) * a.sstride[s];
+    if (fc.size == 2) {
+      B.bstride[kb] = a.sstride[s];
+      B.bre[kb] = fc.re;
+      B.bim[kb] = fc.im;
+      ++kb;
+    } else {
+      sreal += fc.re;
+    }
+  }
+  B.base = base;
+  B.kb = kb;
+  B.sreal = sreal;
+  B.ncol = B.w << kb;
+}
+
+// cp.async of a block's rows (8-byte granules: rows start at any element)
+// and of its chunk's unit table
+TSG_DEVINL void issue_block(const FibreArgs& a, const Blk& B, int nunit, double* Y, int pitch,
+                            FibreUnit* su) {
+  const int nf = a.nf, w = B.w, nb = 1 << B.kb;
+  const int tot = nf * nb * w;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int row = e / w, r = e - row * w;
+    const int i = row / nb, b = row - i * nb;
+    cp_async8(Y + static_cast<size_t>(i) * pitch + b * w + r, a.X + goff(B, b * w, i, a.sf) + r, 8);
+  }
+  const char* src = reinterpret_cast<const char*>(a.units + B.njob);
+  char* dst = reinterpret_cast<char*>(su);
+  for (int e = threadIdx.x; e < nunit * static_cast<int>(sizeof(FibreUnit) / 8); e += blockDim.x)
+    cp_async8(dst + 8 * e, src + 8 * e, 8);
+  cp_async_commit();
+}
+
+template <int NF>
+__global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const FibreArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int nf = a.nf;
+  const int ybuf = a.maxcol * nf;
+  double* sT = sm;                      // NF x NF, row-major, zero padded
+  double* sfc = sT + NF * NF;           // per row: code, a, omega
+  double* Ys[2] = {sfc + 3 * NF, sfc + 3 * NF + ybuf};
+  FibreUnit* sus[2] = {reinterpret_cast<FibreUnit*>(Ys[1] + ybuf),
+                       reinterpret_cast<FibreUnit*>(Ys[1] + ybuf) + kMaxUnits};
+  FibreCell* scell = a.cell_smem ? reinterpret_cast<FibreCell*>(sus[1] + kMaxUnits) : nullptr;
+  __shared__ SmallBuf SB[2];
+  __shared__ int soff[kFibreMaxS + 1];
+  __shared__ int64_t s_next;
+  pdl_wait();
+  for (int e = threadIdx.x; e < NF * NF; e += blockDim.x) {
+    const int i = e / NF, j = e - i * NF;
+    sT[e] = (i < nf && j < nf) ? a.Tt[i * nf + j] : 0.0;
+  }
+  for (int i = threadIdx.x; i < NF; i += blockDim.x) {
+    sfc[3 * i] = i < nf ? a.fcell[4 * i] : 0.0;
+    sfc[3 * i + 1] = i < nf ? a.fcell[4 * i + 1] : 0.0;
+    sfc[3 * i + 2] = i < nf ? a.fcell[4 * i + 2] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int s = 0; s < a.ns; ++s) {
+      soff[s] = o;
+      o += a.ncell[s];
+    }
+    soff[a.ns] = o;
+  }
+  __syncthreads();
+  if (scell)
+    for (int s = 0; s < a.ns; ++s)
+      for (int c = threadIdx.x; c < a.ncell[s]; c += blockDim.x) scell[soff[s] + c] = a.cells[s][c];
+  if (threadIdx.x == 0) {
+    const int64_t b0 = atomicAdd(a.counter, 1);
+    SB[0].blk = b0;
+    if (b0 < a.nblocks) decode_block(a, nullptr, soff, b0, SB[0].B, SB[0].nunit);
+  }
+  __syncthreads();
+  if (SB[0].blk < a.nblocks) issue_block(a, SB[0].B, SB[0].nunit, Ys[0], SB[0].B.ncol, sus[0]);
+  int cur = 0;
+  for (;;) {
+    SmallBuf& C = SB[cur];
+    if (C.blk >= a.nblocks) break;
+    // prefetch the next block into the other buffer
+    SmallBuf& Nx = SB[cur ^ 1];
+    if (threadIdx.x == 0) {
+      const int64_t nb = atomicAdd(a.counter, 1);
+      Nx.blk = nb;
+      if (nb < a.nblocks) decode_block(a, scell, soff, nb, Nx.B, Nx.nunit);
+    }
+    __syncthreads();
+    const bool more = Nx.blk < a.nblocks;
+    if (more) {
+      issue_block(a, Nx.B, Nx.nunit, Ys[cur ^ 1], Nx.B.ncol, sus[cur ^ 1]);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const Blk& B = C.B;
+    const int ncol = B.ncol, w = B.w, kb = B.kb, nunit = C.nunit;
+    double* Y = Ys[cur];
+    const FibreUnit* su = sus[cur];
+    if (threadIdx.x == 0) {
+      const int c2 = 1 << kb, c1 = kb ? 1 << (kb - 1) : 1;
+      for (int u = 0; u <= nunit; ++u) {
+        const int npb = u < nunit ? su[u].npair_before : su[nunit - 1].npair_before + su[nunit - 1].pair0;
+        C.job0[u] = npb * c2 + (u - npb) * c1;
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nunit * nf; e += blockDim.x) {
+      const int u = e / nf, i = e - u * nf;
+      const int k = kb + su[u].pair0;
+      if (k >= 2) unit_butterfly<false>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
+    }
+    __syncthreads();
+    const int njob = C.job0[nunit];
+    for (int j = threadIdx.x; j < njob; j += blockDim.x) {
+      int lo = 0, hi = nunit - 1;  // last unit with job0 <= j
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (C.job0[mid] <= j) lo = mid;
+        else hi = mid - 1;
+      }
+      const int u = lo;
+      const int pair0 = su[u].pair0, k = kb + pair0, rl0 = su[u].rl0;
+      const int l = (j - C.job0[u]) << 1;
+      const int re = ucol(l, rl0, pair0, w);
+      const int im = k ? ucol(l | 1, rl0, pair0, w) : -1;
+      double sr = B.sreal + su[u].sr, si = su[u].si;
+      for (int t = 0; t < kb; ++t) {
+        const int bit = pair0 ? t + 1 : t;
+        sr += B.bre[t];
+        si += ((l >> bit) & 1) ? B.bim[t] : -B.bim[t];
+      }
+      solve_job_reg<NF>(a, sT, sfc, Y, ncol, re, im, sr, si, goff(B, re, 0, a.sf));
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nunit * nf; e += blockDim.x) {
+      const int u = e / nf, i = e - u * nf;
+      const int k = kb + su[u].pair0;
+      if (k >= 2) unit_butterfly<true>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
+    }
+    __syncthreads();
+    {
+      const int nb = 1 << kb;
+      const int tot = nf * nb * w;
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int row = e / w, r = e - row * w;
+        const int i = row / nb, b = row - i * nb;
+        a.X[goff(B, b * w, i, a.sf) + r] = Y[static_cast<size_t>(i) * ncol + b * w + r];
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  pdl_trigger();
+}
+
+// ---- large free modes: blocked back substitution on DMMA ---------------------
+// Rows of f are processed in blocks of <= 8 (never splitting a 2x2 cell,
+// FibreArgs::rb), bottom-up.  Block [i0, i1): the update
+//     Y[i0:i1, :] -= T_f[i0:i1, i1:nf] Y[i1:nf, :]
+// runs on DMMA m8n8k4 over all columns of the shared tile (re and im parts
+// are just columns: T_f is real), four independent accumulator chains per
+// warp; then every job back-substitutes its <= 8 rows with its own shift.
+constexpr int kBigThreads = 256;
+
+template <bool GS>
+__global__ void __launch_bounds__(kBigThreads, 2) fibre_big_kernel(const FibreArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int nf = a.nf;
+  const int pitch = a.pitch;
+  double* Y = sm;
+  double* jsr = Y + static_cast<size_t>(nf) * pitch;
+  double* jsi = jsr + a.maxcol;
+  int* jre = reinterpret_cast<int*>(jsi + a.maxcol);
+  int* jim = jre + a.maxcol;
+  FibreUnit* su = reinterpret_cast<FibreUnit*>((reinterpret_cast<uintptr_t>(jim + a.maxcol) + 15) & ~uintptr_t{15});
+  FibreCell* scell = a.cell_smem ? reinterpret_cast<FibreCell*>(su + kMaxUnits) : nullptr;
+  __shared__ SmallBuf SB;
+  __shared__ int soff[kFibreMaxS + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int s = 0; s < a.ns; ++s) {
+      soff[s] = o;
+      o += a.ncell[s];
+    }
+    soff[a.ns] = o;
+  }
+  __syncthreads();
+  if (scell)
+    for (int s = 0; s < a.ns; ++s)
+      for (int c = threadIdx.x; c < a.ncell[s]; c += blockDim.x) scell[soff[s] + c] = a.cells[s][c];
+  for (;;) {
+    if (threadIdx.x == 0) {
+      SB.blk = atomicAdd(a.counter, 1);
+      if (SB.blk < a.nblocks) decode_block(a, scell, soff, SB.blk, SB.B, SB.nunit);
+    }
+    __syncthreads();
+    if (SB.blk >= a.nblocks) break;
+    const Blk& B = SB.B;
+    const int nunit = SB.nunit;
+    issue_block(a, B, nunit, Y, pitch, su);
+    cp_async_wait<0>();
+    __syncthreads();
+    const int ncol = B.ncol, w = B.w, kb = B.kb;
+    if (threadIdx.x == 0) {
+      const int c2 = 1 << kb, c1 = kb ? 1 << (kb - 1) : 1;
+      for (int u = 0; u <= nunit; ++u) {
+        const int npb = u < nunit ? su[u].npair_before : su[nunit - 1].npair_before + su[nunit - 1].pair0;
+        SB.job0[u] = npb * c2 + (u - npb) * c1;
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nunit * nf; e += blockDim.x) {
+      const int u = e / nf, i = e - u * nf;
+      const int k = kb + su[u].pair0;
+      if (k >= 2) unit_butterfly<false>(Y, pitch, i, su[u].rl0, k, su[u].pair0, w);
+    }
+    const int njob = SB.job0[nunit];
+    for (int j = threadIdx.x; j < njob; j += blockDim.x) {
+      int lo = 0, hi = nunit - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (SB.job0[mid] <= j) lo = mid;
+        else hi = mid - 1;
+      }
+      const int u = lo;
+      const int pair0 = su[u].pair0, k = kb + pair0, rl0 = su[u].rl0;
+      const int l = (j - SB.job0[u]) << 1;
+      jre[j] = ucol(l, rl0, pair0, w);
+      jim[j] = k ? ucol(l | 1, rl0, pair0, w) : -1;
+      double sr = B.sreal + su[u].sr, si = su[u].si;
+      for (int t = 0; t < kb; ++t) {
+        const int bit = pair0 ? t + 1 : t;
+        sr += B.bre[t];
+        si += ((l >> bit) & 1) ? B.bim[t] : -B.bim[t];
+      }
+      jsr[j] = sr;
+      jsi[j] = si;
+    }
+    __syncthreads();
+    const int ntile = (ncol + 7) >> 3;
+    for (int rb = a.nrb - 1; rb >= 0; --rb) {
+      const int i0 = a.rb[rb], i1 = a.rb[rb + 1];
+      if (i1 < nf) {
+        const int ra = i0 + g;
+        const bool arow = ra < i1;
+        const double* trow = a.Tt + static_cast<size_t>(arow ? ra : i0) * nf;
+        for (int nt = warp; nt < ntile; nt += nw) {
+          const int n0 = nt << 3;
+          const int bc = n0 + g < ncol ? n0 + g : 0;
+          const bool bok = n0 + g < ncol;
+          double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+          for (int k = i1; k < nf; k += 16) {
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+              const int kk = k + 4 * ch;
+              if (kk < nf) {
+                const int kr = kk + t4;
+                const bool kin = kr < nf;
+                const double av = (arow && kin) ? __ldg(trow + kr) : 0.0;
+                const double bv = (bok && kin) ? Y[static_cast<size_t>(kr) * pitch + bc] : 0.0;
+                dmma(c[ch][0], c[ch][1], av, bv);
+              }
+            }
+          }
+          const double s0 = (c[0][0] + c[1][0]) + (c[2][0] + c[3][0]);
+          const double s1 = (c[0][1] + c[1][1]) + (c[2][1] + c[3][1]);
+          const int col = n0 + 2 * t4;
+          if (arow) {
+            double* yr = Y + static_cast<size_t>(ra) * pitch;
+            if (col < ncol) yr[col] -= s0;
+            if (col + 1 < ncol) yr[col + 1] -= s1;
+          }
+        }
+        __syncthreads();
+      }
+      // per job: back substitution inside [i0, i1)
+      for (int j = threadIdx.x; j < njob; j += blockDim.x) {
+        const int re = jre[j], im = jim[j];
+        const double sr = jsr[j], si = jsi[j];
+        const bool cx = im >= 0;
+        bool bad = false;
+        for (int i = i1 - 1; i >= i0;) {
+          const double* fc = a.fcell + 4 * i;
+          const double* ti = a.Tt + static_cast<size_t>(i) * nf;
+          if (fc[0] == 2.0 && i - 1 >= i0) {
+            const int i0r = i - 1;
+            const double* t0 = a.Tt + static_cast<size_t>(i0r) * nf;
+            double ar = Y[i0r * pitch + re], ai = cx ? Y[i0r * pitch + im] : 0.0;
+            double br = Y[i * pitch + re], bi = cx ? Y[i * pitch + im] : 0.0;
+            for (int jj = i + 1; jj < i1; ++jj) {
+              const double zr = Y[jj * pitch + re], zi = cx ? Y[jj * pitch + im] : 0.0;
+              ar = fma(-t0[jj], zr, ar);
+              ai = fma(-t0[jj], zi, ai);
+              br = fma(-ti[jj], zr, br);
+              bi = fma(-ti[jj], zi, bi);
+            }
+            const double m00r = t0[i0r] + sr, m11r = ti[i] + sr, m01 = t0[i], m10 = ti[i0r];
+            const double detr = m00r * m11r - si * si - m01 * m10, deti = si * (m00r + m11r);
+            const double ea = fc[1] + sr, ew = fc[2];
+            bad = bad || fmin(hypot(ea, si + ew), hypot(ea, si - ew)) <= a.tiny;
+            const double nar = m11r * ar - si * ai - m01 * br, nai = m11r * ai + si * ar - m01 * bi;
+            const double nbr = m00r * br - si * bi - m10 * ar, nbi = m00r * bi + si * br - m10 * ai;
+            const double dd = detr * detr + deti * deti, ir = detr / dd, ii = -deti / dd;
+            Y[i0r * pitch + re] = nar * ir - nai * ii;
+            Y[i * pitch + re] = nbr * ir - nbi * ii;
+            if (cx) {
+              Y[i0r * pitch + im] = nar * ii + nai * ir;
+              Y[i * pitch + im] = nbr * ii + nbi * ir;
+            }
+            i -= 2;
+          } else {
+            double rr = Y[i * pitch + re], ri = cx ? Y[i * pitch + im] : 0.0;
+            for (int jj = i + 1; jj < i1; ++jj) {
+              const double zr = Y[jj * pitch + re];
+              rr = fma(-ti[jj], zr, rr);
+              if (cx) ri = fma(-ti[jj], Y[jj * pitch + im], ri);
+            }
+            const double dr = ti[i] + sr, dd = dr * dr + si * si;
+            bad = bad || sqrt(dd) <= a.tiny;
+            Y[i * pitch + re] = (rr * dr + ri * si) / dd;
+            if (cx) Y[i * pitch + im] = (ri * dr - rr * si) / dd;
+            i -= 1;
+          }
+        }
+        if (bad) {
+          const int64_t off = goff(B, re, i0, a.sf);
+          atomicMin(a.status, static_cast<int>(off < INT_MAX - 1 ? off : INT_MAX - 1));
+        }
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < nunit * nf; e += blockDim.x) {
+      const int u = e / nf, i = e - u * nf;
+      const int k = kb + su[u].pair0;
+      if (k >= 2) unit_butterfly<true>(Y, pitch, i, su[u].rl0, k, su[u].pair0, w);
+    }
+    __syncthreads();
+    {
+      const int nb = 1 << kb;
+      for (int row = warp; row < nf * nb; row += nw) {
+        const int i = row / nb, b = row - i * nb;
+        double* dst = a.X + goff(B, b * w, i, a.sf);
+        const double* src = Y + static_cast<size_t>(i) * pitch + b * w;
+        for (int r = lane; r < w; r += 32) dst[r] = src[r];
+      }
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
+template <typename K>
+cudaError_t launch_k(K k, const FibreArgs& a, size_t smem, int device, cudaStream_t st,
+                     SolveLaunchInfo* info, int threads = kThreads) {
+  // per (kernel, device): the shared-memory opt-in; per device: the SM count
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> attr_smem;
+  static std::map<int, int> nsm;
+  int grid = 0, occ = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    int& ns = nsm[device];
+    if (!ns) {
+      cudaError_t e = cudaDeviceGetAttribute(&ns, cudaDevAttrMultiProcessorCount, device);
+      if (e != cudaSuccess) return e;
+    }
+    size_t& at = attr_smem[{reinterpret_cast<const void*>(k), device}];
+    if (smem > at) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      at = smem;
+    }
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    grid = ns * occ;
+  }
+  if (a.nblocks < grid) grid = static_cast<int>(a.nblocks > 0 ? a.nblocks : 1);
+  if (info) *info = SolveLaunchInfo{grid, threads, static_cast<int>(smem), occ};
+  return launch_pdl(k, grid, threads, smem, st, a);
+}
+
+template <int NF>
+cudaError_t launch_small(const FibreArgs& a, int device, cudaStream_t st, SolveLaunchInfo* info) {
+  const size_t smem = (static_cast<size_t>(NF) * NF + 3 * NF + 2 * static_cast<size_t>(a.maxcol) * a.nf) * sizeof(double) +
+                      2 * kMaxUnits * sizeof(FibreUnit) + (a.cell_smem ? a.cell_smem : 0) * sizeof(FibreCell);
+  return launch_k(fibre_small_kernel<NF>, a, smem, device, st, info, kSmallThreads);
+}
+
+}  // namespace
+
+int fibre_pitch(int maxcol) { return ((maxcol + 11) / 16) * 16 + 4; }
+size_t fibre_big_smem(int nf, int maxcol, int cell_smem) {
+  return static_cast<size_t>(nf) * fibre_pitch(maxcol) * sizeof(double) +
+         static_cast<size_t>(maxcol) * (2 * sizeof(double) + 2 * sizeof(int)) + 16 +
+         kMaxUnits * sizeof(FibreUnit) + static_cast<size_t>(cell_smem) * sizeof(FibreCell);
+}
+
+bool fibre_small_ok(int nf, int chunk_w) { return nf <= 24 && chunk_w <= kMaxUnits; }
+
+cudaError_t launch_fibre_solve(const FibreArgs& a, int device, cudaStream_t st, SolveLaunchInfo* info) {
+  int wmax = a.maxcol;  // chunk width bound (maxcol = wmax << nsc)
+  (void)wmax;
+  if (a.nf <= 24 && a.small) {
+    if (a.nf <= 8) return launch_small<8>(a, device, st, info);
+    if (a.nf <= 16) return launch_small<16>(a, device, st, info);
+    return launch_small<24>(a, device, st, info);
+  }
+  if (a.big) {
+    const size_t smem = fibre_big_smem(a.nf, a.maxcol, a.cell_smem);
+    return launch_k(fibre_big_kernel<false>, a, smem, device, st, info, kBigThreads);
+  }
+  const size_t smem = (static_cast<size_t>(a.nf <= kTsmemMax ? a.nf * a.nf : 0) +
+                       static_cast<size_t>(a.maxcol) * a.nf) * sizeof(double) +
+                      static_cast<size_t>(a.maxcol) * sizeof(int);
+  return launch_k(fibre_solve_kernel, a, smem, device, st, info);
+}
+
+}  // namespace tsg

@@ -76,6 +76,12 @@ class Plan:
         lib().tsg_plan_info(self.h, ctypes.byref(nt), ext, ctypes.byref(fa))
         return dict(n_tiles=nt.value, tile=list(ext)[:len(self.dims)], flops_alg=fa.value)
 
+    def describe(self) -> str:
+        """The reduced-solve kernel this plan runs (tsg_plan_describe)."""
+        buf = ctypes.create_string_buffer(160)
+        lib().tsg_plan_describe(self.h, buf, 160)
+        return buf.value.decode()
+
     def execute_device(self, b_ptr: int, x_ptr: int) -> TsgReport:
         rep = TsgReport()
         rc = lib().tsg_plan_execute(self.h, ctypes.c_void_p(b_ptr), ctypes.c_void_p(x_ptr), 1,

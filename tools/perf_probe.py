@@ -46,7 +46,7 @@ def run(name, reps, tile=None, check=False):
     sn = sum(dims)
     f_tr = 4.0 * N * sn
     f_solve = info["flops_alg"] - f_tr
-    print(f"{name} dims={dims} tiles={info['n_tiles']} tile={info['tile']} gen={t1-t0:.1f}s setup={t2-t1:.1f}s")
+    print(f"{name} dims={dims} tiles={info['n_tiles']} tile={info['tile']} solve={plan.describe()} gen={t1-t0:.1f}s setup={t2-t1:.1f}s")
     print(f"   fwd {best[0]:.3f} ms ({f_tr/2/best[0]/1e9:.1f} TF)  solve {best[1]:.3f} ms "
           f"({f_solve/best[1]/1e9:.1f} TF alg)  back {best[2]:.3f} ms ({f_tr/2/best[2]/1e9:.1f} TF)  "
           f"total {best[3]:.3f} ms -> {info['flops_alg']/best[3]/1e9:.2f} TF = "
