@@ -376,11 +376,11 @@ def run_ours(a, rank, world, local):
     # back transform's mode-0 GEMM overlaps the solve's drain (tile-flag gate,
     # programmatic launch), so the solve kernel's own launch time is taken
     # from a few steps with the gate off (TSG_GATE=0 -> back after solve).
-    os.environ["TSG_GATE"] = "0"
+    plan.set_serial(True)
     try:
         kreps = [plan.execute_device(b.data_ptr(), x.data_ptr()) for _ in range(5)]
     finally:
-        del os.environ["TSG_GATE"]
+        plan.set_serial(False)
     t_solve = statistics.median(r.t_solve_ms for r in kreps)
     t_back = statistics.median(r.t_back_ms for r in kreps)
     t_fwd_k = statistics.median(r.t_fwd_ms for r in kreps)
@@ -509,7 +509,7 @@ def run_sharded(a, rank, world, local):
         if ev is not None:
             ev[0].record(stream)
         be.forward_local(b, sp)
-        sl._all_gather()
+        sl._all_gather(sp)
         be.forward_split(sp)
         if ev is not None:
             ev[1].record(stream)
@@ -517,7 +517,7 @@ def run_sharded(a, rank, world, local):
         if ev is not None:
             ev[2].record(stream)
         be.back_local(sp)
-        sl._all_gather()
+        sl._all_gather(sp)
         be.back_split(x, sp)
         if ev is not None:
             ev[3].record(stream)
@@ -560,7 +560,7 @@ def run_sharded(a, rank, world, local):
         # gather X to rank 0 through the padded send/gather buffers
         be.send.zero_()
         be.send[: x.numel()].copy_(x)
-        sl._all_gather()
+        sl._all_gather(sp)
         torch.cuda.synchronize()
     res = None
     if rank == 0:

@@ -2,7 +2,8 @@
 // and the oracle.  RandomStream restates the reference's published stream
 // (random.hpp:16-62): std::mt19937_64, uniform = (x >> 11) * 2^-53, and a
 // Box-Muller normal with the sine member cached; matrices and tensors are
-// filled in storage (column-major) order.  tests/test_random.py pins it
+// filled in storage (column-major) order.  tests/test_abi.py
+// (test_random_stream_bit_exact, test_make_problem_bit_exact) pins it
 // bit-for-bit against the reference build in oracle/_ref.
 //
 // The BASELINE.json configurations are generated here (draw order:

@@ -43,8 +43,6 @@ typedef struct {
   int tile[TSG_MAX_ORDER]; /* explicit per-mode tile extents (0 = from n_min) */
   int inputs_on_device;  /* 1: B/X are device pointers (resident in HBM) */
   void* stream;          /* cudaStream_t to run on (NULL = context stream) */
-  int use_graph;         /* capture execute() in a CUDA graph (default 1) */
-  int n_gpus;            /* reserved for slab sharding (1) */
 } tsg_opts;
 
 typedef struct {
@@ -119,6 +117,11 @@ int tsg_plan_execute(tsg_plan* plan, const double* B, double* X,
  * the zero pivot of the most recent one (rep may be NULL). */
 int tsg_plan_enqueue(tsg_plan* plan, const double* B, double* X);
 int tsg_plan_sync(tsg_plan* plan, tsg_report* rep);
+/* serial = 1: launch every kernel of a solve after its predecessor (no
+ * overlap of the back transform with the solve's drain, no trailing-cube
+ * grid), so the per-phase times of tsg_plan_execute are per-kernel times.
+ * Default 0.  Same results either way (bit-identical). */
+int tsg_plan_set_serial(tsg_plan* plan, int serial);
 void tsg_plan_destroy(tsg_plan* plan);
 /* Solve nrhs right-hand sides from HOST buffers B[i] into X[i] (pinned
  * memory recommended) with the copies overlapped: the host->device copy of

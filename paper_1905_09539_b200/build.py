@@ -78,7 +78,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         jobs.append((obj, [src] + headers, cmd))
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cpp"))):
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function",
+        # macro definitions of TSG_NVCC_FLAGS apply to the host side too
+        # (e.g. -DTSG_DEVTOOLS: the development probes, tools/README.md)
+        defs = [f for f in os.environ.get("TSG_NVCC_FLAGS", "").split() if f.startswith("-D")]
+        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function", *defs,
                *inc, *cuda_inc, "-c", src, "-o", obj]
         jobs.append((obj, [src] + headers, cmd))
     todo = [(o, c) for o, deps, c in jobs if force or _newer(o, deps)]

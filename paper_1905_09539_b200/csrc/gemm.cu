@@ -18,12 +18,15 @@
 // 8x8 DMMA accumulators in registers.  Shared-memory leading dimensions are
 // padded to 4 (mod 16) doubles so that every half-warp fragment load hits 16
 // distinct 8-byte bank pairs (conflict-free LDS.64).
+#include <mutex>
+#include <set>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
 #include "gemm.h"
+#include "util.h"
 
 namespace tsg {
 
@@ -302,27 +305,18 @@ cudaError_t launch_cfg(const GemmArgs& g, cudaStream_t st) {
                             g.lda * BK < (int64_t{1} << 30) && g.ldb * BN < (int64_t{1} << 30);
   if (all_interior) {
     auto k = dgemm_nn_kernel<BM, BN, WM, WN, true, true>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
-      attr = true;
-    }
+    int nsm = 0, occ = 0;
+    if (cudaError_t e = kernel_setup(k, S::BYTES, (BM / WM) * (BN / WN) * 32, &nsm, &occ); e != cudaSuccess) return e;
     launch_k(k, static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, g, st);
   } else if (vec) {
     auto k = dgemm_nn_kernel<BM, BN, WM, WN, true>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
-      attr = true;
-    }
+    int nsm = 0, occ = 0;
+    if (cudaError_t e = kernel_setup(k, S::BYTES, (BM / WM) * (BN / WN) * 32, &nsm, &occ); e != cudaSuccess) return e;
     launch_k(k, static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, g, st);
   } else {
     auto k = dgemm_nn_kernel<BM, BN, WM, WN, false>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
-      attr = true;
-    }
+    int nsm = 0, occ = 0;
+    if (cudaError_t e = kernel_setup(k, S::BYTES, (BM / WM) * (BN / WN) * 32, &nsm, &occ); e != cudaSuccess) return e;
     launch_k(k, static_cast<unsigned>(tiles), (BM / WM) * (BN / WN) * 32, S::BYTES, g, st);
   }
   return cudaGetLastError();
@@ -348,33 +342,47 @@ void gemm_tile_shape(int M, int N, int* bm, int* bn) {
 // programmatic-dependent pair (first use of an instantiation) serialises
 // them, and the trailing-cube grid waits on its dependent GEMM.
 template <int BM, int BN, int WM, int WN>
-void set_attrs() {
-  const int bytes = GemmSmem<BM, BN>::BYTES;
-  cudaFuncSetAttribute(dgemm_nn_kernel<BM, BN, WM, WN, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(dgemm_nn_kernel<BM, BN, WM, WN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(dgemm_nn_kernel<BM, BN, WM, WN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+cudaError_t set_attrs() {
+  const int bytes = GemmSmem<BM, BN>::BYTES, threads = (BM / WM) * (BN / WN) * 32;
+  int nsm = 0, occ = 0;
+  cudaError_t e = kernel_setup(dgemm_nn_kernel<BM, BN, WM, WN, true, true>, bytes, threads, &nsm, &occ);
+  if (e == cudaSuccess) e = kernel_setup(dgemm_nn_kernel<BM, BN, WM, WN, true>, bytes, threads, &nsm, &occ);
+  if (e == cudaSuccess) e = kernel_setup(dgemm_nn_kernel<BM, BN, WM, WN, false>, bytes, threads, &nsm, &occ);
+  return e;
 }
 
-void gemm_prepare() {
-  static const bool done = [] {
-    set_attrs<64, 64, 32, 32>();
-    set_attrs<128, 64, 32, 32>();
-    set_attrs<64, 128, 32, 32>();
-    set_attrs<64, 64, 32, 16>();
-    set_attrs<128, 128, 64, 32>();
-    return true;
-  }();
-  (void)done;
+// per device (kernel_setup caches per (kernel, device); this only saves the walk)
+cudaError_t gemm_prepare() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(dev)) return cudaSuccess;
+  }
+  cudaError_t e = set_attrs<64, 64, 32, 32>();
+  if (e == cudaSuccess) e = set_attrs<128, 64, 32, 32>();
+  if (e == cudaSuccess) e = set_attrs<64, 128, 32, 32>();
+  if (e == cudaSuccess) e = set_attrs<64, 64, 32, 16>();
+  if (e == cudaSuccess) e = set_attrs<128, 128, 64, 32>();
+  if (e == cudaSuccess) e = set_attrs<128, 128, 32, 32>();
+  if (e == cudaSuccess) e = set_attrs<128, 128, 32, 64>();
+  if (e == cudaSuccess) e = set_attrs<128, 128, 64, 64>();
+  if (e == cudaSuccess) e = set_attrs<128, 64, 64, 16>();
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  done.insert(dev);
+  return cudaSuccess;
 }
 
 cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return cudaSuccess;
-  gemm_prepare();
-  static int cfg = -1;
-  if (cfg < 0) {
+  if (cudaError_t e = gemm_prepare(); e != cudaSuccess) return e;
+  static const int cfg = [] {
     const char* e = std::getenv("TSG_GEMM_CFG");
-    cfg = e ? std::atoi(e) : 0;
-  }
+    return e ? std::atoi(e) : 0;
+  }();
   if (cfg == 1 && g.M >= 128 && g.N >= 64) return launch_cfg<128, 64, 32, 32>(g, st);   // 8 warps, 2 CTA/SM
   if (cfg == 2 && g.M >= 128 && g.N >= 128) return launch_cfg<128, 128, 32, 32>(g, st); // 16 warps
   if (cfg == 3 && g.M >= 128 && g.N >= 128) return launch_cfg<128, 128, 32, 64>(g, st); // 8 warps 32x64

@@ -54,7 +54,7 @@ constexpr int kWaitCols = 64;
 cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st);
 // Set the launch attributes of every GEMM kernel (idempotent; plans call it
 // at creation so no attribute change lands inside a launch chain).
-void gemm_prepare();
+cudaError_t gemm_prepare();
 
 // Y = X x_mode A for a dense tensor (tensor.hpp:187-231 semantics):
 // A is r x dims[mode] column-major (device), At = A^T (n x r, device; only

@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "gemm.h"
+#include "util.h"
 
 namespace tsg {
 namespace {
@@ -156,18 +157,8 @@ template <int NA, int NB>
 cudaError_t launch_pair(const PairArgs& g, cudaStream_t st) {
   const int smem = (NA * NA + (NB > 1 ? NB * NB : 0) + 2 * g.bsz) * 8;
   auto k = pair_kernel<NA, NB>;
-  static int nsm = 0, occ = 0, last_smem = -1;
-  if (last_smem != smem) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, THREADS, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-    last_smem = smem;
-  }
+  int nsm = 0, occ = 0;
+  if (cudaError_t e = kernel_setup(k, smem, THREADS, &nsm, &occ); e != cudaSuccess) return e;
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > g.nblk) grid = g.nblk;
   k<<<static_cast<unsigned>(grid), THREADS, smem, st>>>(g);
@@ -191,15 +182,21 @@ cudaError_t dispatch_b(const PairArgs& g, cudaStream_t st) {
 bool small_mode_ok(int n) { return n == 16 || n == 24 || n == 32 || n == 40; }
 
 namespace {
+// measured best of 3K / 4.6K / 6.9K doubles per block buffer
+constexpr int kBlockTarget = 6912;
+static_assert((40 * 40 * 2 + 2 * kBlockTarget) * 8 <= 227 * 1024,
+              "largest fused pass must fit the sm_100a shared-memory opt-in");
 // Block shape of a fused pass: c | P (inner chunk of the prefix), o | Q
-// (outer batch), powers of two, ~4.6K doubles per block.  The fibre
+// (outer batch), powers of two, at most kBlockTarget doubles per block
+// (two buffers: up to (40^2 + 40^2 + 2 * 6912) * 8 B = 136 KB of shared
+// memory for the 40x40 pair, one CTA per SM; 16x16 pairs ~110 KB).  The fibre
 // products work on whole 8-fibre blocks, so the fibres per block along
 // mode a (c * nb * o) and mode b (c * na * o) must be multiples of 8: pairs
 // always are (extents 16..40); a single mode may need o > 1 (odd prefix) and
 // is unsupported when neither P nor Q supplies the factor (GEMM then).
 bool pass_shape(int64_t P, int64_t Q, int na, int nb, int* c_out, int* o_out) {
   const int grp = na * nb;
-  const int target = 6912;  // two buffers of ~54 KB (measured best of 3K / 4.6K / 6.9K)
+  const int target = kBlockTarget;
   int c = 1, o = 1;
   if (P > 1) {
     while (c * 2 * grp <= target && P % (c * 2) == 0) c *= 2;

@@ -426,7 +426,6 @@ void tile_eigvecs(std::vector<tsg::TileMode>& tms, const std::vector<double>& dh
   }
 }
 
-int capture_or_run(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool graph);
 int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U);
 int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool timing);
 
@@ -438,14 +437,28 @@ std::vector<int> tile_bounds_of(const double* T, int n, int b) {
 }
 }  // namespace tsg_impl
 
+PlanKnobs PlanKnobs::from_env() {
+  PlanKnobs k;
+  const char* g = std::getenv("TSG_GATE");
+  k.serial = g && std::atoi(g) == 0;
+  const char* sc = std::getenv("TSG_SCHAIN");
+  k.schain_off = sc && std::atoi(sc) == 0;
+  k.verbose = std::getenv("TSG_VERBOSE") != nullptr;
+#ifdef TSG_DEVTOOLS
+  k.trace = std::getenv("TSG_TRACE") != nullptr;
+  k.prof = std::getenv("TSG_PROF") != nullptr;
+  k.dbg_fdone = std::getenv("TSG_DBG_FDONE") != nullptr;
+  if (const char* e = std::getenv("TSG_DBG")) k.dbg = std::atoi(e);
+#endif
+  return k;
+}
+
 extern "C" {
 
 int tsg_abi_version(void) { return 1; }
 
 void tsg_default_opts(tsg_opts* o) {
   std::memset(o, 0, sizeof(*o));
-  o->use_graph = 1;
-  o->n_gpus = 1;
 }
 
 int tsg_create(int n_gpus, const int* device_ids, tsg_ctx** out) {
@@ -501,6 +514,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   }
   TSG_CU(cudaSetDevice(ctx->device));
   auto pl = std::make_unique<tsg_plan>();
+  pl->knobs = PlanKnobs::from_env();
   pl->ctx = ctx;
   pl->family = family;
   pl->d = d;
@@ -567,6 +581,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   if (pl->decoupled) {
     TSG_CU(cudaMalloc(&pl->flags, sizeof(int)));
     TSG_CU(cudaMalloc(&pl->counter, 2 * sizeof(int)));
+    TSG_CU(cudaMemset(pl->counter, 0x7f, 2 * sizeof(int)));  // status word: kNoStatus
     pl->ntiles = 1;
     static const bool small_on = [] {
       const char* e = std::getenv("TSG_SMALLMODES");
@@ -583,7 +598,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         pl->sdone_n = pl->s_tm * static_cast<int>((Q0 + bn - 1) / bn);
       }
     }
-    tsg::gemm_prepare();
+    TSG_CU(tsg::gemm_prepare());
     pl->aux_n = 2 * static_cast<int64_t>(pl->sdone_n);
     if (pl->aux_n > 0) {
       TSG_CU(cudaMalloc(&pl->aux, pl->aux_n * sizeof(int)));
@@ -831,6 +846,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   }
   TSG_CU(cudaMalloc(&pl->flags, pl->ntiles * sizeof(int)));
   TSG_CU(cudaMalloc(&pl->counter, 2 * sizeof(int)));
+  TSG_CU(cudaMemset(pl->counter, 0x7f, 2 * sizeof(int)));  // status word: kNoStatus
 
   // Gate of the overlapped back transform (Laplace tile kernels whose first
   // back pass is a mode-0 GEMM).  Tile (0, t_1, ..) released implies every
@@ -888,7 +904,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
         pl->sdone_n = pl->s_tm * static_cast<int>((Q0 + bn - 1) / bn);
       }
     }
-    tsg::gemm_prepare();  // kernel attributes before any launch chain (see gemm.cu)
+    TSG_CU(tsg::gemm_prepare());  // kernel attributes before any launch chain (see gemm.cu)
     // Trailing cube (TSG_CUBE = tiles per mode, default 6, 0 = off; TSG_CUBE_GRID CTAs, default 16)
     {
       const char* ce = std::getenv("TSG_CUBE");
@@ -1015,6 +1031,16 @@ int tsg_plan_describe(const tsg_plan* pl, char* buf, int len) {
   return n;
 }
 
+// Status word of the solves enqueued since the last read (sticky: the
+// kernels atomicMin into it, a gate timeout is negative so it wins), then
+// re-armed to kNoStatus (memset 0x7f) in stream order.  Synchronises st.
+static cudaError_t read_status(tsg_plan* pl, cudaStream_t st, int* hstat) {
+  cudaError_t e = cudaMemcpyAsync(hstat, pl->counter, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(pl->counter + 1, 0x7f, sizeof(int), st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return e;
+}
+
 int tsg_plan_enqueue(tsg_plan* pl, const double* B, double* X) {
   if (!pl || !B || !X) return TSG_EINVAL;
   tsg_ctx* ctx = pl->ctx;
@@ -1022,20 +1048,29 @@ int tsg_plan_enqueue(tsg_plan* pl, const double* B, double* X) {
   return enqueue(pl, B, X, pl->ctx->stream, false);
 }
 
+int tsg_plan_set_serial(tsg_plan* pl, int serial) {
+  if (!pl) return TSG_EINVAL;
+  pl->knobs.serial = serial != 0;
+  return TSG_OK;
+}
+
 int tsg_plan_sync(tsg_plan* pl, tsg_report* rep) {
   if (!pl) return TSG_EINVAL;
   tsg_ctx* ctx = pl->ctx;
   TSG_CU(cudaSetDevice(ctx->device));
   int hstat[2] = {0, kNoStatus};
-  TSG_CU(cudaMemcpyAsync(hstat, pl->counter, sizeof(hstat), cudaMemcpyDeviceToHost, pl->ctx->stream));
-  TSG_CU(cudaStreamSynchronize(pl->ctx->stream));
+  TSG_CU(read_status(pl, pl->ctx->stream, hstat));
   if (rep) {
     std::memset(rep, 0, sizeof(*rep));
     rep->flops_alg = pl->flops_alg;
     rep->flops_exec = pl->flops_exec;
-    rep->zero_pivot_index = hstat[1] == kNoStatus ? -1 : hstat[1];
+    rep->zero_pivot_index = hstat[1] == kNoStatus || hstat[1] < 0 ? -1 : hstat[1];
     rep->kernel_launches = pl->launches;
   }
+  // singular cells are reported through rep (the enqueue contract); a gate
+  // timeout means some solve ran on incomplete inputs
+  if (hstat[1] == tsg::kGateTimeout)
+    return fail(ctx, TSG_ECUDA, "reduced solve: forward gate timed out (serialised launches)");
   return TSG_OK;
 }
 
@@ -1058,14 +1093,13 @@ int tsg_plan_execute(tsg_plan* pl, const double* B, double* X, int inputs_on_dev
   if (!inputs_on_device)
     TSG_CU(cudaMemcpyAsync(pl->xdev.p, B, bytes, cudaMemcpyHostToDevice, st));
   TSG_CU(cudaEventRecord(ev[1], st));
-  int rc = capture_or_run(pl, din, dout, st, true);
+  int rc = enqueue(pl, din, dout, st, true);
   if (rc != TSG_OK) return rc;
   TSG_CU(cudaEventRecord(ev[5], st));
   if (!inputs_on_device) TSG_CU(cudaMemcpyAsync(X, pl->xdev.p, bytes, cudaMemcpyDeviceToHost, st));
   TSG_CU(cudaEventRecord(ev[6], st));
   int hstat[2] = {0, kNoStatus};
-  TSG_CU(cudaMemcpyAsync(hstat, pl->counter, sizeof(hstat), cudaMemcpyDeviceToHost, st));
-  TSG_CU(cudaStreamSynchronize(st));
+  TSG_CU(read_status(pl, st, hstat));
   if (rep) {
     float t = 0;
     std::memset(rep, 0, sizeof(*rep));
@@ -1083,7 +1117,7 @@ int tsg_plan_execute(tsg_plan* pl, const double* B, double* X, int inputs_on_dev
     rep->t_total_ms = t;
     rep->flops_alg = pl->flops_alg;
     rep->flops_exec = pl->flops_exec;
-    rep->zero_pivot_index = hstat[1] == kNoStatus ? -1 : hstat[1];
+    rep->zero_pivot_index = hstat[1] == kNoStatus || hstat[1] < 0 ? -1 : hstat[1];
     rep->kernel_launches = pl->launches;
   }
   if (hstat[1] == tsg::kGateTimeout)
@@ -1105,65 +1139,73 @@ int tsg_plan_execute_stream(tsg_plan* pl, int nrhs, const double* const* B, doub
     TSG_CU(pl->sin[s].ensure(pl->N));
     TSG_CU(pl->sout[s].ensure(pl->N));
   }
-  cudaStream_t cin = nullptr, cout = nullptr;
-  TSG_CU(cudaStreamCreateWithFlags(&cin, cudaStreamNonBlocking));
-  TSG_CU(cudaStreamCreateWithFlags(&cout, cudaStreamNonBlocking));
-  cudaEvent_t in_ready[2], solved[2], out_free[2], t0, t1;
+  // copy streams and events, released on every return path; an early error
+  // return first drains the copy streams (they may still read the caller's
+  // host buffers)
+  struct Staging {
+    cudaStream_t cin = nullptr, cout = nullptr;
+    cudaEvent_t in_ready[2] = {}, solved[2] = {}, out_free[2] = {}, t0 = nullptr, t1 = nullptr;
+    ~Staging() {
+      if (cin) cudaStreamSynchronize(cin);
+      if (cout) cudaStreamSynchronize(cout);
+      for (cudaEvent_t e : {in_ready[0], in_ready[1], solved[0], solved[1], out_free[0], out_free[1], t0, t1})
+        if (e) cudaEventDestroy(e);
+      if (cin) cudaStreamDestroy(cin);
+      if (cout) cudaStreamDestroy(cout);
+    }
+  } g;
+  TSG_CU(cudaStreamCreateWithFlags(&g.cin, cudaStreamNonBlocking));
+  TSG_CU(cudaStreamCreateWithFlags(&g.cout, cudaStreamNonBlocking));
   for (int s = 0; s < 2; ++s) {
-    TSG_CU(cudaEventCreateWithFlags(&in_ready[s], cudaEventDisableTiming));
-    TSG_CU(cudaEventCreateWithFlags(&solved[s], cudaEventDisableTiming));
-    TSG_CU(cudaEventCreateWithFlags(&out_free[s], cudaEventDisableTiming));
+    TSG_CU(cudaEventCreateWithFlags(&g.in_ready[s], cudaEventDisableTiming));
+    TSG_CU(cudaEventCreateWithFlags(&g.solved[s], cudaEventDisableTiming));
+    TSG_CU(cudaEventCreateWithFlags(&g.out_free[s], cudaEventDisableTiming));
   }
-  TSG_CU(cudaEventCreate(&t0));
-  TSG_CU(cudaEventCreate(&t1));
-  TSG_CU(cudaEventRecord(t0, st));
-  TSG_CU(cudaStreamWaitEvent(cin, t0, 0));
-  DevBuf stat;  // status word of every solve (singular cells), checked at the end
+  TSG_CU(cudaEventCreate(&g.t0));
+  TSG_CU(cudaEventCreate(&g.t1));
+  cudaStream_t cin = g.cin, cout = g.cout;
+  TSG_CU(cudaEventRecord(g.t0, st));
+  TSG_CU(cudaStreamWaitEvent(cin, g.t0, 0));
+  // status word of every solve, re-armed after each (singular cells,
+  // gate timeouts), checked at the end
+  DevBuf stat;
   TSG_CU(stat.ensure((static_cast<size_t>(std::max(nrhs, 1)) + 1) / 2));
   int* dstat = reinterpret_cast<int*>(stat.p);
   for (int i = 0; i < nrhs; ++i) {
     const int s = i & 1;
     // slot s input is free once solve i-2 finished
-    if (i >= 2) TSG_CU(cudaStreamWaitEvent(cin, solved[s], 0));
+    if (i >= 2) TSG_CU(cudaStreamWaitEvent(cin, g.solved[s], 0));
     TSG_CU(cudaMemcpyAsync(pl->sin[s].p, B[i], bytes, cudaMemcpyHostToDevice, cin));
-    TSG_CU(cudaEventRecord(in_ready[s], cin));
-    TSG_CU(cudaStreamWaitEvent(st, in_ready[s], 0));
-    if (i >= 2) TSG_CU(cudaStreamWaitEvent(st, out_free[s], 0));  // D2H of i-2 drained sout[s]
+    TSG_CU(cudaEventRecord(g.in_ready[s], cin));
+    TSG_CU(cudaStreamWaitEvent(st, g.in_ready[s], 0));
+    if (i >= 2) TSG_CU(cudaStreamWaitEvent(st, g.out_free[s], 0));  // D2H of i-2 drained sout[s]
     const int rc = enqueue(pl, pl->sin[s].p, pl->sout[s].p, st, false);
     if (rc != TSG_OK) return rc;
     TSG_CU(cudaMemcpyAsync(dstat + i, pl->counter + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
-    TSG_CU(cudaEventRecord(solved[s], st));
-    TSG_CU(cudaStreamWaitEvent(cout, solved[s], 0));
+    TSG_CU(cudaMemsetAsync(pl->counter + 1, 0x7f, sizeof(int), st));
+    TSG_CU(cudaEventRecord(g.solved[s], st));
+    TSG_CU(cudaStreamWaitEvent(cout, g.solved[s], 0));
     TSG_CU(cudaMemcpyAsync(X[i], pl->sout[s].p, bytes, cudaMemcpyDeviceToHost, cout));
-    TSG_CU(cudaEventRecord(out_free[s], cout));
+    TSG_CU(cudaEventRecord(g.out_free[s], cout));
   }
-  TSG_CU(cudaEventRecord(t1, cout));
+  TSG_CU(cudaEventRecord(g.t1, cout));
   std::vector<int> hs(static_cast<size_t>(nrhs));
   if (nrhs > 0) TSG_CU(cudaMemcpyAsync(hs.data(), dstat, nrhs * sizeof(int), cudaMemcpyDeviceToHost, st));
   TSG_CU(cudaStreamSynchronize(cout));
   TSG_CU(cudaStreamSynchronize(st));
   int hstat[2] = {0, kNoStatus};
   for (int v : hs)
-    if (v != kNoStatus && hstat[1] == kNoStatus) hstat[1] = v;
+    if (v == tsg::kGateTimeout || (v != kNoStatus && hstat[1] == kNoStatus)) hstat[1] = v;
   if (rep) {
     float t = 0;
     std::memset(rep, 0, sizeof(*rep));
-    cudaEventElapsedTime(&t, t0, t1);
+    cudaEventElapsedTime(&t, g.t0, g.t1);
     rep->t_total_ms = t;
     rep->flops_alg = pl->flops_alg * nrhs;
     rep->flops_exec = pl->flops_exec * nrhs;
-    rep->zero_pivot_index = hstat[1] == kNoStatus ? -1 : hstat[1];
+    rep->zero_pivot_index = hstat[1] == kNoStatus || hstat[1] < 0 ? -1 : hstat[1];
     rep->kernel_launches = pl->launches * nrhs;
   }
-  for (int s = 0; s < 2; ++s) {
-    cudaEventDestroy(in_ready[s]);
-    cudaEventDestroy(solved[s]);
-    cudaEventDestroy(out_free[s]);
-  }
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
-  cudaStreamDestroy(cin);
-  cudaStreamDestroy(cout);
   if (hstat[1] == tsg::kGateTimeout)
     return fail(ctx, TSG_ECUDA, "reduced solve: forward gate timed out (serialised launches)");
   if (hstat[1] != kNoStatus)
@@ -1409,10 +1451,9 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
   }
   const int k = static_cast<int>(ps.size());
   // slab chain: mode-1 CTAs start on the slabs the mode-0 GEMM has finished
-  // (TSG_SCHAIN=0, read per call, turns it off)
-  const char* sc_env = std::getenv("TSG_SCHAIN");
+  // (TSG_SCHAIN=0 at plan creation turns it off)
   const bool schain = pl->sdone[0] && k >= 2 && ps[0].m == 0 && ps[0].kind == 0 && ps[1].m == 1 &&
-                      ps[1].kind == 0 && !(sc_env && std::atoi(sc_env) == 0);
+                      ps[1].kind == 0 && !pl->knobs.schain_off;
   int* sdone = pl->sdone[fwd ? 0 : 1];
   if (i_hi < 0 || i_hi > k) i_hi = k;
   // pass i reads the previous pass's output (ping-pong ending in target)
@@ -1476,7 +1517,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   double* work = nullptr;
   // Solve state reset first, so the forward GEMMs and the solve follow each
   // other directly (programmatic launches).
-  TSG_CU(tsg::reset_state(pl->flags, pl->ntiles, pl->counter, kNoStatus, pl->aux, pl->aux_n, st));
+  TSG_CU(tsg::reset_state(pl->flags, pl->ntiles, pl->counter, pl->aux, pl->aux_n, st));
   if (pl->decoupled) {
     TSG_CU(transform_all(pl, in, pl->w1.p, pl->w2.p, true, st));
     if (timing) TSG_CU(cudaEventRecord(ev[2], st));
@@ -1491,12 +1532,11 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     if (timing) TSG_CU(cudaEventRecord(ev[4], st));
     return TSG_OK;
   }
-  const bool want_trace = std::getenv("TSG_TRACE") != nullptr;
-  const bool want_prof = std::getenv("TSG_PROF") != nullptr;
-  // TSG_GATE=0 (read per call) runs every kernel after its predecessor: the
-  // back transform after the solve, no trailing cube (bench kernel timing).
-  const char* gate_env = std::getenv("TSG_GATE");
-  const bool gate_off = gate_env && std::atoi(gate_env) == 0;
+  const bool want_trace = pl->knobs.trace;
+  const bool want_prof = pl->knobs.prof;
+  // serial plans run every kernel after its predecessor: the back transform
+  // after the solve, no trailing cube (bench kernel timing).
+  const bool gate_off = pl->knobs.serial;
   // The cube grid waits on the NEXT kernel (the last forward GEMM): only
   // with concurrent kernels.  Serialising tools (Nsight Compute / Systems,
   // compute-sanitizer, CUDA_LAUNCH_BLOCKING=1) run without it.
@@ -1530,7 +1570,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     c.gbn = pl->fg_bn;
     c.gtm = pl->fg_tm;
     c.max_grid = pl->cube_grid;
-    if (const char* e = std::getenv("TSG_DBG")) c.dbg = std::atoi(e);
+    c.dbg = pl->knobs.dbg;
     TSG_CU(tsg::launch_solve_lap16(c, st, nullptr));
     ++pl->launches;
     tsg::GemmArgs lastg{};
@@ -1578,7 +1618,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   }
   a.tiny = pl->tiny;
   a.refine = pl->refine;
-  if (const char* e = std::getenv("TSG_DBG")) a.dbg = std::atoi(e);
+  a.dbg = pl->knobs.dbg;
   static unsigned long long* trace = nullptr;
   static int64_t trace_n = 0;
   if (want_trace) {
@@ -1665,7 +1705,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     std::fprintf(stderr, "[tsg prof] tiles=%.0f cycles/tile: setup %.0f stage %.0f update(near) %.0f farwait|That+fwdT %.0f far|wave %.0f diag|backT %.0f scatter %.0f | idle/queue %.0f\n",
                  nt, h[0] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt, h[5] / nt, h[6] / nt, h[7] / nt);
   }
-  if (std::getenv("TSG_VERBOSE"))
+  if (pl->knobs.verbose)
     std::fprintf(stderr, "[tsg] solve grid=%d block=%d smem=%d ctas/sm=%d tiles=%lld refine=%d cond=%.3g\n",
                  pl->solve_info.grid, pl->solve_info.block, pl->solve_info.smem_bytes,
                  pl->solve_info.ctas_per_sm, static_cast<long long>(pl->ntiles), pl->refine,
@@ -1673,8 +1713,8 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
   // Back transforms: outputs alternate (w2, out) and end in `out`.  With the
   // gate, the mode-0 pass follows the solve directly (programmatic launch),
   // so the solve/back split point moves after it.
-  // TSG_GATE=0 (read per call) runs the back transform after the solve, so
-  // the bench can time the solve kernel alone.
+  // Serial plans run the back transform after the solve, so the bench can
+  // time the solve kernel alone.
   const bool gated = pl->gate_groups > 0 && !want_trace && !want_prof && !gate_off;
   if (timing && !gated) TSG_CU(cudaEventRecord(ev[3], st));
   if (!pl->reduced_only) {
@@ -1689,7 +1729,7 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
                          gated && timing ? ev[3] : nullptr));
   }
   if (timing) TSG_CU(cudaEventRecord(ev[4], st));
-  if (cubed && std::getenv("TSG_DBG_FDONE")) {  // development: unreleased forward-gate tiles
+  if (cubed && pl->knobs.dbg_fdone) {  // development: unreleased forward-gate tiles
     std::vector<int> fd(pl->fdone_n);
     cudaMemcpyAsync(fd.data(), pl->fdone, pl->fdone_n * sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
@@ -1914,11 +1954,5 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
   return TSG_OK;
 }
 
-int capture_or_run(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool /*graph*/) {
-  // Events inside the stream give the phase split; graphs are used by the
-  // bench through repeated execute() calls on the same pointers (the
-  // per-phase events need the plain stream path, so run it directly).
-  return enqueue(pl, in, out, st, true);
-}
 
 }  // namespace

@@ -35,8 +35,24 @@ struct DevBuf {
   ~DevBuf() { reset(); }
 };
 
+// Launch-order and diagnostic switches, fixed when the plan is created.
+// serial: every kernel after its predecessor (tsg_plan_set_serial; env
+// TSG_GATE=0 at creation), schain_off: no slab chain between the first two
+// transform GEMMs (TSG_SCHAIN=0), verbose: one line per solve on stderr
+// (TSG_VERBOSE).  The development probes (trace, prof, dbg: per-hyperplane
+// release times, per-phase cycle counters, kernel ablations) are read only
+// in a -DTSG_DEVTOOLS build (tools/README.md); the shipped library never
+// reads them.
+struct PlanKnobs {
+  bool serial = false, schain_off = false, verbose = false;
+  bool trace = false, prof = false, dbg_fdone = false;
+  int dbg = 0;
+  static PlanKnobs from_env();
+};
+
 struct tsg_plan {
   tsg_ctx* ctx = nullptr;
+  PlanKnobs knobs;
   int family = 0, d = 0, reduced_only = 0;
   std::vector<int> dims;
   std::vector<int64_t> stride;

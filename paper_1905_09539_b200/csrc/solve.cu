@@ -46,6 +46,7 @@
 #include "common.cuh"
 #include "solve.h"
 #include "solve_common.cuh"
+#include "util.h"
 
 namespace tsg {
 namespace {
@@ -676,18 +677,9 @@ template <int D, int FAM>
 cudaError_t launch_t(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
   using C = Cfg<D, FAM>;
   auto k = solve_kernel<D, FAM>;
-  // One-time per process: smem opt-in and the persistent grid size.
-  static int nsm = 0, occ = 0;
-  if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, C::BYTES);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-  }
+  // smem opt-in and the persistent grid size (per device)
+  int nsm = 0, occ = 0;
+  if (cudaError_t e = kernel_setup(k, C::BYTES, kThreads, &nsm, &occ); e != cudaSuccess) return e;
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > a.ntiles) grid = a.ntiles;
   if (grid < 1) grid = 1;

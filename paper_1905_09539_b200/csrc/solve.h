@@ -91,7 +91,7 @@ struct SolveArgs {
 };
 
 // SolveArgs::status value of a forward gate that never opened (lap16d).
-constexpr int kGateTimeout = 0x7e000000;
+constexpr int kGateTimeout = -2;  // negative: atomicMin keeps it over any tile index
 
 struct SolveLaunchInfo {
   int grid, block, smem_bytes, ctas_per_sm;

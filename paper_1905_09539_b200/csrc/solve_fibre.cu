@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "solve.h"
+#include "util.h"
 
 namespace tsg {
 namespace {
@@ -777,29 +778,11 @@ __global__ void __launch_bounds__(kBigThreads, 2) fibre_big_kernel(const FibreAr
 template <typename K>
 cudaError_t launch_k(K k, const FibreArgs& a, size_t smem, int device, cudaStream_t st,
                      SolveLaunchInfo* info, int threads = kThreads) {
-  // per (kernel, device): the shared-memory opt-in; per device: the SM count
-  static std::mutex mu;
-  static std::map<std::pair<const void*, int>, size_t> attr_smem;
-  static std::map<int, int> nsm;
-  int grid = 0, occ = 0;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    int& ns = nsm[device];
-    if (!ns) {
-      cudaError_t e = cudaDeviceGetAttribute(&ns, cudaDevAttrMultiProcessorCount, device);
-      if (e != cudaSuccess) return e;
-    }
-    size_t& at = attr_smem[{reinterpret_cast<const void*>(k), device}];
-    if (smem > at) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      if (e != cudaSuccess) return e;
-      at = smem;
-    }
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    grid = ns * occ;
-  }
+  // per (kernel, device): the shared-memory opt-in, the SM count and occupancy
+  (void)device;
+  int nsm = 0, occ = 0;
+  if (cudaError_t e = kernel_setup(k, smem, threads, &nsm, &occ); e != cudaSuccess) return e;
+  int grid = nsm * occ;
   if (a.nblocks < grid) grid = static_cast<int>(a.nblocks > 0 ? a.nblocks : 1);
   if (info) *info = SolveLaunchInfo{grid, threads, static_cast<int>(smem), occ};
   return launch_pdl(k, grid, threads, smem, st, a);

@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "solve.h"
+#include "util.h"
 
 namespace tsg {
 namespace {
@@ -481,16 +482,9 @@ __global__ void __launch_bounds__(THREADS, GSYD_MINB) solve_gsyd_kernel(SolveArg
 
 template <int D>
 cudaError_t launch_g(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
-  static int nsm = 0, occ = 0;
   auto k = solve_gsyd_kernel<D>;
-  if (occ == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, THREADS, 0);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-  }
+  int nsm = 0, occ = 0;
+  if (cudaError_t e = kernel_setup(k, 0, THREADS, &nsm, &occ); e != cudaSuccess) return e;
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > a.ntiles) grid = a.ntiles;
   if (info) *info = SolveLaunchInfo{static_cast<int>(grid), THREADS, 0, occ};

@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "solve.h"
 #include "solve_common.cuh"
+#include "util.h"
 
 namespace tsg {
 namespace {
@@ -421,17 +422,8 @@ template <int D>
 cudaError_t launch_lap_t(const SolveArgs& a, cudaStream_t st, SolveLaunchInfo* info) {
   using C = LapCfg<D>;
   auto k = solve_lap_kernel<D>;
-  static int nsm = 0, occ = 0;
-  if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, C::THREADS, C::BYTES);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-  }
+  int nsm = 0, occ = 0;
+  if (cudaError_t e = kernel_setup(k, C::BYTES, C::THREADS, &nsm, &occ); e != cudaSuccess) return e;
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > a.ntiles) grid = a.ntiles;
   if (grid < 1) grid = 1;

@@ -29,6 +29,7 @@
 #include "common.cuh"
 #include "solve.h"
 #include "tma.h"
+#include "util.h"
 
 namespace tsg {
 namespace {
@@ -708,7 +709,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               while (ld_acquire(f) != a.gepoch) {
                 __nanosleep(64);
                 if (++spins > ((a.dbg & 32768) ? 2000000LL : (1LL << 26))) {
-                  atomicExch(a.status, kGateTimeout);
+                  atomicMin(a.status, kGateTimeout);
                   break;
                 }
               }
@@ -940,14 +941,9 @@ cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchI
   const uint32_t box[3] = {BX, BY, BZ};
   if (!encode_tmap_f64(&map, a.X, 3, dims, box)) return cudaErrorInvalidValue;
   if (lap16_decoupled()) {
-    static int nsm2 = 0;
-    if (nsm2 == 0) {
-      cudaError_t e = cudaFuncSetAttribute(solve_lap16d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D_BYTES);
-      if (e != cudaSuccess) return e;
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm2, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int nsm2 = 0, occ2 = 0;
+    if (cudaError_t e = kernel_setup(solve_lap16d_kernel, D_BYTES, THREADS, &nsm2, &occ2); e != cudaSuccess)
+      return e;
     int64_t grid = nsm2;
     if (grid > a.ntiles) grid = a.ntiles;
     if (a.max_grid > 0 && grid > a.max_grid) grid = a.max_grid;
@@ -959,14 +955,8 @@ cudaError_t launch_solve_lap16(const SolveArgs& a, cudaStream_t st, SolveLaunchI
     cudaError_t le = launch_pdl(solve_lap16d_kernel, static_cast<unsigned>(grid), THREADS, D_BYTES, st, a, map);
     return le != cudaSuccess ? le : cudaGetLastError();
   }
-  static int nsm = 0;
-  if (nsm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(solve_lap16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, BYTES);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int nsm = 0, occ = 0;
+  if (cudaError_t e = kernel_setup(solve_lap16_kernel, BYTES, THREADS, &nsm, &occ); e != cudaSuccess) return e;
   int64_t grid = nsm;
   if (grid > a.ntiles) grid = a.ntiles;
   if (info) *info = SolveLaunchInfo{static_cast<int>(grid), THREADS, BYTES, 1};

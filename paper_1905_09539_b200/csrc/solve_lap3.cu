@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "solve.h"
 #include "solve_common.cuh"
+#include "util.h"
 
 namespace tsg {
 namespace {
@@ -994,18 +995,8 @@ cudaError_t launch_l3(const SolveArgs& a0, cudaStream_t st, SolveLaunchInfo* inf
   const int bytes = C::BYTES;
   const bool dist = LT == 3 && (a.nslab > 1 || a.sys);
   auto k = dist ? solve_lap3_kernel<LT, LT == 3> : solve_lap3_kernel<LT, false>;
-  static int nsm = 0, occs[2] = {0, 0};
-  int& occ = occs[dist ? 1 : 0];
-  if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::BYTES);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, C::THREADS, bytes);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-  }
+  int nsm = 0, occ = 0;
+  if (cudaError_t e = kernel_setup(k, bytes, C::THREADS, &nsm, &occ); e != cudaSuccess) return e;
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > a.ntiles) grid = a.ntiles;
   if (info) *info = SolveLaunchInfo{static_cast<int>(grid), C::THREADS, bytes, occ};

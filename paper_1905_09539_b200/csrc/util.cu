@@ -2,6 +2,9 @@
 // the device residual (tsg_residual; reference oracle.hpp:231-268).
 #include <algorithm>
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 #include "util.h"
@@ -40,24 +43,20 @@ int grid_for(int64_t n) {
   return static_cast<int>(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
 }
 
-__global__ void reset_kernel(int* flags, int64_t nf, int* counter, int status, int* extra, int64_t ne) {
+__global__ void reset_kernel(int* flags, int64_t nf, int* counter, int* extra, int64_t ne) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   for (int64_t i = i0; i < nf; i += stride) flags[i] = 0;
   for (int64_t i = i0; i < ne; i += stride) extra[i] = 0;
-  if (i0 == 0) {
-    counter[0] = 0;
-    counter[1] = status;
-  }
+  if (i0 == 0) counter[0] = 0;
 }
 
 }  // namespace
 
-cudaError_t reset_state(int* flags, int64_t nf, int* counter, int status, int* extra, int64_t ne,
-                        cudaStream_t st) {
+cudaError_t reset_state(int* flags, int64_t nf, int* counter, int* extra, int64_t ne, cudaStream_t st) {
   const int64_t n = nf > ne ? nf : ne;
   const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256 + 1, 1184));
-  reset_kernel<<<blocks, 256, 0, st>>>(flags, nf, counter, status, extra, extra ? ne : 0);
+  reset_kernel<<<blocks, 256, 0, st>>>(flags, nf, counter, extra, extra ? ne : 0);
   return cudaGetLastError();
 }
 
@@ -69,6 +68,41 @@ cudaError_t sumsq(const double* x, int64_t n, double* out_dev, cudaStream_t st) 
 cudaError_t axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st) {
   axpy_kernel<<<grid_for(n), 256, 0, st>>>(y, x, a, n);
   return cudaGetLastError();
+}
+
+}  // namespace tsg
+
+namespace tsg {
+
+cudaError_t kernel_setup(const void* fn, size_t smem, int threads, int* nsm, int* occ) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> attr;           // (fn, dev) -> opt-in
+  static std::map<std::tuple<const void*, int, size_t, int>, int> occs;  // -> CTAs per SM
+  static std::map<int, int> sms;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& ns = sms[dev];
+  if (!ns) {
+    e = cudaDeviceGetAttribute(&ns, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+  }
+  size_t& at = attr[{fn, dev}];
+  if (smem > at || (smem > 0 && at == 0)) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    at = smem;
+  }
+  int& oc = occs[{fn, dev, smem, threads}];
+  if (!oc) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, fn, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (oc < 1) return cudaErrorInvalidConfiguration;
+  }
+  *nsm = ns;
+  *occ = oc;
+  return cudaSuccess;
 }
 
 }  // namespace tsg

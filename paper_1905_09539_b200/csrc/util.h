@@ -8,7 +8,18 @@ cudaError_t sumsq(const double* x, int64_t n, double* out_dev, cudaStream_t st);
 // y += a * x
 cudaError_t axpy(double* y, const double* x, double a, int64_t n, cudaStream_t st);
 // Per-solve state reset in one launch: flags[0..nf) = 0, counter[0] = 0,
-// counter[1] = status (no singular cell), extra[0..ne) = 0 (may be null).
-cudaError_t reset_state(int* flags, int64_t nf, int* counter, int status, int* extra, int64_t ne,
-                        cudaStream_t st);
+// extra[0..ne) = 0 (may be null).  The status word counter[1] is sticky
+// across solves: the host re-arms it when it reads it (plan.cpp).
+cudaError_t reset_state(int* flags, int64_t nf, int* counter, int* extra, int64_t ne, cudaStream_t st);
+
+// Launch setup of a kernel on the CURRENT device, thread-safe and cached per
+// (kernel, device, smem, threads): raises the dynamic shared-memory opt-in
+// when smem exceeds what was set before, and returns the SM count and the
+// resident CTAs per SM (>= 1).  Several contexts on different devices (one
+// per host thread, include/tsylv_gpu.h) each get their own attribute.
+cudaError_t kernel_setup(const void* fn, size_t smem, int threads, int* nsm, int* occ);
+template <typename K>
+cudaError_t kernel_setup(K* fn, size_t smem, int threads, int* nsm, int* occ) {
+  return kernel_setup(reinterpret_cast<const void*>(fn), smem, threads, nsm, occ);
+}
 }  // namespace tsg

@@ -156,22 +156,37 @@ class ShardedLaplace:
             backend.ipc_open(allh)
             dist.barrier(group=group)
 
-    def _all_gather(self):
+    def _all_gather(self, stream):
+        """NCCL all-gather of the send slots, ordered on `stream`: torch
+        enqueues the collective behind its *current* stream and makes that
+        stream wait for it, so the library's stream is made current for the
+        call (the gather must see forward_local's output, and forward_split
+        must see the gathered data)."""
+        import torch
         import torch.distributed as dist
-        dist.all_gather_into_tensor(self.be.gather, self.be.send, group=self.group)
+        if self.be.gather.is_cuda:
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=self.be.gather.device)):
+                dist.all_gather_into_tensor(self.be.gather, self.be.send, group=self.group)
+        else:
+            dist.all_gather_into_tensor(self.be.gather, self.be.send, group=self.group)
 
-    def solve(self, b, x, stream: int = 0, check: bool = False):
+    def solve(self, b, x, stream: int | None = None, check: bool = False):
         """b, x: this rank's slab (the whole tensor when emulated) as flat
-        column-major tensors on the backend's device; enqueued on `stream`."""
+        column-major tensors on the backend's device; enqueued on `stream`
+        (a cudaStream_t as int; default: torch's current stream, so inputs
+        written by torch are ordered before the solve)."""
         be = self.be
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream().cuda_stream if b.is_cuda else 0
         be.forward_local(b, stream)
         if not self.emulate:
-            self._all_gather()
+            self._all_gather(stream)
         be.forward_split(stream)
         be.solve(stream, self.group)
         be.back_local(stream)
         if not self.emulate:
-            self._all_gather()
+            self._all_gather(stream)
         be.back_split(x, stream)
         if check:
             be.status(stream)

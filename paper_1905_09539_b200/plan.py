@@ -96,6 +96,13 @@ class Plan:
         if rc != 0:
             raise gpu_error(f"tsg_plan_enqueue failed ({rc}): {self.ctx.error()}")
 
+    def set_serial(self, serial: bool) -> None:
+        """Every kernel after its predecessor (tsg_plan_set_serial): the
+        per-phase times of execute_* become per-kernel launch times."""
+        rc = lib().tsg_plan_set_serial(self.h, 1 if serial else 0)
+        if rc != 0:
+            raise gpu_error(f"tsg_plan_set_serial failed ({rc}): {self.ctx.error()}")
+
     def sync(self) -> TsgReport:
         """Wait for every enqueued solve (tsg_plan_sync); zero pivot of the last."""
         rep = TsgReport()
