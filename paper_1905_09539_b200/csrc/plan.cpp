@@ -1854,25 +1854,37 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
     nblk_rest *= a.ncell[s];
   }
   // mode-0 chunks of whole cells within the shared-memory budget: the
-  // register kernel for n_f <= 24 (three CTAs per SM), else the DMMA-blocked
-  // kernel (two CTAs per SM)
+  // register kernel for n_f <= 24 (three CTAs per SM), else the warp-group
+  // DMMA kernel (blocks of <= kWideCols real columns; fewer when a long free
+  // mode would not leave room for two CTAs per SM), else the DMMA-blocked
+  // kernel (TSG_FIBRE_WIDE=0)
   const bool small = nf <= 24;
   int W = 0;
   int ncell_s = 0;
   for (int m = 1; m < d; ++m)
     if (m != f) ncell_s += static_cast<int>(me[m].cells.size());
   const int cell_smem = ncell_s <= 1024 ? ncell_s : 0;
+  bool wide = false;
   if (small) {
     // two block buffers (the next block streams in while one is solved)
     const int NF = nf <= 8 ? 8 : nf <= 16 ? 16 : 24;
     const long avail = (72 * 1024 - 2 * 128 * 32 - cell_smem * 24) / 8 - NF * NF - 3 * NF;
     W = static_cast<int>(std::min<long>(avail / (2 * (static_cast<long>(nf) << nsc)), 128));
   } else {
-    const size_t per_row = (static_cast<size_t>(nf) * 8 + 24) << nsc;
-    const size_t fixed = static_cast<size_t>(nf) * 16 * 8 + 128 * 32 + 16 + cell_smem * 24;
-    W = 108 * 1024 > fixed ? static_cast<int>(std::min<size_t>((108 * 1024 - fixed) / per_row, 128)) : 0;
+    const char* we = std::getenv("TSG_FIBRE_WIDE");
+    if (!(we && std::atoi(we) == 0)) {
+      for (int mc = tsg::kWideCols; mc >= 8 && !wide; mc /= 2) {
+        if (tsg::fibre_wide_smem(nf, mc, cell_smem) > 110 * 1024) continue;
+        W = mc >> nsc;
+        wide = W >= 2;
+      }
+    }
+    if (!wide) {
+      const size_t per_row = (static_cast<size_t>(nf) * 8 + 24) << nsc;
+      const size_t fixed = static_cast<size_t>(nf) * 16 * 8 + 128 * 32 + 16 + cell_smem * 24;
+      W = 108 * 1024 > fixed ? static_cast<int>(std::min<size_t>((108 * 1024 - fixed) / per_row, 128)) : 0;
+    }
   }
-  if (W < 2) return TSG_OK;  // not admissible: the tile kernels keep the plan
   std::vector<int> chunk{0}, cellrow0(dims[0]);
   const auto& c0 = me[0].cells;
   for (int c = 0; c < static_cast<int>(c0.size()); ++c) {
@@ -1910,9 +1922,10 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
   a.maxcol = wmax << nsc;
   a.small = tsg::fibre_small_ok(nf, wmax) ? 1 : 0;
   if (const char* e = std::getenv("TSG_FIBRE_SMALL")) a.small = a.small && std::atoi(e) != 0;
-  a.big = a.small ? 0 : 1;
+  a.wide = !a.small && wide ? 1 : 0;
+  a.big = a.small || a.wide ? 0 : 1;
   if (const char* e = std::getenv("TSG_FIBRE_BIG")) a.big = a.big && std::atoi(e) != 0;
-  if (a.big) {
+  if (a.big || a.wide) {
     // row blocks of f: <= 8 rows, never splitting a 2x2 cell
     const std::vector<int8_t> code = block_codes(T[f], nf);
     std::vector<int> rb{0};
@@ -1923,6 +1936,10 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
     }
     a.nrb = static_cast<int>(rb.size()) - 1;
     TSG_CU(upload_owned(pl, rb, &a.rb));
+    std::vector<unsigned> rbc(a.nrb, 0u);
+    for (int q = 0; q < a.nrb; ++q)
+      for (int i = rb[q]; i < rb[q + 1]; ++i) rbc[q] |= static_cast<unsigned>(code[i]) << (2 * (i - rb[q]));
+    TSG_CU(upload_owned(pl, rbc, &a.rbcode));
     a.pitch = tsg::fibre_pitch(a.maxcol);
   }
   a.nblocks = static_cast<int64_t>(a.nchunk) * nblk_rest;

@@ -176,9 +176,11 @@ struct FibreArgs {
   int maxcol;                // largest block width (columns = chunk rows x 2^k')
   int small;                 // 1: the register kernel (n_f <= 24, chunks <= 128 rows)
   int big;                   // 1: the DMMA-blocked kernel (row blocks rb, shared pitch)
-  int pitch;                 // big: shared row pitch (= 4 mod 16 doubles)
-  int nrb;                   // big: row blocks of f (<= 8 rows, whole cells)
-  const int* rb;             // big: nrb + 1 row-block bounds
+  int wide;                  // 1: the warp-group kernel (fibre_wide_kernel; rows blocks <= 16)
+  int pitch;                 // big/wide: shared row pitch (= 4 mod 16 doubles)
+  int nrb;                   // big/wide: row blocks of f (<= 8 rows, whole cells)
+  const int* rb;             // big/wide: nrb + 1 row-block bounds
+  const unsigned* rbcode;    // wide: per row block, 2 bits per row (0 1x1, 1/2 rows of a 2x2 cell)
   int* counter;              // block queue head (zeroed before launch)
   int* status;               // first singular element offset (atomicMin)
   double tiny;
@@ -187,5 +189,8 @@ cudaError_t launch_fibre_solve(const FibreArgs& a, int device, cudaStream_t st, 
 bool fibre_small_ok(int nf, int chunk_w);
 int fibre_pitch(int maxcol);
 size_t fibre_big_smem(int nf, int maxcol, int cell_smem);
+// wide kernel: columns per block (maxcol bound) and its shared memory
+constexpr int kWideCols = 32;
+size_t fibre_wide_smem(int nf, int maxcol, int cell_smem);
 
 }  // namespace tsg

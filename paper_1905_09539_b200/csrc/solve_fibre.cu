@@ -25,6 +25,9 @@
 #include <mutex>
 #include <utility>
 
+// DMMA as a side-effect-free asm: the compiler may hoist the L2 loads of T_f
+// of later k steps above earlier products (fibre_wide_kernel's update loop)
+#define TSG_DMMA_VOLATILE 0
 #include "common.cuh"
 #include "solve.h"
 #include "util.h"
@@ -775,6 +778,398 @@ __global__ void __launch_bounds__(kBigThreads, 2) fibre_big_kernel(const FibreAr
   pdl_trigger();
 }
 
+// ---- large free modes: warp-owned column groups on DMMA ----------------------
+// A block (chunk of mode-0 cells x one cell of every other S mode, <= 32
+// real columns of n_f rows) is staged in shared memory and its complex jobs
+// are packed into groups of 16 column slots (a job's re and im columns never
+// straddle two groups).  Each warp owns whole groups and runs the blocked
+// back substitution of its 16 columns alone, bottom-up over row blocks of
+// <= 16 rows of T_f (never splitting a 2x2 cell):
+//     Y[i0:i1, grp] -= T_f[i0:i1, i1:nf] Y[i1:nf, grp]     (2 x 2 DMMA tiles)
+//     per job: back substitution of rows [i0, i1) with its own shift
+// so the only block-wide barriers are around the load, butterflies and store;
+// while one warp is in its latency-bound in-block substitution, the other
+// warps of the SM keep the DMMA pipe busy.
+constexpr int kWideThreads = 64;  // two warps per CTA, several CTAs per SM
+constexpr int kWideUnits = 32;    // mode-0 cells per block (<= kWideCols rows)
+constexpr int kWideSlots = 2 * kWideCols;
+
+struct WideTab {
+  int col[kWideSlots];   // smem column of the slot (-1: padding)
+  int im[kWideSlots];    // re slot of a complex job: its im column; else -1
+  int role[kWideSlots];  // 0: re of a complex job, 1: its im, 2: real job, 3: padding
+  double sr[kWideSlots], si[kWideSlots];
+  int nslot;
+  int jre[kWideCols], jim[kWideCols];
+  double jsr[kWideCols], jsi[kWideCols];
+};
+
+// In-block back substitution of <= 8 rows [i0, i0 + nr) of T_f, one lane
+// per real column: a complex job's re and im columns sit on two lanes
+// (partner lanes, sgn = +1 on the re lane, -1 on the im lane) that exchange
+// only what the complex divisions couple; a real job is its own partner with
+// si = 0.  code: 2 bits per row (0: 1x1 cell, 1/2: first/second row of a
+// 2x2 cell), warp-uniform like i0 and nr, so every lane runs every shuffle.
+// Returns "numerically singular" (|det| <= tiny ||M||_F for a shifted 2x2
+// cell, |d| <= tiny for a 1x1 cell).
+TSG_DEVINL bool diag8(const FibreArgs& a, double* Y, int pitch, int i0, int nr, unsigned code, int col,
+                      int partner, double sgn, double sr, double si, const double* T) {
+  constexpr int R = 8;
+  constexpr int nf = 8;  // T: the block's 8x8 diagonal block of T_f, row-major (shared memory)
+  const bool own = col >= 0;
+  const double t2 = a.tiny * a.tiny;
+  double z[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) z[r] = (own && r < nr) ? Y[(i0 + r) * pitch + col] : 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int j = R - 1; j >= 0; --j) {
+    if (j >= nr) continue;
+    const unsigned c = (code >> (2 * j)) & 3u;
+    if (c == 1u) continue;  // first row of a pair: solved with its second row
+    if (c == 2u && j >= 1) {
+      const double m00r = T[(j - 1) * nf + j - 1] + sr, m11r = T[j * nf + j] + sr;
+      const double m01 = T[(j - 1) * nf + j], m10 = T[j * nf + j - 1];
+      const double pa = __shfl_sync(0xffffffffu, z[j - 1], partner);
+      const double pb = __shfl_sync(0xffffffffu, z[j], partner);
+      const double detr = m00r * m11r - si * si - m01 * m10, deti = si * (m00r + m11r);
+      const double na = m11r * z[j - 1] - sgn * si * pa - m01 * z[j];
+      const double nb = m00r * z[j] - sgn * si * pb - m10 * z[j - 1];
+      const double npa = __shfl_sync(0xffffffffu, na, partner);
+      const double npb = __shfl_sync(0xffffffffu, nb, partner);
+      const double dd = detr * detr + deti * deti, idd = 1.0 / dd;
+      const double fro2 = m00r * m00r + m11r * m11r + m01 * m01 + m10 * m10 + 2.0 * si * si;
+      bad = bad || dd <= t2 * fro2;
+      z[j - 1] = (na * detr + sgn * npa * deti) * idd;
+      z[j] = (nb * detr + sgn * npb * deti) * idd;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r < j - 1) z[r] = fma(-T[r * nf + j], z[j], fma(-T[r * nf + j - 1], z[j - 1], z[r]));
+    } else {
+      const double dr = T[j * nf + j] + sr;
+      const double p = __shfl_sync(0xffffffffu, z[j], partner);
+      const double dd = dr * dr + si * si;
+      bad = bad || dd <= t2;
+      z[j] = (z[j] * dr + sgn * p * si) * (1.0 / dd);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r < j) z[r] = fma(-T[r * nf + j], z[j], z[r]);
+    }
+  }
+  if (own)
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (r < nr) Y[(i0 + r) * pitch + col] = z[r];
+  return own && bad;
+}
+
+// Rows of the block <-> shared memory: the run of w contiguous mode-0
+// elements of (row i of f, pattern b) is at X + pb[b] + i * sf.  Each warp
+// instruction moves 32 / wp such runs (wp = w rounded up to a power of two).
+template <bool LOAD>
+TSG_DEVINL void wide_rows(const FibreArgs& a, double* Y, int pitch, const int64_t* pb, int w, int kb) {
+  const int nf = a.nf, nb = 1 << kb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int lw = 0;
+  while ((1 << lw) < w && lw < 5) ++lw;
+  const int sub = lane >> lw, r = lane & ((1 << lw) - 1), rpi = 32 >> lw;
+  if (r >= w) return;  // w <= kWideCols: one element per lane and run
+  const int step = nw * rpi;  // rows of f per warp instruction sweep
+  for (int b = 0; b < nb; ++b) {
+    const int i_start = warp * rpi + sub;
+    double* y = Y + static_cast<size_t>(i_start) * pitch + b * w + r;
+    const double* x = a.X + pb[b] + static_cast<int64_t>(i_start) * a.sf + r;
+    const int64_t xs = static_cast<int64_t>(step) * a.sf;
+    for (int i = i_start; i < nf; i += step) {
+      if (LOAD) cp_async8(y, x, 8);
+      else *const_cast<double*>(x) = *y;
+      y += step * pitch;
+      x += xs;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int nf = a.nf;
+  const int pitch = a.pitch;
+  const int zcol = pitch - 1;  // never written by a block: reads of padding slots give 0
+  double* Y = sm;
+  double* Td = Y + static_cast<size_t>(nf) * pitch;  // 8x8 diagonal blocks of T_f, row-major
+  FibreUnit* su = reinterpret_cast<FibreUnit*>(Td + 64 * static_cast<size_t>(a.nrb));
+  FibreCell* scell = a.cell_smem ? reinterpret_cast<FibreCell*>(su + kWideUnits) : nullptr;
+  __shared__ SmallBuf SB;
+  __shared__ WideTab W;
+  __shared__ int64_t pb[1 << kFibreMaxS];
+  __shared__ int soff[kFibreMaxS + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int s = 0; s < a.ns; ++s) {
+      soff[s] = o;
+      o += a.ncell[s];
+    }
+    soff[a.ns] = o;
+  }
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) Y[static_cast<size_t>(i) * pitch + zcol] = 0.0;
+  for (int e = threadIdx.x; e < 64 * a.nrb; e += blockDim.x) {
+    const int q = e >> 6, r = (e >> 3) & 7, c = e & 7;
+    const int i = a.rb[q] + r, j = a.rb[q] + c;
+    Td[e] = (i < a.rb[q + 1] && j < a.rb[q + 1]) ? a.Tt[static_cast<size_t>(i) * nf + j] : 0.0;
+  }
+  __syncthreads();
+  if (scell)
+    for (int s = 0; s < a.ns; ++s)
+      for (int c = threadIdx.x; c < a.ncell[s]; c += blockDim.x) scell[soff[s] + c] = a.cells[s][c];
+  int64_t badoff = LLONG_MAX;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      SB.blk = atomicAdd(a.counter, 1);
+      if (SB.blk < a.nblocks) decode_block(a, scell, soff, SB.blk, SB.B, SB.nunit);
+    }
+    __syncthreads();
+    if (SB.blk >= a.nblocks) break;
+    const Blk& B = SB.B;
+    const int nunit = SB.nunit;
+    const int w = B.w, kb = B.kb, nb = 1 << kb;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      int64_t o = B.base;
+      for (int t = 0; t < kb; ++t)
+        if ((b >> t) & 1) o += B.bstride[t];
+      pb[b] = o;
+    }
+    {
+      const char* src = reinterpret_cast<const char*>(a.units + B.njob);
+      char* dst = reinterpret_cast<char*>(su);
+      for (int e = threadIdx.x; e < nunit * static_cast<int>(sizeof(FibreUnit) / 8); e += blockDim.x)
+        cp_async8(dst + 8 * e, src + 8 * e, 8);
+    }
+    __syncthreads();
+    wide_rows<true>(a, Y, pitch, pb, w, kb);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int c2 = 1 << kb, c1 = kb ? 1 << (kb - 1) : 1;
+      for (int u = 0; u <= nunit; ++u) {
+        const int npb = u < nunit ? su[u].npair_before : su[nunit - 1].npair_before + su[nunit - 1].pair0;
+        SB.job0[u] = npb * c2 + (u - npb) * c1;
+      }
+    }
+    // forward butterflies (units with >= 2 complex bits)
+    for (int u = 0; u < nunit; ++u) {
+      const int k = kb + su[u].pair0;
+      if (k < 2) continue;
+      for (int i = threadIdx.x; i < nf; i += blockDim.x) unit_butterfly<false>(Y, pitch, i, su[u].rl0, k, su[u].pair0, w);
+    }
+    __syncthreads();
+    const int njob = SB.job0[nunit];
+    for (int j = threadIdx.x; j < njob; j += blockDim.x) {
+      int lo = 0, hi = nunit - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (SB.job0[mid] <= j) lo = mid;
+        else hi = mid - 1;
+      }
+      const int u = lo;
+      const int pair0 = su[u].pair0, k = kb + pair0, rl0 = su[u].rl0;
+      const int l = (j - SB.job0[u]) << 1;
+      W.jre[j] = ucol(l, rl0, pair0, w);
+      W.jim[j] = k ? ucol(l | 1, rl0, pair0, w) : -1;
+      double sr = B.sreal + su[u].sr, si = su[u].si;
+      for (int t = 0; t < kb; ++t) {
+        const int bit = pair0 ? t + 1 : t;
+        sr += B.bre[t];
+        si += ((l >> bit) & 1) ? B.bim[t] : -B.bim[t];
+      }
+      W.jsr[j] = sr;
+      W.jsi[j] = si;
+    }
+    __syncthreads();
+    // pack the jobs into groups of 16 slots (a complex job never straddles)
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int j = 0; j < njob; ++j) {
+        const bool cx = W.jim[j] >= 0;
+        if (cx && (s & 15) == 15) {
+          W.col[s] = -1;
+          W.im[s] = -1;
+          W.role[s] = 3;
+          ++s;
+        }
+        W.col[s] = W.jre[j];
+        W.im[s] = W.jim[j];
+        W.role[s] = cx ? 0 : 2;
+        W.sr[s] = W.jsr[j];
+        W.si[s] = W.jsi[j];
+        ++s;
+        if (cx) {
+          W.col[s] = W.jim[j];
+          W.im[s] = -1;
+          W.role[s] = 1;
+          ++s;
+        }
+      }
+      for (; s & 15; ++s) {
+        W.col[s] = -1;
+        W.im[s] = -1;
+        W.role[s] = 3;
+      }
+      W.nslot = s;
+    }
+    __syncthreads();
+    const int ngrp = W.nslot >> 4;
+    for (int grp = warp; grp < ngrp; grp += nw) {
+      const int s0 = grp << 4;
+      int cb0 = W.col[s0 + g], cb1 = W.col[s0 + 8 + g];  // B-fragment columns
+      cb0 = cb0 >= 0 ? cb0 : zcol;
+      cb1 = cb1 >= 0 ? cb1 : zcol;
+      const int cw00 = W.col[s0 + 2 * t4], cw01 = W.col[s0 + 2 * t4 + 1];
+      const int cw10 = W.col[s0 + 8 + 2 * t4], cw11 = W.col[s0 + 9 + 2 * t4];
+      // this lane's column in the in-block substitutions (lanes 0..15)
+      const int sl = s0 + (lane & 15);
+      const int role = lane < 16 ? W.role[sl] : 3;
+      const int mycol = role == 3 ? -1 : W.col[sl];
+      const int partner = role == 0 ? lane + 1 : role == 1 ? lane - 1 : lane;
+      const int js = role == 1 ? sl - 1 : sl;  // the job's slot (shift)
+      const double sgn = role == 1 ? -1.0 : 1.0;
+      const double mysr = role == 3 ? 0.0 : W.sr[js], mysi = (role == 0 || role == 1) ? W.si[js] : 0.0;
+      // super-blocks of two 8-row blocks, bottom-up
+      const int nsb = (a.nrb + 1) >> 1;
+      for (int q = nsb - 1; q >= 0; --q) {
+        const int blo = 2 * q, bhi = 2 * q + 1 < a.nrb ? 2 * q + 1 : -1;
+        const int i0 = a.rb[blo], mid = a.rb[blo + 1], i1 = bhi >= 0 ? a.rb[bhi + 1] : mid;
+        if (i1 < nf) {
+          // Y[i0:i1] -= T[i0:i1, i1:nf] Y[i1:nf]; m-tile 0 = rows of block lo, 1 = block hi;
+          // rows beyond a block read a valid row of T_f: their sums are discarded
+          const int ra0 = i0 + g, ra1 = mid + g;
+          const bool v0 = ra0 < mid, v1 = ra1 < i1;
+          const double* tp0 = a.Tt + static_cast<size_t>(v0 ? ra0 : i0) * nf + i1 + t4;
+          const double* tp1 = a.Tt + static_cast<size_t>(v1 ? ra1 : i0) * nf + i1 + t4;
+          const double* yp = Y + static_cast<size_t>(i1 + t4) * pitch;
+          double c[2][2][2][2] = {};  // [k parity][m][n][2]
+          // k16 iterations; the A fragments (T_f rows, L2) of iteration it + 1
+          // are loaded while iteration it multiplies
+          const int nit = (nf - i1) >> 4;
+          double an[4][2];
+#pragma unroll
+          for (int st = 0; st < 4; ++st) {
+            an[st][0] = nit > 0 ? __ldg(tp0 + 4 * st) : 0.0;
+            an[st][1] = nit > 0 ? __ldg(tp1 + 4 * st) : 0.0;
+          }
+          for (int it = 0; it < nit; ++it) {
+            double ac[4][2];
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+              ac[st][0] = an[st][0];
+              ac[st][1] = an[st][1];
+            }
+            const int nx = it + 1 < nit ? 16 : 0;  // last iteration re-reads its own rows
+            tp0 += nx;
+            tp1 += nx;
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+              an[st][0] = __ldg(tp0 + 4 * st);
+              an[st][1] = __ldg(tp1 + 4 * st);
+            }
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+              const double* yk = yp + 4 * st * pitch;
+              const double b0 = yk[cb0], b1 = yk[cb1];
+              const int h = st & 1;
+              dmma(c[h][0][0][0], c[h][0][0][1], ac[st][0], b0);
+              dmma(c[h][0][1][0], c[h][0][1][1], ac[st][0], b1);
+              dmma(c[h][1][0][0], c[h][1][0][1], ac[st][1], b0);
+              dmma(c[h][1][1][0], c[h][1][1][1], ac[st][1], b1);
+            }
+            yp += 16 * pitch;
+          }
+          if (nit > 0) {
+            tp0 += 16;
+            tp1 += 16;
+          }
+          const int k = i1 + 16 * nit;
+          if (k < nf) {  // last 1..15 rows: rows >= nf read as 0
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+              if (k + 4 * st >= nf) break;
+              const bool kin = k + 4 * st + t4 < nf;
+              const double a0 = kin ? __ldg(tp0 + 4 * st) : 0.0, a1 = kin ? __ldg(tp1 + 4 * st) : 0.0;
+              const double* yk = yp + 4 * st * pitch;
+              const double b0 = kin ? yk[cb0] : 0.0, b1 = kin ? yk[cb1] : 0.0;
+              const int h = st & 1;
+              dmma(c[h][0][0][0], c[h][0][0][1], a0, b0);
+              dmma(c[h][0][1][0], c[h][0][1][1], a0, b1);
+              dmma(c[h][1][0][0], c[h][1][0][1], a1, b0);
+              dmma(c[h][1][1][0], c[h][1][1][1], a1, b1);
+            }
+          }
+          if (v0) {
+            double* yr = Y + static_cast<size_t>(ra0) * pitch;
+            if (cw00 >= 0) yr[cw00] -= c[0][0][0][0] + c[1][0][0][0];
+            if (cw01 >= 0) yr[cw01] -= c[0][0][0][1] + c[1][0][0][1];
+            if (cw10 >= 0) yr[cw10] -= c[0][0][1][0] + c[1][0][1][0];
+            if (cw11 >= 0) yr[cw11] -= c[0][0][1][1] + c[1][0][1][1];
+          }
+          if (v1) {
+            double* yr = Y + static_cast<size_t>(ra1) * pitch;
+            if (cw00 >= 0) yr[cw00] -= c[0][1][0][0] + c[1][1][0][0];
+            if (cw01 >= 0) yr[cw01] -= c[0][1][0][1] + c[1][1][0][1];
+            if (cw10 >= 0) yr[cw10] -= c[0][1][1][0] + c[1][1][1][0];
+            if (cw11 >= 0) yr[cw11] -= c[0][1][1][1] + c[1][1][1][1];
+          }
+          __syncwarp();
+        }
+        if (bhi >= 0) {
+          // block hi, then Y[i0:mid] -= T[i0:mid, mid:i1] Y[mid:i1] (k <= 8)
+          if (diag8(a, Y, pitch, mid, i1 - mid, a.rbcode[bhi], mycol, partner, sgn, mysr, mysi, Td + 64 * bhi))
+            badoff = min(badoff, goff(B, mycol, mid, a.sf));
+          __syncwarp();
+          const int ra0 = i0 + g;
+          const bool v0 = ra0 < mid;
+          const double* tp0 = a.Tt + static_cast<size_t>(v0 ? ra0 : i0) * nf + mid + t4;
+          double c0[2][2] = {}, c1[2][2] = {};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int kr = mid + 4 * h + t4;
+            if (mid + 4 * h >= i1) break;
+            const bool kin = kr < i1;
+            const double a0 = kin ? __ldg(tp0 + 4 * h) : 0.0;
+            const double* yk = Y + static_cast<size_t>(kin ? kr : mid) * pitch;
+            const double b0 = kin ? yk[cb0] : 0.0, b1 = kin ? yk[cb1] : 0.0;
+            dmma(c0[h][0], c0[h][1], a0, b0);
+            dmma(c1[h][0], c1[h][1], a0, b1);
+          }
+          if (v0) {
+            double* yr = Y + static_cast<size_t>(ra0) * pitch;
+            if (cw00 >= 0) yr[cw00] -= c0[0][0] + c0[1][0];
+            if (cw01 >= 0) yr[cw01] -= c0[0][1] + c0[1][1];
+            if (cw10 >= 0) yr[cw10] -= c1[0][0] + c1[1][0];
+            if (cw11 >= 0) yr[cw11] -= c1[0][1] + c1[1][1];
+          }
+          __syncwarp();
+        }
+        if (diag8(a, Y, pitch, i0, mid - i0, a.rbcode[blo], mycol, partner, sgn, mysr, mysi, Td + 64 * blo))
+          badoff = min(badoff, goff(B, mycol, i0, a.sf));
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int u = 0; u < nunit; ++u) {
+      const int k = kb + su[u].pair0;
+      if (k < 2) continue;
+      for (int i = threadIdx.x; i < nf; i += blockDim.x) unit_butterfly<true>(Y, pitch, i, su[u].rl0, k, su[u].pair0, w);
+    }
+    __syncthreads();
+    wide_rows<false>(a, Y, pitch, pb, w, kb);
+    __syncthreads();
+  }
+  if (badoff != LLONG_MAX) atomicMin(a.status, static_cast<int>(badoff < INT_MAX - 1 ? badoff : INT_MAX - 1));
+  pdl_trigger();
+}
+
 template <typename K>
 cudaError_t launch_k(K k, const FibreArgs& a, size_t smem, int device, cudaStream_t st,
                      SolveLaunchInfo* info, int threads = kThreads) {
@@ -804,6 +1199,12 @@ size_t fibre_big_smem(int nf, int maxcol, int cell_smem) {
          kMaxUnits * sizeof(FibreUnit) + static_cast<size_t>(cell_smem) * sizeof(FibreCell);
 }
 
+size_t fibre_wide_smem(int nf, int maxcol, int cell_smem) {
+  const int nrb = (nf + 6) / 7;  // bound on the 8-row blocks (a 2x2 cell may shorten one to 7)
+  return (static_cast<size_t>(nf) * fibre_pitch(maxcol) + 64 * static_cast<size_t>(nrb)) * sizeof(double) +
+         kWideUnits * sizeof(FibreUnit) + static_cast<size_t>(cell_smem) * sizeof(FibreCell);
+}
+
 bool fibre_small_ok(int nf, int chunk_w) { return nf <= 24 && chunk_w <= kMaxUnits; }
 
 cudaError_t launch_fibre_solve(const FibreArgs& a, int device, cudaStream_t st, SolveLaunchInfo* info) {
@@ -813,6 +1214,10 @@ cudaError_t launch_fibre_solve(const FibreArgs& a, int device, cudaStream_t st, 
     if (a.nf <= 8) return launch_small<8>(a, device, st, info);
     if (a.nf <= 16) return launch_small<16>(a, device, st, info);
     return launch_small<24>(a, device, st, info);
+  }
+  if (a.wide) {
+    const size_t smem = fibre_wide_smem(a.nf, a.maxcol, a.cell_smem);
+    return launch_k(fibre_wide_kernel, a, smem, device, st, info, kWideThreads);
   }
   if (a.big) {
     const size_t smem = fibre_big_smem(a.nf, a.maxcol, a.cell_smem);
