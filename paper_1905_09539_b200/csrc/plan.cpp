@@ -1525,8 +1525,22 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
     fa.X = pl->w1.p;
     fa.counter = pl->counter;
     fa.status = pl->counter + 1;
+    static unsigned long long* fprof = nullptr;
+    if (pl->knobs.prof) {
+      if (!fprof) TSG_CU(cudaMalloc(&fprof, 16 * sizeof(unsigned long long)));
+      TSG_CU(cudaMemsetAsync(fprof, 0, 16 * sizeof(unsigned long long), st));
+      fa.prof = fprof;
+    }
     TSG_CU(tsg::launch_fibre_solve(fa, ctx->device, st, &pl->solve_info));
     ++pl->launches;
+    if (pl->knobs.prof) {
+      unsigned long long h[16];
+      TSG_CU(cudaMemcpyAsync(h, fprof, sizeof(h), cudaMemcpyDeviceToHost, st));
+      TSG_CU(cudaStreamSynchronize(st));
+      const double nbw = h[6] ? static_cast<double>(h[6]) : 1.0;
+      std::fprintf(stderr, "[tsg profw] per block per warp (cycles): load %.0f  butterfly+pack %.0f  barrier-A waits %.0f  leader subst %.0f  helper partials %.0f  store %.0f  (blocks x warps %.0f)\n",
+                   h[0] / nbw, h[1] / nbw, h[2] / nbw, h[3] / nbw, h[4] / nbw, h[5] / nbw, nbw);
+    }
     if (timing) TSG_CU(cudaEventRecord(ev[3], st));
     TSG_CU(transform_all(pl, pl->w1.p, out, pl->w2.p, false, st));
     if (timing) TSG_CU(cudaEventRecord(ev[4], st));

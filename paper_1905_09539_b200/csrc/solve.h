@@ -184,6 +184,7 @@ struct FibreArgs {
   int* counter;              // block queue head (zeroed before launch)
   int* status;               // first singular element offset (atomicMin)
   double tiny;
+  unsigned long long* prof;  // -DWIDE_PROF=1 builds: per-phase cycle sums (TSG_PROF)
 };
 cudaError_t launch_fibre_solve(const FibreArgs& a, int device, cudaStream_t st, SolveLaunchInfo* info);
 bool fibre_small_ok(int nf, int chunk_w);
@@ -191,6 +192,6 @@ int fibre_pitch(int maxcol);
 size_t fibre_big_smem(int nf, int maxcol, int cell_smem);
 // wide kernel: columns per block (maxcol bound) and its shared memory
 constexpr int kWideCols = 32;
-size_t fibre_wide_smem(int nf, int maxcol, int cell_smem);
+size_t fibre_wide_smem(int nf, int maxcol, int cell_smem, int nrb = 0);
 
 }  // namespace tsg

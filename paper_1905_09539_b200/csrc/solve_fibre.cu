@@ -778,21 +778,42 @@ __global__ void __launch_bounds__(kBigThreads, 2) fibre_big_kernel(const FibreAr
   pdl_trigger();
 }
 
-// ---- large free modes: warp-owned column groups on DMMA ----------------------
+// ---- large free modes: leader/helper teams on DMMA ---------------------------
 // A block (chunk of mode-0 cells x one cell of every other S mode, <= 32
-// real columns of n_f rows) is staged in shared memory and its complex jobs
-// are packed into groups of 16 column slots (a job's re and im columns never
-// straddle two groups).  Each warp owns whole groups and runs the blocked
-// back substitution of its 16 columns alone, bottom-up over row blocks of
-// <= 16 rows of T_f (never splitting a 2x2 cell):
-//     Y[i0:i1, grp] -= T_f[i0:i1, i1:nf] Y[i1:nf, grp]     (2 x 2 DMMA tiles)
-//     per job: back substitution of rows [i0, i1) with its own shift
-// so the only block-wide barriers are around the load, butterflies and store;
-// while one warp is in its latency-bound in-block substitution, the other
-// warps of the SM keep the DMMA pipe busy.
-constexpr int kWideThreads = 64;  // two warps per CTA, several CTAs per SM
-constexpr int kWideUnits = 32;    // mode-0 cells per block (<= kWideCols rows)
+// real columns of n_f rows) is staged in shared memory; its complex jobs are
+// packed into groups of 16 column slots (a job's re and im columns never
+// straddle two groups).  A team of three warps solves one group by blocked
+// back substitution over super-blocks s of two 8-row blocks of T_f
+// (lo = [i0, mid), hi = [mid, i1); never splitting a 2x2 cell), bottom-up,
+// as a two-stage pipeline:
+//   helpers (one per 8-row block of s):  Y[s] -= T_f[s, i1:nf] Y[i1:nf]
+//     (DMMA; the part from the rows of s+1 right after s+1 is solved, the
+//     rest one step early, while the leader substitutes s+1),
+//   leader: the in-block substitution of s (scalar FP64 in registers,
+//     16 lanes, one real column per lane).
+// On sm_100a the FP64 scalar pipe and DMMA share a sub-partition's math
+// pipe: a DFMA dependency chain on a sub-partition that also runs a DMMA
+// stream slows from ~9 to ~260-780 cycles per op (tools/probe/fp64_contend.cu).
+// So the leaders issue no DMMA and sit on sub-partition 0 (hardware warp
+// slot = 0 mod 4), the helpers on sub-partitions 1-3.
+#ifndef WIDE_PROF
+#define WIDE_PROF 0
+#endif
+#if WIDE_PROF
+#define WP_T(v) const long long v = clock64()
+#define WP_ADD(k, t0) (ph[k] += clock64() - (t0))
+#else
+#define WP_T(v)
+#define WP_ADD(k, t0)
+#endif
+constexpr int kTeamWarps = 3;  // leader + two helpers per 16-column group
+constexpr int kWideTeams = 2;
+constexpr int kWideThreads = kTeamWarps * kWideTeams * 32;
 constexpr int kWideSlots = 2 * kWideCols;
+constexpr int kWideUnits = 32;  // mode-0 cells per block (<= kWideCols rows)
+TSG_DEVINL void team_sync(int team) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(team + 1), "r"(kTeamWarps * 32) : "memory");
+}
 
 struct WideTab {
   int col[kWideSlots];   // smem column of the slot (-1: padding)
@@ -804,23 +825,18 @@ struct WideTab {
   double jsr[kWideCols], jsi[kWideCols];
 };
 
-// In-block back substitution of <= 8 rows [i0, i0 + nr) of T_f, one lane
-// per real column: a complex job's re and im columns sit on two lanes
-// (partner lanes, sgn = +1 on the re lane, -1 on the im lane) that exchange
-// only what the complex divisions couple; a real job is its own partner with
-// si = 0.  code: 2 bits per row (0: 1x1 cell, 1/2: first/second row of a
-// 2x2 cell), warp-uniform like i0 and nr, so every lane runs every shuffle.
-// Returns "numerically singular" (|det| <= tiny ||M||_F for a shifted 2x2
-// cell, |d| <= tiny for a 1x1 cell).
-TSG_DEVINL bool diag8(const FibreArgs& a, double* Y, int pitch, int i0, int nr, unsigned code, int col,
-                      int partner, double sgn, double sr, double si, const double* T) {
+// In-block back substitution of <= 8 rows (z in registers, T the 8x8
+// diagonal block in shared memory, row-major), one lane per real column: a
+// complex job's re and im columns sit on two partner lanes (sgn = +1 on the
+// re lane, -1 on the im lane) that exchange only what the complex divisions
+// couple; a real job is its own partner with si = 0.  code: 2 bits per row
+// (0: 1x1 cell, 1/2: first/second row of a 2x2 cell); code, nr and T are
+// warp-uniform, so every lane runs every shuffle.  Returns "numerically
+// singular" (|det| <= tiny ||M||_F for a shifted 2x2 cell, |d| <= tiny for
+// a 1x1 cell).
+TSG_DEVINL bool sub8(double (&z)[8], int nr, unsigned code, int partner, double sgn, double sr, double si,
+                     double t2, const double* T) {
   constexpr int R = 8;
-  constexpr int nf = 8;  // T: the block's 8x8 diagonal block of T_f, row-major (shared memory)
-  const bool own = col >= 0;
-  const double t2 = a.tiny * a.tiny;
-  double z[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) z[r] = (own && r < nr) ? Y[(i0 + r) * pitch + col] : 0.0;
   bool bad = false;
 #pragma unroll
   for (int j = R - 1; j >= 0; --j) {
@@ -828,8 +844,8 @@ TSG_DEVINL bool diag8(const FibreArgs& a, double* Y, int pitch, int i0, int nr, 
     const unsigned c = (code >> (2 * j)) & 3u;
     if (c == 1u) continue;  // first row of a pair: solved with its second row
     if (c == 2u && j >= 1) {
-      const double m00r = T[(j - 1) * nf + j - 1] + sr, m11r = T[j * nf + j] + sr;
-      const double m01 = T[(j - 1) * nf + j], m10 = T[j * nf + j - 1];
+      const double m00r = T[(j - 1) * R + j - 1] + sr, m11r = T[j * R + j] + sr;
+      const double m01 = T[(j - 1) * R + j], m10 = T[j * R + j - 1];
       const double pa = __shfl_sync(0xffffffffu, z[j - 1], partner);
       const double pb = __shfl_sync(0xffffffffu, z[j], partner);
       const double detr = m00r * m11r - si * si - m01 * m10, deti = si * (m00r + m11r);
@@ -844,23 +860,19 @@ TSG_DEVINL bool diag8(const FibreArgs& a, double* Y, int pitch, int i0, int nr, 
       z[j] = (nb * detr + sgn * npb * deti) * idd;
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (r < j - 1) z[r] = fma(-T[r * nf + j], z[j], fma(-T[r * nf + j - 1], z[j - 1], z[r]));
+        if (r < j - 1) z[r] = fma(-T[r * R + j], z[j], fma(-T[r * R + j - 1], z[j - 1], z[r]));
     } else {
-      const double dr = T[j * nf + j] + sr;
+      const double dr = T[j * R + j] + sr;
       const double p = __shfl_sync(0xffffffffu, z[j], partner);
       const double dd = dr * dr + si * si;
       bad = bad || dd <= t2;
       z[j] = (z[j] * dr + sgn * p * si) * (1.0 / dd);
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (r < j) z[r] = fma(-T[r * nf + j], z[j], z[r]);
+        if (r < j) z[r] = fma(-T[r * R + j], z[j], z[r]);
     }
   }
-  if (own)
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (r < nr) Y[(i0 + r) * pitch + col] = z[r];
-  return own && bad;
+  return bad;
 }
 
 // Rows of the block <-> shared memory: the run of w contiguous mode-0
@@ -889,19 +901,24 @@ TSG_DEVINL void wide_rows(const FibreArgs& a, double* Y, int pitch, const int64_
   }
 }
 
+// Shared-memory layout: Y (n_f x pitch), then per super-block s three 8x8
+// blocks of T_f, row-major: [0] T[lo, lo], [1] T[hi, hi], [2] T[lo, hi]
+// (zero padded), then the unit table and the optional S' cell table.
 __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int nf = a.nf;
   const int pitch = a.pitch;
   const int zcol = pitch - 1;  // never written by a block: reads of padding slots give 0
+  const int nsb = (a.nrb + 1) >> 1;
   double* Y = sm;
-  double* Td = Y + static_cast<size_t>(nf) * pitch;  // 8x8 diagonal blocks of T_f, row-major
-  FibreUnit* su = reinterpret_cast<FibreUnit*>(Td + 64 * static_cast<size_t>(a.nrb));
+  double* Td = Y + static_cast<size_t>(nf) * pitch;
+  FibreUnit* su = reinterpret_cast<FibreUnit*>(Td + 192 * static_cast<size_t>(nsb));
   FibreCell* scell = a.cell_smem ? reinterpret_cast<FibreCell*>(su + kWideUnits) : nullptr;
   __shared__ SmallBuf SB;
   __shared__ WideTab W;
   __shared__ int64_t pb[1 << kFibreMaxS];
   __shared__ int soff[kFibreMaxS + 1];
+  __shared__ int hwslot[kWideThreads / 32], lead[kWideTeams];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   pdl_wait();
@@ -913,18 +930,40 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
     }
     soff[a.ns] = o;
   }
+  if (lane == 0) {
+    unsigned hw;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(hw));
+    hwslot[warp] = static_cast<int>(hw);
+  }
   for (int i = threadIdx.x; i < nf; i += blockDim.x) Y[static_cast<size_t>(i) * pitch + zcol] = 0.0;
-  for (int e = threadIdx.x; e < 64 * a.nrb; e += blockDim.x) {
-    const int q = e >> 6, r = (e >> 3) & 7, c = e & 7;
-    const int i = a.rb[q] + r, j = a.rb[q] + c;
-    Td[e] = (i < a.rb[q + 1] && j < a.rb[q + 1]) ? a.Tt[static_cast<size_t>(i) * nf + j] : 0.0;
+  for (int e = threadIdx.x; e < 192 * nsb; e += blockDim.x) {
+    const int sb = e / 192, part = (e / 64) % 3, r = (e >> 3) & 7, c = e & 7;
+    const int lo0 = a.rb[2 * sb], mid = a.rb[2 * sb + 1], hi1 = 2 * sb + 1 < a.nrb ? a.rb[2 * sb + 2] : mid;
+    const int i = (part == 1 ? mid : lo0) + r, j = (part == 0 ? lo0 : mid) + c;
+    const int ie = part == 1 ? hi1 : mid, je = part == 0 ? mid : hi1;
+    Td[e] = (i < ie && j < je) ? a.Tt[static_cast<size_t>(i) * nf + j] : 0.0;
   }
   __syncthreads();
+  // leader of each team: its warp on sub-partition 0 (slot = 0 mod 4) if any
+  if (threadIdx.x < kWideTeams) {
+    const int t = threadIdx.x;
+    int best = 0, bd = 4;
+    for (int u = 0; u < kTeamWarps; ++u) {
+      const int dd = hwslot[t * kTeamWarps + u] & 3;
+      if (dd < bd) bd = dd, best = u;
+    }
+    lead[t] = best;
+  }
   if (scell)
     for (int s = 0; s < a.ns; ++s)
       for (int c = threadIdx.x; c < a.ncell[s]; c += blockDim.x) scell[soff[s] + c] = a.cells[s][c];
   int64_t badoff = LLONG_MAX;
+#if WIDE_PROF
+  long long ph[12] = {};
+#endif
+  const double t2 = a.tiny * a.tiny;
   for (;;) {
+    WP_T(tq);
     if (threadIdx.x == 0) {
       SB.blk = atomicAdd(a.counter, 1);
       if (SB.blk < a.nblocks) decode_block(a, scell, soff, SB.blk, SB.B, SB.nunit);
@@ -951,6 +990,8 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
+    WP_ADD(0, tq);
+    WP_T(tb);
     if (threadIdx.x == 0) {
       const int c2 = 1 << kb, c1 = kb ? 1 << (kb - 1) : 1;
       for (int u = 0; u <= nunit; ++u) {
@@ -969,9 +1010,9 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
     for (int j = threadIdx.x; j < njob; j += blockDim.x) {
       int lo = 0, hi = nunit - 1;
       while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (SB.job0[mid] <= j) lo = mid;
-        else hi = mid - 1;
+        const int md = (lo + hi + 1) >> 1;
+        if (SB.job0[md] <= j) lo = md;
+        else hi = md - 1;
       }
       const int u = lo;
       const int pair0 = su[u].pair0, k = kb + pair0, rl0 = su[u].rl0;
@@ -1020,15 +1061,18 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
       W.nslot = s;
     }
     __syncthreads();
+    WP_ADD(1, tb);
     const int ngrp = W.nslot >> 4;
-    for (int grp = warp; grp < ngrp; grp += nw) {
+    const int team = warp / kTeamWarps;
+    const int tw = (warp % kTeamWarps - lead[team] + kTeamWarps) % kTeamWarps;  // 0 leader, 1/2 helpers
+    for (int grp = team; grp < ngrp; grp += kWideTeams) {
       const int s0 = grp << 4;
       int cb0 = W.col[s0 + g], cb1 = W.col[s0 + 8 + g];  // B-fragment columns
       cb0 = cb0 >= 0 ? cb0 : zcol;
       cb1 = cb1 >= 0 ? cb1 : zcol;
       const int cw00 = W.col[s0 + 2 * t4], cw01 = W.col[s0 + 2 * t4 + 1];
       const int cw10 = W.col[s0 + 8 + 2 * t4], cw11 = W.col[s0 + 9 + 2 * t4];
-      // this lane's column in the in-block substitutions (lanes 0..15)
+      // leader: this lane's column (lanes 0..15)
       const int sl = s0 + (lane & 15);
       const int role = lane < 16 ? W.role[sl] : 3;
       const int mycol = role == 3 ? -1 : W.col[sl];
@@ -1036,127 +1080,120 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
       const int js = role == 1 ? sl - 1 : sl;  // the job's slot (shift)
       const double sgn = role == 1 ? -1.0 : 1.0;
       const double mysr = role == 3 ? 0.0 : W.sr[js], mysi = (role == 0 || role == 1) ? W.si[js] : 0.0;
-      // super-blocks of two 8-row blocks, bottom-up
-      const int nsb = (a.nrb + 1) >> 1;
+      // helper h (tw = 1 + h): 8-row block 2 s + h of every super-block s
+      const int h = tw - 1;
+      double c[2][2][2] = {};  // [n-tile][k parity][2]: partial of the next super-block
+      double la[4];            // A fragments of T_f[rows, rows of s+1] (k = i1 + 4 t4 + st)
       for (int q = nsb - 1; q >= 0; --q) {
-        const int blo = 2 * q, bhi = 2 * q + 1 < a.nrb ? 2 * q + 1 : -1;
-        const int i0 = a.rb[blo], mid = a.rb[blo + 1], i1 = bhi >= 0 ? a.rb[bhi + 1] : mid;
-        if (i1 < nf) {
-          // Y[i0:i1] -= T[i0:i1, i1:nf] Y[i1:nf]; m-tile 0 = rows of block lo, 1 = block hi;
-          // rows beyond a block read a valid row of T_f: their sums are discarded
-          const int ra0 = i0 + g, ra1 = mid + g;
-          const bool v0 = ra0 < mid, v1 = ra1 < i1;
-          const double* tp0 = a.Tt + static_cast<size_t>(v0 ? ra0 : i0) * nf + i1 + t4;
-          const double* tp1 = a.Tt + static_cast<size_t>(v1 ? ra1 : i0) * nf + i1 + t4;
-          const double* yp = Y + static_cast<size_t>(i1 + t4) * pitch;
-          double c[2][2][2][2] = {};  // [k parity][m][n][2]
-          // k16 iterations; the A fragments (T_f rows, L2) of iteration it + 1
-          // are loaded while iteration it multiplies
-          const int nit = (nf - i1) >> 4;
-          double an[4][2];
+        const int i0 = a.rb[2 * q], mid = a.rb[2 * q + 1];
+        const int i1 = 2 * q + 1 < a.nrb ? a.rb[2 * q + 2] : mid;
+        WP_T(tA);
+        team_sync(team);  // rows >= i1 final
+        WP_ADD(2, tA);
+        if (tw > 0) {
+          // finish Y[block] -= T_f[block, i1:nf] Y[i1:nf]: the rows of s+1, then write
+          const int r0 = h == 0 ? i0 : mid, r1 = h == 0 ? mid : i1;
+          if (r0 < r1 && i1 < nf) {
+            const int i2 = a.rb[min(2 * q + 4, a.nrb)];
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+              const int kr = i1 + 4 * t4 + st;
+              const bool kin = kr < i2;
+              const double* yk = Y + static_cast<size_t>(kin ? kr : i1) * pitch;
+              const double b0 = yk[kin ? cb0 : zcol], b1 = yk[kin ? cb1 : zcol];
+              dmma(c[0][st & 1][0], c[0][st & 1][1], la[st], b0);
+              dmma(c[1][st & 1][0], c[1][st & 1][1], la[st], b1);
+            }
+            const int ra = r0 + g;
+            if (ra < r1) {
+              double* yr = Y + static_cast<size_t>(ra) * pitch;
+              if (cw00 >= 0) yr[cw00] -= c[0][0][0] + c[0][1][0];
+              if (cw01 >= 0) yr[cw01] -= c[0][0][1] + c[0][1][1];
+              if (cw10 >= 0) yr[cw10] -= c[1][0][0] + c[1][1][0];
+              if (cw11 >= 0) yr[cw11] -= c[1][0][1] + c[1][1][1];
+            }
+          }
+        }
+        team_sync(team);  // Y[s] fully updated
+        WP_T(tL);
+        if (tw == 0) {
+          // in-block substitution of super-block s: hi, lo -= T[lo, hi] hi, lo
+          double zl[8], zh[8];
+          const bool own = mycol >= 0;
+          const int nl = mid - i0, nh = i1 - mid;
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            zl[r] = (own && r < nl) ? Y[(i0 + r) * pitch + mycol] : 0.0;
+            zh[r] = (own && r < nh) ? Y[(mid + r) * pitch + mycol] : 0.0;
+          }
+          const double* T3 = Td + 192 * q;
+          bool bad = false;
+          if (nh > 0) {
+            bad = sub8(zh, nh, a.rbcode[2 * q + 1], partner, sgn, mysr, mysi, t2, T3 + 64);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              double acc = zl[r];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) acc = fma(-T3[128 + r * 8 + k], zh[k], acc);
+              zl[r] = acc;
+            }
+          }
+          bad = sub8(zl, nl, a.rbcode[2 * q], partner, sgn, mysr, mysi, t2, T3) || bad;
+          if (own) {
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              if (r < nl) Y[(i0 + r) * pitch + mycol] = zl[r];
+              if (r < nh) Y[(mid + r) * pitch + mycol] = zh[r];
+            }
+            if (bad) badoff = min(badoff, goff(B, mycol, i0, a.sf));
+          }
+          WP_ADD(3, tL);
+        } else if (q >= 1) {
+          // partial of super-block s-1 over the final rows k >= i1, and the A
+          // fragments of its update from the rows of s (used next step)
+          const int p0 = a.rb[2 * q - 2], pm = a.rb[2 * q - 1];
+          const int r0 = h == 0 ? p0 : pm, r1 = h == 0 ? pm : i0;
+          const int ra = r0 + g;
+          const double* trow = a.Tt + static_cast<size_t>(ra < r1 ? ra : p0) * nf;
 #pragma unroll
           for (int st = 0; st < 4; ++st) {
-            an[st][0] = nit > 0 ? __ldg(tp0 + 4 * st) : 0.0;
-            an[st][1] = nit > 0 ? __ldg(tp1 + 4 * st) : 0.0;
+            const int kr = i0 + 4 * t4 + st;
+            la[st] = kr < i1 ? __ldg(trow + kr) : 0.0;
           }
-          for (int it = 0; it < nit; ++it) {
-            double ac[4][2];
 #pragma unroll
-            for (int st = 0; st < 4; ++st) {
-              ac[st][0] = an[st][0];
-              ac[st][1] = an[st][1];
+          for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) c[u][v][0] = c[u][v][1] = 0.0;
+          if (r0 < r1) {
+            const double* tp = trow + i1 + t4;
+            const double* yp = Y + static_cast<size_t>(i1 + t4) * pitch;
+            const int nk4 = (nf - i1) >> 2;
+            int j = 0;
+#pragma unroll 4
+            for (; j + 1 < nk4; j += 2) {
+              const double a0 = __ldg(tp + 4 * j), a1 = __ldg(tp + 4 * j + 4);
+              const double* y0 = yp + 4 * j * pitch;
+              const double* y1 = y0 + 4 * pitch;
+              dmma(c[0][0][0], c[0][0][1], a0, y0[cb0]);
+              dmma(c[1][0][0], c[1][0][1], a0, y0[cb1]);
+              dmma(c[0][1][0], c[0][1][1], a1, y1[cb0]);
+              dmma(c[1][1][0], c[1][1][1], a1, y1[cb1]);
             }
-            const int nx = it + 1 < nit ? 16 : 0;  // last iteration re-reads its own rows
-            tp0 += nx;
-            tp1 += nx;
-#pragma unroll
-            for (int st = 0; st < 4; ++st) {
-              an[st][0] = __ldg(tp0 + 4 * st);
-              an[st][1] = __ldg(tp1 + 4 * st);
-            }
-#pragma unroll
-            for (int st = 0; st < 4; ++st) {
-              const double* yk = yp + 4 * st * pitch;
-              const double b0 = yk[cb0], b1 = yk[cb1];
-              const int h = st & 1;
-              dmma(c[h][0][0][0], c[h][0][0][1], ac[st][0], b0);
-              dmma(c[h][0][1][0], c[h][0][1][1], ac[st][0], b1);
-              dmma(c[h][1][0][0], c[h][1][0][1], ac[st][1], b0);
-              dmma(c[h][1][1][0], c[h][1][1][1], ac[st][1], b1);
-            }
-            yp += 16 * pitch;
-          }
-          if (nit > 0) {
-            tp0 += 16;
-            tp1 += 16;
-          }
-          const int k = i1 + 16 * nit;
-          if (k < nf) {  // last 1..15 rows: rows >= nf read as 0
-#pragma unroll
-            for (int st = 0; st < 4; ++st) {
-              if (k + 4 * st >= nf) break;
-              const bool kin = k + 4 * st + t4 < nf;
-              const double a0 = kin ? __ldg(tp0 + 4 * st) : 0.0, a1 = kin ? __ldg(tp1 + 4 * st) : 0.0;
-              const double* yk = yp + 4 * st * pitch;
-              const double b0 = kin ? yk[cb0] : 0.0, b1 = kin ? yk[cb1] : 0.0;
-              const int h = st & 1;
-              dmma(c[h][0][0][0], c[h][0][0][1], a0, b0);
-              dmma(c[h][0][1][0], c[h][0][1][1], a0, b1);
-              dmma(c[h][1][0][0], c[h][1][0][1], a1, b0);
-              dmma(c[h][1][1][0], c[h][1][1][1], a1, b1);
+            for (; 4 * j < nf - i1; ++j) {  // last k4 step (rows >= nf read as 0)
+              const bool kin = i1 + 4 * j + t4 < nf;
+              const double a0 = kin ? __ldg(tp + 4 * j) : 0.0;
+              const double* y0 = yp + static_cast<size_t>(kin ? 4 * j : 0) * pitch;
+              dmma(c[0][0][0], c[0][0][1], a0, y0[kin ? cb0 : zcol]);
+              dmma(c[1][0][0], c[1][0][1], a0, y0[kin ? cb1 : zcol]);
             }
           }
-          if (v0) {
-            double* yr = Y + static_cast<size_t>(ra0) * pitch;
-            if (cw00 >= 0) yr[cw00] -= c[0][0][0][0] + c[1][0][0][0];
-            if (cw01 >= 0) yr[cw01] -= c[0][0][0][1] + c[1][0][0][1];
-            if (cw10 >= 0) yr[cw10] -= c[0][0][1][0] + c[1][0][1][0];
-            if (cw11 >= 0) yr[cw11] -= c[0][0][1][1] + c[1][0][1][1];
-          }
-          if (v1) {
-            double* yr = Y + static_cast<size_t>(ra1) * pitch;
-            if (cw00 >= 0) yr[cw00] -= c[0][1][0][0] + c[1][1][0][0];
-            if (cw01 >= 0) yr[cw01] -= c[0][1][0][1] + c[1][1][0][1];
-            if (cw10 >= 0) yr[cw10] -= c[0][1][1][0] + c[1][1][1][0];
-            if (cw11 >= 0) yr[cw11] -= c[0][1][1][1] + c[1][1][1][1];
-          }
-          __syncwarp();
+          WP_ADD(4, tL);
         }
-        if (bhi >= 0) {
-          // block hi, then Y[i0:mid] -= T[i0:mid, mid:i1] Y[mid:i1] (k <= 8)
-          if (diag8(a, Y, pitch, mid, i1 - mid, a.rbcode[bhi], mycol, partner, sgn, mysr, mysi, Td + 64 * bhi))
-            badoff = min(badoff, goff(B, mycol, mid, a.sf));
-          __syncwarp();
-          const int ra0 = i0 + g;
-          const bool v0 = ra0 < mid;
-          const double* tp0 = a.Tt + static_cast<size_t>(v0 ? ra0 : i0) * nf + mid + t4;
-          double c0[2][2] = {}, c1[2][2] = {};
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int kr = mid + 4 * h + t4;
-            if (mid + 4 * h >= i1) break;
-            const bool kin = kr < i1;
-            const double a0 = kin ? __ldg(tp0 + 4 * h) : 0.0;
-            const double* yk = Y + static_cast<size_t>(kin ? kr : mid) * pitch;
-            const double b0 = kin ? yk[cb0] : 0.0, b1 = kin ? yk[cb1] : 0.0;
-            dmma(c0[h][0], c0[h][1], a0, b0);
-            dmma(c1[h][0], c1[h][1], a0, b1);
-          }
-          if (v0) {
-            double* yr = Y + static_cast<size_t>(ra0) * pitch;
-            if (cw00 >= 0) yr[cw00] -= c0[0][0] + c0[1][0];
-            if (cw01 >= 0) yr[cw01] -= c0[0][1] + c0[1][1];
-            if (cw10 >= 0) yr[cw10] -= c1[0][0] + c1[1][0];
-            if (cw11 >= 0) yr[cw11] -= c1[0][1] + c1[1][1];
-          }
-          __syncwarp();
-        }
-        if (diag8(a, Y, pitch, i0, mid - i0, a.rbcode[blo], mycol, partner, sgn, mysr, mysi, Td + 64 * blo))
-          badoff = min(badoff, goff(B, mycol, i0, a.sf));
-        __syncwarp();
       }
+      team_sync(team);  // the last leader substitution is visible
     }
     __syncthreads();
+    WP_T(ts);
     for (int u = 0; u < nunit; ++u) {
       const int k = kb + su[u].pair0;
       if (k < 2) continue;
@@ -1165,7 +1202,15 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
     __syncthreads();
     wide_rows<false>(a, Y, pitch, pb, w, kb);
     __syncthreads();
+    WP_ADD(5, ts);
+#if WIDE_PROF
+    ph[6] += 1;
+#endif
   }
+#if WIDE_PROF
+  if (a.prof && lane == 0)
+    for (int k = 0; k < 7; ++k) atomicAdd(a.prof + k, static_cast<unsigned long long>(ph[k]));
+#endif
   if (badoff != LLONG_MAX) atomicMin(a.status, static_cast<int>(badoff < INT_MAX - 1 ? badoff : INT_MAX - 1));
   pdl_trigger();
 }
@@ -1199,9 +1244,10 @@ size_t fibre_big_smem(int nf, int maxcol, int cell_smem) {
          kMaxUnits * sizeof(FibreUnit) + static_cast<size_t>(cell_smem) * sizeof(FibreCell);
 }
 
-size_t fibre_wide_smem(int nf, int maxcol, int cell_smem) {
-  const int nrb = (nf + 6) / 7;  // bound on the 8-row blocks (a 2x2 cell may shorten one to 7)
-  return (static_cast<size_t>(nf) * fibre_pitch(maxcol) + 64 * static_cast<size_t>(nrb)) * sizeof(double) +
+size_t fibre_wide_smem(int nf, int maxcol, int cell_smem, int nrb) {
+  if (nrb <= 0) nrb = (nf + 6) / 7;  // bound on the 8-row blocks (a 2x2 cell may shorten one to 7)
+  const size_t nsb = (nrb + 1) / 2;
+  return (static_cast<size_t>(nf) * fibre_pitch(maxcol) + 192 * nsb) * sizeof(double) +
          kWideUnits * sizeof(FibreUnit) + static_cast<size_t>(cell_smem) * sizeof(FibreCell);
 }
 
@@ -1216,7 +1262,7 @@ cudaError_t launch_fibre_solve(const FibreArgs& a, int device, cudaStream_t st, 
     return launch_small<24>(a, device, st, info);
   }
   if (a.wide) {
-    const size_t smem = fibre_wide_smem(a.nf, a.maxcol, a.cell_smem);
+    const size_t smem = fibre_wide_smem(a.nf, a.maxcol, a.cell_smem, a.nrb);
     return launch_k(fibre_wide_kernel, a, smem, device, st, info, kWideThreads);
   }
   if (a.big) {
