@@ -1540,6 +1540,8 @@ int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool t
       const double nbw = h[6] ? static_cast<double>(h[6]) : 1.0;
       std::fprintf(stderr, "[tsg profw] per block per warp (cycles): load %.0f  butterfly+pack %.0f  barrier-A waits %.0f  leader subst %.0f  helper partials %.0f  store %.0f  (blocks x warps %.0f)\n",
                    h[0] / nbw, h[1] / nbw, h[2] / nbw, h[3] / nbw, h[4] / nbw, h[5] / nbw, nbw);
+      std::fprintf(stderr, "[tsg profw] leaders per sub-partition %llu %llu %llu %llu, helpers %llu %llu %llu %llu\n",
+                   h[8], h[9], h[10], h[11], h[12], h[13], h[14], h[15]);
     }
     if (timing) TSG_CU(cudaEventRecord(ev[3], st));
     TSG_CU(transform_all(pl, pl->w1.p, out, pl->w2.p, false, st));

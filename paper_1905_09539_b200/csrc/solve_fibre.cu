@@ -806,8 +806,14 @@ __global__ void __launch_bounds__(kBigThreads, 2) fibre_big_kernel(const FibreAr
 #define WP_T(v)
 #define WP_ADD(k, t0)
 #endif
+#ifndef SUB8_PRO
+#define SUB8_PRO false
+#endif
 constexpr int kTeamWarps = 3;  // leader + two helpers per 16-column group
 constexpr int kWideTeams = 2;
+// six warps per CTA (two CTAs per SM); roles are given by hardware
+// sub-partition (warp slot mod 4, read from %warpid): the leaders on the
+// lowest sub-partitions, the helpers on the others
 constexpr int kWideThreads = kTeamWarps * kWideTeams * 32;
 constexpr int kWideSlots = 2 * kWideCols;
 constexpr int kWideUnits = 32;  // mode-0 cells per block (<= kWideCols rows)
@@ -834,8 +840,9 @@ struct WideTab {
 // warp-uniform, so every lane runs every shuffle.  Returns "numerically
 // singular" (|det| <= tiny ||M||_F for a shifted 2x2 cell, |d| <= tiny for
 // a 1x1 cell).
-TSG_DEVINL bool sub8(double (&z)[8], int nr, unsigned code, int partner, double sgn, double sr, double si,
-                     double t2, const double* T) {
+TSG_DEVINL double rcp_pos(double q);
+TSG_DEVINL bool sub8c(double (&z)[8], int nr, unsigned code, int partner, double sgn, double sr, double si,
+                      double t2, const double* T) {
   constexpr int R = 8;
   bool bad = false;
 #pragma unroll
@@ -846,16 +853,16 @@ TSG_DEVINL bool sub8(double (&z)[8], int nr, unsigned code, int partner, double 
     if (c == 2u && j >= 1) {
       const double m00r = T[(j - 1) * R + j - 1] + sr, m11r = T[j * R + j] + sr;
       const double m01 = T[(j - 1) * R + j], m10 = T[j * R + j - 1];
+      const double detr = m00r * m11r - si * si - m01 * m10, deti = si * (m00r + m11r);
+      const double dd = detr * detr + deti * deti, idd = rcp_pos(dd);
+      const double fro2 = m00r * m00r + m11r * m11r + m01 * m01 + m10 * m10 + 2.0 * si * si;
+      bad = bad || dd <= t2 * fro2;
       const double pa = __shfl_sync(0xffffffffu, z[j - 1], partner);
       const double pb = __shfl_sync(0xffffffffu, z[j], partner);
-      const double detr = m00r * m11r - si * si - m01 * m10, deti = si * (m00r + m11r);
       const double na = m11r * z[j - 1] - sgn * si * pa - m01 * z[j];
       const double nb = m00r * z[j] - sgn * si * pb - m10 * z[j - 1];
       const double npa = __shfl_sync(0xffffffffu, na, partner);
       const double npb = __shfl_sync(0xffffffffu, nb, partner);
-      const double dd = detr * detr + deti * deti, idd = 1.0 / dd;
-      const double fro2 = m00r * m00r + m11r * m11r + m01 * m01 + m10 * m10 + 2.0 * si * si;
-      bad = bad || dd <= t2 * fro2;
       z[j - 1] = (na * detr + sgn * npa * deti) * idd;
       z[j] = (nb * detr + sgn * npb * deti) * idd;
 #pragma unroll
@@ -863,10 +870,87 @@ TSG_DEVINL bool sub8(double (&z)[8], int nr, unsigned code, int partner, double 
         if (r < j - 1) z[r] = fma(-T[r * R + j], z[j], fma(-T[r * R + j - 1], z[j - 1], z[r]));
     } else {
       const double dr = T[j * R + j] + sr;
-      const double p = __shfl_sync(0xffffffffu, z[j], partner);
-      const double dd = dr * dr + si * si;
+      const double dd = dr * dr + si * si, idd = rcp_pos(dd);
       bad = bad || dd <= t2;
-      z[j] = (z[j] * dr + sgn * p * si) * (1.0 / dd);
+      const double p = __shfl_sync(0xffffffffu, z[j], partner);
+      z[j] = (z[j] * dr + sgn * p * si) * idd;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r < j) z[r] = fma(-T[r * R + j], z[j], z[r]);
+    }
+  }
+  return bad;
+}
+
+// 1/q for q > 0 (a sum of squares): MUFU reciprocal estimate and three
+// Newton steps, branch-free (the IEEE division's slow-path check is a call)
+TSG_DEVINL double rcp_pos(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  return fma(r, e, r);
+}
+
+template <bool PRO>
+TSG_DEVINL bool sub8(double (&z)[8], int nr, unsigned code, int partner, double sgn, double sr, double si,
+                     double t2, const double* T) {
+  if (!PRO) return sub8c(z, nr, code, partner, sgn, sr, si, t2, T);
+  constexpr int R = 8;
+  // the pivots first: independent of the data, so the eight reciprocals
+  // overlap instead of sitting on the substitution chain.  1x1 row j:
+  // d = T_jj + s, 1/|d|^2; second row of a 2x2 cell: the shifted cell's
+  // determinant and 1/|det|^2.
+  double pr[R], pi[R], pv[R];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const bool two = ((code >> (2 * j)) & 3u) == 2u && j >= 1;
+    const double djj = T[j * R + j] + sr;
+    double q = djj * djj + si * si;
+    pr[j] = djj;
+    pi[j] = si;
+    if (j >= 1) {
+      const double m00r = T[(j - 1) * R + j - 1] + sr, m01 = T[(j - 1) * R + j], m10 = T[j * R + j - 1];
+      const double detr = m00r * djj - si * si - m01 * m10, deti = si * (m00r + djj);
+      const double q2 = detr * detr + deti * deti;
+      const double fro2 = m00r * m00r + djj * djj + m01 * m01 + m10 * m10 + 2.0 * si * si;
+      pr[j] = two ? detr : djj;
+      pi[j] = two ? deti : si;
+      const bool sing = two ? q2 <= t2 * fro2 : q <= t2;
+      q = two ? q2 : q;
+      const unsigned c = (code >> (2 * j)) & 3u;
+      bad = bad || (j < nr && c != 1u && sing);
+    } else {
+      bad = bad || (nr > 0 && (code & 3u) == 0u && q <= t2);
+    }
+    pv[j] = rcp_pos(q);
+  }
+#pragma unroll
+  for (int j = R - 1; j >= 0; --j) {
+    if (j >= nr) continue;
+    const unsigned c = (code >> (2 * j)) & 3u;
+    if (c == 1u) continue;  // first row of a pair: solved with its second row
+    if (c == 2u && j >= 1) {
+      const double m00r = T[(j - 1) * R + j - 1] + sr, m11r = T[j * R + j] + sr;
+      const double m01 = T[(j - 1) * R + j], m10 = T[j * R + j - 1];
+      const double pa = __shfl_sync(0xffffffffu, z[j - 1], partner);
+      const double pb = __shfl_sync(0xffffffffu, z[j], partner);
+      const double na = m11r * z[j - 1] - sgn * si * pa - m01 * z[j];
+      const double nb = m00r * z[j] - sgn * si * pb - m10 * z[j - 1];
+      const double npa = __shfl_sync(0xffffffffu, na, partner);
+      const double npb = __shfl_sync(0xffffffffu, nb, partner);
+      z[j - 1] = (na * pr[j] + sgn * npa * pi[j]) * pv[j];
+      z[j] = (nb * pr[j] + sgn * npb * pi[j]) * pv[j];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r < j - 1) z[r] = fma(-T[r * R + j], z[j], fma(-T[r * R + j - 1], z[j - 1], z[r]));
+    } else {
+      const double p = __shfl_sync(0xffffffffu, z[j], partner);
+      z[j] = (z[j] * pr[j] + sgn * p * pi[j]) * pv[j];
 #pragma unroll
       for (int r = 0; r < R; ++r)
         if (r < j) z[r] = fma(-T[r * R + j], z[j], z[r]);
@@ -918,7 +1002,7 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
   __shared__ WideTab W;
   __shared__ int64_t pb[1 << kFibreMaxS];
   __shared__ int soff[kFibreMaxS + 1];
-  __shared__ int hwslot[kWideThreads / 32], lead[kWideTeams];
+  __shared__ int hwslot[kWideThreads / 32], wrole[kWideThreads / 32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   pdl_wait();
@@ -944,15 +1028,21 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
     Td[e] = (i < ie && j < je) ? a.Tt[static_cast<size_t>(i) * nf + j] : 0.0;
   }
   __syncthreads();
-  // leader of each team: its warp on sub-partition 0 (slot = 0 mod 4) if any
-  if (threadIdx.x < kWideTeams) {
-    const int t = threadIdx.x;
-    int best = 0, bd = 4;
-    for (int u = 0; u < kTeamWarps; ++u) {
-      const int dd = hwslot[t * kTeamWarps + u] & 3;
-      if (dd < bd) bd = dd, best = u;
-    }
-    lead[t] = best;
+  if (threadIdx.x == 0) {
+    // role = team * 4 + tw (tw 0 leader, 1/2 helpers), or -1 (loads/stores only)
+    int ord[kWideThreads / 32];
+    for (int i = 0; i < nw; ++i) ord[i] = i;
+    for (int i = 1; i < nw; ++i)  // by sub-partition, stable
+      for (int j = i; j > 0 && (hwslot[ord[j]] & 3) < (hwslot[ord[j - 1]] & 3); --j) {
+        const int t = ord[j];
+        ord[j] = ord[j - 1];
+        ord[j - 1] = t;
+      }
+    for (int i = 0; i < nw; ++i) wrole[i] = -1;
+    for (int t = 0; t < kWideTeams; ++t) wrole[ord[t]] = 4 * t;
+    int k = kWideTeams;
+    for (int hh = 1; hh < kTeamWarps; ++hh)
+      for (int t = 0; t < kWideTeams; ++t) wrole[ord[k++]] = 4 * t + hh;
   }
   if (scell)
     for (int s = 0; s < a.ns; ++s)
@@ -1063,9 +1153,9 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
     __syncthreads();
     WP_ADD(1, tb);
     const int ngrp = W.nslot >> 4;
-    const int team = warp / kTeamWarps;
-    const int tw = (warp % kTeamWarps - lead[team] + kTeamWarps) % kTeamWarps;  // 0 leader, 1/2 helpers
-    for (int grp = team; grp < ngrp; grp += kWideTeams) {
+    const int team = wrole[warp] >> 2;
+    const int tw = wrole[warp] < 0 ? kTeamWarps : wrole[warp] & 3;  // 0 leader, 1/2 helpers
+    for (int grp = team; tw < kTeamWarps && grp < ngrp; grp += kWideTeams) {
       const int s0 = grp << 4;
       int cb0 = W.col[s0 + g], cb1 = W.col[s0 + 8 + g];  // B-fragment columns
       cb0 = cb0 >= 0 ? cb0 : zcol;
@@ -1129,7 +1219,7 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
           const double* T3 = Td + 192 * q;
           bool bad = false;
           if (nh > 0) {
-            bad = sub8(zh, nh, a.rbcode[2 * q + 1], partner, sgn, mysr, mysi, t2, T3 + 64);
+            bad = sub8<SUB8_PRO>(zh, nh, a.rbcode[2 * q + 1], partner, sgn, mysr, mysi, t2, T3 + 64);
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
               double acc = zl[r];
@@ -1138,7 +1228,7 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
               zl[r] = acc;
             }
           }
-          bad = sub8(zl, nl, a.rbcode[2 * q], partner, sgn, mysr, mysi, t2, T3) || bad;
+          bad = sub8<SUB8_PRO>(zl, nl, a.rbcode[2 * q], partner, sgn, mysr, mysi, t2, T3) || bad;
           if (own) {
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
@@ -1208,8 +1298,11 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
 #endif
   }
 #if WIDE_PROF
-  if (a.prof && lane == 0)
+  if (a.prof && lane == 0) {
     for (int k = 0; k < 7; ++k) atomicAdd(a.prof + k, static_cast<unsigned long long>(ph[k]));
+    // sub-partition histogram of leaders (8..11) and helpers (12..15)
+    if (wrole[warp] >= 0) atomicAdd(a.prof + ((wrole[warp] & 3) == 0 ? 8 : 12) + (hwslot[warp] & 3), 1ull);
+  }
 #endif
   if (badoff != LLONG_MAX) atomicMin(a.status, static_cast<int>(badoff < INT_MAX - 1 ? badoff : INT_MAX - 1));
   pdl_trigger();
