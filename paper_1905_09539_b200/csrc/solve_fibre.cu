@@ -403,6 +403,7 @@ struct SmallBuf {
   int64_t blk;
   int nunit;
   int job0[kMaxUnits + 1];
+  int64_t pb[1 << kFibreMaxS];  // element offset of every pattern's run at row 0 of f
 };
 
 TSG_DEVINL void decode_block(const FibreArgs& a, const FibreCell* scell, const int* soff, int64_t blk,
@@ -437,17 +438,43 @@ TSG_DEVINL void decode_block(const FibreArgs& a, const FibreCell* scell, const i
   B.ncol = B.w << kb;
 }
 
+TSG_DEVINL void block_patterns(const Blk& B, int64_t* pb) {
+  for (int b = 0; b < (1 << B.kb); ++b) {
+    int64_t o = B.base;
+    for (int t = 0; t < B.kb; ++t)
+      if ((b >> t) & 1) o += B.bstride[t];
+    pb[b] = o;
+  }
+}
+
+// Rows of a block <-> shared memory: the run of w contiguous mode-0
+// elements of (row i of f, pattern b) is at X + pb[b] + i * sf and at
+// Y + i * pitch + b * w.  Each warp instruction moves 32 / wp runs
+// (wp = w rounded up to a power of two, at most 32), no divisions.
+template <bool LOAD>
+TSG_DEVINL void rows_io(const FibreArgs& a, double* Y, int pitch, const int64_t* pb, int w, int kb) {
+  const int nf = a.nf, nb = 1 << kb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int lw = 0;
+  while ((1 << lw) < w && lw < 5) ++lw;
+  const int sub = lane >> lw, r0 = lane & ((1 << lw) - 1), rpi = 32 >> lw;
+  const int step = nw * rpi;  // runs per sweep of all warps
+  for (int run = warp * rpi + sub; run < nf * nb; run += step) {
+    const int i = run >> kb, b = run & (nb - 1);
+    double* y = Y + static_cast<size_t>(i) * pitch + b * w;
+    const double* x = a.X + pb[b] + static_cast<int64_t>(i) * a.sf;
+    for (int r = r0; r < w; r += 1 << lw) {
+      if (LOAD) cp_async8(y + r, x + r, 8);
+      else *const_cast<double*>(x + r) = y[r];
+    }
+  }
+}
+
 // cp.async of a block's rows (8-byte granules: rows start at any element)
 // and of its chunk's unit table
-TSG_DEVINL void issue_block(const FibreArgs& a, const Blk& B, int nunit, double* Y, int pitch,
+TSG_DEVINL void issue_block(const FibreArgs& a, const Blk& B, const int64_t* pb, int nunit, double* Y, int pitch,
                             FibreUnit* su) {
-  const int nf = a.nf, w = B.w, nb = 1 << B.kb;
-  const int tot = nf * nb * w;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int row = e / w, r = e - row * w;
-    const int i = row / nb, b = row - i * nb;
-    cp_async8(Y + static_cast<size_t>(i) * pitch + b * w + r, a.X + goff(B, b * w, i, a.sf) + r, 8);
-  }
+  rows_io<true>(a, Y, pitch, pb, B.w, B.kb);
   const char* src = reinterpret_cast<const char*>(a.units + B.njob);
   char* dst = reinterpret_cast<char*>(su);
   for (int e = threadIdx.x; e < nunit * static_cast<int>(sizeof(FibreUnit) / 8); e += blockDim.x)
@@ -494,10 +521,13 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
   if (threadIdx.x == 0) {
     const int64_t b0 = atomicAdd(a.counter, 1);
     SB[0].blk = b0;
-    if (b0 < a.nblocks) decode_block(a, nullptr, soff, b0, SB[0].B, SB[0].nunit);
+    if (b0 < a.nblocks) {
+      decode_block(a, nullptr, soff, b0, SB[0].B, SB[0].nunit);
+      block_patterns(SB[0].B, SB[0].pb);
+    }
   }
   __syncthreads();
-  if (SB[0].blk < a.nblocks) issue_block(a, SB[0].B, SB[0].nunit, Ys[0], SB[0].B.ncol, sus[0]);
+  if (SB[0].blk < a.nblocks) issue_block(a, SB[0].B, SB[0].pb, SB[0].nunit, Ys[0], SB[0].B.ncol, sus[0]);
   int cur = 0;
   for (;;) {
     SmallBuf& C = SB[cur];
@@ -507,12 +537,15 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
     if (threadIdx.x == 0) {
       const int64_t nb = atomicAdd(a.counter, 1);
       Nx.blk = nb;
-      if (nb < a.nblocks) decode_block(a, scell, soff, nb, Nx.B, Nx.nunit);
+      if (nb < a.nblocks) {
+        decode_block(a, scell, soff, nb, Nx.B, Nx.nunit);
+        block_patterns(Nx.B, Nx.pb);
+      }
     }
     __syncthreads();
     const bool more = Nx.blk < a.nblocks;
     if (more) {
-      issue_block(a, Nx.B, Nx.nunit, Ys[cur ^ 1], Nx.B.ncol, sus[cur ^ 1]);
+      issue_block(a, Nx.B, Nx.pb, Nx.nunit, Ys[cur ^ 1], Nx.B.ncol, sus[cur ^ 1]);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -564,15 +597,7 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
       if (k >= 2) unit_butterfly<true>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
     }
     __syncthreads();
-    {
-      const int nb = 1 << kb;
-      const int tot = nf * nb * w;
-      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int row = e / w, r = e - row * w;
-        const int i = row / nb, b = row - i * nb;
-        a.X[goff(B, b * w, i, a.sf) + r] = Y[static_cast<size_t>(i) * ncol + b * w + r];
-      }
-    }
+    rows_io<false>(a, Y, ncol, C.pb, w, kb);
     __syncthreads();
     cur ^= 1;
   }
@@ -620,13 +645,16 @@ __global__ void __launch_bounds__(kBigThreads, 2) fibre_big_kernel(const FibreAr
   for (;;) {
     if (threadIdx.x == 0) {
       SB.blk = atomicAdd(a.counter, 1);
-      if (SB.blk < a.nblocks) decode_block(a, scell, soff, SB.blk, SB.B, SB.nunit);
+      if (SB.blk < a.nblocks) {
+        decode_block(a, scell, soff, SB.blk, SB.B, SB.nunit);
+        block_patterns(SB.B, SB.pb);
+      }
     }
     __syncthreads();
     if (SB.blk >= a.nblocks) break;
     const Blk& B = SB.B;
     const int nunit = SB.nunit;
-    issue_block(a, B, nunit, Y, pitch, su);
+    issue_block(a, B, SB.pb, nunit, Y, pitch, su);
     cp_async_wait<0>();
     __syncthreads();
     const int ncol = B.ncol, w = B.w, kb = B.kb;
