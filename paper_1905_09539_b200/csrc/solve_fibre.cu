@@ -93,6 +93,19 @@ TSG_DEVINL void butterflies(const FibreArgs& a, const Blk& B, double* Y, bool in
   }
 }
 
+// 1/q for q > 0 (a sum of squares): MUFU reciprocal estimate and three
+// Newton steps, branch-free (the IEEE division's slow-path check is a call)
+TSG_DEVINL double rcp_pos(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Back substitution of one complex (or real, im < 0) fibre along f.
 TSG_DEVINL void solve_job(const FibreArgs& a, const double* T, double* Y, int ncol, int re, int im,
                           double sr, double si, int64_t off_hint) {
@@ -352,11 +365,11 @@ TSG_DEVINL void solve_job_reg(const FibreArgs& a, const double* T, const double*
       const double m01 = T[(j - 1) * NF + j], m10 = T[j * NF + j - 1];
       const double detr = m00r * m11r - si * si - m01 * m10, deti = si * (m00r + m11r);
       const double ea = fc[3 * j + 1] + sr, ew = fc[3 * j + 2];
-      bad = bad || fmin(hypot(ea, si + ew), hypot(ea, si - ew)) <= a.tiny;
+      bad = bad || fmin(ea * ea + (si + ew) * (si + ew), ea * ea + (si - ew) * (si - ew)) <= a.tiny * a.tiny;
       const double ar = zr[j - 1], ai = zi[j - 1], rr = zr[j], ri = zi[j];
       const double nar = m11r * ar - si * ai - m01 * rr, nai = m11r * ai + si * ar - m01 * ri;
       const double nbr = m00r * rr - si * ri - m10 * ar, nbi = m00r * ri + si * rr - m10 * ai;
-      const double dd = detr * detr + deti * deti, ir = detr / dd, ii = -deti / dd;
+      const double idd = rcp_pos(detr * detr + deti * deti), ir = detr * idd, ii = -deti * idd;
       zr[j - 1] = nar * ir - nai * ii;
       zi[j - 1] = nar * ii + nai * ir;
       zr[j] = nbr * ir - nbi * ii;
@@ -371,10 +384,11 @@ TSG_DEVINL void solve_job_reg(const FibreArgs& a, const double* T, const double*
       }
     } else {
       const double dr = T[j * NF + j] + sr, dd = dr * dr + si * si;
-      bad = bad || sqrt(dd) <= a.tiny;
+      bad = bad || dd <= a.tiny * a.tiny;
+      const double idd = rcp_pos(dd);
       const double rr = zr[j], ri = zi[j];
-      zr[j] = (rr * dr + ri * si) / dd;
-      zi[j] = (ri * dr - rr * si) / dd;
+      zr[j] = (rr * dr + ri * si) * idd;
+      zi[j] = (ri * dr - rr * si) * idd;
 #pragma unroll
       for (int i = 0; i < NF; ++i) {
         if (i < j) {
@@ -868,7 +882,6 @@ struct WideTab {
 // warp-uniform, so every lane runs every shuffle.  Returns "numerically
 // singular" (|det| <= tiny ||M||_F for a shifted 2x2 cell, |d| <= tiny for
 // a 1x1 cell).
-TSG_DEVINL double rcp_pos(double q);
 TSG_DEVINL bool sub8c(double (&z)[8], int nr, unsigned code, int partner, double sgn, double sr, double si,
                       double t2, const double* T) {
   constexpr int R = 8;
@@ -908,19 +921,6 @@ TSG_DEVINL bool sub8c(double (&z)[8], int nr, unsigned code, int partner, double
     }
   }
   return bad;
-}
-
-// 1/q for q > 0 (a sum of squares): MUFU reciprocal estimate and three
-// Newton steps, branch-free (the IEEE division's slow-path check is a call)
-TSG_DEVINL double rcp_pos(double q) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-  double e = fma(-q, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-q, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-q, r, 1.0);
-  return fma(r, e, r);
 }
 
 template <bool PRO>
