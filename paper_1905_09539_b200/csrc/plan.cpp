@@ -426,7 +426,7 @@ void tile_eigvecs(std::vector<tsg::TileMode>& tms, const std::vector<double>& dh
   }
 }
 
-int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U);
+int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U, const double* Tc);
 int enqueue(tsg_plan* pl, const double* in, double* out, cudaStream_t st, bool timing);
 
 }  // namespace
@@ -575,7 +575,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   }
   pl->tiny = 0.5 * std::numeric_limits<double>::epsilon() * scale;
   {
-    const int rc = try_decouple(pl.get(), T, U);
+    const int rc = try_decouple(pl.get(), T, U, Tc);
     if (rc != TSG_OK) return rc;
   }
   if (pl->decoupled) {
@@ -611,9 +611,10 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
       snm1 += dims[m] - 1;
     }
     const double Nd = static_cast<double>(pl->N);
-    pl->flops_alg = Nd * snm1 + 4.0 * Nd * sn;
+    pl->flops_alg = (family == 0 ? Nd * snm1 : Nd * ((dims[0] - 1) + sn)) + 4.0 * Nd * sn;
     // complex back substitution: n_f^2 real FMA per pair of real fibres
-    pl->flops_exec = Nd * dims[pl->dec_f] + 4.0 * Nd * sn;
+    // (gsylv: two triangular factors, S and Tc)
+    pl->flops_exec = (family == 0 ? 1.0 : 2.0) * Nd * dims[pl->dec_f] + 4.0 * Nd * sn;
     TSG_CU(pl->w1.ensure(pl->N));
     TSG_CU(pl->w2.ensure(pl->N));
     *out = pl.release();
@@ -1773,44 +1774,67 @@ cudaError_t upload_owned(tsg_plan* pl, const V& v, const typename V::value_type*
   return e;
 }
 
-// Eigen-decoupled path: Laplace plans with transforms, every
+// Eigen-decoupled path.  Laplace plans with transforms: every
 // mode but one free mode f > 0 with a well-conditioned real block-eigenbasis
-// (prod kappa_2 <= kDecoupleKappa).  TSG_DECOUPLE=0 turns it off,
-// TSG_DECOUPLE_NFMAX bounds n_f (default 1024).
-int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
+// (prod kappa_2 <= kDecoupleKappa); the fibres along f are solved with the
+// Kronecker SUM of the other modes' eigenvalues as shift.  gsylv plans: the
+// tail modes 1..d-1 in their eigenbases, f = 0: the pencil (S + z Tc) per
+// fibre with z the PRODUCT of the tail eigenvalues (wide kernel only).  The
+// chunk mode (whose cells form a block's units) is mode 0 for Laplace and
+// mode 1 for gsylv.  TSG_DECOUPLE=0 turns it off, TSG_DECOUPLE_NFMAX bounds
+// n_f (default 1024).
+int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U, const double* Tc) {
   tsg_ctx* ctx = pl->ctx;
   const int d = pl->d;
   const int* dims = pl->dims.data();
+  const bool gs = pl->family == 1;
   const char* env = std::getenv("TSG_DECOUPLE");
-  if (pl->family != 0 || pl->reduced_only || tsg_impl::g_force_lap3 || (env && std::atoi(env) == 0))
-    return TSG_OK;
-  if (d - 1 > tsg::kFibreMaxS) return TSG_OK;
+  if (pl->reduced_only || tsg_impl::g_force_lap3 || (env && std::atoi(env) == 0)) return TSG_OK;
+  if (pl->family > 1 || d < 2) return TSG_OK;
+  const int cm = gs ? 1 : 0;  // chunk mode
+  if (gs ? d - 2 > tsg::kFibreMaxS : d - 1 > tsg::kFibreMaxS) return TSG_OK;
   const char* ne = std::getenv("TSG_DECOUPLE_NFMAX");
   const int nfmax = ne ? std::atoi(ne) : 1024;
-  bool any = false;
-  for (int f = 1; f < d; ++f) any = any || dims[f] <= nfmax;
-  if (!any) return TSG_OK;
   std::vector<tsg_impl::ModeEigen> me(d);
-  std::vector<int> ok(d);
-  for (int m = 0; m < d; ++m) ok[m] = tsg_impl::mode_eigen(T[m], dims[m], me[m]) ? 1 : 0;
+  std::vector<int> ok(d, 0);
+  for (int m = gs ? 1 : 0; m < d; ++m) ok[m] = tsg_impl::mode_eigen(T[m], dims[m], me[m]) ? 1 : 0;
   int best = -1;
   double best_prod = 0;
-  for (int f = 1; f < d; ++f) {
-    if (dims[f] > nfmax) continue;
+  if (gs) {
     double prod = 1;
-    for (int m = 0; m < d; ++m)
-      if (m != f) prod *= ok[m] ? me[m].kappa : 1e300;
-    if (!(prod <= tsg_impl::kDecoupleKappa)) continue;
-    const double kf = ok[f] ? me[f].kappa : 1e300;
-    if (best < 0 || dims[f] < dims[best] || (dims[f] == dims[best] && kf > (ok[best] ? me[best].kappa : 1e300))) {
-      best = f;
+    for (int m = 1; m < d; ++m) prod *= ok[m] ? me[m].kappa : 1e300;
+    if (dims[0] <= nfmax && prod <= tsg_impl::kDecoupleKappa) {
+      best = 0;
       best_prod = prod;
+    }
+  } else {
+    for (int f = 1; f < d; ++f) {
+      if (dims[f] > nfmax) continue;
+      double prod = 1;
+      for (int m = 0; m < d; ++m)
+        if (m != f) prod *= ok[m] ? me[m].kappa : 1e300;
+      if (!(prod <= tsg_impl::kDecoupleKappa)) continue;
+      const double kf = ok[f] ? me[f].kappa : 1e300;
+      if (best < 0 || dims[f] < dims[best] || (dims[f] == dims[best] && kf > (ok[best] ? me[best].kappa : 1e300))) {
+        best = f;
+        best_prod = prod;
+      }
     }
   }
   if (best < 0) return TSG_OK;
   const int f = best;
   const int nf = dims[f];
-  {
+  // S' = the eigen modes other than the chunk mode
+  std::vector<int> sp;
+  for (int m = 0; m < d; ++m)
+    if (m != f && m != cm) sp.push_back(m);
+  int nsc = 0;
+  for (int m : sp) {
+    bool cx = false;
+    for (const auto& c : me[m].cells) cx = cx || c.size == 2;
+    nsc += cx ? 1 : 0;
+  }
+  if (!gs) {
     const std::vector<int8_t> code = block_codes(T[f], nf);
     for (int i = 0; i < nf; ++i)
       if (code[i] == 1) {
@@ -1818,13 +1842,6 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
                      q = at(T[f], nf, i + 1, i + 1);
         if (!(0.25 * (p - q) * (p - q) + b * c < 0)) return TSG_OK;  // not in standard form
       }
-    int nsc = 0;
-    for (int m = 1; m < d; ++m) {
-      if (m == f) continue;
-      bool cx = false;
-      for (const auto& c : me[m].cells) cx = cx || c.size == 2;
-      nsc += cx ? 1 : 0;
-    }
     const size_t tb = nf <= 64 ? static_cast<size_t>(nf) * nf * 8 : 0;
     if (100 * 1024 <= tb + ((static_cast<size_t>(nf) * 8 + 4) << nsc) * 2) return TSG_OK;
   }
@@ -1832,6 +1849,8 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
   a = tsg::FibreArgs{};
   a.nf = nf;
   a.sf = pl->stride[f];
+  a.gs = gs ? 1 : 0;
+  a.sc = pl->stride[cm];
   {
     std::vector<double> tt(static_cast<size_t>(nf) * nf), fc(4 * static_cast<size_t>(nf), 0.0);
     for (int i = 0; i < nf; ++i)
@@ -1839,7 +1858,7 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
     const std::vector<int8_t> code = block_codes(T[f], nf);
     for (int i = 0; i < nf; ++i) {
       fc[4 * i] = code[i];
-      if (code[i] == 1) {
+      if (code[i] == 1 && !gs) {
         const double p = at(T[f], nf, i, i), b = at(T[f], nf, i, i + 1), c = at(T[f], nf, i + 1, i),
                      q = at(T[f], nf, i + 1, i + 1);
         const double disc = 0.25 * (p - q) * (p - q) + b * c;
@@ -1854,31 +1873,30 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
     }
     TSG_CU(upload_owned(pl, tt, &a.Tt));
     TSG_CU(upload_owned(pl, fc, &a.fcell));
+    if (gs) {
+      std::vector<double> tc(static_cast<size_t>(nf) * nf);
+      for (int i = 0; i < nf; ++i)
+        for (int j = 0; j < nf; ++j) tc[static_cast<size_t>(i) * nf + j] = Tc[i + static_cast<size_t>(j) * nf];
+      TSG_CU(upload_owned(pl, tc, &a.Tct));
+    }
   }
-  // S modes other than 0, in mode order
-  int nsc = 0;
   int64_t nblk_rest = 1;
-  for (int m = 1; m < d; ++m) {
-    if (m == f) continue;
+  for (int m : sp) {
     const int s = a.ns++;
     a.sstride[s] = pl->stride[m];
     a.ncell[s] = static_cast<int>(me[m].cells.size());
     TSG_CU(upload_owned(pl, me[m].cells, &a.cells[s]));
-    bool cx = false;
-    for (const auto& c : me[m].cells) cx = cx || c.size == 2;
-    nsc += cx ? 1 : 0;
     nblk_rest *= a.ncell[s];
   }
-  // mode-0 chunks of whole cells within the shared-memory budget: the
-  // register kernel for n_f <= 24 (three CTAs per SM), else the warp-group
-  // DMMA kernel (blocks of <= kWideCols real columns; fewer when a long free
-  // mode would not leave room for two CTAs per SM), else the DMMA-blocked
-  // kernel (TSG_FIBRE_WIDE=0)
-  const bool small = nf <= 24;
+  // chunks of whole chunk-mode cells within the shared-memory budget: the
+  // register kernel for n_f <= 24 (three CTAs per SM), else the team DMMA
+  // kernel (blocks of <= kWideCols real columns; fewer when a long free mode
+  // would not leave room for two CTAs per SM), else the DMMA-blocked kernel
+  // (TSG_FIBRE_WIDE=0; Laplace only)
+  const bool small = nf <= 24 && !gs;
   int W = 0;
   int ncell_s = 0;
-  for (int m = 1; m < d; ++m)
-    if (m != f) ncell_s += static_cast<int>(me[m].cells.size());
+  for (int m : sp) ncell_s += static_cast<int>(me[m].cells.size());
   const int cell_smem = ncell_s <= 1024 ? ncell_s : 0;
   bool wide = false;
   if (small) {
@@ -1888,26 +1906,29 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
     W = static_cast<int>(std::min<long>(avail / (2 * (static_cast<long>(nf) << nsc)), 128));
   } else {
     const char* we = std::getenv("TSG_FIBRE_WIDE");
-    if (!(we && std::atoi(we) == 0)) {
+    if (gs || !(we && std::atoi(we) == 0)) {
       for (int mc = tsg::kWideCols; mc >= 8 && !wide; mc /= 2) {
-        if (tsg::fibre_wide_smem(nf, mc, cell_smem) > 110 * 1024) continue;
+        if (tsg::fibre_wide_smem(nf, mc, cell_smem, 0, gs ? 1 : 0) > 110 * 1024) continue;
         W = mc >> nsc;
         wide = W >= 2;
       }
     }
     if (!wide) {
+      if (gs) return TSG_OK;
       const size_t per_row = (static_cast<size_t>(nf) * 8 + 24) << nsc;
       const size_t fixed = static_cast<size_t>(nf) * 16 * 8 + 128 * 32 + 16 + cell_smem * 24;
       W = 108 * 1024 > fixed ? static_cast<int>(std::min<size_t>((108 * 1024 - fixed) / per_row, 128)) : 0;
     }
   }
-  std::vector<int> chunk{0}, cellrow0(dims[0]);
-  const auto& c0 = me[0].cells;
+  if (W < 2) return TSG_OK;  // not admissible: the tile kernels keep the plan
+  const int ncm = dims[cm];
+  std::vector<int> chunk{0}, cellrow0(ncm);
+  const auto& c0 = me[cm].cells;
   for (int c = 0; c < static_cast<int>(c0.size()); ++c) {
     for (int r = c0[c].start; r < c0[c].start + c0[c].size; ++r) cellrow0[r] = c;
     if (c0[c].start + c0[c].size - chunk.back() > W) chunk.push_back(c0[c].start);
   }
-  chunk.push_back(dims[0]);
+  chunk.push_back(ncm);
   int wmax = 0;
   for (size_t q = 0; q + 1 < chunk.size(); ++q) wmax = std::max(wmax, chunk[q + 1] - chunk[q]);
   a.nchunk = static_cast<int>(chunk.size()) - 1;
@@ -1936,11 +1957,12 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
   TSG_CU(upload_owned(pl, cellrow0, &a.cellrow0));
   TSG_CU(upload_owned(pl, c0, &a.cell0));
   a.maxcol = wmax << nsc;
-  a.small = tsg::fibre_small_ok(nf, wmax) ? 1 : 0;
+  a.small = small && tsg::fibre_small_ok(nf, wmax) ? 1 : 0;
   if (const char* e = std::getenv("TSG_FIBRE_SMALL")) a.small = a.small && std::atoi(e) != 0;
   a.wide = !a.small && wide ? 1 : 0;
   a.big = a.small || a.wide ? 0 : 1;
   if (const char* e = std::getenv("TSG_FIBRE_BIG")) a.big = a.big && std::atoi(e) != 0;
+  if (gs && !a.wide) return TSG_OK;
   if (a.big || a.wide) {
     // row blocks of f: <= 8 rows, never splitting a 2x2 cell
     const std::vector<int8_t> code = block_codes(T[f], nf);
@@ -1959,7 +1981,7 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
     a.pitch = tsg::fibre_pitch(a.maxcol);
   }
   a.nblocks = static_cast<int64_t>(a.nchunk) * nblk_rest;
-  // folded transforms of the S modes
+  // folded transforms of the eigen modes (gsylv mode 0 keeps Q^T / Z)
   for (int m = 0; m < d; ++m) {
     if (m == f) continue;
     const int n = dims[m];
@@ -1978,12 +2000,12 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U) {
   pl->dec_f = f;
   pl->dec_kappa = best_prod;
   pl->tile_ext.assign(d, 2);
-  pl->tile_ext[0] = wmax;
+  pl->tile_ext[cm] = wmax;
   pl->tile_ext[f] = nf;
   pl->ntiles_mode.assign(d, 1);
-  if (std::getenv("TSG_VERBOSE"))
-    std::fprintf(stderr, "[tsg] decoupled solve: free mode %d (n=%d), prod kappa %.3g, blocks %lld, maxcol %d\n",
-                 f, nf, best_prod, static_cast<long long>(a.nblocks), a.maxcol);
+  if (pl->knobs.verbose)
+    std::fprintf(stderr, "[tsg] decoupled solve (%s): free mode %d (n=%d), prod kappa %.3g, blocks %lld, maxcol %d\n",
+                 gs ? "gsylv" : "laplace", f, nf, best_prod, static_cast<long long>(a.nblocks), a.maxcol);
   return TSG_OK;
 }
 

@@ -159,7 +159,10 @@ struct FibreArgs {
   double* X;                 // in place: B^ on entry, X^ on exit
   int nf;                    // extent of the free mode f
   int64_t sf;                // its stride
-  const double* Tt;          // T_f row-major (Tt[i * nf + j] = T_f(i, j))
+  const double* Tt;          // T_f row-major (Tt[i * nf + j] = T_f(i, j)); gsylv: S
+  int gs;                    // 1: gsylv pencil fibres (S + z Tc) x = b, f = 0, z a product of eigenvalues
+  const double* Tct;         // gsylv: Tc row-major
+  int64_t sc;                // stride of the chunk mode (Laplace: mode 0, 1; gsylv: mode 1, n_0)
   const double* fcell;       // per row of f: 4 doubles (code 0/1/2, a, omega, unused)
   int nchunk;
   const int* chunk_lo;       // nchunk + 1 mode-0 row bounds (whole cells)
@@ -192,6 +195,6 @@ int fibre_pitch(int maxcol);
 size_t fibre_big_smem(int nf, int maxcol, int cell_smem);
 // wide kernel: columns per block (maxcol bound) and its shared memory
 constexpr int kWideCols = 32;
-size_t fibre_wide_smem(int nf, int maxcol, int cell_smem, int nrb = 0);
+size_t fibre_wide_smem(int nf, int maxcol, int cell_smem, int nrb = 0, int gs = 0);
 
 }  // namespace tsg

@@ -46,9 +46,9 @@ struct Blk {
   double sreal;
 };
 
-TSG_DEVINL int64_t goff(const Blk& B, int col, int i, int64_t sf) {
+TSG_DEVINL int64_t goff(const Blk& B, int col, int i, int64_t sf, int64_t sc = 1) {
   const int r = col % B.w, b = col / B.w;
-  int64_t o = B.base + r + static_cast<int64_t>(i) * sf;
+  int64_t o = B.base + r * sc + static_cast<int64_t>(i) * sf;
 #pragma unroll
   for (int t = 0; t < kFibreMaxS; ++t)
     if (t < B.kb && ((b >> t) & 1)) o += B.bstride[t];
@@ -428,9 +428,11 @@ TSG_DEVINL void decode_block(const FibreArgs& a, const FibreCell* scell, const i
   B.w = a.chunk_lo[q + 1] - B.r_lo;
   B.njob = a.chunk_u0[q];  // first unit of the chunk (reused field)
   nunit = a.chunk_u0[q + 1] - a.chunk_u0[q];
-  int64_t base = B.r_lo;
+  // sreal: the 1x1 cells' share of the shift: their sum (Laplace) or
+  // product (gsylv: eigenvalues of a Kronecker product)
+  int64_t base = static_cast<int64_t>(B.r_lo) * a.sc;
   int kb = 0;
-  double sreal = 0.0;
+  double sreal = a.gs ? 1.0 : 0.0;
   for (int s = 0; s < a.ns; ++s) {
     const int64_t nx = rest / a.ncell[s];
     const int c = static_cast<int>(rest - nx * a.ncell[s]);
@@ -443,7 +445,7 @@ TSG_DEVINL void decode_block(const FibreArgs& a, const FibreCell* scell, const i
       B.bim[kb] = fc.im;
       ++kb;
     } else {
-      sreal += fc.re;
+      sreal = a.gs ? sreal * fc.re : sreal + fc.re;
     }
   }
   B.base = base;
@@ -987,6 +989,85 @@ TSG_DEVINL bool sub8(double (&z)[8], int nr, unsigned code, int partner, double 
   return bad;
 }
 
+// gsylv: in-block substitution of <= 8 rows of the pencil (S + z Tc) x = r
+// (S quasi-triangular, Tc upper triangular, z = zr + i zi per job), same lane
+// layout as sub8.  Right-looking: once x_j is final, r_k -= S_kj x_j +
+// Tc_kj (z x_j) for k < j; w[j] returns this lane's component of z x_j (the
+// coupling to the block above needs it).  The partner's component of x_j
+// follows from the shuffled numerators, so z x_j costs no extra shuffle.
+TSG_DEVINL bool sub8g(double (&x)[8], double (&wz)[8], int nr, unsigned code, int partner, double sgn, double zr,
+                      double zi, double t2, const double* TS, const double* TC) {
+  constexpr int R = 8;
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < R; ++j) wz[j] = 0.0;
+#pragma unroll
+  for (int j = R - 1; j >= 0; --j) {
+    if (j >= nr) continue;
+    const unsigned c = (code >> (2 * j)) & 3u;
+    if (c == 1u) continue;  // first row of a pair: solved with its second row
+    if (c == 2u && j >= 1) {
+      const int j0 = j - 1;
+      // M = S_cc + z Tc_cc (complex 2x2), entries (re, im)
+      const double m00r = TS[j0 * R + j0] + zr * TC[j0 * R + j0], m00i = zi * TC[j0 * R + j0];
+      const double m01r = TS[j0 * R + j] + zr * TC[j0 * R + j], m01i = zi * TC[j0 * R + j];
+      const double m10r = TS[j * R + j0] + zr * TC[j * R + j0], m10i = zi * TC[j * R + j0];
+      const double m11r = TS[j * R + j] + zr * TC[j * R + j], m11i = zi * TC[j * R + j];
+      const double detr = (m00r * m11r - m00i * m11i) - (m01r * m10r - m01i * m10i);
+      const double deti = (m00r * m11i + m00i * m11r) - (m01r * m10i + m01i * m10r);
+      const double pa = __shfl_sync(0xffffffffu, x[j0], partner);
+      const double pb = __shfl_sync(0xffffffffu, x[j], partner);
+      // own component of (p + i q) y: p y_own - sgn q y_partner
+      const double na = (m11r * x[j0] - sgn * m11i * pa) - (m01r * x[j] - sgn * m01i * pb);
+      const double nb = (m00r * x[j] - sgn * m00i * pb) - (m10r * x[j0] - sgn * m10i * pa);
+      const double npa = __shfl_sync(0xffffffffu, na, partner);
+      const double npb = __shfl_sync(0xffffffffu, nb, partner);
+      const double dd = detr * detr + deti * deti, idd = rcp_pos(dd);
+      const double fro2 = m00r * m00r + m00i * m00i + m01r * m01r + m01i * m01i + m10r * m10r + m10i * m10i +
+                          m11r * m11r + m11i * m11i;
+      bad = bad || dd <= t2 * fro2;
+      const double xa = (na * detr + sgn * npa * deti) * idd, xb = (nb * detr + sgn * npb * deti) * idd;
+      const double xap = (npa * detr - sgn * na * deti) * idd, xbp = (npb * detr - sgn * nb * deti) * idd;
+      x[j0] = xa;
+      x[j] = xb;
+      wz[j0] = zr * xa - sgn * zi * xap;
+      wz[j] = zr * xb - sgn * zi * xbp;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r < j0)
+          x[r] -= (TS[r * R + j0] * xa + TS[r * R + j] * xb) + (TC[r * R + j0] * wz[j0] + TC[r * R + j] * wz[j]);
+    } else {
+      const double mr = TS[j * R + j] + zr * TC[j * R + j], mi = zi * TC[j * R + j];
+      const double p = __shfl_sync(0xffffffffu, x[j], partner);
+      const double dd = mr * mr + mi * mi, idd = rcp_pos(dd);
+      bad = bad || dd <= t2;
+      const double xo = (x[j] * mr + sgn * p * mi) * idd, xp = (p * mr - sgn * x[j] * mi) * idd;
+      x[j] = xo;
+      wz[j] = zr * xo - sgn * zi * xp;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r < j) x[r] -= TS[r * R + j] * xo + TC[r * R + j] * wz[j];
+    }
+  }
+  return bad;
+}
+
+// gsylv blocks: the free mode is mode 0 (contiguous fibres); column
+// (pattern b, chunk row r) of the block is the fibre at X + pb[b] + r * sc.
+template <bool LOAD>
+TSG_DEVINL void gs_rows(const FibreArgs& a, double* Y, int pitch, const int64_t* pb, int w, int kb) {
+  const int nf = a.nf, ncol = w << kb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int col = warp; col < ncol; col += nw) {
+    const int b = col / w, r = col - b * w;
+    const double* x = a.X + pb[b] + static_cast<int64_t>(r) * a.sc;
+    for (int i = lane; i < nf; i += 32) {
+      if (LOAD) cp_async8(Y + static_cast<size_t>(i) * pitch + col, x + i, 8);
+      else *const_cast<double*>(x + i) = Y[static_cast<size_t>(i) * pitch + col];
+    }
+  }
+}
+
 // Rows of the block <-> shared memory: the run of w contiguous mode-0
 // elements of (row i of f, pattern b) is at X + pb[b] + i * sf.  Each warp
 // instruction moves 32 / wp such runs (wp = w rounded up to a power of two).
@@ -1016,7 +1097,9 @@ TSG_DEVINL void wide_rows(const FibreArgs& a, double* Y, int pitch, const int64_
 // Shared-memory layout: Y (n_f x pitch), then per super-block s three 8x8
 // blocks of T_f, row-major: [0] T[lo, lo], [1] T[hi, hi], [2] T[lo, hi]
 // (zero padded), then the unit table and the optional S' cell table.
+template <bool GS>
 __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArgs a) {
+  constexpr int TDS = GS ? 384 : 192;  // Td doubles per super-block (gsylv: S blocks, then Tc blocks)
   extern __shared__ __align__(16) double sm[];
   const int nf = a.nf;
   const int pitch = a.pitch;
@@ -1024,7 +1107,7 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
   const int nsb = (a.nrb + 1) >> 1;
   double* Y = sm;
   double* Td = Y + static_cast<size_t>(nf) * pitch;
-  FibreUnit* su = reinterpret_cast<FibreUnit*>(Td + 192 * static_cast<size_t>(nsb));
+  FibreUnit* su = reinterpret_cast<FibreUnit*>(Td + TDS * static_cast<size_t>(nsb));
   FibreCell* scell = a.cell_smem ? reinterpret_cast<FibreCell*>(su + kWideUnits) : nullptr;
   __shared__ SmallBuf SB;
   __shared__ WideTab W;
@@ -1048,12 +1131,13 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
     hwslot[warp] = static_cast<int>(hw);
   }
   for (int i = threadIdx.x; i < nf; i += blockDim.x) Y[static_cast<size_t>(i) * pitch + zcol] = 0.0;
-  for (int e = threadIdx.x; e < 192 * nsb; e += blockDim.x) {
-    const int sb = e / 192, part = (e / 64) % 3, r = (e >> 3) & 7, c = e & 7;
+  for (int e = threadIdx.x; e < TDS * nsb; e += blockDim.x) {
+    const int sb = e / TDS, ee = e % TDS, mat = ee / 192, part = (ee / 64) % 3, r = (e >> 3) & 7, c = e & 7;
     const int lo0 = a.rb[2 * sb], mid = a.rb[2 * sb + 1], hi1 = 2 * sb + 1 < a.nrb ? a.rb[2 * sb + 2] : mid;
     const int i = (part == 1 ? mid : lo0) + r, j = (part == 0 ? lo0 : mid) + c;
     const int ie = part == 1 ? hi1 : mid, je = part == 0 ? mid : hi1;
-    Td[e] = (i < ie && j < je) ? a.Tt[static_cast<size_t>(i) * nf + j] : 0.0;
+    const double* src = mat ? a.Tct : a.Tt;
+    Td[e] = (i < ie && j < je) ? src[static_cast<size_t>(i) * nf + j] : 0.0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1104,7 +1188,8 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
         cp_async8(dst + 8 * e, src + 8 * e, 8);
     }
     __syncthreads();
-    wide_rows<true>(a, Y, pitch, pb, w, kb);
+    if (GS) gs_rows<true>(a, Y, pitch, pb, w, kb);
+    else wide_rows<true>(a, Y, pitch, pb, w, kb);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
@@ -1137,11 +1222,25 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
       const int l = (j - SB.job0[u]) << 1;
       W.jre[j] = ucol(l, rl0, pair0, w);
       W.jim[j] = k ? ucol(l | 1, rl0, pair0, w) : -1;
-      double sr = B.sreal + su[u].sr, si = su[u].si;
-      for (int t = 0; t < kb; ++t) {
-        const int bit = pair0 ? t + 1 : t;
-        sr += B.bre[t];
-        si += ((l >> bit) & 1) ? B.bim[t] : -B.bim[t];
+      double sr, si;
+      if (GS) {  // product of the cells' eigenvalues
+        sr = B.sreal * su[u].sr;
+        si = B.sreal * su[u].si;
+        for (int t = 0; t < kb; ++t) {
+          const int bit = pair0 ? t + 1 : t;
+          const double er = B.bre[t], ei = ((l >> bit) & 1) ? B.bim[t] : -B.bim[t];
+          const double nr = sr * er - si * ei;
+          si = sr * ei + si * er;
+          sr = nr;
+        }
+      } else {  // sum
+        sr = B.sreal + su[u].sr;
+        si = su[u].si;
+        for (int t = 0; t < kb; ++t) {
+          const int bit = pair0 ? t + 1 : t;
+          sr += B.bre[t];
+          si += ((l >> bit) & 1) ? B.bim[t] : -B.bim[t];
+        }
       }
       W.jsr[j] = sr;
       W.jsi[j] = si;
@@ -1152,10 +1251,11 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
       int s = 0;
       for (int j = 0; j < njob; ++j) {
         const bool cx = W.jim[j] >= 0;
-        if (cx && (s & 15) == 15) {
+        if (cx && (s & 1)) {  // complex jobs on even slots (a lane's two fragment columns)
           W.col[s] = -1;
           W.im[s] = -1;
           W.role[s] = 3;
+          W.sr[s] = W.si[s] = 0.0;
           ++s;
         }
         W.col[s] = W.jre[j];
@@ -1168,6 +1268,8 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
           W.col[s] = W.jim[j];
           W.im[s] = -1;
           W.role[s] = 1;
+          W.sr[s] = W.jsr[j];
+          W.si[s] = W.jsi[j];
           ++s;
         }
       }
@@ -1175,6 +1277,7 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
         W.col[s] = -1;
         W.im[s] = -1;
         W.role[s] = 3;
+        W.sr[s] = W.si[s] = 0.0;
       }
       W.nslot = s;
     }
@@ -1200,8 +1303,15 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
       const double mysr = role == 3 ? 0.0 : W.sr[js], mysi = (role == 0 || role == 1) ? W.si[js] : 0.0;
       // helper h (tw = 1 + h): 8-row block 2 s + h of every super-block s
       const int h = tw - 1;
-      double c[2][2][2] = {};  // [n-tile][k parity][2]: partial of the next super-block
-      double la[4];            // A fragments of T_f[rows, rows of s+1] (k = i1 + 4 t4 + st)
+      double c[2][2][2] = {};   // [n-tile][k parity][2]: partial of the next super-block (S / T_f)
+      double cz[2][2][2] = {};  // gsylv: the same with Tc (scaled by z per column when written)
+      double la[4], lt[4];      // A fragments of T_f (S) / Tc [rows, rows of s+1] (k = i1 + 4 t4 + st)
+      // gsylv: z of the lane's fragment columns (slots 2 t4, 2 t4 + 1 of each n-tile)
+      const bool fcx0 = GS && W.role[s0 + 2 * t4] == 0, fcx1 = GS && W.role[s0 + 8 + 2 * t4] == 0;
+      const double z0r = GS ? W.sr[s0 + 2 * t4] : 0.0, z0i = GS ? W.si[s0 + 2 * t4] : 0.0;
+      const double z1r = GS ? W.sr[s0 + 2 * t4 + 1] : 0.0;
+      const double z2r = GS ? W.sr[s0 + 8 + 2 * t4] : 0.0, z2i = GS ? W.si[s0 + 8 + 2 * t4] : 0.0;
+      const double z3r = GS ? W.sr[s0 + 9 + 2 * t4] : 0.0;
       for (int q = nsb - 1; q >= 0; --q) {
         const int i0 = a.rb[2 * q], mid = a.rb[2 * q + 1];
         const int i1 = 2 * q + 1 < a.nrb ? a.rb[2 * q + 2] : mid;
@@ -1221,14 +1331,38 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
               const double b0 = yk[kin ? cb0 : zcol], b1 = yk[kin ? cb1 : zcol];
               dmma(c[0][st & 1][0], c[0][st & 1][1], la[st], b0);
               dmma(c[1][st & 1][0], c[1][st & 1][1], la[st], b1);
+              if (GS) {
+                dmma(cz[0][st & 1][0], cz[0][st & 1][1], lt[st], b0);
+                dmma(cz[1][st & 1][0], cz[1][st & 1][1], lt[st], b1);
+              }
             }
             const int ra = r0 + g;
             if (ra < r1) {
+              double u00 = c[0][0][0] + c[0][1][0], u01 = c[0][0][1] + c[0][1][1];
+              double u10 = c[1][0][0] + c[1][1][0], u11 = c[1][0][1] + c[1][1][1];
+              if (GS) {  // + z (Tc x): complex (re, im) pair or two real columns
+                const double v00 = cz[0][0][0] + cz[0][1][0], v01 = cz[0][0][1] + cz[0][1][1];
+                const double v10 = cz[1][0][0] + cz[1][1][0], v11 = cz[1][0][1] + cz[1][1][1];
+                if (fcx0) {
+                  u00 += z0r * v00 - z0i * v01;
+                  u01 += z0r * v01 + z0i * v00;
+                } else {
+                  u00 += z0r * v00;
+                  u01 += z1r * v01;
+                }
+                if (fcx1) {
+                  u10 += z2r * v10 - z2i * v11;
+                  u11 += z2r * v11 + z2i * v10;
+                } else {
+                  u10 += z2r * v10;
+                  u11 += z3r * v11;
+                }
+              }
               double* yr = Y + static_cast<size_t>(ra) * pitch;
-              if (cw00 >= 0) yr[cw00] -= c[0][0][0] + c[0][1][0];
-              if (cw01 >= 0) yr[cw01] -= c[0][0][1] + c[0][1][1];
-              if (cw10 >= 0) yr[cw10] -= c[1][0][0] + c[1][1][0];
-              if (cw11 >= 0) yr[cw11] -= c[1][0][1] + c[1][1][1];
+              if (cw00 >= 0) yr[cw00] -= u00;
+              if (cw01 >= 0) yr[cw01] -= u01;
+              if (cw10 >= 0) yr[cw10] -= u10;
+              if (cw11 >= 0) yr[cw11] -= u11;
             }
           }
         }
@@ -1244,26 +1378,41 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
             zl[r] = (own && r < nl) ? Y[(i0 + r) * pitch + mycol] : 0.0;
             zh[r] = (own && r < nh) ? Y[(mid + r) * pitch + mycol] : 0.0;
           }
-          const double* T3 = Td + 192 * q;
+          const double* T3 = Td + TDS * q;
           bool bad = false;
-          if (nh > 0) {
-            bad = sub8<SUB8_PRO>(zh, nh, a.rbcode[2 * q + 1], partner, sgn, mysr, mysi, t2, T3 + 64);
+          if (GS) {
+            double wh[8], wl[8];
+            if (nh > 0) {
+              bad = sub8g(zh, wh, nh, a.rbcode[2 * q + 1], partner, sgn, mysr, mysi, t2, T3 + 64, T3 + 256);
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-              double acc = zl[r];
+              for (int r = 0; r < 8; ++r) {
+                double acc = zl[r];
 #pragma unroll
-              for (int k = 0; k < 8; ++k) acc = fma(-T3[128 + r * 8 + k], zh[k], acc);
-              zl[r] = acc;
+                for (int k = 0; k < 8; ++k) acc = fma(-T3[128 + r * 8 + k], zh[k], fma(-T3[320 + r * 8 + k], wh[k], acc));
+                zl[r] = acc;
+              }
             }
+            bad = sub8g(zl, wl, nl, a.rbcode[2 * q], partner, sgn, mysr, mysi, t2, T3, T3 + 192) || bad;
+          } else {
+            if (nh > 0) {
+              bad = sub8<SUB8_PRO>(zh, nh, a.rbcode[2 * q + 1], partner, sgn, mysr, mysi, t2, T3 + 64);
+#pragma unroll
+              for (int r = 0; r < 8; ++r) {
+                double acc = zl[r];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc = fma(-T3[128 + r * 8 + k], zh[k], acc);
+                zl[r] = acc;
+              }
+            }
+            bad = sub8<SUB8_PRO>(zl, nl, a.rbcode[2 * q], partner, sgn, mysr, mysi, t2, T3) || bad;
           }
-          bad = sub8<SUB8_PRO>(zl, nl, a.rbcode[2 * q], partner, sgn, mysr, mysi, t2, T3) || bad;
           if (own) {
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
               if (r < nl) Y[(i0 + r) * pitch + mycol] = zl[r];
               if (r < nh) Y[(mid + r) * pitch + mycol] = zh[r];
             }
-            if (bad) badoff = min(badoff, goff(B, mycol, i0, a.sf));
+            if (bad) badoff = min(badoff, goff(B, mycol, i0, a.sf, a.sc));
           }
           WP_ADD(3, tL);
         } else if (q >= 1) {
@@ -1272,18 +1421,22 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
           const int p0 = a.rb[2 * q - 2], pm = a.rb[2 * q - 1];
           const int r0 = h == 0 ? p0 : pm, r1 = h == 0 ? pm : i0;
           const int ra = r0 + g;
-          const double* trow = a.Tt + static_cast<size_t>(ra < r1 ? ra : p0) * nf;
+          const size_t roff = static_cast<size_t>(ra < r1 ? ra : p0) * nf;
+          const double* trow = a.Tt + roff;
+          const double* tcrow = GS ? a.Tct + roff : trow;
 #pragma unroll
           for (int st = 0; st < 4; ++st) {
             const int kr = i0 + 4 * t4 + st;
             la[st] = kr < i1 ? __ldg(trow + kr) : 0.0;
+            if (GS) lt[st] = kr < i1 ? __ldg(tcrow + kr) : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < 2; ++u)
 #pragma unroll
-            for (int v = 0; v < 2; ++v) c[u][v][0] = c[u][v][1] = 0.0;
+            for (int v = 0; v < 2; ++v) c[u][v][0] = c[u][v][1] = cz[u][v][0] = cz[u][v][1] = 0.0;
           if (r0 < r1) {
             const double* tp = trow + i1 + t4;
+            const double* tq = tcrow + i1 + t4;
             const double* yp = Y + static_cast<size_t>(i1 + t4) * pitch;
             const int nk4 = (nf - i1) >> 2;
             int j = 0;
@@ -1292,17 +1445,31 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
               const double a0 = __ldg(tp + 4 * j), a1 = __ldg(tp + 4 * j + 4);
               const double* y0 = yp + 4 * j * pitch;
               const double* y1 = y0 + 4 * pitch;
-              dmma(c[0][0][0], c[0][0][1], a0, y0[cb0]);
-              dmma(c[1][0][0], c[1][0][1], a0, y0[cb1]);
-              dmma(c[0][1][0], c[0][1][1], a1, y1[cb0]);
-              dmma(c[1][1][0], c[1][1][1], a1, y1[cb1]);
+              const double b00 = y0[cb0], b01 = y0[cb1], b10 = y1[cb0], b11 = y1[cb1];
+              dmma(c[0][0][0], c[0][0][1], a0, b00);
+              dmma(c[1][0][0], c[1][0][1], a0, b01);
+              dmma(c[0][1][0], c[0][1][1], a1, b10);
+              dmma(c[1][1][0], c[1][1][1], a1, b11);
+              if (GS) {
+                const double e0 = __ldg(tq + 4 * j), e1 = __ldg(tq + 4 * j + 4);
+                dmma(cz[0][0][0], cz[0][0][1], e0, b00);
+                dmma(cz[1][0][0], cz[1][0][1], e0, b01);
+                dmma(cz[0][1][0], cz[0][1][1], e1, b10);
+                dmma(cz[1][1][0], cz[1][1][1], e1, b11);
+              }
             }
             for (; 4 * j < nf - i1; ++j) {  // last k4 step (rows >= nf read as 0)
               const bool kin = i1 + 4 * j + t4 < nf;
               const double a0 = kin ? __ldg(tp + 4 * j) : 0.0;
               const double* y0 = yp + static_cast<size_t>(kin ? 4 * j : 0) * pitch;
-              dmma(c[0][0][0], c[0][0][1], a0, y0[kin ? cb0 : zcol]);
-              dmma(c[1][0][0], c[1][0][1], a0, y0[kin ? cb1 : zcol]);
+              const double b00 = y0[kin ? cb0 : zcol], b01 = y0[kin ? cb1 : zcol];
+              dmma(c[0][0][0], c[0][0][1], a0, b00);
+              dmma(c[1][0][0], c[1][0][1], a0, b01);
+              if (GS) {
+                const double e0 = kin ? __ldg(tq + 4 * j) : 0.0;
+                dmma(cz[0][0][0], cz[0][0][1], e0, b00);
+                dmma(cz[1][0][0], cz[1][0][1], e0, b01);
+              }
             }
           }
           WP_ADD(4, tL);
@@ -1318,7 +1485,8 @@ __global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArg
       for (int i = threadIdx.x; i < nf; i += blockDim.x) unit_butterfly<true>(Y, pitch, i, su[u].rl0, k, su[u].pair0, w);
     }
     __syncthreads();
-    wide_rows<false>(a, Y, pitch, pb, w, kb);
+    if (GS) gs_rows<false>(a, Y, pitch, pb, w, kb);
+    else wide_rows<false>(a, Y, pitch, pb, w, kb);
     __syncthreads();
     WP_ADD(5, ts);
 #if WIDE_PROF
@@ -1365,10 +1533,10 @@ size_t fibre_big_smem(int nf, int maxcol, int cell_smem) {
          kMaxUnits * sizeof(FibreUnit) + static_cast<size_t>(cell_smem) * sizeof(FibreCell);
 }
 
-size_t fibre_wide_smem(int nf, int maxcol, int cell_smem, int nrb) {
+size_t fibre_wide_smem(int nf, int maxcol, int cell_smem, int nrb, int gs) {
   if (nrb <= 0) nrb = (nf + 6) / 7;  // bound on the 8-row blocks (a 2x2 cell may shorten one to 7)
   const size_t nsb = (nrb + 1) / 2;
-  return (static_cast<size_t>(nf) * fibre_pitch(maxcol) + 192 * nsb) * sizeof(double) +
+  return (static_cast<size_t>(nf) * fibre_pitch(maxcol) + (gs ? 384 : 192) * nsb) * sizeof(double) +
          kWideUnits * sizeof(FibreUnit) + static_cast<size_t>(cell_smem) * sizeof(FibreCell);
 }
 
@@ -1383,8 +1551,9 @@ cudaError_t launch_fibre_solve(const FibreArgs& a, int device, cudaStream_t st, 
     return launch_small<24>(a, device, st, info);
   }
   if (a.wide) {
-    const size_t smem = fibre_wide_smem(a.nf, a.maxcol, a.cell_smem, a.nrb);
-    return launch_k(fibre_wide_kernel, a, smem, device, st, info, kWideThreads);
+    const size_t smem = fibre_wide_smem(a.nf, a.maxcol, a.cell_smem, a.nrb, a.gs);
+    if (a.gs) return launch_k(fibre_wide_kernel<true>, a, smem, device, st, info, kWideThreads);
+    return launch_k(fibre_wide_kernel<false>, a, smem, device, st, info, kWideThreads);
   }
   if (a.big) {
     const size_t smem = fibre_big_smem(a.nf, a.maxcol, a.cell_smem);
