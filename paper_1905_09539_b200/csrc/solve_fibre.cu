@@ -1098,7 +1098,7 @@ TSG_DEVINL void wide_rows(const FibreArgs& a, double* Y, int pitch, const int64_
 // blocks of T_f, row-major: [0] T[lo, lo], [1] T[hi, hi], [2] T[lo, hi]
 // (zero padded), then the unit table and the optional S' cell table.
 template <bool GS>
-__global__ void __launch_bounds__(kWideThreads) fibre_wide_kernel(const FibreArgs a) {
+__global__ void __launch_bounds__(kWideThreads, 2) fibre_wide_kernel(const FibreArgs a) {
   constexpr int TDS = GS ? 384 : 192;  // Td doubles per super-block (gsylv: S blocks, then Tc blocks)
   extern __shared__ __align__(16) double sm[];
   const int nf = a.nf;
