@@ -43,6 +43,12 @@ typedef struct {
   int tile[TSG_MAX_ORDER]; /* explicit per-mode tile extents (0 = from n_min) */
   int inputs_on_device;  /* 1: B/X are device pointers (resident in HBM) */
   void* stream;          /* cudaStream_t to run on (NULL = context stream) */
+  /* plans only: modes whose transforms are the identity (bit m), their U may
+   * be NULL; and the free mode of the eigen-decoupled solve (-1: chosen by
+   * the plan).  The slab-sharded decoupled solve (paper_1905_09539_b200/dist.py)
+   * runs a plan's transforms and its fibre solve on different slabs. */
+  int skip_transform_mask;
+  int free_mode;
 } tsg_opts;
 
 typedef struct {
@@ -122,6 +128,12 @@ int tsg_plan_sync(tsg_plan* plan, tsg_report* rep);
  * grid), so the per-phase times of tsg_plan_execute are per-kernel times.
  * Default 0.  Same results either way (bit-identical). */
 int tsg_plan_set_serial(tsg_plan* plan, int serial);
+/* Transforms only (dir 0: forward B x_m U_m^T, 1: back X x_m U_m; the
+ * decoupled plan's folded eigenbasis transforms), in -> out (distinct device
+ * buffers), on `stream` (NULL = context stream). */
+int tsg_plan_transform(tsg_plan* plan, int dir, const double* in, double* out, void* stream);
+/* Eigen-decoupled plans: the free mode (-1 if the plan is not decoupled). */
+int tsg_plan_free_mode(const tsg_plan* plan);
 void tsg_plan_destroy(tsg_plan* plan);
 /* Solve nrhs right-hand sides from HOST buffers B[i] into X[i] (pinned
  * memory recommended) with the copies overlapped: the host->device copy of

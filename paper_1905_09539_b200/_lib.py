@@ -20,7 +20,8 @@ c_dbl_pp = ctypes.POINTER(c_dbl_p)
 
 class TsgOpts(ctypes.Structure):
     _fields_ = [("n_min", ctypes.c_int), ("tile", ctypes.c_int * 8),
-                ("inputs_on_device", ctypes.c_int), ("stream", ctypes.c_void_p)]
+                ("inputs_on_device", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("skip_transform_mask", ctypes.c_int), ("free_mode", ctypes.c_int)]
 
 
 class TsgReport(ctypes.Structure):
@@ -38,6 +39,7 @@ TSG_SYMBOLS = [
     "tsg_laplace_reduced", "tsg_gsylv_solve", "tsg_gsylv_reduced", "tsg_plan_create",
     "tsg_plan_execute", "tsg_plan_execute_stream", "tsg_plan_destroy", "tsg_plan_info",
     "tsg_plan_enqueue", "tsg_plan_sync", "tsg_plan_set_serial", "tsg_plan_describe",
+    "tsg_plan_transform", "tsg_plan_free_mode",
     "tsg_mode_multiply",
     "tsg_residual", "tsg_abi_version",
     "tsg_slab_bounds", "tsg_dplan_create", "tsg_dplan_destroy", "tsg_dplan_info",
@@ -66,6 +68,8 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tsg_plan_enqueue": (I, [P, P, P]),
         "tsg_plan_sync": (I, [P, ctypes.POINTER(TsgReport)]),
         "tsg_plan_set_serial": (I, [P, I]),
+        "tsg_plan_transform": (I, [P, I, P, P, P]),
+        "tsg_plan_free_mode": (I, [P]),
         "tsg_plan_info": (I, [P, ctypes.POINTER(ctypes.c_int64), c_int_p, c_dbl_p]),
         "tsg_plan_describe": (I, [P, ctypes.c_char_p, I]),
         "tsg_residual": (I, [P, I, I, c_int_p, c_dbl_pp, P, P, P, I, c_dbl_p]),

@@ -453,12 +453,19 @@ PlanKnobs PlanKnobs::from_env() {
   return k;
 }
 
+// All-mode transform in -> target (definition below)
+cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double* other, bool fwd,
+                          cudaStream_t st, const tsg::GemmArgs* gate0 = nullptr,
+                          cudaEvent_t after0 = nullptr, int i_lo = 0, int i_hi = -1,
+                          const tsg::GemmArgs* last = nullptr);
+
 extern "C" {
 
 int tsg_abi_version(void) { return 1; }
 
 void tsg_default_opts(tsg_opts* o) {
   std::memset(o, 0, sizeof(*o));
+  o->free_mode = -1;
 }
 
 int tsg_create(int n_gpus, const int* device_ids, tsg_ctx** out) {
@@ -503,7 +510,8 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   for (int m = 0; m < d; ++m) {
     if (dims[m] <= 0) return fail(ctx, TSG_EDIM, "dimensions must be positive");
     if (!T[m]) return fail(ctx, TSG_EDIM, "missing coefficient");
-    if (!reduced_only && !U[m]) return fail(ctx, TSG_EDIM, "missing orthogonal factor");
+    if (!reduced_only && !U[m] && !((o.skip_transform_mask >> m) & 1))
+      return fail(ctx, TSG_EDIM, "missing orthogonal factor");
     if (!quasi_upper(T[m], dims[m]))
       return fail(ctx, TSG_EDIM,
                   "coefficient " + std::to_string(m) + " must be upper quasi-triangular");
@@ -515,6 +523,8 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   TSG_CU(cudaSetDevice(ctx->device));
   auto pl = std::make_unique<tsg_plan>();
   pl->knobs = PlanKnobs::from_env();
+  pl->skip_mask = o.skip_transform_mask & ((1 << d) - 1);
+  pl->force_f = o.free_mode;
   pl->ctx = ctx;
   pl->family = family;
   pl->d = d;
@@ -557,7 +567,7 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
     pdvs[m] = pdv;
     nfs[m] = nf;
     scale += fro(T[m], nn);
-    if (!reduced_only) {
+    if (!reduced_only && !((pl->skip_mask >> m) & 1)) {
       // forward: A = U^T (mode 0), At = U (m > 0); back: A = U, At = U^T.
       // gsylv mode 0: forward Q^T, back Z.
       const double* bk = (family == 1 && m == 0) ? Z : U[m];
@@ -1049,6 +1059,18 @@ int tsg_plan_enqueue(tsg_plan* pl, const double* B, double* X) {
   return enqueue(pl, B, X, pl->ctx->stream, false);
 }
 
+int tsg_plan_transform(tsg_plan* pl, int dir, const double* in, double* out, void* stream) {
+  if (!pl || !in || !out || in == out || pl->reduced_only) return TSG_EINVAL;
+  tsg_ctx* ctx = pl->ctx;
+  TSG_CU(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  TSG_CU(pl->w2.ensure(pl->N));
+  TSG_CU(transform_all(pl, in, out, pl->w2.p, dir == 0, st));
+  return TSG_OK;
+}
+
+int tsg_plan_free_mode(const tsg_plan* pl) { return pl && pl->decoupled ? pl->dec_f : -1; }
+
 int tsg_plan_set_serial(tsg_plan* pl, int serial) {
   if (!pl) return TSG_EINVAL;
   pl->knobs.serial = serial != 0;
@@ -1427,9 +1449,8 @@ cudaError_t launch_plan_solve(tsg_plan* pl, const tsg::SolveArgs& a, cudaStream_
 // GEMMs, except consecutive small modes (n in {16, 24, 32, 40}), which go
 // through the fused shared-memory pass two at a time (modes_small.cu).
 cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double* other, bool fwd,
-                          cudaStream_t st, const tsg::GemmArgs* gate0 = nullptr,
-                          cudaEvent_t after0 = nullptr, int i_lo = 0, int i_hi = -1,
-                          const tsg::GemmArgs* last = nullptr) {
+                          cudaStream_t st, const tsg::GemmArgs* gate0, cudaEvent_t after0, int i_lo, int i_hi,
+                          const tsg::GemmArgs* last) {
   const int d = pl->d;
   struct Pass {
     int m;
@@ -1440,9 +1461,14 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
     const char* e = std::getenv("TSG_SMALLMODES");
     return !e || std::atoi(e) != 0;
   }();
+  auto skip = [&](int m) { return (pl->skip_mask >> m) & 1; };
   for (int m = 0; m < d;) {
     const int* dm = pl->dims.data();
-    if (small_on && m + 1 < d && tsg::small_pass_ok(d, dm, m, true)) {
+    if (skip(m)) {
+      ++m;
+      continue;
+    }
+    if (small_on && m + 1 < d && !skip(m + 1) && tsg::small_pass_ok(d, dm, m, true)) {
       ps.push_back({m, 2});
       m += 2;
     } else {
@@ -1451,6 +1477,11 @@ cudaError_t transform_all(tsg_plan* pl, const double* in, double* target, double
     }
   }
   const int k = static_cast<int>(ps.size());
+  if (k == 0) {  // every transform is the identity
+    if (in != target)
+      return cudaMemcpyAsync(target, in, pl->N * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    return cudaSuccess;
+  }
   // slab chain: mode-1 CTAs start on the slabs the mode-0 GEMM has finished
   // (TSG_SCHAIN=0 at plan creation turns it off)
   const bool schain = pl->sdone[0] && k >= 2 && ps[0].m == 0 && ps[0].kind == 0 && ps[1].m == 1 &&
@@ -1809,7 +1840,7 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U, c
     }
   } else {
     for (int f = 1; f < d; ++f) {
-      if (dims[f] > nfmax) continue;
+      if (dims[f] > nfmax || (pl->force_f >= 0 && f != pl->force_f)) continue;
       double prod = 1;
       for (int m = 0; m < d; ++m)
         if (m != f) prod *= ok[m] ? me[m].kappa : 1e300;
@@ -1983,7 +2014,7 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U, c
   a.nblocks = static_cast<int64_t>(a.nchunk) * nblk_rest;
   // folded transforms of the eigen modes (gsylv mode 0 keeps Q^T / Z)
   for (int m = 0; m < d; ++m) {
-    if (m == f) continue;
+    if (m == f || ((pl->skip_mask >> m) & 1)) continue;
     const int n = dims[m];
     const size_t nn = static_cast<size_t>(n) * n;
     const std::vector<double> ut = transpose(U[m], n);

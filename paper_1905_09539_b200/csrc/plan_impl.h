@@ -53,6 +53,8 @@ struct PlanKnobs {
 struct tsg_plan {
   tsg_ctx* ctx = nullptr;
   PlanKnobs knobs;
+  int skip_mask = 0;   // modes with identity transforms (tsg_opts::skip_transform_mask)
+  int force_f = -1;    // decoupled free mode (tsg_opts::free_mode)
   int family = 0, d = 0, reduced_only = 0;
   std::vector<int> dims;
   std::vector<int64_t> stride;

@@ -40,10 +40,14 @@ class Plan:
     U[0]=Q and the extra Tc, Z factors."""
 
     def __init__(self, ctx: Context, family: int, T: list, U: list | None, Tc=None, Z=None,
-                 reduced_only: bool = False, n_min: int = 0, tile=None):
+                 reduced_only: bool = False, n_min: int = 0, tile=None, skip_transform=(),
+                 free_mode: int = -1):
+        """skip_transform: modes whose transforms are the identity (their U
+        entry may be None); free_mode: the decoupled solve's free mode (-1:
+        the plan's choice).  Both serve the slab-sharded solve (dist.py)."""
         self.ctx = ctx
         self.T = [_f(t) for t in T]
-        self.U = [_f(u) for u in U] if U is not None else None
+        self.U = [(_f(u) if u is not None else np.zeros((1, 1), order="F")) for u in U] if U is not None else None
         self.Tc = _f(Tc) if Tc is not None else None
         self.Z = _f(Z) if Z is not None else None
         self.dims = [t.shape[0] for t in self.T]
@@ -51,6 +55,8 @@ class Plan:
         opts = TsgOpts()
         lib().tsg_default_opts(ctypes.byref(opts))
         opts.n_min = n_min
+        opts.skip_transform_mask = sum(1 << int(m) for m in skip_transform)
+        opts.free_mode = int(free_mode)
         if tile:
             for m, b in enumerate(tile):
                 opts.tile[m] = int(b)
@@ -68,6 +74,17 @@ class Plan:
         if rc != 0:
             raise gpu_error(f"tsg_plan_create failed ({rc}): {ctx.error()}")
         self.n = int(np.prod(self.dims))
+
+    def free_mode(self) -> int:
+        """Free mode of the eigen-decoupled solve (-1: tile-DAG kernels)."""
+        return int(lib().tsg_plan_free_mode(self.h))
+
+    def transform(self, direction: int, in_ptr: int, out_ptr: int, stream: int = 0) -> None:
+        """Transforms only (0 forward, 1 back), device buffers, on `stream`."""
+        rc = lib().tsg_plan_transform(self.h, int(direction), ctypes.c_void_p(in_ptr), ctypes.c_void_p(out_ptr),
+                                      ctypes.c_void_p(stream))
+        if rc != 0:
+            raise gpu_error(f"tsg_plan_transform failed ({rc}): {self.ctx.error()}")
 
     def info(self):
         nt = ctypes.c_int64()
