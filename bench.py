@@ -23,16 +23,17 @@ back transforms X = X~ x_m U_m — on synthetic seeded inputs
   all_configs : C1-C5 (one plan each, K solves enqueued back to back):
           ms per solve, unknowns/s, fraction of the FP64 peak, residual
 
-Multi-GPU (N>1, torchrun, NCCL): the order-3 Laplace configurations (C1, C2,
-C4) run ONE problem sharded into N slabs along the last mode (strong
-scaling): slab-local transforms, NCCL all-gathers for the last-mode
-transforms, and the dataflow solve over peer-mapped slabs (CUDA IPC, NVLink),
-see paper_1905_09539_b200/dist.py.  C3 (d=6) and C5 (gsylv) are not sharded
-yet and run one replica per GPU (weak scaling).  `--sharded` forces the
-sharded path at N=1 (plumbing check).  `--impl reference` times the reference
-CPU solver (rank 0 only; other ranks exit 0) on inputs drawn from the
-reference's own RandomStream (oracle/_ref), so that process never loads the
-product library.
+Multi-GPU (N>1, torchrun, NCCL): the Laplace configurations (C1-C4) run ONE
+problem sharded over the N GPUs (strong scaling), eigen-decoupled: each rank
+holds a slab along the last mode; the transforms of modes 0..d-2 run there,
+two NCCL all-to-alls per solve move the data to slabs along mode 0 and back,
+where the last mode's transforms and the fibre solve along the free mode run
+(paper_1905_09539_b200/dist.py, DecoupledSharded).  `--sharded-ipc` runs the
+tile-DAG path over peer-mapped slabs instead (d = 3).  C5 (gsylv) runs one
+replica per GPU (weak scaling).  `--sharded` forces the sharded path at N=1
+(plumbing check).  `--impl reference` times the reference CPU solver (rank 0
+only; other ranks exit 0) on inputs drawn from the reference's own
+RandomStream (oracle/_ref), so that process never loads the product library.
 """
 from __future__ import annotations
 
@@ -464,11 +465,13 @@ def run_ours(a, rank, world, local):
 
 
 def run_sharded(a, rank, world, local):
-    """One problem, `world` slabs along the last mode (strong scaling)."""
+    """One problem sharded over `world` GPUs (strong scaling), eigen-decoupled:
+    last-mode slabs <-> mode-0 slabs by two NCCL all-to-alls around a local
+    fibre solve (paper_1905_09539_b200.dist.DecoupledSharded).
+    `--sharded-ipc` runs the tile-DAG path with peer-mapped slabs instead."""
     import torch
     import torch.distributed as dist
     import paper_1905_09539_b200 as T
-    from paper_1905_09539_b200.dist import DeviceSlabs, ShardedLaplace
     from paper_1905_09539_b200.plan import Context
 
     torch.cuda.set_device(local)
@@ -479,14 +482,21 @@ def run_sharded(a, rank, world, local):
     p = T.make_problem(kind, dims, seed=1)  # the same problem on every rank
     fs = [T.schur(c) for c in p.coeffs]      # shared host setup
     ctx = Context(local)
-    # sharded setup (peer IPC mappings); if it fails on any rank, every rank
-    # falls back to one independent replica per GPU (reported in the line)
+    # sharded setup; if it fails on any rank, every rank falls back to one
+    # independent replica per GPU (reported in the line)
     err = ""
+    mode = "ipc" if a.sharded_ipc else "decoupled"
     try:
         if os.environ.get("TSG_BENCH_SHARD_FAIL"):  # exercise the fallback (development)
             raise RuntimeError("forced by TSG_BENCH_SHARD_FAIL")
-        be = DeviceSlabs(ctx, rank, world, [f[1] for f in fs], [f[0] for f in fs])
-        sl = ShardedLaplace(be)
+        if mode == "decoupled":
+            from paper_1905_09539_b200.dist import DecoupledSharded, DeviceDecoupled
+            be = DeviceDecoupled(ctx, rank, world, [f[1] for f in fs], [f[0] for f in fs])
+            sl = DecoupledSharded(be)
+        else:
+            from paper_1905_09539_b200.dist import DeviceSlabs, ShardedLaplace
+            be = DeviceSlabs(ctx, rank, world, [f[1] for f in fs], [f[0] for f in fs])
+            sl = ShardedLaplace(be)
     except Exception as e:  # noqa: BLE001
         err = f"{type(e).__name__}: {e}"[:200]
     flag = torch.tensor([1.0 if err else 0.0], device=dev)
@@ -497,7 +507,8 @@ def run_sharded(a, rank, world, local):
                   file=sys.stderr, flush=True)
         a.fallback = err or "sharded setup failed on another rank"
         return run_ours(a, rank, world, local)
-    lo, hi = be.bounds[rank], be.bounds[rank + 1]
+    bounds = be.bd if mode == "decoupled" else be.bounds
+    lo, hi = bounds[rank], bounds[rank + 1]
     b_host = torch.from_numpy(np.ascontiguousarray(p.rhs[..., lo:hi].reshape(-1, order="F"))).pin_memory()
     x_host = torch.empty_like(b_host).pin_memory()
     b = b_host.to(dev)
@@ -505,42 +516,44 @@ def run_sharded(a, rank, world, local):
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
     sp = ctx.stream_ptr()
 
-    def step(ev=None):
-        if ev is not None:
-            ev[0].record(stream)
-        be.forward_local(b, sp)
-        sl._all_gather(sp)
-        be.forward_split(sp)
-        if ev is not None:
-            ev[1].record(stream)
-        be.solve(sp)
-        if ev is not None:
-            ev[2].record(stream)
-        be.back_local(sp)
-        sl._all_gather(sp)
-        be.back_split(x, sp)
-        if ev is not None:
-            ev[3].record(stream)
+    if mode == "decoupled":
+        def step():
+            sl.solve(b, x)
+    else:
+        def step():
+            be.forward_local(b, sp)
+            sl._all_gather(sp)
+            be.forward_split(sp)
+            be.solve(sp)
+            be.back_local(sp)
+            sl._all_gather(sp)
+            be.back_split(x, sp)
 
     with torch.cuda.stream(stream):
         for _ in range(max(a.warmup, 3)):
             step()
-        be.status(sp)
+        if mode == "decoupled":
+            be.check()
+        else:
+            be.status(sp)
         dist.barrier()
         torch.cuda.synchronize()
         clocks = ClockSampler(local)
         clocks.start()
         time.sleep(0.2)
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.steps)]
-        for i in range(a.steps):
-            step(evs[i])
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.steps):
+            step()
+        e1.record(stream)
         stream.synchronize()
         clk = clocks.stop()
-        ms = evs[0][0].elapsed_time(evs[-1][3]) / a.steps
-        t_fwd = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
-        t_solve = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
-        t_back = statistics.median(e[2].elapsed_time(e[3]) for e in evs)
-        be.status(sp)
+        ms = e0.elapsed_time(e1) / a.steps
+        if mode == "decoupled":
+            be.check()
+        else:
+            be.status(sp)
         # end to end: pinned host slab in, solution slab out, every step
         dist.barrier()
         torch.cuda.synchronize()
@@ -554,56 +567,76 @@ def run_sharded(a, rank, world, local):
         f1.record(stream)
         f1.synchronize()
         ms_e2e = f0.elapsed_time(f1) / a.steps
-        t = torch.tensor([ms, ms_e2e, t_fwd, t_solve, t_back], device=dev)
+        t = torch.tensor([ms, ms_e2e], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, ms_e2e, t_fwd, t_solve, t_back = (float(v) for v in t)
-        # gather X to rank 0 through the padded send/gather buffers
-        be.send.zero_()
-        be.send[: x.numel()].copy_(x)
-        sl._all_gather(sp)
+        ms, ms_e2e = (float(v) for v in t)
+        # gather X to rank 0 (padded to the largest slab)
+        rmax = max(bounds[q + 1] - bounds[q] for q in range(world))
+        plane = int(np.prod(dims[:-1]))
+        slot = torch.zeros(rmax * plane, dtype=torch.float64, device=dev)
+        slot[: x.numel()].copy_(x)
+        allx = torch.empty(world * rmax * plane, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(allx, slot)
         torch.cuda.synchronize()
     res = None
     if rank == 0:
-        g = be.gather.cpu().numpy()
+        g = allx.cpu().numpy()
         parts = []
         for q in range(world):
-            rows = be.bounds[q + 1] - be.bounds[q]
-            seg = g[q * be.send_elems:q * be.send_elems + rows * int(np.prod(dims[:-1]))]
+            rows = bounds[q + 1] - bounds[q]
+            seg = g[q * rmax * plane:q * rmax * plane + rows * plane]
             parts.append(seg.reshape(tuple(dims[:-1]) + (rows,), order="F"))
         xs = np.concatenate(parts, axis=len(dims) - 1)
         res = T.residual(p, xs)
         tr_f, solve_f = flops_alg(kind, dims)
+        if mode == "decoupled":
+            par = (f"{world} slabs along mode {len(dims) - 1} (rows {bounds}) for the transforms of "
+                   f"modes 0..{len(dims) - 2}, {world} slabs along mode 0 (rows {be.b0}) for the mode-"
+                   f"{len(dims) - 1} transforms and the fibre solve along mode {be.f}; two NCCL "
+                   "all-to-alls per solve")
+            # our kernels per step: phase A/C transforms (<= d-1 passes each way) + phase B
+            # (state reset, mode-(d-1) transform, fibre solve, back transform)
+            launches = a.steps * (2 * (len(dims) - 1) + 4)
+        else:
+            par = (f"{world} slabs along mode {len(dims) - 1} (rows {bounds}); NCCL all-gather for the "
+                   "last-mode transforms, peer-mapped dataflow solve")
+            launches = 7 * a.steps
         line = {
             "metric": METRIC, "value": N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": a.steps, "warmup": max(a.warmup, 3), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded RandomStream, BASELINE.json distributions)",
-            "config": {"workload": a.config, "desc": desc, "dims": list(dims), "unknowns": N,
-                       "l2": "inputs larger than L2 (8N bytes per tensor > 126 MB L2)",
-                       "parallelism": f"{world} slabs along mode {len(dims) - 1} "
-                                      f"(rows {be.bounds}); NCCL all-gather for the last-mode "
-                                      "transforms, peer-mapped dataflow solve",
-                       "schur_setup": "host LAPACK dgees, outside the timed region"},
-            "phases_ms": {"forward_transforms+allgather": t_fwd, "reduced_solve": t_solve,
-                          "back_transforms+allgather": t_back},
+            "config": config_of(a.config),
+            "details": {"l2": "inputs larger than L2 (8N bytes per tensor > 126 MB L2)",
+                        "parallelism": par, "sharded_path": mode,
+                        "schur_setup": "host LAPACK dgees, outside the timed region"},
             "fp64_tflops_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12,
             "frac_fp64_peak_alg": (tr_f + solve_f) / (ms * 1e-3) / 1e12 / PEAK_FP64_TFLOPS / world,
             "residual": res,
-            "roofline": {"bound": "tensor", "achieved": solve_f / (t_solve * 1e-3) / 1e12 / world,
+            "roofline": {"bound": "tensor", "achieved": tr_f / (ms * 1e-3) / 1e12 / world,
                          "peak": PEAK_FP64_TFLOPS, "unit": "TFLOP/s",
-                         "frac": solve_f / (t_solve * 1e-3) / 1e12 / world / PEAK_FP64_TFLOPS,
+                         "frac": tr_f / (ms * 1e-3) / 1e12 / world / PEAK_FP64_TFLOPS,
                          "traffic": None,
-                         "kernel": "solve_lap3_kernel (sharded dataflow solve), per GPU",
+                         "kernel": "mode transforms (K1) per GPU, whole step incl. all-to-alls",
                          "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak_probe.log"},
             "e2e": {"value": N / (ms_e2e * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N, "ms_per_step": ms_e2e},
-            "gpu_launches": 7 * a.steps,
+            "gpu_launches": launches,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
+    torch.cuda.synchronize()
+    # orderly teardown: the library's stream (used by NCCL through torch's
+    # ExternalStream) outlives every tensor and collective that touched it
+    del slot, allx, b, x, b_host, x_host  # pinned buffers free through events on that stream
+    if mode == "decoupled":
+        be.close()
     del sl, be
     dist.destroy_process_group()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    ctx.close()
 
 
 def main():
@@ -616,11 +649,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-all-configs", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="sharded path even at N=1")
+    ap.add_argument("--sharded-ipc", action="store_true",
+                    help="multi-GPU: the tile-DAG path over peer-mapped slabs instead of the decoupled one")
     a = ap.parse_args()
     rank, world, local = dist_env()
     if a.impl == "reference":
         run_reference(a, rank)
-    elif (world > 1 or a.sharded) and CONFIGS[a.config][0] != 5 and len(CONFIGS[a.config][1]) == 3:
+    elif (world > 1 or a.sharded) and CONFIGS[a.config][0] != 5 and (len(CONFIGS[a.config][1]) == 3
+                                                                       or not a.sharded_ipc):
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")

@@ -1065,6 +1065,8 @@ int tsg_plan_transform(tsg_plan* pl, int dir, const double* in, double* out, voi
   TSG_CU(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   TSG_CU(pl->w2.ensure(pl->N));
+  // the slab-chain flags between the first two GEMMs are per call
+  if (pl->flags) TSG_CU(tsg::reset_state(pl->flags, pl->ntiles, pl->counter, pl->aux, pl->aux_n, st));
   TSG_CU(transform_all(pl, in, out, pl->w2.p, dir == 0, st));
   return TSG_OK;
 }

@@ -219,12 +219,13 @@ class ShardedLaplace:
 
 
 def decoupled_free_mode(dims) -> int:
-    """Free mode of the sharded decoupled solve: the shortest of modes
-    1..d-2 (the shard modes 0 and d-1 must be eigen modes)."""
+    """Free mode of the sharded decoupled solve (CPU stand-in rule): the
+    shortest of modes 1..d-1 (mode 0, the solve-phase shard mode, must be an
+    eigen mode).  The CUDA backend takes the plan's own choice."""
     d = len(dims)
-    if d < 3:
-        raise ValueError("the sharded decoupled solve needs d >= 3")
-    return min(range(1, d - 1), key=lambda m: (dims[m], m))
+    if d < 2:
+        raise ValueError("the sharded decoupled solve needs d >= 2")
+    return min(range(1, d), key=lambda m: (dims[m], m))
 
 
 class DeviceDecoupled:
@@ -238,16 +239,22 @@ class DeviceDecoupled:
         self.U = [_f(u) for u in U]
         self.dims = [t.shape[0] for t in self.T]
         d = len(self.dims)
-        self.f = decoupled_free_mode(self.dims) if f is None else f
+        if d < 3:
+            raise ValueError("the sharded decoupled solve needs d >= 3")
         self.bd = slab_bounds(self.dims[-1], self.T[-1], nranks, tile=1)  # last-mode slabs
         self.b0 = slab_bounds(self.dims[0], self.T[0], nranks, tile=1)    # mode-0 slabs
-        lo, hi = self.bd[rank], self.bd[rank + 1]
-        ta = self.T[:-1] + [np.asfortranarray(self.T[-1][lo:hi, lo:hi])]
-        self.plan_a = Plan(ctx, 0, ta, self.U[:-1] + [None], skip_transform=(d - 1,), free_mode=self.f)
+        # phase B first: its plan picks the free mode (f >= 1, the single-GPU
+        # rule), which phase A then follows
         q0, q1 = self.b0[rank], self.b0[rank + 1]
         tb = [np.asfortranarray(self.T[0][q0:q1, q0:q1])] + self.T[1:]
         self.plan_b = Plan(ctx, 0, tb, [None] * (d - 1) + [self.U[-1]], skip_transform=tuple(range(d - 1)),
-                           free_mode=self.f)
+                           free_mode=-1 if f is None else f)
+        self.f = self.plan_b.free_mode()
+        if self.f < 1:
+            raise gpu_error(f"sharded decoupled solve: phase-B plan not decoupled ({self.plan_b.describe()})")
+        lo, hi = self.bd[rank], self.bd[rank + 1]
+        ta = self.T[:-1] + [np.asfortranarray(self.T[-1][lo:hi, lo:hi])]
+        self.plan_a = Plan(ctx, 0, ta, self.U[:-1] + [None], skip_transform=(d - 1,), free_mode=self.f)
         for p, nm in ((self.plan_a, "A"), (self.plan_b, "B")):
             if p.free_mode() != self.f:
                 raise gpu_error(f"sharded decoupled solve: phase-{nm} plan not decoupled along mode {self.f} "

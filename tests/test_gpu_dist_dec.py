@@ -41,7 +41,7 @@ def test_decoupled_sharded_world1_nccl(ref, gpu):
     os.environ.setdefault("MASTER_PORT", "29561")
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        p = gpu.make_problem(2, (48, 40, 36), seed=22)
+        p = gpu.make_problem(1, (64, 64, 64), seed=22)
         fs = [gpu.schur(a) for a in p.coeffs]
         ctx = Context(0)
         be = DeviceDecoupled(ctx, 0, 1, [f[1] for f in fs], [f[0] for f in fs])
@@ -49,7 +49,8 @@ def test_decoupled_sharded_world1_nccl(ref, gpu):
         b = torch.from_numpy(np.ascontiguousarray(p.rhs).reshape(-1, order="F")).cuda()
         x = torch.empty_like(b)
         torch.cuda.synchronize()
-        sh.solve(b, x, check=True)
+        for _ in range(3):  # repeated solves reuse every buffer and flag
+            sh.solve(b, x, check=True)
         torch.cuda.synchronize()
         xs = x.cpu().numpy().reshape(p.rhs.shape, order="F")
         want, _ = ref.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
