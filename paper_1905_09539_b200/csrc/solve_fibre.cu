@@ -545,9 +545,15 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
   __syncthreads();
   if (SB[0].blk < a.nblocks) issue_block(a, SB[0].B, SB[0].pb, SB[0].nunit, Ys[0], SB[0].B.ncol, sus[0]);
   int cur = 0;
+#if SMALL_PROF
+  long long ph[8] = {};
+#endif
   for (;;) {
     SmallBuf& C = SB[cur];
     if (C.blk >= a.nblocks) break;
+#if SMALL_PROF
+    long long t0 = clock64();
+#endif
     // prefetch the next block into the other buffer
     SmallBuf& Nx = SB[cur ^ 1];
     if (threadIdx.x == 0) {
@@ -559,6 +565,10 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
       }
     }
     __syncthreads();
+#if SMALL_PROF
+    long long t1 = clock64();
+    ph[0] += t1 - t0;
+#endif
     const bool more = Nx.blk < a.nblocks;
     if (more) {
       issue_block(a, Nx.B, Nx.pb, Nx.nunit, Ys[cur ^ 1], Nx.B.ncol, sus[cur ^ 1]);
@@ -567,6 +577,10 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
       cp_async_wait<0>();
     }
     __syncthreads();
+#if SMALL_PROF
+    long long t2 = clock64();
+    ph[1] += t2 - t1;
+#endif
     const Blk& B = C.B;
     const int ncol = B.ncol, w = B.w, kb = B.kb, nunit = C.nunit;
     double* Y = Ys[cur];
@@ -585,6 +599,10 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
       if (k >= 2) unit_butterfly<false>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
     }
     __syncthreads();
+#if SMALL_PROF
+    long long t3 = clock64();
+    ph[2] += t3 - t2;
+#endif
     const int njob = C.job0[nunit];
     for (int j = threadIdx.x; j < njob; j += blockDim.x) {
       int lo = 0, hi = nunit - 1;  // last unit with job0 <= j
@@ -607,6 +625,10 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
       solve_job_reg<NF>(a, sT, sfc, Y, ncol, re, im, sr, si, goff(B, re, 0, a.sf));
     }
     __syncthreads();
+#if SMALL_PROF
+    long long t4 = clock64();
+    ph[3] += t4 - t3;
+#endif
     for (int e = threadIdx.x; e < nunit * nf; e += blockDim.x) {
       const int u = e / nf, i = e - u * nf;
       const int k = kb + su[u].pair0;
@@ -615,8 +637,16 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
     __syncthreads();
     rows_io<false>(a, Y, ncol, C.pb, w, kb);
     __syncthreads();
+#if SMALL_PROF
+    ph[4] += clock64() - t4;
+    ph[6] += 1;
+#endif
     cur ^= 1;
   }
+#if SMALL_PROF
+  if (a.prof && (threadIdx.x & 31) == 0)
+    for (int k = 0; k < 7; ++k) atomicAdd(a.prof + k, static_cast<unsigned long long>(ph[k]));
+#endif
   pdl_trigger();
 }
 
@@ -842,6 +872,9 @@ __global__ void __launch_bounds__(kBigThreads, 2) fibre_big_kernel(const FibreAr
 // slot = 0 mod 4), the helpers on sub-partitions 1-3.
 #ifndef WIDE_PROF
 #define WIDE_PROF 0
+#endif
+#ifndef SMALL_PROF
+#define SMALL_PROF 0
 #endif
 #if WIDE_PROF
 #define WP_T(v) const long long v = clock64()
