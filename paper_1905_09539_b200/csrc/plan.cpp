@@ -525,6 +525,8 @@ int tsg_plan_create(tsg_ctx* ctx, int family, int d, const int* dims, const doub
   pl->knobs = PlanKnobs::from_env();
   pl->skip_mask = o.skip_transform_mask & ((1 << d) - 1);
   pl->force_f = o.free_mode;
+  if (pl->force_f < 0)
+    if (const char* e = std::getenv("TSG_DECOUPLE_F")) pl->force_f = std::atoi(e);  // tuning knob
   pl->ctx = ctx;
   pl->family = family;
   pl->d = d;
@@ -2014,6 +2016,7 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U, c
     a.pitch = tsg::fibre_pitch(a.maxcol);
   }
   a.nblocks = static_cast<int64_t>(a.nchunk) * nblk_rest;
+  if (a.nblocks >= (int64_t{1} << 31)) return TSG_OK;  // the kernels index blocks in 32 bits
   // folded transforms of the eigen modes (gsylv mode 0 keeps Q^T / Z)
   for (int m = 0; m < d; ++m) {
     if (m == f || ((pl->skip_mask >> m) & 1)) continue;

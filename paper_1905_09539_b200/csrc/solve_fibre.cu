@@ -422,8 +422,9 @@ struct SmallBuf {
 
 TSG_DEVINL void decode_block(const FibreArgs& a, const FibreCell* scell, const int* soff, int64_t blk,
                              Blk& B, int& nunit) {
-  int64_t rest = blk / a.nchunk;
-  const int q = static_cast<int>(blk - rest * a.nchunk);
+  // 32-bit index arithmetic (the host keeps nblocks < 2^31)
+  unsigned rest = static_cast<unsigned>(blk) / static_cast<unsigned>(a.nchunk);
+  const int q = static_cast<int>(static_cast<unsigned>(blk) - rest * static_cast<unsigned>(a.nchunk));
   B.r_lo = a.chunk_lo[q];
   B.w = a.chunk_lo[q + 1] - B.r_lo;
   B.njob = a.chunk_u0[q];  // first unit of the chunk (reused field)
@@ -434,8 +435,8 @@ TSG_DEVINL void decode_block(const FibreArgs& a, const FibreCell* scell, const i
   int kb = 0;
   double sreal = a.gs ? 1.0 : 0.0;
   for (int s = 0; s < a.ns; ++s) {
-    const int64_t nx = rest / a.ncell[s];
-    const int c = static_cast<int>(rest - nx * a.ncell[s]);
+    const unsigned nx = rest / static_cast<unsigned>(a.ncell[s]);
+    const int c = static_cast<int>(rest - nx * static_cast<unsigned>(a.ncell[s]));
     rest = nx;
     const FibreCell fc = scell ? scell[soff[s] + c] : a.cells[s][c];
     base += static_cast<int64_t>(fc.start) * a.sstride[s];
@@ -593,10 +594,10 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
       }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < nunit * nf; e += blockDim.x) {
-      const int u = e / nf, i = e - u * nf;
+    for (int u = threadIdx.x >> 5; u < nunit; u += blockDim.x >> 5) {  // a warp per unit, lanes over rows
       const int k = kb + su[u].pair0;
-      if (k >= 2) unit_butterfly<false>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
+      if (k < 2) continue;
+      for (int i = threadIdx.x & 31; i < nf; i += 32) unit_butterfly<false>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
     }
     __syncthreads();
 #if SMALL_PROF
@@ -629,10 +630,10 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
     long long t4 = clock64();
     ph[3] += t4 - t3;
 #endif
-    for (int e = threadIdx.x; e < nunit * nf; e += blockDim.x) {
-      const int u = e / nf, i = e - u * nf;
+    for (int u = threadIdx.x >> 5; u < nunit; u += blockDim.x >> 5) {  // a warp per unit, lanes over rows
       const int k = kb + su[u].pair0;
-      if (k >= 2) unit_butterfly<true>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
+      if (k < 2) continue;
+      for (int i = threadIdx.x & 31; i < nf; i += 32) unit_butterfly<true>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
     }
     __syncthreads();
     rows_io<false>(a, Y, ncol, C.pb, w, kb);
