@@ -887,11 +887,11 @@ __global__ void __launch_bounds__(kBigThreads, 2) fibre_big_kernel(const FibreAr
 #ifndef SUB8_PRO
 #define SUB8_PRO false
 #endif
-constexpr int kTeamWarps = 3;  // leader + two helpers per 16-column group
-constexpr int kWideTeams = 2;
-// six warps per CTA (two CTAs per SM); roles are given by hardware
-// sub-partition (warp slot mod 4, read from %warpid): the leaders on the
-// lowest sub-partitions, the helpers on the others
+constexpr int kTeamWarps = 5;  // leader (two 16-column groups, 32 lanes) + four helpers
+constexpr int kWideTeams = 1;
+// five warps per CTA (two CTAs per SM); roles are given by hardware
+// sub-partition (warp slot mod 4, read from %warpid): the leader on the
+// lowest sub-partition, the helpers on the others
 constexpr int kWideThreads = kTeamWarps * kWideTeams * 32;
 constexpr int kWideSlots = 2 * kWideCols;
 constexpr int kWideUnits = 32;  // mode-0 cells per block (<= kWideCols rows)
@@ -1175,7 +1175,7 @@ __global__ void __launch_bounds__(kWideThreads, 2) fibre_wide_kernel(const Fibre
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    // role = team * 4 + tw (tw 0 leader, 1/2 helpers), or -1 (loads/stores only)
+    // role = team rank (0 leader, 1..4 helpers) by sub-partition, or -1 (loads/stores only)
     int ord[kWideThreads / 32];
     for (int i = 0; i < nw; ++i) ord[i] = i;
     for (int i = 1; i < nw; ++i)  // by sub-partition, stable
@@ -1184,11 +1184,8 @@ __global__ void __launch_bounds__(kWideThreads, 2) fibre_wide_kernel(const Fibre
         ord[j] = ord[j - 1];
         ord[j - 1] = t;
       }
-    for (int i = 0; i < nw; ++i) wrole[i] = -1;
-    for (int t = 0; t < kWideTeams; ++t) wrole[ord[t]] = 4 * t;
-    int k = kWideTeams;
-    for (int hh = 1; hh < kTeamWarps; ++hh)
-      for (int t = 0; t < kWideTeams; ++t) wrole[ord[k++]] = 4 * t + hh;
+    for (int i = 0; i < nw; ++i) wrole[i] = i < kTeamWarps ? 0 : -1;
+    for (int i = 0; i < kTeamWarps && i < nw; ++i) wrole[ord[i]] = i;  // ord[0]: the leader
   }
   if (scell)
     for (int s = 0; s < a.ns; ++s)
@@ -1318,25 +1315,30 @@ __global__ void __launch_bounds__(kWideThreads, 2) fibre_wide_kernel(const Fibre
     __syncthreads();
     WP_ADD(1, tb);
     const int ngrp = W.nslot >> 4;
-    const int team = wrole[warp] >> 2;
-    const int tw = wrole[warp] < 0 ? kTeamWarps : wrole[warp] & 3;  // 0 leader, 1/2 helpers
-    for (int grp = team; tw < kTeamWarps && grp < ngrp; grp += kWideTeams) {
-      const int s0 = grp << 4;
+    const int team = 0;
+    const int tw = wrole[warp] < 0 ? kTeamWarps : wrole[warp];  // 0 leader, 1..4 helpers
+    // groups in pairs: the leader takes group gp on lanes 0..15 and gp + 1 on
+    // lanes 16..31; helper h (tw = 1 + h) the 8-row block (h & 1) of every
+    // super-block of group gp + (h >> 1)
+    for (int gp = 0; tw < kTeamWarps && gp < ngrp; gp += 2) {
+      const int h = tw - 1;
+      const int grp = tw == 0 ? gp + (lane >> 4) : gp + (h >> 1);
+      const bool live = grp < ngrp;
+      const int s0 = (live ? grp : gp) << 4;
       int cb0 = W.col[s0 + g], cb1 = W.col[s0 + 8 + g];  // B-fragment columns
       cb0 = cb0 >= 0 ? cb0 : zcol;
       cb1 = cb1 >= 0 ? cb1 : zcol;
       const int cw00 = W.col[s0 + 2 * t4], cw01 = W.col[s0 + 2 * t4 + 1];
       const int cw10 = W.col[s0 + 8 + 2 * t4], cw11 = W.col[s0 + 9 + 2 * t4];
-      // leader: this lane's column (lanes 0..15)
+      // leader: this lane's column
       const int sl = s0 + (lane & 15);
-      const int role = lane < 16 ? W.role[sl] : 3;
+      const int role = live ? W.role[sl] : 3;
       const int mycol = role == 3 ? -1 : W.col[sl];
       const int partner = role == 0 ? lane + 1 : role == 1 ? lane - 1 : lane;
       const int js = role == 1 ? sl - 1 : sl;  // the job's slot (shift)
       const double sgn = role == 1 ? -1.0 : 1.0;
       const double mysr = role == 3 ? 0.0 : W.sr[js], mysi = (role == 0 || role == 1) ? W.si[js] : 0.0;
-      // helper h (tw = 1 + h): 8-row block 2 s + h of every super-block s
-      const int h = tw - 1;
+      const int hm = h & 1;     // helper: 8-row block 2 s + hm of every super-block s
       double c[2][2][2] = {};   // [n-tile][k parity][2]: partial of the next super-block (S / T_f)
       double cz[2][2][2] = {};  // gsylv: the same with Tc (scaled by z per column when written)
       double la[4], lt[4];      // A fragments of T_f (S) / Tc [rows, rows of s+1] (k = i1 + 4 t4 + st)
@@ -1352,9 +1354,9 @@ __global__ void __launch_bounds__(kWideThreads, 2) fibre_wide_kernel(const Fibre
         WP_T(tA);
         team_sync(team);  // rows >= i1 final
         WP_ADD(2, tA);
-        if (tw > 0) {
+        if (tw > 0 && live) {
           // finish Y[block] -= T_f[block, i1:nf] Y[i1:nf]: the rows of s+1, then write
-          const int r0 = h == 0 ? i0 : mid, r1 = h == 0 ? mid : i1;
+          const int r0 = hm == 0 ? i0 : mid, r1 = hm == 0 ? mid : i1;
           if (r0 < r1 && i1 < nf) {
             const int i2 = a.rb[min(2 * q + 4, a.nrb)];
 #pragma unroll
@@ -1449,11 +1451,11 @@ __global__ void __launch_bounds__(kWideThreads, 2) fibre_wide_kernel(const Fibre
             if (bad) badoff = min(badoff, goff(B, mycol, i0, a.sf, a.sc));
           }
           WP_ADD(3, tL);
-        } else if (q >= 1) {
+        } else if (q >= 1 && live) {
           // partial of super-block s-1 over the final rows k >= i1, and the A
           // fragments of its update from the rows of s (used next step)
           const int p0 = a.rb[2 * q - 2], pm = a.rb[2 * q - 1];
-          const int r0 = h == 0 ? p0 : pm, r1 = h == 0 ? pm : i0;
+          const int r0 = hm == 0 ? p0 : pm, r1 = hm == 0 ? pm : i0;
           const int ra = r0 + g;
           const size_t roff = static_cast<size_t>(ra < r1 ? ra : p0) * nf;
           const double* trow = a.Tt + roff;
@@ -1531,7 +1533,7 @@ __global__ void __launch_bounds__(kWideThreads, 2) fibre_wide_kernel(const Fibre
   if (a.prof && lane == 0) {
     for (int k = 0; k < 7; ++k) atomicAdd(a.prof + k, static_cast<unsigned long long>(ph[k]));
     // sub-partition histogram of leaders (8..11) and helpers (12..15)
-    if (wrole[warp] >= 0) atomicAdd(a.prof + ((wrole[warp] & 3) == 0 ? 8 : 12) + (hwslot[warp] & 3), 1ull);
+    if (wrole[warp] >= 0) atomicAdd(a.prof + (wrole[warp] == 0 ? 8 : 12) + (hwslot[warp] & 3), 1ull);
   }
 #endif
   if (badoff != LLONG_MAX) atomicMin(a.status, static_cast<int>(badoff < INT_MAX - 1 ? badoff : INT_MAX - 1));
