@@ -503,7 +503,9 @@ template <int NF>
 __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const FibreArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int nf = a.nf;
-  const int ybuf = a.maxcol * nf;
+  // shared rows of a block: an odd pitch (ncol | 1) keeps the per-row
+  // butterflies (lanes over rows) free of bank conflicts
+  const int ybuf = (a.maxcol + 1) * nf;
   double* sT = sm;                      // NF x NF, row-major, zero padded
   double* sfc = sT + NF * NF;           // per row: code, a, omega
   double* Ys[2] = {sfc + 3 * NF, sfc + 3 * NF + ybuf};
@@ -544,7 +546,7 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
     }
   }
   __syncthreads();
-  if (SB[0].blk < a.nblocks) issue_block(a, SB[0].B, SB[0].pb, SB[0].nunit, Ys[0], SB[0].B.ncol, sus[0]);
+  if (SB[0].blk < a.nblocks) issue_block(a, SB[0].B, SB[0].pb, SB[0].nunit, Ys[0], SB[0].B.ncol | 1, sus[0]);
   int cur = 0;
 #if SMALL_PROF
   long long ph[8] = {};
@@ -572,7 +574,7 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
 #endif
     const bool more = Nx.blk < a.nblocks;
     if (more) {
-      issue_block(a, Nx.B, Nx.pb, Nx.nunit, Ys[cur ^ 1], Nx.B.ncol, sus[cur ^ 1]);
+      issue_block(a, Nx.B, Nx.pb, Nx.nunit, Ys[cur ^ 1], Nx.B.ncol | 1, sus[cur ^ 1]);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -583,7 +585,7 @@ __global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const Fib
     ph[1] += t2 - t1;
 #endif
     const Blk& B = C.B;
-    const int ncol = B.ncol, w = B.w, kb = B.kb, nunit = C.nunit;
+    const int ncol = B.ncol | 1, w = B.w, kb = B.kb, nunit = C.nunit;  // ncol: the shared pitch
     double* Y = Ys[cur];
     const FibreUnit* su = sus[cur];
     if (threadIdx.x == 0) {
@@ -1555,7 +1557,7 @@ cudaError_t launch_k(K k, const FibreArgs& a, size_t smem, int device, cudaStrea
 
 template <int NF>
 cudaError_t launch_small(const FibreArgs& a, int device, cudaStream_t st, SolveLaunchInfo* info) {
-  const size_t smem = (static_cast<size_t>(NF) * NF + 3 * NF + 2 * static_cast<size_t>(a.maxcol) * a.nf) * sizeof(double) +
+  const size_t smem = (static_cast<size_t>(NF) * NF + 3 * NF + 2 * static_cast<size_t>(a.maxcol + 1) * a.nf) * sizeof(double) +
                       2 * kMaxUnits * sizeof(FibreUnit) + (a.cell_smem ? a.cell_smem : 0) * sizeof(FibreCell);
   return launch_k(fibre_small_kernel<NF>, a, smem, device, st, info, kSmallThreads);
 }
