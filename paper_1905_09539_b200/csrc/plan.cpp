@@ -1935,9 +1935,11 @@ int try_decouple(tsg_plan* pl, const double* const* T, const double* const* U, c
   const int cell_smem = ncell_s <= 1024 ? ncell_s : 0;
   bool wide = false;
   if (small) {
-    // two block buffers (the next block streams in while one is solved)
+    // two block buffers (the next block streams in while one is solved) in
+    // ~100 KB: two CTAs per SM, blocks of >= 128 complex jobs for C3 (C3
+    // fibre solve 5.7 ms at 72 KB / 3 CTAs, 5.25 ms at 100 KB; TSG_FIBRE_SMEM_KB)
     const int NF = nf <= 8 ? 8 : nf <= 16 ? 16 : 24;
-    const long avail = (72 * 1024 - 2 * 128 * 32 - cell_smem * 24) / 8 - NF * NF - 3 * NF;
+    const long avail = ((std::getenv("TSG_FIBRE_SMEM_KB") ? std::atoi(std::getenv("TSG_FIBRE_SMEM_KB")) : 100) * 1024 - 2 * 128 * 32 - cell_smem * 24) / 8 - NF * NF - 3 * NF;
     W = static_cast<int>(std::min<long>(avail / (2 * (static_cast<long>(nf) << nsc)), 128));
   } else {
     const char* we = std::getenv("TSG_FIBRE_WIDE");

@@ -500,7 +500,7 @@ TSG_DEVINL void issue_block(const FibreArgs& a, const Blk& B, const int64_t* pb,
 }
 
 template <int NF>
-__global__ void __launch_bounds__(kSmallThreads, 3) fibre_small_kernel(const FibreArgs a) {
+__global__ void __launch_bounds__(kSmallThreads, 2) fibre_small_kernel(const FibreArgs a) {
   extern __shared__ __align__(16) double sm[];
   const int nf = a.nf;
   // shared rows of a block: an odd pitch (ncol | 1) keeps the per-row
