@@ -66,7 +66,7 @@ inline Tensor<double> gsylv_merged(std::vector<Matrix<double>> t, Matrix<double>
                                        std::min(n_min, matrix_floor_n_min));
     return Tensor<double>(b.dims(), std::vector<double>(x.data(), x.data() + x.size()));
   }
-  const Solvability s = check_solvable_gsylv(t, c);
+  const Solvability s = screen_gsylv_gpu(t, c);
   if (!s.solvable)
     throw singular_error(detail::witness_message("gsylv_merged", s), s.witness, s.witness_values,
                          s.min_abs);
@@ -96,7 +96,7 @@ inline SolveReport<double> solve_gsylv(const GSylvProblem<double>& p, const Solv
 
   std::vector<Matrix<double>> red{g.s};
   for (const auto& x : f) red.push_back(x.t);
-  const Solvability s = check_solvable_gsylv(red, g.t, cfg.singularity_tol);
+  const Solvability s = screen_gsylv_gpu(red, g.t, cfg.singularity_tol);
   if (!s.solvable)
     throw singular_error(detail::witness_message("solve_gsylv", s), s.witness, s.witness_values,
                          s.min_abs);

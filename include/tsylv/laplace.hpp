@@ -118,7 +118,7 @@ inline Tensor<double> laplace_merged(std::vector<Matrix<double>> t, Tensor<doubl
                                            std::min(n_min, matrix_floor_n_min));
     return Tensor<double>(b.dims(), std::vector<double>(x.data(), x.data() + x.size()));
   }
-  const Solvability s = check_solvable_laplace(t);
+  const Solvability s = screen_laplace_gpu(t);
   if (!s.solvable)
     throw singular_error(detail::witness_message("laplace_merged", s), s.witness,
                          s.witness_values, s.min_abs);
@@ -148,7 +148,7 @@ inline SolveReport<double> solve_laplace(const LaplaceProblem<double>& p,
 
   std::vector<Matrix<double>> t;
   for (const auto& s : f) t.push_back(s.t);
-  const Solvability s = check_solvable_laplace(t, cfg.singularity_tol);
+  const Solvability s = screen_laplace_gpu(t, cfg.singularity_tol);
   if (!s.solvable)
     throw singular_error(detail::witness_message("solve_laplace", s), s.witness, s.witness_values,
                          s.min_abs);

@@ -14,6 +14,7 @@
 #include <thread>
 #include <vector>
 
+#include "tsylv/gpu.hpp"
 #include "tsylv/matrix.hpp"
 #include "tsylv/scalar.hpp"
 
@@ -203,6 +204,58 @@ inline Solvability check_solvable_gsylv(const std::vector<Matrix<double>>& t,
   if (tol <= 0) tol = unit_roundoff<double> * scale;
   Solvability s = detail::min_pencil_product(t[0], c, tails);
   s.solvable = s.min_abs > tol;
+  return s;
+}
+
+// The same screens on the GPU (tsg_screen_laplace / tsg_screen_gsylv,
+// csrc/screen.cu): identical tolerance, witness and witness values; the
+// solve entry points use these (the reference runs the scan inside its timed
+// recursion, laplace.hpp:271-274, gsylv.hpp:267-270).
+inline Solvability screen_laplace_gpu(const std::vector<Matrix<double>>& t, double tol = 0) {
+  if (t.empty()) throw dimension_error("check_solvable_laplace: no coefficients");
+  std::vector<EigList> e;
+  std::vector<int> dims;
+  std::vector<const double*> tp;
+  for (const auto& m : t) {
+    e.push_back(quasi_tri_eigenvalues(m));  // validates the factor
+    dims.push_back(m.rows());
+    tp.push_back(m.data());
+  }
+  Solvability s;
+  s.witness.assign(t.size(), 0);
+  int ok = 0;
+  gpu::check(tsg_screen_laplace(gpu::context(), static_cast<int>(t.size()), dims.data(), tp.data(), tol, &s.min_abs,
+                                s.witness.data(), &ok),
+             "check_solvable_laplace");
+  s.solvable = ok != 0;
+  for (size_t m = 0; m < t.size(); ++m) s.witness_values.push_back(e[m][s.witness[m]]);
+  return s;
+}
+
+inline Solvability screen_gsylv_gpu(const std::vector<Matrix<double>>& t, const Matrix<double>& c, double tol = 0) {
+  if (t.size() < 2) throw dimension_error("check_solvable_gsylv: need at least two modes");
+  if (c.rows() != t[0].rows() || c.cols() != t[0].cols())
+    throw dimension_error("check_solvable_gsylv: C must match A_0");
+  if (!is_upper_triangular(c)) throw dimension_error("check_solvable_gsylv: C must be upper triangular");
+  std::vector<EigList> tails;
+  std::vector<int> dims{t[0].rows()};
+  std::vector<const double*> tp;
+  (void)quasi_tri_eigenvalues(t[0]);  // validates A_0
+  for (size_t m = 1; m < t.size(); ++m) {
+    tails.push_back(quasi_tri_eigenvalues(t[m]));
+    dims.push_back(t[m].rows());
+    tp.push_back(t[m].data());
+  }
+  Solvability s;
+  s.witness.assign(t.size(), 0);
+  int ok = 0;
+  gpu::check(tsg_screen_gsylv(gpu::context(), static_cast<int>(t.size()), dims.data(), t[0].data(), c.data(),
+                              tp.data(), tol, &s.min_abs, s.witness.data(), &ok),
+             "check_solvable_gsylv");
+  s.solvable = ok != 0;
+  using C = std::complex<double>;
+  s.witness_values = {C(t[0](s.witness[0], s.witness[0])), C(c(s.witness[0], s.witness[0]))};
+  for (size_t m = 1; m < t.size(); ++m) s.witness_values.push_back(tails[m - 1][s.witness[m]]);
   return s;
 }
 

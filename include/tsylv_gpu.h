@@ -162,6 +162,16 @@ int tsg_mode_multiply(tsg_ctx* ctx, int d, const int* dims, const double* X,
  * (Laplace, family 0) or ||A_0||_F + ||C||_F prod_{m>=1} ||A_m||_F (gsylv,
  * family 1), computed through mode products only.  A holds the d dense
  * ORIGINAL coefficients; C is NULL for Laplace.  B/X follow inputs_on_device. */
+/* Solvability screen on the GPU (reference solvability.hpp:31-116): the
+ * smallest |operator eigenvalue| over every eigenvalue tuple of the
+ * quasi-triangular factors, its first position in the reference's scan order
+ * (witness: Laplace one index per mode; gsylv the 2x2/1x1 block's first row of
+ * S, then one index per tail mode), solvable = min_abs > tol (tol <= 0:
+ * unit roundoff times the sum of the factors' Frobenius norms). */
+int tsg_screen_laplace(tsg_ctx* ctx, int d, const int* dims, const double* const* T, double tol,
+                       double* min_abs, int* witness, int* solvable);
+int tsg_screen_gsylv(tsg_ctx* ctx, int d, const int* dims, const double* S, const double* Tc,
+                     const double* const* Ttail, double tol, double* min_abs, int* witness, int* solvable);
 int tsg_residual(tsg_ctx* ctx, int family, int d, const int* dims,
                  const double* const* A, const double* C, const double* B,
                  const double* X, int inputs_on_device, double* out);

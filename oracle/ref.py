@@ -51,6 +51,7 @@ def lib() -> ctypes.CDLL:
             "ref_residual_laplace": (D, [I, Ip, Dpp, Dp, Dp]),
             "ref_residual_gsylv": (D, [I, Ip, Dpp, Dp, Dp, Dp]),
             "ref_check_solvable_laplace": (I, [I, Ip, Dpp, D, Dp, Ip, Ip, E, I]),
+            "ref_check_solvable_gsylv": (I, [I, Ip, Dpp, Dp, D, Dp, Ip, Ip, E, I]),
             "ref_rng_new": (P, [ctypes.c_uint64]),
             "ref_rng_free": (None, [P]),
             "ref_rng_uniform": (D, [P]),
@@ -344,3 +345,29 @@ class RandomStream:
         out = np.zeros(n * n)
         lib().ref_randn_quasi_triangular(self.h, n, diag_shift, pair_prob, _p(out))
         return out.reshape((n, n), order="F").copy(order="F")
+
+
+def check_solvable_laplace(t, tol=0.0):
+    """The reference's check_solvable_laplace (laplace.hpp:28-43) on reduced
+    coefficients: (min_abs, witness, solvable)."""
+    t = [_f(m) for m in t]
+    pp, keep = _pp(t)
+    mn, ok = ctypes.c_double(), ctypes.c_int()
+    wit = (ctypes.c_int * len(t))()
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_check_solvable_laplace(len(t), _dims([m.shape[0] for m in t]), pp, tol, ctypes.byref(mn),
+                                          wit, ctypes.byref(ok), err, 1024), err)
+    return mn.value, list(wit), bool(ok.value)
+
+
+def check_solvable_gsylv(t, c, tol=0.0):
+    """The reference's check_solvable_gsylv (gsylv.hpp:31-50): t = [S, tails..],
+    c = the upper triangular pencil partner: (min_abs, witness, solvable)."""
+    t = [_f(m) for m in t]
+    pp, keep = _pp(t)
+    mn, ok = ctypes.c_double(), ctypes.c_int()
+    wit = (ctypes.c_int * len(t))()
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_check_solvable_gsylv(len(t), _dims([m.shape[0] for m in t]), pp, _p(_f(c)), tol,
+                                        ctypes.byref(mn), wit, ctypes.byref(ok), err, 1024), err)
+    return mn.value, list(wit), bool(ok.value)

@@ -286,6 +286,19 @@ int ref_check_solvable_laplace(int d, const int* dims, const double* const* t,
   });
 }
 
+int ref_check_solvable_gsylv(int d, const int* dims, const double* const* t, const double* c,
+                             double tol, double* min_abs, int* witness, int* solvable, char* err,
+                             int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<Matrix<double>> coeffs;
+    for (int m = 0; m < d; ++m) coeffs.push_back(mat(dims[m], dims[m], t[m]));
+    Solvability s = check_solvable_gsylv(coeffs, mat(dims[0], dims[0], c), tol);
+    *min_abs = s.min_abs;
+    *solvable = s.solvable ? 1 : 0;
+    for (std::size_t i = 0; i < s.witness.size(); ++i) witness[i] = s.witness[i];
+  });
+}
+
 // ---- RandomStream (random.hpp:19-77) ------------------------------------
 void* ref_rng_new(std::uint64_t seed) { return new RandomStream(seed); }
 void ref_rng_free(void* r) { delete static_cast<RandomStream*>(r); }

@@ -7,13 +7,15 @@ this package is the Python host mirror of the reference's API on top of it.
 from .api import (Arithmetic, GSylvProblem, LaplaceProblem, PhaseTimings, RandomStream,
                   SolveReport, SolverConfig, Strategy, dimension_error, factorization_error,
                   gpu_error, gsylv_merged, gsylv_recursive, laplace_merged, laplace_recursive,
-                  make_problem, mode_multiply, oracle, qz, residual, schur, singular_error,
-                  solve_gsylv, solve_gsylv_tri, solve_laplace, solve_sylvester_tri)
+                  make_problem, mode_multiply, oracle, qz, residual, schur, screen_gsylv,
+                  screen_laplace, singular_error, solve_gsylv, solve_gsylv_tri, solve_laplace,
+                  solve_sylvester_tri)
 
 __all__ = [
     "Arithmetic", "GSylvProblem", "LaplaceProblem", "PhaseTimings", "RandomStream", "SolveReport",
     "SolverConfig", "Strategy", "dimension_error", "factorization_error", "gpu_error",
     "gsylv_merged", "gsylv_recursive", "laplace_merged", "laplace_recursive", "make_problem",
-    "mode_multiply", "oracle", "qz", "residual", "schur", "singular_error", "solve_gsylv",
+    "mode_multiply", "oracle", "qz", "residual", "schur", "screen_gsylv", "screen_laplace",
+    "singular_error", "solve_gsylv",
     "solve_gsylv_tri", "solve_laplace", "solve_sylvester_tri",
 ]

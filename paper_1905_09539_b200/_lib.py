@@ -39,7 +39,7 @@ TSG_SYMBOLS = [
     "tsg_laplace_reduced", "tsg_gsylv_solve", "tsg_gsylv_reduced", "tsg_plan_create",
     "tsg_plan_execute", "tsg_plan_execute_stream", "tsg_plan_destroy", "tsg_plan_info",
     "tsg_plan_enqueue", "tsg_plan_sync", "tsg_plan_set_serial", "tsg_plan_describe",
-    "tsg_plan_transform", "tsg_plan_free_mode",
+    "tsg_plan_transform", "tsg_plan_free_mode", "tsg_screen_laplace", "tsg_screen_gsylv",
     "tsg_mode_multiply",
     "tsg_residual", "tsg_abi_version",
     "tsg_slab_bounds", "tsg_dplan_create", "tsg_dplan_destroy", "tsg_dplan_info",
@@ -70,6 +70,9 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tsg_plan_set_serial": (I, [P, I]),
         "tsg_plan_transform": (I, [P, I, P, P, P]),
         "tsg_plan_free_mode": (I, [P]),
+        "tsg_screen_laplace": (I, [P, I, c_int_p, c_dbl_pp, ctypes.c_double, c_dbl_p, c_int_p, c_int_p]),
+        "tsg_screen_gsylv": (I, [P, I, c_int_p, c_dbl_p, c_dbl_p, c_dbl_pp, ctypes.c_double, c_dbl_p, c_int_p,
+                                 c_int_p]),
         "tsg_plan_info": (I, [P, ctypes.POINTER(ctypes.c_int64), c_int_p, c_dbl_p]),
         "tsg_plan_describe": (I, [P, ctypes.c_char_p, I]),
         "tsg_residual": (I, [P, I, I, c_int_p, c_dbl_pp, P, P, P, I, c_dbl_p]),

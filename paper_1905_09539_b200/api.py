@@ -410,3 +410,49 @@ def make_problem(kind: int, dims, seed: int = 1):
     if kind == 5:
         return GSylvProblem(mats, c.reshape((dims[0], dims[0]), order="F").copy(order="F"), rhs)
     return LaplaceProblem(mats, rhs)
+
+
+# ---- solvability screen (reference solvability.hpp:31-116) ----------------
+_screen_ctx = None
+
+
+def _ctx():
+    global _screen_ctx
+    if _screen_ctx is None:
+        from .plan import Context
+        _screen_ctx = Context(0)
+    return _screen_ctx
+
+
+def screen_laplace(t: list, tol: float = 0.0):
+    """GPU screen of the reduced Laplace operator (quasi-triangular factors):
+    (min |eigenvalue|, witness per mode, solvable) — tsg_screen_laplace."""
+    t = [_f(m) for m in t]
+    d = len(t)
+    pp, keep = _ptrs(t)
+    mn, ok = ctypes.c_double(), ctypes.c_int()
+    wit = (ctypes.c_int * d)()
+    ctx = _ctx()
+    rc = lib().tsg_screen_laplace(ctx.h, d, (ctypes.c_int * d)(*[m.shape[0] for m in t]), pp, tol,
+                                  ctypes.byref(mn), wit, ctypes.byref(ok))
+    if rc != 0:
+        raise gpu_error(f"tsg_screen_laplace failed ({rc}): {ctx.error()}")
+    return mn.value, list(wit), bool(ok.value)
+
+
+def screen_gsylv(s: np.ndarray, tc: np.ndarray, tails: list, tol: float = 0.0):
+    """GPU screen of the reduced gsylv pencil: S, Tc (QZ pair of mode 0) and
+    the tail factors — tsg_screen_gsylv."""
+    s, tc = _f(s), _f(tc)
+    tails = [_f(m) for m in tails]
+    d = 1 + len(tails)
+    pp, keep = _ptrs(tails)
+    mn, ok = ctypes.c_double(), ctypes.c_int()
+    wit = (ctypes.c_int * d)()
+    dims = [s.shape[0]] + [m.shape[0] for m in tails]
+    ctx = _ctx()
+    rc = lib().tsg_screen_gsylv(ctx.h, d, (ctypes.c_int * d)(*dims), _ptr(s), _ptr(tc), pp, tol,
+                                ctypes.byref(mn), wit, ctypes.byref(ok))
+    if rc != 0:
+        raise gpu_error(f"tsg_screen_gsylv failed ({rc}): {ctx.error()}")
+    return mn.value, list(wit), bool(ok.value)
