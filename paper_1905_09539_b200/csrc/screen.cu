@@ -11,11 +11,13 @@
 //             every diagonal block b of S: |S_bb + z T_bb| (1x1) or the
 //             smaller eigenvalue magnitude of the 2x2 pencil block;
 //             index L = b + n_blocks * (j_1 + n_1 (...)).
-// The sums and products are formed in the reference's order, so the values
-// match the host screen to rounding of |.|; the first minimum (smallest L
-// among equal values, the reference's strict `<` scan) comes from two
-// passes: atomicMin of the value's bit pattern (non-negative doubles order
-// like their bits), then atomicMin of L over the tuples attaining it.
+// The sums and products are formed in the reference's order (the inner
+// partial sums / products once per inner index, then the last factor), so
+// the values match the host screen to rounding of |.|; the first minimum
+// (smallest L among equal values, the reference's strict `<` scan) comes
+// from two passes: atomicMin of the value's bit pattern (non-negative
+// doubles order like their bits), then atomicMin of L over the tuples
+// attaining it.
 #include <cstdint>
 #include <cstring>
 
@@ -48,12 +50,14 @@ TSG_DEVINL Cx csqrt(Cx a) {
 }
 
 struct ScreenArgs {
-  int d;
+  int d;              // lists folded into the "inner" array (Laplace: modes 0..d-2; gsylv: all tails)
   int n[8];           // extents of the eigenvalue lists
   const Cx* eig[8];   // eigenvalue lists (Laplace: all modes; gsylv: tails)
-  int64_t total;      // tuples
+  int64_t ninner;     // prod of the inner extents
+  Cx* inner;          // device: the partial sums (Laplace) / products (gsylv) in scan order
+  int nouter;         // Laplace: n_{d-1} (the last mode's eigenvalues, eig[d]); gsylv: pencil blocks
+  const Cx* outer;    // Laplace: the last mode's eigenvalues
   // gsylv pencil blocks
-  int nblk;
   const int* bstart;  // per block: first row
   const int* bsize;   // 1 or 2
   const double* S;    // n0 x n0 column-major
@@ -62,58 +66,65 @@ struct ScreenArgs {
   unsigned long long* key;  // [0] min value bits, [1] min index
 };
 
+// inner[p]: p decoded mode 0 fastest; Laplace ((0 + l_0) + l_1) + ..., gsylv ((1 * m_1) * m_2) ...
 template <bool GS>
-TSG_DEVINL double tuple_value(const ScreenArgs& a, int64_t L) {
-  if (!GS) {
-    int64_t r = L;
-    Cx s{0.0, 0.0};
+__global__ void inner_kernel(const ScreenArgs a) {
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < a.ninner;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    unsigned r = static_cast<unsigned>(p);
+    Cx s = GS ? Cx{1.0, 0.0} : Cx{0.0, 0.0};
     for (int m = 0; m < a.d; ++m) {
-      const int64_t q = r / a.n[m];
-      const int i = static_cast<int>(r - q * a.n[m]);
+      const unsigned q = r / static_cast<unsigned>(a.n[m]);
+      const int i = static_cast<int>(r - q * static_cast<unsigned>(a.n[m]));
       r = q;
-      s = cadd(s, a.eig[m][i]);
+      s = GS ? cmul(s, a.eig[m][i]) : cadd(s, a.eig[m][i]);
     }
-    return cabs(s);
-  } else {
-    const int64_t pz = L / a.nblk;
-    const int b = static_cast<int>(L - pz * a.nblk);
-    int64_t r = pz;
-    Cx z{1.0, 0.0};
-    for (int m = 0; m < a.d; ++m) {
-      const int64_t q = r / a.n[m];
-      const int j = static_cast<int>(r - q * a.n[m]);
-      r = q;
-      z = cmul(z, a.eig[m][j]);
-    }
-    const int i = a.bstart[b];
-    const double* S = a.S;
-    const double* T = a.Tc;
-    const int n0 = a.n0;
-    auto at = [&](const double* M, int r_, int c_) { return M[r_ + static_cast<int64_t>(c_) * n0]; };
-    // C(s) + z * t, t real: (s + z.re t, z.im t)
-    auto pen = [&](int r_, int c_) {
-      const double t = at(T, r_, c_);
-      return Cx{__dadd_rn(at(S, r_, c_), __dmul_rn(z.re, t)), __dmul_rn(z.im, t)};
-    };
-    if (a.bsize[b] == 1) return cabs(pen(i, i));
-    const Cx m00 = pen(i, i), m01 = pen(i, i + 1), m11 = pen(i + 1, i + 1);
-    const Cx m10{at(S, i + 1, i), 0.0};
-    const Cx sm = cadd(m00, m11);
-    const Cx h{__dmul_rn(0.5, sm.re), __dmul_rn(0.5, sm.im)};
-    const Cx p1 = cmul(m00, m11), p2 = cmul(m01, m10);
-    const Cx det{__dsub_rn(p1.re, p2.re), __dsub_rn(p1.im, p2.im)};
-    const Cx hh = cmul(h, h);
-    const Cx rt = csqrt(Cx{__dsub_rn(hh.re, det.re), __dsub_rn(hh.im, det.im)});
-    return fmin(cabs(cadd(h, rt)), cabs(Cx{__dsub_rn(h.re, rt.re), __dsub_rn(h.im, rt.im)}));
+    a.inner[p] = s;
   }
+}
+
+// value of tuple (inner p, outer o): Laplace |inner[p] + lambda_{d-1}[o]|;
+// gsylv: block o of the pencil S + z Tc with z = inner[p]
+template <bool GS>
+TSG_DEVINL double tuple_value(const ScreenArgs& a, Cx z, int o) {
+  if (!GS) return cabs(cadd(z, a.outer[o]));
+  const int i = a.bstart[o];
+  const double* S = a.S;
+  const double* T = a.Tc;
+  const int n0 = a.n0;
+  auto at = [&](const double* M, int r_, int c_) { return M[r_ + static_cast<int64_t>(c_) * n0]; };
+  // C(s) + z * t, t real: (s + z.re t, z.im t)
+  auto pen = [&](int r_, int c_) {
+    const double t = at(T, r_, c_);
+    return Cx{__dadd_rn(at(S, r_, c_), __dmul_rn(z.re, t)), __dmul_rn(z.im, t)};
+  };
+  if (a.bsize[o] == 1) return cabs(pen(i, i));
+  const Cx m00 = pen(i, i), m01 = pen(i, i + 1), m11 = pen(i + 1, i + 1);
+  const Cx m10{at(S, i + 1, i), 0.0};
+  const Cx sm = cadd(m00, m11);
+  const Cx h{__dmul_rn(0.5, sm.re), __dmul_rn(0.5, sm.im)};
+  const Cx p1 = cmul(m00, m11), p2 = cmul(m01, m10);
+  const Cx det{__dsub_rn(p1.re, p2.re), __dsub_rn(p1.im, p2.im)};
+  const Cx hh = cmul(h, h);
+  const Cx rt = csqrt(Cx{__dsub_rn(hh.re, det.re), __dsub_rn(hh.im, det.im)});
+  return fmin(cabs(cadd(h, rt)), cabs(Cx{__dsub_rn(h.re, rt.re), __dsub_rn(h.im, rt.im)}));
+}
+
+// Scan order: Laplace L = p + ninner * o (the last mode slowest); gsylv
+// L = o + nblk * p (blocks fastest).  Each thread owns inner indices p.
+template <bool GS>
+TSG_DEVINL int64_t lin(const ScreenArgs& a, int64_t p, int o) {
+  return GS ? static_cast<int64_t>(o) + static_cast<int64_t>(a.nouter) * p : p + a.ninner * o;
 }
 
 template <bool GS>
 __global__ void __launch_bounds__(kThreads) min_kernel(const ScreenArgs a) {
   double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-  for (int64_t L = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; L < a.total;
-       L += static_cast<int64_t>(gridDim.x) * kThreads)
-    best = fmin(best, tuple_value<GS>(a, L));
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; p < a.ninner;
+       p += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const Cx z = a.inner[p];
+    for (int o = 0; o < a.nouter; ++o) best = fmin(best, tuple_value<GS>(a, z, o));
+  }
   for (int o = 16; o > 0; o >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, o));
   __shared__ double wb[kThreads / 32];
   if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = best;
@@ -128,12 +139,15 @@ template <bool GS>
 __global__ void __launch_bounds__(kThreads) argmin_kernel(const ScreenArgs a) {
   const unsigned long long vkey = *a.key;
   unsigned long long first = ~0ull;
-  for (int64_t L = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; L < a.total;
-       L += static_cast<int64_t>(gridDim.x) * kThreads) {
-    if (static_cast<unsigned long long>(__double_as_longlong(tuple_value<GS>(a, L))) == vkey) {
-      first = static_cast<unsigned long long>(L);
-      break;  // L grows along the thread's sweep: its first hit is its smallest
-    }
+  for (int64_t p = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; p < a.ninner;
+       p += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const Cx z = a.inner[p];
+    for (int o = 0; o < a.nouter; ++o)
+      if (static_cast<unsigned long long>(__double_as_longlong(tuple_value<GS>(a, z, o))) == vkey) {
+        const unsigned long long L = static_cast<unsigned long long>(lin<GS>(a, p, o));
+        first = L < first ? L : first;
+        break;  // the smallest o of this p gives its smallest L in both orders
+      }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long v = __shfl_xor_sync(0xffffffffu, first, o);
@@ -144,8 +158,9 @@ __global__ void __launch_bounds__(kThreads) argmin_kernel(const ScreenArgs a) {
 
 template <bool GS>
 cudaError_t run(ScreenArgs& a, int nsm, cudaStream_t st) {
-  const int64_t want = (a.total + kThreads - 1) / kThreads;
+  const int64_t want = (a.ninner + kThreads - 1) / kThreads;
   const int grid = static_cast<int>(want < 16LL * nsm ? (want > 0 ? want : 1) : 16LL * nsm);
+  inner_kernel<GS><<<grid, kThreads, 0, st>>>(a);
   min_kernel<GS><<<grid, kThreads, 0, st>>>(a);
   argmin_kernel<GS><<<grid, kThreads, 0, st>>>(a);
   return cudaGetLastError();
@@ -155,25 +170,23 @@ cudaError_t run(ScreenArgs& a, int nsm, cudaStream_t st) {
 
 cudaError_t screen_min(const ScreenSpec& sp, cudaStream_t st, double* min_abs, int64_t* index) {
   ScreenArgs a{};
-  a.d = sp.nlists;
-  a.total = 1;
+  const bool gs = sp.S != nullptr;
+  // Laplace: inner = modes 0..d-2, outer = the last mode; gsylv: inner = every tail, outer = the blocks
+  a.d = gs ? sp.nlists : sp.nlists - 1;
+  a.ninner = 1;
   size_t neig = 0;
   for (int m = 0; m < sp.nlists; ++m) {
     a.n[m] = sp.n[m];
-    a.total *= sp.n[m];
     neig += sp.n[m];
+    if (m < a.d) a.ninner *= sp.n[m];
   }
-  const bool gs = sp.S != nullptr;
-  if (gs) {
-    a.nblk = sp.nblk;
-    a.total *= sp.nblk;
-    a.n0 = sp.n0;
-  }
-  // one device allocation: eigenvalue lists, block tables, pencil matrices, keys
+  if (a.ninner >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+  a.nouter = gs ? sp.nblk : sp.n[sp.nlists - 1];
+  if (gs) a.n0 = sp.n0;
   const size_t bytes_eig = neig * sizeof(Cx);
   const size_t nn = gs ? static_cast<size_t>(sp.n0) * sp.n0 : 0;
-  const size_t bytes = 2 * sizeof(unsigned long long) + bytes_eig + 2 * nn * sizeof(double) +
-                       (gs ? 2 * sp.nblk * sizeof(int) : 0);
+  const size_t bytes = 2 * sizeof(unsigned long long) + bytes_eig + static_cast<size_t>(a.ninner) * sizeof(Cx) +
+                       2 * nn * sizeof(double) + (gs ? 2 * sp.nblk * sizeof(int) : 0);
   char* buf = nullptr;
   cudaError_t e = cudaMallocAsync(&buf, bytes, st);
   if (e != cudaSuccess) return e;
@@ -189,7 +202,10 @@ cudaError_t screen_min(const ScreenSpec& sp, cudaStream_t st, double* min_abs, i
                         cudaMemcpyHostToDevice, st);
     off += sp.n[m];
   }
+  if (!gs) a.outer = a.eig[sp.nlists - 1];
   p += bytes_eig;
+  a.inner = reinterpret_cast<Cx*>(p);
+  p += static_cast<size_t>(a.ninner) * sizeof(Cx);
   if (gs && e == cudaSuccess) {
     double* dS = reinterpret_cast<double*>(p);
     double* dT = dS + nn;
