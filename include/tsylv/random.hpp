@@ -117,4 +117,50 @@ inline GSylvProblem<double> baseline_gsylv(const std::vector<int>& dims, std::ui
   return p;
 }
 
+// ---- reduced-form (triangular) instances, real arithmetic ----------------
+// The reference's correctness-suite generators (random.hpp:79-223) for
+// T = double, drawing in the same order: strictly-upper Gaussian entries
+// column by column, then the diagonal.
+
+// Upper triangular, Gaussian entries, diagonal |N(0,1)| + floor_re.
+inline Matrix<double> randn_triangular_posdiag(RandomStream& rng, int n, double floor_re = 1.0) {
+  Matrix<double> m(n, n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i <= j; ++i) m(i, j) = rng.normal();
+  for (int i = 0; i < n; ++i) m(i, i) = std::abs(rng.normal()) + floor_re;
+  return m;
+}
+
+// Upper triangular, diagonal magnitudes in [lo, hi] with a random sign.
+inline Matrix<double> randn_triangular_ringdiag(RandomStream& rng, int n, double lo, double hi) {
+  Matrix<double> m(n, n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i <= j; ++i) m(i, j) = rng.normal();
+  for (int i = 0; i < n; ++i) {
+    const double r = lo + (hi - lo) * rng.uniform();
+    m(i, i) = rng.uniform() < 0.5 ? -r : r;
+  }
+  return m;
+}
+
+// Laplace: diagonals >= 1, so every eigenvalue sum is >= d.
+inline LaplaceProblem<double> random_reduced_laplace(RandomStream& rng, const std::vector<int>& dims) {
+  LaplaceProblem<double> p;
+  for (int n : dims) p.coeffs.push_back(randn_triangular_posdiag(rng, n, 1.0));
+  p.rhs = randn_tensor(rng, dims);
+  return p;
+}
+
+// gsylv: a0_ii >= 1, |c_ii| <= 0.09, |prod of later diagonals| <= 0.9.
+inline GSylvProblem<double> random_reduced_gsylv(RandomStream& rng, const std::vector<int>& dims) {
+  GSylvProblem<double> p;
+  const int n0 = dims[0];
+  p.coeffs.push_back(randn_triangular_posdiag(rng, n0, 1.0));
+  p.c = randn_triangular_ringdiag(rng, n0, 0.05, 0.3);
+  p.c *= 0.3;
+  for (std::size_t m = 1; m < dims.size(); ++m) p.coeffs.push_back(randn_triangular_ringdiag(rng, dims[m], 0.3, 0.95));
+  p.rhs = randn_tensor(rng, dims);
+  return p;
+}
+
 }  // namespace tsylv
