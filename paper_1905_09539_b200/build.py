@@ -25,6 +25,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libtsylv_gpu.so")
+CLI = os.path.join(HERE, "bin", "tsylv")
+CLI_SRC = os.path.join(ROOT, "tools", "tsylv_cli.cpp")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -42,6 +44,39 @@ def blas_lib() -> tuple[str, str]:
         raise RuntimeError("no LAPACK-exporting OpenBLAS found (opencv_python_headless.libs)")
     lib = cands[0]
     return os.path.dirname(lib), lib
+
+
+def json_include() -> str | None:
+    """Directory holding nlohmann/json.hpp (the copy cudnn_frontend ships in
+    this image), for the JSON problem files (include/tsylv/io.hpp)."""
+    for p in site.getsitepackages() + [site.getusersitepackages()]:
+        for hit in glob.glob(os.path.join(p, "include", "*", "thirdparty", "nlohmann", "json.hpp")):
+            return os.path.dirname(os.path.dirname(hit))
+    return None
+
+
+def cxx_user_cmd(src: str, out: str, opt: str = "-O2") -> list[str]:
+    """g++ command for a C++ user of the drop-in headers: include/, the
+    library, its OpenBLAS and (when present) nlohmann/json."""
+    bdir, blib = blas_lib()
+    jinc = json_include()
+    cmd = ["g++", "-std=c++20", opt, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(cuda_home(), "include")]
+    if jinc:
+        cmd += ["-I", jinc]
+    return cmd + [src, "-o", out, LIB, blib, f"-Wl,--disable-new-dtags,-rpath,{HERE}:{bdir}", "-lpthread"]
+
+
+def build_cli(force: bool = False, verbose: bool = False) -> str | None:
+    """The command-line front end (tools/tsylv_cli.cpp, the reference's
+    tools/tsylv.cpp) as paper_1905_09539_b200/bin/tsylv; None without
+    nlohmann/json."""
+    if json_include() is None:
+        return None
+    headers = glob.glob(os.path.join(ROOT, "include", "tsylv", "*.hpp")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+    if force or _newer(CLI, [CLI_SRC, LIB] + headers):
+        os.makedirs(os.path.dirname(CLI), exist_ok=True)
+        _run(cxx_user_cmd(CLI_SRC, CLI), verbose)
+    return CLI
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -101,6 +136,7 @@ def main() -> None:
     ap.add_argument("--verbose", action="store_true")
     a = ap.parse_args()
     print(build(a.force, a.verbose))
+    print(build_cli(a.force, a.verbose))
 
 
 if __name__ == "__main__":
