@@ -54,8 +54,9 @@ inline void fill_gpu(GpuTimings& g, const tsg_report& r) {
   g.flops_exec = r.flops_exec;
 }
 
-inline void require_reduced(const std::vector<Matrix<double>>& t, const Tensor<double>& b,
-                            int n_min, const char* who, bool strict_triangular = false) {
+template <typename T>
+void require_reduced(const std::vector<Matrix<T>>& t, const Tensor<T>& b, int n_min,
+                     const char* who, bool strict_triangular = false) {
   if (n_min < 1) throw dimension_error(std::string(who) + ": n_min must be >= 1");
   if (t.empty() || b.order() != static_cast<int>(t.size()))
     throw dimension_error(std::string(who) + ": rhs order does not match coefficient count");
@@ -68,6 +69,27 @@ inline void require_reduced(const std::vector<Matrix<double>>& t, const Tensor<d
                             (strict_triangular ? " must be upper triangular"
                                                : " must be upper quasi-triangular"));
   }
+}
+
+// solve_laplace / solve_gsylv on complex data: merge + real arithmetic is
+// rejected first, then real arithmetic on complex data (laplace.hpp:304-315).
+inline void check_config_complex(const SolverConfig& cfg, const char* who) {
+  check_config(cfg, who);
+  if (cfg.arithmetic == Arithmetic::real_quasitriangular)
+    throw std::invalid_argument(std::string(who) + ": real arithmetic requires real data");
+}
+
+inline const double* dp(const Complex* p) { return reinterpret_cast<const double*>(p); }
+inline double* dp(Complex* p) { return reinterpret_cast<double*>(p); }
+inline std::vector<const double*> zptrs(const std::vector<Matrix<Complex>>& v) {
+  std::vector<const double*> r;
+  for (const auto& m : v) r.push_back(dp(m.data()));
+  return r;
+}
+inline bool all_triangular(const std::vector<Matrix<Complex>>& v) {
+  for (const auto& m : v)
+    if (!is_upper_triangular(m)) return false;
+  return true;
 }
 
 }  // namespace detail
@@ -142,7 +164,7 @@ inline SolveReport<double> solve_laplace(const LaplaceProblem<double>& p,
   rep.strategy = cfg.strategy;
 
   StopWatch sw;
-  std::vector<SchurFactorization> f;
+  std::vector<SchurFactorization<double>> f;
   for (const auto& a : p.coeffs) f.push_back(schur(a));
   rep.timings.reduction_s = sw.lap();
 
@@ -163,6 +185,119 @@ inline SolveReport<double> solve_laplace(const LaplaceProblem<double>& p,
   Tensor<double> x(p.rhs.dims());
   gpu::check(tsg_laplace_solve(gpu::context(), d, p.rhs.dims().data(), tp.data(), up.data(),
                                p.rhs.data(), x.data(), &o, &r),
+             "solve_laplace");
+  const double gpu_s = sw.lap();
+  const double back_frac = r.t_total_ms > 0 ? (r.t_back_ms + r.t_d2h_ms) / r.t_total_ms : 0.0;
+  rep.timings.back_transform_s = gpu_s * back_frac;
+  rep.timings.recursion_s = gpu_s - rep.timings.back_transform_s;
+  detail::fill_gpu(rep.gpu, r);
+  rep.solution = std::move(x);
+  rep.residual = residual(p, rep.solution);
+  return rep;
+}
+
+// ---- T = Complex: complex Schur (zgees) on the host,
+// the complex GPU path (tsg_zlaplace_*, csrc/zsolve.cu, csrc/zplan.cpp):
+// complex DMMA transforms and the eigen-decoupled triangular fibre solve
+// (wavefront back substitution for ill-conditioned eigenbases).
+
+inline double residual(const LaplaceProblem<Complex>& p, const Tensor<Complex>& x) {
+  validate(p);
+  if (x.dims() != p.rhs.dims()) throw dimension_error("residual: solution shape mismatch");
+  const std::vector<const double*> a = detail::zptrs(p.coeffs);
+  double r = 0;
+  gpu::check(tsg_zresidual(gpu::context(), 0, p.order(), p.rhs.dims().data(), a.data(), nullptr,
+                           detail::dp(p.rhs.data()), detail::dp(x.data()), 0, &r),
+             "residual");
+  return r;
+}
+
+// Reduced form (laplace.hpp:185-195 with T = Complex).  Complex quasi-
+// triangular coefficients (2x2 diagonal blocks) are accepted like the
+// reference; they are first brought to triangular form by a complex Schur
+// decomposition and solved through the full pipeline.
+inline Tensor<Complex> laplace_recursive(const std::vector<Matrix<Complex>>& t,
+                                         Tensor<Complex> b, int n_min) {
+  detail::require_reduced(t, b, n_min, "laplace_recursive");
+  tsg_opts o = detail::gpu_opts(n_min);
+  Tensor<Complex> x(b.dims());
+  if (detail::all_triangular(t)) {
+    const std::vector<const double*> tp = detail::zptrs(t);
+    gpu::check(tsg_zlaplace_reduced(gpu::context(), b.order(), b.dims().data(), tp.data(),
+                                    detail::dp(b.data()), detail::dp(x.data()), &o, nullptr),
+               "laplace_recursive");
+    return x;
+  }
+  std::vector<SchurFactorization<Complex>> f;
+  for (const auto& m : t) f.push_back(schur(m));
+  std::vector<const double*> tp, up;
+  for (const auto& s : f) {
+    tp.push_back(detail::dp(s.t.data()));
+    up.push_back(detail::dp(s.u.data()));
+  }
+  gpu::check(tsg_zlaplace_solve(gpu::context(), b.order(), b.dims().data(), tp.data(), up.data(),
+                                detail::dp(b.data()), detail::dp(x.data()), &o, nullptr),
+             "laplace_recursive");
+  return x;
+}
+
+// laplace.hpp:202-244 with T = Complex: strictly triangular coefficients;
+// d = 2 forwards to solve_sylvester_tri(T_0, conj(T_1), B, min(n_min, 8)).
+inline Tensor<Complex> laplace_merged(std::vector<Matrix<Complex>> t, Tensor<Complex> b,
+                                      int n_min) {
+  detail::require_reduced(t, b, n_min, "laplace_merged", true);
+  const int d = static_cast<int>(t.size());
+  if (d == 2) {
+    Matrix<Complex> bm(b.dim(0), b.dim(1), std::vector<Complex>(b.data(), b.data() + b.size()));
+    Matrix<Complex> x = solve_sylvester_tri(t[0], conjugated(t[1]), std::move(bm),
+                                            std::min(n_min, matrix_floor_n_min));
+    return Tensor<Complex>(b.dims(), std::vector<Complex>(x.data(), x.data() + x.size()));
+  }
+  const Solvability s = check_solvable_laplace(t);
+  if (!s.solvable)
+    throw singular_error(detail::witness_message("laplace_merged", s), s.witness,
+                         s.witness_values, s.min_abs);
+  const std::vector<const double*> tp = detail::zptrs(t);
+  tsg_opts o = detail::gpu_opts(0);
+  Tensor<Complex> x(b.dims());
+  gpu::check(tsg_zlaplace_reduced(gpu::context(), d, b.dims().data(), tp.data(),
+                                  detail::dp(b.data()), detail::dp(x.data()), &o, nullptr),
+             "laplace_merged");
+  return x;
+}
+
+// laplace.hpp:324-344 with T = Complex (laplace_pipeline<Complex>).
+inline SolveReport<Complex> solve_laplace(const LaplaceProblem<Complex>& p,
+                                          const SolverConfig& cfg = {}) {
+  validate(p);
+  detail::check_config_complex(cfg, "solve_laplace");
+  const int d = p.order();
+  SolveReport<Complex> rep;
+  rep.n_min = cfg.n_min > 0 ? cfg.n_min : default_n_min(Family::laplace, d, cfg.strategy);
+  rep.strategy = cfg.strategy;
+
+  StopWatch sw;
+  std::vector<SchurFactorization<Complex>> f;
+  for (const auto& a : p.coeffs) f.push_back(schur(a));
+  rep.timings.reduction_s = sw.lap();
+
+  std::vector<Matrix<Complex>> t;
+  for (const auto& s : f) t.push_back(s.t);
+  const Solvability s = check_solvable_laplace(t, cfg.singularity_tol);
+  if (!s.solvable)
+    throw singular_error(detail::witness_message("solve_laplace", s), s.witness, s.witness_values,
+                         s.min_abs);
+
+  std::vector<const double*> tp, up;
+  for (const auto& x : f) {
+    tp.push_back(detail::dp(x.t.data()));
+    up.push_back(detail::dp(x.u.data()));
+  }
+  tsg_opts o = detail::gpu_opts(cfg.n_min);
+  tsg_report r{};
+  Tensor<Complex> x(p.rhs.dims());
+  gpu::check(tsg_zlaplace_solve(gpu::context(), d, p.rhs.dims().data(), tp.data(), up.data(),
+                                detail::dp(p.rhs.data()), detail::dp(x.data()), &o, &r),
              "solve_laplace");
   const double gpu_s = sw.lap();
   const double back_frac = r.t_total_ms > 0 ? (r.t_back_ms + r.t_d2h_ms) / r.t_total_ms : 0.0;

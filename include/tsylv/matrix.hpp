@@ -69,6 +69,19 @@ Matrix<T> transposed(const Matrix<T>& a) {
   return t;
 }
 
+// Elementwise conjugate and conjugate transpose (matrix.hpp:120-148; the
+// identity / plain transpose for T = double).
+template <typename T>
+Matrix<T> conjugated(const Matrix<T>& a) {
+  Matrix<T> c = a;
+  for (std::size_t i = 0; i < c.size(); ++i) c.data()[i] = conjugate(c.data()[i]);
+  return c;
+}
+template <typename T>
+Matrix<T> adjoint(const Matrix<T>& a) {
+  return conjugated(transposed(a));
+}
+
 template <typename T>
 bool is_upper_triangular(const Matrix<T>& a) {
   for (int j = 0; j < a.cols(); ++j)

@@ -28,6 +28,10 @@ extern "C" {
 void dgetrf_(const int* m, const int* n, double* a, const int* lda, int* ipiv, int* info);
 void dgetrs_(const char* trans, const int* n, const int* nrhs, const double* a, const int* lda,
              const int* ipiv, double* b, const int* ldb, int* info);
+void zgetrf_(const int* m, const int* n, std::complex<double>* a, const int* lda, int* ipiv,
+             int* info);
+void zgetrs_(const char* trans, const int* n, const int* nrhs, const std::complex<double>* a,
+             const int* lda, const int* ipiv, std::complex<double>* b, const int* ldb, int* info);
 }
 
 namespace tsylv::oracle {
@@ -45,7 +49,8 @@ inline std::size_t checked_problem_size(const std::vector<int>& dims, std::size_
   return n;
 }
 
-inline std::vector<int> square_dims(const std::vector<Matrix<double>>& coeffs, const char* who) {
+template <typename T>
+std::vector<int> square_dims(const std::vector<Matrix<T>>& coeffs, const char* who) {
   if (coeffs.empty()) throw dimension_error(std::string(who) + ": no coefficients");
   std::vector<int> dims;
   for (const auto& a : coeffs) {
@@ -55,23 +60,37 @@ inline std::vector<int> square_dims(const std::vector<Matrix<double>>& coeffs, c
   }
   return dims;
 }
+inline void getrf(int n, double* a, int* piv, int* info) { dgetrf_(&n, &n, a, &n, piv, info); }
+inline void getrf(int n, std::complex<double>* a, int* piv, int* info) {
+  zgetrf_(&n, &n, a, &n, piv, info);
+}
+inline void getrs(int n, const double* a, const int* piv, double* b, int* info) {
+  const int one = 1;
+  dgetrs_("N", &n, &one, a, &n, piv, b, &n, info);
+}
+inline void getrs(int n, const std::complex<double>* a, const int* piv, std::complex<double>* b,
+                  int* info) {
+  const int one = 1;
+  zgetrs_("N", &n, &one, a, &n, piv, b, &n, info);
+}
 }  // namespace detail
 
 // sum_m I (x) .. (x) A_m (x) .. (x) I: entry (r, c) of mode m's term is
 // A_m(i, j) where r and c agree in every digit except mode m's (i, j).
-inline Matrix<double> assemble_laplace_matrix(const std::vector<Matrix<double>>& coeffs,
-                                              std::size_t size_cap = default_size_cap) {
+template <typename T>
+Matrix<T> assemble_laplace_matrix(const std::vector<Matrix<T>>& coeffs,
+                                  std::size_t size_cap = default_size_cap) {
   const std::vector<int> dims = detail::square_dims(coeffs, "assemble_laplace_matrix");
   const std::size_t big = detail::checked_problem_size(dims, size_cap, "assemble_laplace_matrix");
-  Matrix<double> op(static_cast<int>(big), static_cast<int>(big));
+  Matrix<T> op(static_cast<int>(big), static_cast<int>(big));
   std::size_t lo = 1;  // stride of mode m
   for (std::size_t m = 0; m < coeffs.size(); ++m) {
     const std::size_t n = static_cast<std::size_t>(dims[m]), hi = big / (lo * n);
     for (std::size_t q = 0; q < hi; ++q)
       for (std::size_t j = 0; j < n; ++j)
         for (std::size_t i = 0; i < n; ++i) {
-          const double a = coeffs[m](static_cast<int>(i), static_cast<int>(j));
-          if (a == 0.0) continue;
+          const T a = coeffs[m](static_cast<int>(i), static_cast<int>(j));
+          if (a == T{}) continue;
           for (std::size_t p = 0; p < lo; ++p)
             op(static_cast<int>(p + lo * (i + n * q)), static_cast<int>(p + lo * (j + n * q))) += a;
         }
@@ -81,15 +100,15 @@ inline Matrix<double> assemble_laplace_matrix(const std::vector<Matrix<double>>&
 }
 
 // I (x) .. (x) A_0 + A_{d-1} (x) .. (x) A_1 (x) C.
-inline Matrix<double> assemble_gsylv_matrix(const std::vector<Matrix<double>>& coeffs,
-                                            const Matrix<double>& c,
-                                            std::size_t size_cap = default_size_cap) {
+template <typename T>
+Matrix<T> assemble_gsylv_matrix(const std::vector<Matrix<T>>& coeffs, const Matrix<T>& c,
+                                std::size_t size_cap = default_size_cap) {
   const std::vector<int> dims = detail::square_dims(coeffs, "assemble_gsylv_matrix");
   if (c.rows() != c.cols() || c.rows() != dims[0])
     throw dimension_error("assemble_gsylv_matrix: C must be square with the order of A_0");
   const std::size_t big = detail::checked_problem_size(dims, size_cap, "assemble_gsylv_matrix");
   const int n = static_cast<int>(big), d = static_cast<int>(dims.size()), n0 = dims[0];
-  Matrix<double> op(n, n);
+  Matrix<T> op(n, n);
   for (int q = 0; q < n / n0; ++q)
     for (int j = 0; j < n0; ++j)
       for (int i = 0; i < n0; ++i) op(q * n0 + i, q * n0 + j) += coeffs[0](i, j);
@@ -98,15 +117,16 @@ inline Matrix<double> assemble_gsylv_matrix(const std::vector<Matrix<double>>& c
     for (int m = 0, v = col; m < d; v /= dims[m], ++m) ci[m] = v % dims[m];
     for (int row = 0; row < n; ++row) {
       for (int m = 0, v = row; m < d; v /= dims[m], ++m) ri[m] = v % dims[m];
-      double v = c(ri[0], ci[0]);
-      for (int m = 1; m < d && v != 0.0; ++m) v *= coeffs[m](ri[m], ci[m]);
+      T v = c(ri[0], ci[0]);
+      for (int m = 1; m < d && v != T{}; ++m) v *= coeffs[m](ri[m], ci[m]);
       op(row, col) += v;
     }
   }
   return op;
 }
 
-inline std::vector<double> dense_solve(Matrix<double> a, std::vector<double> b) {
+template <typename T>
+std::vector<T> dense_solve(Matrix<T> a, std::vector<T> b) {
   if (a.rows() != a.cols()) throw dimension_error("dense_solve: matrix must be square");
   const int n = a.rows();
   if (static_cast<int>(b.size()) != n) throw dimension_error("dense_solve: rhs length mismatch");
@@ -114,36 +134,39 @@ inline std::vector<double> dense_solve(Matrix<double> a, std::vector<double> b) 
   const double tiny = unit_roundoff<double> * a.frobenius_norm();
   std::vector<int> piv(n);
   int info = 0;
-  dgetrf_(&n, &n, a.data(), &n, piv.data(), &info);
+  detail::getrf(n, a.data(), piv.data(), &info);
   if (info < 0) throw std::invalid_argument("dense_solve: dgetrf illegal argument");
   for (int k = 0; k < n; ++k)
     if (std::abs(a(k, k)) <= tiny)
       throw singular_error("dense_solve: numerically singular at column " + std::to_string(k),
                            {k}, {std::complex<double>(a(k, k))}, std::abs(a(k, k)));
-  const int one = 1;
-  dgetrs_("N", &n, &one, a.data(), &n, piv.data(), b.data(), &n, &info);
+  detail::getrs(n, a.data(), piv.data(), b.data(), &info);
   return b;
 }
 
-inline Tensor<double> solve(const LaplaceProblem<double>& p,
-                            std::size_t size_cap = default_size_cap) {
+template <typename T>
+Tensor<T> solve(const LaplaceProblem<T>& p, std::size_t size_cap = default_size_cap) {
   validate(p);
-  std::vector<double> x = dense_solve(assemble_laplace_matrix(p.coeffs, size_cap),
-                                      std::vector<double>(p.rhs.data(), p.rhs.data() + p.rhs.size()));
-  return Tensor<double>(p.rhs.dims(), std::move(x));
+  std::vector<T> x = dense_solve(assemble_laplace_matrix(p.coeffs, size_cap),
+                                 std::vector<T>(p.rhs.data(), p.rhs.data() + p.rhs.size()));
+  return Tensor<T>(p.rhs.dims(), std::move(x));
 }
 
-inline Tensor<double> solve(const GSylvProblem<double>& p, std::size_t size_cap = default_size_cap) {
+template <typename T>
+Tensor<T> solve(const GSylvProblem<T>& p, std::size_t size_cap = default_size_cap) {
   validate(p);
-  std::vector<double> x = dense_solve(assemble_gsylv_matrix(p.coeffs, p.c, size_cap),
-                                      std::vector<double>(p.rhs.data(), p.rhs.data() + p.rhs.size()));
-  return Tensor<double>(p.rhs.dims(), std::move(x));
+  std::vector<T> x = dense_solve(assemble_gsylv_matrix(p.coeffs, p.c, size_cap),
+                                 std::vector<T>(p.rhs.data(), p.rhs.data() + p.rhs.size()));
+  return Tensor<T>(p.rhs.dims(), std::move(x));
 }
 
-inline double residual(const LaplaceProblem<double>& p, const Tensor<double>& x) {
+// T = double and T = Complex: the device residual (tsg_residual / tsg_zresidual)
+template <typename T>
+double residual(const LaplaceProblem<T>& p, const Tensor<T>& x) {
   return tsylv::residual(p, x);
 }
-inline double residual(const GSylvProblem<double>& p, const Tensor<double>& x) {
+template <typename T>
+double residual(const GSylvProblem<T>& p, const Tensor<T>& x) {
   return tsylv::residual(p, x);
 }
 

@@ -23,6 +23,7 @@
 
 #include "tsylv/matrix.hpp"
 #include "tsylv/problems.hpp"
+#include "tsylv/scalar.hpp"
 #include "tsylv/tensor.hpp"
 
 namespace tsylv {
@@ -43,6 +44,22 @@ class RandomStream {
     sin_member_ = rad * std::sin(ang);
     cached_ = true;
     return rad * std::cos(ang);
+  }
+  // Standard normal scalar of type T; complex draws have unit total variance
+  // (random.hpp:50-57).  The reference builds T(normal() * .., normal() * ..)
+  // in one constructor call, whose argument evaluation order is unspecified;
+  // g++ (the toolchain of its CMake build and of oracle/_ref) evaluates the
+  // imaginary argument first, so the stream is consumed imaginary part first
+  // (pinned by tests/test_gpu_complex.py::test_zgenerators_bit_exact).
+  template <typename T>
+  T draw() {
+    if constexpr (is_complex_v<T>) {
+      const double im = normal() * std::numbers::sqrt2 / 2.0;
+      const double re = normal() * std::numbers::sqrt2 / 2.0;
+      return T(re, im);
+    } else {
+      return static_cast<T>(normal());
+    }
   }
 
  private:
@@ -160,6 +177,112 @@ inline GSylvProblem<double> random_reduced_gsylv(RandomStream& rng, const std::v
   p.c *= 0.3;
   for (std::size_t m = 1; m < dims.size(); ++m) p.coeffs.push_back(randn_triangular_ringdiag(rng, dims[m], 0.3, 0.95));
   p.rhs = randn_tensor(rng, dims);
+  return p;
+}
+
+// ---- typed generators (random.hpp:64-223 for any T; T = Complex is the
+// reference's complex correctness suite).  Same draw
+// order as the reference: column-major fills, triangular entries i <= j
+// column by column, then the diagonal.
+template <typename T>
+Matrix<T> randn_matrix(RandomStream& r, int rows, int cols) {
+  Matrix<T> m(rows, cols);
+  for (int j = 0; j < cols; ++j)
+    for (int i = 0; i < rows; ++i) m(i, j) = r.draw<T>();
+  return m;
+}
+template <typename T>
+Tensor<T> randn_tensor(RandomStream& r, const std::vector<int>& dims) {
+  Tensor<T> t(dims);
+  for (std::size_t i = 0; i < t.size(); ++i) t.data()[i] = r.draw<T>();
+  return t;
+}
+template <typename T>
+Matrix<T> randn_triangular(RandomStream& r, int n, double diag_shift = 0) {
+  Matrix<T> m(n, n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i <= j; ++i) m(i, j) = r.draw<T>();
+  for (int i = 0; i < n; ++i) m(i, i) += T(diag_shift);
+  return m;
+}
+template <typename T>
+Matrix<T> randn_triangular_posdiag(RandomStream& r, int n, double floor_re = 1.0) {
+  Matrix<T> m = randn_triangular<T>(r, n, 0);
+  for (int i = 0; i < n; ++i) {
+    const double re = std::abs(r.normal()) + floor_re;
+    if constexpr (is_complex_v<T>) {
+      const double im = 0.4 * r.normal();
+      m(i, i) = T(re, im);
+    } else {
+      m(i, i) = T(re);
+    }
+  }
+  return m;
+}
+template <typename T>
+Matrix<T> randn_triangular_ringdiag(RandomStream& r, int n, double lo, double hi) {
+  Matrix<T> m = randn_triangular<T>(r, n, 0);
+  for (int i = 0; i < n; ++i) {
+    const double rad = lo + (hi - lo) * r.uniform();
+    if constexpr (is_complex_v<T>) {
+      const double th = 2.0 * std::numbers::pi * r.uniform();
+      m(i, i) = T(rad * std::cos(th), rad * std::sin(th));
+    } else {
+      m(i, i) = T(r.uniform() < 0.5 ? -rad : rad);
+    }
+  }
+  return m;
+}
+template <typename T>
+LaplaceProblem<T> random_laplace_problem(RandomStream& r, const std::vector<int>& dims) {
+  LaplaceProblem<T> p;
+  for (int n : dims) {
+    Matrix<T> a = randn_matrix<T>(r, n, n);
+    const double shift = 1.0 + 2.0 * std::sqrt(static_cast<double>(n));
+    for (int i = 0; i < n; ++i) a(i, i) += T(shift);
+    p.coeffs.push_back(std::move(a));
+  }
+  p.rhs = randn_tensor<T>(r, dims);
+  return p;
+}
+template <typename T>
+GSylvProblem<T> random_gsylv_problem(RandomStream& r, const std::vector<int>& dims) {
+  GSylvProblem<T> p;
+  const int n0 = dims[0];
+  {
+    Matrix<T> a = randn_matrix<T>(r, n0, n0);
+    const double shift = 1.0 + 2.0 * std::sqrt(static_cast<double>(n0));
+    for (int i = 0; i < n0; ++i) a(i, i) += T(shift);
+    p.coeffs.push_back(std::move(a));
+  }
+  p.c = randn_matrix<T>(r, n0, n0);
+  p.c *= T(0.25 / std::sqrt(static_cast<double>(n0)));
+  for (std::size_t m = 1; m < dims.size(); ++m) {
+    const int n = dims[m];
+    Matrix<T> a = randn_matrix<T>(r, n, n);
+    a *= T(0.45 / std::sqrt(static_cast<double>(n)));
+    p.coeffs.push_back(std::move(a));
+  }
+  p.rhs = randn_tensor<T>(r, dims);
+  return p;
+}
+template <typename T>
+LaplaceProblem<T> random_reduced_laplace(RandomStream& r, const std::vector<int>& dims) {
+  LaplaceProblem<T> p;
+  for (int n : dims) p.coeffs.push_back(randn_triangular_posdiag<T>(r, n, 1.0));
+  p.rhs = randn_tensor<T>(r, dims);
+  return p;
+}
+template <typename T>
+GSylvProblem<T> random_reduced_gsylv(RandomStream& r, const std::vector<int>& dims) {
+  GSylvProblem<T> p;
+  const int n0 = dims[0];
+  p.coeffs.push_back(randn_triangular_posdiag<T>(r, n0, 1.0));
+  p.c = randn_triangular_ringdiag<T>(r, n0, 0.05, 0.3);
+  p.c *= T(0.3);
+  for (std::size_t m = 1; m < dims.size(); ++m)
+    p.coeffs.push_back(randn_triangular_ringdiag<T>(r, dims[m], 0.3, 0.95));
+  p.rhs = randn_tensor<T>(r, dims);
   return p;
 }
 

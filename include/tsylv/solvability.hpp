@@ -52,6 +52,31 @@ inline EigList quasi_tri_eigenvalues(const Matrix<double>& t) {
   return e;
 }
 
+// Complex (quasi-)triangular factors (complex Schur forms are triangular:
+// the eigenvalues are the diagonal; 2x2 blocks keep the reference's exact
+// block formula, kernels.hpp:309-330).
+inline EigList quasi_tri_eigenvalues(const Matrix<std::complex<double>>& t) {
+  if (!is_upper_quasi_triangular(t))
+    throw dimension_error("quasi_block_sizes: matrix is not upper quasi-triangular");
+  using C = std::complex<double>;
+  const int n = t.rows();
+  EigList e;
+  for (int j = 0; j < n;) {
+    if (j + 1 < n && t(j + 1, j) != C(0)) {
+      const C tr = t(j, j) + t(j + 1, j + 1);
+      const C det = t(j, j) * t(j + 1, j + 1) - t(j, j + 1) * t(j + 1, j);
+      const C r = std::sqrt(tr * tr / 4.0 - det);
+      e.push_back(tr / 2.0 + r);
+      e.push_back(tr / 2.0 - r);
+      j += 2;
+    } else {
+      e.push_back(t(j, j));
+      j += 1;
+    }
+  }
+  return e;
+}
+
 namespace detail {
 
 inline Solvability min_kron_sum(const std::vector<EigList>& eigs) {
@@ -165,6 +190,57 @@ inline Solvability min_pencil_product(const Matrix<double>& s_, const Matrix<dou
   return out;
 }
 
+// Complex pencil screen (solvability.hpp:65-116 with T = Complex): tuples
+// in odometer order, blocks innermost, first strict minimum kept.
+inline Solvability min_pencil_product(const Matrix<std::complex<double>>& a1,
+                                      const Matrix<std::complex<double>>& c,
+                                      const std::vector<EigList>& tails) {
+  using C = std::complex<double>;
+  const int n = a1.rows();
+  std::vector<int> starts, sizes;
+  for (int j = 0; j < n;) {
+    const int sz = (j + 1 < n && a1(j + 1, j) != C(0)) ? 2 : 1;
+    starts.push_back(j);
+    sizes.push_back(sz);
+    j += sz;
+  }
+  const int d = static_cast<int>(tails.size());
+  Solvability out;
+  out.min_abs = std::numeric_limits<double>::infinity();
+  std::vector<int> idx(d, 0);
+  for (;;) {
+    C z = 1;
+    for (int m = 0; m < d; ++m) z *= tails[m][idx[m]];
+    for (size_t b = 0; b < starts.size(); ++b) {
+      const int s0 = starts[b];
+      double mag;
+      if (sizes[b] == 1) {
+        mag = std::abs(a1(s0, s0) + z * c(s0, s0));
+      } else {
+        const C m00 = a1(s0, s0) + z * c(s0, s0), m01 = a1(s0, s0 + 1) + z * c(s0, s0 + 1);
+        const C m10 = a1(s0 + 1, s0), m11 = a1(s0 + 1, s0 + 1) + z * c(s0 + 1, s0 + 1);
+        const C tr = m00 + m11;
+        const C disc = std::sqrt(tr * tr / 4.0 - (m00 * m11 - m01 * m10));
+        mag = std::min(std::abs(tr / 2.0 + disc), std::abs(tr / 2.0 - disc));
+      }
+      if (mag < out.min_abs) {
+        out.min_abs = mag;
+        out.witness.assign(1, s0);
+        out.witness.insert(out.witness.end(), idx.begin(), idx.end());
+        out.witness_values.assign({a1(s0, s0), c(s0, s0)});
+        for (int m = 0; m < d; ++m) out.witness_values.push_back(tails[m][idx[m]]);
+      }
+    }
+    int m = 0;
+    while (m < d && ++idx[m] == static_cast<int>(tails[m].size())) {
+      idx[m] = 0;
+      ++m;
+    }
+    if (m == d) break;
+  }
+  return out;
+}
+
 inline std::string witness_message(const char* who, const Solvability& s) {
   std::string m = std::string(who) + ": operator numerically singular (|eigenvalue| = " +
                   std::to_string(s.min_abs) + " at slots (";
@@ -190,6 +266,41 @@ inline Solvability check_solvable_laplace(const std::vector<Matrix<double>>& t, 
 
 inline Solvability check_solvable_gsylv(const std::vector<Matrix<double>>& t,
                                         const Matrix<double>& c, double tol = 0) {
+  if (t.size() < 2) throw dimension_error("check_solvable_gsylv: need at least two modes");
+  if (c.rows() != t[0].rows() || c.cols() != t[0].cols())
+    throw dimension_error("check_solvable_gsylv: C must match A_0");
+  if (!is_upper_triangular(c)) throw dimension_error("check_solvable_gsylv: C must be upper triangular");
+  double scale = t[0].frobenius_norm() + c.frobenius_norm();
+  std::vector<EigList> tails;
+  for (size_t m = 1; m < t.size(); ++m) {
+    tails.push_back(quasi_tri_eigenvalues(t[m]));
+    scale += t[m].frobenius_norm();
+  }
+  (void)quasi_tri_eigenvalues(t[0]);  // validates A_0
+  if (tol <= 0) tol = unit_roundoff<double> * scale;
+  Solvability s = detail::min_pencil_product(t[0], c, tails);
+  s.solvable = s.min_abs > tol;
+  return s;
+}
+
+// T = Complex (host scan; the GPU screens take real quasi-triangular factors).
+inline Solvability check_solvable_laplace(const std::vector<Matrix<std::complex<double>>>& t,
+                                          double tol = 0) {
+  if (t.empty()) throw dimension_error("check_solvable_laplace: no coefficients");
+  std::vector<EigList> e;
+  double scale = 0;
+  for (const auto& m : t) {
+    e.push_back(quasi_tri_eigenvalues(m));
+    scale += m.frobenius_norm();
+  }
+  if (tol <= 0) tol = unit_roundoff<double> * scale;
+  Solvability s = detail::min_kron_sum(e);
+  s.solvable = s.min_abs > tol;
+  return s;
+}
+
+inline Solvability check_solvable_gsylv(const std::vector<Matrix<std::complex<double>>>& t,
+                                        const Matrix<std::complex<double>>& c, double tol = 0) {
   if (t.size() < 2) throw dimension_error("check_solvable_gsylv: need at least two modes");
   if (c.rows() != t[0].rows() || c.cols() != t[0].cols())
     throw dimension_error("check_solvable_gsylv: C must match A_0");

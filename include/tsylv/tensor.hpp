@@ -87,4 +87,22 @@ inline Tensor<double> mode_multiply(const Tensor<double>& x, const Matrix<double
   return y;
 }
 
+// T = Complex: the complex DMMA GEMM (tsg_zmode_multiply, csrc/zsolve.cu).
+inline Tensor<Complex> mode_multiply(const Tensor<Complex>& x, const Matrix<Complex>& a, int mode) {
+  if (mode < 0 || mode >= x.order()) throw dimension_error("mode_multiply: mode out of range");
+  if (a.cols() != x.dim(mode))
+    throw dimension_error("mode_multiply: A has " + std::to_string(a.cols()) +
+                          " columns, mode extent is " + std::to_string(x.dim(mode)));
+  if (a.rows() <= 0) throw dimension_error("mode_multiply: A must have positive row count");
+  std::vector<int> yd = x.dims();
+  yd[mode] = a.rows();
+  Tensor<Complex> y(yd);
+  gpu::check(tsg_zmode_multiply(gpu::context(), x.order(), x.dims().data(),
+                                reinterpret_cast<const double*>(x.data()), a.rows(),
+                                reinterpret_cast<const double*>(a.data()), mode,
+                                reinterpret_cast<double*>(y.data()), nullptr),
+             "mode_multiply");
+  return y;
+}
+
 }  // namespace tsylv

@@ -176,6 +176,34 @@ int tsg_residual(tsg_ctx* ctx, int family, int d, const int* dims,
                  const double* const* A, const double* C, const double* B,
                  const double* X, int inputs_on_device, double* out);
 
+/* ---- Complex scalars (T = std::complex<double>) -----
+ * Same entry points for complex problems: every matrix and tensor buffer is
+ * interleaved (re, im) FP64, the layout of std::complex<double> arrays.
+ * Factors come from the complex Schur / QZ decompositions (zgees / zgges):
+ * T, S, Tc upper triangular, U, Q, Z unitary; forward transforms use the
+ * adjoints (laplace.hpp:282, gsylv.hpp:278-280).  Replace the T = Complex
+ * instantiations of laplace.hpp:276-298, gsylv.hpp:272-298 (solve),
+ * laplace.hpp:185-195 / gsylv.hpp:149-159 (reduced), tensor.hpp:187-231
+ * (mode product) and oracle.hpp:233-268 (residual).  opts->free_mode picks
+ * the Laplace free mode of the eigen-decoupled solve (-1 = automatic). */
+int tsg_zlaplace_solve(tsg_ctx* ctx, int d, const int* dims, const double* const* T,
+                       const double* const* U, const double* B, double* X,
+                       const tsg_opts* opts, tsg_report* rep);
+int tsg_zlaplace_reduced(tsg_ctx* ctx, int d, const int* dims, const double* const* T,
+                         const double* Bt, double* Xt, const tsg_opts* opts, tsg_report* rep);
+int tsg_zgsylv_solve(tsg_ctx* ctx, int d, const int* dims, const double* S, const double* Tc,
+                     const double* Q, const double* Z, const double* const* Ttail,
+                     const double* const* Utail, const double* B, double* X,
+                     const tsg_opts* opts, tsg_report* rep);
+int tsg_zgsylv_reduced(tsg_ctx* ctx, int d, const int* dims, const double* S, const double* Tc,
+                       const double* const* Ttail, const double* Bt, double* Xt,
+                       const tsg_opts* opts, tsg_report* rep);
+int tsg_zmode_multiply(tsg_ctx* ctx, int d, const int* dims, const double* X, int r,
+                       const double* A, int mode, double* Y, const tsg_opts* opts);
+int tsg_zresidual(tsg_ctx* ctx, int family, int d, const int* dims, const double* const* A,
+                  const double* C, const double* B, const double* X, int inputs_on_device,
+                  double* out);
+
 /* ABI version (bumped on any signature change). */
 
 /* ---- Slab-sharded multi-GPU solve (Laplace-like, d = 3) ---------------------

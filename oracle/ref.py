@@ -62,6 +62,30 @@ def lib() -> ctypes.CDLL:
             "ref_random_reduced_gsylv": (None, [P, I, Ip, Dp, Dp, Dp]),
             "ref_random_gsylv_problem": (None, [P, I, Ip, Dp, Dp, Dp]),
             "ref_randn_quasi_triangular": (None, [P, I, D, D, Dp]),
+            # complex scalars (T = Complex), interleaved buffers
+            "ref_zsolve_laplace": (I, [I, Ip, Dpp, Dp, I, I, I, Dp, Dp, E, I]),
+            "ref_zsolve_gsylv": (I, [I, Ip, Dpp, Dp, Dp, I, I, I, Dp, Dp, E, I]),
+            "ref_zlaplace_recursive": (I, [I, Ip, Dpp, Dp, I, Dp, E, I]),
+            "ref_zlaplace_merged": (I, [I, Ip, Dpp, Dp, I, Dp, E, I]),
+            "ref_zgsylv_recursive": (I, [I, Ip, Dpp, Dp, Dp, I, Dp, E, I]),
+            "ref_zgsylv_merged": (I, [I, Ip, Dpp, Dp, Dp, I, Dp, E, I]),
+            "ref_zsolve_sylvester_tri": (I, [I, I, Dp, Dp, Dp, I, Dp, E, I]),
+            "ref_zsolve_gsylv_tri": (I, [I, I, Dp, Dp, Dp, Dp, I, Dp, E, I]),
+            "ref_zmode_multiply": (I, [I, Ip, Dp, I, Dp, I, Dp, E, I]),
+            "ref_zschur": (I, [I, Dp, Dp, Dp, E, I]),
+            "ref_zqz": (I, [I, Dp, Dp, Dp, Dp, Dp, Dp, E, I]),
+            "ref_zdense_solve_laplace": (I, [I, Ip, Dpp, Dp, Dp, E, I]),
+            "ref_zdense_solve_gsylv": (I, [I, Ip, Dpp, Dp, Dp, Dp, E, I]),
+            "ref_zresidual_laplace": (D, [I, Ip, Dpp, Dp, Dp]),
+            "ref_zresidual_gsylv": (D, [I, Ip, Dpp, Dp, Dp, Dp]),
+            "ref_zcheck_solvable_laplace": (I, [I, Ip, Dpp, D, Dp, Ip, Ip, E, I]),
+            "ref_zcheck_solvable_gsylv": (I, [I, Ip, Dpp, Dp, D, Dp, Ip, Ip, E, I]),
+            "ref_zrandn": (None, [P, Dp, ctypes.c_size_t]),
+            "ref_run_verify": (I, [ctypes.c_uint64, I, E, D, Dp, E, I]),
+            "ref_zrandom_reduced_laplace": (None, [P, I, Ip, Dp, Dp]),
+            "ref_zrandom_laplace_problem": (None, [P, I, Ip, Dp, Dp]),
+            "ref_zrandom_reduced_gsylv": (None, [P, I, Ip, Dp, Dp, Dp]),
+            "ref_zrandom_gsylv_problem": (None, [P, I, Ip, Dp, Dp, Dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -371,3 +395,230 @@ def check_solvable_gsylv(t, c, tol=0.0):
     _chk(lib().ref_check_solvable_gsylv(len(t), _dims([m.shape[0] for m in t]), pp, _p(_f(c)), tol,
                                         ctypes.byref(mn), wit, ctypes.byref(ok), err, 1024), err)
     return mn.value, list(wit), bool(ok.value)
+
+
+# ---- complex scalars (T = Complex) ------------------------------------------
+# The same reference entry points instantiated for std::complex<double>
+# (oracle/ref_driver.cpp ref_z*); numpy complex128 arrays in Fortran order are
+# the interleaved layout of std::complex<double>.
+
+def _z(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.complex128))
+
+
+def _zout(shape):
+    return np.zeros(shape, dtype=np.complex128, order="F")
+
+
+def zsolve_laplace(coeffs, rhs, strategy=1, arithmetic=0, n_min=0):
+    """solve_laplace<Complex> (laplace.hpp:324-344): (X, info[6])."""
+    coeffs = [_z(a) for a in coeffs]
+    rhs = _z(rhs)
+    x = _zout(rhs.shape)
+    info = (ctypes.c_double * 6)()
+    pp, keep = _pp(coeffs)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zsolve_laplace(rhs.ndim, _dims(rhs.shape), pp, _p(rhs), strategy, arithmetic,
+                                  n_min, _p(x), info, err, 1024), err)
+    return x, list(info)
+
+
+def zsolve_gsylv(coeffs, c, rhs, strategy=1, arithmetic=0, n_min=0):
+    """solve_gsylv<Complex> (gsylv.hpp:311-331): (X, info[6])."""
+    coeffs = [_z(a) for a in coeffs]
+    c, rhs = _z(c), _z(rhs)
+    x = _zout(rhs.shape)
+    info = (ctypes.c_double * 6)()
+    pp, keep = _pp(coeffs)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zsolve_gsylv(rhs.ndim, _dims(rhs.shape), pp, _p(c), _p(rhs), strategy,
+                                arithmetic, n_min, _p(x), info, err, 1024), err)
+    return x, list(info)
+
+
+def _zred(fn, t, bt, n_min, tc=None):
+    t = [_z(a) for a in t]
+    bt = _z(bt)
+    x = _zout(bt.shape)
+    pp, keep = _pp(t)
+    err = ctypes.create_string_buffer(1024)
+    if tc is None:
+        rc = fn(bt.ndim, _dims(bt.shape), pp, _p(bt), n_min, _p(x), err, 1024)
+    else:
+        tc = _z(tc)
+        rc = fn(bt.ndim, _dims(bt.shape), pp, _p(tc), _p(bt), n_min, _p(x), err, 1024)
+    _chk(rc, err)
+    return x
+
+
+def zlaplace_recursive(t, bt, n_min):
+    return _zred(lib().ref_zlaplace_recursive, t, bt, n_min)
+
+
+def zlaplace_merged(t, bt, n_min):
+    return _zred(lib().ref_zlaplace_merged, t, bt, n_min)
+
+
+def zgsylv_recursive(t, tc, bt, n_min):
+    return _zred(lib().ref_zgsylv_recursive, t, bt, n_min, tc)
+
+
+def zgsylv_merged(t, tc, bt, n_min):
+    return _zred(lib().ref_zgsylv_merged, t, bt, n_min, tc)
+
+
+def zsolve_sylvester_tri(a1, a2, b, n_min=32):
+    a1, a2, b = _z(a1), _z(a2), _z(b)
+    x = _zout(b.shape)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zsolve_sylvester_tri(a1.shape[0], a2.shape[0], _p(a1), _p(a2), _p(b), n_min,
+                                        _p(x), err, 1024), err)
+    return x
+
+
+def zsolve_gsylv_tri(a1, c, a2, b, n_min=32):
+    a1, c, a2, b = _z(a1), _z(c), _z(a2), _z(b)
+    x = _zout(b.shape)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zsolve_gsylv_tri(a1.shape[0], a2.shape[0], _p(a1), _p(c), _p(a2), _p(b),
+                                    n_min, _p(x), err, 1024), err)
+    return x
+
+
+def zmode_multiply(x, a, mode):
+    x, a = _z(x), _z(a)
+    shape = list(x.shape)
+    shape[mode] = a.shape[0]
+    y = _zout(shape)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zmode_multiply(x.ndim, _dims(x.shape), _p(x), a.shape[0], _p(a), mode, _p(y),
+                                  err, 1024), err)
+    return y
+
+
+def zschur(a):
+    a = _z(a)
+    n = a.shape[0]
+    u, t = _zout((n, n)), _zout((n, n))
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zschur(n, _p(a), _p(u), _p(t), err, 1024), err)
+    return u, t
+
+
+def zqz(a, c):
+    a, c = _z(a), _z(c)
+    n = a.shape[0]
+    q, z, s, t = (_zout((n, n)) for _ in range(4))
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zqz(n, _p(a), _p(c), _p(q), _p(z), _p(s), _p(t), err, 1024), err)
+    return q, z, s, t
+
+
+def zdense_solve_laplace(coeffs, rhs):
+    coeffs = [_z(a) for a in coeffs]
+    rhs = _z(rhs)
+    x = _zout(rhs.shape)
+    pp, keep = _pp(coeffs)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zdense_solve_laplace(rhs.ndim, _dims(rhs.shape), pp, _p(rhs), _p(x), err,
+                                        1024), err)
+    return x
+
+
+def zdense_solve_gsylv(coeffs, c, rhs):
+    coeffs = [_z(a) for a in coeffs]
+    c, rhs = _z(c), _z(rhs)
+    x = _zout(rhs.shape)
+    pp, keep = _pp(coeffs)
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zdense_solve_gsylv(rhs.ndim, _dims(rhs.shape), pp, _p(c), _p(rhs), _p(x), err,
+                                      1024), err)
+    return x
+
+
+def zresidual_laplace(coeffs, rhs, x):
+    coeffs = [_z(a) for a in coeffs]
+    rhs = _z(rhs)
+    pp, keep = _pp(coeffs)
+    return lib().ref_zresidual_laplace(rhs.ndim, _dims(rhs.shape), pp, _p(rhs), _p(_z(x)))
+
+
+def zresidual_gsylv(coeffs, c, rhs, x):
+    coeffs = [_z(a) for a in coeffs]
+    rhs = _z(rhs)
+    pp, keep = _pp(coeffs)
+    return lib().ref_zresidual_gsylv(rhs.ndim, _dims(rhs.shape), pp, _p(_z(c)), _p(rhs),
+                                     _p(_z(x)))
+
+
+def zcheck_solvable_laplace(t, tol=0.0):
+    t = [_z(m) for m in t]
+    pp, keep = _pp(t)
+    mn, ok = ctypes.c_double(), ctypes.c_int()
+    wit = (ctypes.c_int * len(t))()
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zcheck_solvable_laplace(len(t), _dims([m.shape[0] for m in t]), pp, tol,
+                                           ctypes.byref(mn), wit, ctypes.byref(ok), err, 1024), err)
+    return mn.value, list(wit), bool(ok.value)
+
+
+def zcheck_solvable_gsylv(t, c, tol=0.0):
+    t = [_z(m) for m in t]
+    pp, keep = _pp(t)
+    mn, ok = ctypes.c_double(), ctypes.c_int()
+    wit = (ctypes.c_int * len(t))()
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_zcheck_solvable_gsylv(len(t), _dims([m.shape[0] for m in t]), pp, _p(_z(c)),
+                                         tol, ctypes.byref(mn), wit, ctypes.byref(ok), err, 1024),
+         err)
+    return mn.value, list(wit), bool(ok.value)
+
+
+class ZRandomStream(RandomStream):
+    """The reference RandomStream drawing T = Complex instances
+    (random.hpp:64-223 with is_complex_v<T>)."""
+
+    def _zunpack(self, dims, flat):
+        mats, o = [], 0
+        for n in dims:
+            mats.append(flat[o:o + n * n].reshape((n, n), order="F").copy(order="F"))
+            o += n * n
+        return mats
+
+    def zrandn(self, n):
+        out = np.zeros(n, dtype=np.complex128)
+        lib().ref_zrandn(self.h, _p(out), n)
+        return out
+
+    def _draw(self, fn, dims, with_c):
+        co = np.zeros(sum(n * n for n in dims), dtype=np.complex128)
+        c = np.zeros(dims[0] ** 2, dtype=np.complex128)
+        rhs = np.zeros(int(np.prod(dims)), dtype=np.complex128)
+        if with_c:
+            fn(self.h, len(dims), _dims(dims), _p(co), _p(c), _p(rhs))
+            return (self._zunpack(dims, co), c.reshape((dims[0],) * 2, order="F"),
+                    rhs.reshape(dims, order="F"))
+        fn(self.h, len(dims), _dims(dims), _p(co), _p(rhs))
+        return self._zunpack(dims, co), rhs.reshape(dims, order="F")
+
+    def reduced_laplace(self, dims):
+        return self._draw(lib().ref_zrandom_reduced_laplace, dims, False)
+
+    def laplace_problem(self, dims):
+        return self._draw(lib().ref_zrandom_laplace_problem, dims, False)
+
+    def reduced_gsylv(self, dims):
+        return self._draw(lib().ref_zrandom_reduced_gsylv, dims, True)
+
+    def gsylv_problem(self, dims):
+        return self._draw(lib().ref_zrandom_gsylv_problem, dims, True)
+
+
+def run_verify(seed, per_family=50, out_dir="", tol=1e-9):
+    """The reference's run_verify (bench.hpp:255-352), writing its
+    verify_<family>_<k>.json files to out_dir when given."""
+    out = (ctypes.c_double * 4)()
+    err = ctypes.create_string_buffer(1024)
+    _chk(lib().ref_run_verify(seed, per_family, out_dir.encode(), tol, out, err, 1024), err)
+    return {"pass": bool(out[0]), "instances": int(out[1]), "worst_rel": out[2],
+            "worst_residual": out[3]}

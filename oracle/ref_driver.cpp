@@ -25,6 +25,7 @@
 //   0 ok, 1 dimension_error, 2 singular_error, 3 factorization_error,
 //   4 std::invalid_argument (config conflict), 5 anything else.
 #include <cmath>
+#include <complex>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -35,6 +36,9 @@
 #include "tsylv/laplace.hpp"
 #include "tsylv/oracle.hpp"
 #include "tsylv/random.hpp"
+#ifdef REF_HAVE_JSON
+#include "tsylv/bench.hpp"  // run_verify (bench.hpp:255-352); needs nlohmann/json
+#endif
 
 using namespace tsylv;
 
@@ -106,6 +110,42 @@ void fill_info(const SolveReport<double>& rep, double* info) {
   info[3] = rep.timings.recursion_s;
   info[4] = rep.timings.back_transform_s;
   info[5] = rep.n_min;
+}
+
+// ---- complex (T = Complex) helpers: buffers are interleaved (re, im)
+// doubles, the layout of std::complex<double> arrays.
+using C = std::complex<double>;
+const C* cp(const double* p) { return reinterpret_cast<const C*>(p); }
+Matrix<C> zmat(int r, int c, const double* p) {
+  return Matrix<C>(r, c, std::vector<C>(cp(p), cp(p) + static_cast<std::size_t>(r) * c));
+}
+Tensor<C> zten(int d, const int* dims, const double* p) {
+  return Tensor<C>(dims_of(d, dims), std::vector<C>(cp(p), cp(p) + numel(d, dims)));
+}
+void zcopy_out(const Tensor<C>& t, double* out) {
+  std::memcpy(out, t.data(), t.size() * sizeof(C));
+}
+void zfill_info(const SolveReport<C>& rep, double* info) {
+  if (!info) return;
+  info[0] = rep.residual;
+  info[1] = rep.discarded_imag;
+  info[2] = rep.timings.reduction_s;
+  info[3] = rep.timings.recursion_s;
+  info[4] = rep.timings.back_transform_s;
+  info[5] = rep.n_min;
+}
+std::vector<Matrix<C>> zcoeffs(int d, const int* dims, const double* const* t) {
+  std::vector<Matrix<C>> v;
+  for (int m = 0; m < d; ++m) v.push_back(zmat(dims[m], dims[m], t[m]));
+  return v;
+}
+template <typename P>
+void zpack(const P& p, double* coeffs, double* rhs) {
+  for (const auto& a : p.coeffs) {
+    std::memcpy(coeffs, a.data(), a.size() * sizeof(C));
+    coeffs += 2 * a.size();
+  }
+  zcopy_out(p.rhs, rhs);
 }
 
 } // namespace
@@ -424,5 +464,214 @@ int ref_baseline_problem(int kind, int d, const int* dims, std::uint64_t seed,
   copy_out(t, rhs);
   return 0;
 }
+
+// ---- complex scalars (T = Complex): the same entry points on
+// LaplaceProblem<Complex> / GSylvProblem<Complex> (laplace.hpp:324-344,
+// gsylv.hpp:311-331 with is_complex_v<T>), interleaved buffers.
+int ref_zsolve_laplace(int d, const int* dims, const double* const* coeffs, const double* rhs,
+                       int strategy, int arithmetic, int n_min, double* x, double* info,
+                       char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    LaplaceProblem<C> p;
+    p.coeffs = zcoeffs(d, dims, coeffs);
+    p.rhs = zten(d, dims, rhs);
+    SolveReport<C> rep = solve_laplace(p, make_cfg(strategy, arithmetic, n_min));
+    zcopy_out(rep.solution, x);
+    zfill_info(rep, info);
+  });
+}
+
+int ref_zsolve_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
+                     const double* rhs, int strategy, int arithmetic, int n_min, double* x,
+                     double* info, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GSylvProblem<C> p;
+    p.coeffs = zcoeffs(d, dims, coeffs);
+    p.c = zmat(dims[0], dims[0], c);
+    p.rhs = zten(d, dims, rhs);
+    SolveReport<C> rep = solve_gsylv(p, make_cfg(strategy, arithmetic, n_min));
+    zcopy_out(rep.solution, x);
+    zfill_info(rep, info);
+  });
+}
+
+int ref_zlaplace_recursive(int d, const int* dims, const double* const* t, const double* bt,
+                           int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zcopy_out(laplace_recursive(zcoeffs(d, dims, t), zten(d, dims, bt), n_min), x);
+  });
+}
+
+int ref_zlaplace_merged(int d, const int* dims, const double* const* t, const double* bt,
+                        int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zcopy_out(laplace_merged(zcoeffs(d, dims, t), zten(d, dims, bt), n_min), x);
+  });
+}
+
+int ref_zgsylv_recursive(int d, const int* dims, const double* const* t, const double* tc,
+                         const double* bt, int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zcopy_out(gsylv_recursive(zcoeffs(d, dims, t), zmat(dims[0], dims[0], tc), zten(d, dims, bt),
+                              n_min),
+              x);
+  });
+}
+
+int ref_zgsylv_merged(int d, const int* dims, const double* const* t, const double* tc,
+                      const double* bt, int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zcopy_out(gsylv_merged(zcoeffs(d, dims, t), zmat(dims[0], dims[0], tc), zten(d, dims, bt),
+                           n_min),
+              x);
+  });
+}
+
+int ref_zsolve_sylvester_tri(int r, int c, const double* a1, const double* a2, const double* b,
+                             int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Matrix<C> out = solve_sylvester_tri(zmat(r, r, a1), zmat(c, c, a2), zmat(r, c, b), n_min);
+    std::memcpy(x, out.data(), out.size() * sizeof(C));
+  });
+}
+
+int ref_zsolve_gsylv_tri(int r, int c, const double* a1, const double* cm, const double* a2,
+                         const double* b, int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Matrix<C> out = solve_gsylv_tri(zmat(r, r, a1), zmat(r, r, cm), zmat(c, c, a2),
+                                    zmat(r, c, b), n_min);
+    std::memcpy(x, out.data(), out.size() * sizeof(C));
+  });
+}
+
+int ref_zmode_multiply(int d, const int* dims, const double* xin, int r, const double* a,
+                       int mode, double* y, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zcopy_out(mode_multiply(zten(d, dims, xin), zmat(r, dims[mode], a), mode), y);
+  });
+}
+
+int ref_zschur(int n, const double* a, double* u, double* t, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    SchurFactorization<C> f = schur(zmat(n, n, a));
+    std::memcpy(u, f.u.data(), f.u.size() * sizeof(C));
+    std::memcpy(t, f.t.data(), f.t.size() * sizeof(C));
+  });
+}
+
+int ref_zqz(int n, const double* a, const double* c, double* q, double* z, double* s, double* t,
+            char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GeneralizedSchurFactorization<C> f = qz(zmat(n, n, a), zmat(n, n, c));
+    std::memcpy(q, f.u.data(), f.u.size() * sizeof(C));
+    std::memcpy(z, f.z.data(), f.z.size() * sizeof(C));
+    std::memcpy(s, f.s.data(), f.s.size() * sizeof(C));
+    std::memcpy(t, f.t.data(), f.t.size() * sizeof(C));
+  });
+}
+
+int ref_zdense_solve_laplace(int d, const int* dims, const double* const* coeffs,
+                             const double* rhs, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    LaplaceProblem<C> p;
+    p.coeffs = zcoeffs(d, dims, coeffs);
+    p.rhs = zten(d, dims, rhs);
+    zcopy_out(oracle::solve(p), x);
+  });
+}
+
+int ref_zdense_solve_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
+                           const double* rhs, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GSylvProblem<C> p;
+    p.coeffs = zcoeffs(d, dims, coeffs);
+    p.c = zmat(dims[0], dims[0], c);
+    p.rhs = zten(d, dims, rhs);
+    zcopy_out(oracle::solve(p), x);
+  });
+}
+
+double ref_zresidual_laplace(int d, const int* dims, const double* const* coeffs,
+                             const double* rhs, const double* x) {
+  LaplaceProblem<C> p;
+  p.coeffs = zcoeffs(d, dims, coeffs);
+  p.rhs = zten(d, dims, rhs);
+  return oracle::residual(p, zten(d, dims, x));
+}
+
+double ref_zresidual_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
+                           const double* rhs, const double* x) {
+  GSylvProblem<C> p;
+  p.coeffs = zcoeffs(d, dims, coeffs);
+  p.c = zmat(dims[0], dims[0], c);
+  p.rhs = zten(d, dims, rhs);
+  return oracle::residual(p, zten(d, dims, x));
+}
+
+int ref_zcheck_solvable_laplace(int d, const int* dims, const double* const* t, double tol,
+                                double* min_abs, int* witness, int* solvable, char* err,
+                                int errlen) {
+  return guarded(err, errlen, [&] {
+    Solvability s = check_solvable_laplace(zcoeffs(d, dims, t), tol);
+    *min_abs = s.min_abs;
+    *solvable = s.solvable ? 1 : 0;
+    for (std::size_t i = 0; i < s.witness.size(); ++i) witness[i] = s.witness[i];
+  });
+}
+
+int ref_zcheck_solvable_gsylv(int d, const int* dims, const double* const* t, const double* c,
+                              double tol, double* min_abs, int* witness, int* solvable, char* err,
+                              int errlen) {
+  return guarded(err, errlen, [&] {
+    Solvability s = check_solvable_gsylv(zcoeffs(d, dims, t), zmat(dims[0], dims[0], c), tol);
+    *min_abs = s.min_abs;
+    *solvable = s.solvable ? 1 : 0;
+    for (std::size_t i = 0; i < s.witness.size(); ++i) witness[i] = s.witness[i];
+  });
+}
+
+// Complex generators (random.hpp:64-223 with T = Complex); layouts as the
+// real ones, interleaved.
+void ref_zrandn(void* r, double* out, std::size_t n) {
+  auto* s = static_cast<RandomStream*>(r);
+  for (std::size_t i = 0; i < n; ++i) {
+    const C v = s->draw<C>();
+    out[2 * i] = v.real();
+    out[2 * i + 1] = v.imag();
+  }
+}
+void ref_zrandom_reduced_laplace(void* r, int d, const int* dims, double* coeffs, double* rhs) {
+  zpack(random_reduced_laplace<C>(*static_cast<RandomStream*>(r), dims_of(d, dims)), coeffs, rhs);
+}
+void ref_zrandom_laplace_problem(void* r, int d, const int* dims, double* coeffs, double* rhs) {
+  zpack(random_laplace_problem<C>(*static_cast<RandomStream*>(r), dims_of(d, dims)), coeffs, rhs);
+}
+void ref_zrandom_reduced_gsylv(void* r, int d, const int* dims, double* coeffs, double* c,
+                               double* rhs) {
+  auto p = random_reduced_gsylv<C>(*static_cast<RandomStream*>(r), dims_of(d, dims));
+  std::memcpy(c, p.c.data(), p.c.size() * sizeof(C));
+  zpack(p, coeffs, rhs);
+}
+void ref_zrandom_gsylv_problem(void* r, int d, const int* dims, double* coeffs, double* c,
+                               double* rhs) {
+  auto p = random_gsylv_problem<C>(*static_cast<RandomStream*>(r), dims_of(d, dims));
+  std::memcpy(c, p.c.data(), p.c.size() * sizeof(C));
+  zpack(p, coeffs, rhs);
+}
+
+#ifdef REF_HAVE_JSON
+// run_verify (bench.hpp:255-352): the seeded complex reduced-form suite;
+// out: pass, instances, worst_rel, worst_residual.
+int ref_run_verify(std::uint64_t seed, int per_family, const char* out_dir, double tol,
+                   double* out, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    VerifyReport v = run_verify(seed, per_family, out_dir ? out_dir : "", tol);
+    out[0] = v.pass ? 1 : 0;
+    out[1] = v.instances;
+    out[2] = v.worst_rel;
+    out[3] = v.worst_residual;
+  });
+}
+#endif
 
 } // extern "C"

@@ -42,6 +42,8 @@ TSG_SYMBOLS = [
     "tsg_plan_transform", "tsg_plan_free_mode", "tsg_screen_laplace", "tsg_screen_gsylv",
     "tsg_mode_multiply",
     "tsg_residual", "tsg_abi_version",
+    "tsg_zlaplace_solve", "tsg_zlaplace_reduced", "tsg_zgsylv_solve", "tsg_zgsylv_reduced",
+    "tsg_zmode_multiply", "tsg_zresidual",
     "tsg_slab_bounds", "tsg_dplan_create", "tsg_dplan_destroy", "tsg_dplan_info",
     "tsg_dplan_buffers", "tsg_dplan_ipc_export", "tsg_dplan_ipc_import",
     "tsg_dplan_forward_local", "tsg_dplan_forward_split", "tsg_dplan_solve",
@@ -115,6 +117,23 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tsylv_rng_randn": (None, [P, c_dbl_p, ctypes.c_size_t]),
         "tsylv_make_problem": (I, [I, I, c_int_p, ctypes.c_uint64, c_dbl_p, c_dbl_p, c_dbl_p]),
     }
+    # T = Complex facade: the same signatures over interleaved buffers
+    for name in ["solve_laplace", "solve_gsylv", "laplace_recursive", "gsylv_recursive",
+                 "laplace_merged", "gsylv_merged", "solve_sylvester_tri", "solve_gsylv_tri",
+                 "oracle_solve_laplace", "oracle_solve_gsylv", "mode_multiply", "schur", "qz",
+                 "residual_laplace", "residual_gsylv"]:
+        sig["tsylv_z" + name] = sig["tsylv_" + name]
+    sig["tsylv_zrandom_problem"] = (None, [P, I, I, c_int_p, c_dbl_p, c_dbl_p, c_dbl_p])
+    sig["tsg_zlaplace_solve"] = (I, [P, I, c_int_p, c_dbl_pp, c_dbl_pp, P, P,
+                                     ctypes.POINTER(TsgOpts), ctypes.POINTER(TsgReport)])
+    sig["tsg_zlaplace_reduced"] = (I, [P, I, c_int_p, c_dbl_pp, P, P, ctypes.POINTER(TsgOpts),
+                                       ctypes.POINTER(TsgReport)])
+    sig["tsg_zgsylv_solve"] = (I, [P, I, c_int_p, P, P, P, P, c_dbl_pp, c_dbl_pp, P, P,
+                                   ctypes.POINTER(TsgOpts), ctypes.POINTER(TsgReport)])
+    sig["tsg_zgsylv_reduced"] = (I, [P, I, c_int_p, P, P, c_dbl_pp, P, P, ctypes.POINTER(TsgOpts),
+                                     ctypes.POINTER(TsgReport)])
+    sig["tsg_zmode_multiply"] = (I, [P, I, c_int_p, P, I, P, I, P, ctypes.POINTER(TsgOpts)])
+    sig["tsg_zresidual"] = (I, [P, I, I, c_int_p, c_dbl_pp, P, P, P, I, c_dbl_p])
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
         f.restype = res

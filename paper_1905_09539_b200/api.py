@@ -16,6 +16,11 @@ the reference layout, tensor.hpp:19-27); matrices are (n, n) float64 arrays.
     oracle.residual(p, X), oracle.solve(p)   oracle.hpp:205-268
     mode_multiply(X, A, mode)      tensor.hpp:187-231
     schur(A), qz(A, C)             kernels.hpp:78-156 (host LAPACK, shared setup)
+
+Complex problems (T = Complex): pass complex128 arrays
+to the same functions; they dispatch to the tsylv_z* facade (complex Schur /
+QZ on the host, complex DMMA transforms and the eigen-decoupled triangular
+solve on the GPU).
 """
 from __future__ import annotations
 
@@ -126,6 +131,35 @@ def _f(a) -> np.ndarray:
     return np.asfortranarray(np.asarray(a, dtype=np.float64))
 
 
+def _z(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.complex128))
+
+
+def _cplx(*arrays) -> bool:
+    """T = Complex when any input is complex: the
+    tsylv_z* entry points take interleaved std::complex<double> buffers,
+    which is the memory layout of numpy complex128."""
+    for a in arrays:
+        if isinstance(a, (list, tuple)):
+            if any(np.iscomplexobj(v) for v in a):
+                return True
+        elif np.iscomplexobj(a):
+            return True
+    return False
+
+
+def _conv(z: bool):
+    return _z if z else _f
+
+
+def _zeros(shape, z: bool) -> np.ndarray:
+    return np.zeros(shape, dtype=np.complex128 if z else np.float64, order="F")
+
+
+def _fn(name: str, z: bool):
+    return getattr(lib(), name.replace("tsylv_", "tsylv_z", 1) if z else name)
+
+
 def _dims(rhs: np.ndarray) -> ctypes.Array:
     return (ctypes.c_int * rhs.ndim)(*rhs.shape)
 
@@ -167,14 +201,16 @@ def _report(x, info, cfg) -> SolveReport:
 # ---- entry points ------------------------------------------------------------------
 def solve_laplace(p: LaplaceProblem, cfg: SolverConfig | None = None) -> SolveReport:
     cfg = cfg or SolverConfig()
-    coeffs = [_f(a) for a in p.coeffs]
-    rhs = _f(p.rhs)
+    z = _cplx(p.coeffs, p.rhs)
+    cv = _conv(z)
+    coeffs = [cv(a) for a in p.coeffs]
+    rhs = cv(p.rhs)
     _check_problem(coeffs, rhs, "LaplaceProblem")
-    x = np.zeros(rhs.shape, order="F")
+    x = _zeros(rhs.shape, z)
     info = (ctypes.c_double * 14)()
     pp, keep = _ptrs(coeffs)
     err = _err()
-    rc = lib().tsylv_solve_laplace(rhs.ndim, _dims(rhs), pp, _ptr(rhs), int(cfg.strategy),
+    rc = _fn("tsylv_solve_laplace", z)(rhs.ndim, _dims(rhs), pp, _ptr(rhs), int(cfg.strategy),
                                    int(cfg.arithmetic), int(cfg.n_min), _ptr(x), info, err, 1024)
     _raise(rc, err)
     return _report(x, list(info), cfg)
@@ -182,80 +218,90 @@ def solve_laplace(p: LaplaceProblem, cfg: SolverConfig | None = None) -> SolveRe
 
 def solve_gsylv(p: GSylvProblem, cfg: SolverConfig | None = None) -> SolveReport:
     cfg = cfg or SolverConfig()
-    coeffs = [_f(a) for a in p.coeffs]
-    c = _f(p.c)
-    rhs = _f(p.rhs)
+    z = _cplx(p.coeffs, p.c, p.rhs)
+    cv = _conv(z)
+    coeffs = [cv(a) for a in p.coeffs]
+    c = cv(p.c)
+    rhs = cv(p.rhs)
     _check_problem(coeffs, rhs, "GSylvProblem")
     if c.shape != coeffs[0].shape:
         raise dimension_error("GSylvProblem: C must be square with the order of A_0")
-    x = np.zeros(rhs.shape, order="F")
+    x = _zeros(rhs.shape, z)
     info = (ctypes.c_double * 14)()
     pp, keep = _ptrs(coeffs)
     err = _err()
-    rc = lib().tsylv_solve_gsylv(rhs.ndim, _dims(rhs), pp, _ptr(c), _ptr(rhs), int(cfg.strategy),
+    rc = _fn("tsylv_solve_gsylv", z)(rhs.ndim, _dims(rhs), pp, _ptr(c), _ptr(rhs), int(cfg.strategy),
                                  int(cfg.arithmetic), int(cfg.n_min), _ptr(x), info, err, 1024)
     _raise(rc, err)
     return _report(x, list(info), cfg)
 
 
 def laplace_recursive(coeffs: list, b: np.ndarray, n_min: int) -> np.ndarray:
-    coeffs = [_f(a) for a in coeffs]
-    b = _f(b)
+    z = _cplx(coeffs, b)
+    cv = _conv(z)
+    coeffs = [cv(a) for a in coeffs]
+    b = cv(b)
     if b.ndim != len(coeffs):
         raise dimension_error("laplace_recursive: rhs order does not match coefficient count")
-    x = np.zeros(b.shape, order="F")
+    x = _zeros(b.shape, z)
     pp, keep = _ptrs(coeffs)
     err = _err()
-    rc = lib().tsylv_laplace_recursive(b.ndim, _dims(b), pp, _ptr(b), int(n_min), _ptr(x), err, 1024)
+    rc = _fn("tsylv_laplace_recursive", z)(b.ndim, _dims(b), pp, _ptr(b), int(n_min), _ptr(x), err, 1024)
     _raise(rc, err)
     return x
 
 
 def gsylv_recursive(coeffs: list, c: np.ndarray, b: np.ndarray, n_min: int) -> np.ndarray:
-    coeffs = [_f(a) for a in coeffs]
-    c = _f(c)
-    b = _f(b)
+    z = _cplx(coeffs, c, b)
+    cv = _conv(z)
+    coeffs = [cv(a) for a in coeffs]
+    c = cv(c)
+    b = cv(b)
     if b.ndim != len(coeffs):
         raise dimension_error("gsylv_recursive: rhs order does not match coefficient count")
-    x = np.zeros(b.shape, order="F")
+    x = _zeros(b.shape, z)
     pp, keep = _ptrs(coeffs)
     err = _err()
-    rc = lib().tsylv_gsylv_recursive(b.ndim, _dims(b), pp, _ptr(c), _ptr(b), int(n_min), _ptr(x),
+    rc = _fn("tsylv_gsylv_recursive", z)(b.ndim, _dims(b), pp, _ptr(c), _ptr(b), int(n_min), _ptr(x),
                                      err, 1024)
     _raise(rc, err)
     return x
 
 
 def laplace_merged(coeffs: list, b: np.ndarray, n_min: int) -> np.ndarray:
-    coeffs = [_f(a) for a in coeffs]
-    b = _f(b)
+    z = _cplx(coeffs, b)
+    cv = _conv(z)
+    coeffs = [cv(a) for a in coeffs]
+    b = cv(b)
     if b.ndim != len(coeffs):
         raise dimension_error("laplace_merged: rhs order does not match coefficient count")
-    x = np.zeros(b.shape, order="F")
+    x = _zeros(b.shape, z)
     pp, keep = _ptrs(coeffs)
     err = _err()
-    rc = lib().tsylv_laplace_merged(b.ndim, _dims(b), pp, _ptr(b), int(n_min), _ptr(x), err, 1024)
+    rc = _fn("tsylv_laplace_merged", z)(b.ndim, _dims(b), pp, _ptr(b), int(n_min), _ptr(x), err, 1024)
     _raise(rc, err)
     return x
 
 
 def gsylv_merged(coeffs: list, c: np.ndarray, b: np.ndarray, n_min: int) -> np.ndarray:
-    coeffs = [_f(a) for a in coeffs]
-    c = _f(c)
-    b = _f(b)
+    z = _cplx(coeffs, c, b)
+    cv = _conv(z)
+    coeffs = [cv(a) for a in coeffs]
+    c = cv(c)
+    b = cv(b)
     if b.ndim != len(coeffs):
         raise dimension_error("gsylv_merged: rhs order does not match coefficient count")
-    x = np.zeros(b.shape, order="F")
+    x = _zeros(b.shape, z)
     pp, keep = _ptrs(coeffs)
     err = _err()
-    rc = lib().tsylv_gsylv_merged(b.ndim, _dims(b), pp, _ptr(c), _ptr(b), int(n_min), _ptr(x),
+    rc = _fn("tsylv_gsylv_merged", z)(b.ndim, _dims(b), pp, _ptr(c), _ptr(b), int(n_min), _ptr(x),
                                   err, 1024)
     _raise(rc, err)
     return x
 
 
-def _mat2(a, who):
-    a = _f(a)
+def _mat2(a, who, cv=_f):
+    a = cv(a)
     if a.ndim != 2:
         raise dimension_error(f"{who}: expected a matrix")
     return a
@@ -263,15 +309,16 @@ def _mat2(a, who):
 
 def solve_sylvester_tri(a1: np.ndarray, a2: np.ndarray, b: np.ndarray, n_min: int = 32) -> np.ndarray:
     """A1 X + X A2^H = B with (quasi-)triangular A1, A2 (sylvester.hpp:194-215)."""
-    a1, a2, b = (_mat2(v, "solve_sylvester_tri") for v in (a1, a2, b))
+    z = _cplx(a1, a2, b)
+    a1, a2, b = (_mat2(v, "solve_sylvester_tri", _conv(z)) for v in (a1, a2, b))
     if a1.shape[0] != a1.shape[1] or a2.shape[0] != a2.shape[1]:
         raise dimension_error("solve_sylvester_tri: coefficients must be square")
     if b.shape != (a1.shape[0], a2.shape[0]):
         raise dimension_error(f"solve_sylvester_tri: rhs is {b.shape[0]}x{b.shape[1]}, expected "
                               f"{a1.shape[0]}x{a2.shape[0]}")
-    x = np.zeros(b.shape, order="F")
+    x = _zeros(b.shape, z)
     err = _err()
-    rc = lib().tsylv_solve_sylvester_tri(a1.shape[0], a2.shape[0], _ptr(a1), _ptr(a2), _ptr(b),
+    rc = _fn("tsylv_solve_sylvester_tri", z)(a1.shape[0], a2.shape[0], _ptr(a1), _ptr(a2), _ptr(b),
                                          int(n_min), _ptr(x), err, 1024)
     _raise(rc, err)
     return x
@@ -280,7 +327,8 @@ def solve_sylvester_tri(a1: np.ndarray, a2: np.ndarray, b: np.ndarray, n_min: in
 def solve_gsylv_tri(a1: np.ndarray, c: np.ndarray, a2: np.ndarray, b: np.ndarray,
                     n_min: int = 32) -> np.ndarray:
     """A1 X + C X A2^H = B, (A1, C) in generalized Schur form (sylvester.hpp:219-241)."""
-    a1, c, a2, b = (_mat2(v, "solve_gsylv_tri") for v in (a1, c, a2, b))
+    z = _cplx(a1, c, a2, b)
+    a1, c, a2, b = (_mat2(v, "solve_gsylv_tri", _conv(z)) for v in (a1, c, a2, b))
     if a1.shape[0] != a1.shape[1] or a2.shape[0] != a2.shape[1]:
         raise dimension_error("solve_gsylv_tri: coefficients must be square")
     if c.shape != a1.shape:
@@ -288,9 +336,9 @@ def solve_gsylv_tri(a1: np.ndarray, c: np.ndarray, a2: np.ndarray, b: np.ndarray
     if b.shape != (a1.shape[0], a2.shape[0]):
         raise dimension_error(f"solve_gsylv_tri: rhs is {b.shape[0]}x{b.shape[1]}, expected "
                               f"{a1.shape[0]}x{a2.shape[0]}")
-    x = np.zeros(b.shape, order="F")
+    x = _zeros(b.shape, z)
     err = _err()
-    rc = lib().tsylv_solve_gsylv_tri(a1.shape[0], a2.shape[0], _ptr(a1), _ptr(c), _ptr(a2), _ptr(b),
+    rc = _fn("tsylv_solve_gsylv_tri", z)(a1.shape[0], a2.shape[0], _ptr(a1), _ptr(c), _ptr(a2), _ptr(b),
                                      int(n_min), _ptr(x), err, 1024)
     _raise(rc, err)
     return x
@@ -306,65 +354,74 @@ class oracle:
 
     @staticmethod
     def solve(p) -> np.ndarray:
-        coeffs = [_f(a) for a in p.coeffs]
-        rhs = _f(p.rhs)
+        z = _cplx(p.coeffs, p.rhs, getattr(p, "c", None))
+        cv = _conv(z)
+        coeffs = [cv(a) for a in p.coeffs]
+        rhs = cv(p.rhs)
         _check_problem(coeffs, rhs, "oracle::solve")
-        x = np.zeros(rhs.shape, order="F")
+        x = _zeros(rhs.shape, z)
         pp, keep = _ptrs(coeffs)
         err = _err()
         if isinstance(p, GSylvProblem):
-            rc = lib().tsylv_oracle_solve_gsylv(rhs.ndim, _dims(rhs), pp, _ptr(_f(p.c)), _ptr(rhs),
-                                                _ptr(x), err, 1024)
+            rc = _fn("tsylv_oracle_solve_gsylv", z)(rhs.ndim, _dims(rhs), pp, _ptr(cv(p.c)),
+                                                    _ptr(rhs), _ptr(x), err, 1024)
         else:
-            rc = lib().tsylv_oracle_solve_laplace(rhs.ndim, _dims(rhs), pp, _ptr(rhs), _ptr(x),
+            rc = _fn("tsylv_oracle_solve_laplace", z)(rhs.ndim, _dims(rhs), pp, _ptr(rhs), _ptr(x),
                                                   err, 1024)
         _raise(rc, err)
         return x
 
 
 def mode_multiply(x: np.ndarray, a: np.ndarray, mode: int) -> np.ndarray:
-    x = _f(x)
-    a = _f(a)
+    z = _cplx(x, a)
+    x = _conv(z)(x)
+    a = _conv(z)(a)
     if not 0 <= mode < x.ndim:
         raise dimension_error("mode_multiply: mode out of range")
     shape = list(x.shape)
     shape[mode] = a.shape[0]
-    y = np.zeros(shape, order="F")
+    y = _zeros(shape, z)
     err = _err()
-    rc = lib().tsylv_mode_multiply(x.ndim, _dims(x), _ptr(x), int(a.shape[0]), _ptr(a), int(mode),
+    rc = _fn("tsylv_mode_multiply", z)(x.ndim, _dims(x), _ptr(x), int(a.shape[0]), _ptr(a), int(mode),
                                    _ptr(y), err, 1024)
     _raise(rc, err)
     return y
 
 
 def schur(a: np.ndarray):
-    a = _f(a)
+    z = _cplx(a)
+    a = _conv(z)(a)
     n = a.shape[0]
-    u = np.zeros((n, n), order="F")
-    t = np.zeros((n, n), order="F")
+    u = _zeros((n, n), z)
+    t = _zeros((n, n), z)
     err = _err()
-    _raise(lib().tsylv_schur(n, _ptr(a), _ptr(u), _ptr(t), err, 1024), err)
+    _raise(_fn("tsylv_schur", z)(n, _ptr(a), _ptr(u), _ptr(t), err, 1024), err)
     return u, t
 
 
 def qz(a: np.ndarray, c: np.ndarray):
-    a = _f(a)
-    c = _f(c)
+    cz = _cplx(a, c)
+    a = _conv(cz)(a)
+    c = _conv(cz)(c)
     n = a.shape[0]
-    q, z, s, t = (np.zeros((n, n), order="F") for _ in range(4))
+    q, z, s, t = (_zeros((n, n), cz) for _ in range(4))
     err = _err()
-    _raise(lib().tsylv_qz(n, _ptr(a), _ptr(c), _ptr(q), _ptr(z), _ptr(s), _ptr(t), err, 1024), err)
+    _raise(_fn("tsylv_qz", cz)(n, _ptr(a), _ptr(c), _ptr(q), _ptr(z), _ptr(s), _ptr(t), err, 1024),
+           err)
     return q, z, s, t
 
 
 def residual(p, x: np.ndarray) -> float:
-    x = _f(x)
-    coeffs = [_f(a) for a in p.coeffs]
-    rhs = _f(p.rhs)
+    z = _cplx(p.coeffs, p.rhs, x, getattr(p, "c", None))
+    cv = _conv(z)
+    x = cv(x)
+    coeffs = [cv(a) for a in p.coeffs]
+    rhs = cv(p.rhs)
     pp, keep = _ptrs(coeffs)
     if isinstance(p, GSylvProblem):
-        return lib().tsylv_residual_gsylv(rhs.ndim, _dims(rhs), pp, _ptr(_f(p.c)), _ptr(rhs), _ptr(x))
-    return lib().tsylv_residual_laplace(rhs.ndim, _dims(rhs), pp, _ptr(rhs), _ptr(x))
+        return _fn("tsylv_residual_gsylv", z)(rhs.ndim, _dims(rhs), pp, _ptr(cv(p.c)), _ptr(rhs),
+                                             _ptr(x))
+    return _fn("tsylv_residual_laplace", z)(rhs.ndim, _dims(rhs), pp, _ptr(rhs), _ptr(x))
 
 
 class RandomStream:
@@ -388,6 +445,31 @@ class RandomStream:
         out = np.empty(n)
         lib().tsylv_rng_randn(self._h, _ptr(out), n)
         return out
+
+
+def random_problem(which: str, dims, seed: int = 1, scalar=np.complex128):
+    """The reference's correctness-suite instances drawn from its stream
+    (random.hpp:150-221) with T = Complex: which = "laplace" (dense,
+    random_laplace_problem), "reduced_laplace", "gsylv", "reduced_gsylv"."""
+    if scalar is not np.complex128:
+        raise ValueError("random_problem: only complex128 (the real configs use make_problem)")
+    code = {"laplace": 0, "reduced_laplace": 1, "gsylv": 2, "reduced_gsylv": 3}[which]
+    dims = [int(n) for n in dims]
+    d = len(dims)
+    co = np.zeros(sum(n * n for n in dims), dtype=np.complex128)
+    c = np.zeros(dims[0] ** 2, dtype=np.complex128)
+    rhs = np.zeros(int(np.prod(dims)), dtype=np.complex128)
+    rs = RandomStream(seed)
+    lib().tsylv_zrandom_problem(rs._h, code, d, (ctypes.c_int * d)(*dims), _ptr(co), _ptr(c),
+                                _ptr(rhs))
+    mats, o = [], 0
+    for n in dims:
+        mats.append(co[o:o + n * n].reshape((n, n), order="F").copy(order="F"))
+        o += n * n
+    rhs = rhs.reshape(dims, order="F")
+    if code >= 2:
+        return GSylvProblem(mats, c.reshape((dims[0], dims[0]), order="F").copy(order="F"), rhs)
+    return LaplaceProblem(mats, rhs)
 
 
 def make_problem(kind: int, dims, seed: int = 1):

@@ -3,6 +3,7 @@
 // C++ user of the reference API gets.  Signatures mirror oracle/ref_driver.cpp
 // one-for-one, so parity tests call both sides the same way.  Status codes
 // are those of tsylv_gpu.h.
+#include <complex>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -66,6 +67,33 @@ SolverConfig cfg_of(int strategy, int arithmetic, int n_min) {
 // info: residual, discarded_imag, reduction_s, recursion_s, back_transform_s,
 // n_min, gpu fwd/solve/back/h2d/d2h/total ms, flops_alg, flops_exec (14).
 void fill_info(const SolveReport<double>& r, double* info) {
+  if (!info) return;
+  const double v[14] = {r.residual, r.discarded_imag, r.timings.reduction_s, r.timings.recursion_s,
+                        r.timings.back_transform_s, static_cast<double>(r.n_min), r.gpu.fwd_ms,
+                        r.gpu.solve_ms, r.gpu.back_ms, r.gpu.h2d_ms, r.gpu.d2h_ms, r.gpu.total_ms,
+                        r.gpu.flops_alg, r.gpu.flops_exec};
+  std::memcpy(info, v, sizeof(v));
+}
+
+// complex (interleaved) buffers
+using Z = std::complex<double>;
+const Z* zc(const double* p) { return reinterpret_cast<const Z*>(p); }
+Matrix<Z> zmat(int r, int c, const double* p) {
+  return Matrix<Z>(r, c, std::vector<Z>(zc(p), zc(p) + static_cast<size_t>(r) * c));
+}
+Tensor<Z> zten(int d, const int* dims, const double* p) {
+  return Tensor<Z>(dv(d, dims), std::vector<Z>(zc(p), zc(p) + numel(d, dims)));
+}
+std::vector<Matrix<Z>> zmats(int d, const int* dims, const double* const* t) {
+  std::vector<Matrix<Z>> v;
+  for (int m = 0; m < d; ++m) v.push_back(zmat(dims[m], dims[m], t[m]));
+  return v;
+}
+template <typename M>
+void zout(const M& m, double* x) {
+  std::memcpy(x, m.data(), m.size() * sizeof(Z));
+}
+void zfill_info(const SolveReport<Z>& r, double* info) {
   if (!info) return;
   const double v[14] = {r.residual, r.discarded_imag, r.timings.reduction_s, r.timings.recursion_s,
                         r.timings.back_transform_s, static_cast<double>(r.n_min), r.gpu.fwd_ms,
@@ -195,7 +223,7 @@ int tsylv_mode_multiply(int d, const int* dims, const double* xin, int r, const 
 
 int tsylv_schur(int n, const double* a, double* u, double* t, char* err, int errlen) {
   return guarded(err, errlen, [&] {
-    SchurFactorization f = schur(mat(n, n, a));
+    SchurFactorization<double> f = schur(mat(n, n, a));
     std::memcpy(u, f.u.data(), f.u.size() * sizeof(double));
     std::memcpy(t, f.t.data(), f.t.size() * sizeof(double));
   });
@@ -204,7 +232,7 @@ int tsylv_schur(int n, const double* a, double* u, double* t, char* err, int err
 int tsylv_qz(int n, const double* a, const double* c, double* q, double* z, double* s, double* t,
              char* err, int errlen) {
   return guarded(err, errlen, [&] {
-    GeneralizedSchurFactorization f = qz(mat(n, n, a), mat(n, n, c));
+    GeneralizedSchurFactorization<double> f = qz(mat(n, n, a), mat(n, n, c));
     std::memcpy(q, f.u.data(), f.u.size() * sizeof(double));
     std::memcpy(z, f.z.data(), f.z.size() * sizeof(double));
     std::memcpy(s, f.s.data(), f.s.size() * sizeof(double));
@@ -279,6 +307,163 @@ int tsylv_make_problem(int kind, int d, const int* dims, std::uint64_t seed, dou
     return TSG_OK;
   }
   return TSG_EDIM;
+}
+
+// ---- T = Complex: interleaved complex buffers ------
+int tsylv_zsolve_laplace(int d, const int* dims, const double* const* coeffs, const double* rhs,
+                         int strategy, int arithmetic, int n_min, double* x, double* info,
+                         char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    LaplaceProblem<Z> p;
+    p.coeffs = zmats(d, dims, coeffs);
+    p.rhs = zten(d, dims, rhs);
+    SolveReport<Z> r = solve_laplace(p, cfg_of(strategy, arithmetic, n_min));
+    zout(r.solution, x);
+    zfill_info(r, info);
+  });
+}
+
+int tsylv_zsolve_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
+                       const double* rhs, int strategy, int arithmetic, int n_min, double* x,
+                       double* info, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GSylvProblem<Z> p;
+    p.coeffs = zmats(d, dims, coeffs);
+    p.c = zmat(dims[0], dims[0], c);
+    p.rhs = zten(d, dims, rhs);
+    SolveReport<Z> r = solve_gsylv(p, cfg_of(strategy, arithmetic, n_min));
+    zout(r.solution, x);
+    zfill_info(r, info);
+  });
+}
+
+int tsylv_zlaplace_recursive(int d, const int* dims, const double* const* t, const double* bt,
+                             int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen,
+                 [&] { zout(laplace_recursive(zmats(d, dims, t), zten(d, dims, bt), n_min), x); });
+}
+
+int tsylv_zlaplace_merged(int d, const int* dims, const double* const* t, const double* bt,
+                          int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen,
+                 [&] { zout(laplace_merged(zmats(d, dims, t), zten(d, dims, bt), n_min), x); });
+}
+
+int tsylv_zgsylv_recursive(int d, const int* dims, const double* const* t, const double* tc,
+                           const double* bt, int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zout(gsylv_recursive(zmats(d, dims, t), zmat(dims[0], dims[0], tc), zten(d, dims, bt), n_min),
+         x);
+  });
+}
+
+int tsylv_zgsylv_merged(int d, const int* dims, const double* const* t, const double* tc,
+                        const double* bt, int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zout(gsylv_merged(zmats(d, dims, t), zmat(dims[0], dims[0], tc), zten(d, dims, bt), n_min), x);
+  });
+}
+
+int tsylv_zsolve_sylvester_tri(int r, int c, const double* a1, const double* a2, const double* b,
+                               int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zout(solve_sylvester_tri(zmat(r, r, a1), zmat(c, c, a2), zmat(r, c, b), n_min), x);
+  });
+}
+
+int tsylv_zsolve_gsylv_tri(int r, int c, const double* a1, const double* cm, const double* a2,
+                           const double* b, int n_min, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zout(solve_gsylv_tri(zmat(r, r, a1), zmat(r, r, cm), zmat(c, c, a2), zmat(r, c, b), n_min), x);
+  });
+}
+
+int tsylv_zoracle_solve_laplace(int d, const int* dims, const double* const* coeffs,
+                                const double* rhs, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    LaplaceProblem<Z> p;
+    p.coeffs = zmats(d, dims, coeffs);
+    p.rhs = zten(d, dims, rhs);
+    zout(oracle::solve(p), x);
+  });
+}
+
+int tsylv_zoracle_solve_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
+                              const double* rhs, double* x, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GSylvProblem<Z> p;
+    p.coeffs = zmats(d, dims, coeffs);
+    p.c = zmat(dims[0], dims[0], c);
+    p.rhs = zten(d, dims, rhs);
+    zout(oracle::solve(p), x);
+  });
+}
+
+int tsylv_zmode_multiply(int d, const int* dims, const double* xin, int r, const double* a,
+                         int mode, double* y, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    zout(mode_multiply(zten(d, dims, xin), zmat(r, dims[mode], a), mode), y);
+  });
+}
+
+int tsylv_zschur(int n, const double* a, double* u, double* t, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    SchurFactorization<Z> f = schur(zmat(n, n, a));
+    zout(f.u, u);
+    zout(f.t, t);
+  });
+}
+
+int tsylv_zqz(int n, const double* a, const double* c, double* q, double* z, double* s, double* t,
+              char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    GeneralizedSchurFactorization<Z> f = qz(zmat(n, n, a), zmat(n, n, c));
+    zout(f.u, q);
+    zout(f.z, z);
+    zout(f.s, s);
+    zout(f.t, t);
+  });
+}
+
+double tsylv_zresidual_laplace(int d, const int* dims, const double* const* coeffs,
+                               const double* rhs, const double* x) {
+  LaplaceProblem<Z> p;
+  p.coeffs = zmats(d, dims, coeffs);
+  p.rhs = zten(d, dims, rhs);
+  return oracle::residual(p, zten(d, dims, x));
+}
+
+double tsylv_zresidual_gsylv(int d, const int* dims, const double* const* coeffs, const double* c,
+                             const double* rhs, const double* x) {
+  GSylvProblem<Z> p;
+  p.coeffs = zmats(d, dims, coeffs);
+  p.c = zmat(dims[0], dims[0], c);
+  p.rhs = zten(d, dims, rhs);
+  return oracle::residual(p, zten(d, dims, x));
+}
+
+// Complex correctness-suite generators (random.hpp:64-223, T = Complex):
+// which 0 random_laplace_problem, 1 random_reduced_laplace,
+// 2 random_gsylv_problem, 3 random_reduced_gsylv.  Coefficients packed back
+// to back, then C (gsylv), then rhs; interleaved.
+void tsylv_zrandom_problem(void* r, int which, int d, const int* dims, double* coeffs, double* c,
+                           double* rhs) {
+  auto& rng = *static_cast<RandomStream*>(r);
+  auto pack = [&](const auto& p) {
+    for (const auto& a : p.coeffs) {
+      zout(a, coeffs);
+      coeffs += 2 * a.size();
+    }
+    zout(p.rhs, rhs);
+  };
+  if (which == 0) pack(random_laplace_problem<Z>(rng, dv(d, dims)));
+  else if (which == 1) pack(random_reduced_laplace<Z>(rng, dv(d, dims)));
+  else {
+    GSylvProblem<Z> p = which == 2 ? random_gsylv_problem<Z>(rng, dv(d, dims))
+                                   : random_reduced_gsylv<Z>(rng, dv(d, dims));
+    zout(p.c, c);
+    pack(p);
+  }
 }
 
 }  // extern "C"

@@ -139,8 +139,8 @@ int main(int argc, char** argv) {
     CHECK(bad("{\"family\": \"laplace\", \"dims\": [2, 0], \"coeffs\": [[[1, 0], [0, 1]], [[1]]], \"rhs\": []}"));
     CHECK(bad("{\"family\": \"laplace\", \"dims\": [1, 1], \"coeffs\": [[[1]], [[\"x\"]]], \"rhs\": [1]}"));
     CHECK(bad("{\"family\": \"laplace\", \"dims\": [2, 1], \"coeffs\": [[[1, 0], [0]], [[1]]], \"rhs\": [1, 2]}"));
-    // complex scalars are refused, not misread
-    CHECK(bad("{\"family\": \"laplace\", \"complex\": true, \"dims\": [1, 1], \"coeffs\": [[[[1, 0]]], [[[1, "
+    // complex files need [re, im] pairs (a bare number is not a complex scalar)
+    CHECK(bad("{\"family\": \"laplace\", \"complex\": true, \"dims\": [1, 1], \"coeffs\": [[[1]], [[[1, "
               "0]]]], \"rhs\": [[1, 0]]}"));
     CHECK(throws_io([&] { load_problem((dir / "missing.json").string()); }));
   }

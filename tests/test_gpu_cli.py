@@ -121,19 +121,68 @@ def test_bench_scaling_with_baseline_and_oom(cli):
     assert ",oom,9" in so  # 64^2 doubles x3 does not
 
 
-def test_verify_writes_timing_free_files(cli, tmp_path):
+def _zarr(v):
+    a = np.asarray(v, dtype=float)
+    return a[..., 0] + 1j * a[..., 1]
+
+
+def test_verify_writes_timing_free_files(cli, ref, tmp_path):
+    """run_verify (bench.hpp:255-352): the reference's complex reduced-form
+    suite; the files must hold the reference's own instances (bit-identical
+    envelopes) and solutions within 1e-10 of the reference's run_verify."""
     out = tmp_path / "verify_out"
     rc, so, se = run(cli, "verify", "--seed", 12, "--count", 2, "--out", out)
     assert rc == 0, se + so
     assert "instances: 4" in so and "verify: PASS" in so
+    ref_out = tmp_path / "verify_ref"
+    ref_out.mkdir()
+    vr = ref.run_verify(12, 2, str(ref_out))
+    assert vr["pass"] and vr["instances"] == 4
     for name in ("verify_laplace_0.json", "verify_laplace_1.json", "verify_gsylv_0.json", "verify_gsylv_1.json"):
         assert (out / name).exists()
+        mine, theirs = json.loads((out / name).read_text()), json.loads((ref_out / name).read_text())
+        assert mine["complex"] is True
+        for key in ("family", "complex", "dims", "coeffs", "rhs") + (("c_coeff",) if "gsylv" in name else ()):
+            assert mine[key] == theirs[key], (name, key)
+        assert rel_diff(_zarr(mine["solution"]), _zarr(theirs["solution"])) <= 1e-10, name
+        assert mine["report"]["n_min"] == theirs["report"]["n_min"]
+        assert mine["report"]["strategy"] == theirs["report"]["strategy"] == "merge"
     text = (out / "verify_laplace_0.json").read_text()
     assert "timings" not in text
-    x, doc = read_solution(out / "verify_gsylv_1.json")
-    co = [np.array(a) for a in doc["coeffs"]]
-    rhs = np.array(doc["rhs"]).reshape(doc["dims"], order="F")
-    assert R.residual_gsylv(co, np.array(doc["c_coeff"]), rhs, x) <= 1e-12
+    doc = json.loads((out / "verify_gsylv_1.json").read_text())
+    co = [_zarr(a) for a in doc["coeffs"]]
+    rhs = _zarr(doc["rhs"]).reshape(doc["dims"], order="F")
+    x = _zarr(doc["solution"]).reshape(doc["dims"], order="F")
+    assert ref.zresidual_gsylv(co, _zarr(doc["c_coeff"]), rhs, x) <= 1e-12
     # an impossible tolerance fails the suite with exit code 4
     rc, so, se = run(cli, "verify", "--seed", 12, "--count", 1, "--tol", 1e-300)
     assert rc == 4 and "verify: FAIL" in so
+
+
+def test_solve_complex_problem_file(cli, ref, tmp_path):
+    """A complex problem file ("complex": true, [re, im] scalars) solves on
+    the GPU to the reference's solve_laplace<Complex> / solve_gsylv<Complex>."""
+    rs = ref.ZRandomStream(17)
+    for family in ("laplace", "gsylv"):
+        if family == "laplace":
+            co, b = rs.laplace_problem([6, 5, 4])
+            c = None
+            want, _ = ref.zsolve_laplace(co, b)
+        else:
+            co, c, b = rs.gsylv_problem([6, 5, 4])
+            want, _ = ref.zsolve_gsylv(co, c, b)
+        pair = lambda a: np.stack([a.real, a.imag], axis=-1).tolist()  # noqa: E731
+        doc = {"family": family, "complex": True, "dims": list(b.shape), "coeffs": [pair(a) for a in co],
+               "rhs": pair(b.reshape(-1, order="F"))}
+        if c is not None:
+            doc["c_coeff"] = pair(c)
+        inp = tmp_path / f"z{family}.json"
+        inp.write_text(json.dumps(doc))
+        out = tmp_path / f"z{family}_sol.json"
+        rc, so, se = run(cli, "solve", "--in", inp, "--out", out)
+        assert rc == 0, se + so
+        sol = json.loads(out.read_text())
+        assert sol["complex"] is True
+        x = _zarr(sol["solution"]).reshape(sol["dims"], order="F")
+        assert rel_diff(x, want) <= 1e-10
+        assert sol["report"]["residual"] <= 1e-12

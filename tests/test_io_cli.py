@@ -68,9 +68,9 @@ def test_bad_files_exit_1(cli, tmp_path):
     assert run(cli, "solve", "--in", str(tmp_path / "nope.json"))[0] == 1
     cplx = tmp_path / "complex.json"
     cplx.write_text(json.dumps({"family": "laplace", "complex": True, "dims": [1, 1],
-                                "coeffs": [[[[1, 0]]], [[[2, 0]]]], "rhs": [[1, 0]]}))
+                                "coeffs": [[[1]], [[[2, 0]]]], "rhs": [[1, 0]]}))
     rc, out = run(cli, "solve", "--in", str(cplx))
-    assert rc == 1 and "complex" in out
+    assert rc == 1 and "[re, im] pair" in out
     shape = tmp_path / "shape.json"
     shape.write_text(json.dumps({"family": "laplace", "dims": [2, 2], "coeffs": [[[1]], [[1]]], "rhs": [1, 2, 3, 4]}))
     assert run(cli, "solve", "--in", str(shape))[0] == 1

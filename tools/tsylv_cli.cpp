@@ -167,7 +167,8 @@ struct VerifyFlags {
   double tol = 1e-9;
 };
 
-void print_report(const char* family, const std::vector<int>& dims, const SolveReport<double>& rep) {
+template <typename T>
+void print_report(const char* family, const std::vector<int>& dims, const SolveReport<T>& rep) {
   std::string shape;
   for (std::size_t i = 0; i < dims.size(); ++i) shape += (i ? "x" : "") + std::to_string(dims[i]);
   std::printf("family: %s\ndims: %s\nstrategy: %s\nn_min: %d\n", family, shape.c_str(),
@@ -186,12 +187,15 @@ int run_solve(const SolveFlags& f) {
   const AnyProblem any = load_problem(f.in);
   std::visit(
       [&](const auto& p) {
-        constexpr bool lap = std::is_same_v<std::decay_t<decltype(p)>, LaplaceProblem<double>>;
-        SolveReport<double> rep;
-        if constexpr (lap)
-          rep = solve_laplace(p, cfg);
-        else
-          rep = solve_gsylv(p, cfg);
+        using P = std::decay_t<decltype(p)>;
+        constexpr bool lap =
+            std::is_same_v<P, LaplaceProblem<double>> || std::is_same_v<P, LaplaceProblem<Complex>>;
+        const auto rep = [&] {
+          if constexpr (lap)
+            return solve_laplace(p, cfg);
+          else
+            return solve_gsylv(p, cfg);
+        }();
         print_report(lap ? "laplace" : "gsylv", p.dims(), rep);
         if (!f.out.empty()) save_solution(f.out, p, rep);
       },
