@@ -432,7 +432,7 @@ def run_ours(a, rank, world, local):
         dom = {"kernel": "solve kernel (reduced dataflow solve, K2+K3)", "ncu": "solve",
                "achieved": solve_f / (t_solve * 1e-3) / 1e12, "launch_ms": t_solve}
     else:
-        dom = {"kernel": "dgemm_nn_kernel (mode transforms, K1)", "ncu": "dgemm",
+        dom = {"kernel": "dgemm_tma_kernel (mode transforms, K1: TMA-staged DMMA GEMM)", "ncu": "dgemm",
                "achieved": tr_f / ((t_fwd + t_back) * 1e-3) / 1e12,
                "launch_ms": (t_fwd + t_back) / (2 * d)}
     traffic = traffic_from_profiles(a.config, dom["ncu"])

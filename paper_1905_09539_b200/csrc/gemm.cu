@@ -13,6 +13,10 @@
 // Y_slab = X_slab A^T (A = the tensor slab, B = the coefficient transposed
 // on the host once).
 //
+// This file: the cp.async kernel (narrow shapes, misaligned operands, the
+// tile-flag-gated back transform); products with both extents >= 64 go to
+// the TMA-staged kernel of gemm_tma.cu by default.
+//
 // Design: CTA tile BM x BN x 16, 3-stage cp.async ring (L2-only .cg 16 B
 // copies, zero-fill at the edges), 8 warps each owning a WM x WN patch of
 // 8x8 DMMA accumulators in registers.  Shared-memory leading dimensions are
@@ -370,6 +374,7 @@ cudaError_t gemm_prepare() {
   if (e == cudaSuccess) e = set_attrs<128, 128, 32, 64>();
   if (e == cudaSuccess) e = set_attrs<128, 128, 64, 64>();
   if (e == cudaSuccess) e = set_attrs<128, 64, 64, 16>();
+  if (e == cudaSuccess) e = gemm_tma_prepare();
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lk(mu);
   done.insert(dev);
@@ -383,6 +388,15 @@ cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st) {
     const char* e = std::getenv("TSG_GEMM_CFG");
     return e ? std::atoi(e) : 0;
   }();
+  // Default for both extents >= 64: the TMA-staged 64x64 kernel
+  // (gemm_tma.cu; C4 transforms 34.9 -> 35.6 TF/s, profiles/r02l_*);
+  // TSG_GEMM_TMA=0 keeps the cp.async kernel below (development A/B).  The
+  // gated back transform of the tile-DAG path (wflags) stays on cp.async.
+  static const int tma = [] {
+    const char* e = std::getenv("TSG_GEMM_TMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (tma && cfg == 0 && g.M >= 64 && g.N >= 64 && gemm_tma_ok(g)) return dgemm_nn_tma(g, st);
   if (cfg == 1 && g.M >= 128 && g.N >= 64) return launch_cfg<128, 64, 32, 32>(g, st);   // 8 warps, 2 CTA/SM
   if (cfg == 2 && g.M >= 128 && g.N >= 128) return launch_cfg<128, 128, 32, 32>(g, st); // 16 warps
   if (cfg == 3 && g.M >= 128 && g.N >= 128) return launch_cfg<128, 128, 32, 64>(g, st); // 8 warps 32x64

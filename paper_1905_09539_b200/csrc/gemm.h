@@ -56,6 +56,14 @@ cudaError_t dgemm_nn(const GemmArgs& g, cudaStream_t st);
 // at creation so no attribute change lands inside a launch chain).
 cudaError_t gemm_prepare();
 
+// TMA-staged variant (gemm_tma.cu): the same product with the operand tiles
+// moved by cp.async.bulk.tensor into swizzled stages behind mbarriers.
+// gemm_tma_ok: the call has no tile-flag gates and its operands satisfy the
+// tensor-map alignment rules (16-byte base and strides).
+bool gemm_tma_ok(const GemmArgs& g);
+cudaError_t dgemm_nn_tma(const GemmArgs& g, cudaStream_t st);
+cudaError_t gemm_tma_prepare();
+
 // Y = X x_mode A for a dense tensor (tensor.hpp:187-231 semantics):
 // A is r x dims[mode] column-major (device), At = A^T (n x r, device; only
 // used for mode > 0).  Y has dims[mode] replaced by r.

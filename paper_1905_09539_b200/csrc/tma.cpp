@@ -43,4 +43,24 @@ bool encode_tmap_f64(CUtensorMap* map, const double* base, int rank, const uint6
   return r == CUDA_SUCCESS;
 }
 
+bool encode_tmap_f64_strided(CUtensorMap* map, const double* base, int rank, const uint64_t* dims,
+                             const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128) {
+  auto fn = get_encode();
+  if (!fn || rank < 1 || rank > 5) return false;
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = 1;
+    if (i > 0) gs[i - 1] = strides_bytes[i - 1];
+  }
+  const CUresult r =
+      fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, static_cast<cuuint32_t>(rank),
+         const_cast<double*>(base), gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace tsg

@@ -11,6 +11,11 @@ namespace tsg {
 // dims[r], box[r] in elements.  Out-of-bounds box elements are zero-filled.
 bool encode_tmap_f64(CUtensorMap* map, const double* base, int rank, const uint64_t* dims,
                      const uint32_t* box);
+// General form: explicit byte strides of dims 1..rank-1 (multiples of 16),
+// optional SWIZZLE_128B (inner box extent <= 16 doubles; the shared-memory
+// destination must then be 1024-byte aligned).
+bool encode_tmap_f64_strided(CUtensorMap* map, const double* base, int rank, const uint64_t* dims,
+                             const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128);
 
 }  // namespace tsg
 
@@ -60,6 +65,9 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async;\n" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             uint64_t* bar) {
