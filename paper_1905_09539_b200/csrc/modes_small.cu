@@ -8,8 +8,12 @@
 // in shared memory in that order (inner fastest): c consecutive indices of
 // the contiguous prefix (modes < a) when a > 0, else o consecutive indices
 // of the suffix (modes > b), so every block is a few contiguous runs.  Each
-// thread owns whole fibres along the mode being applied (in place, the
-// fibre lives in registers), with the n x n matrices in shared memory.
+// warp owns whole 8-fibre groups along the mode being applied (in place:
+// DMMA accumulators, written back once the group's rows are read), with the
+// n x n matrices as register fragments.  Rows of c * n_a doubles are padded
+// to 4 (mod 8) doubles in shared memory, so the four k of a DMMA step of
+// mode b (c * n_a apart, a multiple of 8 doubles) fall on distinct banks;
+// results go back as 16-byte stores of two neighbouring fibres.
 // Reference: mode_multiply (tensor.hpp:187-231) at laplace.hpp:282/297.
 #include <cstdint>
 
@@ -33,22 +37,28 @@ struct PairArgs {
   int64_t P, Q;     // prefix (modes < a) and suffix (modes > b) sizes
   int64_t nblk;     // blocks
   int bsz;          // doubles per block = c * na * nb * o
+  int row, pitch;   // c * na and its padded pitch in shared memory (4 mod 8 doubles)
   int vec;          // 16-byte chunks (runs of even length at even offsets)
 };
 
-// y[f, i] = sum_k M(i, k) x[f, k] for the fibres of the block along a
-// coordinate of extent N and stride st (in the block): fibre index f
-// enumerates (lo < st) x (hi) with element offset lo + st * (k + N * hi).
-// DMMA: M (N x N, registers) is the A operand, each warp takes whole
-// 8-fibre blocks (B operand from shared memory) and writes them back in
-// place once all their rows are read.
-template <int N>
-TSG_DEVINL void fibres(double* blk, const double* M, int st, int nf) {
+// y[f, i] = sum_k M(i, k) x[f, k] for the fibres of the block along one
+// coordinate: fibre f = lo + lext * hi sits at blk + lo + hstr * hi and its
+// element k at + kstr * k.  DMMA: M (N x N, registers) is the A operand,
+// each warp takes whole 8-fibre groups (B operand from shared memory) and
+// writes them back in place once all their rows are read.
+// POW2: lext = 1 << llog (mode a: the prefix chunk c), any value; otherwise
+// lext is a multiple of 8 (mode b: c * n_a), a group never straddles two hi
+// and (lo, hi) advance incrementally — no integer division in the loop.
+// When lext is even, fibres 2t and 2t + 1 of a group are neighbours in
+// memory and a lane stores its two accumulator columns as one 16-byte word.
+template <int N, bool POW2>
+TSG_DEVINL void fibres(double* blk, const double* M, int lext, int llog, int kstr, int hstr, int nf) {
   constexpr int RB = N / 8, KS = N / 4;
   // N <= 32: the matrix fragments live in registers; larger N reads them
   // from shared memory per k-step (conflict-free: N = 8 mod 32 for 40)
   constexpr bool REG = N <= 32;
   constexpr int KR = REG ? KS : 1;
+  constexpr int NW = THREADS / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   double af[RB][KR];
@@ -58,13 +68,33 @@ TSG_DEVINL void fibres(double* blk, const double* M, int st, int nf) {
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) af[rb][ks] = M[(8 * rb + gq) + N * (4 * ks + tq)];
   }
-  for (int fb = warp; fb < (nf >> 3); fb += THREADS / 32) {
-    // fibre of this lane as B column: f = 8 fb + gq; as C column: 8 fb + 2 tq + h
-    const int fB = 8 * fb + gq;
-    const double* pB = blk + (fB % st) + static_cast<int64_t>(st) * N * (fB / st);
+  const bool pairst = POW2 ? (lext >= 2) : true;
+  // group base (fibre 8 fb) of this warp, advanced by NW groups per round
+  int lo = 0, hi = 0;
+  if constexpr (!POW2) {
+    lo = 8 * warp;
+    while (lo >= lext) lo -= lext, ++hi;
+  }
+  for (int fb = warp; fb < (nf >> 3); fb += NW) {
+    // fibre of this lane as B column: f = 8 fb + gq; as C columns: 8 fb + 2 tq (+ 1)
+    int oB, oC0, oC1;
+    if constexpr (POW2) {
+      const int fB = 8 * fb + gq, fC = 8 * fb + 2 * tq;
+      oB = (fB & (lext - 1)) + hstr * (fB >> llog);
+      oC0 = (fC & (lext - 1)) + hstr * (fC >> llog);
+      oC1 = ((fC + 1) & (lext - 1)) + hstr * ((fC + 1) >> llog);
+    } else {
+      const int g0 = lo + hstr * hi;
+      oB = g0 + gq;
+      oC0 = g0 + 2 * tq;
+      oC1 = oC0 + 1;
+      lo += 8 * NW;
+      while (lo >= lext) lo -= lext, ++hi;
+    }
+    const double* pB = blk + oB + kstr * tq;
     double bf[KS];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) bf[ks] = pB[st * (4 * ks + tq)];
+    for (int ks = 0; ks < KS; ++ks) bf[ks] = pB[kstr * 4 * ks];
     double c[RB][2];
 #pragma unroll
     for (int rb = 0; rb < RB; ++rb) c[rb][0] = c[rb][1] = 0.0;
@@ -76,12 +106,19 @@ TSG_DEVINL void fibres(double* blk, const double* M, int st, int nf) {
         else dmma(c[rb][0], c[rb][1], M[(8 * rb + gq) + N * (4 * ks + tq)], bf[ks]);
       }
     __syncwarp();  // every row of the warp's 8 fibres has been read
+    if (pairst) {
+      double* pC = blk + oC0 + kstr * gq;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int fC = 8 * fb + 2 * tq + h;
-      double* pC = blk + (fC % st) + static_cast<int64_t>(st) * N * (fC / st);
+      for (int rb = 0; rb < RB; ++rb)
+        *reinterpret_cast<double2*>(pC + kstr * 8 * rb) = make_double2(c[rb][0], c[rb][1]);
+    } else {
+      double* pC0 = blk + oC0 + kstr * gq;
+      double* pC1 = blk + oC1 + kstr * gq;
 #pragma unroll
-      for (int rb = 0; rb < RB; ++rb) pC[st * (8 * rb + gq)] = c[rb][h];
+      for (int rb = 0; rb < RB; ++rb) {
+        pC0[kstr * 8 * rb] = c[rb][0];
+        pC1[kstr * 8 * rb] = c[rb][1];
+      }
     }
     __syncwarp();
   }
@@ -103,50 +140,67 @@ __global__ void __launch_bounds__(THREADS) pair_kernel(PairArgs g) {
   const int c = g.c, o = g.o;
   constexpr int GRP = NA * NB;
   const int64_t npc = g.P / c;
-  // element e of a block: (ic, gi, io) at base + ic + P * (gi + GRP * io);
-  // runs of c consecutive elements are contiguous, as is the whole block
-  // when P == 1, so pairs (e, e + 1) with e even are 16-byte chunks
+  // Block element e (dense order ic, ia, ib, io) = x + row * r with
+  // x = ic + c * ia < row = c * NA and r = ib + NB * io: it lives at
+  // x + pitch * r in shared memory and at base + ic + P * (ia + NA * r) in
+  // the tensor.  Runs of c consecutive elements are contiguous, as is the
+  // whole block when P == 1, so pairs (e, e + 1) with e even are 16-byte
+  // chunks.  A thread's elements are `step` apart and c divides step, so
+  // ic is fixed per thread and the tensor offset is an arithmetic
+  // progression (a wrap of x moves ia by -NA and r by +1: no change); the
+  // shared offset gains the row padding on a wrap.  No division per element.
+  const int row = g.row, pitch = g.pitch, pad = pitch - row;
+  const int bufsz = pitch * (g.bsz / row);
   const bool vec = g.vec != 0;
+  const int step = vec ? 2 * THREADS : THREADS;
+  const int dx = step % row, dr = step / row;
+  const int e0 = vec ? 2 * threadIdx.x : threadIdx.x;
+  const int x0 = e0 % row, r0 = e0 / row;
+  const int s0 = x0 + pitch * r0, ds = dx + pitch * dr;
+  const int64_t g0 = (x0 & (c - 1)) + g.P * ((x0 >> g.lc) + static_cast<int64_t>(NA) * r0);
+  const int64_t dg = g.P * ((dx >> g.lc) + static_cast<int64_t>(NA) * dr);
   auto base_of = [&](int64_t bk) {
     const int64_t pc = bk % npc, sc = bk / npc;
     return pc * c + sc * static_cast<int64_t>(o) * g.P * GRP;
   };
-  auto off_of = [&](int e) {
-    const int ic = e & (c - 1), rest = e >> g.lc;
-    const int gi = rest % GRP, io = rest / GRP;
-    return ic + g.P * (gi + static_cast<int64_t>(GRP) * io);
-  };
   auto gather = [&](int64_t bk, double* blk) {
-    const int64_t base = base_of(bk);
-    if (vec) {
-      for (int e = 2 * threadIdx.x; e < g.bsz; e += 2 * THREADS) cp_async16(blk + e, g.X + base + off_of(e), 16);
-    } else {
-      for (int e = threadIdx.x; e < g.bsz; e += THREADS) cp_async8(blk + e, g.X + base + off_of(e), 8);
+    const double* src = g.X + base_of(bk) + g0;
+    double* dstp = blk + s0;
+    int x = x0;
+    for (int e = e0; e < g.bsz; e += step) {
+      if (vec) cp_async16(dstp, src, 16);
+      else cp_async8(dstp, src, 8);
+      src += dg, dstp += ds, x += dx;
+      if (x >= row) x -= row, dstp += pad;
     }
     cp_async_commit();
   };
   int64_t bk = blockIdx.x;
   if (bk < g.nblk) gather(bk, buf0);
   for (int it = 0; bk < g.nblk; bk += gridDim.x, ++it) {
-    double* blk = buf0 + (it & 1) * g.bsz;
-    double* nxt = buf0 + ((it + 1) & 1) * g.bsz;
+    double* blk = buf0 + (it & 1) * bufsz;
+    double* nxt = buf0 + ((it + 1) & 1) * bufsz;
     const int64_t bn = bk + gridDim.x;
     if (bn < g.nblk) gather(bn, nxt);  // the other buffer was scattered last round
     else cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    fibres<NA>(blk, ma, c, g.bsz / NA);  // mode a: stride c in the block
+    // mode a: fibres (ic; ib, io), rows c apart
+    fibres<NA, true>(blk, ma, c, g.lc, c, pitch, g.bsz / NA);
     if constexpr (NB > 1) {
       __syncthreads();
-      fibres<NB>(blk, mb, c * NA, g.bsz / NB);
+      // mode b: fibres (ic, ia; io), rows one pitch apart (row = c * NA, a multiple of 8)
+      fibres<NB, false>(blk, mb, row, 0, pitch, pitch * NB, g.bsz / NB);
     }
     __syncthreads();
-    const int64_t base = base_of(bk);
-    if (vec) {
-      for (int e = 2 * threadIdx.x; e < g.bsz; e += 2 * THREADS)
-        *reinterpret_cast<double2*>(g.Y + base + off_of(e)) = *reinterpret_cast<const double2*>(blk + e);
-    } else {
-      for (int e = threadIdx.x; e < g.bsz; e += THREADS) g.Y[base + off_of(e)] = blk[e];
+    double* dst = g.Y + base_of(bk) + g0;
+    const double* srcp = blk + s0;
+    int x = x0;
+    for (int e = e0; e < g.bsz; e += step) {
+      if (vec) *reinterpret_cast<double2*>(dst) = *reinterpret_cast<const double2*>(srcp);
+      else *dst = *srcp;
+      dst += dg, srcp += ds, x += dx;
+      if (x >= row) x -= row, srcp += pad;
     }
     __syncthreads();  // blk is the next round's prefetch target
   }
@@ -155,7 +209,7 @@ __global__ void __launch_bounds__(THREADS) pair_kernel(PairArgs g) {
 
 template <int NA, int NB>
 cudaError_t launch_pair(const PairArgs& g, cudaStream_t st) {
-  const int smem = (NA * NA + (NB > 1 ? NB * NB : 0) + 2 * g.bsz) * 8;
+  const int smem = (NA * NA + (NB > 1 ? NB * NB : 0) + 2 * g.pitch * (g.bsz / g.row)) * 8;
   auto k = pair_kernel<NA, NB>;
   int nsm = 0, occ = 0;
   if (cudaError_t e = kernel_setup(k, smem, THREADS, &nsm, &occ); e != cudaSuccess) return e;
@@ -184,7 +238,7 @@ bool small_mode_ok(int n) { return n == 16 || n == 24 || n == 32 || n == 40; }
 namespace {
 // measured best of 3K / 4.6K / 6.9K doubles per block buffer
 constexpr int kBlockTarget = 6912;
-static_assert((40 * 40 * 2 + 2 * kBlockTarget) * 8 <= 227 * 1024,
+static_assert((40 * 40 * 2 + 2 * (kBlockTarget + 4 * (kBlockTarget / 16))) * 8 <= 227 * 1024,
               "largest fused pass must fit the sm_100a shared-memory opt-in");
 // Block shape of a fused pass: c | P (inner chunk of the prefix), o | Q
 // (outer batch), powers of two, at most kBlockTarget doubles per block
@@ -199,7 +253,7 @@ bool pass_shape(int64_t P, int64_t Q, int na, int nb, int* c_out, int* o_out) {
   const int target = kBlockTarget;
   int c = 1, o = 1;
   if (P > 1) {
-    while (c * 2 * grp <= target && P % (c * 2) == 0) c *= 2;
+    while (c * 2 * grp <= target && P % (c * 2) == 0 && c * 2 <= THREADS) c *= 2;  // c | THREADS: see pair_kernel
   } else {
     while (o * 2 * grp <= target && Q % (o * 2) == 0) o *= 2;
   }
@@ -241,6 +295,8 @@ cudaError_t mode_pair_small(const double* X, double* Y, int d, const int* dims, 
   const int grp = g.na * g.nb;
   if (!pass_shape(g.P, g.Q, g.na, g.nb, &g.c, &g.o)) return cudaErrorNotSupported;
   g.bsz = g.c * grp * g.o;
+  g.row = g.c * g.na;
+  g.pitch = g.row + (4 - g.row % 8 + 8) % 8;   // 4 (mod 8) doubles: see the header
   g.lc = 0;
   while ((1 << g.lc) < g.c) ++g.lc;
   g.nblk = (g.P / g.c) * (g.Q / g.o);
