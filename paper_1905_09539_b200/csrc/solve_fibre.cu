@@ -476,7 +476,42 @@ TSG_DEVINL void rows_io(const FibreArgs& a, double* Y, int pitch, const int64_t*
   while ((1 << lw) < w && lw < 5) ++lw;
   const int sub = lane >> lw, r0 = lane & ((1 << lw) - 1), rpi = 32 >> lw;
   const int step = nw * rpi;  // runs per sweep of all warps
-  for (int run = warp * rpi + sub; run < nf * nb; run += step) {
+  const int nrun = nf * nb;
+  if (w <= 32) {
+    // One element per lane and run; four runs in flight per lane: the
+    // pattern-offset lookups, address products and (on the way out) the
+    // shared loads of a sweep are independent, which hides their latency at
+    // the kernel's low occupancy.
+    constexpr int U = 4;
+    const bool act = r0 < w;
+    for (int run0 = warp * rpi + sub; run0 < nrun; run0 += U * step) {
+      double* ys[U];
+      const double* xs[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int run = run0 + u * step;
+        ok[u] = act && run < nrun;
+        const int i = run >> kb, b = ok[u] ? run & (nb - 1) : 0;
+        ys[u] = Y + static_cast<size_t>(i) * pitch + b * w + r0;
+        xs[u] = a.X + pb[b] + static_cast<int64_t>(i) * a.sf + r0;
+      }
+      if (LOAD) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u]) cp_async8(ys[u], xs[u], 8);
+      } else {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ok[u] ? *ys[u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (ok[u]) *const_cast<double*>(xs[u]) = v[u];
+      }
+    }
+    return;
+  }
+  for (int run = warp * rpi + sub; run < nrun; run += step) {
     const int i = run >> kb, b = run & (nb - 1);
     double* y = Y + static_cast<size_t>(i) * pitch + b * w;
     const double* x = a.X + pb[b] + static_cast<int64_t>(i) * a.sf;
