@@ -529,7 +529,11 @@ def run_sharded(a, rank, world, local):
             raise RuntimeError("forced by TSG_BENCH_SHARD_FAIL")
         if mode == "decoupled":
             from paper_1905_09539_b200.dist import DecoupledSharded, DeviceDecoupled
-            be = DeviceDecoupled(ctx, rank, world, [f[1] for f in fs], [f[0] for f in fs])
+            # pipeline chunks per slab: the all-to-alls overlap the phase-A/C transforms
+            # of the neighbouring chunks; 1 = one exchange per direction
+            nchunk = a.chunks if a.chunks > 0 else (4 if world > 1 else 1)
+            nchunk = max(1, min(nchunk, min(dims[-1] // world // 8, 16) or 1))
+            be = DeviceDecoupled(ctx, rank, world, [f[1] for f in fs], [f[0] for f in fs], chunks=nchunk)
             sl = DecoupledSharded(be)
         else:
             from paper_1905_09539_b200.dist import DeviceSlabs, ShardedLaplace
@@ -631,10 +635,11 @@ def run_sharded(a, rank, world, local):
             par = (f"{world} slabs along mode {len(dims) - 1} (rows {bounds}) for the transforms of "
                    f"modes 0..{len(dims) - 2}, {world} slabs along mode 0 (rows {be.b0}) for the mode-"
                    f"{len(dims) - 1} transforms and the fibre solve along mode {be.f}; two NCCL "
-                   "all-to-alls per solve")
+                   f"all-to-alls per solve, each pipelined in {len(be.cb) - 1} chunk(s) of the slab "
+                   "against the neighbouring chunks' transforms")
             # our kernels per step: phase A/C transforms (<= d-1 passes each way) + phase B
             # (state reset, mode-(d-1) transform, fibre solve, back transform)
-            launches = a.steps * (2 * (len(dims) - 1) + 4)
+            launches = a.steps * (2 * (len(dims) - 1) * (len(be.cb) - 1) + 4)
         else:
             par = (f"{world} slabs along mode {len(dims) - 1} (rows {bounds}); NCCL all-gather for the "
                    "last-mode transforms, peer-mapped dataflow solve")
@@ -687,6 +692,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-all-configs", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="sharded path even at N=1")
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="sharded path: pipeline chunks per slab (0 = 4 when N > 1, else 1)")
     ap.add_argument("--sharded-ipc", action="store_true",
                     help="multi-GPU: the tile-DAG path over peer-mapped slabs instead of the decoupled one")
     a = ap.parse_args()

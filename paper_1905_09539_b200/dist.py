@@ -228,10 +228,34 @@ def decoupled_free_mode(dims) -> int:
     return min(range(1, d), key=lambda m: (dims[m], m))
 
 
-class DeviceDecoupled:
-    """CUDA backend of DecoupledSharded for one rank (two tsg plans)."""
+def chunk_bounds(T_last: np.ndarray, bd: list[int], chunks: int) -> list[list[int]]:
+    """Per rank, the bounds (chunks + 1, relative to the slab start) of the
+    pipeline chunks of its last-mode slab: balanced, never inside a 2x2 cell
+    of T_last (so every chunk is a valid sub-problem shape), possibly empty
+    when the slab has fewer cells than chunks.  Every rank computes the table
+    for all ranks (the receive side of the all-to-alls needs it)."""
+    T_last = _f(T_last)
+    out = []
+    for r in range(len(bd) - 1):
+        lo, hi = bd[r], bd[r + 1]
+        if chunks <= 1 or hi - lo <= 1:
+            out.append([0] + [hi - lo] * max(chunks, 1))
+            continue
+        cuts = [0]
+        for c in range(1, chunks):
+            t = max(cuts[-1], min(hi - lo, round(c * (hi - lo) / chunks)))
+            if 0 < t < hi - lo and T_last[lo + t, lo + t - 1] != 0.0:
+                t += 1  # not inside a 2x2 cell
+            cuts.append(min(t, hi - lo))
+        out.append(cuts + [hi - lo])
+    return out
 
-    def __init__(self, ctx, rank: int, nranks: int, T: list, U: list, f: int | None = None):
+
+class DeviceDecoupled:
+    """CUDA backend of DecoupledSharded for one rank (the phase-B plan and one
+    phase-A plan per distinct chunk extent)."""
+
+    def __init__(self, ctx, rank: int, nranks: int, T: list, U: list, f: int | None = None, chunks: int = 1):
         import torch
         from .plan import Plan
         self.ctx, self.rank, self.nranks = ctx, rank, nranks
@@ -253,12 +277,25 @@ class DeviceDecoupled:
         if self.f < 1:
             raise gpu_error(f"sharded decoupled solve: phase-B plan not decoupled ({self.plan_b.describe()})")
         lo, hi = self.bd[rank], self.bd[rank + 1]
-        ta = self.T[:-1] + [np.asfortranarray(self.T[-1][lo:hi, lo:hi])]
-        self.plan_a = Plan(ctx, 0, ta, self.U[:-1] + [None], skip_transform=(d - 1,), free_mode=self.f)
-        for p, nm in ((self.plan_a, "A"), (self.plan_b, "B")):
+        # phase A runs per pipeline chunk of the slab (chunks = 1: the slab);
+        # the last mode is not transformed there, so a plan serves every chunk
+        # of its extent
+        self.cb_all = chunk_bounds(self.T[-1], self.bd, chunks)
+        self.cb = self.cb_all[rank]
+        self.plans_a = {}
+        for c in range(len(self.cb) - 1):
+            c0, c1 = lo + self.cb[c], lo + self.cb[c + 1]
+            if c1 - c0 <= 0 or c1 - c0 in self.plans_a:
+                continue
+            ta = self.T[:-1] + [np.asfortranarray(self.T[-1][c0:c1, c0:c1])]
+            self.plans_a[c1 - c0] = Plan(ctx, 0, ta, self.U[:-1] + [None], skip_transform=(d - 1,),
+                                         free_mode=self.f)
+        self.plan_a = self.plans_a.get(hi - lo)  # the whole-slab plan (chunks = 1)
+        for p, nm in [(self.plan_b, "B")] + [(q, "A") for q in self.plans_a.values()]:
             if p.free_mode() != self.f:
                 raise gpu_error(f"sharded decoupled solve: phase-{nm} plan not decoupled along mode {self.f} "
                                 f"({p.describe()})")
+        self.slab_elems = int(np.prod(self.dims[:-1]))
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self.stream = ctx.stream_ptr()
 
@@ -266,11 +303,26 @@ class DeviceDecoupled:
         import torch
         return torch.empty(int(n), dtype=torch.float64, device=self.dev)
 
+    def _a(self, direction: int, src, dst) -> None:
+        """Phase-A transforms of a whole slab or of one chunk (the extent
+        follows from the buffer length)."""
+        rows = src.numel() // self.slab_elems
+        if rows in self.plans_a:
+            self.plans_a[rows].transform(direction, src.data_ptr(), dst.data_ptr(), self.stream)
+            return
+        # a whole slab handed to a chunked backend: chunk by chunk
+        if rows != self.bd[self.rank + 1] - self.bd[self.rank]:
+            raise gpu_error(f"sharded decoupled solve: no phase-A plan for {rows} last-mode rows")
+        for c in range(len(self.cb) - 1):
+            e0, e1 = self.cb[c] * self.slab_elems, self.cb[c + 1] * self.slab_elems
+            if e1 > e0:
+                self._a(direction, src[e0:e1], dst[e0:e1])
+
     def a_forward(self, b, out) -> None:
-        self.plan_a.transform(0, b.data_ptr(), out.data_ptr(), self.stream)
+        self._a(0, b, out)
 
     def a_back(self, x, out) -> None:
-        self.plan_a.transform(1, x.data_ptr(), out.data_ptr(), self.stream)
+        self._a(1, x, out)
 
     def b_solve(self, z, out) -> None:
         self.plan_b.enqueue_device(z.data_ptr(), out.data_ptr())
@@ -281,9 +333,11 @@ class DeviceDecoupled:
             raise gpu_error(f"sharded decoupled solve: singular base cell ({rep.zero_pivot_index})")
 
     def close(self):
-        for p in (getattr(self, "plan_a", None), getattr(self, "plan_b", None)):
+        for p in list(getattr(self, "plans_a", {}).values()) + [getattr(self, "plan_b", None)]:
             if p is not None:
                 p.close()
+        self.plans_a = {}
+        self.plan_a = self.plan_b = None
 
 
 class DecoupledSharded:
@@ -336,8 +390,15 @@ class DecoupledSharded:
 
     def solve(self, b, x, check: bool = False):
         """b, x: this rank's last-mode slab (flat, column-major), on the
-        backend's device; everything is ordered on the backend's stream."""
+        backend's device; everything is ordered on the backend's stream.
+        With a chunked backend (DeviceDecoupled(chunks=K)) the slab is
+        pipelined in K pieces along the last mode: chunk c's all-to-all runs
+        on the communication stream while chunk c + 1 is transformed (and, on
+        the way back, chunk c is back-transformed while chunk c + 1 is still
+        in flight), so only ~1/K of each exchange is exposed."""
         be = self.be
+        if len(getattr(be, "cb", [0, 0])) > 2:
+            return self._solve_chunked(b, x, check)
         P, n0 = be.nranks, be.dims[0]
         rd = self.rows_d[be.rank]
         be.a_forward(b, self.ya)
@@ -368,15 +429,147 @@ class DecoupledSharded:
             be.check()
         return x
 
+    # -- chunked pipeline -------------------------------------------------
+    def _chunk_views(self, c: int):
+        """Per peer q, the views that chunk c exchanges with q: `mine[q]` in
+        the packed send/receive slot of this rank's chunk c (blocks
+        (rows_c, mid, Q_q) in rank order inside the chunk's piece of sa / ra)
+        and `theirs[q]` = the rows of q's chunk c inside block q of the
+        phase-B buffers zb / xb (block q is (R_q, mid, Q_r): its chunk rows
+        are contiguous)."""
+        be = self.be
+        r, P = be.rank, be.nranks
+        r0 = self.rows_0[r]
+        rows_c = be.cb[c + 1] - be.cb[c]
+        e0 = be.cb[c] * self.mid * be.dims[0]
+        mine, o = [], e0
+        for q in range(P):
+            k = rows_c * self.mid * self.rows_0[q]
+            mine.append((o, o + k))
+            o += k
+        theirs, blk = [], 0
+        for q in range(P):
+            cq0, cq1 = be.cb_all[q][c], be.cb_all[q][c + 1]
+            theirs.append((blk + cq0 * self.mid * r0, blk + cq1 * self.mid * r0))
+            blk += self.rows_d[q] * self.mid * r0
+        return mine, theirs
 
-def decoupled_emulated_solve(ctx, T: list, U: list, b_full: np.ndarray, nslabs: int) -> np.ndarray:
+    def _exchange(self, out, out_rng, inp, in_rng, comm, after):
+        """All-to-all of the given (start, stop) pieces: inp[in_rng[q]] -> rank
+        q, out[out_rng[q]] <- rank q.  CUDA: list-based NCCL all_to_all
+        straight between the views, asynchronous on the communication stream
+        once `after` (an event of the compute stream) has fired; returns the
+        callable that makes the compute stream wait for it.  CPU (gloo, tests):
+        all_to_all_single through contiguous staging, completed on return."""
+        import torch
+        import torch.distributed as dist
+        be = self.be
+        outs = [out[a:z] for a, z in out_rng]
+        ins = [inp[a:z] for a, z in in_rng]
+        if be.nranks == 1 and not (dist.is_available() and dist.is_initialized()):
+            self._run_torch(lambda: outs[0].copy_(ins[0]))
+            return lambda: None
+        if out.is_cuda:
+            with torch.cuda.stream(comm):
+                comm.wait_event(after)
+                work = dist.all_to_all(outs, ins, group=self.group, async_op=True)
+            return work.wait  # called under the compute stream: a stream-side wait
+        stage_in = torch.cat(ins) if ins else inp[:0]
+        stage_out = torch.empty(sum(z - a for a, z in out_rng), dtype=out.dtype)
+        dist.all_to_all_single(stage_out, stage_in, [z - a for a, z in out_rng], [z - a for a, z in in_rng],
+                               group=self.group)
+        o = 0
+        for v in outs:
+            v.copy_(stage_out[o:o + v.numel()])
+            o += v.numel()
+        return lambda: None
+
+    def _solve_chunked(self, b, x, check: bool = False):
+        import torch
+        be = self.be
+        P, n0 = be.nranks, be.dims[0]
+        K = len(be.cb) - 1
+        cuda = self.ya.is_cuda
+        if cuda:
+            compute = torch.cuda.ExternalStream(be.stream, device=self.ya.device)
+            if getattr(self, "_comm", None) is None:
+                self._comm = torch.cuda.Stream(device=self.ya.device)
+            comm = self._comm
+        else:
+            compute = comm = None
+
+        def on_compute(fn):
+            if cuda:
+                with torch.cuda.stream(compute):
+                    return fn()
+            return fn()
+
+        def mark():
+            if not cuda:
+                return None
+            ev = torch.cuda.Event()
+            ev.record(compute)
+            return ev
+
+        views = [self._chunk_views(c) for c in range(K)]
+        slab = self.mid * n0
+        # forward: transform + pack chunk c, then its exchange overlaps chunk c + 1
+        waits = []
+        for c in range(K):
+            rows_c = be.cb[c + 1] - be.cb[c]
+            e0, e1 = be.cb[c] * slab, be.cb[c + 1] * slab
+            mine, theirs = views[c]
+            if rows_c > 0:
+                be.a_forward(b[e0:e1], self.ya[e0:e1])
+
+                def pack(rows_c=rows_c, e0=e0, e1=e1, mine=mine):
+                    v = self.ya[e0:e1].view(rows_c, self.mid, n0)
+                    for q in range(P):
+                        a, z = mine[q]
+                        self.sa[a:z].view(rows_c, self.mid, self.rows_0[q]).copy_(v[:, :, be.b0[q]:be.b0[q + 1]])
+                on_compute(pack)
+            waits.append(self._exchange(self.zb, theirs, self.sa, mine, comm, mark()))
+        for w in waits:
+            on_compute(w)
+        be.b_solve(self.zb, self.xb)
+        # back: every chunk's exchange is queued behind the solve; chunk c is
+        # unpacked and back-transformed as soon as it has landed
+        done = mark()
+        waits = [self._exchange(self.ra, views[c][0], self.xb, views[c][1], comm, done) for c in range(K)]
+        for c in range(K):
+            rows_c = be.cb[c + 1] - be.cb[c]
+            e0, e1 = be.cb[c] * slab, be.cb[c + 1] * slab
+            mine = views[c][0]
+            on_compute(waits[c])
+            if rows_c == 0:
+                continue
+
+            def unpack(rows_c=rows_c, e0=e0, e1=e1, mine=mine):
+                v = self.ya[e0:e1].view(rows_c, self.mid, n0)
+                for q in range(P):
+                    a, z = mine[q]
+                    v[:, :, be.b0[q]:be.b0[q + 1]].copy_(self.ra[a:z].view(rows_c, self.mid, self.rows_0[q]))
+            on_compute(unpack)
+            be.a_back(self.ya[e0:e1], x[e0:e1])
+        if cuda:
+            # the next solve's first pack overwrites sa: it must not pass the
+            # exchanges still reading it (they completed before b_solve), and
+            # the communication stream must not run ahead of this solve
+            comm.wait_event(mark())
+        if check and hasattr(be, "check"):
+            be.check()
+        return x
+
+
+def decoupled_emulated_solve(ctx, T: list, U: list, b_full: np.ndarray, nslabs: int, chunks: int = 1) -> np.ndarray:
     """All slabs of the sharded decoupled solve in one process on one GPU:
     the same plans and pack/unpack as the ranks, the all-to-alls done by
-    copies between the slabs' buffers (validation on a single device)."""
+    copies between the slabs' buffers (validation on a single device).
+    chunks > 1: phase A runs on the per-chunk plans of the pipelined solve."""
     import torch
     dims = [t.shape[0] for t in T]
     d = len(dims)
-    bes = [DeviceDecoupled(ctx, r, nslabs, T, U) for r in range(nslabs)]
+    bes = [DeviceDecoupled(ctx, r, nslabs, T, U, chunks=chunks) for r in range(nslabs)]
     sh = [DecoupledSharded(be) for be in bes]
     bd, b0 = bes[0].bd, bes[0].b0
     st = torch.cuda.ExternalStream(ctx.stream_ptr())

@@ -47,14 +47,17 @@ def _block_eigenbasis(t):
 
 
 class CpuDecoupled:
-    def __init__(self, rank, nranks, T, U):
-        from paper_1905_09539_b200.dist import decoupled_free_mode, slab_bounds
+    def __init__(self, rank, nranks, T, U, chunks=1):
+        from paper_1905_09539_b200.dist import chunk_bounds, decoupled_free_mode, slab_bounds
         self.rank, self.nranks, self.stream = rank, nranks, 0
         self.T, self.U = T, U
         self.dims = [t.shape[0] for t in T]
         self.f = decoupled_free_mode(self.dims)
         self.bd = slab_bounds(self.dims[-1], T[-1], nranks, tile=1)
         self.b0 = slab_bounds(self.dims[0], T[0], nranks, tile=1)
+        # pipeline chunks of every rank's slab (chunks = 1: the slab itself)
+        self.cb_all = chunk_bounds(T[-1], self.bd, chunks)
+        self.cb = self.cb_all[rank]
         d = len(T)
         self.P = [None if m == self.f else _block_eigenbasis(T[m]) for m in range(d)]
         self.L = [None if m == self.f else np.linalg.solve(self.P[m], T[m] @ self.P[m]) for m in range(d)]
@@ -68,18 +71,18 @@ class CpuDecoupled:
     def _bwd(self, m):
         return self.U[m] if m == self.f else self.U[m] @ self.P[m]
 
-    def _shape_a(self):
-        lo, hi = self.bd[self.rank], self.bd[self.rank + 1]
-        return tuple(self.dims[:-1]) + (hi - lo,)
+    def _shape_a(self, v):
+        # a whole slab or one pipeline chunk of it: the extent follows from the length
+        return tuple(self.dims[:-1]) + (v.numel() // int(np.prod(self.dims[:-1])),)
 
     def a_forward(self, b, out):
-        y = b.numpy().reshape(self._shape_a(), order="F")
+        y = b.numpy().reshape(self._shape_a(b), order="F")
         for m in range(len(self.dims) - 1):
             y = R.mode_multiply(y, self._fwd(m), m)
         out.copy_(torch.from_numpy(np.asfortranarray(y).reshape(-1, order="F")))
 
     def a_back(self, x, out):
-        y = x.numpy().reshape(self._shape_a(), order="F")
+        y = x.numpy().reshape(self._shape_a(x), order="F")
         for m in range(len(self.dims) - 1):
             y = R.mode_multiply(y, self._bwd(m), m)
         out.copy_(torch.from_numpy(np.asfortranarray(y).reshape(-1, order="F")))
@@ -95,7 +98,7 @@ class CpuDecoupled:
         out.copy_(torch.from_numpy(np.asfortranarray(xs).reshape(-1, order="F")))
 
 
-def _worker(rank, world, port, kind, dims, q):
+def _worker(rank, world, port, kind, dims, chunks, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -103,7 +106,7 @@ def _worker(rank, world, port, kind, dims, q):
         from paper_1905_09539_b200.dist import DecoupledSharded
         coeffs, _, rhs = R.baseline_problem(kind, dims, seed=9)
         f = [R.schur(a) for a in coeffs]   # (U, T) per mode, shared setup
-        be = CpuDecoupled(rank, world, [t for _, t in f], [u for u, _ in f])
+        be = CpuDecoupled(rank, world, [t for _, t in f], [u for u, _ in f], chunks)
         lo, hi = be.bd[rank], be.bd[rank + 1]
         b = torch.from_numpy(np.asfortranarray(rhs[..., lo:hi]).reshape(-1, order="F").copy())
         x = torch.zeros_like(b)
@@ -112,7 +115,7 @@ def _worker(rank, world, port, kind, dims, q):
         want = R.solve_laplace(coeffs, rhs, n_min=4)[..., lo:hi]
         got = x.numpy().reshape(want.shape, order="F")
         err = float(np.linalg.norm(got - want) / np.linalg.norm(want))
-        q.put((rank, lo, hi, be.b0, err))
+        q.put((rank, lo, hi, be.b0, err, be.cb))
     finally:
         dist.destroy_process_group()
 
@@ -123,13 +126,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,kind,dims", [(2, 2, (8, 6, 10)), (3, 2, (9, 5, 12)), (2, 1, (8, 7, 6)),
-                                             (3, 2, (6, 4, 3, 9))])
-def test_decoupled_sharded_gloo(world, kind, dims):
+@pytest.mark.parametrize("world,kind,dims,chunks", [
+    (2, 2, (8, 6, 10), 1), (3, 2, (9, 5, 12), 1), (2, 1, (8, 7, 6), 1), (3, 2, (6, 4, 3, 9), 1),
+    # pipelined exchanges: 2-4 chunks per slab (ragged, and more chunks than some slabs have cells)
+    (2, 2, (8, 6, 10), 2), (3, 2, (9, 5, 12), 3), (2, 2, (7, 5, 9), 4), (3, 2, (6, 4, 3, 9), 2)])
+def test_decoupled_sharded_gloo(world, kind, dims, chunks):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, dims, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, dims, chunks, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=240) for _ in range(world)]
@@ -140,6 +145,8 @@ def test_decoupled_sharded_gloo(world, kind, dims):
     assert res[0][1] == 0 and res[-1][2] == dims[-1]
     b0 = res[0][3]
     assert b0[0] == 0 and b0[-1] == dims[0] and all(b1 > a1 for a1, b1 in zip(b0, b0[1:]))
-    for r, lo, hi, _, err in res:
+    for r, lo, hi, _, err, cb in res:
         assert hi > lo
         assert err < 1e-10, (r, err)
+        assert len(cb) == chunks + 1 and cb[0] == 0 and cb[-1] == hi - lo
+        assert all(b1 >= a1 for a1, b1 in zip(cb, cb[1:]))

@@ -31,20 +31,39 @@ def test_decoupled_sharded_emulated(ref, gpu, kind, dims, nslabs):
     assert res <= 1e-12, res
 
 
-def test_decoupled_sharded_world1_nccl(ref, gpu):
-    """The real orchestration (NCCL process group of one rank)."""
+@pytest.mark.parametrize("kind,dims,nslabs,chunks", [(2, (24, 20, 18), 2, 2), (2, (33, 20, 27), 3, 4),
+                                                     (2, (20, 12, 10, 16), 3, 3)])
+def test_decoupled_sharded_emulated_chunk_plans(ref, gpu, kind, dims, nslabs, chunks):
+    """Phase A on the per-chunk plans of the pipelined solve (ragged chunks,
+    snapped off the 2x2 cells of the last mode)."""
+    from paper_1905_09539_b200.dist import decoupled_emulated_solve
+    from paper_1905_09539_b200.plan import Context
+    p = gpu.make_problem(kind, dims, seed=23)
+    fs = [gpu.schur(a) for a in p.coeffs]
+    x = decoupled_emulated_solve(Context(0), [f[1] for f in fs], [f[0] for f in fs], p.rhs, nslabs, chunks=chunks)
+    want, _ = ref.solve_laplace(p.coeffs, p.rhs, strategy=0, arithmetic=1)
+    assert rel_diff(x, want) <= 1e-10
+    assert ref.residual_laplace(p.coeffs, p.rhs, x) <= 1e-12
+
+
+@pytest.mark.parametrize("chunks,dims", [(1, (64, 64, 64)), (3, (64, 64, 64)), (4, (40, 24, 50))])
+def test_decoupled_sharded_world1_nccl(ref, gpu, chunks, dims):
+    """The real orchestration (NCCL process group of one rank); chunks > 1:
+    the pipelined exchanges (list all_to_all on the communication stream,
+    event-ordered against the compute stream)."""
     import torch
     import torch.distributed as dist
     from paper_1905_09539_b200.dist import DecoupledSharded, DeviceDecoupled
     from paper_1905_09539_b200.plan import Context
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29561")
+    os.environ["MASTER_PORT"] = str(29561 + chunks)
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        p = gpu.make_problem(1, (64, 64, 64), seed=22)
+        p = gpu.make_problem(1 if dims[0] == 64 else 2, dims, seed=22)
         fs = [gpu.schur(a) for a in p.coeffs]
         ctx = Context(0)
-        be = DeviceDecoupled(ctx, 0, 1, [f[1] for f in fs], [f[0] for f in fs])
+        be = DeviceDecoupled(ctx, 0, 1, [f[1] for f in fs], [f[0] for f in fs], chunks=chunks)
+        assert len(be.cb) == chunks + 1
         sh = DecoupledSharded(be)
         b = torch.from_numpy(np.ascontiguousarray(p.rhs).reshape(-1, order="F")).cuda()
         x = torch.empty_like(b)
