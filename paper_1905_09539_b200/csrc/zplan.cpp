@@ -319,7 +319,7 @@ int zsolve(tsg_ctx* ctx, int family, int d, const int* dims, const double* const
     }
   }
   // fibre solve tables
-  DevBuf dS, dTc, dlam;
+  DevBuf dS, dTc, dScm, dTccm, dlam;
   tsg::ZFibreArgs fa{};
   tsg::ZLevelArgs la{};
   std::vector<DevBuf> dTt(d);
@@ -331,9 +331,13 @@ int zsolve(tsg_ctx* ctx, int family, int d, const int* dims, const double* const
   if (path != kWavefront) {
     const ZMat St = transpose(family == 1 ? Tm[0] : Tm[f]);
     TSG_CU(up(dS, St.a.data(), St.a.size()));
+    // column-major copies: operands of the blocked solve's GEMM updates
+    const ZMat& Scm = family == 1 ? Tm[0] : Tm[f];
+    TSG_CU(up(dScm, Scm.a.data(), Scm.a.size()));
     if (family == 1) {
       const ZMat Tct = transpose(Tcm);
       TSG_CU(up(dTc, Tct.a.data(), Tct.a.size()));
+      TSG_CU(up(dTccm, Tcm.a.data(), Tcm.a.size()));
     }
     std::vector<C> lam;
     fa.x = nullptr;
@@ -353,6 +357,8 @@ int zsolve(tsg_ctx* ctx, int family, int d, const int* dims, const double* const
     fa.nfib = N / dims[f];
     fa.St = dS.p;
     fa.Tct = family == 1 ? dTc.p : nullptr;
+    fa.S = dScm.p;
+    fa.Tc = family == 1 ? dTccm.p : nullptr;
     fa.lam = dlam.p;
     fa.product = family;
     fa.tiny2 = tiny * tiny;
@@ -384,6 +390,7 @@ int zsolve(tsg_ctx* ctx, int family, int d, const int* dims, const double* const
 
   // ---- buffers and timing
   DevBuf bt, xt, rr, dB, dX;
+  DevBuf tmp, corr;  // refinement scratch: released with the others, after the last kernel
   TSG_CU(bt.ensure(2 * N));
   TSG_CU(xt.ensure(2 * N));
   TSG_CU(run.s1.ensure(2 * N));
@@ -405,8 +412,8 @@ int zsolve(tsg_ctx* ctx, int family, int d, const int* dims, const double* const
   auto dec_solve = [&](const double* v, double* out) -> cudaError_t {
     if (cudaError_t e = run.chain(v, out, efwd_ops); e != cudaSuccess) return e;
     fa.x = out;
-    if (cudaError_t e = tsg::zfibre_solve(fa, st); e != cudaSuccess) return e;
-    ++run.launches;
+    fa.work = family == 1 ? run.s1.p : nullptr;  // the chains' scratch is idle during the solve
+    if (cudaError_t e = tsg::zfibre_solve(fa, st, &run.launches, &run.flops); e != cudaSuccess) return e;
     if (eback_ops.empty()) return cudaSuccess;
     // back to the Schur basis through the scratch pair (out is neither)
     if (cudaError_t e = cudaMemcpyAsync(run.s2.p, out, N * sizeof(C), cudaMemcpyDeviceToDevice, st);
@@ -419,8 +426,8 @@ int zsolve(tsg_ctx* ctx, int family, int d, const int* dims, const double* const
     TSG_CU(run.chain(bin, fwd_out, fwd_ops));
     TSG_CU(cudaEventRecord(ev[2], st));
     fa.x = fwd_out;
-    TSG_CU(tsg::zfibre_solve(fa, st));
-    ++run.launches;
+    fa.work = family == 1 ? run.s1.p : nullptr;  // the chains' scratch is idle during the solve
+    TSG_CU(tsg::zfibre_solve(fa, st, &run.launches, &run.flops));
     TSG_CU(cudaEventRecord(ev[3], st));
     TSG_CU(run.chain(fwd_out, on_dev ? xout : bt.p, back_ops));
     xout = on_dev ? xout : bt.p;
@@ -440,7 +447,6 @@ int zsolve(tsg_ctx* ctx, int family, int d, const int* dims, const double* const
       bref = bt.p;
     }
     TSG_CU(cudaEventRecord(ev[2], st));
-    DevBuf tmp, corr;
     TSG_CU(tmp.ensure(2 * N));
     TSG_CU(corr.ensure(2 * N));
     TSG_CU(dec_solve(bref, xt.p));

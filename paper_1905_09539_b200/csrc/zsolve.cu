@@ -174,53 +174,91 @@ __global__ void __launch_bounds__(ZNT, 2) zgemm_kernel(ZGemmArgs g) {
 }
 
 // ---------------------------------------------------------------------------
-// Decoupled fibre solve: thread = one fibre along mode f.  Fibres are
-// enumerated with the modes before f fastest, so a warp's loads of row i
-// are contiguous when f > 0.  Left-looking back substitution (rows from the
-// bottom); the row-major S / Tc rows are read by every lane at the same
-// address (broadcast).
-__global__ void __launch_bounds__(128) zfibre_kernel(const ZFibreArgs a) {
-  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (q >= a.nfib) return;
-  const int64_t lo = q % a.sf, hi = q / a.sf;
-  // the other modes' eigenvalues combine into z
-  cplx z = a.product ? cplx{1.0, 0.0} : cplx{0.0, 0.0};
-  int64_t r = lo;
-  for (int m = 0; m < a.f; ++m) {
-    const int i = static_cast<int>(r % a.dims[m]);
-    r /= a.dims[m];
-    const cplx l = ld2(a.lam + 2 * (a.lam_off[m] + i));
-    z = a.product ? cmul(z, l) : cadd(z, l);
-  }
-  r = hi;
-  for (int m = a.f + 1; m < a.d; ++m) {
-    const int i = static_cast<int>(r % a.dims[m]);
-    r /= a.dims[m];
-    const cplx l = ld2(a.lam + 2 * (a.lam_off[m] + i));
-    z = a.product ? cmul(z, l) : cadd(z, l);
-  }
-  const int n = a.nf;
-  double* __restrict__ x = a.x + 2 * (lo + hi * a.sf * n);
-  const int64_t s2 = 2 * a.sf;
-  for (int i = n - 1; i >= 0; --i) {
-    cplx acc = ld2(x + i * s2);
-    const double* srow = a.St + 2 * static_cast<int64_t>(i) * n;
-    const double* trow = a.Tct ? a.Tct + 2 * static_cast<int64_t>(i) * n : nullptr;
-    for (int j = i + 1; j < n; ++j) {
-      cplx c = ld2(srow + 2 * j);
-      if (trow) c = cadd(c, cmul(z, ld2(trow + 2 * j)));
-      acc = cfms(acc, c, ld2(x + j * s2));
+// Decoupled fibre solve, diagonal block rows [i_lo, i_hi) (<= ZFB rows) of
+// every fibre along mode f: thread = one fibre, a CTA stages the block rows of
+// its ZFT fibres in shared memory (coalesced: rows of f > 0 are contiguous
+// across fibres, fibres of f = 0 are contiguous along the rows), substitutes
+// them bottom-up (the rows below the block were applied by the GEMM updates
+// of zfibre_solve; the row-major S / Tc rows are read by every lane at the
+// same address) and writes x back — for gsylv also z x into `work`, the
+// operand of the Tc updates of the blocks above.
+constexpr int ZFB = 32;         // rows per diagonal block
+constexpr int ZFT = 128;        // fibres per CTA
+constexpr int ZFP = ZFB + 1;    // shared pitch (complex elements) per fibre
+constexpr int ZFSMEM = ZFT * ZFP * 2 * static_cast<int>(sizeof(double));
+
+__global__ void __launch_bounds__(ZFT) zfibre_kernel(const ZFibreArgs a) {
+  extern __shared__ __align__(16) double zsm[];
+  const int64_t q0 = blockIdx.x * static_cast<int64_t>(ZFT);
+  const int nfib = static_cast<int>(a.nfib - q0 < ZFT ? a.nfib - q0 : ZFT);
+  const int n = a.nf, lo_r = a.i_lo, nr = a.i_hi - a.i_lo;
+  const int64_t sf = a.sf;
+  // element (fibre q, row i): x + 2 * ((q % sf) + i * sf + (q / sf) * sf * n)
+  auto fibre_base = [&](int64_t q) { return (q % sf) + (q / sf) * sf * n; };
+  if (a.f == 0) {  // sf == 1: a fibre's rows are contiguous
+    for (int e = threadIdx.x; e < nfib * nr; e += ZFT) {
+      const int t = e / nr, i = e - t * nr;
+      st2(zsm + 2 * (t * ZFP + i), ld2(a.x + 2 * ((q0 + t) * n + lo_r + i)));
     }
-    cplx dg = ld2(srow + 2 * i);
-    dg = trow ? cadd(dg, cmul(z, ld2(trow + 2 * i))) : cadd(dg, z);
-    const double m2 = dg.r * dg.r + dg.i * dg.i;
-    if (!(m2 > a.tiny2)) {
-      atomicMin(a.status, static_cast<int>(q < 0x7fffffff ? q : 0x7ffffffe));
-      st2(x + i * s2, {0.0, 0.0});
-      continue;
+  } else if (threadIdx.x < nfib) {
+    const double* xp = a.x + 2 * (fibre_base(q0 + threadIdx.x) + lo_r * sf);
+    for (int i = 0; i < nr; ++i) st2(zsm + 2 * (threadIdx.x * ZFP + i), ld2(xp + 2 * i * sf));
+  }
+  __syncthreads();
+  if (threadIdx.x < nfib) {
+    const int64_t q = q0 + threadIdx.x;
+    const int64_t lo = q % sf, hi = q / sf;
+    // the other modes' eigenvalues combine into z
+    cplx z = a.product ? cplx{1.0, 0.0} : cplx{0.0, 0.0};
+    int64_t r = lo;
+    for (int m = 0; m < a.f; ++m) {
+      const int i = static_cast<int>(r % a.dims[m]);
+      r /= a.dims[m];
+      const cplx l = ld2(a.lam + 2 * (a.lam_off[m] + i));
+      z = a.product ? cmul(z, l) : cadd(z, l);
     }
-    const double inv = 1.0 / m2;
-    st2(x + i * s2, {(acc.r * dg.r + acc.i * dg.i) * inv, (acc.i * dg.r - acc.r * dg.i) * inv});
+    r = hi;
+    for (int m = a.f + 1; m < a.d; ++m) {
+      const int i = static_cast<int>(r % a.dims[m]);
+      r /= a.dims[m];
+      const cplx l = ld2(a.lam + 2 * (a.lam_off[m] + i));
+      z = a.product ? cmul(z, l) : cadd(z, l);
+    }
+    double* xs = zsm + 2 * (threadIdx.x * ZFP);
+    for (int i = nr - 1; i >= 0; --i) {
+      cplx acc = ld2(xs + 2 * i);
+      const double* srow = a.St + 2 * (static_cast<int64_t>(lo_r + i) * n + lo_r);
+      const double* trow = a.Tct ? a.Tct + 2 * (static_cast<int64_t>(lo_r + i) * n + lo_r) : nullptr;
+      for (int j = i + 1; j < nr; ++j) {
+        cplx c = ld2(srow + 2 * j);
+        if (trow) c = cadd(c, cmul(z, ld2(trow + 2 * j)));
+        acc = cfms(acc, c, ld2(xs + 2 * j));
+      }
+      cplx dg = ld2(srow + 2 * i);
+      dg = trow ? cadd(dg, cmul(z, ld2(trow + 2 * i))) : cadd(dg, z);
+      const double m2 = dg.r * dg.r + dg.i * dg.i;
+      if (!(m2 > a.tiny2)) {
+        atomicMin(a.status, static_cast<int>(q < 0x7fffffff ? q : 0x7ffffffe));
+        st2(xs + 2 * i, {0.0, 0.0});
+        continue;
+      }
+      const double inv = 1.0 / m2;
+      st2(xs + 2 * i, {(acc.r * dg.r + acc.i * dg.i) * inv, (acc.i * dg.r - acc.r * dg.i) * inv});
+    }
+    if (a.work && a.i_lo > 0) {  // z x for the Tc updates of the blocks above (f = 0)
+      double* wp = a.work + 2 * (q * n + lo_r);
+      for (int i = 0; i < nr; ++i) st2(wp + 2 * i, cmul(z, ld2(xs + 2 * i)));
+    }
+  }
+  __syncthreads();
+  if (a.f == 0) {
+    for (int e = threadIdx.x; e < nfib * nr; e += ZFT) {
+      const int t = e / nr, i = e - t * nr;
+      st2(a.x + 2 * ((q0 + t) * n + lo_r + i), ld2(zsm + 2 * (t * ZFP + i)));
+    }
+  } else if (threadIdx.x < nfib) {
+    double* xp = a.x + 2 * (fibre_base(q0 + threadIdx.x) + lo_r * sf);
+    for (int i = 0; i < nr; ++i) st2(xp + 2 * i * sf, ld2(zsm + 2 * (threadIdx.x * ZFP + i)));
   }
 }
 
@@ -321,11 +359,69 @@ cudaError_t zmode_product(const double* X, double* Y, int d, const int* dims, in
   return zgemm(g, st);
 }
 
-cudaError_t zfibre_solve(const ZFibreArgs& a, cudaStream_t st) {
-  if (a.nfib <= 0) return cudaSuccess;
-  const int64_t blocks = (a.nfib + 127) / 128;
-  zfibre_kernel<<<static_cast<unsigned>(blocks), 128, 0, st>>>(a);
-  return cudaGetLastError();
+cudaError_t zfibre_solve(const ZFibreArgs& a0, cudaStream_t st, int* launches, double* flops) {
+  if (a0.nfib <= 0 || a0.nf <= 0) return cudaSuccess;
+  ZFibreArgs a = a0;
+  const int n = a.nf;
+  const bool gs = a.Tct != nullptr;
+  // blocked only with the operands of the GEMM updates at hand
+  const bool blocked = n > ZFB && (a.f > 0 || a.S) && (!gs || (a.f == 0 && a.Tc && a.work));
+  if (!blocked && n > ZFB) return cudaErrorInvalidValue;
+  if (gs && a.f != 0) return cudaErrorInvalidValue;
+  int nsm = 0, occ = 0;
+  if (cudaError_t e = kernel_setup(zfibre_kernel, ZFSMEM, ZFT, &nsm, &occ); e != cudaSuccess) return e;
+  const int64_t blocks = (a.nfib + ZFT - 1) / ZFT;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const int64_t P = a.sf, Q = a.nfib / a.sf;
+  for (int hi = n; hi > 0;) {
+    const int lo = hi > ZFB ? hi - ZFB : 0;
+    if (hi < n) {
+      // x[lo:hi] -= S[lo:hi, hi:n] x[hi:n]  (+ Tc[lo:hi, hi:n] (z x)[hi:n])
+      ZGemmArgs g{};
+      g.alpha = -1.0;
+      g.beta = 1.0;
+      g.K = n - hi;
+      if (a.f == 0) {
+        if (Q > 0x7fffffffLL) return cudaErrorInvalidValue;
+        g.M = hi - lo;
+        g.N = static_cast<int>(Q);
+        g.lda = g.ldb = g.ldc = n;
+        g.batch = 1;
+        g.A = a.S + 2 * (lo + static_cast<int64_t>(hi) * n);
+        g.B = a.x + 2 * static_cast<int64_t>(hi);
+        g.C = a.x + 2 * static_cast<int64_t>(lo);
+        if (cudaError_t e = zgemm(g, st); e != cudaSuccess) return e;
+        if (gs) {
+          g.A = a.Tc + 2 * (lo + static_cast<int64_t>(hi) * n);
+          g.B = a.work + 2 * static_cast<int64_t>(hi);
+          if (cudaError_t e = zgemm(g, st); e != cudaSuccess) return e;
+        }
+      } else {
+        // per slab: X_q[:, lo:hi] -= X_q[:, hi:n] (S[lo:hi, hi:n])^T; St is S^T column-major
+        if (P > 0x7fffffffLL) return cudaErrorInvalidValue;
+        g.M = static_cast<int>(P);
+        g.N = hi - lo;
+        g.lda = g.ldc = P;
+        g.ldb = n;
+        g.sA = g.sC = P * n;
+        g.sB = 0;
+        g.batch = Q;
+        g.A = a.x + 2 * (static_cast<int64_t>(hi) * P);
+        g.B = a.St + 2 * (hi + static_cast<int64_t>(lo) * n);
+        g.C = a.x + 2 * (static_cast<int64_t>(lo) * P);
+        if (cudaError_t e = zgemm(g, st); e != cudaSuccess) return e;
+      }
+      if (launches) *launches += gs ? 2 : 1;
+      if (flops) *flops += (gs ? 16.0 : 8.0) * static_cast<double>(a.nfib) * (hi - lo) * (n - hi);
+    }
+    a.i_lo = lo;
+    a.i_hi = hi;
+    zfibre_kernel<<<static_cast<unsigned>(blocks), ZFT, ZFSMEM, st>>>(a);
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+    if (launches) *launches += 1;
+    hi = lo;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t zlevel_solve(ZLevelArgs a, cudaStream_t st, int* launches) {

@@ -31,6 +31,12 @@ cudaError_t zmode_product(const double* X, double* Y, int d, const int* dims, in
 //   (S + z Tc) x_fibre = r_fibre,  z = sum_m lam_m[i_m] (product = 0,
 //   Laplace; Tc = NULL means the identity) or prod_m lam_m[i_m] (product =
 //   1, gsylv) over the modes m != f.  St / Tct are row-major (transposed).
+// Blocked: rows of f in blocks of 32 from the bottom; the coupling to the rows
+// already solved is a complex DMMA GEMM with the off-diagonal block of S (and
+// of Tc against the z-scaled solved rows kept in `work`), the 32-row diagonal
+// block is substituted per fibre from shared memory (zfibre_kernel).  S / Tc
+// are the column-major copies (needed for f = 0), work holds N complex
+// elements (gsylv only).
 struct ZFibreArgs {
   double* x;
   int d, f, nf;
@@ -39,13 +45,17 @@ struct ZFibreArgs {
   int64_t nfib;  // N / nf
   const double* St;
   const double* Tct;
+  const double* S;    // column-major S (f = 0 updates); may be null when f > 0
+  const double* Tc;   // column-major Tc (gsylv)
+  double* work;       // gsylv: z x of the solved rows (N complex elements)
+  int i_lo, i_hi;     // rows of the diagonal block of one launch (set by zfibre_solve)
   const double* lam;  // packed eigenvalues, mode m at lam_off[m]
   int lam_off[kZMaxOrder];
   int product;
   double tiny2;  // |pivot|^2 <= tiny2 -> singular (status = min fibre index)
   int* status;
 };
-cudaError_t zfibre_solve(const ZFibreArgs& a, cudaStream_t st);
+cudaError_t zfibre_solve(const ZFibreArgs& a, cudaStream_t st, int* launches = nullptr, double* flops = nullptr);
 
 // Fully triangular reduced Laplace solve by wavefronts (one launch per
 // level); Tt[m] row-major T_m.  x: B~ in, X~ out.
