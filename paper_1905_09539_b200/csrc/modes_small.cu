@@ -16,6 +16,7 @@
 // results go back as 16-byte stores of two neighbouring fibres.
 // Reference: mode_multiply (tensor.hpp:187-231) at laplace.hpp:282/297.
 #include <cstdint>
+#include <cstdio>
 
 #include "common.cuh"
 #include "gemm.h"
@@ -25,6 +26,18 @@ namespace tsg {
 namespace {
 
 constexpr int THREADS = 256;
+#ifndef PAIR_PROF
+#define PAIR_PROF 0
+#endif
+#if PAIR_PROF
+// development: per-phase cycle counters of pair_kernel (tools/mkalt.py <name> -DPAIR_PROF=1)
+__device__ unsigned long long g_pair_prof[8];
+#define PP_T(v) const long long v = clock64()
+#define PP_ADD(k, t0) (pph[k] += clock64() - (t0))
+#else
+#define PP_T(v)
+#define PP_ADD(k, t0)
+#endif
 
 struct PairArgs {
   const double* X;
@@ -176,23 +189,41 @@ __global__ void __launch_bounds__(THREADS) pair_kernel(PairArgs g) {
     cp_async_commit();
   };
   int64_t bk = blockIdx.x;
+#if PAIR_PROF
+  long long pph[8] = {};
+#endif
   if (bk < g.nblk) gather(bk, buf0);
   for (int it = 0; bk < g.nblk; bk += gridDim.x, ++it) {
     double* blk = buf0 + (it & 1) * bufsz;
     double* nxt = buf0 + ((it + 1) & 1) * bufsz;
     const int64_t bn = bk + gridDim.x;
+    PP_T(t0);
     if (bn < g.nblk) gather(bn, nxt);  // the other buffer was scattered last round
     else cp_async_commit();
+    PP_ADD(0, t0);
+    PP_T(t1);
     cp_async_wait<1>();
+    PP_ADD(1, t1);
+    PP_T(t2);
     __syncthreads();
+    PP_ADD(2, t2);
+    PP_T(t3);
     // mode a: fibres (ic; ib, io), rows c apart
     fibres<NA, true>(blk, ma, c, g.lc, c, pitch, g.bsz / NA);
+    PP_ADD(3, t3);
     if constexpr (NB > 1) {
+      PP_T(t4);
       __syncthreads();
+      PP_ADD(2, t4);
+      PP_T(t5);
       // mode b: fibres (ic, ia; io), rows one pitch apart (row = c * NA, a multiple of 8)
       fibres<NB, false>(blk, mb, row, 0, pitch, pitch * NB, g.bsz / NB);
+      PP_ADD(4, t5);
     }
+    PP_T(t6);
     __syncthreads();
+    PP_ADD(2, t6);
+    PP_T(t7);
     double* dst = g.Y + base_of(bk) + g0;
     const double* srcp = blk + s0;
     int x = x0;
@@ -202,9 +233,19 @@ __global__ void __launch_bounds__(THREADS) pair_kernel(PairArgs g) {
       dst += dg, srcp += ds, x += dx;
       if (x >= row) x -= row, srcp += pad;
     }
+    PP_ADD(5, t7);
+    PP_T(t8);
     __syncthreads();  // blk is the next round's prefetch target
+    PP_ADD(2, t8);
+#if PAIR_PROF
+    pph[6] += 1;
+#endif
   }
   cp_async_wait_all();
+#if PAIR_PROF
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 7; ++k) atomicAdd(&g_pair_prof[k], static_cast<unsigned long long>(pph[k]));
+#endif
 }
 
 template <int NA, int NB>
@@ -215,7 +256,21 @@ cudaError_t launch_pair(const PairArgs& g, cudaStream_t st) {
   if (cudaError_t e = kernel_setup(k, smem, THREADS, &nsm, &occ); e != cudaSuccess) return e;
   int64_t grid = static_cast<int64_t>(nsm) * occ;
   if (grid > g.nblk) grid = g.nblk;
+#if PAIR_PROF
+  unsigned long long z[8] = {};
+  cudaMemcpyToSymbolAsync(g_pair_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+#endif
   k<<<static_cast<unsigned>(grid), THREADS, smem, st>>>(g);
+#if PAIR_PROF
+  unsigned long long h[8];
+  cudaMemcpyFromSymbolAsync(h, g_pair_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  const double nb = h[6] ? static_cast<double>(h[6]) : 1.0;
+  std::fprintf(stderr, "[tsg profp] %dx%d c=%d o=%d vec=%d grid=%lld smem=%d | per block per warp (cycles): gather issue %.0f  "
+               "cp.async wait %.0f  barriers %.0f  mode a %.0f  mode b %.0f  scatter %.0f  (blocks x warps %.0f)\n",
+               NA, NB, g.c, g.o, g.vec, static_cast<long long>(grid), smem, h[0] / nb, h[1] / nb, h[2] / nb, h[3] / nb,
+               h[4] / nb, h[5] / nb, nb);
+#endif
   return cudaGetLastError();
 }
 
