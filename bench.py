@@ -639,7 +639,8 @@ def run_sharded(a, rank, world, local):
                    "against the neighbouring chunks' transforms")
             # our kernels per step: phase A/C transforms (<= d-1 passes each way) + phase B
             # (state reset, mode-(d-1) transform, fibre solve, back transform)
-            launches = a.steps * (2 * (len(dims) - 1) * (len(be.cb) - 1) + 4)
+            # + the re-sharding pack and unpack kernels (tsg_slab_pack), one each per chunk
+            launches = a.steps * ((2 * (len(dims) - 1) + 2) * (len(be.cb) - 1) + 4)
         else:
             par = (f"{world} slabs along mode {len(dims) - 1} (rows {bounds}); NCCL all-gather for the "
                    "last-mode transforms, peer-mapped dataflow solve")

@@ -229,6 +229,13 @@ typedef struct tsg_dplan tsg_dplan;
 /* Slab row bounds (nranks + 1 entries) of a mode of extent n with
  * quasi-triangular factor T, for base tiles of extent `tile`. */
 int tsg_slab_bounds(int n, const double* T, int tile, int nranks, int* bounds);
+/* Re-sharding pack (dir 0) / unpack (dir 1) of the decoupled sharded solve on
+ * the device: `rows` contiguous runs of n0 doubles <-> nranks segments, segment
+ * q = columns [b0[q], b0[q+1]) of every run, (rows, w_q) row-major at offset
+ * rows * b0[q] (the send layout of the all-to-all; b0: nranks + 1 host ints,
+ * nranks <= 64).  src and dst are device buffers of rows * n0 doubles. */
+int tsg_slab_pack(tsg_ctx* ctx, const double* src, double* dst, long long rows, int n0, int nranks,
+                  const int* b0, int dir, void* stream);
 int tsg_dplan_create(tsg_ctx* ctx, int rank, int nranks, int emulate, int d, const int* dims,
                      const double* const* T, const double* const* U, const tsg_opts* opts,
                      tsg_dplan** out);

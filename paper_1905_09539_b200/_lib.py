@@ -44,7 +44,7 @@ TSG_SYMBOLS = [
     "tsg_residual", "tsg_abi_version",
     "tsg_zlaplace_solve", "tsg_zlaplace_reduced", "tsg_zgsylv_solve", "tsg_zgsylv_reduced",
     "tsg_zmode_multiply", "tsg_zresidual",
-    "tsg_slab_bounds", "tsg_dplan_create", "tsg_dplan_destroy", "tsg_dplan_info",
+    "tsg_slab_bounds", "tsg_slab_pack", "tsg_dplan_create", "tsg_dplan_destroy", "tsg_dplan_info",
     "tsg_dplan_buffers", "tsg_dplan_ipc_export", "tsg_dplan_ipc_import",
     "tsg_dplan_forward_local", "tsg_dplan_forward_split", "tsg_dplan_solve",
     "tsg_dplan_back_local", "tsg_dplan_back_split", "tsg_dplan_status",
@@ -79,6 +79,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "tsg_plan_describe": (I, [P, ctypes.c_char_p, I]),
         "tsg_residual": (I, [P, I, I, c_int_p, c_dbl_pp, P, P, P, I, c_dbl_p]),
         "tsg_slab_bounds": (I, [I, c_dbl_p, I, I, c_int_p]),
+        "tsg_slab_pack": (I, [P, P, P, ctypes.c_longlong, I, I, c_int_p, I, P]),
         "tsg_dplan_create": (I, [P, I, I, I, I, c_int_p, c_dbl_pp, c_dbl_pp, ctypes.POINTER(TsgOpts),
                                  ctypes.POINTER(P)]),
         "tsg_dplan_destroy": (None, [P]),

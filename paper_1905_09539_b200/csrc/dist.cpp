@@ -29,6 +29,7 @@
 #include "../../include/tsylv_gpu.h"
 #include "gemm.h"
 #include "plan_impl.h"
+#include "util.h"
 #include "solve.h"
 
 using tsg_impl::fail;
@@ -113,6 +114,19 @@ int tsg_slab_bounds(int n, const double* T, int tile, int nranks, int* bounds) {
   for (int q = 0; q <= nranks; ++q) bounds[q] = s[q];
   for (int q = 0; q < nranks; ++q)
     if (bounds[q + 1] <= bounds[q]) return TSG_EDIM;
+  return TSG_OK;
+}
+
+int tsg_slab_pack(tsg_ctx* ctx, const double* src, double* dst, long long rows, int n0, int nranks,
+                  const int* b0, int dir, void* stream) {
+  if (!ctx || !src || !dst || !b0 || rows < 0 || n0 <= 0) return TSG_EINVAL;
+  if (nranks < 1 || nranks > tsg::kMaxPackRanks || b0[0] != 0 || b0[nranks] != n0)
+    return fail(ctx, TSG_EINVAL, "slab_pack: bounds must run from 0 to n0 over at most 64 ranks");
+  for (int q = 0; q < nranks; ++q)
+    if (b0[q + 1] < b0[q]) return fail(ctx, TSG_EINVAL, "slab_pack: bounds must be non-decreasing");
+  TSG_CU(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  TSG_CU(tsg::slab_pack(src, dst, rows, n0, nranks, b0, dir != 0, st));
   return TSG_OK;
 }
 

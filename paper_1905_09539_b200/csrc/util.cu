@@ -51,7 +51,47 @@ __global__ void reset_kernel(int* flags, int64_t nf, int* counter, int* extra, i
   if (i0 == 0) counter[0] = 0;
 }
 
+struct PackBounds {
+  int b[kMaxPackRanks + 1];
+};
+
+// threadIdx.x runs over the n0 columns (coalesced on the run side, and on the
+// segment side within a segment), threadIdx.y and the grid over the runs; a
+// thread's columns keep their segment, so the segment lookup is outside the
+// row loop.
+template <bool UNPACK>
+__global__ void __launch_bounds__(256) slab_pack_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                                        int64_t rows, int n0, int nranks, PackBounds pb) {
+  const int64_t rstep = static_cast<int64_t>(gridDim.x) * blockDim.y;
+  for (int i0 = threadIdx.x; i0 < n0; i0 += blockDim.x) {
+    int q = 0;
+    while (q + 1 < nranks && i0 >= pb.b[q + 1]) ++q;
+    const int w = pb.b[q + 1] - pb.b[q];
+    const int64_t seg = rows * pb.b[q] + (i0 - pb.b[q]);
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y; r < rows; r += rstep) {
+      if (UNPACK) dst[r * n0 + i0] = src[seg + r * w];
+      else dst[seg + r * w] = src[r * n0 + i0];
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t slab_pack(const double* src, double* dst, int64_t rows, int n0, int nranks, const int* b0,
+                      int dir, cudaStream_t st) {
+  if (rows <= 0 || n0 <= 0) return cudaSuccess;
+  if (nranks < 1 || nranks > kMaxPackRanks || b0[0] != 0 || b0[nranks] != n0) return cudaErrorInvalidValue;
+  PackBounds pb{};
+  for (int q = 0; q <= nranks; ++q) pb.b[q] = b0[q];
+  int bx = 32;
+  while (bx < n0 && bx < 256) bx *= 2;
+  const dim3 block(bx, 256 / bx);
+  const int64_t want = (rows + block.y - 1) / block.y;
+  const int grid = static_cast<int>(std::min<int64_t>(want, 148 * 8));
+  if (dir) slab_pack_kernel<true><<<grid, block, 0, st>>>(src, dst, rows, n0, nranks, pb);
+  else slab_pack_kernel<false><<<grid, block, 0, st>>>(src, dst, rows, n0, nranks, pb);
+  return cudaGetLastError();
+}
 
 cudaError_t reset_state(int* flags, int64_t nf, int* counter, int* extra, int64_t ne, cudaStream_t st) {
   const int64_t n = nf > ne ? nf : ne;

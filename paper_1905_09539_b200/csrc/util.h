@@ -12,6 +12,14 @@ cudaError_t axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s
 // across solves: the host re-arms it when it reads it (plan.cpp).
 cudaError_t reset_state(int* flags, int64_t nf, int* counter, int* extra, int64_t ne, cudaStream_t st);
 
+// Re-sharding pack / unpack of the decoupled multi-GPU solve (dist.py): `rows`
+// contiguous runs of n0 doubles <-> nranks segments, segment q holding columns
+// [b0[q], b0[q+1]) of every run ((rows, w_q) row-major, at offset rows * b0[q]).
+// dir 0: runs -> segments (pack), 1: segments -> runs (unpack).
+constexpr int kMaxPackRanks = 64;
+cudaError_t slab_pack(const double* src, double* dst, int64_t rows, int n0, int nranks, const int* b0,
+                      int dir, cudaStream_t st);
+
 // Launch setup of a kernel on the CURRENT device, thread-safe and cached per
 // (kernel, device, smem, threads): raises the dynamic shared-memory opt-in
 // when smem exceeds what was set before, and returns the SM count and the

@@ -327,6 +327,18 @@ class DeviceDecoupled:
     def b_solve(self, z, out) -> None:
         self.plan_b.enqueue_device(z.data_ptr(), out.data_ptr())
 
+    def repack(self, src, dst, unpack: bool) -> None:
+        """Re-sharding pack (runs of n0 -> per-peer mode-0 column segments, the
+        all-to-all send layout) or unpack of one slab / chunk on the device
+        (tsg_slab_pack, the library's own kernel), on the backend's stream."""
+        n0 = self.dims[0]
+        b0 = (ctypes.c_int * (self.nranks + 1))(*self.b0)
+        rc = lib().tsg_slab_pack(self.ctx.h, ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()),
+                                 src.numel() // n0, n0, self.nranks, b0, 1 if unpack else 0,
+                                 ctypes.c_void_p(self.stream))
+        if rc != 0:
+            raise gpu_error(f"tsg_slab_pack failed ({rc}): {self.ctx.last_error()}")
+
     def check(self) -> None:
         rep = self.plan_b.sync()
         if rep.zero_pivot_index >= 0:
@@ -411,7 +423,10 @@ class DecoupledSharded:
                 k = self.send1[q]
                 self.sa[o:o + k].view(rd, self.mid, self.rows_0[q]).copy_(v[:, :, be.b0[q]:be.b0[q + 1]])
                 o += k
-        self._run_torch(pack)
+        if hasattr(be, "repack"):
+            be.repack(self.ya, self.sa, False)
+        else:
+            self._run_torch(pack)
         self._a2a(self.zb, self.sa, self.recv1, self.send1)
         be.b_solve(self.zb, self.xb)
         self._a2a(self.ra, self.xb, self.send1, self.recv1)
@@ -423,7 +438,10 @@ class DecoupledSharded:
                 k = self.send1[q]
                 v[:, :, be.b0[q]:be.b0[q + 1]].copy_(self.ra[o:o + k].view(rd, self.mid, self.rows_0[q]))
                 o += k
-        self._run_torch(unpack)
+        if hasattr(be, "repack"):
+            be.repack(self.ra, self.ya, True)
+        else:
+            self._run_torch(unpack)
         be.a_back(self.ya, x)
         if check and hasattr(be, "check"):
             be.check()
@@ -527,7 +545,10 @@ class DecoupledSharded:
                     for q in range(P):
                         a, z = mine[q]
                         self.sa[a:z].view(rows_c, self.mid, self.rows_0[q]).copy_(v[:, :, be.b0[q]:be.b0[q + 1]])
-                on_compute(pack)
+                if hasattr(be, "repack"):
+                    be.repack(self.ya[e0:e1], self.sa[e0:e1], False)
+                else:
+                    on_compute(pack)
             waits.append(self._exchange(self.zb, theirs, self.sa, mine, comm, mark()))
         for w in waits:
             on_compute(w)
@@ -549,7 +570,10 @@ class DecoupledSharded:
                 for q in range(P):
                     a, z = mine[q]
                     v[:, :, be.b0[q]:be.b0[q + 1]].copy_(self.ra[a:z].view(rows_c, self.mid, self.rows_0[q]))
-            on_compute(unpack)
+            if hasattr(be, "repack"):
+                be.repack(self.ra[e0:e1], self.ya[e0:e1], True)
+            else:
+                on_compute(unpack)
             be.a_back(self.ya[e0:e1], x[e0:e1])
         if cuda:
             # the next solve's first pack overwrites sa: it must not pass the
@@ -579,12 +603,7 @@ def decoupled_emulated_solve(ctx, T: list, U: list, b_full: np.ndarray, nslabs: 
         xs = [torch.empty_like(v) for v in bs]
         for r in range(nslabs):
             bes[r].a_forward(bs[r], sh[r].ya)
-            v = sh[r].ya.view(sh[r].rows_d[r], sh[r].mid, dims[0])
-            o = 0
-            for q in range(nslabs):
-                k = sh[r].send1[q]
-                sh[r].sa[o:o + k].view(sh[r].rows_d[r], sh[r].mid, sh[r].rows_0[q]).copy_(v[:, :, b0[q]:b0[q + 1]])
-                o += k
+            bes[r].repack(sh[r].ya, sh[r].sa, False)  # the library's pack kernel, as on the ranks
         # all-to-all 1: rank q's receive block from r = r's send block for q
         for q in range(nslabs):
             o = 0
@@ -604,12 +623,7 @@ def decoupled_emulated_solve(ctx, T: list, U: list, b_full: np.ndarray, nslabs: 
                 sh[r].ra[o:o + k].copy_(sh[q].xb[so:so + k])
                 o += k
         for r in range(nslabs):
-            v = sh[r].ya.view(sh[r].rows_d[r], sh[r].mid, dims[0])
-            o = 0
-            for q in range(nslabs):
-                k = sh[r].send1[q]
-                v[:, :, b0[q]:b0[q + 1]].copy_(sh[r].ra[o:o + k].view(sh[r].rows_d[r], sh[r].mid, sh[r].rows_0[q]))
-                o += k
+            bes[r].repack(sh[r].ra, sh[r].ya, True)
             bes[r].a_back(sh[r].ya, xs[r])
         torch.cuda.synchronize()
     for be in bes:

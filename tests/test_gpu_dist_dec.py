@@ -77,3 +77,33 @@ def test_decoupled_sharded_world1_nccl(ref, gpu, chunks, dims):
         be.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rows,n0,b0", [(7, 24, [0, 24]), (5, 24, [0, 10, 24]), (33, 70, [0, 9, 9, 40, 70]),
+                                        (4, 1024, [0, 130, 256, 700, 1024]), (1000, 12, [0, 5, 12])])
+def test_slab_pack_kernel(gpu, rows, n0, b0):
+    """tsg_slab_pack (the all-to-all send layout) against numpy, both directions;
+    ragged and empty segments, n0 below a warp and above a block."""
+    import ctypes
+
+    import torch
+    from paper_1905_09539_b200._lib import lib
+    from paper_1905_09539_b200.plan import Context
+    ctx = Context(0)
+    P = len(b0) - 1
+    rng = np.random.default_rng(rows * n0)
+    v = rng.standard_normal((rows, n0))
+    want = np.concatenate([v[:, b0[q]:b0[q + 1]].reshape(-1) for q in range(P)])
+    src = torch.from_numpy(v.reshape(-1)).cuda()
+    dst = torch.zeros_like(src)
+    bb = (ctypes.c_int * (P + 1))(*b0)
+    for direction, a, b in ((0, src, dst), (1, dst, torch.zeros_like(src))):
+        rc = lib().tsg_slab_pack(ctx.h, ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()), rows, n0, P,
+                                 bb, direction, ctypes.c_void_p(ctx.stream_ptr()))
+        assert rc == 0, ctx.last_error()
+        torch.cuda.synchronize()
+        got = b.cpu().numpy()
+        assert np.array_equal(got, want if direction == 0 else v.reshape(-1))
+    bad = (ctypes.c_int * (P + 1))(*([1] + list(b0[1:])))
+    assert lib().tsg_slab_pack(ctx.h, ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()), rows, n0, P,
+                               bad, 0, None) != 0
