@@ -316,15 +316,17 @@ TSG_DEVINL void unit_bfly_k(double* y, int rl0, int pair0, int w) {
         v[l1] = re0 + im1;
         v[l1 | 1] = im0 - re1;
       } else {
-        v[l] = 0.5 * (re0 + re1);
-        v[l | 1] = 0.5 * (im0 + im1);
-        v[l1] = 0.5 * (im0 - im1);
-        v[l1 | 1] = -0.5 * (re0 - re1);
+        // unnormalised: the K - 1 halvings are one exact scaling at the end
+        v[l] = re0 + re1;
+        v[l | 1] = im0 + im1;
+        v[l1] = im0 - im1;
+        v[l1 | 1] = re1 - re0;
       }
     }
   }
+  constexpr double scale = INV ? 1.0 / static_cast<double>(1 << (K - 1)) : 1.0;
 #pragma unroll
-  for (int l = 0; l < NL; ++l) y[ucol(l, rl0, pair0, w)] = v[l];
+  for (int l = 0; l < NL; ++l) y[ucol(l, rl0, pair0, w)] = INV ? v[l] * scale : v[l];
 }
 
 template <bool INV>
@@ -478,36 +480,48 @@ TSG_DEVINL void rows_io(const FibreArgs& a, double* Y, int pitch, const int64_t*
   const int step = nw * rpi;  // runs per sweep of all warps
   const int nrun = nf * nb;
   if (w <= 32) {
-    // One element per lane and run; four runs in flight per lane: the
-    // pattern-offset lookups, address products and (on the way out) the
-    // shared loads of a sweep are independent, which hides their latency at
-    // the kernel's low occupancy.
-    constexpr int U = 4;
-    const bool act = r0 < w;
-    for (int run0 = warp * rpi + sub; run0 < nrun; run0 += U * step) {
-      double* ys[U];
-      const double* xs[U];
-      bool ok[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int run = run0 + u * step;
-        ok[u] = act && run < nrun;
-        const int i = run >> kb, b = ok[u] ? run & (nb - 1) : 0;
-        ys[u] = Y + static_cast<size_t>(i) * pitch + b * w + r0;
-        xs[u] = a.X + pb[b] + static_cast<int64_t>(i) * a.sf + r0;
+    // One element per lane and run.  A lane's runs keep their pattern b (or
+    // cycle through nb / step of them), so a lane walks the rows of f with
+    // two pointer increments per element: no index decode, no pattern-offset
+    // lookup in the loop; four rows in flight per lane.
+    (void)nrun;
+    if (r0 >= w) return;
+    const int rsub = warp * rpi + sub;  // this lane's first run (< step; step and nb are powers of two)
+    const int64_t sf = a.sf;
+    auto walk = [&](double* y, const double* x, int i0, int di) {
+      const int64_t dx = static_cast<int64_t>(di) * sf;
+      const int dy = di * pitch;
+      int i = i0;
+      for (; i + 3 * di < nf; i += 4 * di) {
+        if (LOAD) {
+          cp_async8(y, x, 8);
+          cp_async8(y + dy, x + dx, 8);
+          cp_async8(y + 2 * dy, x + 2 * dx, 8);
+          cp_async8(y + 3 * dy, x + 3 * dx, 8);
+        } else {
+          const double v0 = y[0], v1 = y[dy], v2 = y[2 * dy], v3 = y[3 * dy];
+          double* xo = const_cast<double*>(x);
+          xo[0] = v0;
+          xo[dx] = v1;
+          xo[2 * dx] = v2;
+          xo[3 * dx] = v3;
+        }
+        y += 4 * dy;
+        x += 4 * dx;
       }
-      if (LOAD) {
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (ok[u]) cp_async8(ys[u], xs[u], 8);
-      } else {
-        double v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = ok[u] ? *ys[u] : 0.0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (ok[u]) *const_cast<double*>(xs[u]) = v[u];
+      for (; i < nf; i += di) {
+        if (LOAD) cp_async8(y, x, 8);
+        else *const_cast<double*>(x) = *y;
+        y += dy;
+        x += dx;
       }
+    };
+    if (nb >= step) {
+      for (int b = rsub; b < nb; b += step) walk(Y + b * w + r0, a.X + pb[b] + r0, 0, 1);
+    } else {
+      const int b = rsub & (nb - 1), i0 = rsub >> kb;
+      walk(Y + static_cast<size_t>(i0) * pitch + b * w + r0, a.X + pb[b] + static_cast<int64_t>(i0) * sf + r0, i0,
+           step >> kb);
     }
     return;
   }
@@ -584,7 +598,7 @@ __global__ void __launch_bounds__(kSmallThreads, 2) fibre_small_kernel(const Fib
   if (SB[0].blk < a.nblocks) issue_block(a, SB[0].B, SB[0].pb, SB[0].nunit, Ys[0], SB[0].B.ncol | 1, sus[0]);
   int cur = 0;
 #if SMALL_PROF
-  long long ph[8] = {};
+  long long ph[14] = {};
 #endif
   for (;;) {
     SmallBuf& C = SB[cur];
@@ -610,6 +624,9 @@ __global__ void __launch_bounds__(kSmallThreads, 2) fibre_small_kernel(const Fib
     const bool more = Nx.blk < a.nblocks;
     if (more) {
       issue_block(a, Nx.B, Nx.pb, Nx.nunit, Ys[cur ^ 1], Nx.B.ncol | 1, sus[cur ^ 1]);
+#if SMALL_PROF
+      ph[8] += clock64() - t1;  // issue of the next block's loads alone
+#endif
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -631,11 +648,18 @@ __global__ void __launch_bounds__(kSmallThreads, 2) fibre_small_kernel(const Fib
       }
     }
     __syncthreads();
+#if SMALL_PROF
+    ph[9] += clock64() - t2;  // job table (thread 0) + barrier
+    const long long t2b = clock64();
+#endif
     for (int u = threadIdx.x >> 5; u < nunit; u += blockDim.x >> 5) {  // a warp per unit, lanes over rows
       const int k = kb + su[u].pair0;
       if (k < 2) continue;
       for (int i = threadIdx.x & 31; i < nf; i += 32) unit_butterfly<false>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
     }
+#if SMALL_PROF
+    ph[10] += clock64() - t2b;  // this warp's forward butterflies (before the barrier)
+#endif
     __syncthreads();
 #if SMALL_PROF
     long long t3 = clock64();
@@ -662,6 +686,9 @@ __global__ void __launch_bounds__(kSmallThreads, 2) fibre_small_kernel(const Fib
       }
       solve_job_reg<NF>(a, sT, sfc, Y, ncol, re, im, sr, si, goff(B, re, 0, a.sf));
     }
+#if SMALL_PROF
+    ph[11] += clock64() - t3;  // this warp's jobs (before the barrier)
+#endif
     __syncthreads();
 #if SMALL_PROF
     long long t4 = clock64();
@@ -672,8 +699,17 @@ __global__ void __launch_bounds__(kSmallThreads, 2) fibre_small_kernel(const Fib
       if (k < 2) continue;
       for (int i = threadIdx.x & 31; i < nf; i += 32) unit_butterfly<true>(Y, ncol, i, su[u].rl0, k, su[u].pair0, w);
     }
+#if SMALL_PROF
+    ph[12] += clock64() - t4;  // this warp's inverse butterflies (before the barrier)
+#endif
     __syncthreads();
+#if SMALL_PROF
+    const long long t5 = clock64();
+#endif
     rows_io<false>(a, Y, ncol, C.pb, w, kb);
+#if SMALL_PROF
+    ph[13] += clock64() - t5;  // this warp's stores (before the barrier)
+#endif
     __syncthreads();
 #if SMALL_PROF
     ph[4] += clock64() - t4;
@@ -682,8 +718,11 @@ __global__ void __launch_bounds__(kSmallThreads, 2) fibre_small_kernel(const Fib
     cur ^= 1;
   }
 #if SMALL_PROF
-  if (a.prof && (threadIdx.x & 31) == 0)
+  if (a.prof && (threadIdx.x & 31) == 0) {
     for (int k = 0; k < 7; ++k) atomicAdd(a.prof + k, static_cast<unsigned long long>(ph[k]));
+    // finer split in the slots the team kernel uses for its role histogram
+    for (int k = 8; k < 14; ++k) atomicAdd(a.prof + k, static_cast<unsigned long long>(ph[k]));
+  }
 #endif
   pdl_trigger();
 }
